@@ -1,0 +1,143 @@
+/* visrt-b200 — C-ABI of the B200-native visibility pre-processing hot path.
+ *
+ * The reference (arxiv 2501.02747 artifact, /root/reference/proj) has no FFI;
+ * its boundary is the C++ API of namespace rt. Each entry point below is what
+ * that API's hot-path functions bind to (see INTEGRATION.md for the C++ drop-in
+ * layer and the ctypes binding):
+ *
+ *   visrt_scene_create        <- Scene::finalize / facet ingest
+ *                                (include/rt/scene.hpp:81-88, src/scene.cpp:65-182,
+ *                                 src/geom.cpp:126-140, src/scene.cpp:213-254)
+ *   visrt_pair_visibility     <- build_matrix pair loop + occlusion_judgment
+ *                                (include/rt/vismatrix.hpp:113,141;
+ *                                 src/vismatrix.cpp:253-302, 597-675)
+ *   visrt_pair_detail         <- occlusion_judgment verdict kind + blocker set
+ *                                (src/vismatrix.cpp:275-301)
+ *   visrt_point_regions       <- illuminated_region for (snapshot, face) batches
+ *                                (include/rt/vistable.hpp:116-117, src/vistable.cpp:287-334)
+ *   visrt_image_tree          <- TraceAccelerator::trace / Engine::expand + resolve_sequence
+ *                                (include/rt/raytracer.hpp:96-118, src/raytracer.cpp:205-444)
+ *
+ * Conventions: plain pointers and sizes; caller-owned output buffers; every
+ * call returns a status (0 ok) and never throws; the message of the last
+ * failure on the calling thread is visrt_last_error(). Status codes map to
+ * the reference exception types: 1 VisibilityError, 2 PlacementError,
+ * 3 SceneError, 4 CUDA error, 5 capacity/usage error.
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ */
+#ifndef VISRT_H
+#define VISRT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VISRT_OK 0
+#define VISRT_E_VISIBILITY 1
+#define VISRT_E_PLACEMENT 2
+#define VISRT_E_SCENE 3
+#define VISRT_E_CUDA 4
+#define VISRT_E_USAGE 5
+
+#define VISRT_MAX_VERTS 8
+
+typedef struct visrt_scene visrt_scene;
+
+/* Facet soup (or closed-shell scene) in host memory. */
+typedef struct {
+    int32_t nfaces;
+    const int32_t* vert_off;   /* [nfaces+1] prefix offsets, in vertices            */
+    const double* verts;       /* [3*vert_off[nfaces]] xyz per vertex, rings in order */
+    const int32_t* building;   /* [nfaces] building index, -1 = none; NULL = soup   */
+} visrt_facets_v1;
+
+typedef struct {
+    int64_t pairs;             /* unordered pairs evaluated                          */
+    int64_t candidates;        /* pairs passing the first_order_pair prefilter       */
+    int64_t admitted;          /* pairs not Occluded (bit set)                       */
+    double  tests_alg;         /* sum S(i,j)*(N-2) over evaluated pairs (reference work) */
+    int64_t tests_exec;        /* segment-vs-facet tests the kernel executed         */
+    float   ms;                /* device time of the call (CUDA events)              */
+} visrt_stats;
+
+const char* visrt_last_error(void);
+int visrt_version(void);
+
+/* Ingest on the host with the reference's arithmetic, upload the facet SoA to
+ * device `device`. */
+int visrt_scene_create(const visrt_facets_v1* facets, int device, visrt_scene** out);
+void visrt_scene_destroy(visrt_scene* scene);
+int visrt_scene_nfaces(const visrt_scene* scene);
+/* Host copies of ingest products: normal[3n], orientation[n] (0 H, 1 V, 2 O),
+ * plane segments seg[n*3*6] (a.x a.y b.x b.y n.x n.y), seg_ok[n*3]. Any NULL skipped. */
+int visrt_scene_ingest(const visrt_scene* scene, double* normal, int32_t* orientation,
+                       double* seg, int32_t* seg_ok);
+
+/* (1) Inter-visibility matrix.
+ * flags: VISRT_PAIRS_ALL        — (B) every i<j, bit = occlusion verdict != Occluded;
+ *        VISRT_PAIRS_PREFILTERED — (A) candidates of first_order_pair's gate only
+ *                                 (non-oblique, mutually_front, required_planes != {}).
+ * bits: row-major N x ceil(N/64) uint64 words, symmetric (bit (i,j) and (j,i)).
+ * Device-resident variant writes into scene-owned memory: visrt_matrix_bits_device(). */
+#define VISRT_PAIRS_ALL 0x1u
+#define VISRT_PAIRS_PREFILTERED 0x2u
+int visrt_pair_visibility(visrt_scene* scene, uint32_t flags, uint64_t* bits_host,
+                          visrt_stats* stats, void* stream);
+const uint64_t* visrt_matrix_bits_device(const visrt_scene* scene);
+/* Candidate list of the last PREFILTERED call (ordered by (i, j)), with the
+ * verdict bit per candidate. Two-call sizing: pass NULL to get the count. */
+int64_t visrt_candidates(const visrt_scene* scene, int32_t* ci, int32_t* cj, uint8_t* admitted);
+
+/* Verdict kind (0 Visible, 1 PartiallyVisible, 2 Occluded) and blocker sets for
+ * a pair list (ref = ci, aim = cj). blockers: CSR (blk_off[npairs+1], blk_idx)
+ * sorted by face index; pass blk_idx = NULL to size (blk_off still filled). */
+int visrt_pair_detail(visrt_scene* scene, int64_t npairs, const int32_t* ci, const int32_t* cj,
+                      int8_t* kind, int64_t* blk_off, int32_t* blk_idx, int64_t blk_cap,
+                      visrt_stats* stats, void* stream);
+
+/* (2) Per-snapshot point regions: illuminated_region(source, face) for every
+ * (source k, face f). Per (k, f): present (1 / 0 none / -1 source on plane),
+ * per plane tag t in {XY, YZ, XZ}: has[t], clipped[t], sub[2t], sub[2t+1]. */
+typedef struct {
+    int8_t present;
+    int8_t has[3];
+    int8_t clipped[3];
+    int8_t pad;
+    double sub[6];
+} visrt_region;
+int visrt_point_regions(visrt_scene* scene, int64_t nsrc, const double* src_xyz,
+                        visrt_region* out, visrt_stats* stats, void* stream);
+
+/* (3) Image-tree expansion (TraceAccelerator::trace, allow_diffraction = false).
+ * The chain filter is given as the admitted order-1 bit matrix plus optional
+ * order-2 chains (triples a->b->c admitted into the filter). Per snapshot k
+ * (tx[k], rx[k] or rx[0] when rx_fixed): paths written to a CSR over
+ * snapshots: path_off[nsnap+1]; per path: nrefl, faces[4], points[3*6]. */
+typedef struct visrt_tracer visrt_tracer;
+int visrt_tracer_create(visrt_scene* scene, int max_refl, const uint64_t* admitted_bits,
+                        int64_t ntriples, const int32_t* triples, visrt_tracer** out);
+void visrt_tracer_destroy(visrt_tracer* tracer);
+typedef struct {
+    int32_t nrefl;
+    int32_t faces[4];
+    int32_t pad;
+    double points[18];     /* tx, reflection points..., rx */
+    double length;
+} visrt_path;
+typedef struct {
+    int64_t nodes;         /* image-tree nodes expanded (TraceStats::nodes_expanded) */
+    int64_t sequences;     /* sequences resolved (TraceStats::sequences_checked)     */
+    int64_t paths;
+    float   ms;
+} visrt_trace_stats;
+int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const double* rx,
+                int rx_fixed, int64_t* path_off, visrt_path* paths, int64_t path_cap,
+                visrt_trace_stats* stats, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,507 @@
+/* TEST INFRASTRUCTURE ONLY — CPU oracle (checker) for the visibility hot path.
+ *
+ * Plain-C restatement of the reference's FP64 algorithm. Every function cites
+ * the reference file:line it follows (paths relative to /root/reference/proj).
+ * Bit-exactness rules: compiled with -ffp-contract=off (no FMA, like the
+ * reference's default x86-64 build), and every expression keeps the
+ * reference's association order (Vec3 ops are component-wise, dot() is
+ * ((x*x' + y*y') + z*z')).
+ *
+ * Pinned against oracle/_ref (the compiled reference) and tests/golden/.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load it; the product library never links it.
+ */
+#include "visrt_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define VO_EPS 1e-9     /* kEps, include/rt/geom.hpp:14 */
+#define VO_MAXV 8
+
+typedef struct { double x, y, z; } v3;
+typedef struct { double x, y; } v2;
+
+static inline v3 sub3(v3 a, v3 b) { v3 r = {a.x - b.x, a.y - b.y, a.z - b.z}; return r; }
+static inline v3 add3(v3 a, v3 b) { v3 r = {a.x + b.x, a.y + b.y, a.z + b.z}; return r; }
+static inline v3 mul3(v3 a, double s) { v3 r = {a.x * s, a.y * s, a.z * s}; return r; }
+static inline v3 div3(v3 a, double s) { v3 r = {a.x / s, a.y / s, a.z / s}; return r; }
+/* include/rt/geom.hpp:29-32 */
+static inline double dot3(v3 a, v3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static inline v3 cross3(v3 a, v3 b) {
+    v3 r = {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+    return r;
+}
+static inline double norm3(v3 a) { return sqrt(dot3(a, a)); }
+static inline v2 sub2(v2 a, v2 b) { v2 r = {a.x - b.x, a.y - b.y}; return r; }
+static inline double dot2(v2 a, v2 b) { return a.x * b.x + a.y * b.y; }
+static inline double cross2(v2 a, v2 b) { return a.x * b.y - a.y * b.x; }
+static inline double norm2(v2 a) { return sqrt(dot2(a, a)); }
+/* std::min / std::max / std::clamp semantics */
+static inline double smin(double a, double b) { return (b < a) ? b : a; }
+static inline double smax(double a, double b) { return (a < b) ? b : a; }
+static inline double sclamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+/* project / lift, src/geom.cpp:21-37 */
+static inline v2 project(v3 p, int plane) {
+    v2 r;
+    if (plane == 0) { r.x = p.x; r.y = p.y; }
+    else if (plane == 1) { r.x = p.y; r.y = p.z; }
+    else { r.x = p.x; r.y = p.z; }
+    return r;
+}
+static inline v3 lift(v2 q, int plane, double d) {
+    v3 r;
+    if (plane == 0) { r.x = q.x; r.y = q.y; r.z = d; }
+    else if (plane == 1) { r.x = d; r.y = q.x; r.z = q.y; }
+    else { r.x = q.x; r.y = d; r.z = q.y; }
+    return r;
+}
+/* dropped_coord, src/vistable.cpp:23-30 */
+static inline double dropped(v3 p, int plane) { return plane == 0 ? p.z : (plane == 1 ? p.x : p.y); }
+
+typedef struct {
+    int nv;
+    v3 pts[VO_MAXV];
+    v3 n;
+    int orient;            /* 0 Horizontal, 1 Vertical, 2 Oblique */
+    int seg_ok[3];
+    v2 seg_a[3], seg_b[3], seg_n[3];
+} vo_face;
+
+struct vo_scene {
+    int32_t n;
+    vo_face* f;
+};
+
+/* ConvexPolygon::from_points (Newell normal), src/geom.cpp:126-140; normalized src/geom.cpp:15-19 */
+static int newell(const vo_face* f, v3* out) {
+    v3 n = {0, 0, 0};
+    for (int i = 0; i < f->nv; ++i) {
+        v3 a = f->pts[i], b = f->pts[(i + 1) % f->nv];
+        n.x += (a.y - b.y) * (a.z + b.z);
+        n.y += (a.z - b.z) * (a.x + b.x);
+        n.z += (a.x - b.x) * (a.y + b.y);
+    }
+    double len = norm3(n);
+    if (len < VO_EPS) return -1;
+    *out = div3(n, len);
+    return 0;
+}
+
+/* classify_orientation, src/scene.cpp:19-24 */
+static int classify(v3 n) {
+    double ax = fabs(n.x), ay = fabs(n.y), az = fabs(n.z);
+    if (ax <= 1e-9 && ay <= 1e-9) return 0;
+    if (az <= 1e-9) return 1;
+    return 2;
+}
+
+/* plane_segment, src/scene.cpp:213-254 */
+static int plane_segment(const vo_face* f, int plane, v2* a_out, v2* b_out, v2* n_out) {
+    v2 pts[VO_MAXV];
+    for (int i = 0; i < f->nv; ++i) pts[i] = project(f->pts[i], plane);
+    v2 lo = pts[0], hi = pts[0];
+    for (int i = 0; i < f->nv; ++i) {
+        lo.x = smin(lo.x, pts[i].x); lo.y = smin(lo.y, pts[i].y);
+        hi.x = smax(hi.x, pts[i].x); hi.y = smax(hi.y, pts[i].y);
+    }
+    v2 a, b;
+    if (hi.x - lo.x <= VO_EPS && hi.y - lo.y <= VO_EPS) {
+        return 0;
+    } else if (hi.x - lo.x <= VO_EPS) {
+        a.x = lo.x; a.y = lo.y; b.x = lo.x; b.y = hi.y;
+    } else if (hi.y - lo.y <= VO_EPS) {
+        a.x = lo.x; a.y = lo.y; b.x = hi.x; b.y = lo.y;
+    } else {
+        v2 d = {hi.x - lo.x, hi.y - lo.y};
+        double tmin = DBL_MAX, tmax = -DBL_MAX;
+        v2 pmin = {0, 0}, pmax = {0, 0};
+        for (int i = 0; i < f->nv; ++i) {
+            v2 rel = {pts[i].x - lo.x, pts[i].y - lo.y};
+            if (fabs(cross2(d, rel)) > VO_EPS * (norm2(d) + 1.0)) return 0;
+            double t = dot2(d, rel);
+            if (t < tmin) { tmin = t; pmin = pts[i]; }
+            if (t > tmax) { tmax = t; pmax = pts[i]; }
+        }
+        a = pmin;
+        b = pmax;
+    }
+    v2 n2 = project(f->n, plane);
+    double len = norm2(n2);
+    if (len <= VO_EPS) return 0;
+    double inv = 1.0 / len;
+    n_out->x = n2.x * inv;
+    n_out->y = n2.y * inv;
+    *a_out = a;
+    *b_out = b;
+    return 1;
+}
+
+vo_scene* vo_scene_create(int32_t nfaces, const int32_t* vert_off, const double* verts) {
+    vo_scene* s = (vo_scene*)calloc(1, sizeof(vo_scene));
+    s->n = nfaces;
+    s->f = (vo_face*)calloc((size_t)nfaces, sizeof(vo_face));
+    for (int32_t i = 0; i < nfaces; ++i) {
+        vo_face* f = &s->f[i];
+        f->nv = vert_off[i + 1] - vert_off[i];
+        if (f->nv < 3 || f->nv > VO_MAXV) { vo_scene_free(s); return NULL; }
+        for (int k = 0; k < f->nv; ++k) {
+            const double* p = verts + 3 * (vert_off[i] + k);
+            f->pts[k].x = p[0]; f->pts[k].y = p[1]; f->pts[k].z = p[2];
+        }
+        if (newell(f, &f->n) != 0) { vo_scene_free(s); return NULL; }
+        f->orient = classify(f->n);
+        for (int pl = 0; pl < 3; ++pl) {
+            f->seg_ok[pl] = plane_segment(f, pl, &f->seg_a[pl], &f->seg_b[pl], &f->seg_n[pl]);
+        }
+    }
+    return s;
+}
+
+void vo_scene_free(vo_scene* s) {
+    if (!s) return;
+    free(s->f);
+    free(s);
+}
+
+int32_t vo_nfaces(const vo_scene* s) { return s->n; }
+
+int32_t vo_face_info(const vo_scene* s, int32_t i, double* normal, int32_t* orientation) {
+    normal[0] = s->f[i].n.x; normal[1] = s->f[i].n.y; normal[2] = s->f[i].n.z;
+    *orientation = s->f[i].orient;
+    return s->f[i].nv;
+}
+
+int32_t vo_plane_segment(const vo_scene* s, int32_t i, int32_t plane, double* o) {
+    const vo_face* f = &s->f[i];
+    if (!f->seg_ok[plane]) return 0;
+    o[0] = f->seg_a[plane].x; o[1] = f->seg_a[plane].y;
+    o[2] = f->seg_b[plane].x; o[3] = f->seg_b[plane].y;
+    o[4] = f->seg_n[plane].x; o[5] = f->seg_n[plane].y;
+    return 1;
+}
+
+/* Plane::signed_distance, include/rt/geom.hpp:97 (plane point = pts[0], geom.hpp:110) */
+static inline double sdist(const vo_face* f, v3 p) { return dot3(sub3(p, f->pts[0]), f->n); }
+
+/* ConvexPolygon::contains, src/geom.cpp:155-167 */
+static int contains(const vo_face* f, v3 p) {
+    if (fabs(sdist(f, p)) > VO_EPS) return 0;
+    for (int i = 0; i < f->nv; ++i) {
+        v3 a = f->pts[i], b = f->pts[(i + 1) % f->nv];
+        v3 edge = sub3(b, a);
+        double len = norm3(edge);
+        if (len < VO_EPS) continue;
+        v3 inward = div3(cross3(f->n, edge), len);
+        if (dot3(sub3(p, a), inward) < -VO_EPS) return 0;
+    }
+    return 1;
+}
+
+/* segment_face_intersection, src/geom.cpp:169-180 */
+static int seg_hits(const vo_face* f, v3 a, v3 b) {
+    double da = sdist(f, a);
+    double db = sdist(f, b);
+    if (fabs(da) <= VO_EPS || fabs(db) <= VO_EPS) return 0;
+    if (da * db > 0.0) return 0;
+    double t = da / (da - db);
+    v3 p = add3(a, mul3(sub3(b, a), t));
+    return contains(f, p);
+}
+
+int32_t vo_segment_hits_face(const vo_scene* s, const double* a, const double* b, int32_t face) {
+    v3 A = {a[0], a[1], a[2]}, B = {b[0], b[1], b[2]};
+    return seg_hits(&s->f[face], A, B);
+}
+
+/* mutually_front, src/vismatrix.cpp:160-169 */
+static int has_front_point(const vo_face* of, const vo_face* probe) {
+    for (int k = 0; k < probe->nv; ++k)
+        if (sdist(of, probe->pts[k]) > VO_EPS) return 1;
+    return 0;
+}
+int32_t vo_mutually_front(const vo_scene* s, int32_t i, int32_t j) {
+    return has_front_point(&s->f[i], &s->f[j]) && has_front_point(&s->f[j], &s->f[i]);
+}
+
+/* required_planes, src/vismatrix.cpp:171-181 */
+int32_t vo_required_planes(const vo_scene* s, int32_t i, int32_t j) {
+    int32_t m = 0;
+    for (int pl = 0; pl < 3; ++pl) {
+        if (!s->f[i].seg_ok[pl] || !s->f[j].seg_ok[pl]) continue;
+        double d = fabs(dot2(s->f[i].seg_n[pl], s->f[j].seg_n[pl]));
+        if (d >= 1.0 - 1e-9 || d <= 1e-9) m |= 1 << pl;
+    }
+    return m;
+}
+
+/* first_order_pair gate, src/vismatrix.cpp:597-604 */
+int32_t vo_prefilter(const vo_scene* s, int32_t i, int32_t j) {
+    if (s->f[i].orient == 2 || s->f[j].orient == 2) return 0;
+    if (!vo_mutually_front(s, i, j)) return 0;
+    return vo_required_planes(s, i, j) != 0;
+}
+
+/* centroid, src/geom.cpp:142-146 */
+static v3 centroid(const vo_face* f) {
+    v3 c = {0, 0, 0};
+    for (int k = 0; k < f->nv; ++k) c = add3(c, f->pts[k]);
+    return div3(c, (double)f->nv);
+}
+
+/* face_samples, src/vismatrix.cpp:226-249. Returns count (<= 8 + 1 + 24). */
+static int face_samples(const vo_face* f, v3* out) {
+    int n = 0;
+    for (int k = 0; k < f->nv; ++k) out[n++] = f->pts[k];
+    v3 c = centroid(f);
+    out[n++] = c;
+    if (f->nv == 4) {
+        for (int i = 0; i < 4; ++i) {
+            for (int j = 0; j < 4; ++j) {
+                double u = (i + 0.5) / 4.0;
+                double v = (j + 0.5) / 4.0;
+                v3 p = add3(add3(add3(mul3(f->pts[0], (1 - u) * (1 - v)), mul3(f->pts[1], u * (1 - v))),
+                                 mul3(f->pts[2], u * v)),
+                            mul3(f->pts[3], (1 - u) * v));
+                out[n++] = p;
+            }
+        }
+    } else {
+        static const double ss[3] = {0.25, 0.5, 0.75};
+        for (int k = 0; k < f->nv; ++k)
+            for (int q = 0; q < 3; ++q) out[n++] = add3(c, mul3(sub3(f->pts[k], c), ss[q]));
+    }
+    return n;
+}
+
+/* sightlines, src/vismatrix.cpp:263-273 */
+static int sightlines(const vo_face* r, const vo_face* a, v3* P, v3* Q) {
+    v3 sr[8 + 1 + 24], sa[8 + 1 + 24];
+    int cr = face_samples(r, sr), ca = face_samples(a, sa);
+    int nr = r->nv, na = a->nv, n = 0;
+    for (int i = 0; i < nr; ++i)
+        for (int j = 0; j < na; ++j) { P[n] = sr[i]; Q[n] = sa[j]; ++n; }
+    P[n] = sr[nr]; Q[n] = sa[na]; ++n;
+    int gr = cr - nr - 1, ga = ca - na - 1;
+    int grid = gr < ga ? gr : ga;
+    for (int k = 0; k < grid; ++k) { P[n] = sr[nr + 1 + k]; Q[n] = sa[na + 1 + k]; ++n; }
+    return n;
+}
+
+int32_t vo_sightline_count(const vo_scene* s, int32_t i, int32_t j) {
+    v3 P[128], Q[128];
+    return sightlines(&s->f[i], &s->f[j], P, Q);
+}
+
+/* occlusion_judgment, src/vismatrix.cpp:253-302 (no early exit; blockers collected) */
+static int occlusion(const vo_scene* s, int32_t i, int32_t j, unsigned char* mark, int want_blockers) {
+    v3 P[128], Q[128];
+    int ns = sightlines(&s->f[i], &s->f[j], P, Q);
+    int blocked = 0;
+    for (int k = 0; k < ns; ++k) {
+        if (norm3(sub3(Q[k], P[k])) <= VO_EPS) continue;
+        int hit = 0;
+        for (int32_t o = 0; o < s->n; ++o) {
+            if (o == i || o == j) continue;
+            if (seg_hits(&s->f[o], P[k], Q[k])) {
+                hit = 1;
+                if (want_blockers) mark[o] = 1;
+                else break;   /* kind only: first hit decides this sightline */
+            }
+        }
+        if (hit) ++blocked;
+    }
+    if (blocked == 0) return 0;
+    if (blocked == ns) return 2;
+    return 1;
+}
+
+int32_t vo_occlusion(const vo_scene* s, int32_t i, int32_t j, int32_t* blockers, int32_t cap,
+                     int32_t* nblk) {
+    unsigned char* mark = (unsigned char*)calloc((size_t)s->n, 1);
+    int kind = occlusion(s, i, j, mark, 1);
+    int32_t c = 0;
+    for (int32_t o = 0; o < s->n; ++o) {
+        if (!mark[o]) continue;
+        if (c < cap) blockers[c] = o;
+        ++c;
+    }
+    *nblk = c;
+    free(mark);
+    return kind;
+}
+
+typedef struct {
+    const vo_scene* s;
+    int64_t n;
+    const int32_t* pi;
+    const int32_t* pj;
+    int8_t* kind;
+    int64_t next;
+    pthread_mutex_t mu;
+} batch_ctx;
+
+static void* batch_worker(void* arg) {
+    batch_ctx* c = (batch_ctx*)arg;
+    for (;;) {
+        pthread_mutex_lock(&c->mu);
+        int64_t k0 = c->next;
+        c->next += 64;
+        pthread_mutex_unlock(&c->mu);
+        if (k0 >= c->n) break;
+        int64_t k1 = k0 + 64 < c->n ? k0 + 64 : c->n;
+        for (int64_t k = k0; k < k1; ++k) c->kind[k] = (int8_t)occlusion(c->s, c->pi[k], c->pj[k], NULL, 0);
+    }
+    return NULL;
+}
+
+int32_t vo_occlusion_batch(const vo_scene* s, int64_t npairs, const int32_t* pi, const int32_t* pj,
+                           int8_t* kind, int32_t threads) {
+    batch_ctx c = {s, npairs, pi, pj, kind, 0, PTHREAD_MUTEX_INITIALIZER};
+    if (threads < 1) threads = 1;
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, batch_worker, &c);
+    batch_worker(&c);
+    for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+    free(th);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------
+ * (2) illuminated_region — src/vistable.cpp:287-334 and helpers 38-193
+ * ------------------------------------------------------------------------ */
+
+/* sightline_clear, src/vistable.cpp:38-44 */
+static int sightline_clear(const vo_scene* s, v3 a, v3 b, int skip) {
+    for (int32_t o = 0; o < s->n; ++o) {
+        if (o == skip) continue;
+        if (seg_hits(&s->f[o], a, b)) return 0;
+    }
+    return 1;
+}
+
+typedef struct {
+    v2 a, b;
+    int nv;
+    v2 us[VO_MAXV];
+} face_param_t;
+
+/* face_param, src/vistable.cpp:84-98 */
+static int face_param(const vo_face* f, int plane, face_param_t* fp) {
+    if (!f->seg_ok[plane]) return 0;
+    fp->a = f->seg_a[plane];
+    fp->b = f->seg_b[plane];
+    v2 d = sub2(fp->b, fp->a);
+    double len2 = dot2(d, d);
+    if (len2 <= VO_EPS * VO_EPS) return 0;
+    fp->nv = f->nv;
+    for (int k = 0; k < f->nv; ++k) {
+        v2 q = project(f->pts[k], plane);
+        fp->us[k].x = dot2(sub2(q, fp->a), d) / len2;
+        fp->us[k].y = dropped(f->pts[k], plane);
+    }
+    return 1;
+}
+
+/* column_span, src/vistable.cpp:102-126 */
+static int column_span(const face_param_t* fp, double u, double* lo_o, double* hi_o) {
+    double lo = 0.0, hi = 0.0;
+    int any = 0;
+    for (int i = 0; i < fp->nv; ++i) {
+        v2 a = fp->us[i], b = fp->us[(i + 1) % fp->nv];
+        double da = a.x - u, db = b.x - u;
+        double s;
+        if (fabs(da) <= 1e-12) {
+            s = a.y;
+            if (!any) { lo = hi = s; any = 1; } else { lo = smin(lo, s); hi = smax(hi, s); }
+        }
+        if ((da < 0.0) != (db < 0.0) && fabs(da - db) > 1e-15) {
+            s = a.y + (b.y - a.y) * (da / (da - db));
+            if (!any) { lo = hi = s; any = 1; } else { lo = smin(lo, s); hi = smax(hi, s); }
+        }
+    }
+    if (!any) return 0;
+    *lo_o = lo;
+    *hi_o = hi;
+    return 1;
+}
+
+/* col_vis lambda, src/vistable.cpp:146-159 */
+static int col_vis(const vo_scene* s, v3 src, int32_t face, const face_param_t* fp, int plane, double u) {
+    double uc = sclamp(u, 0.0, 1.0);
+    double s0, s1;
+    if (!column_span(fp, uc, &s0, &s1)) return 0;
+    double inset = (s1 - s0) * 1e-6;
+    for (int j = 0; j < 7; ++j) {
+        double f = (double)j / 6;
+        double sv = smin(s1 - inset, smax(s0 + inset, s0 + (s1 - s0) * f));
+        v2 q = {fp->a.x + (fp->b.x - fp->a.x) * uc, fp->a.y + (fp->b.y - fp->a.y) * uc};
+        v3 p = lift(q, plane, sv);
+        if (sightline_clear(s, src, p, face)) return 1;
+    }
+    return 0;
+}
+
+/* refine lambda, src/vistable.cpp:164-173 */
+static double refine(const vo_scene* s, v3 src, int32_t face, const face_param_t* fp, int plane,
+                     double lo, double hi, int lo_vis) {
+    for (int it = 0; it < 50 && hi - lo > 1e-15; ++it) {
+        double mid = 0.5 * (lo + hi);
+        if (col_vis(s, src, face, fp, plane, mid) == lo_vis) lo = mid;
+        else hi = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+/* visible_intervals → largest interval only (what illuminated_region keeps),
+ * src/vistable.cpp:140-193 + max_element at 307-311. Returns 0 if empty. */
+static int best_interval(const vo_scene* s, v3 src, int32_t face, const face_param_t* fp, int plane,
+                         double* b0, double* b1) {
+    char vis[65];
+    for (int i = 0; i < 65; ++i) vis[i] = (char)col_vis(s, src, face, fp, plane, (double)i / 64);
+    const double step = 1.0 / 64;
+    int found = 0;
+    int i = 0;
+    while (i < 65) {
+        if (!vis[i]) { ++i; continue; }
+        double start = (double)i / 64;
+        if (i > 0) start = refine(s, src, face, fp, plane, start - step, start, 0);
+        int j = i;
+        while (j + 1 < 65 && vis[j + 1]) ++j;
+        double end = (double)j / 64;
+        if (j + 1 < 65) end = refine(s, src, face, fp, plane, end, end + step, 1);
+        /* std::max_element with comp a[1]-a[0] < b[1]-b[0]: first largest wins */
+        if (!found || (*b1 - *b0) < (end - start)) { *b0 = start; *b1 = end; }
+        found = 1;
+        i = j + 1;
+    }
+    return found;
+}
+
+int32_t vo_illuminated_region(const vo_scene* s, const double* srcp, int32_t face, vo_region* out) {
+    memset(out, 0, sizeof(*out));
+    const vo_face* f = &s->f[face];
+    v3 src = {srcp[0], srcp[1], srcp[2]};
+    double dist = sdist(f, src);
+    if (fabs(dist) <= VO_EPS) { out->present = -1; return 0; }
+    if (dist < 0.0) return 0;
+    int any = 0;
+    for (int pl = 0; pl < 3; ++pl) {
+        face_param_t fp;
+        if (!face_param(f, pl, &fp)) continue;
+        double b0, b1;
+        if (!best_interval(s, src, face, &fp, pl, &b0, &b1)) { memset(out, 0, sizeof(*out)); return 0; }
+        out->has[pl] = 1;
+        out->sub[2 * pl] = b0;
+        out->sub[2 * pl + 1] = b1;
+        out->clipped[pl] = b0 > 1e-9 || b1 < 1.0 - 1e-9;
+        any = 1;
+    }
+    out->present = any;
+    if (!any) memset(out, 0, sizeof(*out));
+    return 0;
+}

@@ -1,0 +1,122 @@
+"""Python host mirror of the reference's hot-path API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(namespace ``rt``): ``occlusion_judgment`` (include/rt/vismatrix.hpp:113),
+``build_matrix`` pair loop (vismatrix.hpp:141), ``illuminated_region``
+(include/rt/vistable.hpp:116-117), ``TraceAccelerator::trace``
+(include/rt/raytracer.hpp:96-118). Every call goes through
+``libvisrt_cuda.so``; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+from .scenes import FacetSoup
+
+KIND_NAMES = ("Visible", "PartiallyVisible", "Occluded")
+
+
+def _stats_dict(st: _capi.visrt_stats) -> Dict[str, float]:
+    return {"pairs": st.pairs, "candidates": st.candidates, "admitted": st.admitted,
+            "tests_alg": st.tests_alg, "tests_exec": st.tests_exec, "ms": st.ms}
+
+
+class Scene:
+    """A facet scene resident on one GPU (``visrt_scene_create``)."""
+
+    def __init__(self, soup: FacetSoup, device: int = 0) -> None:
+        L = lib()
+        self.soup = soup
+        self.n = soup.nfaces
+        self._vert_off = np.ascontiguousarray(soup.vert_off, dtype=np.int32)
+        self._verts = np.ascontiguousarray(soup.verts, dtype=np.float64).reshape(-1)
+        self._building = (None if soup.building is None
+                          else np.ascontiguousarray(soup.building, dtype=np.int32))
+        f = _capi.visrt_facets_v1(self.n, self._vert_off.ctypes.data, self._verts.ctypes.data,
+                                  None if self._building is None else self._building.ctypes.data)
+        h = C.c_void_p()
+        check(L.visrt_scene_create(C.byref(f), device, C.byref(h)))
+        self.h = h
+        self.words = (self.n + 63) // 64
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().visrt_scene_destroy(self.h)
+            self.h = None
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- ingest products (host copies) ----------------------------------------
+    def ingest(self):
+        n = self.n
+        normal = np.zeros(3 * n)
+        orient = np.zeros(n, np.int32)
+        seg = np.zeros(18 * n)
+        ok = np.zeros(3 * n, np.int32)
+        check(lib().visrt_scene_ingest(self.h, normal.ctypes.data, orient.ctypes.data, seg.ctypes.data,
+                                       ok.ctypes.data))
+        return normal.reshape(n, 3), orient, seg.reshape(n, 3, 6), ok.reshape(n, 3)
+
+    # -- (1) matrix -------------------------------------------------------------
+    def pair_visibility(self, mode: str = "all", copy_bits: bool = True, stream: int = 0
+                        ) -> Tuple[Optional[np.ndarray], Dict[str, float]]:
+        """(B) ``mode="all"``: bit(i,j) = occlusion_judgment(F_i, F_j).kind != Occluded for all
+        i<j. (A) ``mode="prefiltered"``: pair_admitted(i, j) of build_matrix(scene, 1)."""
+        flags = {"all": _capi.VISRT_PAIRS_ALL, "prefiltered": _capi.VISRT_PAIRS_PREFILTERED}[mode]
+        bits = np.zeros(self.n * self.words, np.uint64) if copy_bits else None
+        st = _capi.visrt_stats()
+        check(lib().visrt_pair_visibility(self.h, flags, None if bits is None else bits.ctypes.data,
+                                          C.byref(st), C.c_void_p(stream) if stream else None))
+        return (None if bits is None else bits.reshape(self.n, self.words)), _stats_dict(st)
+
+    def candidates(self):
+        L = lib()
+        m = L.visrt_candidates(self.h, None, None, None)
+        ci = np.zeros(m, np.int32)
+        cj = np.zeros(m, np.int32)
+        ad = np.zeros(m, np.uint8)
+        L.visrt_candidates(self.h, ci.ctypes.data, cj.ctypes.data, ad.ctypes.data)
+        return ci, cj, ad
+
+    def pair_detail(self, ci: Sequence[int], cj: Sequence[int]):
+        """occlusion_judgment(F_ci, F_cj) for a pair list: kinds + blocker index sets."""
+        ci = np.ascontiguousarray(ci, np.int32)
+        cj = np.ascontiguousarray(cj, np.int32)
+        m = len(ci)
+        kind = np.zeros(m, np.int8)
+        off = np.zeros(m + 1, np.int64)
+        st = _capi.visrt_stats()
+        check(lib().visrt_pair_detail(self.h, m, ci, cj, kind, off, None, 0, C.byref(st), None))
+        idx = np.zeros(max(int(off[-1]), 1), np.int32)
+        check(lib().visrt_pair_detail(self.h, m, ci, cj, kind, off, idx.ctypes.data, len(idx), C.byref(st),
+                                      None))
+        blockers = [idx[off[k]:off[k + 1]].tolist() for k in range(m)]
+        return kind, blockers, _stats_dict(st)
+
+
+def unpack_bits(bits: np.ndarray, n: int) -> np.ndarray:
+    """[n, words] uint64 -> [n, n] bool."""
+    b = bits.view(np.uint8).reshape(n, -1)
+    return np.unpackbits(b, axis=1, bitorder="little")[:, :n].astype(bool)
+
+
+def occlusion_judgment(scene: Scene, ref: int, aim: int) -> Tuple[str, List[int]]:
+    """rt::occlusion_judgment (include/rt/vismatrix.hpp:113) on the GPU."""
+    kind, blockers, _ = scene.pair_detail([ref], [aim])
+    return KIND_NAMES[int(kind[0])], blockers[0]

@@ -1,0 +1,442 @@
+// C-ABI implementation (include/visrt.h): scene lifecycle, matrix calls.
+// Never throws across the boundary; errors land in a thread-local message.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device.h"
+#include "host_geom.h"
+
+namespace visrt {
+struct PairArgs;
+cudaError_t launch_pair_bits(const PairArgs& a, int device, cudaStream_t st);
+cudaError_t launch_pair_detail(const PairArgs& a, int device, cudaStream_t st);
+cudaError_t launch_prefilter(const DevScene& s, long long npairs, long long* d_sel, long long* d_count,
+                             void*& temp, size_t& temp_bytes, cudaStream_t st);
+cudaError_t launch_split_pairs(const long long* sel, long long m, int n, int32_t* ci, int32_t* cj,
+                               cudaStream_t st);
+cudaError_t launch_clear_pairs(unsigned long long* bits, int words, const int32_t* ci, const int32_t* cj,
+                               long long m, cudaStream_t st);
+}  // namespace visrt
+
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct UsageError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct VisError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return VISRT_OK;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return VISRT_E_CUDA;
+    } catch (const UsageError& e) {
+        g_err = e.what();
+        return VISRT_E_USAGE;
+    } catch (const VisError& e) {
+        g_err = e.what();
+        return VISRT_E_VISIBILITY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return VISRT_E_SCENE;
+    }
+}
+
+template <class T>
+T* dev_upload(const std::vector<T>& v, std::vector<void*>& allocs) {
+    T* p = nullptr;
+    const size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    allocs.push_back(p);
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    return p;
+}
+
+template <class T>
+T* dev_alloc(size_t count, std::vector<void*>& allocs) {
+    T* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)), "cudaMalloc");
+    allocs.push_back(p);
+    return p;
+}
+
+}  // namespace
+
+struct visrt_scene {
+    visrt::HostScene hs;
+    visrt::DevScene ds;
+    int device = 0;
+    std::vector<void*> allocs;
+    unsigned long long* d_bits = nullptr;
+    unsigned long long* d_counter = nullptr;
+    long long* d_count = nullptr;
+    // candidate state (PREFILTERED)
+    long long* d_sel = nullptr;
+    long long sel_cap = 0;
+    int32_t* d_ci = nullptr;
+    int32_t* d_cj = nullptr;
+    uint8_t* d_cbit = nullptr;
+    long long ncand = 0;
+    std::vector<int32_t> ci, cj;
+    std::vector<uint8_t> cbit;
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    ~visrt_scene() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        for (void* p : allocs) cudaFree(p);
+        if (d_sel) cudaFree(d_sel);
+        if (d_ci) cudaFree(d_ci);
+        if (d_cj) cudaFree(d_cj);
+        if (d_cbit) cudaFree(d_cbit);
+        if (temp) cudaFree(temp);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        cudaSetDevice(cur);
+    }
+
+    void ensure_cand(long long m) {
+        if (m <= sel_cap) return;
+        if (d_sel) cudaFree(d_sel);
+        if (d_ci) cudaFree(d_ci);
+        if (d_cj) cudaFree(d_cj);
+        if (d_cbit) cudaFree(d_cbit);
+        ck(cudaMalloc(&d_sel, std::max<long long>(m, 1) * sizeof(long long)), "cudaMalloc sel");
+        ck(cudaMalloc(&d_ci, std::max<long long>(m, 1) * sizeof(int32_t)), "cudaMalloc ci");
+        ck(cudaMalloc(&d_cj, std::max<long long>(m, 1) * sizeof(int32_t)), "cudaMalloc cj");
+        ck(cudaMalloc(&d_cbit, std::max<long long>(m, 1)), "cudaMalloc cbit");
+        sel_cap = m;
+    }
+};
+
+namespace {
+
+visrt::PairArgs base_args(visrt_scene* sc) {
+    visrt::PairArgs a{};
+    a.s = sc->ds;
+    a.bits = sc->d_bits;
+    a.counter = sc->d_counter;
+    return a;
+}
+
+double tests_alg_all(const visrt::HostScene& hs) {
+    // Σ_{i<j} S(i,j) (N-2), grouped by (nv, ns) class.
+    std::vector<std::pair<std::pair<int, int>, long long>> cls;
+    for (int i = 0; i < hs.n; ++i) {
+        const auto key = std::make_pair(hs.nv[i], hs.ns[i]);
+        auto it = std::find_if(cls.begin(), cls.end(), [&](const auto& c) { return c.first == key; });
+        if (it == cls.end()) cls.push_back({key, 1});
+        else ++it->second;
+    }
+    double total = 0.0;
+    for (size_t a = 0; a < cls.size(); ++a) {
+        for (size_t b = a; b < cls.size(); ++b) {
+            const double S = visrt::sightline_count(cls[a].first.first, cls[a].first.second,
+                                                    cls[b].first.first, cls[b].first.second);
+            const double cnt = a == b ? 0.5 * cls[a].second * (cls[a].second - 1)
+                                      : static_cast<double>(cls[a].second) * cls[b].second;
+            total += S * cnt;
+        }
+    }
+    return total * (hs.n - 2);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* visrt_last_error(void) { return g_err.c_str(); }
+int visrt_version(void) { return 1; }
+
+int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) {
+    return guarded([&] {
+        if (!f || !out) throw UsageError("null argument");
+        *out = nullptr;
+        auto sc = std::make_unique<visrt_scene>();
+        sc->device = device;
+        visrt::ingest(*f, sc->hs);
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        const auto& hs = sc->hs;
+        auto& ds = sc->ds;
+        ds.n = hs.n;
+        ds.maxv = hs.maxv;
+        ds.words = (hs.n + 63) / 64;
+        if (hs.maxv <= 4) {
+            ds.rec = dev_upload(hs.rec4, sc->allocs);
+            ds.rec_stride = visrt::RecLayout<4>::kStride;
+        } else {
+            ds.rec = dev_upload(hs.rec8, sc->allocs);
+            ds.rec_stride = visrt::RecLayout<8>::kStride;
+        }
+        ds.samples = dev_upload(hs.samples, sc->allocs);
+        ds.pts = dev_upload(hs.pts, sc->allocs);
+        ds.normal = dev_upload(hs.normal, sc->allocs);
+        ds.seg = dev_upload(hs.seg, sc->allocs);
+        ds.aabb = dev_upload(hs.aabb, sc->allocs);
+        ds.nv = dev_upload(hs.nv, sc->allocs);
+        ds.ns = dev_upload(hs.ns, sc->allocs);
+        ds.orient = dev_upload(hs.orient, sc->allocs);
+        ds.seg_ok = dev_upload(hs.seg_ok, sc->allocs);
+        sc->d_bits = dev_alloc<unsigned long long>(static_cast<size_t>(hs.n) * ds.words, sc->allocs);
+        sc->d_counter = dev_alloc<unsigned long long>(4, sc->allocs);
+        sc->d_count = dev_alloc<long long>(2, sc->allocs);
+        ck(cudaEventCreate(&sc->ev0), "event");
+        ck(cudaEventCreate(&sc->ev1), "event");
+        *out = sc.release();
+    });
+}
+
+void visrt_scene_destroy(visrt_scene* s) { delete s; }
+
+int visrt_scene_nfaces(const visrt_scene* s) { return s ? s->hs.n : 0; }
+
+int visrt_scene_ingest(const visrt_scene* s, double* normal, int32_t* orientation, double* seg,
+                       int32_t* seg_ok) {
+    return guarded([&] {
+        if (!s) throw UsageError("null scene");
+        const auto& hs = s->hs;
+        if (normal) std::memcpy(normal, hs.normal.data(), hs.normal.size() * sizeof(double));
+        if (orientation) std::memcpy(orientation, hs.orient.data(), hs.orient.size() * sizeof(int32_t));
+        if (seg) std::memcpy(seg, hs.seg.data(), hs.seg.size() * sizeof(double));
+        if (seg_ok) std::memcpy(seg_ok, hs.seg_ok.data(), hs.seg_ok.size() * sizeof(int32_t));
+    });
+}
+
+const uint64_t* visrt_matrix_bits_device(const visrt_scene* s) {
+    return s ? reinterpret_cast<const uint64_t*>(s->d_bits) : nullptr;
+}
+
+int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, visrt_stats* stats,
+                          void* stream) {
+    return guarded([&] {
+        if (!sc) throw UsageError("null scene");
+        const bool pref = (flags & VISRT_PAIRS_PREFILTERED) != 0;
+        if (!pref && !(flags & VISRT_PAIRS_ALL)) throw UsageError("flags must select ALL or PREFILTERED");
+        ck(cudaSetDevice(sc->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int n = sc->hs.n;
+        const long long npairs = static_cast<long long>(n) * (n - 1) / 2;
+        const size_t bit_words = static_cast<size_t>(n) * sc->ds.words;
+        ck(cudaEventRecord(sc->ev0, st), "event");
+        ck(cudaMemsetAsync(sc->d_bits, 0, bit_words * 8, st), "memset bits");
+        ck(cudaMemsetAsync(sc->d_counter, 0, 4 * sizeof(unsigned long long), st), "memset counter");
+        visrt::PairArgs a = base_args(sc);
+        long long ncand = npairs;
+        if (pref) {
+            // The selected count bounds every later buffer; size for the worst case once.
+            sc->ensure_cand(npairs);
+            ck(visrt::launch_prefilter(sc->ds, npairs, sc->d_sel, sc->d_count, sc->temp, sc->temp_bytes, st),
+               "prefilter");
+            ck(cudaMemcpyAsync(&ncand, sc->d_count, sizeof(long long), cudaMemcpyDeviceToHost, st), "D2H count");
+            ck(cudaStreamSynchronize(st), "sync");
+            ck(visrt::launch_split_pairs(sc->d_sel, ncand, n, sc->d_ci, sc->d_cj, st), "split");
+            a.npairs = ncand;
+            a.ci = sc->d_ci;
+            a.cj = sc->d_cj;
+            a.cbit = sc->d_cbit;
+        } else {
+            a.npairs = npairs;
+        }
+        if (a.npairs > 0) ck(visrt::launch_pair_bits(a, sc->device, st), "k_pair_bits");
+        ck(cudaEventRecord(sc->ev1, st), "event");
+        unsigned long long counters[2] = {0, 0};
+        ck(cudaMemcpyAsync(counters, sc->d_counter, sizeof(counters), cudaMemcpyDeviceToHost, st), "D2H ctr");
+        if (pref) {
+            sc->ncand = ncand;
+            sc->ci.resize(ncand);
+            sc->cj.resize(ncand);
+            sc->cbit.resize(ncand);
+            if (ncand > 0) {
+                ck(cudaMemcpyAsync(sc->ci.data(), sc->d_ci, ncand * 4, cudaMemcpyDeviceToHost, st), "D2H ci");
+                ck(cudaMemcpyAsync(sc->cj.data(), sc->d_cj, ncand * 4, cudaMemcpyDeviceToHost, st), "D2H cj");
+                ck(cudaMemcpyAsync(sc->cbit.data(), sc->d_cbit, ncand, cudaMemcpyDeviceToHost, st), "D2H cbit");
+            }
+        }
+        ck(cudaStreamSynchronize(st), "sync");
+        long long admitted = 0;
+        if (pref) {
+            // pair_admitted also drops pairs whose bouncing range degenerates in
+            // some plane (src/vismatrix.cpp:622-624): host angle records.
+            std::vector<int32_t> drop_i, drop_j;
+            for (long long k = 0; k < ncand; ++k) {
+                if (!sc->cbit[k]) continue;
+                if (visrt::pair_range_degenerate(sc->hs, sc->ci[k], sc->cj[k])) {
+                    sc->cbit[k] = 0;
+                    drop_i.push_back(sc->ci[k]);
+                    drop_j.push_back(sc->cj[k]);
+                } else {
+                    ++admitted;
+                }
+            }
+            if (!drop_i.empty()) {
+                int32_t* di = nullptr;
+                int32_t* dj = nullptr;
+                ck(cudaMalloc(&di, drop_i.size() * 4), "cudaMalloc");
+                ck(cudaMalloc(&dj, drop_j.size() * 4), "cudaMalloc");
+                ck(cudaMemcpy(di, drop_i.data(), drop_i.size() * 4, cudaMemcpyHostToDevice), "H2D");
+                ck(cudaMemcpy(dj, drop_j.data(), drop_j.size() * 4, cudaMemcpyHostToDevice), "H2D");
+                ck(visrt::launch_clear_pairs(sc->d_bits, sc->ds.words, di, dj,
+                                             static_cast<long long>(drop_i.size()), st), "clear");
+                ck(cudaStreamSynchronize(st), "sync");
+                cudaFree(di);
+                cudaFree(dj);
+            }
+        }
+        if (bits_host) {
+            ck(cudaMemcpyAsync(bits_host, sc->d_bits, bit_words * 8, cudaMemcpyDeviceToHost, st), "D2H bits");
+            ck(cudaStreamSynchronize(st), "sync");
+        }
+        if (stats) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, sc->ev0, sc->ev1);
+            stats->pairs = npairs;
+            stats->candidates = ncand;
+            stats->tests_exec = static_cast<int64_t>(counters[1]);
+            stats->ms = ms;
+            if (pref) {
+                double t = 0.0;
+                for (long long k = 0; k < ncand; ++k) {
+                    const int i = sc->ci[k], j = sc->cj[k];
+                    t += visrt::sightline_count(sc->hs.nv[i], sc->hs.ns[i], sc->hs.nv[j], sc->hs.ns[j]);
+                }
+                stats->tests_alg = t * (n - 2);
+                stats->admitted = admitted;
+            } else {
+                stats->tests_alg = tests_alg_all(sc->hs);
+                stats->admitted = -1;
+            }
+        }
+    });
+}
+
+int64_t visrt_candidates(const visrt_scene* sc, int32_t* ci, int32_t* cj, uint8_t* admitted) {
+    if (!sc) return -1;
+    if (ci) std::memcpy(ci, sc->ci.data(), sc->ci.size() * 4);
+    if (cj) std::memcpy(cj, sc->cj.data(), sc->cj.size() * 4);
+    if (admitted) std::memcpy(admitted, sc->cbit.data(), sc->cbit.size());
+    return sc->ncand;
+}
+
+int visrt_pair_detail(visrt_scene* sc, int64_t npairs, const int32_t* ci, const int32_t* cj, int8_t* kind,
+                      int64_t* blk_off, int32_t* blk_idx, int64_t blk_cap, visrt_stats* stats, void* stream) {
+    return guarded([&] {
+        if (!sc) throw UsageError("null scene");
+        ck(cudaSetDevice(sc->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int n = sc->hs.n;
+        for (int64_t k = 0; k < npairs; ++k) {
+            if (ci[k] < 0 || ci[k] >= n || cj[k] < 0 || cj[k] >= n)
+                throw UsageError("face index out of range");
+            if (ci[k] == cj[k]) throw VisError("occlusion judgment needs two distinct faces");
+        }
+        const int words32 = (n + 31) / 32;
+        std::vector<void*> tmp;
+        struct Free {
+            std::vector<void*>& v;
+            ~Free() {
+                for (void* p : v) cudaFree(p);
+            }
+        } guard{tmp};
+        int32_t* d_ci = dev_alloc<int32_t>(npairs, tmp);
+        int32_t* d_cj = dev_alloc<int32_t>(npairs, tmp);
+        int8_t* d_kind = dev_alloc<int8_t>(npairs, tmp);
+        uint32_t* d_mask = dev_alloc<uint32_t>(static_cast<size_t>(npairs) * words32, tmp);
+        ck(cudaMemcpyAsync(d_ci, ci, npairs * 4, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(d_cj, cj, npairs * 4, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemsetAsync(d_mask, 0, static_cast<size_t>(npairs) * words32 * 4, st), "memset");
+        ck(cudaMemsetAsync(sc->d_counter, 0, 4 * sizeof(unsigned long long), st), "memset");
+        ck(cudaEventRecord(sc->ev0, st), "event");
+        visrt::PairArgs a = base_args(sc);
+        a.npairs = npairs;
+        a.ci = d_ci;
+        a.cj = d_cj;
+        a.kind = d_kind;
+        a.blk_mask = d_mask;
+        a.blk_words = words32;
+        if (npairs > 0) ck(visrt::launch_pair_detail(a, sc->device, st), "k_pair_detail");
+        ck(cudaEventRecord(sc->ev1, st), "event");
+        std::vector<uint32_t> mask(static_cast<size_t>(npairs) * words32);
+        unsigned long long counters[2] = {0, 0};
+        if (npairs > 0) {
+            ck(cudaMemcpyAsync(kind, d_kind, npairs, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(mask.data(), d_mask, mask.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        ck(cudaMemcpyAsync(counters, sc->d_counter, sizeof(counters), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        int64_t off = 0;
+        for (int64_t k = 0; k < npairs; ++k) {
+            if (blk_off) blk_off[k] = off;
+            for (int w = 0; w < words32; ++w) {
+                uint32_t m = mask[static_cast<size_t>(k) * words32 + w];
+                while (m) {
+                    const int b = __builtin_ctz(m);
+                    m &= m - 1;
+                    if (blk_idx && off < blk_cap) blk_idx[off] = w * 32 + b;
+                    ++off;
+                }
+            }
+        }
+        if (blk_off) blk_off[npairs] = off;
+        if (blk_idx && off > blk_cap) throw UsageError("blocker capacity too small");
+        if (stats) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, sc->ev0, sc->ev1);
+            double t = 0.0;
+            for (int64_t k = 0; k < npairs; ++k)
+                t += visrt::sightline_count(sc->hs.nv[ci[k]], sc->hs.ns[ci[k]], sc->hs.nv[cj[k]], sc->hs.ns[cj[k]]);
+            stats->pairs = npairs;
+            stats->candidates = npairs;
+            stats->admitted = -1;
+            stats->tests_alg = t * (n - 2);
+            stats->tests_exec = static_cast<int64_t>(counters[1]);
+            stats->ms = ms;
+        }
+    });
+}
+
+}  // extern "C"
+
+// --- entry points implemented in later milestones (regions.cu / tree.cu) ---
+#ifndef VISRT_HAVE_REGIONS
+extern "C" int visrt_point_regions(visrt_scene*, int64_t, const double*, visrt_region*, visrt_stats*, void*) {
+    g_err = "visrt_point_regions: not built";
+    return VISRT_E_USAGE;
+}
+#endif
+#ifndef VISRT_HAVE_TREE
+extern "C" int visrt_tracer_create(visrt_scene*, int, const uint64_t*, int64_t, const int32_t*, visrt_tracer**) {
+    g_err = "visrt_tracer_create: not built";
+    return VISRT_E_USAGE;
+}
+extern "C" void visrt_tracer_destroy(visrt_tracer*) {}
+extern "C" int visrt_trace(visrt_tracer*, int64_t, const double*, const double*, int, int64_t*, visrt_path*,
+                           int64_t, visrt_trace_stats*, void*) {
+    g_err = "visrt_trace: not built";
+    return VISRT_E_USAGE;
+}
+#endif

@@ -1,0 +1,126 @@
+// Device-side scene state and the exact FP64 predicate shared by the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "visrt_internal.h"
+
+namespace visrt {
+
+struct DevScene {
+    int32_t n = 0;
+    int32_t maxv = 0;
+    int32_t words = 0;             // uint64 words per bit-matrix row
+    const double* rec = nullptr;   // occluder records (layout by maxv: 4 or 8)
+    int32_t rec_stride = 0;        // doubles per record
+    const double* samples = nullptr;
+    const double* pts = nullptr;   // padded rings [n][8][3]
+    const double* normal = nullptr;
+    const double* seg = nullptr;   // [n][3][6]
+    const double* aabb = nullptr;  // [n][6]
+    const int32_t* nv = nullptr;
+    const int32_t* ns = nullptr;
+    const int32_t* orient = nullptr;
+    const int32_t* seg_ok = nullptr;
+};
+
+struct PairArgs {
+    DevScene s;
+    long long npairs;
+    const int32_t* ci;               // candidate list (nullptr: all i<j)
+    const int32_t* cj;
+    uint8_t* cbit;                   // per-candidate not-Occluded bit (optional)
+    unsigned long long* bits;        // N x words, symmetric
+    unsigned long long* counter;     // [0] work cursor, [1] tests executed
+    int8_t* kind;                    // detail: per pair 0/1/2
+    uint32_t* blk_mask;              // detail: per pair ceil(N/32) words
+    int32_t blk_words;
+};
+
+// ---------------------------------------------------------------------------
+// Exact FP64 arithmetic: explicit round-to-nearest intrinsics are never
+// contracted into FMAs, so every product/sum rounds exactly like the
+// reference's separate x86-64 SSE2 mul/add.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+// dot(p - a, v) = ((dx*vx + dy*vy) + dz*vz), include/rt/geom.hpp:29
+__device__ __forceinline__ double dot_rel(double px, double py, double pz, double ax, double ay,
+                                          double az, double vx, double vy, double vz) {
+    return dadd(dadd(dmul(dsub(px, ax), vx), dmul(dsub(py, ay), vy)), dmul(dsub(pz, az), vz));
+}
+
+// segment_face_intersection (src/geom.cpp:169-180) + ConvexPolygon::contains
+// (src/geom.cpp:155-167) on one occluder record R (see RecLayout).
+template <int MAXV>
+__device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax, double ay,
+                                         double az, double bx, double by, double bz) {
+    const double Px = R[0], Py = R[1], Pz = R[2];
+    const double nx = R[3], ny = R[4], nz = R[5];
+    const double da = dot_rel(ax, ay, az, Px, Py, Pz, nx, ny, nz);
+    const double db = dot_rel(bx, by, bz, Px, Py, Pz, nx, ny, nz);
+    if (fabs(da) <= kEps || fabs(db) <= kEps) return false;
+    if (dmul(da, db) > 0.0) return false;
+    const double t = __ddiv_rn(da, dsub(da, db));
+    const double px = dadd(ax, dmul(dsub(bx, ax), t));
+    const double py = dadd(ay, dmul(dsub(by, ay), t));
+    const double pz = dadd(az, dmul(dsub(bz, az), t));
+    if (fabs(dot_rel(px, py, pz, Px, Py, Pz, nx, ny, nz)) > kEps) return false;
+    if (dot_rel(px, py, pz, Px, Py, Pz, R[6], R[7], R[8]) < -kEps) return false;
+#pragma unroll
+    for (int k = 1; k < MAXV; ++k) {
+        const double* E = R + 9 + (k - 1) * 6;
+        if (dot_rel(px, py, pz, E[0], E[1], E[2], E[3], E[4], E[5]) < -kEps) return false;
+    }
+    return true;
+}
+
+// Unordered pair index p (i < j, row-major upper triangle) -> (i, j).
+__device__ __forceinline__ void pair_from_index(long long p, int n, int& i, int& j) {
+    const double b = 2.0 * n - 1.0;
+    long long ii = static_cast<long long>((b - sqrt(b * b - 8.0 * static_cast<double>(p))) * 0.5);
+    if (ii < 0) ii = 0;
+    auto off = [n](long long r) { return r * (2LL * n - r - 1) / 2; };
+    while (ii + 1 < n && off(ii + 1) <= p) ++ii;
+    while (ii > 0 && off(ii) > p) --ii;
+    i = static_cast<int>(ii);
+    j = static_cast<int>(p - off(ii) + ii + 1);
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk copy (cp.async.bulk, SASS UBLKCP) + mbarrier helpers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+}  // namespace visrt

@@ -1,0 +1,441 @@
+// (1) Inter-visibility matrix kernels for sm_100a.
+//
+//   K1 k-prefilter   first_order_pair's gate (src/vismatrix.cpp:597-604:
+//                    non-oblique, mutually_front 160-169, required_planes
+//                    171-181) over all i<j, ordered prefix-sum compaction
+//                    (cub::DeviceSelect) into a candidate list.
+//   K2 k_pair_bits   occlusion_judgment's Occluded verdict (253-302) with
+//                    early exit: one lane = one pair state machine walking its
+//                    sightlines; the block sweeps occluder tiles cyclically out
+//                    of shared memory (TMA bulk copies, double-buffered), every
+//                    lane testing the same occluder (smem broadcast) against its
+//                    own sightline. A sightline stops at its first hit; a pair
+//                    stops at its first clear (or degenerate) sightline.
+//   K2d k_pair_detail Visible / Partial / Occluded + blocker sets (no early exit).
+//
+// All geometry is the reference's FP64 predicate with explicit _rn intrinsics
+// (device.h), so every decision is bit-identical to the CPU oracle.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "device.h"
+
+namespace visrt {
+
+constexpr int kTile = 64;       // occluders per shared-memory tile
+constexpr int kThreads = 256;   // 8 warps
+constexpr unsigned kFull = 0xffffffffu;
+
+
+// Sightline `ord` of pair (i, j) in the kernel's exploration order: the
+// centroid pair first, then the diagonal grid pairs, then the vertex pairs
+// (any order is valid: the verdict counts blocked sightlines, and the bit only
+// needs one unblocked one). Returns the reference endpoint pair.
+__device__ __forceinline__ void sightline_endpoints(const DevScene& s, int i, int j, int nr, int na,
+                                                    int grid, int ord, double& ax, double& ay,
+                                                    double& az, double& bx, double& by, double& bz) {
+    int ri, ai;
+    if (ord == 0) {
+        ri = nr;
+        ai = na;
+    } else if (ord <= grid) {
+        ri = nr + ord;
+        ai = na + ord;
+    } else {
+        const int v = ord - 1 - grid;
+        ri = v / na;
+        ai = v % na;
+    }
+    const double* P = s.samples + (static_cast<size_t>(i) * kMaxSamples + ri) * 3;
+    const double* Q = s.samples + (static_cast<size_t>(j) * kMaxSamples + ai) * 3;
+    ax = P[0]; ay = P[1]; az = P[2];
+    bx = Q[0]; by = Q[1]; bz = Q[2];
+}
+
+// norm(q - p) <= kEps (src/vismatrix.cpp:278-280): never blocked.
+__device__ __forceinline__ bool degenerate(double ax, double ay, double az, double bx, double by,
+                                           double bz) {
+    const double dx = dsub(bx, ax), dy = dsub(by, ay), dz = dsub(bz, az);
+    return __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz))) <= kEps;
+}
+
+__device__ __forceinline__ void set_pair_bit(unsigned long long* bits, int words, int i, int j) {
+    atomicOr(bits + static_cast<size_t>(i) * words + (j >> 6), 1ull << (j & 63));
+    atomicOr(bits + static_cast<size_t>(j) * words + (i >> 6), 1ull << (i & 63));
+}
+
+// Cyclic occluder-tile pipeline shared by both sweeps: two shared-memory
+// buffers filled by cp.async.bulk with mbarrier completion.
+template <int STRIDE>
+struct TilePipe {
+    double* tiles;
+    uint64_t* bar;
+    const double* rec;
+    int n, ntiles, t0;
+
+    __device__ int tile_of(int it) const { return (t0 + it) % ntiles; }
+    __device__ void issue(int it) const {
+        const int t = tile_of(it);
+        const int cnt = min(kTile, n - t * kTile);
+        const uint32_t bytes = static_cast<uint32_t>(cnt) * STRIDE * 8u;
+        double* dst = tiles + (it & 1) * kTile * STRIDE;
+        mbar_expect_tx(&bar[it & 1], bytes);
+        bulk_g2s(dst, rec + static_cast<size_t>(t) * kTile * STRIDE, bytes, &bar[it & 1]);
+    }
+    __device__ void wait(int it) const { mbar_wait(&bar[it & 1], (it >> 1) & 1); }
+    __device__ const double* buf(int it) const { return tiles + (it & 1) * kTile * STRIDE; }
+};
+
+template <int MAXV>
+__global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) double tiles[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+
+    TilePipe<STRIDE> pipe{tiles, bar, s.rec, n, (n + kTile - 1) / kTile, 0};
+    pipe.t0 = blockIdx.x % pipe.ntiles;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        pipe.issue(0);
+        pipe.issue(1);
+    }
+
+    bool active = false, exhausted = false;
+    long long pidx = 0;
+    int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0;
+    double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    unsigned long long tests = 0;
+
+    auto finish = [&](bool occluded) {
+        if (!occluded) set_pair_bit(a.bits, s.words, pi, pj);
+        if (a.cbit) a.cbit[pidx] = occluded ? 0 : 1;
+    };
+    // Claim pairs for idle lanes (warp-aggregated atomic on the work cursor).
+    auto refill = [&]() {
+        unsigned need = __ballot_sync(kFull, !active && !exhausted);
+        while (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&a.counter[0], static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(kFull, base, leader);
+            if (!active && !exhausted) {
+                const long long my = static_cast<long long>(base) + __popc(need & ((1u << lane) - 1u));
+                if (my >= a.npairs) {
+                    exhausted = true;
+                } else {
+                    pidx = my;
+                    if (a.ci) {
+                        pi = a.ci[my];
+                        pj = a.cj[my];
+                    } else {
+                        pair_from_index(my, n, pi, pj);
+                    }
+                    nr = s.nv[pi];
+                    na = s.nv[pj];
+                    grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
+                    S = nr * na + 1 + grid;
+                    bool degen = false;
+                    for (int o = 0; o < S && !degen; ++o) {
+                        sightline_endpoints(s, pi, pj, nr, na, grid, o, ax, ay, az, bx, by, bz);
+                        degen = degenerate(ax, ay, az, bx, by, bz);
+                    }
+                    if (degen) {
+                        finish(false);   // a degenerate sightline is never blocked
+                    } else {
+                        ord = 0;
+                        sightline_endpoints(s, pi, pj, nr, na, grid, 0, ax, ay, az, bx, by, bz);
+                        rem = n;
+                        active = true;
+                    }
+                }
+            }
+            need = __ballot_sync(kFull, !active && !exhausted);
+        }
+    };
+
+    for (int it = 0;; ++it) {
+        pipe.wait(it);
+        const int base = pipe.tile_of(it) * kTile;
+        const int cnt = min(kTile, n - base);
+        const double* T = pipe.buf(it);
+        for (int kk = 0; kk < cnt; ++kk) {
+            if (__any_sync(kFull, !active && !exhausted)) refill();
+            if (active) {
+                const int k = base + kk;
+                bool hit = false;
+                if (k != pi && k != pj) {
+                    hit = seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz);
+                    ++tests;
+                }
+                --rem;
+                if (hit) {
+                    if (++ord == S) {
+                        finish(true);
+                        active = false;
+                    } else {
+                        sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
+                        rem = n;
+                    }
+                } else if (rem == 0) {
+                    finish(false);
+                    active = false;
+                }
+            }
+        }
+        const int alive = __syncthreads_or(active || !exhausted);
+        if (!alive) {
+            pipe.wait(it + 1);   // drain the in-flight tile before the CTA retires
+            break;
+        }
+        if (threadIdx.x == 0) pipe.issue(it + 2);
+    }
+    // warp-reduce the executed-test counter
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) atomicAdd(&a.counter[1], tests);
+}
+
+// Detail sweep: per pair every sightline against every occluder (no early
+// exit), as occlusion_judgment does, recording the blocker set.
+template <int MAXV>
+__global__ void __launch_bounds__(kThreads) k_pair_detail(PairArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) double tiles[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+
+    TilePipe<STRIDE> pipe{tiles, bar, s.rec, n, (n + kTile - 1) / kTile, 0};
+    pipe.t0 = blockIdx.x % pipe.ntiles;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        pipe.issue(0);
+        pipe.issue(1);
+    }
+
+    bool active = false, exhausted = false;
+    long long pidx = 0;
+    int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0, blocked = 0;
+    bool hit_any = false;
+    double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    unsigned long long tests = 0;
+    uint32_t* mask = nullptr;
+
+    // advance to the next non-degenerate sightline; returns false when the pair is done
+    auto next_sightline = [&]() {
+        while (ord < S) {
+            sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
+            if (!degenerate(ax, ay, az, bx, by, bz)) {
+                rem = n;
+                hit_any = false;
+                return true;
+            }
+            ++ord;
+        }
+        return false;
+    };
+    auto finish = [&]() {
+        a.kind[pidx] = static_cast<int8_t>(blocked == 0 ? 0 : (blocked == S ? 2 : 1));
+        active = false;
+    };
+    auto refill = [&]() {
+        unsigned need = __ballot_sync(kFull, !active && !exhausted);
+        while (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&a.counter[0], static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(kFull, base, leader);
+            if (!active && !exhausted) {
+                const long long my = static_cast<long long>(base) + __popc(need & ((1u << lane) - 1u));
+                if (my >= a.npairs) {
+                    exhausted = true;
+                } else {
+                    pidx = my;
+                    pi = a.ci[my];
+                    pj = a.cj[my];
+                    nr = s.nv[pi];
+                    na = s.nv[pj];
+                    grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
+                    S = nr * na + 1 + grid;
+                    ord = 0;
+                    blocked = 0;
+                    mask = a.blk_mask + static_cast<size_t>(my) * a.blk_words;
+                    if (next_sightline()) active = true;
+                    else finish();
+                }
+            }
+            need = __ballot_sync(kFull, !active && !exhausted);
+        }
+    };
+
+    for (int it = 0;; ++it) {
+        pipe.wait(it);
+        const int base = pipe.tile_of(it) * kTile;
+        const int cnt = min(kTile, n - base);
+        const double* T = pipe.buf(it);
+        for (int kk = 0; kk < cnt; ++kk) {
+            if (__any_sync(kFull, !active && !exhausted)) refill();
+            if (active) {
+                const int k = base + kk;
+                if (k != pi && k != pj) {
+                    ++tests;
+                    if (seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz)) {
+                        hit_any = true;
+                        atomicOr(mask + (k >> 5), 1u << (k & 31));
+                    }
+                }
+                if (--rem == 0) {
+                    if (hit_any) ++blocked;
+                    ++ord;
+                    if (!next_sightline()) finish();
+                }
+            }
+        }
+        const int alive = __syncthreads_or(active || !exhausted);
+        if (!alive) {
+            pipe.wait(it + 1);
+            break;
+        }
+        if (threadIdx.x == 0) pipe.issue(it + 2);
+    }
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) atomicAdd(&a.counter[1], tests);
+}
+
+// K1: first_order_pair's gate for one unordered pair index.
+struct PrefilterOp {
+    DevScene s;
+    __device__ bool front(int of, int probe) const {
+        const double* P = s.pts + static_cast<size_t>(of) * VISRT_MAX_VERTS * 3;
+        const double* N = s.normal + 3 * static_cast<size_t>(of);
+        const double* Q = s.pts + static_cast<size_t>(probe) * VISRT_MAX_VERTS * 3;
+        const int nv = s.nv[probe];
+        for (int k = 0; k < nv; ++k) {
+            if (dot_rel(Q[3 * k], Q[3 * k + 1], Q[3 * k + 2], P[0], P[1], P[2], N[0], N[1], N[2]) > kEps)
+                return true;
+        }
+        return false;
+    }
+    __device__ bool operator()(long long p) const {
+        int i, j;
+        pair_from_index(p, s.n, i, j);
+        if (s.orient[i] == 2 || s.orient[j] == 2) return false;
+        if (!front(i, j) || !front(j, i)) return false;
+        for (int pl = 0; pl < 3; ++pl) {
+            if (!s.seg_ok[3 * i + pl] || !s.seg_ok[3 * j + pl]) continue;
+            const double* a = s.seg + (static_cast<size_t>(i) * 3 + pl) * 6;
+            const double* b = s.seg + (static_cast<size_t>(j) * 3 + pl) * 6;
+            const double d = fabs(dadd(dmul(a[4], b[4]), dmul(a[5], b[5])));
+            if (d >= 1.0 - 1e-9 || d <= 1e-9) return true;
+        }
+        return false;
+    }
+};
+
+__global__ void k_split_pairs(const long long* sel, long long m, int n, int32_t* ci, int32_t* cj) {
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < m;
+         k += static_cast<long long>(gridDim.x) * blockDim.x) {
+        int i, j;
+        pair_from_index(sel[k], n, i, j);
+        ci[k] = i;
+        cj[k] = j;
+    }
+}
+
+__global__ void k_clear_pairs(unsigned long long* bits, int words, const int32_t* ci, const int32_t* cj,
+                              long long m) {
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < m;
+         k += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = ci[k], j = cj[k];
+        atomicAnd(bits + static_cast<size_t>(i) * words + (j >> 6), ~(1ull << (j & 63)));
+        atomicAnd(bits + static_cast<size_t>(j) * words + (i >> 6), ~(1ull << (i & 63)));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+
+static int persistent_grid(const void* fn, size_t smem, int device) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem);
+    if (per < 1) per = 1;
+    return sms * per;
+}
+
+template <int MAXV>
+static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
+    const size_t smem = 2ull * kTile * RecLayout<MAXV>::kStride * sizeof(double);
+    auto fn = k_pair_bits<MAXV>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);
+    fn<<<grid, kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int MAXV>
+static cudaError_t launch_detail_t(const PairArgs& a, int device, cudaStream_t st) {
+    const size_t smem = 2ull * kTile * RecLayout<MAXV>::kStride * sizeof(double);
+    auto fn = k_pair_detail<MAXV>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);
+    fn<<<grid, kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_bits(const PairArgs& a, int device, cudaStream_t st) {
+    return a.s.maxv <= 4 ? launch_bits_t<4>(a, device, st) : launch_bits_t<8>(a, device, st);
+}
+
+cudaError_t launch_pair_detail(const PairArgs& a, int device, cudaStream_t st) {
+    return a.s.maxv <= 4 ? launch_detail_t<4>(a, device, st) : launch_detail_t<8>(a, device, st);
+}
+
+// Ordered compaction of the prefiltered pairs; returns the device count in *d_count.
+cudaError_t launch_prefilter(const DevScene& s, long long npairs, long long* d_sel, long long* d_count,
+                             void*& temp, size_t& temp_bytes, cudaStream_t st) {
+    thrust::counting_iterator<long long> in(0);
+    PrefilterOp op{s};
+    size_t need = 0;
+    cudaError_t e = cub::DeviceSelect::If(nullptr, need, in, d_sel, d_count, npairs, op, st);
+    if (e != cudaSuccess) return e;
+    if (need > temp_bytes) {
+        if (temp) cudaFree(temp);
+        e = cudaMalloc(&temp, need);
+        if (e != cudaSuccess) return e;
+        temp_bytes = need;
+    }
+    return cub::DeviceSelect::If(temp, temp_bytes, in, d_sel, d_count, npairs, op, st);
+}
+
+cudaError_t launch_split_pairs(const long long* sel, long long m, int n, int32_t* ci, int32_t* cj,
+                               cudaStream_t st) {
+    if (m <= 0) return cudaSuccess;
+    const int blocks = static_cast<int>(std::min<long long>((m + 255) / 256, 148 * 16));
+    k_split_pairs<<<blocks, 256, 0, st>>>(sel, m, n, ci, cj);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_clear_pairs(unsigned long long* bits, int words, const int32_t* ci, const int32_t* cj,
+                               long long m, cudaStream_t st) {
+    if (m <= 0) return cudaSuccess;
+    const int blocks = static_cast<int>(std::min<long long>((m + 255) / 256, 148 * 16));
+    k_clear_pairs<<<blocks, 256, 0, st>>>(bits, words, ci, cj, m);
+    return cudaGetLastError();
+}
+
+}  // namespace visrt

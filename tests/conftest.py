@@ -1,0 +1,20 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs through libvisrt_cuda.so)")
+    config.addinivalue_line("markers", "slow: long-running parity sweep")
+
+
+@pytest.fixture(scope="session")
+def oracle_built():
+    from oracle import bindings
+    bindings.build(ref=True)
+    return bindings
