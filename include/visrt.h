@@ -75,6 +75,11 @@ int visrt_scene_nfaces(const visrt_scene* scene);
  * plane segments seg[n*3*6] (a.x a.y b.x b.y n.x n.y), seg_ok[n*3]. Any NULL skipped. */
 int visrt_scene_ingest(const visrt_scene* scene, double* normal, int32_t* orientation,
                        double* seg, int32_t* seg_ok);
+/* Bytes the scene upload copied host->device (the e2e H2D accounting). */
+int64_t visrt_scene_upload_bytes(const visrt_scene* scene);
+/* Measured device FP64 / FP32 arithmetic peaks (non-FMA DADD+DMUL ops/s and
+ * FFMA-counted flop/s) from a short microbenchmark on `device`. */
+int visrt_measure_peaks(int device, double* fp64_ops_per_s, double* fp32_flops_per_s);
 
 /* (1) Inter-visibility matrix.
  * flags: VISRT_PAIRS_ALL        — (B) every i<j, bit = occlusion verdict != Occluded;

@@ -25,7 +25,8 @@ _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 # every symbol include/visrt.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "visrt_last_error", "visrt_version", "visrt_scene_create", "visrt_scene_destroy",
-    "visrt_scene_nfaces", "visrt_scene_ingest", "visrt_pair_visibility", "visrt_matrix_bits_device",
+    "visrt_scene_nfaces", "visrt_scene_ingest", "visrt_scene_upload_bytes", "visrt_measure_peaks",
+    "visrt_pair_visibility", "visrt_matrix_bits_device",
     "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace",
 ]
@@ -101,6 +102,9 @@ def lib():
     L.visrt_scene_destroy.argtypes = [C.c_void_p]
     L.visrt_scene_nfaces.argtypes = [C.c_void_p]
     L.visrt_scene_ingest.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.visrt_scene_upload_bytes.restype = C.c_int64
+    L.visrt_scene_upload_bytes.argtypes = [C.c_void_p]
+    L.visrt_measure_peaks.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.visrt_pair_visibility.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(visrt_stats),
                                         C.c_void_p]
     L.visrt_matrix_bits_device.restype = C.c_void_p

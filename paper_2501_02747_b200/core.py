@@ -62,6 +62,10 @@ class Scene:
     def __exit__(self, *exc):
         self.close()
 
+    @property
+    def upload_bytes(self) -> int:
+        return int(lib().visrt_scene_upload_bytes(self.h))
+
     # -- ingest products (host copies) ----------------------------------------
     def ingest(self):
         n = self.n
@@ -108,6 +112,14 @@ class Scene:
                                       None))
         blockers = [idx[off[k]:off[k + 1]].tolist() for k in range(m)]
         return kind, blockers, _stats_dict(st)
+
+
+def measure_peaks(device: int = 0) -> Tuple[float, float]:
+    """(FP64 non-FMA ops/s, FP32 FFMA flop/s) measured on `device`."""
+    f64 = C.c_double()
+    f32 = C.c_double()
+    check(lib().visrt_measure_peaks(device, C.byref(f64), C.byref(f32)))
+    return f64.value, f32.value
 
 
 def unpack_bits(bits: np.ndarray, n: int) -> np.ndarray:

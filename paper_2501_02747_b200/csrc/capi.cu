@@ -89,6 +89,7 @@ struct visrt_scene {
     visrt::DevScene ds;
     int device = 0;
     std::vector<void*> allocs;
+    int64_t upload_bytes = 0;
     unsigned long long* d_bits = nullptr;
     unsigned long long* d_counter = nullptr;
     long long* d_count = nullptr;
@@ -202,6 +203,14 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.ns = dev_upload(hs.ns, sc->allocs);
         ds.orient = dev_upload(hs.orient, sc->allocs);
         ds.seg_ok = dev_upload(hs.seg_ok, sc->allocs);
+        ds.box = dev_upload(hs.box, sc->allocs);
+        sc->upload_bytes = static_cast<int64_t>(
+            (hs.maxv <= 4 ? hs.rec4.size() : hs.rec8.size()) * 8 + hs.samples.size() * 8 + hs.pts.size() * 8 +
+            hs.normal.size() * 8 + hs.seg.size() * 8 + hs.aabb.size() * 8 + hs.nv.size() * 4 + hs.ns.size() * 4 +
+            hs.orient.size() * 4 + hs.seg_ok.size() * 4 + hs.box.size() * 4);
+        ds.ox = hs.origin[0];
+        ds.oy = hs.origin[1];
+        ds.oz = hs.origin[2];
         sc->d_bits = dev_alloc<unsigned long long>(static_cast<size_t>(hs.n) * ds.words, sc->allocs);
         sc->d_counter = dev_alloc<unsigned long long>(4, sc->allocs);
         sc->d_count = dev_alloc<long long>(2, sc->allocs);
@@ -214,6 +223,8 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
 void visrt_scene_destroy(visrt_scene* s) { delete s; }
 
 int visrt_scene_nfaces(const visrt_scene* s) { return s ? s->hs.n : 0; }
+
+int64_t visrt_scene_upload_bytes(const visrt_scene* s) { return s ? s->upload_bytes : 0; }
 
 int visrt_scene_ingest(const visrt_scene* s, double* normal, int32_t* orientation, double* seg,
                        int32_t* seg_ok) {

@@ -24,7 +24,46 @@ struct DevScene {
     const int32_t* ns = nullptr;
     const int32_t* orient = nullptr;
     const int32_t* seg_ok = nullptr;
+    const float* box = nullptr;    // [n][8] fp32 culling boxes (centre rel. origin, dilated half)
+    double ox = 0, oy = 0, oz = 0; // box origin
 };
+
+// A sightline in the fp32 culling frame: midpoint (relative to the scene
+// origin), half extent and its absolute value.
+struct SegF {
+    float mx, my, mz, ex, ey, ez, ax, ay, az;
+};
+
+__device__ __forceinline__ SegF make_segf(const DevScene& s, double ax, double ay, double az, double bx,
+                                          double by, double bz) {
+    SegF g;
+    g.mx = static_cast<float>(0.5 * (ax + bx) - s.ox);
+    g.my = static_cast<float>(0.5 * (ay + by) - s.oy);
+    g.mz = static_cast<float>(0.5 * (az + bz) - s.oz);
+    g.ex = static_cast<float>(0.5 * (bx - ax));
+    g.ey = static_cast<float>(0.5 * (by - ay));
+    g.ez = static_cast<float>(0.5 * (bz - az));
+    g.ax = fabsf(g.ex);
+    g.ay = fabsf(g.ey);
+    g.az = fabsf(g.ez);
+    return g;
+}
+
+// Conservative segment-vs-box separating-axis test in fp32 (3 box axes + 3
+// edge-cross axes). false => the segment cannot meet the face (the box is
+// dilated by box_margin(), which bounds every fp32 rounding here), so the
+// exact FP64 predicate is skipped; true => run the exact predicate.
+__device__ __forceinline__ bool sat_maybe(const float* __restrict__ B, const SegF& g) {
+    const float dx = g.mx - B[0], dy = g.my - B[1], dz = g.mz - B[2];
+    const float hx = B[4], hy = B[5], hz = B[6];
+    bool ok = fabsf(dx) <= hx + g.ax;
+    ok &= fabsf(dy) <= hy + g.ay;
+    ok &= fabsf(dz) <= hz + g.az;
+    ok &= fabsf(__fmaf_rn(dy, g.ez, -dz * g.ey)) <= __fmaf_rn(hy, g.az, hz * g.ay);
+    ok &= fabsf(__fmaf_rn(dz, g.ex, -dx * g.ez)) <= __fmaf_rn(hx, g.az, hz * g.ax);
+    ok &= fabsf(__fmaf_rn(dx, g.ey, -dy * g.ex)) <= __fmaf_rn(hx, g.ay, hy * g.ax);
+    return ok;
+}
 
 struct PairArgs {
     DevScene s;

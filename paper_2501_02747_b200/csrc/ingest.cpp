@@ -7,6 +7,7 @@
 //   plane_segment (XY/YZ/XZ)         src/scene.cpp:213-254
 //   contains() per-edge inward       src/geom.cpp:155-167
 //   face_samples / centroid          src/vismatrix.cpp:226-249, src/geom.cpp:142-146
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <stdexcept>
@@ -191,6 +192,46 @@ void ingest(const visrt_facets_v1& f, HostScene& hs) {
         }
         double* bb = &hs.aabb[static_cast<size_t>(i) * 6];
         bb[0] = lo.x; bb[1] = lo.y; bb[2] = lo.z; bb[3] = hi.x; bb[4] = hi.y; bb[5] = hi.z;
+    }
+    // fp32 culling boxes relative to the scene centre.
+    {
+        double lo[3] = {hs.aabb[0], hs.aabb[1], hs.aabb[2]};
+        double hi[3] = {hs.aabb[3], hs.aabb[4], hs.aabb[5]};
+        for (int i = 0; i < n; ++i)
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = smin(lo[d], hs.aabb[6 * i + d]);
+                hi[d] = smax(hi[d], hs.aabb[6 * i + 3 + d]);
+            }
+        hs.extent = 0;
+        for (int d = 0; d < 3; ++d) {
+            hs.origin[d] = std::floor(0.5 * (lo[d] + hi[d]));
+            hs.extent = smax(hs.extent, smax(std::abs(hi[d] - hs.origin[d]), std::abs(lo[d] - hs.origin[d])));
+        }
+        hs.box.assign(static_cast<size_t>(n) * 8, 0.0f);
+        for (int i = 0; i < n; ++i) {
+            // eps-miter of the face: 1e-9 / sin(theta/2) at its sharpest vertex
+            double miter = 1e-9;
+            const int nv = hs.nv[i];
+            for (int k = 0; k < nv; ++k) {
+                const double* p0 = &hs.pts[(static_cast<size_t>(i) * VISRT_MAX_VERTS + (k + nv - 1) % nv) * 3];
+                const double* p1 = &hs.pts[(static_cast<size_t>(i) * VISRT_MAX_VERTS + k) * 3];
+                const double* p2 = &hs.pts[(static_cast<size_t>(i) * VISRT_MAX_VERTS + (k + 1) % nv) * 3];
+                const V3 u = sub({p0[0], p0[1], p0[2]}, {p1[0], p1[1], p1[2]});
+                const V3 v = sub({p2[0], p2[1], p2[2]}, {p1[0], p1[1], p1[2]});
+                const double nu = norm(u), nvv = norm(v);
+                if (nu < kEps || nvv < kEps) { miter = 1.0; continue; }   // degenerate edge: be generous
+                const double c = std::max(-1.0, std::min(1.0, dot(u, v) / (nu * nvv)));
+                const double s = std::sin(0.5 * std::acos(c));
+                miter = std::max(miter, s > 1e-12 ? 2e-9 / s : 1.0);
+            }
+            const double m = box_margin(hs.extent, miter);
+            const double* bb = &hs.aabb[static_cast<size_t>(i) * 6];
+            float* o = &hs.box[static_cast<size_t>(i) * 8];
+            for (int d = 0; d < 3; ++d) {
+                o[d] = static_cast<float>(0.5 * (bb[d] + bb[3 + d]) - hs.origin[d]);
+                o[4 + d] = static_cast<float>(0.5 * (bb[3 + d] - bb[d]) + m);
+            }
+        }
     }
     // Occluder records in the narrowest layout that fits.
     if (hs.maxv <= 4) {

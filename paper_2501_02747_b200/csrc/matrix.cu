@@ -63,62 +63,112 @@ __device__ __forceinline__ void set_pair_bit(unsigned long long* bits, int words
     atomicOr(bits + static_cast<size_t>(i) * words + (j >> 6), 1ull << (j & 63));
     atomicOr(bits + static_cast<size_t>(j) * words + (i >> 6), 1ull << (i & 63));
 }
-
 // Cyclic occluder-tile pipeline shared by both sweeps: two shared-memory
-// buffers filled by cp.async.bulk with mbarrier completion.
+// buffers, each holding kTile FP64 occluder records plus their fp32 culling
+// boxes, filled by cp.async.bulk (TMA bulk copy) with mbarrier completion.
 template <int STRIDE>
 struct TilePipe {
-    double* tiles;
+    static constexpr int kBufDoubles = kTile * STRIDE + kTile * 4;   // records + boxes (8 floats)
+    double* smem;
     uint64_t* bar;
     const double* rec;
+    const float* box;
     int n, ntiles, t0;
 
     __device__ int tile_of(int it) const { return (t0 + it) % ntiles; }
     __device__ void issue(int it) const {
         const int t = tile_of(it);
         const int cnt = min(kTile, n - t * kTile);
-        const uint32_t bytes = static_cast<uint32_t>(cnt) * STRIDE * 8u;
-        double* dst = tiles + (it & 1) * kTile * STRIDE;
-        mbar_expect_tx(&bar[it & 1], bytes);
-        bulk_g2s(dst, rec + static_cast<size_t>(t) * kTile * STRIDE, bytes, &bar[it & 1]);
+        const uint32_t rbytes = static_cast<uint32_t>(cnt) * STRIDE * 8u;
+        const uint32_t bbytes = static_cast<uint32_t>(cnt) * 32u;
+        double* dst = smem + (it & 1) * kBufDoubles;
+        mbar_expect_tx(&bar[it & 1], rbytes + bbytes);
+        bulk_g2s(dst, rec + static_cast<size_t>(t) * kTile * STRIDE, rbytes, &bar[it & 1]);
+        bulk_g2s(dst + kTile * STRIDE, box + static_cast<size_t>(t) * kTile * 8, bbytes, &bar[it & 1]);
     }
     __device__ void wait(int it) const { mbar_wait(&bar[it & 1], (it >> 1) & 1); }
-    __device__ const double* buf(int it) const { return tiles + (it & 1) * kTile * STRIDE; }
+    __device__ const double* recs(int it) const { return smem + (it & 1) * kBufDoubles; }
+    __device__ const float* boxes(int it) const {
+        return reinterpret_cast<const float*>(smem + (it & 1) * kBufDoubles + kTile * STRIDE);
+    }
+    __device__ void init(int blk) {
+        t0 = blk % ntiles;
+        if (threadIdx.x == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            issue(0);
+            issue(1);
+        }
+    }
 };
+
+// Survivor mask of one tile: bit kk set when the fp32 SAT cannot rule out
+// occluder base+kk (the lane's own two faces excluded).
+__device__ __forceinline__ unsigned long long tile_survivors(const float* __restrict__ Bx, int cnt, int base,
+                                                            const SegF& g, int pi, int pj) {
+    unsigned long long mask = 0;
+#pragma unroll 4
+    for (int kk = 0; kk < cnt; ++kk)
+        if (sat_maybe(Bx + kk * 8, g)) mask |= 1ull << kk;
+    if (pi >= base && pi < base + cnt) mask &= ~(1ull << (pi - base));
+    if (pj >= base && pj < base + cnt) mask &= ~(1ull << (pj - base));
+    return mask;
+}
 
 template <int MAXV>
 __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) double tiles[];
+    extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) uint64_t bar[2];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-
-    TilePipe<STRIDE> pipe{tiles, bar, s.rec, n, (n + kTile - 1) / kTile, 0};
-    pipe.t0 = blockIdx.x % pipe.ntiles;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        pipe.issue(0);
-        pipe.issue(1);
-    }
+    TilePipe<STRIDE> pipe{smem, bar, s.rec, s.box, n, (n + kTile - 1) / kTile, 0};
+    pipe.init(blockIdx.x);
 
     bool active = false, exhausted = false;
     long long pidx = 0;
     int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0;
+    int bc0 = -1, bc1 = -1;   // blocker cache: last occluders that blocked a sightline
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    SegF g{};
     unsigned long long tests = 0;
 
     auto finish = [&](bool occluded) {
         if (!occluded) set_pair_bit(a.bits, s.words, pi, pj);
         if (a.cbit) a.cbit[pidx] = occluded ? 0 : 1;
+        active = false;
     };
-    // Claim pairs for idle lanes (warp-aggregated atomic on the work cursor).
+    auto exact = [&](int k) {
+        ++tests;
+        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
+    };
+    // Next sightline of the current pair. Sightlines the cached blockers
+    // already block are settled on the spot (one exact test each); the first
+    // one they do not block starts a full cyclic sweep of ntiles tiles.
+    auto advance = [&]() {
+        for (;;) {
+            if (++ord == S) {
+                finish(true);   // every sightline blocked: Occluded
+                return;
+            }
+            sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
+            if (bc0 >= 0 && bc0 != pi && bc0 != pj && exact(bc0)) continue;
+            if (bc1 >= 0 && bc1 != pi && bc1 != pj && exact(bc1)) {
+                const int t = bc0;
+                bc0 = bc1;
+                bc1 = t;
+                continue;
+            }
+            g = make_segf(s, ax, ay, az, bx, by, bz);
+            rem = pipe.ntiles;
+            return;
+        }
+    };
     auto refill = [&]() {
         unsigned need = __ballot_sync(kFull, !active && !exhausted);
         while (need) {
@@ -147,13 +197,12 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
                         sightline_endpoints(s, pi, pj, nr, na, grid, o, ax, ay, az, bx, by, bz);
                         degen = degenerate(ax, ay, az, bx, by, bz);
                     }
+                    active = true;
                     if (degen) {
                         finish(false);   // a degenerate sightline is never blocked
                     } else {
-                        ord = 0;
-                        sightline_endpoints(s, pi, pj, nr, na, grid, 0, ax, ay, az, bx, by, bz);
-                        rem = n;
-                        active = true;
+                        ord = -1;
+                        advance();
                     }
                 }
             }
@@ -161,35 +210,35 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
         }
     };
 
+    refill();
     for (int it = 0;; ++it) {
         pipe.wait(it);
         const int base = pipe.tile_of(it) * kTile;
         const int cnt = min(kTile, n - base);
-        const double* T = pipe.buf(it);
-        for (int kk = 0; kk < cnt; ++kk) {
-            if (__any_sync(kFull, !active && !exhausted)) refill();
-            if (active) {
-                const int k = base + kk;
-                bool hit = false;
-                if (k != pi && k != pj) {
-                    hit = seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz);
-                    ++tests;
-                }
-                --rem;
-                if (hit) {
-                    if (++ord == S) {
-                        finish(true);
-                        active = false;
-                    } else {
-                        sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
-                        rem = n;
-                    }
-                } else if (rem == 0) {
-                    finish(false);
-                    active = false;
+        if (active) {
+            unsigned long long mask = tile_survivors(pipe.boxes(it), cnt, base, g, pi, pj);
+            const double* T = pipe.recs(it);
+            int hk = -1;
+            while (mask) {
+                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+                mask &= mask - 1;
+                ++tests;
+                if (seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz)) {
+                    hk = base + kk;
+                    break;
                 }
             }
+            if (hk >= 0) {
+                if (hk != bc0) {
+                    bc1 = bc0;
+                    bc0 = hk;
+                }
+                advance();
+            } else if (--rem == 0) {
+                finish(false);   // a sightline clear of every occluder
+            }
         }
+        refill();
         const int alive = __syncthreads_or(active || !exhausted);
         if (!alive) {
             pipe.wait(it + 1);   // drain the in-flight tile before the CTA retires
@@ -197,7 +246,6 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
         }
         if (threadIdx.x == 0) pipe.issue(it + 2);
     }
-    // warp-reduce the executed-test counter
     for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
     if (lane == 0) atomicAdd(&a.counter[1], tests);
 }
@@ -207,47 +255,34 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
 template <int MAXV>
 __global__ void __launch_bounds__(kThreads) k_pair_detail(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) double tiles[];
+    extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) uint64_t bar[2];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
+    TilePipe<STRIDE> pipe{smem, bar, s.rec, s.box, n, (n + kTile - 1) / kTile, 0};
+    pipe.init(blockIdx.x);
 
-    TilePipe<STRIDE> pipe{tiles, bar, s.rec, n, (n + kTile - 1) / kTile, 0};
-    pipe.t0 = blockIdx.x % pipe.ntiles;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        pipe.issue(0);
-        pipe.issue(1);
-    }
-
-    bool active = false, exhausted = false;
+    bool active = false, exhausted = false, hit_any = false;
     long long pidx = 0;
     int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0, blocked = 0;
-    bool hit_any = false;
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    SegF g{};
     unsigned long long tests = 0;
-    uint32_t* mask = nullptr;
+    uint32_t* mask_out = nullptr;
 
-    // advance to the next non-degenerate sightline; returns false when the pair is done
+    // next non-degenerate sightline (degenerate ones are never blocked)
     auto next_sightline = [&]() {
         while (ord < S) {
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
             if (!degenerate(ax, ay, az, bx, by, bz)) {
-                rem = n;
+                g = make_segf(s, ax, ay, az, bx, by, bz);
+                rem = pipe.ntiles;
                 hit_any = false;
-                return true;
+                return;
             }
             ++ord;
         }
-        return false;
-    };
-    auto finish = [&]() {
         a.kind[pidx] = static_cast<int8_t>(blocked == 0 ? 0 : (blocked == S ? 2 : 1));
         active = false;
     };
@@ -272,38 +307,40 @@ __global__ void __launch_bounds__(kThreads) k_pair_detail(PairArgs a) {
                     S = nr * na + 1 + grid;
                     ord = 0;
                     blocked = 0;
-                    mask = a.blk_mask + static_cast<size_t>(my) * a.blk_words;
-                    if (next_sightline()) active = true;
-                    else finish();
+                    mask_out = a.blk_mask + static_cast<size_t>(my) * a.blk_words;
+                    active = true;
+                    next_sightline();
                 }
             }
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
 
+    refill();
     for (int it = 0;; ++it) {
         pipe.wait(it);
         const int base = pipe.tile_of(it) * kTile;
         const int cnt = min(kTile, n - base);
-        const double* T = pipe.buf(it);
-        for (int kk = 0; kk < cnt; ++kk) {
-            if (__any_sync(kFull, !active && !exhausted)) refill();
-            if (active) {
-                const int k = base + kk;
-                if (k != pi && k != pj) {
-                    ++tests;
-                    if (seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz)) {
-                        hit_any = true;
-                        atomicOr(mask + (k >> 5), 1u << (k & 31));
-                    }
-                }
-                if (--rem == 0) {
-                    if (hit_any) ++blocked;
-                    ++ord;
-                    if (!next_sightline()) finish();
+        if (active) {
+            unsigned long long mask = tile_survivors(pipe.boxes(it), cnt, base, g, pi, pj);
+            const double* T = pipe.recs(it);
+            while (mask) {
+                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+                mask &= mask - 1;
+                ++tests;
+                if (seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz)) {
+                    hit_any = true;
+                    const int k = base + kk;
+                    atomicOr(mask_out + (k >> 5), 1u << (k & 31));
                 }
             }
+            if (--rem == 0) {
+                if (hit_any) ++blocked;
+                ++ord;
+                next_sightline();
+            }
         }
+        refill();
         const int alive = __syncthreads_or(active || !exhausted);
         if (!alive) {
             pipe.wait(it + 1);
@@ -379,7 +416,7 @@ static int persistent_grid(const void* fn, size_t smem, int device) {
 
 template <int MAXV>
 static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
-    const size_t smem = 2ull * kTile * RecLayout<MAXV>::kStride * sizeof(double);
+    const size_t smem = 2ull * TilePipe<RecLayout<MAXV>::kStride>::kBufDoubles * sizeof(double);
     auto fn = k_pair_bits<MAXV>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);
@@ -389,7 +426,7 @@ static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st)
 
 template <int MAXV>
 static cudaError_t launch_detail_t(const PairArgs& a, int device, cudaStream_t st) {
-    const size_t smem = 2ull * kTile * RecLayout<MAXV>::kStride * sizeof(double);
+    const size_t smem = 2ull * TilePipe<RecLayout<MAXV>::kStride>::kBufDoubles * sizeof(double);
     auto fn = k_pair_detail<MAXV>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);

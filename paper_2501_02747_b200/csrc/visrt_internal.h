@@ -45,7 +45,22 @@ struct HostScene {
     std::vector<double> rec8;         // occluder records, MAXV = 8 layout
     std::vector<double> aabb;         // [n][6] lo.xyz hi.xyz
     std::vector<int32_t> building;    // [n], -1 none
+    // fp32 conservative culling boxes: centre (relative to `origin`) and
+    // dilated half-size, [n][8] = cx cy cz 0 hx hy hz 0 (see box_margin()).
+    std::vector<float> box;
+    double origin[3] = {0, 0, 0};
+    double extent = 0;                // max |coordinate - origin| over the scene
 };
+
+// Dilation of the fp32 culling boxes. A true hit of segment_face_intersection
+// lies on the segment (t in (0,1), rounding ~1e-12 m) and inside the face's
+// eps-mitered polygon (|plane dist| <= 1e-9, every edge dot >= -1e-9: at most
+// 1e-9/sin(theta_min/2) outside the polygon). The fp32 SAT compares products of
+// magnitude <= (2*extent)^2 with relative error ~4*2^-24; its absolute error is
+// absorbed by a dilation of 2^-20*extent*16. 0.01 m adds a further floor.
+inline double box_margin(double extent, double miter) {
+    return 0.01 + 16.0 * extent * 9.5367431640625e-7 + 4.0 * miter;
+}
 
 // Host ingest with the reference's exact arithmetic. Throws std::runtime_error
 // with the reference's SceneError-style message on invalid input.
