@@ -15,6 +15,8 @@
 //
 // All geometry is the reference's FP64 predicate with explicit _rn intrinsics
 // (device.h), so every decision is bit-identical to the CPU oracle.
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -63,72 +65,138 @@ __device__ __forceinline__ void set_pair_bit(unsigned long long* bits, int words
     atomicOr(bits + static_cast<size_t>(i) * words + (j >> 6), 1ull << (j & 63));
     atomicOr(bits + static_cast<size_t>(j) * words + (i >> 6), 1ull << (i & 63));
 }
-// Cyclic occluder-tile pipeline shared by both sweeps: two shared-memory
-// buffers, each holding kTile FP64 occluder records plus their fp32 culling
-// boxes, filled by cp.async.bulk (TMA bulk copy) with mbarrier completion.
-template <int STRIDE>
-struct TilePipe {
-    static constexpr int kBufDoubles = kTile * STRIDE + kTile * 4;   // records + boxes (8 floats)
-    double* smem;
+// ---------------------------------------------------------------------------
+// Occluder sweep. Every lane walks the occluders cyclically in "virtual
+// tiles" of kTile; per virtual tile it first runs the fp32 culling test on all
+// kTile boxes (uniform index -> shared-memory broadcast), collecting a
+// survivor mask, then runs the exact FP64 predicate on the survivors only
+// (records read through L1/L2). Two box sources:
+//   RESIDENT: all N culling boxes staged once in shared memory (one TMA bulk
+//             copy); warps then run free, with no block barriers;
+//   STREAM:   scenes too large for that stream kStreamTile-box tiles through
+//             a double-buffered TMA ring with one block barrier per tile.
+// ---------------------------------------------------------------------------
+constexpr int kStreamTile = 256;          // boxes per streamed tile (4 virtual tiles)
+constexpr int kResidentMaxBoxes = 6144;   // 192 KB of fp32 boxes
+
+struct BoxStream {
+    float* sbox;        // RESIDENT: [n][8]; STREAM: 2 x [kStreamTile][8]
     uint64_t* bar;
-    const double* rec;
     const float* box;
     int n, ntiles, t0;
 
     __device__ int tile_of(int it) const { return (t0 + it) % ntiles; }
     __device__ void issue(int it) const {
         const int t = tile_of(it);
-        const int cnt = min(kTile, n - t * kTile);
-        const uint32_t rbytes = static_cast<uint32_t>(cnt) * STRIDE * 8u;
-        const uint32_t bbytes = static_cast<uint32_t>(cnt) * 32u;
-        double* dst = smem + (it & 1) * kBufDoubles;
-        mbar_expect_tx(&bar[it & 1], rbytes + bbytes);
-        bulk_g2s(dst, rec + static_cast<size_t>(t) * kTile * STRIDE, rbytes, &bar[it & 1]);
-        bulk_g2s(dst + kTile * STRIDE, box + static_cast<size_t>(t) * kTile * 8, bbytes, &bar[it & 1]);
+        const int cnt = min(kStreamTile, n - t * kStreamTile);
+        const uint32_t bytes = static_cast<uint32_t>(cnt) * 32u;
+        mbar_expect_tx(&bar[it & 1], bytes);
+        bulk_g2s(sbox + (it & 1) * kStreamTile * 8, box + static_cast<size_t>(t) * kStreamTile * 8, bytes,
+                 &bar[it & 1]);
     }
     __device__ void wait(int it) const { mbar_wait(&bar[it & 1], (it >> 1) & 1); }
-    __device__ const double* recs(int it) const { return smem + (it & 1) * kBufDoubles; }
-    __device__ const float* boxes(int it) const {
-        return reinterpret_cast<const float*>(smem + (it & 1) * kBufDoubles + kTile * STRIDE);
-    }
-    __device__ void init(int blk) {
-        t0 = blk % ntiles;
-        if (threadIdx.x == 0) {
-            mbar_init(&bar[0], 1);
-            mbar_init(&bar[1], 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            issue(0);
-            issue(1);
-        }
-    }
+    __device__ const float* tile(int it) const { return sbox + (it & 1) * kStreamTile * 8; }
 };
 
-// Survivor mask of one tile: bit kk set when the fp32 SAT cannot rule out
-// occluder base+kk (the lane's own two faces excluded).
-__device__ __forceinline__ unsigned long long tile_survivors(const float* __restrict__ Bx, int cnt, int base,
+template <bool RESIDENT>
+__device__ __forceinline__ void sweep_init(BoxStream& bs) {
+    if (threadIdx.x == 0) {
+        mbar_init(&bs.bar[0], 1);
+        mbar_init(&bs.bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (RESIDENT) {
+            // one bulk copy per 64 KB chunk (the size operand is 32-bit, chunks keep it small)
+            const uint32_t total = static_cast<uint32_t>(bs.n) * 32u;
+            mbar_expect_tx(&bs.bar[0], total);
+            for (uint32_t off = 0; off < total; off += 65536u) {
+                const uint32_t b = min(65536u, total - off);
+                bulk_g2s(reinterpret_cast<char*>(bs.sbox) + off, reinterpret_cast<const char*>(bs.box) + off, b,
+                         &bs.bar[0]);
+            }
+        } else {
+            bs.issue(0);
+            bs.issue(1);
+        }
+    }
+    if (RESIDENT) bs.wait(0);
+}
+
+// Survivor mask of one virtual tile (boxes B[0..cnt)), own faces excluded.
+__device__ __forceinline__ unsigned long long tile_survivors(const float* __restrict__ B, int cnt, int base,
                                                             const SegF& g, int pi, int pj) {
     unsigned long long mask = 0;
 #pragma unroll 4
     for (int kk = 0; kk < cnt; ++kk)
-        if (sat_maybe(Bx + kk * 8, g)) mask |= 1ull << kk;
+        if (sat_maybe(B + kk * 8, g)) mask |= 1ull << kk;
     if (pi >= base && pi < base + cnt) mask &= ~(1ull << (pi - base));
     if (pj >= base && pj < base + cnt) mask &= ~(1ull << (pj - base));
     return mask;
 }
 
-template <int MAXV>
-__global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
+// Faces whose (exact) AABBs are more than 1e-6 m apart have no coincident
+// samples, hence no degenerate sightline (samples lie in the face AABB up to
+// ~1e-11 m of rounding).
+__device__ __forceinline__ bool may_touch(const DevScene& s, int i, int j) {
+    const double* A = s.aabb + 6 * static_cast<size_t>(i);
+    const double* B = s.aabb + 6 * static_cast<size_t>(j);
+    bool sep = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sep |= (B[d] > A[3 + d] + 1e-6) | (A[d] > B[3 + d] + 1e-6);
+    return !sep;
+}
+
+// Drives `vtile(boxes, base, cnt)` (one virtual tile for the whole warp) and
+// `refill()` until the warp (RESIDENT) or the block (STREAM) runs dry.
+template <bool RESIDENT, class VTile, class Busy, class Refill>
+__device__ __forceinline__ void sweep_loop(BoxStream& bs, VTile&& vtile, Busy&& busy, Refill&& refill) {
+    const int n = bs.n;
+    const int nvt = (n + kTile - 1) / kTile;
+    if (RESIDENT) {
+        const int warp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        int vt = warp % nvt;
+        for (;;) {
+            const int base = vt * kTile;
+            vtile(bs.sbox + static_cast<size_t>(base) * 8, base, min(kTile, n - base));
+            refill();
+            if (!__any_sync(kFull, busy())) break;
+            if (++vt == nvt) vt = 0;
+        }
+    } else {
+        for (int it = 0;; ++it) {
+            bs.wait(it);
+            const int tb = bs.tile_of(it) * kStreamTile;
+            const int tcnt = min(kStreamTile, n - tb);
+            const float* T = bs.tile(it);
+            for (int v = 0; v < tcnt; v += kTile) {
+                vtile(T + v * 8, tb + v, min(kTile, tcnt - v));
+                refill();
+            }
+            const int alive = __syncthreads_or(busy());
+            if (!alive) {
+                bs.wait(it + 1);   // drain the in-flight tile before the CTA retires
+                break;
+            }
+            if (threadIdx.x == 0) bs.issue(it + 2);
+        }
+    }
+}
+
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(128) float sbox[];
     __shared__ __align__(8) uint64_t bar[2];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    TilePipe<STRIDE> pipe{smem, bar, s.rec, s.box, n, (n + kTile - 1) / kTile, 0};
-    pipe.init(blockIdx.x);
+    // RESIDENT sweeps are counted in virtual tiles, STREAM sweeps too
+    const int nvt = (n + kTile - 1) / kTile;
+    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
+    bs.t0 = blockIdx.x % bs.ntiles;
+    sweep_init<RESIDENT>(bs);
 
     bool active = false, exhausted = false;
     long long pidx = 0;
@@ -147,9 +215,9 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
         ++tests;
         return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
     };
-    // Next sightline of the current pair. Sightlines the cached blockers
-    // already block are settled on the spot (one exact test each); the first
-    // one they do not block starts a full cyclic sweep of ntiles tiles.
+    // Next sightline of the current pair. Sightlines a cached blocker already
+    // blocks are settled on the spot (one exact test each); the first one the
+    // cache does not block starts a full cyclic sweep of nvt virtual tiles.
     auto advance = [&]() {
         for (;;) {
             if (++ord == S) {
@@ -165,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
                 continue;
             }
             g = make_segf(s, ax, ay, az, bx, by, bz);
-            rem = pipe.ntiles;
+            rem = nvt;
             return;
         }
     };
@@ -193,9 +261,11 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
                     grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
                     S = nr * na + 1 + grid;
                     bool degen = false;
-                    for (int o = 0; o < S && !degen; ++o) {
-                        sightline_endpoints(s, pi, pj, nr, na, grid, o, ax, ay, az, bx, by, bz);
-                        degen = degenerate(ax, ay, az, bx, by, bz);
+                    if (may_touch(s, pi, pj)) {
+                        for (int o = 0; o < S && !degen; ++o) {
+                            sightline_endpoints(s, pi, pj, nr, na, grid, o, ax, ay, az, bx, by, bz);
+                            degen = degenerate(ax, ay, az, bx, by, bz);
+                        }
                     }
                     active = true;
                     if (degen) {
@@ -209,59 +279,50 @@ __global__ void __launch_bounds__(kThreads) k_pair_bits(PairArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
+    auto vtile = [&](const float* B, int base, int cnt) {
+        if (!active) return;
+        unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
+        int hk = -1;
+        while (mask) {
+            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            if (exact(base + kk)) {
+                hk = base + kk;
+                break;
+            }
+        }
+        if (hk >= 0) {
+            if (hk != bc0) {
+                bc1 = bc0;
+                bc0 = hk;
+            }
+            advance();
+        } else if (--rem == 0) {
+            finish(false);   // a sightline clear of every occluder
+        }
+    };
+    auto busy = [&]() { return active || !exhausted; };
 
     refill();
-    for (int it = 0;; ++it) {
-        pipe.wait(it);
-        const int base = pipe.tile_of(it) * kTile;
-        const int cnt = min(kTile, n - base);
-        if (active) {
-            unsigned long long mask = tile_survivors(pipe.boxes(it), cnt, base, g, pi, pj);
-            const double* T = pipe.recs(it);
-            int hk = -1;
-            while (mask) {
-                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-                mask &= mask - 1;
-                ++tests;
-                if (seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz)) {
-                    hk = base + kk;
-                    break;
-                }
-            }
-            if (hk >= 0) {
-                if (hk != bc0) {
-                    bc1 = bc0;
-                    bc0 = hk;
-                }
-                advance();
-            } else if (--rem == 0) {
-                finish(false);   // a sightline clear of every occluder
-            }
-        }
-        refill();
-        const int alive = __syncthreads_or(active || !exhausted);
-        if (!alive) {
-            pipe.wait(it + 1);   // drain the in-flight tile before the CTA retires
-            break;
-        }
-        if (threadIdx.x == 0) pipe.issue(it + 2);
-    }
+    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
     for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
     if (lane == 0) atomicAdd(&a.counter[1], tests);
 }
 
 // Detail sweep: per pair every sightline against every occluder (no early
 // exit), as occlusion_judgment does, recording the blocker set.
-template <int MAXV>
-__global__ void __launch_bounds__(kThreads) k_pair_detail(PairArgs a) {
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(128) float sbox[];
     __shared__ __align__(8) uint64_t bar[2];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    TilePipe<STRIDE> pipe{smem, bar, s.rec, s.box, n, (n + kTile - 1) / kTile, 0};
-    pipe.init(blockIdx.x);
+    const int nvt = (n + kTile - 1) / kTile;
+    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
+    bs.t0 = blockIdx.x % bs.ntiles;
+    sweep_init<RESIDENT>(bs);
 
     bool active = false, exhausted = false, hit_any = false;
     long long pidx = 0;
@@ -277,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_detail(PairArgs a) {
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
             if (!degenerate(ax, ay, az, bx, by, bz)) {
                 g = make_segf(s, ax, ay, az, bx, by, bz);
-                rem = pipe.ntiles;
+                rem = nvt;
                 hit_any = false;
                 return;
             }
@@ -315,39 +376,29 @@ __global__ void __launch_bounds__(kThreads) k_pair_detail(PairArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
+    auto vtile = [&](const float* B, int base, int cnt) {
+        if (!active) return;
+        unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
+        while (mask) {
+            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            ++tests;
+            if (seg_hits<MAXV>(s.rec + static_cast<size_t>(base + kk) * STRIDE, ax, ay, az, bx, by, bz)) {
+                hit_any = true;
+                const int k = base + kk;
+                atomicOr(mask_out + (k >> 5), 1u << (k & 31));
+            }
+        }
+        if (--rem == 0) {
+            if (hit_any) ++blocked;
+            ++ord;
+            next_sightline();
+        }
+    };
+    auto busy = [&]() { return active || !exhausted; };
 
     refill();
-    for (int it = 0;; ++it) {
-        pipe.wait(it);
-        const int base = pipe.tile_of(it) * kTile;
-        const int cnt = min(kTile, n - base);
-        if (active) {
-            unsigned long long mask = tile_survivors(pipe.boxes(it), cnt, base, g, pi, pj);
-            const double* T = pipe.recs(it);
-            while (mask) {
-                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-                mask &= mask - 1;
-                ++tests;
-                if (seg_hits<MAXV>(T + kk * STRIDE, ax, ay, az, bx, by, bz)) {
-                    hit_any = true;
-                    const int k = base + kk;
-                    atomicOr(mask_out + (k >> 5), 1u << (k & 31));
-                }
-            }
-            if (--rem == 0) {
-                if (hit_any) ++blocked;
-                ++ord;
-                next_sightline();
-            }
-        }
-        refill();
-        const int alive = __syncthreads_or(active || !exhausted);
-        if (!alive) {
-            pipe.wait(it + 1);
-            break;
-        }
-        if (threadIdx.x == 0) pipe.issue(it + 2);
-    }
+    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
     for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
     if (lane == 0) atomicAdd(&a.counter[1], tests);
 }
@@ -414,24 +465,43 @@ static int persistent_grid(const void* fn, size_t smem, int device) {
     return sms * per;
 }
 
-template <int MAXV>
-static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
-    const size_t smem = 2ull * TilePipe<RecLayout<MAXV>::kStride>::kBufDoubles * sizeof(double);
-    auto fn = k_pair_bits<MAXV>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+template <class K>
+static cudaError_t launch_persistent(K fn, size_t smem, const PairArgs& a, int device, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
     const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);
     fn<<<grid, kThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
+// VISRT_FORCE_STREAM=1 forces the streamed-tile path (tests cover both paths
+// on small scenes).
+static bool use_resident(int n) {
+    static const bool force_stream = [] {
+        const char* e = std::getenv("VISRT_FORCE_STREAM");
+        return e && e[0] == '1';
+    }();
+    return !force_stream && n <= kResidentMaxBoxes;
+}
+
+static size_t sweep_smem(int n, bool resident) {
+    return resident ? ((static_cast<size_t>(n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
+}
+
+template <int MAXV>
+static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
+    const bool res = use_resident(a.s.n);
+    const size_t smem = sweep_smem(a.s.n, res);
+    return res ? launch_persistent(k_pair_bits<MAXV, true>, smem, a, device, st)
+               : launch_persistent(k_pair_bits<MAXV, false>, smem, a, device, st);
+}
+
 template <int MAXV>
 static cudaError_t launch_detail_t(const PairArgs& a, int device, cudaStream_t st) {
-    const size_t smem = 2ull * TilePipe<RecLayout<MAXV>::kStride>::kBufDoubles * sizeof(double);
-    auto fn = k_pair_detail<MAXV>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);
-    fn<<<grid, kThreads, smem, st>>>(a);
-    return cudaGetLastError();
+    const bool res = use_resident(a.s.n);
+    const size_t smem = sweep_smem(a.s.n, res);
+    return res ? launch_persistent(k_pair_detail<MAXV, true>, smem, a, device, st)
+               : launch_persistent(k_pair_detail<MAXV, false>, smem, a, device, st);
 }
 
 cudaError_t launch_pair_bits(const PairArgs& a, int device, cudaStream_t st) {

@@ -102,3 +102,21 @@ def test_matrix_all_pairs_sampled_rows(oracle_built, cfg):
     pi, pj = np.minimum(pi, pj)[keep], np.maximum(pi, pj)[keep]
     kinds = oracle_built.Oracle(soup).occlusion_batch(pi, pj)
     np.testing.assert_array_equal(M[pi, pj], kinds != 2)
+
+
+def test_matrix_stream_path_config1(oracle_built, cfg1, monkeypatch):
+    """The streamed-tile sweep (used when the culling boxes exceed shared
+    memory, e.g. config 4) must give the same bits as the resident sweep."""
+    import subprocess, sys, os, json
+    code = ("import sys, json; sys.path.insert(0, %r);"
+            "from paper_2501_02747_b200 import scenes;"
+            "from paper_2501_02747_b200.core import Scene;"
+            "sc = Scene(scenes.workload(1).scene); b, st = sc.pair_visibility('all');"
+            "k, bl, _ = sc.pair_detail([0, 3, 5], [40, 77, 100]);"
+            "print(json.dumps([b.tolist(), k.tolist(), bl]))") % os.path.dirname(os.path.dirname(__file__))
+    out = {}
+    for force in ("0", "1"):
+        env = dict(os.environ, VISRT_FORCE_STREAM=force)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+        out[force] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["0"] == out["1"]
