@@ -114,6 +114,31 @@ class Scene:
         return kind, blockers, _stats_dict(st)
 
 
+REGION_DTYPE = np.dtype([("present", np.int8), ("has", np.int8, 3), ("clipped", np.int8, 3), ("pad", np.int8),
+                         ("sub", np.float64, 6)])
+
+
+def point_regions_array(scene: Scene, src: np.ndarray, stream: int = 0):
+    """illuminated_region(src[k], face f) for every (k, f) — one batched GPU call
+    (rt::illuminated_region, include/rt/vistable.hpp:116-117). Returns a
+    structured array [nsrc, nfaces] (present: 1 region / 0 none / -1 source on
+    the face plane, the reference's VisibilityError) and the call stats."""
+    src = np.ascontiguousarray(np.asarray(src, np.float64).reshape(-1, 3))
+    out = np.zeros((len(src), scene.n), REGION_DTYPE)
+    st = _capi.visrt_stats()
+    check(lib().visrt_point_regions(scene.h, len(src), src.reshape(-1),
+                                    out.ctypes.data_as(C.POINTER(_capi.visrt_region)), C.byref(st),
+                                    C.c_void_p(stream) if stream else None))
+    return out, _stats_dict(st)
+
+
+def point_regions(scene: Scene, src: np.ndarray) -> List[List[dict]]:
+    arr, _ = point_regions_array(scene, src)
+    return [[{"present": int(r["present"]), "has": [int(x) for x in r["has"]],
+              "clipped": [int(x) for x in r["clipped"]], "sub": [float(x) for x in r["sub"]]}
+             for r in row] for row in arr]
+
+
 def measure_peaks(device: int = 0) -> Tuple[float, float]:
     """(FP64 non-FMA ops/s, FP32 FFMA flop/s) measured on `device`."""
     f64 = C.c_double()

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "capi_internal.h"
 #include "device.h"
 #include "host_geom.h"
 
@@ -30,38 +31,14 @@ namespace {
 
 thread_local std::string g_err;
 
-struct CudaError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct UsageError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct VisError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
+using visrt::ck;
+using visrt::CudaError;
+using visrt::UsageError;
+using visrt::VisError;
 
 template <class F>
 int guarded(F&& f) {
-    try {
-        f();
-        return VISRT_OK;
-    } catch (const CudaError& e) {
-        g_err = e.what();
-        return VISRT_E_CUDA;
-    } catch (const UsageError& e) {
-        g_err = e.what();
-        return VISRT_E_USAGE;
-    } catch (const VisError& e) {
-        g_err = e.what();
-        return VISRT_E_VISIBILITY;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return VISRT_E_SCENE;
-    }
+    return visrt::capi_guard(std::forward<F>(f));
 }
 
 template <class T>
@@ -76,10 +53,7 @@ T* dev_upload(const std::vector<T>& v, std::vector<void*>& allocs) {
 
 template <class T>
 T* dev_alloc(size_t count, std::vector<void*>& allocs) {
-    T* p = nullptr;
-    ck(cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)), "cudaMalloc");
-    allocs.push_back(p);
-    return p;
+    return visrt::dalloc<T>(count, allocs);
 }
 
 }  // namespace
@@ -134,6 +108,13 @@ struct visrt_scene {
         sel_cap = m;
     }
 };
+
+namespace visrt {
+void set_last_error(const std::string& msg) { g_err = msg; }
+const DevScene& scene_dev(const visrt_scene* s) { return s->ds; }
+const HostScene& scene_host(const visrt_scene* s) { return s->hs; }
+int scene_device(const visrt_scene* s) { return s->device; }
+}  // namespace visrt
 
 namespace {
 
@@ -433,12 +414,6 @@ int visrt_pair_detail(visrt_scene* sc, int64_t npairs, const int32_t* ci, const 
 }  // extern "C"
 
 // --- entry points implemented in later milestones (regions.cu / tree.cu) ---
-#ifndef VISRT_HAVE_REGIONS
-extern "C" int visrt_point_regions(visrt_scene*, int64_t, const double*, visrt_region*, visrt_stats*, void*) {
-    g_err = "visrt_point_regions: not built";
-    return VISRT_E_USAGE;
-}
-#endif
 #ifndef VISRT_HAVE_TREE
 extern "C" int visrt_tracer_create(visrt_scene*, int, const uint64_t*, int64_t, const int32_t*, visrt_tracer**) {
     g_err = "visrt_tracer_create: not built";

@@ -1,0 +1,478 @@
+// (2) Per-snapshot point regions: illuminated_region(source, face) for every
+// (snapshot source, face), batched over all snapshots at once (K4).
+//
+// Reference: src/vistable.cpp:287-334 (illuminated_region), 140-193
+// (visible_intervals: 65 columns x <= 7 transverse samples, bisection
+// refine() <= 50 iterations), 102-126 (column_span), 84-98 (face_param),
+// 38-44 (sightline_clear).
+//
+// One lane = one (source, face) region, a sequential state machine:
+//   plane XY, YZ, XZ (those with a face_param) ->
+//     SCAN   columns u_i = i/64, each col_vis(u) = first clear of <= 7
+//            sightlines source -> face point;
+//     REFINE for each visible run, bisect its interior boundaries (same
+//            midpoints, same 1e-15 stop, same iteration cap);
+//     best interval (first largest) -> sub[2], clipped.
+// Every sightline is one culled any-hit sweep (sweep.h) over all faces but
+// the target, with the 2-entry blocker cache. The lane's arithmetic follows
+// the reference operation by operation, so sub[] is bit-identical.
+#include <cstdlib>
+
+#include "device.h"
+#include "sweep.h"
+
+namespace visrt {
+
+struct RegionArgs {
+    DevScene s;
+    long long ntasks;             // nsrc * n
+    const double* src;            // [nsrc][3]
+    visrt_region* out;            // [nsrc][n]
+    unsigned long long* counter;  // [0] cursor, [1] exact tests, [2] sightlines
+};
+
+__device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double dmax_std(double a, double b) { return (a < b) ? b : a; }
+
+// face_param (src/vistable.cpp:84-98) recomputed on the fly from the face
+// ring: (u, s) of vertex k.
+__device__ __forceinline__ void face_us(const DevScene& s, int f, int pl, int k, double ax, double ay, double dx,
+                                        double dy, double len2, double& u, double& sv) {
+    const double* P = s.pts + (static_cast<size_t>(f) * VISRT_MAX_VERTS + k) * 3;
+    double qx, qy;
+    if (pl == 0) {
+        qx = P[0]; qy = P[1]; sv = P[2];
+    } else if (pl == 1) {
+        qx = P[1]; qy = P[2]; sv = P[0];
+    } else {
+        qx = P[0]; qy = P[2]; sv = P[1];
+    }
+    u = __ddiv_rn(dadd(dmul(dsub(qx, ax), dx), dmul(dsub(qy, ay), dy)), len2);
+}
+
+// column_span (src/vistable.cpp:102-126)
+__device__ bool column_span(const DevScene& s, int f, int pl, double ax, double ay, double dx, double dy,
+                            double len2, double u, double& lo_o, double& hi_o) {
+    const int nv = s.nv[f];
+    double lo = 0.0, hi = 0.0;
+    bool any = false;
+    double u0, s0v;
+    face_us(s, f, pl, 0, ax, ay, dx, dy, len2, u0, s0v);
+    double ua = u0, sa = s0v;
+    for (int i = 0; i < nv; ++i) {
+        double ub, sb;
+        if (i + 1 < nv) face_us(s, f, pl, i + 1, ax, ay, dx, dy, len2, ub, sb);
+        else { ub = u0; sb = s0v; }
+        const double da = dsub(ua, u), db = dsub(ub, u);
+        if (fabs(da) <= 1e-12) {
+            if (!any) { lo = hi = sa; any = true; }
+            else { lo = dmin_std(lo, sa); hi = dmax_std(hi, sa); }
+        }
+        if ((da < 0.0) != (db < 0.0) && fabs(dsub(da, db)) > 1e-15) {
+            const double sv = dadd(sa, dmul(dsub(sb, sa), __ddiv_rn(da, dsub(da, db))));
+            if (!any) { lo = hi = sv; any = true; }
+            else { lo = dmin_std(lo, sv); hi = dmax_std(hi, sv); }
+        }
+        ua = ub;
+        sa = sb;
+    }
+    lo_o = lo;
+    hi_o = hi;
+    return any;
+}
+
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) float sbox[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+    const int nvt = (n + kTile - 1) / kTile;
+    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
+    bs.t0 = blockIdx.x % bs.ntiles;
+    sweep_init<RESIDENT>(bs);
+
+    // ---- lane state --------------------------------------------------------
+    bool active = false, exhausted = false, querying = false;
+    long long tid = 0;
+    int f = 0, pl = 0;
+    double sx = 0, sy = 0, sz = 0;      // source
+    double ax = 0, ay = 0, dx = 0, dy = 0, len2 = 0;   // face_param of plane pl
+    // SCAN / REFINE
+    int phase = 0;                      // 0 scan, 1 refine
+    int col = 0;                        // scan column
+    unsigned long long vis = 0;         // columns 0..63
+    bool vis64 = false;                 // column 64
+    int run_i = 0, run_j = 0, which = 0, it = 0;
+    double lo = 0, hi = 0, r_start = 0;
+    bool lo_vis = false;
+    bool have_best = false;
+    double best0 = 0, best1 = 0;
+    // col_vis in progress
+    double cu = 0, cs0 = 0, cs1 = 0, inset = 0;
+    int samp = 0;
+    // region output
+    int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
+    double sub[6] = {0, 0, 0, 0, 0, 0};
+    // sightline query
+    double qx = 0, qy = 0, qz = 0;
+    SegF g{};
+    int rem = 0, bc0 = -1, bc1 = -1;
+    unsigned long long tests = 0, queries = 0;
+
+    auto vis_at = [&](int i) { return i == 64 ? vis64 : ((vis >> i) & 1ull) != 0; };
+    auto exact = [&](int k) {
+        ++tests;
+        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz);
+    };
+    auto write_out = [&](int8_t present) {
+        visrt_region r;
+        r.present = present;
+        r.pad = 0;
+        for (int t = 0; t < 3; ++t) {
+            r.has[t] = present == 1 ? has[t] : 0;
+            r.clipped[t] = present == 1 ? clp[t] : 0;
+        }
+        for (int t = 0; t < 6; ++t) r.sub[t] = present == 1 ? sub[t] : 0.0;
+        a.out[tid] = r;
+        active = false;
+        querying = false;
+    };
+    // Set up sample `samp` of the current column; returns false when all 7
+    // samples are used (column not visible). Samples the blocker cache
+    // already blocks are settled here.
+    auto next_sample = [&]() -> bool {
+        for (; samp < 7; ++samp) {
+            const double fj = __ddiv_rn(static_cast<double>(samp), 6.0);
+            const double sv = dmin_std(dsub(cs1, inset), dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), fj))));
+            const double px = dadd(ax, dmul(dx, cu));
+            const double py = dadd(ay, dmul(dy, cu));
+            if (pl == 0) { qx = px; qy = py; qz = sv; }
+            else if (pl == 1) { qx = sv; qy = px; qz = py; }
+            else { qx = px; qy = sv; qz = py; }
+            ++queries;
+            if (bc0 >= 0 && bc0 != f && exact(bc0)) continue;
+            if (bc1 >= 0 && bc1 != f && exact(bc1)) {
+                const int t = bc0;
+                bc0 = bc1;
+                bc1 = t;
+                continue;
+            }
+            g = make_segf(s, sx, sy, sz, qx, qy, qz);
+            rem = nvt;
+            return true;
+        }
+        return false;
+    };
+    // Begin col_vis(u); returns true when a sweep is pending, false when the
+    // column was decided without one (result in `res`).
+    auto begin_col = [&](double u, bool& res) -> bool {
+        cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
+        if (!column_span(s, f, pl, ax, ay, dx, dy, len2, cu, cs0, cs1)) {
+            res = false;
+            return false;
+        }
+        inset = dmul(dsub(cs1, cs0), 1e-6);
+        samp = 0;
+        if (next_sample()) return true;
+        res = false;
+        return false;
+    };
+    // Drive the state machine until a sweep is pending or the region is done.
+    // `have` / `res`: a col_vis result to consume first.
+    auto pump = [&](bool have, bool res) {
+        for (;;) {
+            if (have) {
+                have = false;
+                if (phase == 0) {
+                    if (res) {
+                        if (col == 64) vis64 = true;
+                        else vis |= 1ull << col;
+                    }
+                    ++col;
+                } else {
+                    // refine step (src/vistable.cpp:164-173)
+                    const double mid = dmul(0.5, dadd(lo, hi));
+                    if (res == lo_vis) lo = mid;
+                    else hi = mid;
+                    ++it;
+                }
+            }
+            if (phase == 0) {
+                if (col < 65) {
+                    bool r = false;
+                    if (begin_col(__ddiv_rn(static_cast<double>(col), 64.0), r)) {
+                        querying = true;
+                        return;
+                    }
+                    have = true;
+                    res = r;
+                    continue;
+                }
+                // scan done: set up runs (src/vistable.cpp:175-192)
+                phase = 1;
+                run_i = 0;
+                which = -1;
+                have_best = false;
+            }
+            // ---- REFINE ----
+            if (which >= 0 && it < 50 && dsub(hi, lo) > 1e-15) {
+                bool r = false;
+                if (begin_col(dmul(0.5, dadd(lo, hi)), r)) {
+                    querying = true;
+                    return;
+                }
+                have = true;
+                res = r;
+                continue;
+            }
+            if (which == 0) {
+                // start refined: r_start
+                r_start = dmul(0.5, dadd(lo, hi));
+                which = -2;   // proceed to the end boundary
+            } else if (which == 1) {
+                const double end = dmul(0.5, dadd(lo, hi));
+                if (!have_best || dsub(best1, best0) < dsub(end, r_start)) {
+                    best0 = r_start;
+                    best1 = end;
+                    have_best = true;
+                }
+                run_i = run_j + 1;
+                which = -1;
+            }
+            if (which == -2) {
+                // end boundary of run [run_i .. run_j]
+                if (run_j + 1 < 65) {
+                    lo = __ddiv_rn(static_cast<double>(run_j), 64.0);
+                    hi = dadd(lo, __ddiv_rn(1.0, 64.0));
+                    lo_vis = true;
+                    it = 0;
+                    which = 1;
+                    continue;
+                }
+                const double end = __ddiv_rn(static_cast<double>(run_j), 64.0);
+                if (!have_best || dsub(best1, best0) < dsub(end, r_start)) {
+                    best0 = r_start;
+                    best1 = end;
+                    have_best = true;
+                }
+                run_i = run_j + 1;
+                which = -1;
+            }
+            // which == -1: find the next run
+            while (run_i < 65 && !vis_at(run_i)) ++run_i;
+            if (run_i < 65) {
+                run_j = run_i;
+                while (run_j + 1 < 65 && vis_at(run_j + 1)) ++run_j;
+                r_start = __ddiv_rn(static_cast<double>(run_i), 64.0);
+                if (run_i > 0) {
+                    hi = r_start;
+                    lo = dsub(r_start, __ddiv_rn(1.0, 64.0));
+                    lo_vis = false;
+                    it = 0;
+                    which = 0;
+                } else {
+                    which = -2;
+                }
+                continue;
+            }
+            // all runs done: plane result
+            if (!have_best) {
+                write_out(0);   // fully hidden in this plane: no region
+                return;
+            }
+            has[pl] = 1;
+            sub[2 * pl] = best0;
+            sub[2 * pl + 1] = best1;
+            clp[pl] = (best0 > 1e-9 || best1 < 1.0 - 1e-9) ? 1 : 0;
+            // next plane with a face_param
+            for (;;) {
+                if (++pl == 3) {
+                    write_out((has[0] | has[1] | has[2]) ? 1 : 0);
+                    return;
+                }
+                if (!s.seg_ok[3 * f + pl]) continue;
+                const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;
+                ax = sg[0];
+                ay = sg[1];
+                dx = dsub(sg[2], sg[0]);
+                dy = dsub(sg[3], sg[1]);
+                len2 = dadd(dmul(dx, dx), dmul(dy, dy));
+                if (len2 <= kEps * kEps) continue;
+                break;
+            }
+            phase = 0;
+            col = 0;
+            vis = 0;
+            vis64 = false;
+        }
+    };
+    auto start_task = [&](long long t) {
+        tid = t;
+        const long long k = t / n;
+        f = static_cast<int>(t - k * n);
+        sx = a.src[3 * k];
+        sy = a.src[3 * k + 1];
+        sz = a.src[3 * k + 2];
+        for (int q = 0; q < 3; ++q) { has[q] = 0; clp[q] = 0; sub[2 * q] = 0; sub[2 * q + 1] = 0; }
+        active = true;
+        // back-face test (src/vistable.cpp:289-294)
+        const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
+        const double* N = s.normal + 3 * static_cast<size_t>(f);
+        const double dist = dot_rel(sx, sy, sz, P[0], P[1], P[2], N[0], N[1], N[2]);
+        if (fabs(dist) <= kEps) { write_out(-1); return; }
+        if (dist < 0.0) { write_out(0); return; }
+        pl = -1;
+        for (;;) {
+            if (++pl == 3) { write_out(0); return; }
+            if (!s.seg_ok[3 * f + pl]) continue;
+            const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;
+            ax = sg[0];
+            ay = sg[1];
+            dx = dsub(sg[2], sg[0]);
+            dy = dsub(sg[3], sg[1]);
+            len2 = dadd(dmul(dx, dx), dmul(dy, dy));
+            if (len2 <= kEps * kEps) continue;
+            break;
+        }
+        phase = 0;
+        col = 0;
+        vis = 0;
+        vis64 = false;
+        pump(false, false);
+    };
+    auto refill = [&]() {
+        unsigned need = __ballot_sync(kFull, !active && !exhausted);
+        while (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&a.counter[0], static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(kFull, base, leader);
+            if (!active && !exhausted) {
+                const long long my = static_cast<long long>(base) + __popc(need & ((1u << lane) - 1u));
+                if (my >= a.ntasks) exhausted = true;
+                else start_task(my);
+            }
+            need = __ballot_sync(kFull, !active && !exhausted);
+        }
+    };
+    // One virtual tile of the current sightline sweep.
+    auto vtile = [&](const float* B, int base, int cnt) {
+        if (!querying) return;
+        unsigned long long mask = tile_survivors(B, cnt, base, g, f, -1);
+        int hk = -1;
+        while (mask) {
+            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            if (exact(base + kk)) {
+                hk = base + kk;
+                break;
+            }
+        }
+        if (hk >= 0) {
+            if (hk != bc0) {
+                bc1 = bc0;
+                bc0 = hk;
+            }
+            // blocked sample: try the next sample of this column
+            ++samp;
+            if (next_sample()) return;
+            querying = false;
+            pump(true, false);
+        } else if (--rem == 0) {
+            querying = false;
+            pump(true, true);   // clear sightline: column visible
+        }
+    };
+    auto busy = [&]() { return active || !exhausted; };
+
+    refill();
+    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
+    for (int o = 16; o > 0; o >>= 1) {
+        tests += __shfl_down_sync(kFull, tests, o);
+        queries += __shfl_down_sync(kFull, queries, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&a.counter[1], tests);
+        atomicAdd(&a.counter[2], queries);
+    }
+}
+
+static int persistent_grid_r(const void* fn, size_t smem, int device) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem);
+    if (per < 1) per = 1;
+    return sms * per;
+}
+
+template <class K>
+static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a, int device, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device), kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int MAXV>
+static cudaError_t launch_regions_t(const RegionArgs& a, int device, cudaStream_t st) {
+    const char* e = std::getenv("VISRT_FORCE_STREAM");
+    const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
+    const size_t smem = res ? ((static_cast<size_t>(a.s.n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
+    return res ? launch_r(k_point_regions<MAXV, true>, smem, a, device, st)
+               : launch_r(k_point_regions<MAXV, false>, smem, a, device, st);
+}
+
+cudaError_t launch_point_regions(const RegionArgs& a, int device, cudaStream_t st) {
+    return a.s.maxv <= 4 ? launch_regions_t<4>(a, device, st) : launch_regions_t<8>(a, device, st);
+}
+
+}  // namespace visrt
+
+// ---------------------------------------------------------------------------
+// C-ABI entry (include/visrt.h)
+// ---------------------------------------------------------------------------
+#include "capi_internal.h"
+
+extern "C" int visrt_point_regions(visrt_scene* sc, int64_t nsrc, const double* src_xyz, visrt_region* out,
+                                   visrt_stats* stats, void* stream) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const visrt::DevScene& ds = visrt::scene_dev(sc);
+        const long long ntasks = static_cast<long long>(nsrc) * ds.n;
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        double* d_src = visrt::dalloc<double>(static_cast<size_t>(nsrc) * 3, tmp);
+        visrt_region* d_out = visrt::dalloc<visrt_region>(static_cast<size_t>(ntasks), tmp);
+        unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(4, tmp);
+        visrt::ck(cudaMemcpyAsync(d_src, src_xyz, nsrc * 3 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D src");
+        visrt::ck(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(unsigned long long), st), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        visrt::RegionArgs a{ds, ntasks, d_src, d_out, d_ctr};
+        if (ntasks > 0) visrt::ck(visrt::launch_point_regions(a, visrt::scene_device(sc), st), "k_point_regions");
+        cudaEventRecord(e1, st);
+        unsigned long long ctr[4] = {0, 0, 0, 0};
+        if (ntasks > 0)
+            visrt::ck(cudaMemcpyAsync(out, d_out, ntasks * sizeof(visrt_region), cudaMemcpyDeviceToHost, st), "D2H");
+        visrt::ck(cudaMemcpyAsync(ctr, d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st), "D2H");
+        visrt::ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (stats) {
+            stats->pairs = ntasks;
+            stats->candidates = static_cast<int64_t>(ctr[2]);   // sightline queries
+            stats->admitted = -1;
+            stats->tests_alg = 0;
+            stats->tests_exec = static_cast<int64_t>(ctr[1]);
+            stats->ms = ms;
+        }
+    });
+}

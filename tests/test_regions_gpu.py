@@ -1,0 +1,81 @@
+"""(2) Per-snapshot Tx/Rx -> facet tables: illuminated_region for every
+(snapshot, face), GPU vs the CPU oracle. Bit-exact on presence, the
+VisibilityError case (source on the face plane), per-plane `has`, `clipped`
+and the sub-interval doubles."""
+import numpy as np
+import pytest
+
+from paper_2501_02747_b200 import scenes
+from paper_2501_02747_b200.core import Scene, point_regions_array
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(o, soup, src, arr, faces=None):
+    bad = []
+    faces = range(soup.nfaces) if faces is None else faces
+    for k in range(len(src)):
+        for f in faces:
+            e = o.illuminated_region(src[k], f)
+            g = arr[k, f]
+            got = (int(g["present"]), [int(x) for x in g["has"]], [int(x) for x in g["clipped"]],
+                   [float(x) for x in g["sub"]])
+            exp = (e["present"], e["has"], e["clipped"], e["sub"])
+            if got != exp:
+                bad.append((k, f, got, exp))
+    return bad
+
+
+def test_regions_config1_tx_rx(oracle_built):
+    wl = scenes.workload(1)
+    o = oracle_built.Oracle(wl.scene)
+    src = np.concatenate([wl.tx[::9], wl.rx])
+    with Scene(wl.scene) as sc:
+        arr, st = point_regions_array(sc, src)
+    bad = _compare(o, wl.scene, src, arr)
+    assert not bad, bad[:5]
+    assert (arr["present"] == 1).sum() > 0
+
+
+def test_regions_on_plane_and_backface(oracle_built):
+    wl = scenes.workload(1)
+    soup = wl.scene
+    # sources on face planes (VisibilityError in the reference) and behind faces
+    pts = soup.face_points(0)
+    src = np.array([pts.mean(axis=0), pts[0] + np.array([0.0, 0.0, 0.5]), [50.0, 50.0, 200.0]])
+    o = oracle_built.Oracle(soup)
+    with Scene(soup) as sc:
+        arr, _ = point_regions_array(sc, src)
+    assert not _compare(o, soup, src, arr)
+    assert arr[0, 0]["present"] == -1
+
+
+def test_regions_config3_sampled(oracle_built):
+    wl = scenes.workload(3)
+    o = oracle_built.Oracle(wl.scene)
+    src = np.concatenate([wl.tx[::250], wl.rx[::250]])
+    with Scene(wl.scene) as sc:
+        arr, st = point_regions_array(sc, src)
+    rng = np.random.default_rng(3)
+    faces = sorted(rng.choice(wl.scene.nfaces, 60, replace=False).tolist())
+    bad = _compare(o, wl.scene, src, arr, faces)
+    assert not bad, bad[:5]
+
+
+def test_regions_match_reference_region(oracle_built):
+    if not oracle_built.have_ref():
+        pytest.skip("oracle/_ref not built")
+    wl = scenes.workload(1)
+    r = oracle_built.RefOracle(wl.scene)
+    src = wl.tx[::33]
+    with Scene(wl.scene) as sc:
+        arr, _ = point_regions_array(sc, src)
+    for k in range(len(src)):
+        for f in range(wl.scene.nfaces):
+            e = r.illuminated_region(src[k], f)
+            g = arr[k, f]
+            assert int(g["present"]) == e["present"]
+            if e["present"] == 1:
+                assert [int(x) for x in g["has"]] == e["has"]
+                assert [int(x) for x in g["clipped"]] == e["clipped"]
+                assert [float(x) for x in g["sub"]] == e["sub"]

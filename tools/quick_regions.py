@@ -1,0 +1,19 @@
+"""Quick per-snapshot region timing (development aid)."""
+import sys, time
+import numpy as np
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2501_02747_b200 import scenes
+from paper_2501_02747_b200.core import Scene, point_regions_array
+for arg in sys.argv[1:] or ["1:101", "3:200"]:
+    cfg, nsrc = (int(x) for x in arg.split(":"))
+    wl = scenes.workload(cfg)
+    src = np.concatenate([wl.tx, wl.rx])[:nsrc]
+    with Scene(wl.scene) as sc:
+        for rep in range(2):
+            t0 = time.perf_counter()
+            arr, st = point_regions_array(sc, src)
+            t1 = time.perf_counter()
+        pres = (arr["present"] == 1).sum()
+        print(f"cfg{cfg} N={wl.scene.nfaces} nsrc={len(src)}: kernel {st['ms']:.2f} ms wall {1e3*(t1-t0):.1f} ms "
+              f"regions {arr.size} present {pres} sightlines {st['candidates']:.3e} exact {st['tests_exec']:.3e} "
+              f"-> {arr.size/st['ms']*1e3:.3e} regions/s", flush=True)
