@@ -117,10 +117,12 @@ int visrt_point_regions(visrt_scene* scene, int64_t nsrc, const double* src_xyz,
                         visrt_region* out, visrt_stats* stats, void* stream);
 
 /* (3) Image-tree expansion (TraceAccelerator::trace, allow_diffraction = false).
- * The chain filter is given as the admitted order-1 bit matrix plus optional
- * order-2 chains (triples a->b->c admitted into the filter). Per snapshot k
- * (tx[k], rx[k] or rx[0] when rx_fixed): paths written to a CSR over
- * snapshots: path_off[nsnap+1]; per path: nrefl, faces[4], points[3*6]. */
+ * The chain filter (build_chain_filter, src/raytracer.cpp:319-340) is given as
+ * the admitted order-1 bit matrix (pair_admitted; NULL = the scene's device
+ * bits of the last PREFILTERED visrt_pair_visibility) plus the order-2 chains
+ * (triples p->t->a, required for max_refl 3). Per snapshot k (tx[k], rx[k] or
+ * rx[0] when rx_fixed) the accelerated image tree is expanded level by level
+ * on the GPU; results stay in the tracer until fetched. */
 typedef struct visrt_tracer visrt_tracer;
 int visrt_tracer_create(visrt_scene* scene, int max_refl, const uint64_t* admitted_bits,
                         int64_t ntriples, const int32_t* triples, visrt_tracer** out);
@@ -128,19 +130,24 @@ void visrt_tracer_destroy(visrt_tracer* tracer);
 typedef struct {
     int32_t nrefl;
     int32_t faces[4];
-    int32_t pad;
+    int32_t snap;
     double points[18];     /* tx, reflection points..., rx */
     double length;
 } visrt_path;
 typedef struct {
     int64_t nodes;         /* image-tree nodes expanded (TraceStats::nodes_expanded) */
     int64_t sequences;     /* sequences resolved (TraceStats::sequences_checked)     */
-    int64_t paths;
-    float   ms;
+    int64_t paths;         /* paths found (TraceStats::paths_found)                  */
+    int64_t leg_tests;     /* exact segment-vs-face tests run on path legs            */
+    float   ms;            /* device time of the whole batch                          */
 } visrt_trace_stats;
 int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const double* rx,
-                int rx_fixed, int64_t* path_off, visrt_path* paths, int64_t path_cap,
-                visrt_trace_stats* stats, void* stream);
+                int rx_fixed, visrt_trace_stats* stats, void* stream);
+/* Fetch the last visrt_trace results: per-snapshot CSR (path_off[nsnap+1]),
+ * paths grouped by snapshot, each group sorted by face sequence; nodes[nsnap]
+ * per-snapshot node counts. Any pointer may be NULL; returns the path count. */
+int64_t visrt_trace_results(const visrt_tracer* tracer, int64_t* path_off, visrt_path* paths,
+                            int64_t path_cap, int64_t* nodes);
 
 #ifdef __cplusplus
 }

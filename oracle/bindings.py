@@ -44,6 +44,34 @@ class vo_region(C.Structure):
                 ("sub", C.c_double * 6)]
 
 
+class vo_path(C.Structure):
+    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("points", C.c_double * 18),
+                ("length", C.c_double)]
+
+
+_u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+
+def chain_filter_arrays(n: int, admitted: np.ndarray, triples=None):
+    """Chain filter in the oracle's layout: admitted[n, n] (uint8) and the
+    order-2 continuations as CSR over directed admitted pairs (row-major rank).
+    `triples`: iterable of (p, t, a) order-2 chains (None: order <= 2 only)."""
+    adm = np.ascontiguousarray(admitted.astype(np.uint8).reshape(n, n))
+    pi, pj = np.nonzero(adm)
+    rank = {(int(p), int(t)): r for r, (p, t) in enumerate(zip(pi, pj))}
+    lists = [[] for _ in range(len(pi))]
+    if triples is not None:
+        for p, t, a in triples:
+            lists[rank[(int(p), int(t))]].append(int(a))
+    off = np.zeros(len(pi) + 1, np.int64)
+    idx = []
+    for r, l in enumerate(lists):
+        l = sorted(set(l))
+        idx.extend(l)
+        off[r + 1] = off[r] + len(l)
+    return adm, off, np.asarray(idx if idx else [0], np.int32)
+
+
 class Oracle:
     """C restatement of the reference hot path (see oracle/visrt_oracle.c)."""
 
@@ -69,6 +97,9 @@ class Oracle:
             L.vo_occlusion_batch.argtypes = [C.c_void_p, C.c_int64, _i32p, _i32p, _i8p, C.c_int32]
             L.vo_sightline_count.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
             L.vo_illuminated_region.argtypes = [C.c_void_p, _f64p, C.c_int32, C.POINTER(vo_region)]
+            L.vo_trace.restype = C.c_int64
+            L.vo_trace.argtypes = [C.c_void_p, _u8p, _i64p, _i32p, C.c_int32, _f64p, _f64p,
+                                   C.POINTER(vo_path), C.c_int64, _i64p]
             cls._lib = L
         return cls._lib
 
@@ -125,6 +156,24 @@ class Oracle:
         r = vo_region()
         self.lib().vo_illuminated_region(self.h, np.ascontiguousarray(src, np.float64), face, C.byref(r))
         return {"present": r.present, "has": list(r.has), "clipped": list(r.clipped), "sub": list(r.sub)}
+
+    def trace(self, filt, max_refl: int, tx, rx):
+        """TraceAccelerator::trace (no diffraction) with the chain filter
+        `filt` = chain_filter_arrays(...). Returns (paths, stats) with paths
+        as dicts {faces, points, length}; stats = nodes, sequences, paths."""
+        adm, off, idx = filt
+        cap = 1 << 16
+        out = (vo_path * cap)()
+        st = np.zeros(3, np.int64)
+        n = self.lib().vo_trace(self.h, adm.reshape(-1), off, idx, max_refl,
+                                np.ascontiguousarray(tx, np.float64), np.ascontiguousarray(rx, np.float64),
+                                out, cap, st)
+        if n < 0:
+            raise ValueError("PlacementError: transmitter and receiver coincide")
+        paths = [{"faces": list(out[k].faces[: out[k].nrefl]),
+                  "points": list(out[k].points[: 3 * (out[k].nrefl + 2)]), "length": out[k].length}
+                 for k in range(min(n, cap))]
+        return paths, st
 
 
 # ---------------------------------------------------------------------------

@@ -52,6 +52,23 @@ typedef struct {
 } vo_region;
 int32_t vo_illuminated_region(const vo_scene* s, const double* src, int32_t face, vo_region* out);
 
+/* (3) TraceAccelerator::trace, allow_diffraction = false, for a soup scene
+ * (no buildings, no edges, no oblique faces needed). Chain filter: order-1
+ * continuations = admitted rows (adm[i*n + j] != 0), order-2 continuations =
+ * CSR over directed admitted pairs in row-major order (c2_off[npairs+1],
+ * c2_idx), i.e. the key (p, t) is the rank of (p, t) among admitted pairs.
+ * Paths: nrefl, faces[4], points[3*(nrefl+2)], length. Returns path count,
+ * or -1 (PlacementError: tx ~ rx). stats: nodes, sequences, paths. */
+typedef struct {
+    int32_t nrefl;
+    int32_t faces[4];
+    double points[18];
+    double length;
+} vo_path;
+int64_t vo_trace(const vo_scene* s, const uint8_t* adm, const int64_t* c2_off, const int32_t* c2_idx,
+                 int32_t max_refl, const double* tx, const double* rx, vo_path* out, int64_t cap,
+                 int64_t* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ EXPORTS = [
     "visrt_scene_nfaces", "visrt_scene_ingest", "visrt_scene_upload_bytes", "visrt_measure_peaks",
     "visrt_pair_visibility", "visrt_matrix_bits_device",
     "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_tracer_create",
-    "visrt_tracer_destroy", "visrt_trace",
+    "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -51,12 +51,13 @@ class visrt_region(C.Structure):
 
 
 class visrt_path(C.Structure):
-    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("pad", C.c_int32),
+    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("snap", C.c_int32),
                 ("points", C.c_double * 18), ("length", C.c_double)]
 
 
 class visrt_trace_stats(C.Structure):
-    _fields_ = [("nodes", C.c_int64), ("sequences", C.c_int64), ("paths", C.c_int64), ("ms", C.c_float)]
+    _fields_ = [("nodes", C.c_int64), ("sequences", C.c_int64), ("paths", C.c_int64),
+                ("leg_tests", C.c_int64), ("ms", C.c_float)]
 
 
 class VisrtError(RuntimeError):
@@ -118,8 +119,10 @@ def lib():
     L.visrt_tracer_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
                                       C.POINTER(C.c_void_p)]
     L.visrt_tracer_destroy.argtypes = [C.c_void_p]
-    L.visrt_trace.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_int, _i64p, C.c_void_p, C.c_int64,
-                              C.POINTER(visrt_trace_stats), C.c_void_p]
+    L.visrt_trace.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_int, C.POINTER(visrt_trace_stats),
+                              C.c_void_p]
+    L.visrt_trace_results.restype = C.c_int64
+    L.visrt_trace_results.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     _lib = L
     return L
 

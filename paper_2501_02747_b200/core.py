@@ -139,6 +139,71 @@ def point_regions(scene: Scene, src: np.ndarray) -> List[List[dict]]:
              for r in row] for row in arr]
 
 
+class Tracer:
+    """rt::TraceAccelerator (include/rt/raytracer.hpp:96-118) over the GPU image
+    tree: the chain filter is the admitted matrix (pair_admitted) plus the
+    order-2 chains (p, t, a) for max_refl 3. ``trace`` runs a whole batch of
+    snapshots (allow_diffraction = false: the facet soups carry no edges)."""
+
+    def __init__(self, scene: Scene, max_refl: int, admitted_bits: Optional[np.ndarray] = None,
+                 triples: Optional[np.ndarray] = None) -> None:
+        self.scene = scene
+        self.max_refl = max_refl
+        bits = None if admitted_bits is None else np.ascontiguousarray(admitted_bits, np.uint64)
+        tri = None if triples is None else np.ascontiguousarray(np.asarray(triples, np.int32).reshape(-1, 3))
+        h = C.c_void_p()
+        check(lib().visrt_tracer_create(scene.h, max_refl, None if bits is None else bits.ctypes.data,
+                                        0 if tri is None else len(tri), None if tri is None else tri.ctypes.data,
+                                        C.byref(h)))
+        self.h = h
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().visrt_tracer_destroy(self.h)
+            self.h = None
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def trace_raw(self, tx: np.ndarray, rx: np.ndarray, stream: int = 0):
+        tx = np.ascontiguousarray(np.asarray(tx, np.float64).reshape(-1, 3))
+        rx = np.ascontiguousarray(np.asarray(rx, np.float64).reshape(-1, 3))
+        fixed = 1 if len(rx) == 1 and len(tx) != 1 else 0
+        st = _capi.visrt_trace_stats()
+        check(lib().visrt_trace(self.h, len(tx), tx.reshape(-1), rx.reshape(-1), fixed, C.byref(st),
+                                C.c_void_p(stream) if stream else None))
+        L = lib()
+        npaths = L.visrt_trace_results(self.h, None, None, 0, None)
+        off = np.zeros(len(tx) + 1, np.int64)
+        nodes = np.zeros(len(tx), np.int64)
+        paths = (_capi.visrt_path * max(npaths, 1))()
+        L.visrt_trace_results(self.h, off.ctypes.data, C.cast(paths, C.c_void_p), npaths, nodes.ctypes.data)
+        return off, paths, nodes, {"nodes": st.nodes, "sequences": st.sequences, "paths": st.paths,
+                                   "leg_tests": st.leg_tests, "ms": st.ms}
+
+    def trace(self, tx: np.ndarray, rx: np.ndarray):
+        """Per snapshot: list of paths {faces, points, length} ordered by face
+        sequence, plus per-snapshot node counts and stats."""
+        off, paths, nodes, st = self.trace_raw(tx, rx)
+        out = []
+        for k in range(len(off) - 1):
+            row = []
+            for q in range(off[k], off[k + 1]):
+                p = paths[q]
+                row.append({"faces": list(p.faces[: p.nrefl]), "points": list(p.points[: 3 * (p.nrefl + 2)]),
+                            "length": p.length})
+            out.append(row)
+        return out, nodes, st
+
+
+def path_identity(ids: Sequence[str], faces: Sequence[int]) -> str:
+    """Path::identity (src/raytracer.cpp:448-456) for a reflection-only path."""
+    return "LOS" if not faces else "/".join("R:" + ids[f] for f in faces)
+
+
 def measure_peaks(device: int = 0) -> Tuple[float, float]:
     """(FP64 non-FMA ops/s, FP32 FFMA flop/s) measured on `device`."""
     f64 = C.c_double()

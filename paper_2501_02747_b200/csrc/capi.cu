@@ -414,15 +414,3 @@ int visrt_pair_detail(visrt_scene* sc, int64_t npairs, const int32_t* ci, const 
 }  // extern "C"
 
 // --- entry points implemented in later milestones (regions.cu / tree.cu) ---
-#ifndef VISRT_HAVE_TREE
-extern "C" int visrt_tracer_create(visrt_scene*, int, const uint64_t*, int64_t, const int32_t*, visrt_tracer**) {
-    g_err = "visrt_tracer_create: not built";
-    return VISRT_E_USAGE;
-}
-extern "C" void visrt_tracer_destroy(visrt_tracer*) {}
-extern "C" int visrt_trace(visrt_tracer*, int64_t, const double*, const double*, int, int64_t*, visrt_path*,
-                           int64_t, visrt_trace_stats*, void*) {
-    g_err = "visrt_trace: not built";
-    return VISRT_E_USAGE;
-}
-#endif

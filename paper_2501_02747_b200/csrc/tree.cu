@@ -1,0 +1,744 @@
+// (3) Image-tree expansion for sm_100a (K6): TraceAccelerator::trace batched
+// over snapshots, level by level.
+//
+// Reference: src/raytracer.cpp:400-430 (Engine::expand: level 1 over every
+// face, deeper levels over the ChainFilter continuations + obliques, skip the
+// immediate repeat, prune when the parent image is within kEps of / behind the
+// candidate plane), 383-394 (attempt), 205-278 (resolve_sequence: forward
+// images, backward unfolding with strict plane crossing + contains, legs
+// longer than kEps, Occluder::clear per leg), 319-340 (build_chain_filter).
+//
+//   k_tree_expand  one warp per parent node: the warp walks the parent's
+//                  candidate pool 32 at a time, prunes, and appends the
+//                  surviving children with ballot/popc prefix sums + one
+//                  atomic per warp (prefix-sum compaction into the next
+//                  frontier).
+//   k_tree_unfold  one thread per node of a level: forward images, backward
+//                  unfolding, leg lengths; valid sequences are compacted
+//                  into a candidate list.
+//   k_tree_legs    one lane per candidate: each leg is a culled any-hit sweep
+//                  (sweep.h) over all faces; candidates whose legs are all
+//                  clear become paths.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <vector>
+
+#include "capi_internal.h"
+#include "device.h"
+#include "sweep.h"
+
+namespace visrt {
+
+struct TreeNode {
+    int32_t snap, depth, f0, f1, f2, rank, filtered, pad;
+    double ix, iy, iz;
+};
+
+struct Cand {
+    int32_t snap, depth, f[3], pad;
+    double pts[15];
+    double length;
+};
+
+struct TreeArgs {
+    DevScene s;
+    const int32_t* off1;      // conts1 CSR over faces (admitted aims, ascending)
+    const int32_t* idx1;
+    const long long* off2;    // conts2 CSR over directed admitted pairs (row-major rank)
+    const int32_t* idx2;
+    const int32_t* obl;
+    int32_t nobl;
+    const double* tx;
+    const double* rx;
+    int32_t rx_fixed;
+    int32_t snap0, nsnap;     // batch
+    int32_t max_refl;
+    const TreeNode* in;       // nullptr: the batch's snapshot roots
+    long long nin;
+    TreeNode* out;
+    unsigned long long* nout;
+    long long cap;
+    unsigned long long* nodes_per_snap;   // [total snapshots]
+    Cand* cand;
+    unsigned long long* ncand;
+    long long cand_cap;
+    visrt_path* paths;
+    unsigned long long* npaths;
+    long long path_cap;
+    unsigned long long* counter;          // [0] cursor, [1] leg tests
+};
+
+__device__ __forceinline__ double sdist_face(const DevScene& s, int f, double x, double y, double z) {
+    const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
+    const double* N = s.normal + 3 * static_cast<size_t>(f);
+    return dot_rel(x, y, z, P[0], P[1], P[2], N[0], N[1], N[2]);
+}
+
+// mirror_point (src/geom.cpp:122-124): p - n * (2 * signed_distance(p))
+__device__ __forceinline__ void mirror_face(const DevScene& s, int f, double& x, double& y, double& z) {
+    const double* N = s.normal + 3 * static_cast<size_t>(f);
+    const double d2 = dmul(2.0, sdist_face(s, f, x, y, z));
+    x = dsub(x, dmul(N[0], d2));
+    y = dsub(y, dmul(N[1], d2));
+    z = dsub(z, dmul(N[2], d2));
+}
+
+// ConvexPolygon::contains (src/geom.cpp:155-167) on an occluder record.
+template <int MAXV>
+__device__ __forceinline__ bool rec_contains(const double* __restrict__ R, double px, double py, double pz) {
+    if (fabs(dot_rel(px, py, pz, R[0], R[1], R[2], R[3], R[4], R[5])) > kEps) return false;
+    if (dot_rel(px, py, pz, R[0], R[1], R[2], R[6], R[7], R[8]) < -kEps) return false;
+#pragma unroll
+    for (int k = 1; k < MAXV; ++k) {
+        const double* E = R + 9 + (k - 1) * 6;
+        if (dot_rel(px, py, pz, E[0], E[1], E[2], E[3], E[4], E[5]) < -kEps) return false;
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a) {
+    const DevScene& s = a.s;
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const long long nparents = a.in ? a.nin : a.nsnap;
+    for (long long p = warp; p < nparents; p += nwarps) {
+        TreeNode par;
+        if (a.in) {
+            par = a.in[p];
+        } else {
+            par = TreeNode{};
+            par.snap = a.snap0 + static_cast<int>(p);
+            par.depth = 0;
+            par.f0 = par.f1 = par.f2 = -1;
+            par.rank = -1;
+            par.filtered = 1;
+            par.ix = a.tx[3 * static_cast<size_t>(par.snap)];
+            par.iy = a.tx[3 * static_cast<size_t>(par.snap) + 1];
+            par.iz = a.tx[3 * static_cast<size_t>(par.snap) + 2];
+        }
+        const int d = par.depth;
+        const int last = d == 0 ? -1 : (d == 1 ? par.f0 : (d == 2 ? par.f1 : par.f2));
+        // candidate pool: all faces at the root or for an unfiltered prefix;
+        // else the chain continuations of the prefix, then the obliques
+        const int32_t* list = nullptr;
+        long long lo = 0, hi = s.n;
+        bool all = d == 0 || !par.filtered;
+        if (!all) {
+            if (d == 1) {
+                lo = a.off1[par.f0];
+                hi = a.off1[par.f0 + 1];
+                list = a.idx1;
+            } else if (d == 2 && par.rank >= 0) {
+                lo = a.off2[par.rank];
+                hi = a.off2[par.rank + 1];
+                list = a.idx2;
+            } else {
+                lo = hi = 0;
+            }
+        }
+        const long long npool = (hi - lo) + (all ? 0 : a.nobl);
+        for (long long q0 = 0; q0 < npool; q0 += 32) {
+            const long long q = q0 + lane;
+            bool ok = false;
+            int c = -1;
+            int rank = -1;
+            if (q < npool) {
+                if (q < hi - lo) {
+                    c = list ? list[lo + q] : static_cast<int>(lo + q);
+                    if (!all && d == 1) rank = static_cast<int>(lo + q);
+                } else {
+                    c = a.obl[q - (hi - lo)];
+                }
+                ok = c != last && sdist_face(s, c, par.ix, par.iy, par.iz) > kEps;
+            }
+            const unsigned m = __ballot_sync(kFull, ok);
+            if (!m) continue;
+            unsigned long long base = 0;
+            if (lane == 0) {
+                base = atomicAdd(a.nout, static_cast<unsigned long long>(__popc(m)));
+                atomicAdd(a.nodes_per_snap + par.snap, static_cast<unsigned long long>(__popc(m)));
+            }
+            base = __shfl_sync(kFull, base, 0);
+            if (ok) {
+                const long long slot = static_cast<long long>(base) + __popc(m & ((1u << lane) - 1u));
+                if (slot < a.cap) {
+                    TreeNode ch;
+                    ch.snap = par.snap;
+                    ch.depth = d + 1;
+                    ch.f0 = d == 0 ? c : par.f0;
+                    ch.f1 = d == 1 ? c : par.f1;
+                    ch.f2 = d == 2 ? c : par.f2;
+                    ch.rank = d == 1 ? rank : -1;
+                    ch.filtered = par.filtered && s.orient[c] != 2;
+                    ch.pad = 0;
+                    ch.ix = par.ix;
+                    ch.iy = par.iy;
+                    ch.iz = par.iz;
+                    mirror_face(s, c, ch.ix, ch.iy, ch.iz);
+                    a.out[slot] = ch;
+                }
+            }
+        }
+    }
+}
+
+// resolve_sequence up to the occlusion tests: one thread per node (or per
+// snapshot root for the line-of-sight sequence).
+template <int MAXV>
+__global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    const DevScene& s = a.s;
+    const long long nt = a.in ? a.nin : a.nsnap;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < nt; t += stride) {
+        int snap, d;
+        int f[3] = {-1, -1, -1};
+        if (a.in) {
+            const TreeNode& nd = a.in[t];
+            snap = nd.snap;
+            d = nd.depth;
+            f[0] = nd.f0;
+            f[1] = nd.f1;
+            f[2] = nd.f2;
+        } else {
+            snap = a.snap0 + static_cast<int>(t);
+            d = 0;
+        }
+        const double* T = a.tx + 3 * static_cast<size_t>(snap);
+        const double* Rx = a.rx_fixed ? a.rx : a.rx + 3 * static_cast<size_t>(snap);
+        double img[4][3];
+        img[0][0] = T[0];
+        img[0][1] = T[1];
+        img[0][2] = T[2];
+        bool ok = true;
+        for (int k = 0; k < d && ok; ++k) {
+            if (sdist_face(s, f[k], img[k][0], img[k][1], img[k][2]) <= kEps) {
+                ok = false;
+                break;
+            }
+            img[k + 1][0] = img[k][0];
+            img[k + 1][1] = img[k][1];
+            img[k + 1][2] = img[k][2];
+            mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
+        }
+        double refl[3][3];
+        double cx = Rx[0], cy = Rx[1], cz = Rx[2];
+        for (int k = d - 1; k >= 0 && ok; --k) {
+            const double da = sdist_face(s, f[k], cx, cy, cz);
+            const double db = sdist_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
+            if (dmul(da, db) >= 0.0) {   // segment_plane_crossing, src/geom.cpp:182-189
+                ok = false;
+                break;
+            }
+            const double tt = __ddiv_rn(da, dsub(da, db));
+            const double px = dadd(cx, dmul(dsub(img[k + 1][0], cx), tt));
+            const double py = dadd(cy, dmul(dsub(img[k + 1][1], cy), tt));
+            const double pz = dadd(cz, dmul(dsub(img[k + 1][2], cz), tt));
+            if (!rec_contains<MAXV>(s.rec + static_cast<size_t>(f[k]) * STRIDE, px, py, pz)) {
+                ok = false;
+                break;
+            }
+            refl[k][0] = px;
+            refl[k][1] = py;
+            refl[k][2] = pz;
+            cx = px;
+            cy = py;
+            cz = pz;
+        }
+        if (!ok) continue;
+        Cand c;
+        c.snap = snap;
+        c.depth = d;
+        c.f[0] = f[0];
+        c.f[1] = f[1];
+        c.f[2] = f[2];
+        c.pad = 0;
+        c.pts[0] = T[0];
+        c.pts[1] = T[1];
+        c.pts[2] = T[2];
+        for (int k = 0; k < d; ++k) {
+            c.pts[3 * (k + 1)] = refl[k][0];
+            c.pts[3 * (k + 1) + 1] = refl[k][1];
+            c.pts[3 * (k + 1) + 2] = refl[k][2];
+        }
+        c.pts[3 * (d + 1)] = Rx[0];
+        c.pts[3 * (d + 1) + 1] = Rx[1];
+        c.pts[3 * (d + 1) + 2] = Rx[2];
+        double length = 0.0;
+        for (int i = 0; i <= d && ok; ++i) {
+            const double dx = dsub(c.pts[3 * i], c.pts[3 * (i + 1)]);
+            const double dy = dsub(c.pts[3 * i + 1], c.pts[3 * (i + 1) + 1]);
+            const double dz = dsub(c.pts[3 * i + 2], c.pts[3 * (i + 1) + 2]);
+            const double seg = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+            if (seg <= kEps) ok = false;
+            length = dadd(length, seg);
+        }
+        if (!ok) continue;
+        c.length = length;
+        const unsigned long long slot = atomicAdd(a.ncand, 1ull);
+        if (static_cast<long long>(slot) < a.cand_cap) a.cand[slot] = c;
+    }
+}
+
+// Occluder::clear on every leg of every candidate (lane per candidate).
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) float sbox[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+    const int nvt = (n + kTile - 1) / kTile;
+    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
+    bs.t0 = blockIdx.x % bs.ntiles;
+    sweep_init<RESIDENT>(bs);
+    const long long ncand = static_cast<long long>(*a.ncand) < a.cand_cap ? static_cast<long long>(*a.ncand)
+                                                                          : a.cand_cap;
+
+    bool active = false, exhausted = false;
+    long long cid = 0;
+    int leg = 0, legs = 0, rem = 0, bc0 = -1, bc1 = -1;
+    double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    SegF g{};
+    unsigned long long tests = 0;
+
+    auto emit = [&]() {
+        const Cand& c = a.cand[cid];
+        const unsigned long long slot = atomicAdd(a.npaths, 1ull);
+        if (static_cast<long long>(slot) < a.path_cap) {
+            visrt_path p;
+            p.nrefl = c.depth;
+            p.faces[0] = c.f[0];
+            p.faces[1] = c.f[1];
+            p.faces[2] = c.f[2];
+            p.faces[3] = -1;
+            p.snap = c.snap;
+            for (int i = 0; i < 18; ++i) p.points[i] = i < 3 * (c.depth + 2) ? c.pts[i] : 0.0;
+            p.length = c.length;
+            a.paths[slot] = p;
+        }
+        active = false;
+    };
+    auto exact = [&](int k) {
+        ++tests;
+        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
+    };
+    // set up leg `leg`; legs a cached blocker already blocks end the candidate
+    auto start_leg = [&]() {
+        for (;;) {
+            if (leg == legs) {
+                emit();
+                return;
+            }
+            const double* P = a.cand[cid].pts + 3 * leg;
+            ax = P[0];
+            ay = P[1];
+            az = P[2];
+            bx = P[3];
+            by = P[4];
+            bz = P[5];
+            if ((bc0 >= 0 && exact(bc0)) || (bc1 >= 0 && exact(bc1))) {
+                active = false;   // blocked leg: no path
+                return;
+            }
+            g = make_segf(s, ax, ay, az, bx, by, bz);
+            rem = nvt;
+            return;
+        }
+    };
+    auto refill = [&]() {
+        unsigned need = __ballot_sync(kFull, !active && !exhausted);
+        while (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&a.counter[0], static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(kFull, base, leader);
+            if (!active && !exhausted) {
+                const long long my = static_cast<long long>(base) + __popc(need & ((1u << lane) - 1u));
+                if (my >= ncand) {
+                    exhausted = true;
+                } else {
+                    cid = my;
+                    legs = a.cand[my].depth + 1;
+                    leg = 0;
+                    active = true;
+                    start_leg();
+                }
+            }
+            need = __ballot_sync(kFull, !active && !exhausted);
+        }
+    };
+    auto vtile = [&](const float* B, int base, int cnt) {
+        if (!active) return;
+        unsigned long long mask = tile_survivors(B, cnt, base, g, -1, -1);
+        int hk = -1;
+        while (mask) {
+            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            if (exact(base + kk)) {
+                hk = base + kk;
+                break;
+            }
+        }
+        if (hk >= 0) {
+            if (hk != bc0) {
+                bc1 = bc0;
+                bc0 = hk;
+            }
+            active = false;   // blocked: the sequence supports no path
+        } else if (--rem == 0) {
+            ++leg;
+            start_leg();
+        }
+    };
+    auto busy = [&]() { return active || !exhausted; };
+
+    refill();
+    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) atomicAdd(&a.counter[1], tests);
+}
+
+static int grid_of(const void* fn, int threads, size_t smem, int device) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+    return sms * std::max(per, 1);
+}
+
+template <int MAXV>
+static void launch_legs_t(const TreeArgs& a, int device, cudaStream_t st) {
+    const char* e = std::getenv("VISRT_FORCE_STREAM");
+    const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
+    const size_t smem = res ? ((static_cast<size_t>(a.s.n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
+    if (res) {
+        auto fn = k_tree_legs<MAXV, true>;
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+        fn<<<grid_of(reinterpret_cast<const void*>(fn), kThreads, smem, device), kThreads, smem, st>>>(a);
+    } else {
+        auto fn = k_tree_legs<MAXV, false>;
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");
+        fn<<<grid_of(reinterpret_cast<const void*>(fn), kThreads, smem, device), kThreads, smem, st>>>(a);
+    }
+    ck(cudaGetLastError(), "k_tree_legs");
+}
+
+}  // namespace visrt
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+using visrt::ck;
+
+struct visrt_tracer {
+    visrt_scene* scene = nullptr;
+    int max_refl = 0;
+    std::vector<void*> allocs;
+    int32_t* off1 = nullptr;
+    int32_t* idx1 = nullptr;
+    long long* off2 = nullptr;
+    int32_t* idx2 = nullptr;
+    int32_t* obl = nullptr;
+    int32_t nobl = 0;
+    // results of the last trace
+    int64_t nsnap = 0;
+    std::vector<visrt_path> paths;
+    std::vector<int64_t> path_off;
+    std::vector<int64_t> nodes;
+    ~visrt_tracer() {
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+extern "C" int visrt_tracer_create(visrt_scene* sc, int max_refl, const uint64_t* admitted_bits, int64_t ntriples,
+                                   const int32_t* triples, visrt_tracer** out) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        if (!out) throw visrt::UsageError("null out");
+        *out = nullptr;
+        if (max_refl < 0) throw visrt::VisError("reflection order must be non-negative");
+        if (max_refl > 3)
+            throw visrt::UsageError("max_refl > 3 needs order-3 chains, which this build does not represent");
+        if (max_refl == 3 && !triples && ntriples > 0) throw visrt::UsageError("triples required");
+        const visrt::HostScene& hs = visrt::scene_host(sc);
+        const int n = hs.n;
+        const int words = (n + 63) / 64;
+        std::vector<uint64_t> bits(static_cast<size_t>(n) * words);
+        if (admitted_bits) {
+            std::memcpy(bits.data(), admitted_bits, bits.size() * 8);
+        } else {
+            ck(cudaMemcpy(bits.data(), visrt_matrix_bits_device(sc), bits.size() * 8, cudaMemcpyDeviceToHost),
+               "D2H bits");
+        }
+        auto tr = std::make_unique<visrt_tracer>();
+        tr->scene = sc;
+        tr->max_refl = max_refl;
+        // conts1: admitted aims per face, ascending (build_chain_filter sorts + uniques)
+        std::vector<int32_t> off1(n + 1, 0), idx1;
+        for (int p = 0; p < n; ++p) {
+            for (int w = 0; w < words; ++w) {
+                uint64_t m = bits[static_cast<size_t>(p) * words + w];
+                while (m) {
+                    const int b = __builtin_ctzll(m);
+                    m &= m - 1;
+                    idx1.push_back(w * 64 + b);
+                }
+            }
+            off1[p + 1] = static_cast<int32_t>(idx1.size());
+        }
+        // conts2: per directed admitted pair (rank = position in idx1), sorted unique
+        std::vector<long long> off2(idx1.size() + 1, 0);
+        std::vector<int32_t> idx2;
+        if (ntriples > 0) {
+            std::vector<std::pair<long long, int32_t>> keyed;
+            keyed.reserve(ntriples);
+            for (int64_t k = 0; k < ntriples; ++k) {
+                const int p = triples[3 * k], t = triples[3 * k + 1], c = triples[3 * k + 2];
+                const int32_t* b = idx1.data() + off1[p];
+                const int32_t* e = idx1.data() + off1[p + 1];
+                const int32_t* it = std::lower_bound(b, e, t);
+                if (it == e || *it != t) throw visrt::UsageError("triple prefix is not an admitted pair");
+                keyed.push_back({static_cast<long long>(it - idx1.data()), c});
+            }
+            std::sort(keyed.begin(), keyed.end());
+            keyed.erase(std::unique(keyed.begin(), keyed.end()), keyed.end());
+            for (const auto& kv : keyed) {
+                off2[kv.first + 1]++;
+                idx2.push_back(kv.second);
+            }
+            for (size_t r = 0; r < idx1.size(); ++r) off2[r + 1] += off2[r];
+        }
+        std::vector<int32_t> obl;
+        for (int f = 0; f < n; ++f)
+            if (hs.orient[f] == 2) obl.push_back(f);
+        auto up = [&](const void* src, size_t bytes) {
+            void* p = nullptr;
+            ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc");
+            tr->allocs.push_back(p);
+            if (bytes) ck(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "H2D");
+            return p;
+        };
+        tr->off1 = static_cast<int32_t*>(up(off1.data(), off1.size() * 4));
+        tr->idx1 = static_cast<int32_t*>(up(idx1.data(), idx1.size() * 4));
+        tr->off2 = static_cast<long long*>(up(off2.data(), off2.size() * 8));
+        tr->idx2 = static_cast<int32_t*>(up(idx2.data(), idx2.size() * 4));
+        tr->obl = static_cast<int32_t*>(up(obl.data(), obl.size() * 4));
+        tr->nobl = static_cast<int32_t>(obl.size());
+        *out = tr.release();
+    });
+}
+
+extern "C" void visrt_tracer_destroy(visrt_tracer* t) { delete t; }
+
+namespace {
+
+// Scene::inside_building (src/scene.cpp:199-211) for closed-shell scenes.
+bool inside_building(const visrt::HostScene& hs, const double* p) {
+    int nb = 0;
+    for (int f = 0; f < hs.n; ++f) nb = std::max(nb, hs.building[f] + 1);
+    for (int b = 0; b < nb; ++b) {
+        bool inside = true, any = false;
+        for (int f = 0; f < hs.n && inside; ++f) {
+            if (hs.building[f] != b) continue;
+            any = true;
+            const double* P = &hs.pts[static_cast<size_t>(f) * VISRT_MAX_VERTS * 3];
+            const double* N = &hs.normal[3 * static_cast<size_t>(f)];
+            const double d = (p[0] - P[0]) * N[0] + (p[1] - P[1]) * N[1] + (p[2] - P[2]) * N[2];
+            if (d >= -visrt::kEps) inside = false;
+        }
+        if (any && inside) return true;
+    }
+    return false;
+}
+
+}  // namespace
+
+extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, const double* rx, int rx_fixed,
+                           visrt_trace_stats* stats, void* stream) {
+    return visrt::capi_guard([&] {
+        if (!tr) throw visrt::UsageError("null tracer");
+        visrt::ScopedDevice dev(tr->scene);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const visrt::HostScene& hs = visrt::scene_host(tr->scene);
+        const visrt::DevScene& ds = visrt::scene_dev(tr->scene);
+        const int device = visrt::scene_device(tr->scene);
+        // Engine ctor placement checks (src/raytracer.cpp:355-363)
+        for (int64_t k = 0; k < nsnap; ++k) {
+            const double* T = tx + 3 * k;
+            const double* R = rx_fixed ? rx : rx + 3 * k;
+            const double dx = T[0] - R[0], dy = T[1] - R[1], dz = T[2] - R[2];
+            if (std::sqrt(dx * dx + dy * dy + dz * dz) <= visrt::kEps)
+                throw visrt::PlaceError("transmitter and receiver coincide");
+            if (inside_building(hs, T)) throw visrt::PlaceError("transmitter lies inside a building volume");
+            if (inside_building(hs, R)) throw visrt::PlaceError("receiver lies inside a building volume");
+        }
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        double* d_tx = visrt::dalloc<double>(static_cast<size_t>(nsnap) * 3, tmp);
+        double* d_rx = visrt::dalloc<double>(static_cast<size_t>(rx_fixed ? 1 : nsnap) * 3, tmp);
+        ck(cudaMemcpyAsync(d_tx, tx, nsnap * 24, cudaMemcpyHostToDevice, st), "H2D tx");
+        ck(cudaMemcpyAsync(d_rx, rx, (rx_fixed ? 1 : nsnap) * 24, cudaMemcpyHostToDevice, st), "H2D rx");
+        unsigned long long* d_nodes = visrt::dalloc<unsigned long long>(std::max<int64_t>(nsnap, 1), tmp);
+        ck(cudaMemsetAsync(d_nodes, 0, std::max<int64_t>(nsnap, 1) * 8, st), "memset");
+        unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(8, tmp);   // nout, ncand, npaths, cursor, tests
+        // frontier / candidate / path buffers (capacity-bounded; batches adapt)
+        const long long node_cap = 1ll << 24;   // 16.7M nodes per level per batch (0.9 GB)
+        const long long cand_cap = 1ll << 22;
+        const long long path_cap = 1ll << 22;
+        visrt::TreeNode* lvl[2] = {visrt::dalloc<visrt::TreeNode>(node_cap, tmp),
+                                   visrt::dalloc<visrt::TreeNode>(node_cap, tmp)};
+        visrt::Cand* d_cand = visrt::dalloc<visrt::Cand>(cand_cap, tmp);
+        visrt_path* d_paths = visrt::dalloc<visrt_path>(path_cap, tmp);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+
+        visrt::TreeArgs a{};
+        a.s = ds;
+        a.off1 = tr->off1;
+        a.idx1 = tr->idx1;
+        a.off2 = tr->off2;
+        a.idx2 = tr->idx2;
+        a.obl = tr->obl;
+        a.nobl = tr->nobl;
+        a.tx = d_tx;
+        a.rx = d_rx;
+        a.rx_fixed = rx_fixed;
+        a.max_refl = tr->max_refl;
+        a.nodes_per_snap = d_nodes;
+        a.cand = d_cand;
+        a.cand_cap = cand_cap;
+        a.paths = d_paths;
+        a.path_cap = path_cap;
+        std::vector<visrt_path> host_paths;
+        int64_t total_nodes = 0, total_seq = 0, leg_tests = 0;
+        unsigned long long* c_nout = d_ctr + 0;
+        unsigned long long* c_ncand = d_ctr + 1;
+        unsigned long long* c_npath = d_ctr + 2;
+        const int eb = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_expand), 256, 0, device);
+        const int ub = visrt::grid_of(reinterpret_cast<const void*>(ds.maxv <= 4 ? visrt::k_tree_unfold<4>
+                                                                                  : visrt::k_tree_unfold<8>),
+                                      256, 0, device);
+        // One batch of snapshots: expand level by level; unfold + leg sweeps per
+        // level; returns false when a level overflowed (caller halves the batch).
+        auto run_batch = [&](int s0, int ns) -> bool {
+            ck(cudaMemsetAsync(d_ctr, 0, 8 * 8, st), "memset");
+            a.snap0 = s0;
+            a.nsnap = ns;
+            long long seqs = ns;   // line-of-sight sequences
+            auto resolve_level = [&](const visrt::TreeNode* in, long long nin) -> bool {
+                a.in = in;
+                a.nin = nin;
+                ck(cudaMemsetAsync(c_ncand, 0, 8, st), "memset");
+                ck(cudaMemsetAsync(d_ctr + 3, 0, 8, st), "memset");
+                if (ds.maxv <= 4) visrt::k_tree_unfold<4><<<ub, 256, 0, st>>>(a);
+                else visrt::k_tree_unfold<8><<<ub, 256, 0, st>>>(a);
+                ck(cudaGetLastError(), "k_tree_unfold");
+                a.ncand = c_ncand;
+                a.npaths = c_npath;
+                a.counter = d_ctr + 3;
+                if (ds.maxv <= 4) visrt::launch_legs_t<4>(a, device, st);
+                else visrt::launch_legs_t<8>(a, device, st);
+                unsigned long long nc = 0;
+                ck(cudaMemcpyAsync(&nc, c_ncand, 8, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaStreamSynchronize(st), "sync");
+                return static_cast<long long>(nc) <= cand_cap;
+            };
+            a.ncand = c_ncand;
+            if (!resolve_level(nullptr, ns)) return false;
+            const visrt::TreeNode* in = nullptr;
+            long long nin = ns;
+            for (int depth = 0; depth < tr->max_refl; ++depth) {
+                a.in = in;
+                a.nin = nin;
+                a.out = lvl[depth & 1];
+                a.nout = c_nout;
+                a.cap = node_cap;
+                ck(cudaMemsetAsync(c_nout, 0, 8, st), "memset");
+                visrt::k_tree_expand<<<eb, 256, 0, st>>>(a);
+                ck(cudaGetLastError(), "k_tree_expand");
+                unsigned long long no = 0;
+                ck(cudaMemcpyAsync(&no, c_nout, 8, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaStreamSynchronize(st), "sync");
+                if (static_cast<long long>(no) > node_cap) return false;
+                seqs += static_cast<long long>(no);
+                if (no == 0) break;
+                if (!resolve_level(lvl[depth & 1], static_cast<long long>(no))) return false;
+                in = lvl[depth & 1];
+                nin = static_cast<long long>(no);
+            }
+            unsigned long long np = 0, tests = 0;
+            ck(cudaMemcpyAsync(&np, c_npath, 8, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(&tests, d_ctr + 4, 8, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            if (static_cast<long long>(np) > path_cap) return false;
+            const size_t old = host_paths.size();
+            host_paths.resize(old + np);
+            if (np) ck(cudaMemcpy(host_paths.data() + old, d_paths, np * sizeof(visrt_path), cudaMemcpyDeviceToHost),
+                       "D2H paths");
+            total_seq += seqs;
+            leg_tests += static_cast<int64_t>(tests);
+            return true;
+        };
+        int batch = static_cast<int>(std::min<int64_t>(nsnap, 4096));
+        for (int s0 = 0; s0 < nsnap;) {
+            const int ns = static_cast<int>(std::min<int64_t>(batch, nsnap - s0));
+            if (!run_batch(s0, ns)) {
+                if (ns == 1) throw visrt::UsageError("one snapshot exceeds the frontier capacity");
+                batch = std::max(1, ns / 2);
+                // discard partial node counts of the failed batch
+                std::vector<unsigned long long> zero(ns, 0);
+                ck(cudaMemcpy(d_nodes + s0, zero.data(), ns * 8, cudaMemcpyHostToDevice), "reset");
+                continue;
+            }
+            s0 += ns;
+        }
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::vector<unsigned long long> nodes(std::max<int64_t>(nsnap, 1));
+        ck(cudaMemcpy(nodes.data(), d_nodes, nodes.size() * 8, cudaMemcpyDeviceToHost), "D2H nodes");
+        // group by snapshot, order by face sequence (deterministic output)
+        std::sort(host_paths.begin(), host_paths.end(), [](const visrt_path& x, const visrt_path& y) {
+            if (x.snap != y.snap) return x.snap < y.snap;
+            if (x.nrefl != y.nrefl) return x.nrefl < y.nrefl;
+            return std::lexicographical_compare(x.faces, x.faces + x.nrefl, y.faces, y.faces + y.nrefl);
+        });
+        tr->nsnap = nsnap;
+        tr->paths = std::move(host_paths);
+        tr->path_off.assign(nsnap + 1, 0);
+        for (const auto& p : tr->paths) tr->path_off[p.snap + 1]++;
+        for (int64_t k = 0; k < nsnap; ++k) tr->path_off[k + 1] += tr->path_off[k];
+        tr->nodes.assign(nsnap, 0);
+        for (int64_t k = 0; k < nsnap; ++k) {
+            tr->nodes[k] = static_cast<int64_t>(nodes[k]);
+            total_nodes += tr->nodes[k];
+        }
+        if (stats) {
+            stats->nodes = total_nodes;
+            stats->sequences = total_seq;
+            stats->paths = static_cast<int64_t>(tr->paths.size());
+            stats->leg_tests = leg_tests;
+            stats->ms = ms;
+        }
+    });
+}
+
+extern "C" int64_t visrt_trace_results(const visrt_tracer* tr, int64_t* path_off, visrt_path* paths, int64_t cap,
+                                       int64_t* nodes) {
+    if (!tr) return -1;
+    if (path_off) std::copy(tr->path_off.begin(), tr->path_off.end(), path_off);
+    if (paths) std::copy_n(tr->paths.begin(), std::min<int64_t>(cap, tr->paths.size()), paths);
+    if (nodes) std::copy(tr->nodes.begin(), tr->nodes.end(), nodes);
+    return static_cast<int64_t>(tr->paths.size());
+}
