@@ -116,6 +116,14 @@ typedef struct {
 int visrt_point_regions(visrt_scene* scene, int64_t nsrc, const double* src_xyz,
                         visrt_region* out, visrt_stats* stats, void* stream);
 
+/* Order-2 chains of build_matrix(scene, 2) (src/vismatrix.cpp:715-797): every
+ * triple p->t->a of admitted pairs that passes chain_triple_feasible and
+ * second_order_check in each shared working plane. admitted_bits NULL = the
+ * scene's device bits of the last PREFILTERED call. out == NULL: count only.
+ * Triples are returned sorted by (p, t, a). */
+int visrt_chain_triples(visrt_scene* scene, const uint64_t* admitted_bits, int32_t* out, int64_t cap,
+                        int64_t* ntriples, visrt_stats* stats, void* stream);
+
 /* (3) Image-tree expansion (TraceAccelerator::trace, allow_diffraction = false).
  * The chain filter (build_chain_filter, src/raytracer.cpp:319-340) is given as
  * the admitted order-1 bit matrix (pair_admitted; NULL = the scene's device

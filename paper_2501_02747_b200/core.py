@@ -139,6 +139,21 @@ def point_regions(scene: Scene, src: np.ndarray) -> List[List[dict]]:
              for r in row] for row in arr]
 
 
+def chain_triples(scene: Scene, admitted_bits: Optional[np.ndarray] = None):
+    """Order-2 chains (p, t, a) of build_matrix(scene, 2) computed on the GPU
+    (chain_triple_feasible + second_order_check per shared plane), sorted."""
+    bits = None if admitted_bits is None else np.ascontiguousarray(admitted_bits, np.uint64)
+    cnt = C.c_int64()
+    st = _capi.visrt_stats()
+    L = lib()
+    check(L.visrt_chain_triples(scene.h, None if bits is None else bits.ctypes.data, None, 0, C.byref(cnt),
+                                C.byref(st), None))
+    out = np.zeros((max(cnt.value, 1), 3), np.int32)
+    check(L.visrt_chain_triples(scene.h, None if bits is None else bits.ctypes.data, out.ctypes.data,
+                                cnt.value, C.byref(cnt), C.byref(st), None))
+    return out[: cnt.value], _stats_dict(st)
+
+
 class Tracer:
     """rt::TraceAccelerator (include/rt/raytracer.hpp:96-118) over the GPU image
     tree: the chain filter is the admitted matrix (pair_admitted) plus the

@@ -1,0 +1,515 @@
+// Order-2 chain growth for sm_100a (K7): which triples p -> t -> a of admitted
+// pairs survive build_matrix's Markov-2 filter (src/vismatrix.cpp:715-797):
+//   feasible(p,t,a) = chain_triple_feasible(p,t,a)                (457-476)
+//                   and for every plane in required_planes(t,a) that (p,t)
+//                   also has: second_order_check(p,t,a,plane) != None (387-455)
+// One thread per candidate triple (warp per prefix pair (p,t), lanes over the
+// admitted aims of t), exact FP64 with the reference's operation order; the
+// surviving triples are compacted with ballot/popc + one atomic per warp.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "capi_internal.h"
+#include "device.h"
+
+namespace visrt {
+
+namespace {
+
+constexpr unsigned kAll = 0xffffffffu;
+
+struct V2 {
+    double x, y;
+};
+struct V3 {
+    double x, y, z;
+};
+
+__device__ __forceinline__ V3 v3sub(V3 a, V3 b) { return {dsub(a.x, b.x), dsub(a.y, b.y), dsub(a.z, b.z)}; }
+__device__ __forceinline__ V3 v3add(V3 a, V3 b) { return {dadd(a.x, b.x), dadd(a.y, b.y), dadd(a.z, b.z)}; }
+__device__ __forceinline__ V3 v3mul(V3 a, double s) { return {dmul(a.x, s), dmul(a.y, s), dmul(a.z, s)}; }
+__device__ __forceinline__ double v3dot(V3 a, V3 b) {
+    return dadd(dadd(dmul(a.x, b.x), dmul(a.y, b.y)), dmul(a.z, b.z));
+}
+__device__ __forceinline__ V3 v3cross(V3 a, V3 b) {
+    return {dsub(dmul(a.y, b.z), dmul(a.z, b.y)), dsub(dmul(a.z, b.x), dmul(a.x, b.z)),
+            dsub(dmul(a.x, b.y), dmul(a.y, b.x))};
+}
+__device__ __forceinline__ V2 v2sub(V2 a, V2 b) { return {dsub(a.x, b.x), dsub(a.y, b.y)}; }
+__device__ __forceinline__ double v2dot(V2 a, V2 b) { return dadd(dmul(a.x, b.x), dmul(a.y, b.y)); }
+__device__ __forceinline__ double v2cross(V2 a, V2 b) { return dsub(dmul(a.x, b.y), dmul(a.y, b.x)); }
+__device__ __forceinline__ double v2norm(V2 a) { return __dsqrt_rn(v2dot(a, a)); }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }   // std::min
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }   // std::max
+
+// Caps for MAXV-vertex faces: clip <= 2*MAXV points, hull input <= 4*MAXV,
+// slice section <= 4*MAXV + C(4*MAXV, 2).
+template <int MAXV>
+struct Caps {
+    static constexpr int kClip = 2 * MAXV;
+    static constexpr int kPts = 4 * MAXV;
+    static constexpr int kSec = kPts + kPts * (kPts - 1) / 2;
+};
+
+struct PlaneD {
+    V3 p, n;
+    __device__ double sd(V3 q) const { return v3dot(v3sub(q, p), n); }
+};
+
+__device__ __forceinline__ V3 face_pt(const DevScene& s, int f, int k) {
+    const double* P = s.pts + (static_cast<size_t>(f) * VISRT_MAX_VERTS + k) * 3;
+    return {P[0], P[1], P[2]};
+}
+
+// clip_polygon_halfspace, src/geom.cpp:191-207
+template <int MAXV>
+__device__ int clip_halfspace(const DevScene& s, int f, const PlaneD& pl, V3* out) {
+    const int n = s.nv[f];
+    int c = 0;
+    for (int i = 0; i < n; ++i) {
+        const V3 a = face_pt(s, f, i), b = face_pt(s, f, (i + 1) % n);
+        const double da = pl.sd(a), db = pl.sd(b);
+        if (da >= -kEps) out[c++] = a;
+        if ((da > kEps && db < -kEps) || (da < -kEps && db > kEps))
+            out[c++] = v3add(a, v3mul(v3sub(b, a), __ddiv_rn(da, dsub(da, db))));
+    }
+    return c < 3 ? 0 : c;
+}
+
+// convex_hull_2d, src/geom.cpp:219-242 (sort, tolerance-unique against the
+// last kept point like std::unique, Andrew's monotone chain). In place;
+// `hull` needs 2*n slots. Returns the hull size (or n unchanged if n < 3).
+__device__ int convex_hull(V2* pts, int n, V2* hull) {
+    if (n < 3) return n;
+    // insertion sort by (x, y)
+    for (int i = 1; i < n; ++i) {
+        const V2 v = pts[i];
+        int j = i - 1;
+        while (j >= 0 && (v.x < pts[j].x || (v.x == pts[j].x && v.y < pts[j].y))) {
+            pts[j + 1] = pts[j];
+            --j;
+        }
+        pts[j + 1] = v;
+    }
+    int m = 1;
+    for (int i = 1; i < n; ++i) {
+        if (fabs(dsub(pts[m - 1].x, pts[i].x)) < kEps && fabs(dsub(pts[m - 1].y, pts[i].y)) < kEps) continue;
+        pts[m++] = pts[i];
+    }
+    n = m;
+    if (n < 3) return n;
+    int k = 0;
+    for (int i = 0; i < n; ++i) {
+        while (k >= 2 && v2cross(v2sub(hull[k - 1], hull[k - 2]), v2sub(pts[i], hull[k - 2])) <= 0) --k;
+        hull[k++] = pts[i];
+    }
+    for (int i = n - 1, t = k + 1; i-- > 0;) {
+        while (k >= t && v2cross(v2sub(hull[k - 1], hull[k - 2]), v2sub(pts[i], hull[k - 2])) <= 0) --k;
+        hull[k++] = pts[i];
+    }
+    k -= 1;
+    for (int i = 0; i < k; ++i) pts[i] = hull[i];
+    return k;
+}
+
+// axis_separates / separating_axis / has_finite_edge, src/geom.cpp:245-279
+__device__ bool axis_separates(const V2* a, int na, const V2* b, int nb, V2 axis) {
+    double amin = 1e300, amax = -1e300, bmin = 1e300, bmax = -1e300;
+    for (int i = 0; i < na; ++i) {
+        const double d = v2dot(a[i], axis);
+        amin = smin(amin, d);
+        amax = smax(amax, d);
+    }
+    for (int i = 0; i < nb; ++i) {
+        const double d = v2dot(b[i], axis);
+        bmin = smin(bmin, d);
+        bmax = smax(bmax, d);
+    }
+    return amax < dsub(bmin, kEps) || bmax < dsub(amin, kEps);
+}
+__device__ bool separating_axis(const V2* a, int na, const V2* b, int nb) {
+    for (int i = 0; i < na; ++i) {
+        const V2 e = v2sub(a[(i + 1) % na], a[i]);
+        const double len = v2norm(e);
+        if (len <= 1e-12) continue;
+        if (axis_separates(a, na, b, nb, {__ddiv_rn(-e.y, len), __ddiv_rn(e.x, len)})) return true;
+        if (axis_separates(a, na, b, nb, {__ddiv_rn(e.x, len), __ddiv_rn(e.y, len)})) return true;
+    }
+    return false;
+}
+__device__ bool has_finite_edge(const V2* p, int n) {
+    for (int i = 0; i < n; ++i)
+        if (v2norm(v2sub(p[(i + 1) % n], p[i])) > 1e-12) return true;
+    return false;
+}
+
+// chain_triple_feasible, src/vismatrix.cpp:457-476
+template <int MAXV>
+__device__ bool triple_feasible(const DevScene& s, int a, int b, int c) {
+    const double* N = s.normal + 3 * static_cast<size_t>(b);
+    const PlaneD pl{face_pt(s, b, 0), {N[0], N[1], N[2]}};
+    V3 pts[Caps<MAXV>::kPts];
+    const int nl = clip_halfspace<MAXV>(s, a, pl, pts);
+    if (nl < 2) return false;
+    V3 tgt[Caps<MAXV>::kClip];
+    const int nt = clip_halfspace<MAXV>(s, c, pl, tgt);
+    if (nt < 2) return false;
+    int np = nl;
+    for (int i = 0; i < nt; ++i) {
+        const double d2 = dmul(2.0, pl.sd(tgt[i]));   // mirror_point
+        pts[np++] = v3sub(tgt[i], v3mul(pl.n, d2));
+    }
+    // PlaneFrame::from_plane, src/geom.cpp:209-217
+    const V3 axis = fabs(pl.n.x) < 0.9 ? V3{1, 0, 0} : V3{0, 1, 0};
+    V3 u = v3cross(pl.n, axis);
+    const double un = __dsqrt_rn(v3dot(u, u));
+    if (un < kEps) return false;   // normalized() would throw; cannot happen for unit normals
+    u = {__ddiv_rn(u.x, un), __ddiv_rn(u.y, un), __ddiv_rn(u.z, un)};
+    const V3 v = v3cross(pl.n, u);
+    auto to2d = [&](V3 p) {
+        const V3 r = v3sub(p, pl.p);
+        return V2{v3dot(r, u), v3dot(r, v)};
+    };
+    // hull_plane_slice, src/geom.cpp:292-307
+    double d[Caps<MAXV>::kPts];
+    for (int i = 0; i < np; ++i) d[i] = pl.sd(pts[i]);
+    V2 sec[Caps<MAXV>::kSec];
+    int ns = 0;
+    for (int i = 0; i < np; ++i) {
+        if (fabs(d[i]) <= kEps) sec[ns++] = to2d(pts[i]);
+        for (int j = i + 1; j < np; ++j) {
+            if ((d[i] > kEps && d[j] < -kEps) || (d[i] < -kEps && d[j] > kEps)) {
+                const double t = __ddiv_rn(d[i], dsub(d[i], d[j]));
+                sec[ns++] = to2d(v3add(pts[i], v3mul(v3sub(pts[j], pts[i]), t)));
+            }
+        }
+    }
+    V2 hull[2 * Caps<MAXV>::kSec];
+    ns = convex_hull(sec, ns, hull);
+    if (ns == 0) return false;
+    V2 mid2d[VISRT_MAX_VERTS];
+    const int nm = s.nv[b];
+    for (int k = 0; k < nm; ++k) mid2d[k] = to2d(face_pt(s, b, k));
+    // convex_polygons_overlap_2d, src/geom.cpp:282-290
+    if (separating_axis(sec, ns, mid2d, nm) || separating_axis(mid2d, nm, sec, ns)) return false;
+    if (!has_finite_edge(sec, ns) && !has_finite_edge(mid2d, nm)) return v2norm(v2sub(sec[0], mid2d[0])) <= kEps;
+    return true;
+}
+
+// ---- interval sets, src/vismatrix.cpp:43-97 (<= 4 intervals here) ----
+struct ISet {
+    int n;
+    double lo[4], hi[4];
+};
+
+__device__ void normalize_set(ISet& s) {
+    // sort lexicographically (std::array<double,2> operator<)
+    for (int i = 1; i < s.n; ++i) {
+        const double a = s.lo[i], b = s.hi[i];
+        int j = i - 1;
+        while (j >= 0 && (a < s.lo[j] || (a == s.lo[j] && b < s.hi[j]))) {
+            s.lo[j + 1] = s.lo[j];
+            s.hi[j + 1] = s.hi[j];
+            --j;
+        }
+        s.lo[j + 1] = a;
+        s.hi[j + 1] = b;
+    }
+    int m = 0;
+    for (int i = 0; i < s.n; ++i) {
+        if (dsub(s.hi[i], s.lo[i]) < 0) continue;
+        if (m > 0 && s.lo[i] <= dadd(s.hi[m - 1], 1e-15)) {
+            s.hi[m - 1] = smax(s.hi[m - 1], s.hi[i]);
+        } else {
+            s.lo[m] = s.lo[i];
+            s.hi[m] = s.hi[i];
+            ++m;
+        }
+    }
+    s.n = m;
+}
+
+__device__ void affine_halfline(double a, double b, bool leq, double lo, double hi, ISet& out) {
+    out.n = 0;
+    if (!leq) {
+        a = -a;
+        b = -b;
+    }
+    if (fabs(a) < 1e-300) {
+        if (b <= 0) {
+            out.n = 1;
+            out.lo[0] = lo;
+            out.hi[0] = hi;
+        }
+        return;
+    }
+    const double t = __ddiv_rn(-b, a);
+    if (a > 0) {
+        if (t < lo) return;
+        out.n = 1;
+        out.lo[0] = lo;
+        out.hi[0] = smin(t, hi);
+        return;
+    }
+    if (t > hi) return;
+    out.n = 1;
+    out.lo[0] = smax(t, lo);
+    out.hi[0] = hi;
+}
+
+__device__ bool clip_param_to_upper(V2 p0, V2 p1, double& lo, double& hi) {
+    lo = 0.0;
+    hi = 1.0;
+    const double y0 = p0.y, y1 = p1.y;
+    const double dy = dsub(y1, y0);
+    if (fabs(dy) < 1e-300) return y0 >= -kEps;
+    const double tcross = __ddiv_rn(-y0, dy);
+    if (dy > 0) lo = smax(0.0, tcross);
+    else hi = smin(1.0, tcross);
+    return dsub(hi, lo) > 1e-12;
+}
+
+// second_order_check verdict != None, src/vismatrix.cpp:387-455
+__device__ bool second_order_reachable(const DevScene& s, int orig, int mid, int test, int pl) {
+    const double* so = s.seg + (static_cast<size_t>(orig) * 3 + pl) * 6;
+    const double* sm = s.seg + (static_cast<size_t>(mid) * 3 + pl) * 6;
+    const double* st = s.seg + (static_cast<size_t>(test) * 3 + pl) * 6;
+    // segment_frame, 114-128
+    V2 origin{sm[0], sm[1]};
+    const V2 dd{dsub(sm[2], sm[0]), dsub(sm[3], sm[1])};
+    const double len = v2norm(dd);
+    const double inv = __ddiv_rn(1.0, len);
+    V2 ux{dmul(dd.x, inv), dmul(dd.y, inv)};
+    const V2 uy{sm[4], sm[5]};
+    if (v2cross(ux, uy) < 0) {
+        origin = {sm[2], sm[3]};
+        ux = {dmul(ux.x, -1.0), dmul(ux.y, -1.0)};
+    }
+    auto map = [&](double x, double y) {
+        const V2 r{dsub(x, origin.x), dsub(y, origin.y)};
+        return V2{v2dot(r, ux), v2dot(r, uy)};
+    };
+    const double length = v2norm(V2{dsub(sm[2], sm[0]), dsub(sm[3], sm[1])});
+    V2 p0 = map(so[0], so[1]);
+    V2 p1 = map(so[2], so[3]);
+    {
+        double lo, hi;
+        if (!clip_param_to_upper(p0, p1, lo, hi)) return false;
+        const V2 q0{dadd(p0.x, dmul(lo, dsub(p1.x, p0.x))), dadd(p0.y, dmul(lo, dsub(p1.y, p0.y)))};
+        const V2 q1{dadd(p0.x, dmul(hi, dsub(p1.x, p0.x))), dadd(p0.y, dmul(hi, dsub(p1.y, p0.y)))};
+        p0 = q0;
+        p1 = q1;
+    }
+    const V2 c0 = map(st[0], st[1]);
+    const V2 c1 = map(st[2], st[3]);
+    double dlo, dhi;
+    if (!clip_param_to_upper(c0, c1, dlo, dhi)) return false;
+    const V2 m0{c0.x, -c0.y};
+    const V2 md{dsub(c1.x, c0.x), -dsub(c1.y, c0.y)};
+    auto condition = [&](V2 p, double bound, bool leq, ISet& out) {
+        const double a_num = dsub(dmul(md.x, p.y), dmul(p.x, md.y));
+        const double b_num = dsub(dmul(m0.x, p.y), dmul(p.x, m0.y));
+        const double a_den = -md.y;
+        const double b_den = dsub(p.y, m0.y);
+        affine_halfline(dsub(a_num, dmul(bound, a_den)), dsub(b_num, dmul(bound, b_den)), leq, dlo, dhi, out);
+    };
+    ISet r0, r1, l0, l1;
+    condition(p0, length, true, r0);
+    condition(p1, length, true, r1);
+    condition(p0, 0.0, false, l0);
+    condition(p1, 0.0, false, l1);
+    ISet right{0, {}, {}}, left{0, {}, {}};
+    for (int i = 0; i < r0.n; ++i) { right.lo[right.n] = r0.lo[i]; right.hi[right.n++] = r0.hi[i]; }
+    for (int i = 0; i < r1.n; ++i) { right.lo[right.n] = r1.lo[i]; right.hi[right.n++] = r1.hi[i]; }
+    normalize_set(right);
+    for (int i = 0; i < l0.n; ++i) { left.lo[left.n] = l0.lo[i]; left.hi[left.n++] = l0.hi[i]; }
+    for (int i = 0; i < l1.n; ++i) { left.lo[left.n] = l1.lo[i]; left.hi[left.n++] = l1.hi[i]; }
+    normalize_set(left);
+    ISet reach{0, {}, {}};
+    for (int i = 0; i < right.n; ++i)
+        for (int j = 0; j < left.n; ++j) {
+            const double lo = smax(right.lo[i], left.lo[j]);
+            const double hi = smin(right.hi[i], left.hi[j]);
+            if (lo <= hi) {
+                reach.lo[reach.n] = lo;
+                reach.hi[reach.n++] = hi;
+            }
+        }
+    normalize_set(reach);
+    double total = 0;
+    for (int i = 0; i < reach.n; ++i) total = dadd(total, dsub(reach.hi[i], reach.lo[i]));
+    return !(total <= 1e-12);
+}
+
+// required_planes bitmask (src/vismatrix.cpp:171-181) from the device plane segments
+__device__ int req_planes(const DevScene& s, int i, int j) {
+    int m = 0;
+    for (int pl = 0; pl < 3; ++pl) {
+        if (!s.seg_ok[3 * i + pl] || !s.seg_ok[3 * j + pl]) continue;
+        const double* a = s.seg + (static_cast<size_t>(i) * 3 + pl) * 6;
+        const double* b = s.seg + (static_cast<size_t>(j) * 3 + pl) * 6;
+        const double d = fabs(dadd(dmul(a[4], b[4]), dmul(a[5], b[5])));
+        if (d >= 1.0 - 1e-9 || d <= 1e-9) m |= 1 << pl;
+    }
+    return m;
+}
+
+struct ChainArgs {
+    DevScene s;
+    const int32_t* off1;
+    const int32_t* idx1;
+    const int32_t* pair_p;      // directed admitted pair (p, t) per rank
+    long long npairs;
+    int32_t* out;               // triples (p, t, a)
+    unsigned long long* nout;
+    long long cap;
+    unsigned long long* cursor;
+};
+
+template <int MAXV>
+__global__ void __launch_bounds__(128) k_chain_triples(ChainArgs a) {
+    const DevScene& s = a.s;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long r = 0;
+        if (lane == 0) r = atomicAdd(a.cursor, 1ull);
+        r = __shfl_sync(kAll, r, 0);
+        if (static_cast<long long>(r) >= a.npairs) break;
+        const int p = a.pair_p[r];
+        const int t = a.idx1[r];
+        const int lo = a.off1[t], hi = a.off1[t + 1];
+        const int rp_pt = req_planes(s, p, t);
+        for (int q0 = lo; q0 < hi; q0 += 32) {
+            const int q = q0 + lane;
+            bool ok = false;
+            int c = -1;
+            if (q < hi) {
+                c = a.idx1[q];
+                ok = triple_feasible<MAXV>(s, p, t, c);
+                if (ok) {
+                    const int planes = req_planes(s, t, c) & rp_pt;
+                    for (int pl = 0; pl < 3 && ok; ++pl)
+                        if (planes >> pl & 1) ok = second_order_reachable(s, p, t, c, pl);
+                }
+            }
+            const unsigned m = __ballot_sync(kAll, ok);
+            if (!m) continue;
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(a.nout, static_cast<unsigned long long>(__popc(m)));
+            base = __shfl_sync(kAll, base, 0);
+            if (ok) {
+                const long long slot = static_cast<long long>(base) + __popc(m & ((1u << lane) - 1u));
+                if (slot < a.cap) {
+                    a.out[3 * slot] = p;
+                    a.out[3 * slot + 1] = t;
+                    a.out[3 * slot + 2] = c;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace
+}  // namespace visrt
+
+using visrt::ck;
+
+// Order-2 chains of build_matrix(scene, 2) as (p, t, a) triples, from the
+// admitted matrix (NULL: the scene's device bits of the last PREFILTERED call).
+// out == NULL: count only (result cached for the next call).
+extern "C" int visrt_chain_triples(visrt_scene* sc, const uint64_t* admitted_bits, int32_t* out, int64_t cap,
+                                   int64_t* ntriples, visrt_stats* stats, void* stream) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const visrt::HostScene& hs = visrt::scene_host(sc);
+        const visrt::DevScene& ds = visrt::scene_dev(sc);
+        const int n = hs.n, words = (n + 63) / 64;
+        std::vector<uint64_t> bits(static_cast<size_t>(n) * words);
+        if (admitted_bits) std::memcpy(bits.data(), admitted_bits, bits.size() * 8);
+        else ck(cudaMemcpy(bits.data(), visrt_matrix_bits_device(sc), bits.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+        std::vector<int32_t> off1(n + 1, 0), idx1, pp;
+        for (int p = 0; p < n; ++p) {
+            for (int w = 0; w < words; ++w) {
+                uint64_t m = bits[static_cast<size_t>(p) * words + w];
+                while (m) {
+                    const int b = __builtin_ctzll(m);
+                    m &= m - 1;
+                    idx1.push_back(w * 64 + b);
+                    pp.push_back(p);
+                }
+            }
+            off1[p + 1] = static_cast<int32_t>(idx1.size());
+        }
+        long long total = 0;
+        for (size_t r = 0; r < idx1.size(); ++r) total += off1[idx1[r] + 1] - off1[idx1[r]];
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        auto up = [&](const std::vector<int32_t>& v) {
+            int32_t* d = visrt::dalloc<int32_t>(std::max<size_t>(v.size(), 1), tmp);
+            if (!v.empty()) ck(cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice), "H2D");
+            return d;
+        };
+        visrt::ChainArgs a{};
+        a.s = ds;
+        a.off1 = up(off1);
+        a.idx1 = up(idx1);
+        a.pair_p = up(pp);
+        a.npairs = static_cast<long long>(idx1.size());
+        a.cap = std::max<long long>(total, 1);
+        a.out = visrt::dalloc<int32_t>(static_cast<size_t>(a.cap) * 3, tmp);
+        unsigned long long* ctr = visrt::dalloc<unsigned long long>(2, tmp);
+        a.nout = ctr;
+        a.cursor = ctr + 1;
+        ck(cudaMemsetAsync(ctr, 0, 16, st), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        int sms = 0, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, visrt::scene_device(sc));
+        if (a.npairs > 0) {
+            if (ds.maxv <= 4) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, visrt::k_chain_triples<4>, 128, 0);
+                visrt::k_chain_triples<4><<<sms * std::max(per, 1), 128, 0, st>>>(a);
+            } else {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, visrt::k_chain_triples<8>, 128, 0);
+                visrt::k_chain_triples<8><<<sms * std::max(per, 1), 128, 0, st>>>(a);
+            }
+            ck(cudaGetLastError(), "k_chain_triples");
+        }
+        cudaEventRecord(e1, st);
+        unsigned long long nout = 0;
+        ck(cudaMemcpyAsync(&nout, ctr, 8, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ntriples = static_cast<int64_t>(nout);
+        if (out) {
+            if (static_cast<int64_t>(nout) > cap) throw visrt::UsageError("triple capacity too small");
+            std::vector<int32_t> h(static_cast<size_t>(nout) * 3);
+            if (nout) ck(cudaMemcpy(h.data(), a.out, h.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+            // deterministic order: by (p, t) rank, then a (the growth order of build_matrix)
+            std::vector<size_t> ord(nout);
+            for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
+            std::sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
+                for (int q = 0; q < 3; ++q)
+                    if (h[3 * x + q] != h[3 * y + q]) return h[3 * x + q] < h[3 * y + q];
+                return false;
+            });
+            for (size_t k = 0; k < ord.size(); ++k)
+                for (int q = 0; q < 3; ++q) out[3 * k + q] = h[3 * ord[k] + q];
+        }
+        if (stats) {
+            stats->pairs = static_cast<int64_t>(idx1.size());
+            stats->candidates = total;
+            stats->admitted = static_cast<int64_t>(nout);
+            stats->tests_alg = static_cast<double>(total);
+            stats->tests_exec = total;
+            stats->ms = ms;
+        }
+    });
+}

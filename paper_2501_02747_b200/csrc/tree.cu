@@ -446,6 +446,10 @@ struct visrt_tracer {
     int32_t* idx2 = nullptr;
     int32_t* obl = nullptr;
     int32_t nobl = 0;
+    // frontier / candidate / path buffers, allocated on the first trace
+    visrt::TreeNode* lvl[2] = {nullptr, nullptr};
+    visrt::Cand* cand = nullptr;
+    visrt_path* dpaths = nullptr;
     // results of the last trace
     int64_t nsnap = 0;
     std::vector<visrt_path> paths;
@@ -591,10 +595,15 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         const long long node_cap = 1ll << 24;   // 16.7M nodes per level per batch (0.9 GB)
         const long long cand_cap = 1ll << 22;
         const long long path_cap = 1ll << 22;
-        visrt::TreeNode* lvl[2] = {visrt::dalloc<visrt::TreeNode>(node_cap, tmp),
-                                   visrt::dalloc<visrt::TreeNode>(node_cap, tmp)};
-        visrt::Cand* d_cand = visrt::dalloc<visrt::Cand>(cand_cap, tmp);
-        visrt_path* d_paths = visrt::dalloc<visrt_path>(path_cap, tmp);
+        if (!tr->lvl[0]) {
+            tr->lvl[0] = visrt::dalloc<visrt::TreeNode>(node_cap, tr->allocs);
+            tr->lvl[1] = visrt::dalloc<visrt::TreeNode>(node_cap, tr->allocs);
+            tr->cand = visrt::dalloc<visrt::Cand>(cand_cap, tr->allocs);
+            tr->dpaths = visrt::dalloc<visrt_path>(path_cap, tr->allocs);
+        }
+        visrt::TreeNode* lvl[2] = {tr->lvl[0], tr->lvl[1]};
+        visrt::Cand* d_cand = tr->cand;
+        visrt_path* d_paths = tr->dpaths;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
