@@ -169,7 +169,7 @@ def run_reference(args, rank, world):
     except Exception:
         kind = "port"
         o = bindings.Oracle(soup)
-    per_step = max(1000, cores * 60)
+    per_step = max(4000, cores * 500)
     times, tests = [], []
     for step in range(args.warmup + args.steps):
         pi, pj = _sample_pairs(soup.nfaces, per_step, 5000 + step)
@@ -258,16 +258,9 @@ def run_visrt(args, rank, world):
     e2e_s = sum(e2e_times) / len(e2e_times)
 
     # ---- reductions over ranks ------------------------------------------
-    ms_max = ms_local
-    e2e_max = e2e_s
-    total_tests = tests_alg
-    if dist is not None:
-        t = torch.tensor([ms_local, e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max, e2e_max = float(t[0]), float(t[1])
-        tt = torch.tensor([tests_alg], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        total_tests = float(tt[0])
+    from paper_2501_02747_b200.dist import reduce_step_metrics
+    ms_max, total_tests = reduce_step_metrics(ms_local, tests_alg, device="cuda")
+    e2e_max, _ = reduce_step_metrics(e2e_s, 0.0, device="cuda")
     if rank == 0:
         fp64_peak, fp32_peak = measure_peaks(local)
         kern = sum(kern_ms) / len(kern_ms)

@@ -81,6 +81,7 @@ struct visrt_scene {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     ~visrt_scene() {
+        if (device < 0) return;   // host-only handle
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(device);
@@ -162,6 +163,11 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         auto sc = std::make_unique<visrt_scene>();
         sc->device = device;
         visrt::ingest(*f, sc->hs);
+        if (device < 0) {   // host-only handle: ingest products, no device state
+            sc->ds.n = sc->hs.n;
+            *out = sc.release();
+            return;
+        }
         ck(cudaSetDevice(device), "cudaSetDevice");
         const auto& hs = sc->hs;
         auto& ds = sc->ds;
@@ -229,7 +235,7 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
         if (!sc) throw UsageError("null scene");
         const bool pref = (flags & VISRT_PAIRS_PREFILTERED) != 0;
         if (!pref && !(flags & VISRT_PAIRS_ALL)) throw UsageError("flags must select ALL or PREFILTERED");
-        ck(cudaSetDevice(sc->device), "cudaSetDevice");
+        visrt::ScopedDevice dev_guard(sc);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int n = sc->hs.n;
         const long long npairs = static_cast<long long>(n) * (n - 1) / 2;
@@ -338,7 +344,7 @@ int visrt_pair_detail(visrt_scene* sc, int64_t npairs, const int32_t* ci, const 
                       int64_t* blk_off, int32_t* blk_idx, int64_t blk_cap, visrt_stats* stats, void* stream) {
     return guarded([&] {
         if (!sc) throw UsageError("null scene");
-        ck(cudaSetDevice(sc->device), "cudaSetDevice");
+        visrt::ScopedDevice dev_guard(sc);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int n = sc->hs.n;
         for (int64_t k = 0; k < npairs; ++k) {

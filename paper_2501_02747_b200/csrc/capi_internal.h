@@ -62,6 +62,7 @@ int scene_device(const visrt_scene* s);
 struct ScopedDevice {
     explicit ScopedDevice(const visrt_scene* s) {
         if (!s) throw UsageError("null scene");
+        if (scene_device(s) < 0) throw UsageError("host-only scene handle (device < 0) has no device state");
         ck(cudaSetDevice(scene_device(s)), "cudaSetDevice");
     }
 };

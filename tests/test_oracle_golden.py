@@ -1,0 +1,134 @@
+"""CPU: the C restatement oracle (oracle/visrt_oracle.c) pinned against the
+reference's golden vectors (tests/golden, generated from the compiled
+reference) and the reference's own known-answer tests
+(proj/tests/test_vismatrix.cpp, test_vistable.cpp, test_raytracer.cpp)."""
+import numpy as np
+import pytest
+
+import golden_util as G
+
+FIX = ["two_buildings", "street_canyon", "screened_wall", "manhattan", "config1"]
+
+
+@pytest.fixture(scope="module", params=FIX)
+def fixture(request, oracle_built):
+    d = G.load(request.param)
+    s = G.soup(d)
+    return d, s, oracle_built.Oracle(s), oracle_built
+
+
+def test_kinds_all_pairs(fixture):
+    d, s, o, _ = fixture
+    pi, pj = G.pairs(s.nfaces)
+    np.testing.assert_array_equal(o.occlusion_batch(pi, pj), G.kinds(d))
+
+
+def test_blockers(fixture):
+    d, s, o, _ = fixture
+    for key, exp in list(d.get("blockers", {}).items())[:400]:
+        i, j = (int(x) for x in key.split(","))
+        k, blk = o.occlusion(i, j)
+        assert k == 1
+        assert sorted(blk) == sorted(exp)
+
+
+def test_admitted_pairs(fixture):
+    """pair_admitted of build_matrix(scene, 1) = prefilter and not Occluded
+    (no degenerate bouncing ranges occur in these scenes)."""
+    d, s, o, _ = fixture
+    n = s.nfaces
+    adm = G.admitted_matrix(d)
+    pi, pj = G.pairs(n)
+    kinds = G.kinds(d)
+    got = np.zeros((n, n), bool)
+    for i, j, k in zip(pi, pj, kinds):
+        if k != 2 and o.prefilter(int(i), int(j)):
+            got[i, j] = got[j, i] = True
+    np.testing.assert_array_equal(got, adm)
+
+
+def test_matrix1_entry_planes(fixture):
+    d, s, o, _ = fixture
+    for e in d["matrix1"]:
+        assert o.required_planes(e["ref"], e["aim"]) >> e["plane"] & 1
+
+
+def test_regions(fixture):
+    d, s, o, _ = fixture
+    for rec in d["regions"]:
+        src = G.unhex(rec["source"])
+        for f, row in enumerate(rec["regions"]):
+            e = o.illuminated_region(src, f)
+            got = (e["present"], e["has"], e["clipped"], e["sub"])
+            exp = G.region_tuple(row)
+            if exp[0] != 1:   # none / VisibilityError carry no plane records
+                assert got[0] == exp[0], (f, got, exp)
+            else:
+                assert got == exp, (f, got, exp)
+
+
+def test_traces(fixture):
+    d, s, o, ob = fixture
+    n = s.nfaces
+    adm = G.admitted_matrix(d)
+    filt2 = ob.chain_filter_arrays(n, adm)
+    filt3 = ob.chain_filter_arrays(n, adm, d["triples"])
+    for t in d["traces"]:
+        filt = filt3 if t["order"] == 3 else filt2
+        paths, st = o.trace(filt, t["order"], G.unhex(t["tx"]), G.unhex(t["rx"]))
+        got = sorted(("LOS" if not p["faces"] else "/".join("R:" + s.ids[f] for f in p["faces"]),
+                      p["points"], p["length"]) for p in paths)
+        exp = sorted((p["identity"], G.unhex(p["points"]), G.unhex(p["length"])) for p in t["paths"])
+        assert got == exp
+        assert st[0] == t["nodes"]
+        assert st[1] == t["sequences"]
+
+
+# ---- the reference's own known-answer tests -----------------------------------
+
+def test_two_buildings_table1_rows():
+    """proj/tests/test_vismatrix.cpp:72-127: the six published first-order rows."""
+    d = G.load("two_buildings")
+    faces = d["faces"]
+    lab = lambda i, pl: (faces[i]["label_xy"] if pl == 0 else faces[i]["label_vert"]) or faces[i]["id"]
+    rows = sorted((lab(e["ref"], e["plane"]), lab(e["aim"], e["plane"]), e["kind"]) for e in d["matrix1"])
+    assert rows == sorted([("AB", "EF", "PAR"), ("EF", "AB", "PAR"), ("FG", "HJ", "PAR"),
+                           ("FG", "HI", "PER"), ("HI", "FG", "PER"), ("HJ", "FG", "PAR")])
+    ids = [f["id"] for f in faces]
+    ab = [e for e in d["matrix1"] if ids[e["ref"]] == "B1_n" and ids[e["aim"]] == "B2_s" and e["plane"] == 0][0]
+    assert np.allclose(G.unhex(ab["ranges"]), [45.0, 90.0, 45.0, 90.0])
+    fg = [e for e in d["matrix1"] if ids[e["ref"]] == "B1_n" and ids[e["aim"]] == "B2_s" and e["plane"] == 1][0]
+    assert np.allclose(G.unhex(fg["ranges"])[2:], [18.43494882292201, 26.56505117707799])
+    roof = [e for e in d["matrix1"] if ids[e["ref"]] == "B1_n" and ids[e["aim"]] == "B2_roof"][0]
+    assert [ids[b] for b in roof["blockers"]] == ["B2_s"]
+
+
+def test_street_canyon_and_manhattan_counts():
+    """test_vismatrix.cpp:129-145 (10 entries), 242-283 (17 order-2 chains),
+    309-313 (Manhattan order 1 = 950 entries)."""
+    assert len(G.load("street_canyon")["matrix1"]) == 10
+    assert len(G.load("street_canyon")["triples"]) == 17
+    assert len(G.load("manhattan")["matrix1"]) == 950
+
+
+def test_street_canyon_clipped_region():
+    """test_vistable.cpp:55-96: source (5, 28, 11) lights B1_n above the low
+    roof's shadow line; the reference's own value is 8.75/30 shifted by the
+    kEps tolerance."""
+    d = G.load("street_canyon")
+    ids = [f["id"] for f in d["faces"]]
+    rec = d["regions"][0]
+    assert G.unhex(rec["source"]) == [5.0, 28.0, 11.0]
+    present, has, clipped, sub = G.region_tuple(rec["regions"][ids.index("B1_n")])
+    assert present == 1 and clipped[1] == 1 and clipped[0] == 0
+    assert abs(sub[2] - 8.75 / 30.0) < 1e-8 and sub[3] == 1.0
+    assert G.region_tuple(rec["regions"][ids.index("ground")])[0] == 0   # in the low building's shadow
+
+
+def test_two_buildings_trace_set():
+    """test_raytracer.cpp:170-199: LOS, single bounces off both walls and the
+    ping-pong double bounces between (3,15,2) and (7,16,3)."""
+    d = G.load("two_buildings")
+    t3 = [t for t in d["traces"] if t["order"] == 3 and G.unhex(t["tx"]) == [3.0, 15.0, 2.0]][0]
+    ids = {p["identity"] for p in t3["paths"]}
+    assert {"LOS", "R:B1_n", "R:B2_s", "R:B1_n/R:B2_s", "R:B2_s/R:B1_n"} <= ids
