@@ -39,6 +39,8 @@
 #include "rt/vismatrix.hpp"
 #include "rt/vistable.hpp"
 
+#include "ref_capi.h"
+
 namespace R = visrt_ref;
 
 namespace {
@@ -102,6 +104,42 @@ void* vref_scene_from_soup(int32_t nfaces, const int32_t* vert_off, const double
             rs->scene.face_ptrs_.push_back(&rs->soup[static_cast<size_t>(i)]);
             rs->scene.face_index_[rs->soup[static_cast<size_t>(i)].id] = i;
         }
+        return rs;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// Closed-shell scene through the reference's own Scene::finalize: faces with
+// building index b >= 0 go to buildings[b] (ids '\0'-separated), the one face
+// with b < 0 (if any) is the ground.
+void* vref_scene_from_shells(int32_t nfaces, const int32_t* vert_off, const double* verts, const char* ids,
+                             const int32_t* building, int32_t nbuildings, const char* building_ids) {
+    try {
+        auto* rs = new RefScene();
+        rs->scene.materials.push_back({"concrete", 5.31, 0.139});
+        const char* bp = building_ids;
+        for (int32_t b = 0; b < nbuildings; ++b) {
+            R::Building bd;
+            bd.id = bp;
+            bp += bd.id.size() + 1;
+            rs->scene.buildings.push_back(std::move(bd));
+        }
+        const char* idp = ids;
+        for (int32_t i = 0; i < nfaces; ++i) {
+            R::Face f;
+            f.id = idp;
+            idp += f.id.size() + 1;
+            f.material = "concrete";
+            std::vector<R::Vec3> pts;
+            for (int32_t k = vert_off[i]; k < vert_off[i + 1]; ++k)
+                pts.push_back({verts[3 * k], verts[3 * k + 1], verts[3 * k + 2]});
+            f.poly = R::ConvexPolygon::from_points(std::move(pts));
+            if (building[i] >= 0) rs->scene.buildings[static_cast<size_t>(building[i])].faces.push_back(std::move(f));
+            else rs->scene.ground = std::move(f);
+        }
+        rs->scene.finalize();
         return rs;
     } catch (const std::exception& e) {
         g_err = e.what();
@@ -239,25 +277,6 @@ int32_t vref_segment_hits_face(void* h, const double* a, const double* b, int32_
 // build_matrix (proj/src/vismatrix.cpp:638-799) — entries exported flat
 // ---------------------------------------------------------------------------
 
-struct vref_entry {
-    int32_t order;
-    int32_t chain[5];
-    int32_t chain_len;
-    int32_t plane;
-    int32_t kind;      // 0 PAR, 1 PER
-    int32_t verdict;   // 0 Full, 1 Partial
-    int32_t has_criterion;
-    int32_t nblockers;
-    int32_t nsub;
-    int32_t naim_image;
-    double ranges[12];     // at_a: vertex.x, vertex.y, low, high, ref_dir.x, ref_dir.y; at_b: same
-    double criterion[4];   // at_a low/high, at_b low/high
-    double sub[8];         // up to 4 subranges
-    double aim_image[24];  // up to 8 points
-    int32_t blockers[64];
-    char edge_a[64];
-    char edge_b[64];
-};
 
 void* vref_build_matrix(void* h, int32_t order) {
     try {
@@ -323,16 +342,6 @@ int32_t vref_matrix_entry(void* h, void* m, int64_t k, vref_entry* out) {
 // (2) illuminated_region (proj/src/vistable.cpp:287-334)
 // ---------------------------------------------------------------------------
 
-struct vref_region {
-    int32_t present;      // 0 none (back-facing / hidden), 1 present, -1 VisibilityError
-    int32_t nplanes;
-    int32_t plane[3];
-    int32_t clipped[3];
-    double sub[6];
-    double image[6];
-    double sub_ab[12];    // sub_a.x, sub_a.y, sub_b.x, sub_b.y per plane
-    double angles[12];    // alpha_full, beta_full, alpha, beta per plane
-};
 
 int32_t vref_illuminated_region(void* h, const double* src, int32_t face, vref_region* out) {
     const R::Scene& s = static_cast<RefScene*>(h)->scene;
@@ -441,15 +450,6 @@ void* vref_accel_create(void* h, void* m, int32_t max_refl) {
 
 void vref_accel_free(void* a) { delete static_cast<R::TraceAccelerator*>(a); }
 
-struct vref_path {
-    int32_t ninter;
-    int32_t face[6];      // reflection face indices (-1 for diffraction)
-    int32_t is_diff[6];
-    double points[24];    // source, interactions..., receiver
-    double length;
-    double delay;
-    char identity[256];
-};
 
 static int64_t export_paths(const R::Scene& s, const std::vector<R::Path>& paths, vref_path* out,
                             int64_t cap) {

@@ -1,0 +1,74 @@
+/* TEST INFRASTRUCTURE ONLY — C-ABI of the compiled-reference adapter
+ * (oracle/ref_capi.cpp -> oracle/_ref/libvisrt_ref.so). */
+#ifndef VISRT_REF_CAPI_H
+#define VISRT_REF_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    int32_t order;
+    int32_t chain[5];
+    int32_t chain_len;
+    int32_t plane;
+    int32_t kind;      /* 0 PAR, 1 PER */
+    int32_t verdict;   /* 0 Full, 1 Partial */
+    int32_t has_criterion;
+    int32_t nblockers;
+    int32_t nsub;
+    int32_t naim_image;
+    double ranges[12];     /* at_a: vertex.x, vertex.y, low, high, ref_dir.x, ref_dir.y; at_b: same */
+    double criterion[4];   /* at_a low/high, at_b low/high */
+    double sub[8];         /* up to 4 subranges */
+    double aim_image[24];  /* up to 8 points */
+    int32_t blockers[64];
+    char edge_a[64];
+    char edge_b[64];
+} vref_entry;
+
+typedef struct {
+    int32_t present;      /* 0 none, 1 present, -1 VisibilityError */
+    int32_t nplanes;
+    int32_t plane[3];
+    int32_t clipped[3];
+    double sub[6];
+    double image[6];
+    double sub_ab[12];
+    double angles[12];    /* alpha_full, beta_full, alpha, beta per plane */
+} vref_region;
+
+typedef struct {
+    int32_t ninter;
+    int32_t face[6];
+    int32_t is_diff[6];
+    double points[24];
+    double length;
+    double delay;
+    char identity[256];
+} vref_path;
+
+const char* vref_last_error(void);
+void* vref_scene_from_soup(int32_t nfaces, const int32_t* vert_off, const double* verts, const char* ids);
+void* vref_scene_from_shells(int32_t nfaces, const int32_t* vert_off, const double* verts, const char* ids,
+                             const int32_t* building, int32_t nbuildings, const char* building_ids);
+void vref_scene_free(void* h);
+int32_t vref_nfaces(void* h);
+void* vref_build_matrix(void* h, int32_t order);
+void vref_matrix_free(void* m);
+void vref_matrix_set_max_order(void* m, int32_t order);
+int64_t vref_matrix_size(void* m);
+int32_t vref_matrix_entry(void* h, void* m, int64_t k, vref_entry* out);
+int32_t vref_occlusion(void* h, int32_t i, int32_t j, int32_t* blockers, int32_t cap, int32_t* nblk);
+int32_t vref_illuminated_region(void* h, const double* src, int32_t face, vref_region* out);
+void* vref_accel_create(void* h, void* m, int32_t max_refl);
+void vref_accel_free(void* a);
+int64_t vref_accel_trace(void* h, void* a, const double* tx, const double* rx, int32_t diffraction,
+                         vref_path* out, int64_t cap, int64_t* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -61,7 +61,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out.decode())
     subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs +
                    ["-lcudart"], check=True)
+    build_rt()
     return LIB
+
+
+RT_LIB = os.path.join(HERE, "librt_b200.so")
+
+
+def build_rt() -> str:
+    """The C++ drop-in layer (namespace rt over the C-ABI), host code only."""
+    src = os.path.join(HERE, "cpp", "rt.cpp")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-shared", "-o", RT_LIB, src,
+                    "-I", os.path.join(HERE, "cpp"), "-L", HERE, "-lvisrt_cuda", "-Wl,-rpath,$ORIGIN"], check=True)
+    return RT_LIB
 
 
 if __name__ == "__main__":

@@ -1,0 +1,753 @@
+// visrt-b200 C++ drop-in layer (see rt.hpp). Every geometric decision comes
+// from the C-ABI (GPU); this file only materialises the reference's records:
+// ids, angle records (atan2 on the host, as the reference), aim images,
+// ordering. Compiled with -ffp-contract=off.
+#include "rt.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+#include <unordered_set>
+
+#include "../../include/visrt.h"
+
+namespace rt {
+namespace {
+
+[[noreturn]] void fail(int rc) {
+    const std::string msg = visrt_last_error();
+    if (rc == VISRT_E_VISIBILITY) throw VisibilityError(msg);
+    if (rc == VISRT_E_PLACEMENT) throw PlacementError(msg);
+    if (rc == VISRT_E_SCENE) throw SceneError(msg);
+    throw std::runtime_error("visrt: " + msg);
+}
+void check(int rc) {
+    if (rc != VISRT_OK) fail(rc);
+}
+
+double dot(const Vec3& a, const Vec3& b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+double norm(const Vec3& a) { return std::sqrt(dot(a, a)); }
+double dot2(const Vec2& a, const Vec2& b) { return a.x * b.x + a.y * b.y; }
+double cross2(const Vec2& a, const Vec2& b) { return a.x * b.y - a.y * b.x; }
+double norm2(const Vec2& a) { return std::sqrt(dot2(a, a)); }
+Vec2 sub2(const Vec2& a, const Vec2& b) { return {a.x - b.x, a.y - b.y}; }
+Vec2 project(const Vec3& p, PlaneTag t) {
+    if (t == PlaneTag::XY) return {p.x, p.y};
+    if (t == PlaneTag::YZ) return {p.y, p.z};
+    return {p.x, p.z};
+}
+double signed_distance(const Face& f, const Vec3& p) { return dot(p - f.poly.pts.front(), f.poly.normal); }
+Vec3 mirror(const Face& f, const Vec3& p) { return p - f.poly.normal * (2.0 * signed_distance(f, p)); }
+Orientation classify(const Vec3& n) {   // src/scene.cpp:19-24
+    const double ax = std::abs(n.x), ay = std::abs(n.y), az = std::abs(n.z);
+    if (ax <= 1e-9 && ay <= 1e-9) return Orientation::Horizontal;
+    if (az <= 1e-9) return Orientation::Vertical;
+    return Orientation::Oblique;
+}
+
+// oriented_angle_deg / clamp_visibility_angle, src/geom.cpp:64-77
+double oriented_angle(const Vec2& d, const Vec2& n, const Vec2& v) {
+    constexpr double kRad2Deg = 180.0 / 3.14159265358979323846;
+    const double s = cross2(d, n) >= 0.0 ? 1.0 : -1.0;
+    double a = std::atan2(s * cross2(d, v), dot2(d, v)) * kRad2Deg;
+    if (a < 0.0) a += 360.0;
+    if (a >= 360.0) a -= 360.0;
+    return a;
+}
+double clamp_angle(double a) { return a < 180.0 ? a : 0.0; }
+
+struct Segs {   // plane segments of every face, from the C-ABI ingest
+    std::vector<double> seg;
+    std::vector<int32_t> ok;
+    bool has(int f, int pl) const { return ok[3 * static_cast<size_t>(f) + pl] != 0; }
+    PlaneSegment get(int f, int pl) const {
+        const double* s = &seg[(static_cast<size_t>(f) * 3 + pl) * 6];
+        return {{s[0], s[1]}, {s[2], s[3]}, {s[4], s[5]}};
+    }
+};
+
+Segs scene_segs(const Scene& sc) {
+    Segs s;
+    const int n = static_cast<int>(sc.faces().size());
+    s.seg.resize(static_cast<size_t>(n) * 18);
+    s.ok.resize(static_cast<size_t>(n) * 3);
+    check(visrt_scene_ingest(sc.device_scene(), nullptr, nullptr, s.seg.data(), s.ok.data()));
+    return s;
+}
+
+// required_planes, src/vismatrix.cpp:171-181
+std::vector<PlaneTag> required_planes(const Segs& s, int i, int j) {
+    std::vector<PlaneTag> out;
+    for (int pl = 0; pl < 3; ++pl) {
+        if (!s.has(i, pl) || !s.has(j, pl)) continue;
+        const double d = std::abs(dot2(s.get(i, pl).normal, s.get(j, pl).normal));
+        if (d >= 1.0 - 1e-9 || d <= 1e-9) out.push_back(static_cast<PlaneTag>(pl));
+    }
+    return out;
+}
+
+// bounding_edge_id, src/vismatrix.cpp:316-330
+std::string bounding_edge_id(const Scene& sc, const Face& face, PlaneTag plane, const Vec2& endpoint) {
+    if (face.building.empty()) return "";
+    for (const Edge& e : sc.edges()) {
+        if (e.building != face.building) continue;
+        if (std::find(e.faces.begin(), e.faces.end(), face.id) == e.faces.end()) continue;
+        const Vec2 pa = project(e.a, plane), pb = project(e.b, plane);
+        if (norm2(sub2(pa, endpoint)) <= 1e-9 && norm2(sub2(pb, endpoint)) <= 1e-9) return e.id;
+    }
+    return "";
+}
+
+// angle_record / first_order_ranges / clamp_complement, src/vismatrix.cpp:332-385
+AngleRecord angle_record(const Scene& sc, const Face& ref, PlaneTag plane, const Vec2& at, const Vec2& other,
+                         const Vec2& outward, const PlaneSegment& aim) {
+    AngleRecord rec;
+    rec.vertex = at;
+    rec.outward = outward;
+    const Vec2 d = sub2(other, at);
+    const double inv = 1.0 / norm2(d);
+    rec.ref_dir = {d.x * inv, d.y * inv};
+    rec.edge_id = bounding_edge_id(sc, ref, plane, at);
+    auto angle_to = [&](const Vec2& t) {
+        const Vec2 v = sub2(t, at);
+        if (norm2(v) <= kEps) return 0.0;
+        return clamp_angle(oriented_angle(rec.ref_dir, outward, v));
+    };
+    const double a1 = angle_to(aim.a), a2 = angle_to(aim.b);
+    rec.low = std::min(a1, a2);
+    rec.high = std::max(a1, a2);
+    return rec;
+}
+AngularBouncingRange first_order_ranges(const Scene& sc, const Segs& s, int ref, int aim, PlaneTag plane) {
+    const PlaneSegment sr = s.get(ref, static_cast<int>(plane)), sa = s.get(aim, static_cast<int>(plane));
+    const Face& f = sc.face(ref);
+    return {angle_record(sc, f, plane, sr.a, sr.b, sr.normal, sa), angle_record(sc, f, plane, sr.b, sr.a, sr.normal, sa)};
+}
+AngularBouncingRange clamp_complement(const AngularBouncingRange& r) {
+    auto flip = [](const AngleRecord& rec) {
+        AngleRecord out = rec;
+        const double a = clamp_angle(180.0 - rec.low), b = clamp_angle(180.0 - rec.high);
+        out.low = std::min(a, b);
+        out.high = std::max(a, b);
+        return out;
+    };
+    return {flip(r.at_a), flip(r.at_b)};
+}
+InterfaceRelation relation(const Scene& sc, const Segs& s, int ref, int aim, PlaneTag plane) {
+    const double d = std::abs(dot2(s.get(ref, static_cast<int>(plane)).normal, s.get(aim, static_cast<int>(plane)).normal));
+    InterfaceRelation r;
+    r.plane = plane;
+    r.chain = {sc.face(ref).id, sc.face(aim).id};
+    r.chain_orientations = {sc.face(ref).orientation, sc.face(aim).orientation};
+    r.kind = d >= 1.0 - 1e-9 ? RelationKind::Parallel : RelationKind::Perpendicular;
+    return r;
+}
+std::vector<Vec3> chain_image(const Scene& sc, const std::vector<int>& chain) {   // 306-314
+    const Face& aim = sc.face(chain.back());
+    std::vector<Vec3> img(aim.poly.pts.begin(), aim.poly.pts.end());
+    for (size_t k = chain.size() - 1; k-- > 0;)
+        for (Vec3& p : img) p = mirror(sc.face(chain[k]), p);
+    return img;
+}
+
+// second_order_check verdict + reachable set (src/vismatrix.cpp:43-147, 387-455):
+// the host re-derives the record fields of a chain the GPU found feasible.
+using Interval = std::array<double, 2>;
+using ISet = std::vector<Interval>;
+ISet normalize(ISet s) {
+    std::sort(s.begin(), s.end());
+    ISet out;
+    for (const Interval& iv : s) {
+        if (iv[1] - iv[0] < 0) continue;
+        if (!out.empty() && iv[0] <= out.back()[1] + 1e-15) out.back()[1] = std::max(out.back()[1], iv[1]);
+        else out.push_back(iv);
+    }
+    return out;
+}
+ISet halfline(double a, double b, bool leq, double lo, double hi) {
+    if (!leq) {
+        a = -a;
+        b = -b;
+    }
+    if (std::abs(a) < 1e-300) return b <= 0 ? ISet{{lo, hi}} : ISet{};
+    const double t = -b / a;
+    if (a > 0) return t < lo ? ISet{} : ISet{{lo, std::min(t, hi)}};
+    return t > hi ? ISet{} : ISet{{std::max(t, lo), hi}};
+}
+bool clip_upper(const Vec2& p0, const Vec2& p1, double& lo, double& hi) {
+    lo = 0.0;
+    hi = 1.0;
+    const double dy = p1.y - p0.y;
+    if (std::abs(dy) < 1e-300) return p0.y >= -kEps;
+    const double tc = -p0.y / dy;
+    if (dy > 0) lo = std::max(0.0, tc);
+    else hi = std::min(1.0, tc);
+    return hi - lo > 1e-12;
+}
+ChainVerdict second_order(const Segs& s, int o, int m, int t, PlaneTag plane, ISet& reach_out) {
+    const int pl = static_cast<int>(plane);
+    const PlaneSegment so = s.get(o, pl), sm = s.get(m, pl), st = s.get(t, pl);
+    Vec2 origin = sm.a;
+    const Vec2 d = sub2(sm.b, sm.a);
+    const double inv = 1.0 / norm2(d);
+    Vec2 ux{d.x * inv, d.y * inv};
+    if (cross2(ux, sm.normal) < 0) {
+        origin = sm.b;
+        ux = {ux.x * -1.0, ux.y * -1.0};
+    }
+    auto map = [&](const Vec2& p) { const Vec2 r = sub2(p, origin); return Vec2{dot2(r, ux), dot2(r, sm.normal)}; };
+    const double length = norm2(sub2(sm.b, sm.a));
+    Vec2 p0 = map(so.a), p1 = map(so.b);
+    double lo, hi;
+    if (!clip_upper(p0, p1, lo, hi)) return ChainVerdict::None;
+    const Vec2 q0{p0.x + lo * (p1.x - p0.x), p0.y + lo * (p1.y - p0.y)};
+    const Vec2 q1{p0.x + hi * (p1.x - p0.x), p0.y + hi * (p1.y - p0.y)};
+    p0 = q0;
+    p1 = q1;
+    const Vec2 c0 = map(st.a), c1 = map(st.b);
+    double dlo, dhi;
+    if (!clip_upper(c0, c1, dlo, dhi)) return ChainVerdict::None;
+    const Vec2 m0{c0.x, -c0.y}, md{c1.x - c0.x, -(c1.y - c0.y)};
+    auto cond = [&](const Vec2& p, double bound, bool leq) {
+        const double a_num = md.x * p.y - p.x * md.y, b_num = m0.x * p.y - p.x * m0.y;
+        const double a_den = -md.y, b_den = p.y - m0.y;
+        return halfline(a_num - bound * a_den, b_num - bound * b_den, leq, dlo, dhi);
+    };
+    ISet right = cond(p0, length, true), r1 = cond(p1, length, true);
+    right.insert(right.end(), r1.begin(), r1.end());
+    right = normalize(right);
+    ISet left = cond(p0, 0.0, false), l1 = cond(p1, 0.0, false);
+    left.insert(left.end(), l1.begin(), l1.end());
+    left = normalize(left);
+    ISet reach;
+    for (const Interval& x : right)
+        for (const Interval& y : left) {
+            const double a = std::max(x[0], y[0]), b = std::min(x[1], y[1]);
+            if (a <= b) reach.push_back({a, b});
+        }
+    reach = normalize(reach);
+    double len = 0;
+    for (const Interval& iv : reach) len += iv[1] - iv[0];
+    if (len <= 1e-12) return ChainVerdict::None;
+    reach_out = reach;
+    if (reach.size() == 1 && reach.front()[0] <= 1e-9 && reach.front()[1] >= 1.0 - 1e-9) {
+        reach_out.clear();
+        return ChainVerdict::Full;
+    }
+    return ChainVerdict::Partial;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+ConvexPolygon ConvexPolygon::from_points(std::vector<Vec3> pts) {
+    if (pts.size() < 3) throw std::invalid_argument("polygon needs at least three vertices");
+    Vec3 n{0, 0, 0};
+    for (size_t i = 0; i < pts.size(); ++i) {   // Newell, src/geom.cpp:126-140
+        const Vec3& a = pts[i];
+        const Vec3& b = pts[(i + 1) % pts.size()];
+        n.x += (a.y - b.y) * (a.z + b.z);
+        n.y += (a.z - b.z) * (a.x + b.x);
+        n.z += (a.x - b.x) * (a.y + b.y);
+    }
+    const double len = norm(n);
+    if (len < kEps) throw std::invalid_argument("cannot normalize zero-length vector");
+    ConvexPolygon p;
+    p.normal = {n.x / len, n.y / len, n.z / len};
+    p.pts = std::move(pts);
+    return p;
+}
+
+Scene::~Scene() {
+    if (dev_) visrt_scene_destroy(dev_);
+}
+
+void Scene::finalize() {
+    face_ptrs_.clear();
+    face_index_.clear();
+    edges_.clear();
+    auto reg = [&](Face& f) {
+        if (face_index_.count(f.id)) throw SceneError("duplicate face id '" + f.id + "'");
+        f.orientation = classify(f.poly.normal);
+        f.index = static_cast<int>(face_ptrs_.size());
+        face_index_[f.id] = f.index;
+        face_ptrs_.push_back(&f);
+    };
+    using Key = std::tuple<double, double, double>;
+    for (Building& b : buildings) {
+        if (b.faces.empty()) throw SceneError("building '" + b.id + "' has no faces");
+        Vec3 c{0, 0, 0};
+        double cnt = 0;
+        for (const Face& f : b.faces)
+            for (const Vec3& p : f.poly.pts) {
+                c = c + p;
+                cnt += 1;
+            }
+        c = c * (1.0 / cnt);
+        for (Face& f : b.faces) {
+            f.building = b.id;
+            Vec3 fc{0, 0, 0};
+            for (const Vec3& p : f.poly.pts) fc = fc + p;
+            const double k = static_cast<double>(f.poly.pts.size());
+            fc = {fc.x / k, fc.y / k, fc.z / k};
+            if (dot(f.poly.normal, fc - c) <= 0)
+                throw SceneError("face '" + f.id + "' of building '" + b.id + "' does not point outward");
+            reg(f);
+        }
+        // closed shell: every edge shared by exactly two faces; edge ids in key order
+        std::map<std::pair<Key, Key>, std::vector<const Face*>> ef;
+        for (const Face& f : b.faces) {
+            const size_t n = f.poly.pts.size();
+            for (size_t i = 0; i < n; ++i) {
+                Key a{f.poly.pts[i].x, f.poly.pts[i].y, f.poly.pts[i].z};
+                Key e{f.poly.pts[(i + 1) % n].x, f.poly.pts[(i + 1) % n].y, f.poly.pts[(i + 1) % n].z};
+                if (e < a) std::swap(a, e);
+                ef[{a, e}].push_back(&f);
+            }
+        }
+        size_t i = 0;
+        for (const auto& [k, fs] : ef) {
+            if (fs.size() != 2)
+                throw SceneError("building '" + b.id + "' is not a closed shell (open edge on face '" + fs.front()->id + "')");
+            Edge e;
+            e.a = {std::get<0>(k.first), std::get<1>(k.first), std::get<2>(k.first)};
+            e.b = {std::get<0>(k.second), std::get<1>(k.second), std::get<2>(k.second)};
+            e.faces = {fs[0]->id, fs[1]->id};
+            e.building = b.id;
+            e.id = b.id + "/e" + std::to_string(i++);
+            edges_.push_back(e);
+        }
+    }
+    if (ground) {
+        ground->building.clear();
+        if (classify(ground->poly.normal) != Orientation::Horizontal || ground->poly.normal.z <= 0)
+            throw SceneError("ground face '" + ground->id + "' must be horizontal, facing up");
+        reg(*ground);
+    }
+    if (face_ptrs_.empty()) throw SceneError("scene has no faces");
+}
+
+std::unique_ptr<Scene> Scene::from_facets(const std::vector<std::string>& ids,
+                                          const std::vector<std::vector<Vec3>>& rings) {
+    auto s = std::make_unique<Scene>();
+    s->soup_.reserve(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) {
+        Face f;
+        f.id = ids[i];
+        f.poly = ConvexPolygon::from_points(rings[i]);
+        f.orientation = classify(f.poly.normal);
+        f.index = static_cast<int>(i);
+        s->soup_.push_back(std::move(f));
+    }
+    for (Face& f : s->soup_) {
+        s->face_index_[f.id] = f.index;
+        s->face_ptrs_.push_back(&f);
+    }
+    return s;
+}
+
+const Face& Scene::face(const std::string& id) const {
+    auto it = face_index_.find(id);
+    if (it == face_index_.end()) throw SceneError("unknown face id '" + id + "'");
+    return *face_ptrs_[static_cast<size_t>(it->second)];
+}
+
+bool Scene::inside_building(const Vec3& p) const {
+    for (const Building& b : buildings) {
+        bool inside = true;
+        for (const Face& f : b.faces)
+            if (signed_distance(f, p) >= -kEps) {
+                inside = false;
+                break;
+            }
+        if (inside) return true;
+    }
+    return false;
+}
+
+visrt_scene* Scene::device_scene() const {
+    if (dev_) return dev_;
+    std::vector<int32_t> off{0}, bld;
+    std::vector<double> verts;
+    std::map<std::string, int> bidx;
+    for (const Building& b : buildings) bidx.emplace(b.id, static_cast<int>(bidx.size()));
+    for (const Face* f : face_ptrs_) {
+        for (const Vec3& p : f->poly.pts) {
+            verts.push_back(p.x);
+            verts.push_back(p.y);
+            verts.push_back(p.z);
+        }
+        off.push_back(off.back() + static_cast<int32_t>(f->poly.pts.size()));
+        bld.push_back(f->building.empty() ? -1 : bidx.at(f->building));
+    }
+    visrt_facets_v1 fc{static_cast<int32_t>(face_ptrs_.size()), off.data(), verts.data(),
+                       buildings.empty() ? nullptr : bld.data()};
+    check(visrt_scene_create(&fc, 0, &dev_));
+    return dev_;
+}
+
+std::optional<PlaneSegment> plane_segment(const Face& face, PlaneTag plane) {
+    std::vector<int32_t> off{0, static_cast<int32_t>(face.poly.pts.size())};
+    std::vector<double> v;
+    for (const Vec3& p : face.poly.pts) {
+        v.push_back(p.x);
+        v.push_back(p.y);
+        v.push_back(p.z);
+    }
+    visrt_facets_v1 fc{1, off.data(), v.data(), nullptr};
+    visrt_scene* h = nullptr;
+    check(visrt_scene_create(&fc, -1, &h));   // host-only ingest, the reference arithmetic
+    double seg[18];
+    int32_t ok[3];
+    const int rc = visrt_scene_ingest(h, nullptr, nullptr, seg, ok);
+    visrt_scene_destroy(h);
+    check(rc);
+    const int pl = static_cast<int>(plane);
+    if (!ok[pl]) return std::nullopt;
+    return PlaneSegment{{seg[6 * pl], seg[6 * pl + 1]}, {seg[6 * pl + 2], seg[6 * pl + 3]},
+                        {seg[6 * pl + 4], seg[6 * pl + 5]}};
+}
+
+// ---------------------------------------------------------------------------
+std::vector<const InterVisEntry*> InterVisMatrix::find(int order, const std::string& ref, const std::string& aim) const {
+    std::vector<const InterVisEntry*> out;
+    auto it = index_.find({order, ref, aim});
+    if (it != index_.end())
+        for (size_t i : it->second) out.push_back(&entries_[i]);
+    return out;
+}
+const InterVisEntry* InterVisMatrix::find(int order, const std::string& ref, const std::string& aim,
+                                          PlaneTag plane) const {
+    auto it = index_.find({order, ref, aim});
+    if (it == index_.end()) return nullptr;
+    for (size_t i : it->second)
+        if (entries_[i].relation.plane == plane) return &entries_[i];
+    return nullptr;
+}
+bool InterVisMatrix::pair_admitted(const std::string& ref, const std::string& aim) const {
+    return index_.count({1, ref, aim}) > 0;
+}
+std::vector<std::string> InterVisMatrix::aims_of(const std::string& ref) const {
+    std::vector<std::string> out;
+    for (const InterVisEntry& e : entries_)
+        if (e.order == 1 && e.ref == ref && std::find(out.begin(), out.end(), e.aim) == out.end()) out.push_back(e.aim);
+    return out;
+}
+void InterVisMatrix::add(InterVisEntry entry) {
+    auto& slot = index_[{entry.order, entry.ref, entry.aim}];
+    for (size_t i : slot)
+        if (entries_[i].relation.plane == entry.relation.plane && entries_[i].relation.chain == entry.relation.chain)
+            throw VisibilityError("duplicate matrix entry for ('" + entry.ref + "','" + entry.aim + "')");
+    slot.push_back(entries_.size());
+    entries_.push_back(std::move(entry));
+}
+
+OcclusionVerdict occlusion_judgment(const Face& ref, const Face& aim, const Scene& scene) {
+    if (ref.id == aim.id)
+        throw VisibilityError("occlusion judgment needs two distinct faces (got '" + ref.id + "')");
+    const int32_t ci = ref.index, cj = aim.index;
+    int8_t kind = 0;
+    int64_t off[2] = {0, 0};
+    visrt_stats st{};
+    check(visrt_pair_detail(scene.device_scene(), 1, &ci, &cj, &kind, off, nullptr, 0, &st, nullptr));
+    std::vector<int32_t> blk(static_cast<size_t>(off[1]) + 1);
+    check(visrt_pair_detail(scene.device_scene(), 1, &ci, &cj, &kind, off, blk.data(), off[1], &st, nullptr));
+    OcclusionVerdict v;
+    v.kind = static_cast<OcclusionVerdict::Kind>(kind);
+    std::set<std::string> ids;
+    for (int64_t k = 0; k < off[1]; ++k) ids.insert(scene.face(blk[static_cast<size_t>(k)]).id);
+    v.blockers.assign(ids.begin(), ids.end());
+    return v;
+}
+
+InterVisMatrix build_matrix(const Scene& scene, int max_order) {
+    if (max_order < 1 || max_order > 4) throw VisibilityError("max reflection order must be between 1 and 4");
+    visrt_scene* dev = scene.device_scene();
+    const int n = static_cast<int>(scene.faces().size());
+    InterVisMatrix matrix;
+    matrix.set_max_order(max_order);
+    visrt_stats st{};
+    check(visrt_pair_visibility(dev, VISRT_PAIRS_PREFILTERED, nullptr, &st, nullptr));
+    const int64_t m = visrt_candidates(dev, nullptr, nullptr, nullptr);
+    std::vector<int32_t> ci(m), cj(m);
+    std::vector<uint8_t> adm(m);
+    visrt_candidates(dev, ci.data(), cj.data(), adm.data());
+    std::vector<int32_t> ai, aj;
+    for (int64_t k = 0; k < m; ++k)
+        if (adm[k]) {
+            ai.push_back(ci[k]);
+            aj.push_back(cj[k]);
+        }
+    // verdict kinds + blockers of the admitted pairs (Partial pairs record them)
+    std::vector<int8_t> kind(ai.size());
+    std::vector<int64_t> boff(ai.size() + 1);
+    check(visrt_pair_detail(dev, static_cast<int64_t>(ai.size()), ai.data(), aj.data(), kind.data(), boff.data(),
+                            nullptr, 0, &st, nullptr));
+    std::vector<int32_t> bidx(static_cast<size_t>(boff.back()) + 1);
+    check(visrt_pair_detail(dev, static_cast<int64_t>(ai.size()), ai.data(), aj.data(), kind.data(), boff.data(),
+                            bidx.data(), boff.back(), &st, nullptr));
+    const Segs segs = scene_segs(scene);
+    // first_order_pair entries, pair order (src/vismatrix.cpp:597-634, 673-675)
+    for (size_t q = 0; q < ai.size(); ++q) {
+        std::vector<std::string> blockers;
+        if (kind[q] == 1) {
+            std::set<std::string> ids;
+            for (int64_t k = boff[q]; k < boff[q + 1]; ++k) ids.insert(scene.face(bidx[static_cast<size_t>(k)]).id);
+            blockers.assign(ids.begin(), ids.end());
+        }
+        for (PlaneTag plane : required_planes(segs, ai[q], aj[q])) {
+            for (int dir = 0; dir < 2; ++dir) {
+                const int r = dir == 0 ? ai[q] : aj[q], a = dir == 0 ? aj[q] : ai[q];
+                InterVisEntry e;
+                e.order = 1;
+                e.ref = scene.face(r).id;
+                e.aim = scene.face(a).id;
+                e.relation = relation(scene, segs, r, a, plane);
+                e.ranges = first_order_ranges(scene, segs, r, a, plane);
+                e.blockers = blockers;
+                e.aim_image = chain_image(scene, {r, a});
+                matrix.add(std::move(e));
+            }
+        }
+    }
+    if (max_order < 2) return matrix;
+    // chains: the GPU decides every feasible triple; the frontier growth and
+    // the record fields follow src/vismatrix.cpp:682-797
+    int64_t nt = 0;
+    check(visrt_chain_triples(dev, nullptr, nullptr, 0, &nt, &st, nullptr));
+    std::vector<int32_t> tri(static_cast<size_t>(nt) * 3 + 3);
+    check(visrt_chain_triples(dev, nullptr, tri.data(), nt, &nt, &st, nullptr));
+    std::unordered_set<uint64_t> feasible;
+    auto key3 = [n](int a, int b, int c) {
+        return (static_cast<uint64_t>(a) * n + static_cast<uint64_t>(b)) * n + static_cast<uint64_t>(c);
+    };
+    for (int64_t k = 0; k < nt; ++k) feasible.insert(key3(tri[3 * k], tri[3 * k + 1], tri[3 * k + 2]));
+    std::vector<std::vector<int>> aims(n);
+    for (size_t q = 0; q < ai.size(); ++q) {
+        aims[ai[q]].push_back(aj[q]);
+        aims[aj[q]].push_back(ai[q]);
+    }
+    for (auto& v : aims) std::sort(v.begin(), v.end());   // aims_of order = ascending index
+    std::vector<std::vector<int>> frontier;
+    for (int i = 0; i < n; ++i)
+        for (int a : aims[i]) frontier.push_back({i, a});
+    for (int order = 2; order <= max_order; ++order) {
+        std::vector<std::vector<int>> next;
+        for (const auto& chain : frontier) {
+            const int t = chain.back(), p = chain[chain.size() - 2];
+            for (int a : aims[t]) {
+                if (!feasible.count(key3(p, t, a))) continue;
+                const auto planes = required_planes(segs, t, a);
+                const auto first_planes = required_planes(segs, p, t);
+                InterVisEntry e;
+                e.order = order;
+                std::vector<int> grown = chain;
+                grown.push_back(a);
+                e.ref = scene.face(grown.front()).id;
+                e.aim = scene.face(a).id;
+                e.relation = relation(scene, segs, t, a, planes.front());
+                e.ranges = first_order_ranges(scene, segs, t, a, planes.front());
+                e.criterion = clamp_complement(first_order_ranges(scene, segs, p, t, first_planes.front()));
+                // triple_ext record fields (src/vismatrix.cpp:725-748)
+                e.verdict = ChainVerdict::Partial;
+                bool recorded = false;
+                for (PlaneTag pl : planes) {
+                    if (std::find(first_planes.begin(), first_planes.end(), pl) == first_planes.end()) continue;
+                    ISet reach;
+                    const ChainVerdict v = second_order(segs, p, t, a, pl, reach);
+                    if (!recorded) {
+                        e.relation.plane = pl;
+                        e.verdict = v;
+                        for (const auto& iv : reach) e.subranges.push_back(iv);
+                        recorded = true;
+                    } else if (v != ChainVerdict::Full) {
+                        e.verdict = ChainVerdict::Partial;
+                    }
+                }
+                e.relation.chain.clear();
+                e.relation.chain_orientations.clear();
+                for (int idx : grown) {
+                    e.relation.chain.push_back(scene.face(idx).id);
+                    e.relation.chain_orientations.push_back(scene.face(idx).orientation);
+                }
+                e.aim_image = chain_image(scene, grown);
+                next.push_back(grown);
+                matrix.add(std::move(e));
+            }
+        }
+        frontier = std::move(next);
+    }
+    return matrix;
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+double boundary_angle(const Vec2& at, const Vec2& other, const Vec2& outward, const Vec2& image) {
+    const Vec2 ref = sub2(other, at), ray = sub2(at, image);
+    if (norm2(ray) <= kEps || norm2(ref) <= kEps) return 0.0;
+    return clamp_angle(oriented_angle(ref, outward, ray));
+}
+Vec2 mirror_across(const Vec2& q, const Vec2& a, const Vec2& b) {
+    const Vec2 d = sub2(b, a);
+    const double len2 = dot2(d, d);
+    const double t = dot2(sub2(q, a), d) / len2;
+    const Vec2 foot{a.x + d.x * t, a.y + d.y * t};
+    return {foot.x * 2.0 - q.x, foot.y * 2.0 - q.y};
+}
+}  // namespace
+
+std::vector<std::vector<std::optional<IlluminatedRegion>>> illuminated_regions(const std::vector<Vec3>& sources,
+                                                                               const Scene& scene) {
+    visrt_scene* dev = scene.device_scene();
+    const size_t n = scene.faces().size();
+    std::vector<double> src;
+    for (const Vec3& s : sources) {
+        src.push_back(s.x);
+        src.push_back(s.y);
+        src.push_back(s.z);
+    }
+    std::vector<visrt_region> out(sources.size() * n);
+    visrt_stats st{};
+    check(visrt_point_regions(dev, static_cast<int64_t>(sources.size()), src.data(), out.data(), &st, nullptr));
+    const Segs segs = scene_segs(scene);
+    std::vector<std::vector<std::optional<IlluminatedRegion>>> res(sources.size());
+    for (size_t k = 0; k < sources.size(); ++k) {
+        res[k].resize(n);
+        for (size_t f = 0; f < n; ++f) {
+            const visrt_region& r = out[k * n + f];
+            if (r.present != 1) continue;   // none (-1: source on the plane, handled by the caller)
+            IlluminatedRegion reg;
+            reg.face = scene.face(static_cast<int>(f)).id;
+            reg.source = sources[k];
+            for (int pl = 0; pl < 3; ++pl) {
+                if (!r.has[pl]) continue;
+                const PlaneSegment sg = segs.get(static_cast<int>(f), pl);
+                PlaneIllumination pi;
+                pi.plane = static_cast<PlaneTag>(pl);
+                pi.face_a = sg.a;
+                pi.face_b = sg.b;
+                pi.outward = sg.normal;
+                pi.image = mirror_across(project(sources[k], pi.plane), sg.a, sg.b);
+                pi.sub = {r.sub[2 * pl], r.sub[2 * pl + 1]};
+                const Vec2 dir = sub2(sg.b, sg.a);
+                pi.sub_a = {sg.a.x + dir.x * pi.sub[0], sg.a.y + dir.y * pi.sub[0]};
+                pi.sub_b = {sg.a.x + dir.x * pi.sub[1], sg.a.y + dir.y * pi.sub[1]};
+                pi.alpha_full = boundary_angle(pi.face_a, pi.face_b, pi.outward, pi.image);
+                pi.beta_full = boundary_angle(pi.face_b, pi.face_a, pi.outward, pi.image);
+                pi.alpha = boundary_angle(pi.sub_a, pi.sub_b, pi.outward, pi.image);
+                pi.beta = boundary_angle(pi.sub_b, pi.sub_a, pi.outward, pi.image);
+                pi.clipped = r.clipped[pl] != 0;
+                if (pi.sub[0] > 1e-9) pi.clip_points.push_back(pi.sub_a);
+                if (pi.sub[1] < 1.0 - 1e-9) pi.clip_points.push_back(pi.sub_b);
+                reg.planes.push_back(pi);
+            }
+            res[k][f] = std::move(reg);
+        }
+    }
+    return res;
+}
+
+std::optional<IlluminatedRegion> illuminated_region(const Vec3& source, const Face& face, const Scene& scene) {
+    const double dist = signed_distance(face, source);
+    if (std::abs(dist) <= kEps) throw VisibilityError("source lies on the plane of face '" + face.id + "'");
+    if (dist < 0.0) return std::nullopt;
+    auto all = illuminated_regions({source}, scene);
+    return all[0][static_cast<size_t>(face.index)];
+}
+
+// ---------------------------------------------------------------------------
+std::string Path::identity() const {
+    if (interactions.empty()) return "LOS";
+    std::string id;
+    for (size_t i = 0; i < interactions.size(); ++i) {
+        if (i) id += '/';
+        id += (interactions[i].kind == InteractionKind::Reflection ? "R:" : "D:") + interactions[i].id;
+    }
+    return id;
+}
+
+TraceAccelerator::TraceAccelerator(const Scene& scene, const InterVisMatrix& matrix, int max_refl)
+    : scene_(&scene), max_refl_(max_refl) {
+    if (max_refl < 0) throw VisibilityError("reflection order must be non-negative");
+    if (max_refl > matrix.max_order())
+        throw VisibilityError("matrix order " + std::to_string(matrix.max_order()) +
+                              " is lower than the requested reflection order " + std::to_string(max_refl));
+    const int n = static_cast<int>(scene.faces().size());
+    const int words = (n + 63) / 64;
+    std::vector<uint64_t> bits(static_cast<size_t>(n) * words, 0);
+    std::vector<int32_t> tri;
+    for (const InterVisEntry& e : matrix.entries()) {   // build_chain_filter, src/raytracer.cpp:319-340
+        const auto& c = e.relation.chain;
+        if (static_cast<int>(c.size()) > max_refl || c.size() < 2) continue;
+        if (c.size() == 2) {
+            const int r = scene.face(c[0]).index, a = scene.face(c[1]).index;
+            bits[static_cast<size_t>(r) * words + a / 64] |= 1ull << (a % 64);
+        } else if (c.size() == 3) {
+            for (const auto& id : c) tri.push_back(scene.face(id).index);
+        }
+    }
+    check(visrt_tracer_create(scene.device_scene(), max_refl, bits.data(), static_cast<int64_t>(tri.size() / 3),
+                              tri.empty() ? nullptr : tri.data(), &tracer_));
+}
+
+TraceAccelerator::~TraceAccelerator() {
+    if (tracer_) visrt_tracer_destroy(tracer_);
+}
+
+std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<Vec3>& tx, const std::vector<Vec3>& rx,
+                                                             std::vector<TraceStats>* stats) const {
+    std::vector<double> t, r;
+    for (const Vec3& p : tx) {
+        t.push_back(p.x);
+        t.push_back(p.y);
+        t.push_back(p.z);
+    }
+    for (const Vec3& p : rx) {
+        r.push_back(p.x);
+        r.push_back(p.y);
+        r.push_back(p.z);
+    }
+    visrt_trace_stats st{};
+    check(visrt_trace(tracer_, static_cast<int64_t>(tx.size()), t.data(), r.data(), rx.size() == 1 ? 1 : 0, &st,
+                      nullptr));
+    const int64_t np = visrt_trace_results(tracer_, nullptr, nullptr, 0, nullptr);
+    std::vector<int64_t> off(tx.size() + 1), nodes(tx.size());
+    std::vector<visrt_path> ps(static_cast<size_t>(np) + 1);
+    visrt_trace_results(tracer_, off.data(), ps.data(), np, nodes.data());
+    std::vector<std::vector<Path>> out(tx.size());
+    for (size_t k = 0; k < tx.size(); ++k) {
+        for (int64_t q = off[k]; q < off[k + 1]; ++q) {
+            const visrt_path& vp = ps[static_cast<size_t>(q)];
+            Path p;
+            p.source = tx[k];
+            p.receiver = rx.size() == 1 ? rx[0] : rx[k];
+            for (int i = 0; i < vp.nrefl + 2; ++i) p.points.push_back({vp.points[3 * i], vp.points[3 * i + 1], vp.points[3 * i + 2]});
+            for (int i = 0; i < vp.nrefl; ++i)
+                p.interactions.push_back({InteractionKind::Reflection, scene_->face(vp.faces[i]).id, p.points[1 + i]});
+            p.length = vp.length;
+            p.delay = vp.length / kSpeedOfLight;
+            out[k].push_back(std::move(p));
+        }
+        std::sort(out[k].begin(), out[k].end(), [](const Path& a, const Path& b) { return a.identity() < b.identity(); });
+        if (stats) {
+            TraceStats ts;
+            ts.nodes_expanded = nodes[k];
+            ts.sequences_checked = nodes[k] + 1;
+            ts.paths_found = static_cast<long long>(out[k].size());
+            stats->push_back(ts);
+        }
+    }
+    return out;
+}
+
+std::vector<Path> TraceAccelerator::trace(const Vec3& tx, const Vec3& rx, bool allow_diffraction,
+                                          TraceStats* stats) const {
+    if (allow_diffraction && !scene_->edges().empty())
+        throw std::invalid_argument("TraceAccelerator: the diffraction branch is not part of this build");
+    std::vector<TraceStats> st;
+    auto out = trace_batch({tx}, {rx}, stats ? &st : nullptr);
+    if (stats) *stats = st[0];
+    return std::move(out[0]);
+}
+
+}  // namespace rt

@@ -1,0 +1,251 @@
+// visrt-b200 C++ drop-in layer: the hot-path subset of the reference's public
+// C++ API (namespace rt, /root/reference/proj/include/rt/*.hpp) re-created on
+// top of the C-ABI (include/visrt.h). Same names, argument meaning and
+// exception types/messages for:
+//   Scene / Face / Building / plane_segment          include/rt/scene.hpp:38-106
+//   occlusion_judgment, build_matrix, InterVisMatrix include/rt/vismatrix.hpp:37-141
+//   illuminated_region                                include/rt/vistable.hpp:116-117
+//   TraceAccelerator / Path / TraceStats              include/rt/raytracer.hpp:25-118
+// Geometry is decided on the GPU (sm_100a kernels); the host materialises the
+// string-keyed records (ids, angle records with atan2, aim images) exactly as
+// the reference does. There is no CPU fallback for any hot-path decision.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+struct visrt_scene;
+struct visrt_tracer;
+
+namespace rt {
+
+inline constexpr double kEps = 1e-9;
+inline constexpr double kSpeedOfLight = 299792458.0;
+
+struct Vec3 {
+    double x = 0.0, y = 0.0, z = 0.0;
+    Vec3 operator+(const Vec3& o) const { return {x + o.x, y + o.y, z + o.z}; }
+    Vec3 operator-(const Vec3& o) const { return {x - o.x, y - o.y, z - o.z}; }
+    Vec3 operator*(double s) const { return {x * s, y * s, z * s}; }
+};
+struct Vec2 {
+    double x = 0.0, y = 0.0;
+};
+enum class PlaneTag { XY, YZ, XZ };
+enum class Orientation { Horizontal, Vertical, Oblique };
+
+class SceneError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+class VisibilityError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+class PlacementError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+struct ConvexPolygon {
+    std::vector<Vec3> pts;
+    Vec3 normal;
+    static ConvexPolygon from_points(std::vector<Vec3> pts);  // Newell normal
+};
+
+struct FaceLabels {
+    std::string xy, vert;
+};
+
+struct Face {
+    std::string id;
+    std::string building;
+    std::string material;
+    ConvexPolygon poly;
+    Orientation orientation = Orientation::Vertical;
+    FaceLabels labels;
+    int index = -1;
+    const std::string& label(PlaneTag p) const {
+        if (p == PlaneTag::XY) return labels.xy.empty() ? id : labels.xy;
+        return labels.vert.empty() ? id : labels.vert;
+    }
+};
+
+struct Edge {
+    std::string id;
+    Vec3 a, b;
+    std::array<std::string, 2> faces;
+    std::string building;
+};
+
+struct Building {
+    std::string id;
+    std::vector<Face> faces;
+};
+
+struct PlaneSegment {
+    Vec2 a, b, normal;
+};
+
+class Scene {
+  public:
+    std::vector<Building> buildings;
+    std::optional<Face> ground;
+
+    Scene() = default;
+    Scene(const Scene&) = delete;             // faces() holds pointers into the scene
+    Scene& operator=(const Scene&) = delete;
+    ~Scene();
+
+    /// Closed-shell scenes (reference semantics: indices, orientations, edges).
+    void finalize();
+    /// Facet soup (open boxes on tiled ground): no buildings, no edges.
+    static std::unique_ptr<Scene> from_facets(const std::vector<std::string>& ids,
+                                              const std::vector<std::vector<Vec3>>& rings);
+
+    const std::vector<const Face*>& faces() const { return face_ptrs_; }
+    const Face& face(int index) const { return *face_ptrs_.at(static_cast<size_t>(index)); }
+    const Face& face(const std::string& id) const;
+    const std::vector<Edge>& edges() const { return edges_; }
+    bool inside_building(const Vec3& p) const;
+
+    /// The device-resident copy (created on first use on CUDA device 0).
+    visrt_scene* device_scene() const;
+
+  private:
+    std::vector<const Face*> face_ptrs_;
+    std::vector<Face> soup_;
+    std::map<std::string, int> face_index_;
+    std::vector<Edge> edges_;
+    mutable visrt_scene* dev_ = nullptr;
+};
+
+std::optional<PlaneSegment> plane_segment(const Face& face, PlaneTag plane);
+
+// ---------------------------------------------------------------------------
+enum class RelationKind { Parallel, Perpendicular };
+enum class ChainVerdict { Full, Partial, None };
+
+struct InterfaceRelation {
+    RelationKind kind = RelationKind::Parallel;
+    PlaneTag plane = PlaneTag::XY;
+    std::vector<std::string> chain;
+    std::vector<Orientation> chain_orientations;
+};
+struct AngleRecord {
+    std::string edge_id;
+    Vec2 vertex, ref_dir, outward;
+    double low = 0.0, high = 0.0;
+};
+struct AngularBouncingRange {
+    AngleRecord at_a, at_b;
+};
+struct OcclusionVerdict {
+    enum class Kind { Visible, PartiallyVisible, Occluded };
+    Kind kind = Kind::Visible;
+    std::vector<std::string> blockers;
+};
+struct InterVisEntry {
+    int order = 1;
+    std::string ref, aim;
+    InterfaceRelation relation;
+    AngularBouncingRange ranges;
+    std::optional<AngularBouncingRange> criterion;
+    ChainVerdict verdict = ChainVerdict::Full;
+    std::vector<std::array<double, 2>> subranges;
+    std::vector<std::string> blockers;
+    std::vector<Vec3> aim_image;
+};
+
+class InterVisMatrix {
+  public:
+    int max_order() const { return max_order_; }
+    const std::vector<InterVisEntry>& entries() const { return entries_; }
+    std::vector<const InterVisEntry*> find(int order, const std::string& ref, const std::string& aim) const;
+    const InterVisEntry* find(int order, const std::string& ref, const std::string& aim, PlaneTag plane) const;
+    bool pair_admitted(const std::string& ref, const std::string& aim) const;
+    std::vector<std::string> aims_of(const std::string& ref) const;
+    void add(InterVisEntry entry);
+    void set_max_order(int order) { max_order_ = order; }
+
+  private:
+    int max_order_ = 1;
+    std::vector<InterVisEntry> entries_;
+    std::map<std::tuple<int, std::string, std::string>, std::vector<size_t>> index_;
+};
+
+OcclusionVerdict occlusion_judgment(const Face& ref, const Face& aim, const Scene& scene);
+InterVisMatrix build_matrix(const Scene& scene, int max_order);
+
+// ---------------------------------------------------------------------------
+struct PlaneIllumination {
+    PlaneTag plane = PlaneTag::XY;
+    Vec2 image, face_a, face_b, outward;
+    double alpha_full = 0.0, beta_full = 0.0;
+    std::array<double, 2> sub{0.0, 1.0};
+    Vec2 sub_a, sub_b;
+    double alpha = 0.0, beta = 0.0;
+    bool clipped = false;
+    std::vector<Vec2> clip_points;
+};
+struct IlluminatedRegion {
+    std::string face;
+    Vec3 source;
+    std::vector<PlaneIllumination> planes;
+    const PlaneIllumination* plane(PlaneTag tag) const {
+        for (const auto& p : planes)
+            if (p.plane == tag) return &p;
+        return nullptr;
+    }
+};
+std::optional<IlluminatedRegion> illuminated_region(const Vec3& source, const Face& face, const Scene& scene);
+/// Batched form (one GPU call for every (source, face)): regions[k][f].
+std::vector<std::vector<std::optional<IlluminatedRegion>>> illuminated_regions(const std::vector<Vec3>& sources,
+                                                                               const Scene& scene);
+
+// ---------------------------------------------------------------------------
+enum class InteractionKind { Reflection, Diffraction };
+struct Interaction {
+    InteractionKind kind = InteractionKind::Reflection;
+    std::string id;
+    Vec3 point;
+};
+struct Path {
+    std::vector<Interaction> interactions;
+    Vec3 source, receiver;
+    std::vector<Vec3> points;
+    double length = 0.0, delay = 0.0;
+    std::string identity() const;
+};
+struct TraceStats {
+    long long nodes_expanded = 0, sequences_checked = 0, occlusion_tests = 0, paths_found = 0;
+};
+
+class TraceAccelerator {
+  public:
+    TraceAccelerator(const Scene& scene, const InterVisMatrix& matrix, int max_refl);
+    ~TraceAccelerator();
+    TraceAccelerator(const TraceAccelerator&) = delete;
+    TraceAccelerator& operator=(const TraceAccelerator&) = delete;
+    /// allow_diffraction must be false for scenes without edges (facet soups).
+    std::vector<Path> trace(const Vec3& tx, const Vec3& rx, bool allow_diffraction,
+                            TraceStats* stats = nullptr) const;
+    /// Batched form: one GPU expansion over every snapshot (rx.size() == 1: fixed receiver).
+    std::vector<std::vector<Path>> trace_batch(const std::vector<Vec3>& tx, const std::vector<Vec3>& rx,
+                                               std::vector<TraceStats>* stats = nullptr) const;
+    int max_reflections() const { return max_refl_; }
+
+  private:
+    const Scene* scene_;
+    int max_refl_;
+    visrt_tracer* tracer_ = nullptr;
+};
+
+}  // namespace rt

@@ -1,0 +1,214 @@
+// Drop-in parity: the visrt-b200 C++ layer (namespace rt, GPU underneath)
+// against the UNMODIFIED reference (visrt_ref::, through oracle/ref_capi.h) on
+// one scene file written by tests/test_cpp_dropin.py. Every compared field is
+// bit-exact (doubles compared with ==). Exit code = number of mismatches.
+//
+// Scene file:  nfaces nbuildings / building ids / per face: id b nv x y z ... /
+//              nsrc / sources / ntrace / tx ty tz rx ry rz / max_order
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../oracle/ref_capi.h"
+#include "../../paper_2501_02747_b200/cpp/rt.hpp"
+
+static int g_bad = 0;
+#define EXPECT(cond, what)                                                     \
+    do {                                                                       \
+        if (!(cond)) {                                                         \
+            if (g_bad < 20) std::cerr << "MISMATCH " << what << std::endl;     \
+            ++g_bad;                                                           \
+        }                                                                      \
+    } while (0)
+
+int main(int argc, char** argv) {
+    if (argc < 2) return 2;
+    std::ifstream in(argv[1]);
+    int n = 0, nb = 0;
+    in >> n >> nb;
+    std::vector<std::string> bids(nb), ids(n);
+    std::vector<int> bidx(n);
+    std::vector<std::vector<rt::Vec3>> rings(n);
+    for (auto& b : bids) in >> b;
+    std::vector<int32_t> off{0};
+    std::vector<double> verts;
+    for (int i = 0; i < n; ++i) {
+        int nv = 0;
+        in >> ids[i] >> bidx[i] >> nv;
+        for (int k = 0; k < nv; ++k) {
+            rt::Vec3 p;
+            in >> std::hexfloat >> p.x >> p.y >> p.z;
+            rings[i].push_back(p);
+            verts.insert(verts.end(), {p.x, p.y, p.z});
+        }
+        off.push_back(off.back() + nv);
+    }
+    int nsrc = 0;
+    in >> nsrc;
+    std::vector<rt::Vec3> src(nsrc);
+    for (auto& s : src) in >> std::hexfloat >> s.x >> s.y >> s.z;
+    int ntr = 0;
+    in >> ntr;
+    std::vector<std::pair<rt::Vec3, rt::Vec3>> tr(ntr);
+    for (auto& t : tr) in >> std::hexfloat >> t.first.x >> t.first.y >> t.first.z >> t.second.x >> t.second.y >> t.second.z;
+    int max_order = 2;
+    in >> max_order;
+
+    // --- both scenes -----------------------------------------------------
+    std::string idcat, bcat;
+    for (auto& s : ids) idcat += s + '\0';
+    for (auto& s : bids) bcat += s + '\0';
+    std::unique_ptr<rt::Scene> owned;
+    rt::Scene* mine = nullptr;
+    void* ref = nullptr;
+    if (nb > 0) {
+        owned = std::make_unique<rt::Scene>();
+        owned->buildings.resize(nb);
+        for (int b = 0; b < nb; ++b) owned->buildings[b].id = bids[b];
+        for (int i = 0; i < n; ++i) {
+            rt::Face f;
+            f.id = ids[i];
+            f.poly = rt::ConvexPolygon::from_points(rings[i]);
+            if (bidx[i] >= 0) owned->buildings[bidx[i]].faces.push_back(std::move(f));
+            else owned->ground = std::move(f);
+        }
+        owned->finalize();
+        ref = vref_scene_from_shells(n, off.data(), verts.data(), idcat.c_str(), bidx.data(), nb, bcat.c_str());
+    } else {
+        owned = rt::Scene::from_facets(ids, rings);
+        ref = vref_scene_from_soup(n, off.data(), verts.data(), idcat.c_str());
+    }
+    mine = owned.get();
+    if (!ref) {
+        std::cerr << "reference scene: " << vref_last_error() << std::endl;
+        return 99;
+    }
+    EXPECT(static_cast<int>(mine->faces().size()) == vref_nfaces(ref), "face count");
+    auto id_of = [&](int i) { return mine->face(i).id; };
+
+    // --- build_matrix ----------------------------------------------------
+    const rt::InterVisMatrix M = rt::build_matrix(*mine, max_order);
+    void* RM = vref_build_matrix(ref, max_order);
+    const int64_t ne = vref_matrix_size(RM);
+    EXPECT(static_cast<int64_t>(M.entries().size()) == ne, "entry count " << M.entries().size() << " vs " << ne);
+    for (int64_t k = 0; k < ne && k < static_cast<int64_t>(M.entries().size()); ++k) {
+        vref_entry r;
+        vref_matrix_entry(ref, RM, k, &r);
+        const rt::InterVisEntry& e = M.entries()[static_cast<size_t>(k)];
+        std::ostringstream w;
+        w << "entry " << k;
+        EXPECT(e.order == r.order, w.str() << " order");
+        EXPECT(static_cast<int>(e.relation.chain.size()) == r.chain_len, w.str() << " chain len");
+        for (int c = 0; c < r.chain_len && c < static_cast<int>(e.relation.chain.size()); ++c)
+            EXPECT(e.relation.chain[c] == id_of(r.chain[c]), w.str() << " chain");
+        EXPECT(static_cast<int>(e.relation.plane) == r.plane, w.str() << " plane");
+        EXPECT(static_cast<int>(e.relation.kind) == r.kind, w.str() << " kind");
+        EXPECT(static_cast<int>(e.verdict) == r.verdict, w.str() << " verdict");
+        const rt::AngleRecord* recs[2] = {&e.ranges.at_a, &e.ranges.at_b};
+        for (int q = 0; q < 2; ++q) {
+            const double* d = r.ranges + 6 * q;
+            EXPECT(recs[q]->vertex.x == d[0] && recs[q]->vertex.y == d[1], w.str() << " vertex");
+            EXPECT(recs[q]->low == d[2] && recs[q]->high == d[3], w.str() << " angles");
+            EXPECT(recs[q]->ref_dir.x == d[4] && recs[q]->ref_dir.y == d[5], w.str() << " ref_dir");
+        }
+        EXPECT(e.ranges.at_a.edge_id == r.edge_a && e.ranges.at_b.edge_id == r.edge_b, w.str() << " edge ids");
+        EXPECT(e.criterion.has_value() == (r.has_criterion != 0), w.str() << " criterion presence");
+        if (e.criterion && r.has_criterion)
+            EXPECT(e.criterion->at_a.low == r.criterion[0] && e.criterion->at_a.high == r.criterion[1] &&
+                       e.criterion->at_b.low == r.criterion[2] && e.criterion->at_b.high == r.criterion[3],
+                   w.str() << " criterion");
+        EXPECT(static_cast<int>(e.subranges.size()) == r.nsub, w.str() << " subranges");
+        for (int q = 0; q < r.nsub && q < static_cast<int>(e.subranges.size()); ++q)
+            EXPECT(e.subranges[q][0] == r.sub[2 * q] && e.subranges[q][1] == r.sub[2 * q + 1], w.str() << " sub");
+        EXPECT(static_cast<int>(e.blockers.size()) == r.nblockers, w.str() << " blocker count");
+        for (int q = 0; q < r.nblockers && q < static_cast<int>(e.blockers.size()); ++q)
+            EXPECT(e.blockers[q] == id_of(r.blockers[q]), w.str() << " blocker");
+        EXPECT(static_cast<int>(e.aim_image.size()) == r.naim_image, w.str() << " aim image size");
+        for (int q = 0; q < r.naim_image && q < static_cast<int>(e.aim_image.size()); ++q)
+            EXPECT(e.aim_image[q].x == r.aim_image[3 * q] && e.aim_image[q].y == r.aim_image[3 * q + 1] &&
+                       e.aim_image[q].z == r.aim_image[3 * q + 2],
+                   w.str() << " aim image");
+    }
+    std::cout << "build_matrix(" << max_order << "): " << ne << " entries compared" << std::endl;
+
+    // --- occlusion_judgment (every 5th pair) -------------------------------
+    int npj = 0;
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; j += 5) {
+            const rt::OcclusionVerdict v = rt::occlusion_judgment(mine->face(i), mine->face(j), *mine);
+            int32_t blk[4096];
+            int32_t nblk = 0;
+            const int k = vref_occlusion(ref, i, j, blk, 4096, &nblk);
+            EXPECT(static_cast<int>(v.kind) == k, "verdict " << i << "," << j);
+            EXPECT(static_cast<int>(v.blockers.size()) == nblk, "blockers " << i << "," << j);
+            for (int q = 0; q < nblk && q < static_cast<int>(v.blockers.size()); ++q)
+                EXPECT(v.blockers[q] == id_of(blk[q]), "blocker id " << i << "," << j);
+            ++npj;
+        }
+    std::cout << "occlusion_judgment: " << npj << " pairs compared" << std::endl;
+
+    // --- illuminated_region (every field, angles included) ---------------
+    const auto regs = rt::illuminated_regions(src, *mine);
+    for (int s = 0; s < nsrc; ++s)
+        for (int f = 0; f < n; ++f) {
+            vref_region r;
+            const double sp[3] = {src[s].x, src[s].y, src[s].z};
+            vref_illuminated_region(ref, sp, f, &r);
+            const auto& g = regs[s][f];
+            EXPECT(g.has_value() == (r.present == 1), "region presence " << s << "," << f);
+            if (!g || r.present != 1) continue;
+            EXPECT(static_cast<int>(g->planes.size()) == r.nplanes, "region planes " << s << "," << f);
+            for (int p = 0; p < r.nplanes && p < static_cast<int>(g->planes.size()); ++p) {
+                const rt::PlaneIllumination& pi = g->planes[p];
+                EXPECT(static_cast<int>(pi.plane) == r.plane[p], "plane tag");
+                EXPECT(pi.sub[0] == r.sub[2 * p] && pi.sub[1] == r.sub[2 * p + 1], "sub " << s << "," << f);
+                EXPECT(pi.clipped == (r.clipped[p] != 0), "clipped");
+                EXPECT(pi.image.x == r.image[2 * p] && pi.image.y == r.image[2 * p + 1], "image");
+                EXPECT(pi.sub_a.x == r.sub_ab[4 * p] && pi.sub_a.y == r.sub_ab[4 * p + 1] &&
+                           pi.sub_b.x == r.sub_ab[4 * p + 2] && pi.sub_b.y == r.sub_ab[4 * p + 3],
+                       "sub_a/sub_b");
+                EXPECT(pi.alpha_full == r.angles[4 * p] && pi.beta_full == r.angles[4 * p + 1] &&
+                           pi.alpha == r.angles[4 * p + 2] && pi.beta == r.angles[4 * p + 3],
+                       "boundary angles " << s << "," << f);
+            }
+        }
+    std::cout << "illuminated_region: " << nsrc << " sources x " << n << " faces compared" << std::endl;
+
+    // --- TraceAccelerator up to max_order (+1 via set_max_order) ----------
+    rt::InterVisMatrix M2 = M;
+    M2.set_max_order(max_order + 1 <= 3 ? max_order + 1 : max_order);
+    vref_matrix_set_max_order(RM, M2.max_order());
+    for (int order = 1; order <= M2.max_order(); ++order) {
+        rt::TraceAccelerator acc(*mine, M2, order);
+        void* RA = vref_accel_create(ref, RM, order);
+        for (int t = 0; t < ntr; ++t) {
+            rt::TraceStats st;
+            const auto paths = acc.trace(tr[t].first, tr[t].second, false, &st);
+            std::vector<vref_path> rp(16384);
+            int64_t rst[4];
+            const double tx[3] = {tr[t].first.x, tr[t].first.y, tr[t].first.z};
+            const double rx[3] = {tr[t].second.x, tr[t].second.y, tr[t].second.z};
+            const int64_t np = vref_accel_trace(ref, RA, tx, rx, 0, rp.data(), 16384, rst);
+            EXPECT(static_cast<int64_t>(paths.size()) == np, "path count order " << order << " trace " << t);
+            EXPECT(st.nodes_expanded == rst[0] && st.sequences_checked == rst[1], "trace stats " << order << "," << t);
+            for (int64_t q = 0; q < np && q < static_cast<int64_t>(paths.size()); ++q) {
+                const rt::Path& p = paths[static_cast<size_t>(q)];
+                EXPECT(p.identity() == rp[q].identity, "identity " << p.identity() << " vs " << rp[q].identity);
+                EXPECT(p.length == rp[q].length && p.delay == rp[q].delay, "length/delay");
+                for (size_t v = 0; v < p.points.size(); ++v)
+                    EXPECT(p.points[v].x == rp[q].points[3 * v] && p.points[v].y == rp[q].points[3 * v + 1] &&
+                               p.points[v].z == rp[q].points[3 * v + 2],
+                           "path point");
+            }
+        }
+        vref_accel_free(RA);
+    }
+    std::cout << "TraceAccelerator: orders 1.." << M2.max_order() << " x " << ntr << " traces compared" << std::endl;
+    vref_matrix_free(RM);
+    vref_scene_free(ref);
+    std::cout << (g_bad ? "FAIL " : "OK ") << g_bad << " mismatches" << std::endl;
+    return g_bad > 255 ? 255 : g_bad;
+}
