@@ -61,6 +61,8 @@ typedef struct {
     double  tests_alg;         /* sum S(i,j)*(N-2) over evaluated pairs (reference work) */
     int64_t tests_exec;        /* segment-vs-facet tests the kernel executed         */
     float   ms;                /* device time of the call (CUDA events)              */
+    int64_t sweeps;            /* culled occluder sweeps started (one per sightline)  */
+    int64_t tiles;             /* 64-occluder tiles culled by lanes (SAT work / 64)   */
 } visrt_stats;
 
 const char* visrt_last_error(void);

@@ -42,7 +42,8 @@ class visrt_facets_v1(C.Structure):
 
 class visrt_stats(C.Structure):
     _fields_ = [("pairs", C.c_int64), ("candidates", C.c_int64), ("admitted", C.c_int64),
-                ("tests_alg", C.c_double), ("tests_exec", C.c_int64), ("ms", C.c_float)]
+                ("tests_alg", C.c_double), ("tests_exec", C.c_int64), ("ms", C.c_float),
+                ("sweeps", C.c_int64), ("tiles", C.c_int64)]
 
 
 class visrt_region(C.Structure):

@@ -23,7 +23,8 @@ KIND_NAMES = ("Visible", "PartiallyVisible", "Occluded")
 
 def _stats_dict(st: _capi.visrt_stats) -> Dict[str, float]:
     return {"pairs": st.pairs, "candidates": st.candidates, "admitted": st.admitted,
-            "tests_alg": st.tests_alg, "tests_exec": st.tests_exec, "ms": st.ms}
+            "tests_alg": st.tests_alg, "tests_exec": st.tests_exec, "ms": st.ms,
+            "sweeps": st.sweeps, "tiles": st.tiles}
 
 
 class Scene:

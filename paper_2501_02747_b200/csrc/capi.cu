@@ -262,7 +262,7 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
         }
         if (a.npairs > 0) ck(visrt::launch_pair_bits(a, sc->device, st), "k_pair_bits");
         ck(cudaEventRecord(sc->ev1, st), "event");
-        unsigned long long counters[2] = {0, 0};
+        unsigned long long counters[4] = {0, 0, 0, 0};
         ck(cudaMemcpyAsync(counters, sc->d_counter, sizeof(counters), cudaMemcpyDeviceToHost, st), "D2H ctr");
         if (pref) {
             sc->ncand = ncand;
@@ -315,6 +315,8 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
             stats->pairs = npairs;
             stats->candidates = ncand;
             stats->tests_exec = static_cast<int64_t>(counters[1]);
+            stats->sweeps = static_cast<int64_t>(counters[2]);
+            stats->tiles = static_cast<int64_t>(counters[3]);
             stats->ms = ms;
             if (pref) {
                 double t = 0.0;

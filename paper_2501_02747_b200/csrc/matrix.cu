@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     int bc0 = -1, bc1 = -1;   // blocker cache: last occluders that blocked a sightline
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
     SegF g{};
-    unsigned long long tests = 0;
+    unsigned long long tests = 0, sweeps = 0, tiles = 0;
 
     auto finish = [&](bool occluded) {
         if (!occluded) set_pair_bit(a.bits, s.words, pi, pj);
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
             }
             g = make_segf(s, ax, ay, az, bx, by, bz);
             rem = nvt;
+            ++sweeps;
             return;
         }
     };
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     };
     auto vtile = [&](const float* B, int base, int cnt) {
         if (!active) return;
+        ++tiles;
         unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
         int hk = -1;
         while (mask) {
@@ -185,8 +187,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
 
     refill();
     sweep_loop<RESIDENT>(bs, vtile, busy, refill);
-    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
-    if (lane == 0) atomicAdd(&a.counter[1], tests);
+    for (int o = 16; o > 0; o >>= 1) {
+        tests += __shfl_down_sync(kFull, tests, o);
+        sweeps += __shfl_down_sync(kFull, sweeps, o);
+        tiles += __shfl_down_sync(kFull, tiles, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&a.counter[1], tests);
+        atomicAdd(&a.counter[2], sweeps);
+        atomicAdd(&a.counter[3], tiles);
+    }
 }
 
 // Detail sweep: per pair every sightline against every occluder (no early

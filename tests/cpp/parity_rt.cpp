@@ -6,6 +6,7 @@
 // Scene file:  nfaces nbuildings / building ids / per face: id b nv x y z ... /
 //              nsrc / sources / ntrace / tx ty tz rx ry rz / max_order
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <iostream>
 #include <sstream>
@@ -24,6 +25,13 @@ static int g_bad = 0;
         }                                                                      \
     } while (0)
 
+// hex-float token (libstdc++ streams do not parse hexfloat input)
+static double rd(std::istream& in) {
+    std::string tok;
+    in >> tok;
+    return std::strtod(tok.c_str(), nullptr);
+}
+
 int main(int argc, char** argv) {
     if (argc < 2) return 2;
     std::ifstream in(argv[1]);
@@ -40,7 +48,9 @@ int main(int argc, char** argv) {
         in >> ids[i] >> bidx[i] >> nv;
         for (int k = 0; k < nv; ++k) {
             rt::Vec3 p;
-            in >> std::hexfloat >> p.x >> p.y >> p.z;
+            p.x = rd(in);
+            p.y = rd(in);
+            p.z = rd(in);
             rings[i].push_back(p);
             verts.insert(verts.end(), {p.x, p.y, p.z});
         }
@@ -49,11 +59,22 @@ int main(int argc, char** argv) {
     int nsrc = 0;
     in >> nsrc;
     std::vector<rt::Vec3> src(nsrc);
-    for (auto& s : src) in >> std::hexfloat >> s.x >> s.y >> s.z;
+    for (auto& s : src) {
+        s.x = rd(in);
+        s.y = rd(in);
+        s.z = rd(in);
+    }
     int ntr = 0;
     in >> ntr;
     std::vector<std::pair<rt::Vec3, rt::Vec3>> tr(ntr);
-    for (auto& t : tr) in >> std::hexfloat >> t.first.x >> t.first.y >> t.first.z >> t.second.x >> t.second.y >> t.second.z;
+    for (auto& t : tr) {
+        t.first.x = rd(in);
+        t.first.y = rd(in);
+        t.first.z = rd(in);
+        t.second.x = rd(in);
+        t.second.y = rd(in);
+        t.second.z = rd(in);
+    }
     int max_order = 2;
     in >> max_order;
 

@@ -15,4 +15,4 @@ for cfg in [int(a) for a in sys.argv[1:]] or [1, 2]:
                 t1 = time.perf_counter()
             print(f"cfg{cfg} N={soup.nfaces} {mode}: kernel {st['ms']:.3f} ms wall {1e3*(t1-t0):.2f} ms "
                   f"cand {st['candidates']} tests_alg {st['tests_alg']:.3e} exec {st['tests_exec']:.3e} "
-                  f"alg/s {st['tests_alg']/st['ms']*1e3:.3e}", flush=True)
+                  f"alg/s {st['tests_alg']/st['ms']*1e3:.3e} sweeps {st['sweeps']:.3e} tiles {st['tiles']:.3e}", flush=True)
