@@ -26,6 +26,13 @@ struct DevScene {
     const int32_t* seg_ok = nullptr;
     const float* box = nullptr;    // [n][8] fp32 culling boxes (centre rel. origin, dilated half)
     double ox = 0, oy = 0, oz = 0; // box origin
+    // two-level culling hierarchy (Morton order, sweep.h)
+    const float* sbox = nullptr;   // [n][8] member boxes, Morton order
+    const float* tbox = nullptr;   // [ntiles][8] tile union boxes
+    const double* srec = nullptr;  // occluder records, Morton order
+    const int32_t* perm = nullptr; // Morton position -> face index
+    const int32_t* inv = nullptr;  // face index -> Morton position
+    int32_t ntiles = 0, nchunks = 0;
 };
 
 // A sightline in the fp32 culling frame: midpoint (relative to the scene

@@ -256,6 +256,73 @@ void ingest(const visrt_facets_v1& f, HostScene& hs) {
         write_record<8>(pts, hs.nv[i], {hs.normal[3 * i], hs.normal[3 * i + 1], hs.normal[3 * i + 2]},
                         &hs.rec8[static_cast<size_t>(i) * RecLayout<8>::kStride]);
     }
+    build_hierarchy(hs);
+}
+
+// Two-level culling hierarchy (sweep.h): Morton order of the xy AABB centres
+// (16 bits per axis over the scene extent, ties by face index), tiles of 64
+// consecutive faces, tile box = union of the member boxes rounded outward.
+// Only the ORDER in which occluders are examined changes; every verdict is
+// still the exact predicate's.
+void build_hierarchy(HostScene& hs) {
+    const int n = hs.n;
+    const double ext = std::max(hs.extent, 1.0);
+    auto spread = [](uint32_t v) {
+        uint64_t x = v & 0xffffu;
+        x = (x | (x << 8)) & 0x00ff00ffu;
+        x = (x | (x << 4)) & 0x0f0f0f0fu;
+        x = (x | (x << 2)) & 0x33333333u;
+        x = (x | (x << 1)) & 0x55555555u;
+        return x;
+    };
+    std::vector<std::pair<uint64_t, int32_t>> key(n);
+    for (int i = 0; i < n; ++i) {
+        const double* bb = &hs.aabb[static_cast<size_t>(i) * 6];
+        const double cx = 0.5 * (bb[0] + bb[3]) - hs.origin[0];
+        const double cy = 0.5 * (bb[1] + bb[4]) - hs.origin[1];
+        const auto q = [&](double c) {
+            const double u = (c + ext) / (2.0 * ext);
+            return static_cast<uint32_t>(std::min(65535.0, std::max(0.0, u * 65535.0)));
+        };
+        key[i] = {spread(q(cx)) | (spread(q(cy)) << 1), i};
+    }
+    std::sort(key.begin(), key.end());
+    hs.perm.resize(n);
+    hs.inv.resize(n);
+    for (int k = 0; k < n; ++k) {
+        hs.perm[k] = key[k].second;
+        hs.inv[key[k].second] = k;
+    }
+    const bool narrow = hs.maxv <= 4;
+    const int stride = narrow ? RecLayout<4>::kStride : RecLayout<8>::kStride;
+    const std::vector<double>& rec = narrow ? hs.rec4 : hs.rec8;
+    hs.srec.resize(static_cast<size_t>(n) * stride);
+    hs.sbox.resize(static_cast<size_t>(n) * 8);
+    for (int k = 0; k < n; ++k) {
+        const int f = hs.perm[k];
+        std::copy_n(&rec[static_cast<size_t>(f) * stride], stride, &hs.srec[static_cast<size_t>(k) * stride]);
+        std::copy_n(&hs.box[static_cast<size_t>(f) * 8], 8, &hs.sbox[static_cast<size_t>(k) * 8]);
+    }
+    hs.ntiles = (n + 63) / 64;
+    hs.nchunks = (hs.ntiles + 63) / 64;
+    hs.tbox.assign(static_cast<size_t>(hs.ntiles) * 8, 0.0f);
+    for (int t = 0; t < hs.ntiles; ++t) {
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (int k = t * 64; k < std::min(n, t * 64 + 64); ++k) {
+            const float* b = &hs.sbox[static_cast<size_t>(k) * 8];
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = std::min(lo[d], static_cast<double>(b[d]) - static_cast<double>(b[4 + d]));
+                hi[d] = std::max(hi[d], static_cast<double>(b[d]) + static_cast<double>(b[4 + d]));
+            }
+        }
+        float* o = &hs.tbox[static_cast<size_t>(t) * 8];
+        for (int d = 0; d < 3; ++d) {
+            // a member box lies inside [lo, hi]; the fp32 centre/half of the
+            // union are padded by a few ulps of the extent so it still does
+            o[d] = static_cast<float>(0.5 * (lo[d] + hi[d]));
+            o[4 + d] = static_cast<float>(0.5 * (hi[d] - lo[d]) + 1e-4 + 8.0 * ext * 1.1920928955078125e-7);
+        }
+    }
 }
 
 }  // namespace visrt

@@ -84,15 +84,12 @@ __device__ bool column_span(const DevScene& s, int f, int pl, double ax, double 
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float sbox[];
-    __shared__ __align__(8) uint64_t bar[2];
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const int nvt = (n + kTile - 1) / kTile;
-    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
-    bs.t0 = blockIdx.x % bs.ntiles;
-    sweep_init<RESIDENT>(bs);
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
 
     // ---- lane state --------------------------------------------------------
     bool active = false, exhausted = false, querying = false;
@@ -118,14 +115,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     double sub[6] = {0, 0, 0, 0, 0, 0};
     // sightline query
     double qx = 0, qy = 0, qz = 0;
-    SegF g{};
-    int rem = 0, bc0 = -1, bc1 = -1;
+    Sweep sw{};
+    int sf = 0, bc0 = -1, bc1 = -1;     // sf: Morton index of the target face; cache: Morton indices
     unsigned long long tests = 0, queries = 0;
+    (void)n;
 
     auto vis_at = [&](int i) { return i == 64 ? vis64 : ((vis >> i) & 1ull) != 0; };
     auto exact = [&](int k) {
         ++tests;
-        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz);
+        return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz);
     };
     auto write_out = [&](int8_t present) {
         visrt_region r;
@@ -153,15 +151,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
             else if (pl == 1) { qx = sv; qy = px; qz = py; }
             else { qx = px; qy = sv; qz = py; }
             ++queries;
-            if (bc0 >= 0 && bc0 != f && exact(bc0)) continue;
-            if (bc1 >= 0 && bc1 != f && exact(bc1)) {
+            if (bc0 >= 0 && bc0 != sf && exact(bc0)) continue;
+            if (bc1 >= 0 && bc1 != sf && exact(bc1)) {
                 const int t = bc0;
                 bc0 = bc1;
                 bc1 = t;
                 continue;
             }
-            g = make_segf(s, sx, sy, sz, qx, qy, qz);
-            rem = nvt;
+            sw.start(make_segf(s, sx, sy, sz, qx, qy, qz), sf, -1, home_chunk(s, f), ctx.nchunks);
             return true;
         }
         return false;
@@ -313,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
         tid = t;
         const long long k = t / n;
         f = static_cast<int>(t - k * n);
+        sf = s.inv[f];
         sx = a.src[3 * k];
         sy = a.src[3 * k + 1];
         sz = a.src[3 * k + 2];
@@ -359,9 +357,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
         }
     };
     // One virtual tile of the current sightline sweep.
-    auto vtile = [&](const float* B, int base, int cnt) {
+    // One 64-box culling batch of the current sightline sweep.
+    auto step = [&]() {
         if (!querying) return;
-        unsigned long long mask = tile_survivors(B, cnt, base, g, f, -1);
+        int base;
+        unsigned long long mask = sweep_batch(sw, ctx, base);
         int hk = -1;
         while (mask) {
             const int kk = __ffsll(static_cast<long long>(mask)) - 1;
@@ -381,15 +381,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
             if (next_sample()) return;
             querying = false;
             pump(true, false);
-        } else if (--rem == 0) {
+        } else if (sw.done()) {
             querying = false;
             pump(true, true);   // clear sightline: column visible
         }
     };
-    auto busy = [&]() { return active || !exhausted; };
 
     refill();
-    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
+    for (;;) {
+        step();
+        refill();
+        if (!__any_sync(kFull, active || !exhausted)) break;
+    }
     for (int o = 16; o > 0; o >>= 1) {
         tests += __shfl_down_sync(kFull, tests, o);
         queries += __shfl_down_sync(kFull, queries, o);
@@ -420,7 +423,7 @@ template <int MAXV>
 static cudaError_t launch_regions_t(const RegionArgs& a, int device, cudaStream_t st) {
     const char* e = std::getenv("VISRT_FORCE_STREAM");
     const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
-    const size_t smem = res ? ((static_cast<size_t>(a.s.n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
+    const size_t smem = sweep_smem_bytes(a.s.n, a.s.ntiles, res);
     return res ? launch_r(k_point_regions<MAXV, true>, smem, a, device, st)
                : launch_r(k_point_regions<MAXV, false>, smem, a, device, st);
 }

@@ -1,132 +1,139 @@
 // Culled any-hit occluder sweep shared by the matrix (K2), region (K4) and
-// tree (K6) kernels. See matrix.cu for the design notes.
+// tree (K6) kernels.
+//
+// Two-level culling hierarchy (built once per scene by the host ingest):
+//   * faces are Morton-ordered by the xy centre of their AABB and grouped in
+//     tiles of 64 consecutive faces; every tile has a union culling box;
+//   * level 1: 64 tile boxes per 64-bit candidate mask (a "chunk");
+//   * level 2: the 64 member boxes of each candidate tile -> survivor mask;
+//   * survivors run the exact FP64 predicate (device.h seg_hits) on records
+//     stored in the same Morton order.
+// Every lane runs its own sweep, but each warp iteration is ONE 64-box fp32
+// SAT batch for every active lane (level-1 chunk or level-2 tile, selected by
+// a per-lane pointer), so the hot loop stays converged; the short exact-test
+// tail is the only divergent part. Tile boxes always live in shared memory;
+// member boxes too when they fit (RESIDENT, N <= kResidentMaxBoxes), else they
+// are read through L1/L2. No block barrier after the one-time TMA staging.
 #pragma once
 
 #include "device.h"
 
 namespace visrt {
 
-constexpr int kTile = 64;       // occluders per virtual tile (one 64-bit survivor mask)
+constexpr int kTile = 64;       // faces per tile / tiles per chunk (64-bit masks)
 constexpr int kThreads = 256;   // 8 warps
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kResidentMaxBoxes = 6144;   // 192 KB of fp32 member boxes
 
-// ---------------------------------------------------------------------------
-// Occluder sweep. Every lane walks the occluders cyclically in "virtual
-// tiles" of kTile; per virtual tile it first runs the fp32 culling test on all
-// kTile boxes (uniform index -> shared-memory broadcast), collecting a
-// survivor mask, then runs the exact FP64 predicate on the survivors only
-// (records read through L1/L2). Two box sources:
-//   RESIDENT: all N culling boxes staged once in shared memory (one TMA bulk
-//             copy); warps then run free, with no block barriers;
-//   STREAM:   scenes too large for that stream kStreamTile-box tiles through
-//             a double-buffered TMA ring with one block barrier per tile.
-// ---------------------------------------------------------------------------
-constexpr int kStreamTile = 256;          // boxes per streamed tile (4 virtual tiles)
-constexpr int kResidentMaxBoxes = 6144;   // 192 KB of fp32 boxes
-
-struct BoxStream {
-    float* sbox;        // RESIDENT: [n][8]; STREAM: 2 x [kStreamTile][8]
-    uint64_t* bar;
-    const float* box;
-    int n, ntiles, t0;
-
-    __device__ int tile_of(int it) const { return (t0 + it) % ntiles; }
-    __device__ void issue(int it) const {
-        const int t = tile_of(it);
-        const int cnt = min(kStreamTile, n - t * kStreamTile);
-        const uint32_t bytes = static_cast<uint32_t>(cnt) * 32u;
-        mbar_expect_tx(&bar[it & 1], bytes);
-        bulk_g2s(sbox + (it & 1) * kStreamTile * 8, box + static_cast<size_t>(t) * kStreamTile * 8, bytes,
-                 &bar[it & 1]);
-    }
-    __device__ void wait(int it) const { mbar_wait(&bar[it & 1], (it >> 1) & 1); }
-    __device__ const float* tile(int it) const { return sbox + (it & 1) * kStreamTile * 8; }
-};
-
-template <bool RESIDENT>
-__device__ __forceinline__ void sweep_init(BoxStream& bs) {
-    if (threadIdx.x == 0) {
-        mbar_init(&bs.bar[0], 1);
-        mbar_init(&bs.bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (RESIDENT) {
-            // one bulk copy per 64 KB chunk (the size operand is 32-bit, chunks keep it small)
-            const uint32_t total = static_cast<uint32_t>(bs.n) * 32u;
-            mbar_expect_tx(&bs.bar[0], total);
-            for (uint32_t off = 0; off < total; off += 65536u) {
-                const uint32_t b = min(65536u, total - off);
-                bulk_g2s(reinterpret_cast<char*>(bs.sbox) + off, reinterpret_cast<const char*>(bs.box) + off, b,
-                         &bs.bar[0]);
-            }
-        } else {
-            bs.issue(0);
-            bs.issue(1);
-        }
-    }
-    if (RESIDENT) bs.wait(0);
-}
-
-// Survivor mask of one virtual tile (boxes B[0..cnt)), own faces excluded.
-__device__ __forceinline__ unsigned long long tile_survivors(const float* __restrict__ B, int cnt, int base,
-                                                            const SegF& g, int pi, int pj) {
+// 64-box SAT batch -> mask (bit kk: box kk may meet the segment).
+__device__ __forceinline__ unsigned long long sat64(const float* __restrict__ B, int cnt, const SegF& g) {
     unsigned long long mask = 0;
 #pragma unroll 4
     for (int kk = 0; kk < cnt; ++kk)
         if (sat_maybe(B + kk * 8, g)) mask |= 1ull << kk;
-    if (pi >= base && pi < base + cnt) mask &= ~(1ull << (pi - base));
-    if (pj >= base && pj < base + cnt) mask &= ~(1ull << (pj - base));
     return mask;
 }
 
-// Faces whose (exact) AABBs are more than 1e-6 m apart have no coincident
-// samples, hence no degenerate sightline (samples lie in the face AABB up to
-// ~1e-11 m of rounding).
-__device__ __forceinline__ bool may_touch(const DevScene& s, int i, int j) {
-    const double* A = s.aabb + 6 * static_cast<size_t>(i);
-    const double* B = s.aabb + 6 * static_cast<size_t>(j);
-    bool sep = false;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) sep |= (B[d] > A[3 + d] + 1e-6) | (A[d] > B[3 + d] + 1e-6);
-    return !sep;
+struct SweepCtx {
+    const float* tbox;   // [ntiles][8] (shared memory)
+    const float* mbox;   // [n][8] member boxes (shared or global)
+    int n, ntiles, nchunks;
+};
+
+// Per-lane state of one segment sweep.
+struct Sweep {
+    SegF g;
+    int skip0, skip1;           // Morton-order indices never tested (the pair's own faces)
+    int chunk, left;            // level-1 cursor (cyclic) and chunks still to scan
+    int cbase;                  // first tile of the current candidate mask
+    unsigned long long cand;    // candidate tiles of the current chunk
+
+    __device__ void start(const SegF& seg, int s0, int s1, int start_chunk, int nchunks) {
+        g = seg;
+        skip0 = s0;
+        skip1 = s1;
+        chunk = start_chunk;
+        left = nchunks;
+        cand = 0;
+        cbase = 0;
+    }
+    __device__ bool done() const { return cand == 0 && left == 0; }
+};
+
+// One 64-box batch of the lane's sweep. Returns the survivor mask of a
+// level-2 tile (faces base..base+63 in Morton order, own faces removed) or 0
+// after a level-1 chunk. `base` receives the tile's first face index.
+__device__ __forceinline__ unsigned long long sweep_batch(Sweep& sw, const SweepCtx& c, int& base) {
+    const float* ptr;
+    int cnt;
+    bool level1;
+    if (sw.cand == 0) {
+        level1 = true;
+        const int t0 = sw.chunk * kTile;
+        cnt = min(kTile, c.ntiles - t0);
+        ptr = c.tbox + static_cast<size_t>(t0) * 8;
+        base = t0;
+    } else {
+        level1 = false;
+        const int t = sw.cbase + __ffsll(static_cast<long long>(sw.cand)) - 1;
+        sw.cand &= sw.cand - 1;
+        base = t * kTile;
+        cnt = min(kTile, c.n - base);
+        ptr = c.mbox + static_cast<size_t>(base) * 8;
+    }
+    unsigned long long mask = sat64(ptr, cnt, sw.g);
+    if (level1) {
+        sw.cand = mask;
+        sw.cbase = base;
+        sw.chunk = sw.chunk + 1 == c.nchunks ? 0 : sw.chunk + 1;
+        --sw.left;
+        return 0;
+    }
+    if (sw.skip0 >= base && sw.skip0 < base + kTile) mask &= ~(1ull << (sw.skip0 - base));
+    if (sw.skip1 >= base && sw.skip1 < base + kTile) mask &= ~(1ull << (sw.skip1 - base));
+    return mask;
 }
 
-// Drives `vtile(boxes, base, cnt)` (one virtual tile for the whole warp) and
-// `refill()` until the warp (RESIDENT) or the block (STREAM) runs dry.
-template <bool RESIDENT, class VTile, class Busy, class Refill>
-__device__ __forceinline__ void sweep_loop(BoxStream& bs, VTile&& vtile, Busy&& busy, Refill&& refill) {
-    const int n = bs.n;
-    const int nvt = (n + kTile - 1) / kTile;
-    if (RESIDENT) {
-        const int warp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-        int vt = warp % nvt;
-        for (;;) {
-            const int base = vt * kTile;
-            vtile(bs.sbox + static_cast<size_t>(base) * 8, base, min(kTile, n - base));
-            refill();
-            if (!__any_sync(kFull, busy())) break;
-            if (++vt == nvt) vt = 0;
-        }
-    } else {
-        for (int it = 0;; ++it) {
-            bs.wait(it);
-            const int tb = bs.tile_of(it) * kStreamTile;
-            const int tcnt = min(kStreamTile, n - tb);
-            const float* T = bs.tile(it);
-            for (int v = 0; v < tcnt; v += kTile) {
-                vtile(T + v * 8, tb + v, min(kTile, tcnt - v));
-                refill();
-            }
-            const int alive = __syncthreads_or(busy());
-            if (!alive) {
-                bs.wait(it + 1);   // drain the in-flight tile before the CTA retires
-                break;
-            }
-            if (threadIdx.x == 0) bs.issue(it + 2);
-        }
+// Block setup: stage the tile boxes (and the member boxes when RESIDENT) in
+// shared memory with TMA bulk copies (cp.async.bulk, one mbarrier).
+template <bool RESIDENT>
+__device__ __forceinline__ SweepCtx sweep_setup(const DevScene& s, float* smem, uint64_t* bar) {
+    SweepCtx c;
+    c.n = s.n;
+    c.ntiles = s.ntiles;
+    c.nchunks = s.nchunks;
+    float* st = smem;
+    float* sm = smem + static_cast<size_t>(s.ntiles) * 8;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t tb = static_cast<uint32_t>(s.ntiles) * 32u;
+        const uint32_t mb = RESIDENT ? static_cast<uint32_t>(s.n) * 32u : 0u;
+        mbar_expect_tx(bar, tb + mb);
+        for (uint32_t off = 0; off < tb; off += 32768u)
+            bulk_g2s(reinterpret_cast<char*>(st) + off, reinterpret_cast<const char*>(s.tbox) + off,
+                     min(32768u, tb - off), bar);
+        for (uint32_t off = 0; off < mb; off += 32768u)
+            bulk_g2s(reinterpret_cast<char*>(sm) + off, reinterpret_cast<const char*>(s.sbox) + off,
+                     min(32768u, mb - off), bar);
+    }
+    mbar_wait(bar, 0);
+    c.tbox = st;
+    c.mbox = RESIDENT ? sm : s.sbox;
+    return c;
+}
+
+inline size_t sweep_smem_bytes(int n, int ntiles, bool resident) {
+    return (static_cast<size_t>(ntiles) + (resident ? static_cast<size_t>(n) : 0)) * 32 + 128;
+}
+
+// Morton chunk holding original face f (a sweep starting there meets the
+// face's own neighbourhood — the likeliest blockers — first).
+__device__ __forceinline__ int home_chunk(const DevScene& s, int f) {
+    return f < 0 ? 0 : (s.inv[f] / kTile) / kTile;
 }
 
 }  // namespace visrt

@@ -289,23 +289,19 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float sbox[];
-    __shared__ __align__(8) uint64_t bar[2];
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
     const DevScene& s = a.s;
-    const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const int nvt = (n + kTile - 1) / kTile;
-    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
-    bs.t0 = blockIdx.x % bs.ntiles;
-    sweep_init<RESIDENT>(bs);
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
     const long long ncand = static_cast<long long>(*a.ncand) < a.cand_cap ? static_cast<long long>(*a.ncand)
                                                                           : a.cand_cap;
 
     bool active = false, exhausted = false;
     long long cid = 0;
-    int leg = 0, legs = 0, rem = 0, bc0 = -1, bc1 = -1;
+    int leg = 0, legs = 0, bc0 = -1, bc1 = -1;   // cache: Morton indices
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
-    SegF g{};
+    Sweep sw{};
     unsigned long long tests = 0;
 
     auto emit = [&]() {
@@ -327,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
     };
     auto exact = [&](int k) {
         ++tests;
-        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
+        return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
     };
     // set up leg `leg`; legs a cached blocker already blocks end the candidate
     auto start_leg = [&]() {
@@ -347,8 +343,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
                 active = false;   // blocked leg: no path
                 return;
             }
-            g = make_segf(s, ax, ay, az, bx, by, bz);
-            rem = nvt;
+            const Cand& c = a.cand[cid];
+            sw.start(make_segf(s, ax, ay, az, bx, by, bz), -1, -1,
+                     home_chunk(s, leg == 0 ? (c.depth ? c.f[0] : -1) : c.f[leg - 1]), ctx.nchunks);
             return;
         }
     };
@@ -374,9 +371,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
-    auto vtile = [&](const float* B, int base, int cnt) {
+    auto step = [&]() {
         if (!active) return;
-        unsigned long long mask = tile_survivors(B, cnt, base, g, -1, -1);
+        int base;
+        unsigned long long mask = sweep_batch(sw, ctx, base);
         int hk = -1;
         while (mask) {
             const int kk = __ffsll(static_cast<long long>(mask)) - 1;
@@ -392,15 +390,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
                 bc0 = hk;
             }
             active = false;   // blocked: the sequence supports no path
-        } else if (--rem == 0) {
+        } else if (sw.done()) {
             ++leg;
             start_leg();
         }
     };
-    auto busy = [&]() { return active || !exhausted; };
 
     refill();
-    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
+    for (;;) {
+        step();
+        refill();
+        if (!__any_sync(kFull, active || !exhausted)) break;
+    }
     for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
     if (lane == 0) atomicAdd(&a.counter[1], tests);
 }
@@ -416,7 +417,7 @@ template <int MAXV>
 static void launch_legs_t(const TreeArgs& a, int device, cudaStream_t st) {
     const char* e = std::getenv("VISRT_FORCE_STREAM");
     const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
-    const size_t smem = res ? ((static_cast<size_t>(a.s.n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
+    const size_t smem = sweep_smem_bytes(a.s.n, a.s.ntiles, res);
     if (res) {
         auto fn = k_tree_legs<MAXV, true>;
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), "attr");

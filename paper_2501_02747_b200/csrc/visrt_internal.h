@@ -50,6 +50,12 @@ struct HostScene {
     std::vector<float> box;
     double origin[3] = {0, 0, 0};
     double extent = 0;                // max |coordinate - origin| over the scene
+    // two-level culling hierarchy: Morton order of the xy AABB centres,
+    // tiles of 64 consecutive faces with union boxes (sweep.h)
+    std::vector<int32_t> perm, inv;
+    std::vector<float> sbox, tbox;
+    std::vector<double> srec;         // records in Morton order (layout of rec4/rec8)
+    int32_t ntiles = 0, nchunks = 0;
 };
 
 // Dilation of the fp32 culling boxes. A true hit of segment_face_intersection
@@ -65,6 +71,7 @@ inline double box_margin(double extent, double miter) {
 // Host ingest with the reference's exact arithmetic. Throws std::runtime_error
 // with the reference's SceneError-style message on invalid input.
 void ingest(const visrt_facets_v1& f, HostScene& hs);
+void build_hierarchy(HostScene& hs);
 
 // Sightline count S(i,j) of occlusion_judgment (src/vismatrix.cpp:263-273).
 inline int sightline_count(int nr, int nsr, int na, int nsa) {
