@@ -95,14 +95,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     Sweep sw{};
     unsigned long long tests = 0, sweeps = 0, batches = 0;
 
+    // Phase-1 mode (a.first_blk): only the first sightline (the centroid pair)
+    // is decided here; a blocked one hands the pair to k_pair_rest with its
+    // blocker, a clear or degenerate one settles the pair.
+    const bool phase1 = a.first_blk != nullptr;
     auto finish = [&](bool occluded) {
         if (!occluded) set_pair_bit(a.bits, s.words, pi, pj);
         if (a.cbit) a.cbit[pidx] = occluded ? 0 : 1;
+        if (phase1) a.first_blk[pidx] = -1;
         active = false;
     };
     auto exact = [&](int k) {
         ++tests;
         return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
+    };
+    auto defer = [&](int k) {   // phase 1: sightline 0 blocked by k
+        a.first_blk[pidx] = k;
+        active = false;
     };
     // Next sightline of the current pair. Sightlines a cached blocker already
     // blocks are settled on the spot (one exact test each); the first one the
@@ -114,11 +123,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                 return;
             }
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
-            if (bc0 >= 0 && bc0 != si && bc0 != sj && exact(bc0)) continue;
+            if (bc0 >= 0 && bc0 != si && bc0 != sj && exact(bc0)) {
+                if (phase1) {
+                    defer(bc0);
+                    return;
+                }
+                continue;
+            }
             if (bc1 >= 0 && bc1 != si && bc1 != sj && exact(bc1)) {
                 const int t = bc0;
                 bc0 = bc1;
                 bc1 = t;
+                if (phase1) {
+                    defer(bc0);
+                    return;
+                }
                 continue;
             }
             sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
@@ -171,33 +190,122 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
         }
     };
 
+    __shared__ int slots[kThreads];
+    int* slot = slots + (threadIdx.x & ~31);
     refill();
     for (;;) {
+        unsigned long long mask = 0;
+        int base = 0;
         if (active) {
             ++batches;
-            int base;
-            unsigned long long mask = sweep_batch(sw, ctx, base);
-            int hk = -1;
-            while (mask) {
-                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-                mask &= mask - 1;
-                if (exact(base + kk)) {
-                    hk = base + kk;
-                    break;
-                }
-            }
+            mask = sweep_batch(sw, ctx, base);
+        }
+        const int hk = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests, 0ull,
+                                        [](int, unsigned long long) {});
+        if (active) {
             if (hk >= 0) {
                 if (hk != bc0) {
                     bc1 = bc0;
                     bc0 = hk;
                 }
-                advance();
+                if (phase1) defer(hk);
+                else advance();
             } else if (sw.done()) {
                 finish(false);   // a sightline clear of every occluder
             }
         }
         refill();
         if (!__any_sync(kFull, active || !exhausted)) break;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        tests += __shfl_down_sync(kFull, tests, o);
+        sweeps += __shfl_down_sync(kFull, sweeps, o);
+        batches += __shfl_down_sync(kFull, batches, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&a.counter[1], tests);
+        atomicAdd(&a.counter[2], sweeps);
+        atomicAdd(&a.counter[3], batches);
+    }
+}
+
+// Phase 2 of the (B)/(A) bit: the pairs whose centroid sightline was blocked.
+// One warp per pair, one lane per remaining sightline (32 for quad pairs):
+// every lane first tests the phase-1 blocker (same record for all lanes:
+// broadcast load), only the sightlines it does not block are swept — together,
+// as one converged batch loop, since they share the pair's neighbourhood —
+// and the pair stops at the first clear sightline.
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 3) k_pair_rest(PairArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
+    __shared__ int slots[kThreads];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+    int* slot = slots + (threadIdx.x & ~31);
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    unsigned long long tests = 0, sweeps = 0, batches = 0;
+    for (;;) {
+        unsigned long long w = 0;
+        if (lane == 0) w = atomicAdd(&a.counter[0], 1ull);
+        w = __shfl_sync(kFull, w, 0);
+        if (static_cast<long long>(w) >= a.npend) break;
+        const long long p = a.pend[w];
+        const int k0 = a.first_blk[p];
+        int pi, pj;
+        if (a.ci) {
+            pi = a.ci[p];
+            pj = a.cj[p];
+        } else {
+            pair_from_index(p, n, pi, pj);
+        }
+        const int si = s.inv[pi], sj = s.inv[pj];
+        const int nr = s.nv[pi], na = s.nv[pj];
+        const int grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
+        const int S = nr * na + 1 + grid;
+        bool clear = false;
+        for (int r0 = 1; r0 < S && !clear; r0 += 32) {
+            const int ord = r0 + lane;
+            double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+            bool need = false;
+            Sweep sw{};
+            if (ord < S) {
+                sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
+                ++tests;
+                if (!seg_hits<MAXV>(s.srec + static_cast<size_t>(k0) * STRIDE, ax, ay, az, bx, by, bz)) {
+                    sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
+                    need = true;
+                    ++sweeps;
+                }
+            }
+            bool mine_clear = false;
+            while (__any_sync(kFull, need)) {
+                unsigned long long mask = 0;
+                int base = 0;
+                if (need) {
+                    ++batches;
+                    mask = sweep_batch(sw, ctx, base);
+                }
+                const int hk = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests, 0ull,
+                                                [](int, unsigned long long) {});
+                if (need) {
+                    if (hk >= 0) {
+                        need = false;   // blocked
+                    } else if (sw.done()) {
+                        need = false;
+                        mine_clear = true;
+                    }
+                }
+                if (__any_sync(kFull, mine_clear)) break;
+            }
+            clear = __any_sync(kFull, mine_clear);
+        }
+        if (lane == 0) {
+            if (clear) set_pair_bit(a.bits, s.words, pi, pj);
+            if (a.cbit) a.cbit[p] = clear ? 1 : 0;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         tests += __shfl_down_sync(kFull, tests, o);
@@ -276,21 +384,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
         }
     };
 
+    __shared__ int slots[kThreads];
+    int* slot = slots + (threadIdx.x & ~31);
+    const int32_t* perm = s.perm;
     refill();
     for (;;) {
+        unsigned long long mask = 0;
+        int base = 0;
+        if (active) mask = sweep_batch(sw, ctx, base);
+        const int h = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests,
+                                       reinterpret_cast<unsigned long long>(mask_out),
+                                       [perm](int k, unsigned long long out) {
+                                           const int f = perm[k];
+                                           atomicOr(reinterpret_cast<uint32_t*>(out) + (f >> 5), 1u << (f & 31));
+                                       });
         if (active) {
-            int base;
-            unsigned long long mask = sweep_batch(sw, ctx, base);
-            while (mask) {
-                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-                mask &= mask - 1;
-                ++tests;
-                if (seg_hits<MAXV>(s.srec + static_cast<size_t>(base + kk) * STRIDE, ax, ay, az, bx, by, bz)) {
-                    hit_any = true;
-                    const int k = s.perm[base + kk];
-                    atomicOr(mask_out + (k >> 5), 1u << (k & 31));
-                }
-            }
+            if (h >= 0) hit_any = true;
             if (sw.done()) {
                 if (hit_any) ++blocked;
                 ++ord;
@@ -409,6 +518,40 @@ cudaError_t launch_pair_bits(const PairArgs& a, int device, cudaStream_t st) {
 
 cudaError_t launch_pair_detail(const PairArgs& a, int device, cudaStream_t st) {
     return a.s.maxv <= 4 ? launch_detail_t<4>(a, device, st) : launch_detail_t<8>(a, device, st);
+}
+
+template <int MAXV>
+static cudaError_t launch_rest_t(const PairArgs& a, int device, cudaStream_t st) {
+    const bool res = use_resident(a.s.n);
+    const size_t smem = sweep_smem(a.s, res);
+    return res ? launch_persistent(k_pair_rest<MAXV, true>, smem, a, device, st)
+               : launch_persistent(k_pair_rest<MAXV, false>, smem, a, device, st);
+}
+
+cudaError_t launch_pair_rest(const PairArgs& a, int device, cudaStream_t st) {
+    return a.s.maxv <= 4 ? launch_rest_t<4>(a, device, st) : launch_rest_t<8>(a, device, st);
+}
+
+struct PendingOp {
+    const int32_t* fb;
+    __device__ bool operator()(long long p) const { return fb[p] >= 0; }
+};
+
+// Ordered list of the pairs phase 1 left pending (first_blk >= 0).
+cudaError_t launch_select_pending(const int32_t* first_blk, long long npairs, long long* d_out, long long* d_count,
+                                  void*& temp, size_t& temp_bytes, cudaStream_t st) {
+    thrust::counting_iterator<long long> in(0);
+    PendingOp op{first_blk};
+    size_t need = 0;
+    cudaError_t e = cub::DeviceSelect::If(nullptr, need, in, d_out, d_count, npairs, op, st);
+    if (e != cudaSuccess) return e;
+    if (need > temp_bytes) {
+        if (temp) cudaFree(temp);
+        e = cudaMalloc(&temp, need);
+        if (e != cudaSuccess) return e;
+        temp_bytes = need;
+    }
+    return cub::DeviceSelect::If(temp, temp_bytes, in, d_out, d_count, npairs, op, st);
 }
 
 // Ordered compaction of the prefiltered pairs; returns the device count in *d_count.

@@ -358,19 +358,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     };
     // One virtual tile of the current sightline sweep.
     // One 64-box culling batch of the current sightline sweep.
+    __shared__ int slots[kThreads];
+    int* slot = slots + (threadIdx.x & ~31);
     auto step = [&]() {
+        unsigned long long mask = 0;
+        int base = 0;
+        if (querying) mask = sweep_batch(sw, ctx, base);
+        const int hk = coop_exact<MAXV>(s.srec, mask, base, sx, sy, sz, qx, qy, qz, slot, tests, 0ull,
+                                        [](int, unsigned long long) {});
         if (!querying) return;
-        int base;
-        unsigned long long mask = sweep_batch(sw, ctx, base);
-        int hk = -1;
-        while (mask) {
-            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-            mask &= mask - 1;
-            if (exact(base + kk)) {
-                hk = base + kk;
-                break;
-            }
-        }
         if (hk >= 0) {
             if (hk != bc0) {
                 bc1 = bc0;

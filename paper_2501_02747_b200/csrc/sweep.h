@@ -94,6 +94,67 @@ __device__ __forceinline__ unsigned long long sweep_batch(Sweep& sw, const Sweep
     return mask;
 }
 
+// Warp-cooperative exact phase. Every lane holds the survivor mask of its own
+// level-2 tile (Morton faces base..base+63) for its own segment a->b; the
+// warp pools all survivors and deals them out 32 at a time, so each round
+// issues 32 independent record loads and runs dense FP64 work instead of a
+// divergent per-lane loop. Each lane's smallest hit (Morton index) comes back
+// through `slot` (per-warp shared memory, 32 ints); with `all` every hit is
+// also handed to on_hit(k, owner's payload) (blocker sets). Returns the lane's own
+// first hit or -1. Must be called by all 32 lanes (inactive lanes: mask 0).
+template <int MAXV, class OnHit>
+__device__ __forceinline__ int coop_exact(const double* __restrict__ srec, unsigned long long mask, int base,
+                                          double ax, double ay, double az, double bx, double by, double bz,
+                                          int* slot, unsigned long long& tests, unsigned long long payload,
+                                          OnHit&& on_hit) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    const int lane = threadIdx.x & 31;
+    const int cnt = __popcll(mask);
+    int pre = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, pre, o);
+        if (lane >= o) pre += v;
+    }
+    const int total = __shfl_sync(kFull, pre, 31);
+    if (total == 0) return -1;
+    const int excl = pre - cnt;
+    slot[lane] = 0x7fffffff;
+    __syncwarp();
+    for (int r = 0; r < total; r += 32) {
+        const int gi = r + lane;
+        // owner lane: the last lane whose exclusive prefix is <= gi
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int e = __shfl_sync(kFull, excl, (o + step) & 31);
+            if (o + step < 32 && e <= gi) o += step;
+        }
+        const unsigned long long om = __shfl_sync(kFull, mask, o);
+        const int oexcl = __shfl_sync(kFull, excl, o);
+        const int obase = __shfl_sync(kFull, base, o);
+        const double oax = __shfl_sync(kFull, ax, o), oay = __shfl_sync(kFull, ay, o),
+                     oaz = __shfl_sync(kFull, az, o);
+        const double obx = __shfl_sync(kFull, bx, o), oby = __shfl_sync(kFull, by, o),
+                     obz = __shfl_sync(kFull, bz, o);
+        const unsigned long long opay = __shfl_sync(kFull, payload, o);
+        if (gi < total) {
+            // the (gi - oexcl)-th set bit of the owner's mask
+            unsigned long long m = om;
+            for (int q = gi - oexcl; q > 0; --q) m &= m - 1;
+            const int k = obase + __ffsll(static_cast<long long>(m)) - 1;
+            ++tests;
+            if (seg_hits<MAXV>(srec + static_cast<size_t>(k) * STRIDE, oax, oay, oaz, obx, oby, obz)) {
+                atomicMin(slot + o, k);
+                on_hit(k, opay);
+            }
+        }
+    }
+    __syncwarp();
+    const int h = slot[lane];
+    return h == 0x7fffffff ? -1 : h;
+}
+
 // Block setup: stage the tile boxes (and the member boxes when RESIDENT) in
 // shared memory with TMA bulk copies (cp.async.bulk, one mbarrier).
 template <bool RESIDENT>

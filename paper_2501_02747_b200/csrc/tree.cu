@@ -371,19 +371,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
+    __shared__ int slots[kThreads];
+    int* slot = slots + (threadIdx.x & ~31);
     auto step = [&]() {
+        unsigned long long mask = 0;
+        int base = 0;
+        if (active) mask = sweep_batch(sw, ctx, base);
+        const int hk = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests, 0ull,
+                                        [](int, unsigned long long) {});
         if (!active) return;
-        int base;
-        unsigned long long mask = sweep_batch(sw, ctx, base);
-        int hk = -1;
-        while (mask) {
-            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-            mask &= mask - 1;
-            if (exact(base + kk)) {
-                hk = base + kk;
-                break;
-            }
-        }
         if (hk >= 0) {
             if (hk != bc0) {
                 bc1 = bc0;
