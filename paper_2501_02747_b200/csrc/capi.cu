@@ -22,9 +22,6 @@ cudaError_t launch_prefilter(const DevScene& s, long long npairs, long long* d_s
                              void*& temp, size_t& temp_bytes, cudaStream_t st);
 cudaError_t launch_split_pairs(const long long* sel, long long m, int n, int32_t* ci, int32_t* cj,
                                cudaStream_t st);
-cudaError_t launch_pair_rest(const PairArgs& a, int device, cudaStream_t st);
-cudaError_t launch_select_pending(const int32_t* first_blk, long long npairs, long long* d_out, long long* d_count,
-                                  void*& temp, size_t& temp_bytes, cudaStream_t st);
 cudaError_t launch_clear_pairs(unsigned long long* bits, int words, const int32_t* ci, const int32_t* cj,
                                long long m, cudaStream_t st);
 }  // namespace visrt
@@ -93,26 +90,10 @@ struct visrt_scene {
         if (d_ci) cudaFree(d_ci);
         if (d_cj) cudaFree(d_cj);
         if (d_cbit) cudaFree(d_cbit);
-        if (d_fb) cudaFree(d_fb);
-        if (d_pend) cudaFree(d_pend);
         if (temp) cudaFree(temp);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         cudaSetDevice(cur);
-    }
-
-    // two-phase bit buffers
-    int32_t* d_fb = nullptr;
-    long long* d_pend = nullptr;
-    long long phase_cap = 0;
-    long long npending = 0;
-    void ensure_phase(long long m) {
-        if (m <= phase_cap) return;
-        if (d_fb) cudaFree(d_fb);
-        if (d_pend) cudaFree(d_pend);
-        ck(cudaMalloc(&d_fb, std::max<long long>(m, 1) * sizeof(int32_t)), "cudaMalloc first_blk");
-        ck(cudaMalloc(&d_pend, std::max<long long>(m, 1) * sizeof(long long)), "cudaMalloc pending");
-        phase_cap = m;
     }
 
     void ensure_cand(long long m) {
@@ -210,13 +191,6 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.orient = dev_upload(hs.orient, sc->allocs);
         ds.seg_ok = dev_upload(hs.seg_ok, sc->allocs);
         ds.box = dev_upload(hs.box, sc->allocs);
-        ds.sbox = dev_upload(hs.sbox, sc->allocs);
-        ds.tbox = dev_upload(hs.tbox, sc->allocs);
-        ds.srec = dev_upload(hs.srec, sc->allocs);
-        ds.perm = dev_upload(hs.perm, sc->allocs);
-        ds.inv = dev_upload(hs.inv, sc->allocs);
-        ds.ntiles = hs.ntiles;
-        ds.nchunks = hs.nchunks;
         sc->upload_bytes = static_cast<int64_t>(
             (hs.maxv <= 4 ? hs.rec4.size() : hs.rec8.size()) * 8 + hs.samples.size() * 8 + hs.pts.size() * 8 +
             hs.normal.size() * 8 + hs.seg.size() * 8 + hs.aabb.size() * 8 + hs.nv.size() * 4 + hs.ns.size() * 4 +
@@ -286,23 +260,7 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
         } else {
             a.npairs = npairs;
         }
-        if (a.npairs > 0) {
-            // phase 1: centroid sightline of every pair (lane per pair)
-            sc->ensure_phase(a.npairs);
-            a.first_blk = sc->d_fb;
-            ck(visrt::launch_pair_bits(a, sc->device, st), "k_pair_bits");
-            // phase 2: pairs whose centroid sightline was blocked (warp per pair)
-            ck(visrt::launch_select_pending(sc->d_fb, a.npairs, sc->d_pend, sc->d_count + 1, sc->temp,
-                                            sc->temp_bytes, st), "select pending");
-            long long npend = 0;
-            ck(cudaMemcpyAsync(&npend, sc->d_count + 1, sizeof(long long), cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemsetAsync(sc->d_counter, 0, sizeof(unsigned long long), st), "memset cursor");
-            ck(cudaStreamSynchronize(st), "sync");
-            a.pend = sc->d_pend;
-            a.npend = npend;
-            sc->npending = npend;
-            if (npend > 0) ck(visrt::launch_pair_rest(a, sc->device, st), "k_pair_rest");
-        }
+        if (a.npairs > 0) ck(visrt::launch_pair_bits(a, sc->device, st), "k_pair_bits");
         ck(cudaEventRecord(sc->ev1, st), "event");
         unsigned long long counters[4] = {0, 0, 0, 0};
         ck(cudaMemcpyAsync(counters, sc->d_counter, sizeof(counters), cudaMemcpyDeviceToHost, st), "D2H ctr");

@@ -64,58 +64,40 @@ __device__ __forceinline__ void set_pair_bit(unsigned long long* bits, int words
     atomicOr(bits + static_cast<size_t>(i) * words + (j >> 6), 1ull << (j & 63));
     atomicOr(bits + static_cast<size_t>(j) * words + (i >> 6), 1ull << (i & 63));
 }
-
-// Faces whose (exact) AABBs are more than 1e-6 m apart have no coincident
-// samples, hence no degenerate sightline (samples lie in the face AABB up to
-// ~1e-11 m of rounding).
-__device__ __forceinline__ bool may_touch(const DevScene& s, int i, int j) {
-    const double* A = s.aabb + 6 * static_cast<size_t>(i);
-    const double* B = s.aabb + 6 * static_cast<size_t>(j);
-    bool sep = false;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) sep |= (B[d] > A[3 + d] + 1e-6) | (A[d] > B[3 + d] + 1e-6);
-    return !sep;
-}
-
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t bar[1];
+    extern __shared__ __align__(128) float sbox[];
+    __shared__ __align__(8) uint64_t bar[2];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    // RESIDENT sweeps are counted in virtual tiles, STREAM sweeps too
+    const int nvt = (n + kTile - 1) / kTile;
+    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
+    bs.t0 = blockIdx.x % bs.ntiles;
+    sweep_init<RESIDENT>(bs);
 
     bool active = false, exhausted = false;
     long long pidx = 0;
-    int pi = 0, pj = 0, si = 0, sj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0;
-    int bc0 = -1, bc1 = -1;   // blocker cache (Morton indices of the last blockers)
+    int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0;
+    int bc0 = -1, bc1 = -1;   // blocker cache: last occluders that blocked a sightline
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
-    Sweep sw{};
-    unsigned long long tests = 0, sweeps = 0, batches = 0;
+    SegF g{};
+    unsigned long long tests = 0, sweeps = 0, tiles = 0;
 
-    // Phase-1 mode (a.first_blk): only the first sightline (the centroid pair)
-    // is decided here; a blocked one hands the pair to k_pair_rest with its
-    // blocker, a clear or degenerate one settles the pair.
-    const bool phase1 = a.first_blk != nullptr;
     auto finish = [&](bool occluded) {
         if (!occluded) set_pair_bit(a.bits, s.words, pi, pj);
         if (a.cbit) a.cbit[pidx] = occluded ? 0 : 1;
-        if (phase1) a.first_blk[pidx] = -1;
         active = false;
     };
     auto exact = [&](int k) {
         ++tests;
-        return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
-    };
-    auto defer = [&](int k) {   // phase 1: sightline 0 blocked by k
-        a.first_blk[pidx] = k;
-        active = false;
+        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
     };
     // Next sightline of the current pair. Sightlines a cached blocker already
     // blocks are settled on the spot (one exact test each); the first one the
-    // cache does not block starts a culled sweep over every other face.
+    // cache does not block starts a full cyclic sweep of nvt virtual tiles.
     auto advance = [&]() {
         for (;;) {
             if (++ord == S) {
@@ -123,24 +105,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                 return;
             }
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
-            if (bc0 >= 0 && bc0 != si && bc0 != sj && exact(bc0)) {
-                if (phase1) {
-                    defer(bc0);
-                    return;
-                }
-                continue;
-            }
-            if (bc1 >= 0 && bc1 != si && bc1 != sj && exact(bc1)) {
+            if (bc0 >= 0 && bc0 != pi && bc0 != pj && exact(bc0)) continue;
+            if (bc1 >= 0 && bc1 != pi && bc1 != pj && exact(bc1)) {
                 const int t = bc0;
                 bc0 = bc1;
                 bc1 = t;
-                if (phase1) {
-                    defer(bc0);
-                    return;
-                }
                 continue;
             }
-            sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
+            g = make_segf(s, ax, ay, az, bx, by, bz);
+            rem = nvt;
             ++sweeps;
             return;
         }
@@ -164,8 +137,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                     } else {
                         pair_from_index(my, n, pi, pj);
                     }
-                    si = s.inv[pi];
-                    sj = s.inv[pj];
                     nr = s.nv[pi];
                     na = s.nv[pj];
                     grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
@@ -189,133 +160,42 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
+    auto vtile = [&](const float* B, int base, int cnt) {
+        if (!active) return;
+        ++tiles;
+        unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
+        int hk = -1;
+        while (mask) {
+            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            if (exact(base + kk)) {
+                hk = base + kk;
+                break;
+            }
+        }
+        if (hk >= 0) {
+            if (hk != bc0) {
+                bc1 = bc0;
+                bc0 = hk;
+            }
+            advance();
+        } else if (--rem == 0) {
+            finish(false);   // a sightline clear of every occluder
+        }
+    };
+    auto busy = [&]() { return active || !exhausted; };
 
-    __shared__ int slots[kThreads];
-    int* slot = slots + (threadIdx.x & ~31);
     refill();
-    for (;;) {
-        unsigned long long mask = 0;
-        int base = 0;
-        if (active) {
-            ++batches;
-            mask = sweep_batch(sw, ctx, base);
-        }
-        const int hk = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests, 0ull,
-                                        [](int, unsigned long long) {});
-        if (active) {
-            if (hk >= 0) {
-                if (hk != bc0) {
-                    bc1 = bc0;
-                    bc0 = hk;
-                }
-                if (phase1) defer(hk);
-                else advance();
-            } else if (sw.done()) {
-                finish(false);   // a sightline clear of every occluder
-            }
-        }
-        refill();
-        if (!__any_sync(kFull, active || !exhausted)) break;
-    }
+    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
     for (int o = 16; o > 0; o >>= 1) {
         tests += __shfl_down_sync(kFull, tests, o);
         sweeps += __shfl_down_sync(kFull, sweeps, o);
-        batches += __shfl_down_sync(kFull, batches, o);
+        tiles += __shfl_down_sync(kFull, tiles, o);
     }
     if (lane == 0) {
         atomicAdd(&a.counter[1], tests);
         atomicAdd(&a.counter[2], sweeps);
-        atomicAdd(&a.counter[3], batches);
-    }
-}
-
-// Phase 2 of the (B)/(A) bit: the pairs whose centroid sightline was blocked.
-// One warp per pair, one lane per remaining sightline (32 for quad pairs):
-// every lane first tests the phase-1 blocker (same record for all lanes:
-// broadcast load), only the sightlines it does not block are swept — together,
-// as one converged batch loop, since they share the pair's neighbourhood —
-// and the pair stops at the first clear sightline.
-template <int MAXV, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads, 3) k_pair_rest(PairArgs a) {
-    constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t bar[1];
-    __shared__ int slots[kThreads];
-    const DevScene& s = a.s;
-    const int n = s.n;
-    const int lane = threadIdx.x & 31;
-    int* slot = slots + (threadIdx.x & ~31);
-    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
-    unsigned long long tests = 0, sweeps = 0, batches = 0;
-    for (;;) {
-        unsigned long long w = 0;
-        if (lane == 0) w = atomicAdd(&a.counter[0], 1ull);
-        w = __shfl_sync(kFull, w, 0);
-        if (static_cast<long long>(w) >= a.npend) break;
-        const long long p = a.pend[w];
-        const int k0 = a.first_blk[p];
-        int pi, pj;
-        if (a.ci) {
-            pi = a.ci[p];
-            pj = a.cj[p];
-        } else {
-            pair_from_index(p, n, pi, pj);
-        }
-        const int si = s.inv[pi], sj = s.inv[pj];
-        const int nr = s.nv[pi], na = s.nv[pj];
-        const int grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
-        const int S = nr * na + 1 + grid;
-        bool clear = false;
-        for (int r0 = 1; r0 < S && !clear; r0 += 32) {
-            const int ord = r0 + lane;
-            double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
-            bool need = false;
-            Sweep sw{};
-            if (ord < S) {
-                sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
-                ++tests;
-                if (!seg_hits<MAXV>(s.srec + static_cast<size_t>(k0) * STRIDE, ax, ay, az, bx, by, bz)) {
-                    sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
-                    need = true;
-                    ++sweeps;
-                }
-            }
-            bool mine_clear = false;
-            while (__any_sync(kFull, need)) {
-                unsigned long long mask = 0;
-                int base = 0;
-                if (need) {
-                    ++batches;
-                    mask = sweep_batch(sw, ctx, base);
-                }
-                const int hk = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests, 0ull,
-                                                [](int, unsigned long long) {});
-                if (need) {
-                    if (hk >= 0) {
-                        need = false;   // blocked
-                    } else if (sw.done()) {
-                        need = false;
-                        mine_clear = true;
-                    }
-                }
-                if (__any_sync(kFull, mine_clear)) break;
-            }
-            clear = __any_sync(kFull, mine_clear);
-        }
-        if (lane == 0) {
-            if (clear) set_pair_bit(a.bits, s.words, pi, pj);
-            if (a.cbit) a.cbit[p] = clear ? 1 : 0;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        tests += __shfl_down_sync(kFull, tests, o);
-        sweeps += __shfl_down_sync(kFull, sweeps, o);
-        batches += __shfl_down_sync(kFull, batches, o);
-    }
-    if (lane == 0) {
-        atomicAdd(&a.counter[1], tests);
-        atomicAdd(&a.counter[2], sweeps);
-        atomicAdd(&a.counter[3], batches);
+        atomicAdd(&a.counter[3], tiles);
     }
 }
 
@@ -324,17 +204,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_rest(PairArgs a) {
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t bar[1];
+    extern __shared__ __align__(128) float sbox[];
+    __shared__ __align__(8) uint64_t bar[2];
     const DevScene& s = a.s;
+    const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    const int nvt = (n + kTile - 1) / kTile;
+    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
+    bs.t0 = blockIdx.x % bs.ntiles;
+    sweep_init<RESIDENT>(bs);
 
     bool active = false, exhausted = false, hit_any = false;
     long long pidx = 0;
-    int pi = 0, pj = 0, si = 0, sj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, blocked = 0;
+    int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0, blocked = 0;
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
-    Sweep sw{};
+    SegF g{};
     unsigned long long tests = 0;
     uint32_t* mask_out = nullptr;
 
@@ -343,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
         while (ord < S) {
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
             if (!degenerate(ax, ay, az, bx, by, bz)) {
-                sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
+                g = make_segf(s, ax, ay, az, bx, by, bz);
+                rem = nvt;
                 hit_any = false;
                 return;
             }
@@ -367,8 +252,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
                     pidx = my;
                     pi = a.ci[my];
                     pj = a.cj[my];
-                    si = s.inv[pi];
-                    sj = s.inv[pj];
                     nr = s.nv[pi];
                     na = s.nv[pj];
                     grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
@@ -383,32 +266,29 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
-
-    __shared__ int slots[kThreads];
-    int* slot = slots + (threadIdx.x & ~31);
-    const int32_t* perm = s.perm;
-    refill();
-    for (;;) {
-        unsigned long long mask = 0;
-        int base = 0;
-        if (active) mask = sweep_batch(sw, ctx, base);
-        const int h = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests,
-                                       reinterpret_cast<unsigned long long>(mask_out),
-                                       [perm](int k, unsigned long long out) {
-                                           const int f = perm[k];
-                                           atomicOr(reinterpret_cast<uint32_t*>(out) + (f >> 5), 1u << (f & 31));
-                                       });
-        if (active) {
-            if (h >= 0) hit_any = true;
-            if (sw.done()) {
-                if (hit_any) ++blocked;
-                ++ord;
-                next_sightline();
+    auto vtile = [&](const float* B, int base, int cnt) {
+        if (!active) return;
+        unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
+        while (mask) {
+            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            ++tests;
+            if (seg_hits<MAXV>(s.rec + static_cast<size_t>(base + kk) * STRIDE, ax, ay, az, bx, by, bz)) {
+                hit_any = true;
+                const int k = base + kk;
+                atomicOr(mask_out + (k >> 5), 1u << (k & 31));
             }
         }
-        refill();
-        if (!__any_sync(kFull, active || !exhausted)) break;
-    }
+        if (--rem == 0) {
+            if (hit_any) ++blocked;
+            ++ord;
+            next_sightline();
+        }
+    };
+    auto busy = [&]() { return active || !exhausted; };
+
+    refill();
+    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
     for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
     if (lane == 0) atomicAdd(&a.counter[1], tests);
 }
@@ -484,8 +364,8 @@ static cudaError_t launch_persistent(K fn, size_t smem, const PairArgs& a, int d
     return cudaGetLastError();
 }
 
-// VISRT_FORCE_STREAM=1 keeps the member boxes in global memory (L1/L2) even
-// when they fit in shared memory (tests cover both paths on small scenes).
+// VISRT_FORCE_STREAM=1 forces the streamed-tile path (tests cover both paths
+// on small scenes).
 static bool use_resident(int n) {
     static const bool force_stream = [] {
         const char* e = std::getenv("VISRT_FORCE_STREAM");
@@ -494,12 +374,14 @@ static bool use_resident(int n) {
     return !force_stream && n <= kResidentMaxBoxes;
 }
 
-static size_t sweep_smem(const DevScene& s, bool resident) { return sweep_smem_bytes(s.n, s.ntiles, resident); }
+static size_t sweep_smem(int n, bool resident) {
+    return resident ? ((static_cast<size_t>(n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
+}
 
 template <int MAXV>
 static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
     const bool res = use_resident(a.s.n);
-    const size_t smem = sweep_smem(a.s, res);
+    const size_t smem = sweep_smem(a.s.n, res);
     return res ? launch_persistent(k_pair_bits<MAXV, true>, smem, a, device, st)
                : launch_persistent(k_pair_bits<MAXV, false>, smem, a, device, st);
 }
@@ -507,7 +389,7 @@ static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st)
 template <int MAXV>
 static cudaError_t launch_detail_t(const PairArgs& a, int device, cudaStream_t st) {
     const bool res = use_resident(a.s.n);
-    const size_t smem = sweep_smem(a.s, res);
+    const size_t smem = sweep_smem(a.s.n, res);
     return res ? launch_persistent(k_pair_detail<MAXV, true>, smem, a, device, st)
                : launch_persistent(k_pair_detail<MAXV, false>, smem, a, device, st);
 }
@@ -518,40 +400,6 @@ cudaError_t launch_pair_bits(const PairArgs& a, int device, cudaStream_t st) {
 
 cudaError_t launch_pair_detail(const PairArgs& a, int device, cudaStream_t st) {
     return a.s.maxv <= 4 ? launch_detail_t<4>(a, device, st) : launch_detail_t<8>(a, device, st);
-}
-
-template <int MAXV>
-static cudaError_t launch_rest_t(const PairArgs& a, int device, cudaStream_t st) {
-    const bool res = use_resident(a.s.n);
-    const size_t smem = sweep_smem(a.s, res);
-    return res ? launch_persistent(k_pair_rest<MAXV, true>, smem, a, device, st)
-               : launch_persistent(k_pair_rest<MAXV, false>, smem, a, device, st);
-}
-
-cudaError_t launch_pair_rest(const PairArgs& a, int device, cudaStream_t st) {
-    return a.s.maxv <= 4 ? launch_rest_t<4>(a, device, st) : launch_rest_t<8>(a, device, st);
-}
-
-struct PendingOp {
-    const int32_t* fb;
-    __device__ bool operator()(long long p) const { return fb[p] >= 0; }
-};
-
-// Ordered list of the pairs phase 1 left pending (first_blk >= 0).
-cudaError_t launch_select_pending(const int32_t* first_blk, long long npairs, long long* d_out, long long* d_count,
-                                  void*& temp, size_t& temp_bytes, cudaStream_t st) {
-    thrust::counting_iterator<long long> in(0);
-    PendingOp op{first_blk};
-    size_t need = 0;
-    cudaError_t e = cub::DeviceSelect::If(nullptr, need, in, d_out, d_count, npairs, op, st);
-    if (e != cudaSuccess) return e;
-    if (need > temp_bytes) {
-        if (temp) cudaFree(temp);
-        e = cudaMalloc(&temp, need);
-        if (e != cudaSuccess) return e;
-        temp_bytes = need;
-    }
-    return cub::DeviceSelect::If(temp, temp_bytes, in, d_out, d_count, npairs, op, st);
 }
 
 // Ordered compaction of the prefiltered pairs; returns the device count in *d_count.
