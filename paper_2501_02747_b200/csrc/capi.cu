@@ -191,6 +191,13 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.orient = dev_upload(hs.orient, sc->allocs);
         ds.seg_ok = dev_upload(hs.seg_ok, sc->allocs);
         ds.box = dev_upload(hs.box, sc->allocs);
+        ds.sbox = dev_upload(hs.sbox, sc->allocs);
+        ds.tbox = dev_upload(hs.tbox, sc->allocs);
+        ds.srec = dev_upload(hs.srec, sc->allocs);
+        ds.perm = dev_upload(hs.perm, sc->allocs);
+        ds.inv = dev_upload(hs.inv, sc->allocs);
+        ds.ntiles = hs.ntiles;
+        ds.nchunks = hs.nchunks;
         sc->upload_bytes = static_cast<int64_t>(
             (hs.maxv <= 4 ? hs.rec4.size() : hs.rec8.size()) * 8 + hs.samples.size() * 8 + hs.pts.size() * 8 +
             hs.normal.size() * 8 + hs.seg.size() * 8 + hs.aabb.size() * 8 + hs.nv.size() * 4 + hs.ns.size() * 4 +

@@ -64,27 +64,36 @@ __device__ __forceinline__ void set_pair_bit(unsigned long long* bits, int words
     atomicOr(bits + static_cast<size_t>(i) * words + (j >> 6), 1ull << (j & 63));
     atomicOr(bits + static_cast<size_t>(j) * words + (i >> 6), 1ull << (i & 63));
 }
+
+// Faces whose (exact) AABBs are more than 1e-6 m apart have no coincident
+// samples, hence no degenerate sightline (samples lie in the face AABB up to
+// ~1e-11 m of rounding).
+__device__ __forceinline__ bool may_touch(const DevScene& s, int i, int j) {
+    const double* A = s.aabb + 6 * static_cast<size_t>(i);
+    const double* B = s.aabb + 6 * static_cast<size_t>(j);
+    bool sep = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sep |= (B[d] > A[3 + d] + 1e-6) | (A[d] > B[3 + d] + 1e-6);
+    return !sep;
+}
+
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float sbox[];
-    __shared__ __align__(8) uint64_t bar[2];
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    // RESIDENT sweeps are counted in virtual tiles, STREAM sweeps too
-    const int nvt = (n + kTile - 1) / kTile;
-    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
-    bs.t0 = blockIdx.x % bs.ntiles;
-    sweep_init<RESIDENT>(bs);
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
 
     bool active = false, exhausted = false;
     long long pidx = 0;
-    int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0;
-    int bc0 = -1, bc1 = -1;   // blocker cache: last occluders that blocked a sightline
+    int pi = 0, pj = 0, si = 0, sj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0;
+    int bc0 = -1, bc1 = -1;   // blocker cache (Morton indices of the last blockers)
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
-    SegF g{};
-    unsigned long long tests = 0, sweeps = 0, tiles = 0;
+    Sweep sw{};
+    unsigned long long tests = 0, sweeps = 0, batches = 0;
 
     auto finish = [&](bool occluded) {
         if (!occluded) set_pair_bit(a.bits, s.words, pi, pj);
@@ -93,11 +102,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     };
     auto exact = [&](int k) {
         ++tests;
-        return seg_hits<MAXV>(s.rec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
+        return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
     };
     // Next sightline of the current pair. Sightlines a cached blocker already
     // blocks are settled on the spot (one exact test each); the first one the
-    // cache does not block starts a full cyclic sweep of nvt virtual tiles.
+    // cache does not block starts a culled sweep over every other face.
     auto advance = [&]() {
         for (;;) {
             if (++ord == S) {
@@ -105,15 +114,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                 return;
             }
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
-            if (bc0 >= 0 && bc0 != pi && bc0 != pj && exact(bc0)) continue;
-            if (bc1 >= 0 && bc1 != pi && bc1 != pj && exact(bc1)) {
+            if (bc0 >= 0 && bc0 != si && bc0 != sj && exact(bc0)) continue;
+            if (bc1 >= 0 && bc1 != si && bc1 != sj && exact(bc1)) {
                 const int t = bc0;
                 bc0 = bc1;
                 bc1 = t;
                 continue;
             }
-            g = make_segf(s, ax, ay, az, bx, by, bz);
-            rem = nvt;
+            sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
             ++sweeps;
             return;
         }
@@ -137,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                     } else {
                         pair_from_index(my, n, pi, pj);
                     }
+                    si = s.inv[pi];
+                    sj = s.inv[pj];
                     nr = s.nv[pi];
                     na = s.nv[pj];
                     grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
@@ -160,42 +170,44 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
-    auto vtile = [&](const float* B, int base, int cnt) {
-        if (!active) return;
-        ++tiles;
-        unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
-        int hk = -1;
-        while (mask) {
-            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-            mask &= mask - 1;
-            if (exact(base + kk)) {
-                hk = base + kk;
-                break;
-            }
-        }
-        if (hk >= 0) {
-            if (hk != bc0) {
-                bc1 = bc0;
-                bc0 = hk;
-            }
-            advance();
-        } else if (--rem == 0) {
-            finish(false);   // a sightline clear of every occluder
-        }
-    };
-    auto busy = [&]() { return active || !exhausted; };
 
     refill();
-    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
+    for (;;) {
+        if (active) {
+            ++batches;
+            int base;
+            unsigned long long mask = sweep_batch(sw, ctx, base);
+            int hk = -1;
+            while (mask) {
+                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+                mask &= mask - 1;
+                if (exact(base + kk)) {
+                    hk = base + kk;
+                    break;
+                }
+            }
+            if (hk >= 0) {
+                if (hk != bc0) {
+                    bc1 = bc0;
+                    bc0 = hk;
+                }
+                advance();
+            } else if (sw.done()) {
+                finish(false);   // a sightline clear of every occluder
+            }
+        }
+        refill();
+        if (!__any_sync(kFull, active || !exhausted)) break;
+    }
     for (int o = 16; o > 0; o >>= 1) {
         tests += __shfl_down_sync(kFull, tests, o);
         sweeps += __shfl_down_sync(kFull, sweeps, o);
-        tiles += __shfl_down_sync(kFull, tiles, o);
+        batches += __shfl_down_sync(kFull, batches, o);
     }
     if (lane == 0) {
         atomicAdd(&a.counter[1], tests);
         atomicAdd(&a.counter[2], sweeps);
-        atomicAdd(&a.counter[3], tiles);
+        atomicAdd(&a.counter[3], batches);
     }
 }
 
@@ -204,21 +216,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    extern __shared__ __align__(128) float sbox[];
-    __shared__ __align__(8) uint64_t bar[2];
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
     const DevScene& s = a.s;
-    const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const int nvt = (n + kTile - 1) / kTile;
-    BoxStream bs{sbox, bar, s.box, n, (n + kStreamTile - 1) / kStreamTile, 0};
-    bs.t0 = blockIdx.x % bs.ntiles;
-    sweep_init<RESIDENT>(bs);
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
 
     bool active = false, exhausted = false, hit_any = false;
     long long pidx = 0;
-    int pi = 0, pj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, rem = 0, blocked = 0;
+    int pi = 0, pj = 0, si = 0, sj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0, blocked = 0;
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
-    SegF g{};
+    Sweep sw{};
     unsigned long long tests = 0;
     uint32_t* mask_out = nullptr;
 
@@ -227,8 +235,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
         while (ord < S) {
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
             if (!degenerate(ax, ay, az, bx, by, bz)) {
-                g = make_segf(s, ax, ay, az, bx, by, bz);
-                rem = nvt;
+                sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
                 hit_any = false;
                 return;
             }
@@ -252,6 +259,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
                     pidx = my;
                     pi = a.ci[my];
                     pj = a.cj[my];
+                    si = s.inv[pi];
+                    sj = s.inv[pj];
                     nr = s.nv[pi];
                     na = s.nv[pj];
                     grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
@@ -266,29 +275,31 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_detail(PairArgs a) {
             need = __ballot_sync(kFull, !active && !exhausted);
         }
     };
-    auto vtile = [&](const float* B, int base, int cnt) {
-        if (!active) return;
-        unsigned long long mask = tile_survivors(B, cnt, base, g, pi, pj);
-        while (mask) {
-            const int kk = __ffsll(static_cast<long long>(mask)) - 1;
-            mask &= mask - 1;
-            ++tests;
-            if (seg_hits<MAXV>(s.rec + static_cast<size_t>(base + kk) * STRIDE, ax, ay, az, bx, by, bz)) {
-                hit_any = true;
-                const int k = base + kk;
-                atomicOr(mask_out + (k >> 5), 1u << (k & 31));
-            }
-        }
-        if (--rem == 0) {
-            if (hit_any) ++blocked;
-            ++ord;
-            next_sightline();
-        }
-    };
-    auto busy = [&]() { return active || !exhausted; };
 
     refill();
-    sweep_loop<RESIDENT>(bs, vtile, busy, refill);
+    for (;;) {
+        if (active) {
+            int base;
+            unsigned long long mask = sweep_batch(sw, ctx, base);
+            while (mask) {
+                const int kk = __ffsll(static_cast<long long>(mask)) - 1;
+                mask &= mask - 1;
+                ++tests;
+                if (seg_hits<MAXV>(s.srec + static_cast<size_t>(base + kk) * STRIDE, ax, ay, az, bx, by, bz)) {
+                    hit_any = true;
+                    const int k = s.perm[base + kk];
+                    atomicOr(mask_out + (k >> 5), 1u << (k & 31));
+                }
+            }
+            if (sw.done()) {
+                if (hit_any) ++blocked;
+                ++ord;
+                next_sightline();
+            }
+        }
+        refill();
+        if (!__any_sync(kFull, active || !exhausted)) break;
+    }
     for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
     if (lane == 0) atomicAdd(&a.counter[1], tests);
 }
@@ -364,8 +375,8 @@ static cudaError_t launch_persistent(K fn, size_t smem, const PairArgs& a, int d
     return cudaGetLastError();
 }
 
-// VISRT_FORCE_STREAM=1 forces the streamed-tile path (tests cover both paths
-// on small scenes).
+// VISRT_FORCE_STREAM=1 keeps the member boxes in global memory (L1/L2) even
+// when they fit in shared memory (tests cover both paths on small scenes).
 static bool use_resident(int n) {
     static const bool force_stream = [] {
         const char* e = std::getenv("VISRT_FORCE_STREAM");
@@ -374,14 +385,12 @@ static bool use_resident(int n) {
     return !force_stream && n <= kResidentMaxBoxes;
 }
 
-static size_t sweep_smem(int n, bool resident) {
-    return resident ? ((static_cast<size_t>(n) * 32 + 127) / 128) * 128 : 2ull * kStreamTile * 32;
-}
+static size_t sweep_smem(const DevScene& s, bool resident) { return sweep_smem_bytes(s.n, s.ntiles, resident); }
 
 template <int MAXV>
 static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
     const bool res = use_resident(a.s.n);
-    const size_t smem = sweep_smem(a.s.n, res);
+    const size_t smem = sweep_smem(a.s, res);
     return res ? launch_persistent(k_pair_bits<MAXV, true>, smem, a, device, st)
                : launch_persistent(k_pair_bits<MAXV, false>, smem, a, device, st);
 }
@@ -389,7 +398,7 @@ static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st)
 template <int MAXV>
 static cudaError_t launch_detail_t(const PairArgs& a, int device, cudaStream_t st) {
     const bool res = use_resident(a.s.n);
-    const size_t smem = sweep_smem(a.s.n, res);
+    const size_t smem = sweep_smem(a.s, res);
     return res ? launch_persistent(k_pair_detail<MAXV, true>, smem, a, device, st)
                : launch_persistent(k_pair_detail<MAXV, false>, smem, a, device, st);
 }
