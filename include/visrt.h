@@ -118,6 +118,30 @@ typedef struct {
 int visrt_point_regions(visrt_scene* scene, int64_t nsrc, const double* src_xyz,
                         visrt_region* out, visrt_stats* stats, void* stream);
 
+/* (2) Per-snapshot point tables (point_vis_table rows, src/vistable.cpp:478-521)
+ * for a list of matrix entries of order 1 or 2: entry e = (order, chain[0..2],
+ * plane) with chain = reflectors..., aim. For every (source k, entry e) the
+ * kernels decide whether TableBuilder::reach(reflectors) succeeds (the row
+ * exists) and whether the beam is Full in the entry's plane, from the GPU
+ * regions (illuminated_region) and the exact beam cascade (beam_coverage,
+ * src/vistable.cpp:225-272, 432-467). Output bitsets row_bits/full_bits:
+ * [nsrc][ceil(nent/32)] uint32 (bit e of source k). regions_out (optional):
+ * the regions as visrt_point_regions would return them. */
+typedef struct {
+    int32_t order;        /* 1 or 2 */
+    int32_t chain[3];     /* reflectors..., aim (order 1: chain[0], chain[1]) */
+    int32_t plane;        /* the entry's working plane (PlaneTag) */
+} visrt_entry;
+int visrt_point_tables(visrt_scene* scene, int64_t nsrc, const double* src_xyz, int64_t nent,
+                       const visrt_entry* entries, uint32_t* row_bits, uint32_t* full_bits,
+                       visrt_region* regions_out, visrt_stats* stats, void* stream);
+
+/* Batched sightline_clear (src/vistable.cpp:38-44 with skip = -1, i.e.
+ * Occluder::clear semantics): clear[k] = no face blocks the open segment
+ * a[k] -> b[k]. */
+int visrt_segments_clear(visrt_scene* scene, int64_t nseg, const double* a_xyz, const double* b_xyz,
+                         uint8_t* clear, visrt_stats* stats, void* stream);
+
 /* Order-2 chains of build_matrix(scene, 2) (src/vismatrix.cpp:715-797): every
  * triple p->t->a of admitted pairs that passes chain_triple_feasible and
  * second_order_check in each shared working plane. admitted_bits NULL = the

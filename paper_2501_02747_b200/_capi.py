@@ -27,7 +27,8 @@ EXPORTS = [
     "visrt_last_error", "visrt_version", "visrt_scene_create", "visrt_scene_destroy",
     "visrt_scene_nfaces", "visrt_scene_ingest", "visrt_scene_upload_bytes", "visrt_measure_peaks",
     "visrt_pair_visibility", "visrt_matrix_bits_device",
-    "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_chain_triples", "visrt_tracer_create",
+    "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_point_tables", "visrt_segments_clear",
+    "visrt_chain_triples", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results",
 ]
 
@@ -117,6 +118,10 @@ def lib():
                                     C.c_int64, C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_point_regions.argtypes = [C.c_void_p, C.c_int64, _f64p, C.POINTER(visrt_region),
                                       C.POINTER(visrt_stats), C.c_void_p]
+    L.visrt_point_tables.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.POINTER(visrt_stats), C.c_void_p]
+    L.visrt_segments_clear.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_void_p, C.POINTER(visrt_stats),
+                                       C.c_void_p]
     L.visrt_chain_triples.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                       C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_tracer_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,

@@ -140,6 +140,68 @@ def point_regions(scene: Scene, src: np.ndarray) -> List[List[dict]]:
              for r in row] for row in arr]
 
 
+ENTRY_DTYPE = np.dtype([("order", np.int32), ("chain", np.int32, 3), ("plane", np.int32)])
+
+
+def point_tables(scene: Scene, src: np.ndarray, entries: np.ndarray, want_regions: bool = False):
+    """For every (source k, matrix entry e) of order 1/2: does TableBuilder::reach
+    succeed (row of point_vis_table) and is the beam Full in the entry's
+    plane — GPU regions + beam cascade in one batched call. Returns
+    (rows[nsrc, nent] bool, full[nsrc, nent] bool, regions or None, stats)."""
+    src = np.ascontiguousarray(np.asarray(src, np.float64).reshape(-1, 3))
+    ent = np.ascontiguousarray(entries, ENTRY_DTYPE)
+    nsrc, nent = len(src), len(ent)
+    words = (nent + 31) // 32
+    rows = np.zeros((nsrc, max(words, 1)), np.uint32)
+    full = np.zeros((nsrc, max(words, 1)), np.uint32)
+    regs = np.zeros((nsrc, scene.n), REGION_DTYPE) if want_regions else None
+    st = _capi.visrt_stats()
+    check(lib().visrt_point_tables(scene.h, nsrc, src.reshape(-1), nent, ent.ctypes.data, rows.ctypes.data,
+                                   full.ctypes.data, None if regs is None else regs.ctypes.data, C.byref(st), None))
+    unpack = lambda b: np.unpackbits(b.view(np.uint8), axis=1, bitorder="little")[:, :nent].astype(bool)
+    return unpack(rows), unpack(full), regs, _stats_dict(st)
+
+
+def segments_clear(scene: Scene, a: np.ndarray, b: np.ndarray):
+    """Batched sightline_clear(a, b, skip=-1) on the GPU."""
+    a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1, 3))
+    b = np.ascontiguousarray(np.asarray(b, np.float64).reshape(-1, 3))
+    out = np.zeros(len(a), np.uint8)
+    st = _capi.visrt_stats()
+    check(lib().visrt_segments_clear(scene.h, len(a), a.reshape(-1), b.reshape(-1), out.ctypes.data, C.byref(st),
+                                     None))
+    return out.astype(bool), _stats_dict(st)
+
+
+def point_vis_table(scene: Scene, src, entries: np.ndarray, ids: Sequence[str], labels=None):
+    """rt::point_vis_table rows (src/vistable.cpp:478-521) for one source and
+    the given matrix entries: (order, chain ids, aim id, plane, verdict,
+    ref_display, aim_display), sorted like the reference."""
+    rows, full, regs, _ = point_tables(scene, np.asarray(src).reshape(1, 3), entries, want_regions=True)
+    reg = regs[0]
+
+    def display(f, plane):
+        name = ids[f] if labels is None else (labels[f][0] if plane == 0 else labels[f][1]) or ids[f]
+        r = reg[f]
+        if r["present"] == 1 and r["has"][plane] and r["clipped"][plane]:
+            name += "'"
+        return name
+
+    out = []
+    for e, ok in enumerate(rows[0]):
+        if not ok:
+            continue
+        E = entries[e]
+        refl = [int(x) for x in E["chain"][: E["order"]]]
+        aim = int(E["chain"][E["order"]])
+        pl = int(E["plane"])
+        out.append({"order": int(E["order"]), "chain": [ids[f] for f in refl], "aim": ids[aim], "plane": pl,
+                    "verdict": "Full" if full[0, e] else "Partial", "ref_display": display(refl[-1], pl),
+                    "aim_display": display(aim, pl)})
+    out.sort(key=lambda r: (r["order"], r["chain"], r["aim"], r["plane"]))
+    return out
+
+
 def chain_triples(scene: Scene, admitted_bits: Optional[np.ndarray] = None):
     """Order-2 chains (p, t, a) of build_matrix(scene, 2) computed on the GPU
     (chain_triple_feasible + second_order_check per shared plane), sorted."""

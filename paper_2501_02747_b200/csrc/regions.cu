@@ -428,6 +428,221 @@ cudaError_t launch_point_regions(const RegionArgs& a, int device, cudaStream_t s
     return a.s.maxv <= 4 ? launch_regions_t<4>(a, device, st) : launch_regions_t<8>(a, device, st);
 }
 
+// ---------------------------------------------------------------------------
+// K5: TableBuilder::reach for matrix entries of order 1 / 2 (beam cascade).
+// ---------------------------------------------------------------------------
+
+struct BeamArgs {
+    DevScene s;
+    long long nsrc, nent;
+    const double* src;
+    const visrt_region* regions;   // [nsrc][n]
+    const visrt_entry* ent;
+    uint32_t* row_bits;            // [nsrc][words]
+    uint32_t* full_bits;
+    int32_t words;
+};
+
+struct Cov {
+    int verdict;                   // 0 Full, 1 Partial, 2 None
+    double lo, hi;
+};
+
+// beam_coverage, src/vistable.cpp:225-272 (apex, window [wa, wb], outward; target qa->qb)
+__device__ Cov beam_coverage(double apx, double apy, double wax, double way, double wbx, double wby, double ox,
+                             double oy, double qax, double qay, double qbx, double qby) {
+    Cov r{2, 0.0, 0.0};
+    const double eax = dsub(wax, apx), eay = dsub(way, apy);
+    const double ebx = dsub(wbx, apx), eby = dsub(wby, apy);
+    const double inner = dsub(dmul(eax, eby), dmul(eay, ebx));
+    const double scale = dmul(__dsqrt_rn(dadd(dmul(eax, eax), dmul(eay, eay))),
+                              __dsqrt_rn(dadd(dmul(ebx, ebx), dmul(eby, eby))));
+    const double smax1 = scale < 1.0 ? 1.0 : scale;   // std::max(scale, 1.0)
+    if (fabs(inner) <= dmul(1e-14, smax1)) return r;
+    const double sgn = inner > 0.0 ? 1.0 : -1.0;
+    double lo = 0.0, hi = 1.0;
+    auto apply = [&](double c0, double c1) {
+        if (fabs(c1) <= dmul(1e-15, dadd(fabs(c0), 1.0))) {
+            if (c0 < 0.0) {
+                lo = 1.0;
+                hi = 0.0;
+            }
+            return;
+        }
+        const double t = __ddiv_rn(-c0, c1);
+        if (c1 > 0.0) lo = (lo < t) ? t : lo;     // std::max(lo, t)
+        else hi = (t < hi) ? t : hi;              // std::min(hi, t)
+    };
+    const double dqx = dsub(qbx, qax), dqy = dsub(qby, qay);
+    apply(dadd(dmul(dsub(qax, wax), ox), dmul(dsub(qay, way), oy)), dadd(dmul(dqx, ox), dmul(dqy, oy)));
+    const double rax = dsub(qax, apx), ray = dsub(qay, apy);
+    apply(dmul(sgn, dsub(dmul(eax, ray), dmul(eay, rax))), dmul(sgn, dsub(dmul(eax, dqy), dmul(eay, dqx))));
+    apply(dmul(-sgn, dsub(dmul(ebx, ray), dmul(eby, rax))), dmul(-sgn, dsub(dmul(ebx, dqy), dmul(eby, dqx))));
+    if (dsub(hi, lo) <= 1e-12) return r;
+    r.lo = lo;
+    r.hi = hi;
+    if (lo <= 1e-9 && hi >= 1.0 - 1e-9) {
+        r.verdict = 0;
+        r.lo = 0.0;
+        r.hi = 1.0;
+    } else {
+        r.verdict = 1;
+    }
+    return r;
+}
+
+__device__ __forceinline__ void proj(int pl, double x, double y, double z, double& u, double& v) {
+    if (pl == 0) { u = x; v = y; }
+    else if (pl == 1) { u = y; v = z; }
+    else { u = x; v = z; }
+}
+
+__global__ void __launch_bounds__(256) k_beam_rows(BeamArgs a) {
+    const DevScene& s = a.s;
+    const long long total = a.nsrc * a.nent;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long k = t / a.nent;
+        const int e = static_cast<int>(t - k * a.nent);
+        const visrt_entry E = a.ent[e];
+        const int head = E.chain[0];
+        const visrt_region& R = a.regions[static_cast<size_t>(k) * s.n + head];
+        bool row = false, full = false;
+        if (R.present == 1) {
+            if (E.order == 1) {
+                row = true;   // reach({head}) = region(head)
+                full = R.has[E.plane] && !R.clipped[E.plane];
+            } else {
+                // step(reach({head}), head, mid), src/vistable.cpp:432-467
+                const int mid = E.chain[1];
+                const double* P = s.pts + static_cast<size_t>(head) * VISRT_MAX_VERTS * 3;
+                const double* N = s.normal + 3 * static_cast<size_t>(head);
+                const double sx = a.src[3 * k], sy = a.src[3 * k + 1], sz = a.src[3 * k + 2];
+                const double d2 = dmul(2.0, dot_rel(sx, sy, sz, P[0], P[1], P[2], N[0], N[1], N[2]));
+                const double ix = dsub(sx, dmul(N[0], d2)), iy = dsub(sy, dmul(N[1], d2)),
+                             iz = dsub(sz, dmul(N[2], d2));   // mirror_point
+                bool any = false, ok = true, full_pl = false, has_pl = false;
+                for (int pl = 0; pl < 3 && ok; ++pl) {
+                    if (!s.seg_ok[3 * head + pl] || !s.seg_ok[3 * mid + pl]) continue;
+                    const double* fs = s.seg + (static_cast<size_t>(head) * 3 + pl) * 6;
+                    const double* gs = s.seg + (static_cast<size_t>(mid) * 3 + pl) * 6;
+                    const double dd = fabs(dadd(dmul(fs[4], gs[4]), dmul(fs[5], gs[5])));
+                    if (!(dd >= 1.0 - 1e-9 || dd <= 1e-9)) continue;   // required_planes(f, g)
+                    double w0x, w0y, w1x, w1y;
+                    bool was_full = true;
+                    if (R.has[pl]) {
+                        const double dx = dsub(fs[2], fs[0]), dy = dsub(fs[3], fs[1]);
+                        w0x = dadd(fs[0], dmul(dx, R.sub[2 * pl]));
+                        w0y = dadd(fs[1], dmul(dy, R.sub[2 * pl]));
+                        w1x = dadd(fs[0], dmul(dx, R.sub[2 * pl + 1]));
+                        w1y = dadd(fs[1], dmul(dy, R.sub[2 * pl + 1]));
+                        was_full = !R.clipped[pl];
+                    } else {
+                        w0x = fs[0];
+                        w0y = fs[1];
+                        w1x = fs[2];
+                        w1y = fs[3];
+                    }
+                    double apx, apy;
+                    proj(pl, ix, iy, iz, apx, apy);
+                    const Cov c = beam_coverage(apx, apy, w0x, w0y, w1x, w1y, fs[4], fs[5], gs[0], gs[1], gs[2], gs[3]);
+                    if (c.verdict == 2) {
+                        ok = false;
+                        break;
+                    }
+                    any = true;
+                    if (pl == E.plane) {
+                        has_pl = true;
+                        full_pl = was_full && c.verdict == 0;
+                    }
+                }
+                row = ok && any;
+                full = row && has_pl && full_pl;
+            }
+        }
+        const size_t w = static_cast<size_t>(k) * a.words + (e >> 5);
+        if (row) atomicOr(a.row_bits + w, 1u << (e & 31));
+        if (full) atomicOr(a.full_bits + w, 1u << (e & 31));
+    }
+}
+
+// Batched sightline_clear: lane per segment, culled any-hit sweep, no face skipped.
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 3) k_segments_clear(DevScene s, long long nseg, const double* A,
+                                                                const double* B, uint8_t* clear,
+                                                                unsigned long long* counter) {
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
+    __shared__ int slots[kThreads];
+    const int lane = threadIdx.x & 31;
+    int* slot = slots + (threadIdx.x & ~31);
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    bool active = false, exhausted = false;
+    long long id = 0;
+    double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
+    Sweep sw{};
+    unsigned long long tests = 0;
+    auto refill = [&]() {
+        unsigned need = __ballot_sync(kFull, !active && !exhausted);
+        while (need) {
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&counter[0], static_cast<unsigned long long>(__popc(need)));
+            base = __shfl_sync(kFull, base, leader);
+            if (!active && !exhausted) {
+                const long long my = static_cast<long long>(base) + __popc(need & ((1u << lane) - 1u));
+                if (my >= nseg) {
+                    exhausted = true;
+                } else {
+                    id = my;
+                    ax = A[3 * my]; ay = A[3 * my + 1]; az = A[3 * my + 2];
+                    bx = B[3 * my]; by = B[3 * my + 1]; bz = B[3 * my + 2];
+                    sw.start(make_segf(s, ax, ay, az, bx, by, bz), -1, -1, 0, ctx.nchunks);
+                    active = true;
+                }
+            }
+            need = __ballot_sync(kFull, !active && !exhausted);
+        }
+    };
+    refill();
+    for (;;) {
+        unsigned long long mask = 0;
+        int base = 0;
+        if (active) mask = sweep_batch(sw, ctx, base);
+        const int hk = coop_exact<MAXV>(s.srec, mask, base, ax, ay, az, bx, by, bz, slot, tests, 0ull,
+                                        [](int, unsigned long long) {});
+        if (active) {
+            if (hk >= 0) {
+                clear[id] = 0;
+                active = false;
+            } else if (sw.done()) {
+                clear[id] = 1;
+                active = false;
+            }
+        }
+        refill();
+        if (!__any_sync(kFull, active || !exhausted)) break;
+    }
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) atomicAdd(&counter[1], tests);
+}
+
+template <int MAXV>
+static cudaError_t launch_segments_t(const DevScene& s, long long nseg, const double* A, const double* B,
+                                     uint8_t* clear, unsigned long long* ctr, int device, cudaStream_t st) {
+    const char* e = std::getenv("VISRT_FORCE_STREAM");
+    const bool res = !(e && e[0] == '1') && s.n <= kResidentMaxBoxes;
+    const size_t smem = sweep_smem_bytes(s.n, s.ntiles, res);
+    auto go = [&](auto fn) {
+        cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (err != cudaSuccess) return err;
+        fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device), kThreads, smem, st>>>(s, nseg, A, B,
+                                                                                                       clear, ctr);
+        return cudaGetLastError();
+    };
+    return res ? go(k_segments_clear<MAXV, true>) : go(k_segments_clear<MAXV, false>);
+}
+
 }  // namespace visrt
 
 // ---------------------------------------------------------------------------
@@ -470,6 +685,114 @@ extern "C" int visrt_point_regions(visrt_scene* sc, int64_t nsrc, const double* 
             stats->candidates = static_cast<int64_t>(ctr[2]);   // sightline queries
             stats->admitted = -1;
             stats->tests_alg = 0;
+            stats->tests_exec = static_cast<int64_t>(ctr[1]);
+            stats->ms = ms;
+        }
+    });
+}
+
+extern "C" int visrt_point_tables(visrt_scene* sc, int64_t nsrc, const double* src_xyz, int64_t nent,
+                                  const visrt_entry* entries, uint32_t* row_bits, uint32_t* full_bits,
+                                  visrt_region* regions_out, visrt_stats* stats, void* stream) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const visrt::DevScene& ds = visrt::scene_dev(sc);
+        for (int64_t e = 0; e < nent; ++e) {
+            if (entries[e].order < 1 || entries[e].order > 2)
+                throw visrt::UsageError("point tables cover matrix entries of order 1 and 2");
+            for (int c = 0; c <= entries[e].order; ++c)
+                if (entries[e].chain[c] < 0 || entries[e].chain[c] >= ds.n) throw visrt::UsageError("bad face index");
+            if (entries[e].plane < 0 || entries[e].plane > 2) throw visrt::UsageError("bad plane tag");
+        }
+        const long long ntasks = static_cast<long long>(nsrc) * ds.n;
+        const int words = static_cast<int>((nent + 31) / 32);
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        double* d_src = visrt::dalloc<double>(static_cast<size_t>(nsrc) * 3, tmp);
+        visrt_region* d_reg = visrt::dalloc<visrt_region>(static_cast<size_t>(ntasks), tmp);
+        visrt_entry* d_ent = visrt::dalloc<visrt_entry>(static_cast<size_t>(nent), tmp);
+        uint32_t* d_rows = visrt::dalloc<uint32_t>(static_cast<size_t>(nsrc) * words, tmp);
+        uint32_t* d_full = visrt::dalloc<uint32_t>(static_cast<size_t>(nsrc) * words, tmp);
+        unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(4, tmp);
+        visrt::ck(cudaMemcpyAsync(d_src, src_xyz, nsrc * 3 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        if (nent) visrt::ck(cudaMemcpyAsync(d_ent, entries, nent * sizeof(visrt_entry), cudaMemcpyHostToDevice, st), "H2D");
+        visrt::ck(cudaMemsetAsync(d_rows, 0, static_cast<size_t>(nsrc) * words * 4, st), "memset");
+        visrt::ck(cudaMemsetAsync(d_full, 0, static_cast<size_t>(nsrc) * words * 4, st), "memset");
+        visrt::ck(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(unsigned long long), st), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        visrt::RegionArgs ra{ds, ntasks, d_src, d_reg, d_ctr};
+        if (ntasks > 0) visrt::ck(visrt::launch_point_regions(ra, visrt::scene_device(sc), st), "k_point_regions");
+        visrt::BeamArgs ba{ds, nsrc, nent, d_src, d_reg, d_ent, d_rows, d_full, words};
+        if (nsrc * nent > 0) {
+            const long long work = nsrc * nent;
+            const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 148 * 32));
+            visrt::k_beam_rows<<<blocks, 256, 0, st>>>(ba);
+            visrt::ck(cudaGetLastError(), "k_beam_rows");
+        }
+        cudaEventRecord(e1, st);
+        if (nsrc * words > 0) {
+            visrt::ck(cudaMemcpyAsync(row_bits, d_rows, static_cast<size_t>(nsrc) * words * 4, cudaMemcpyDeviceToHost, st), "D2H");
+            visrt::ck(cudaMemcpyAsync(full_bits, d_full, static_cast<size_t>(nsrc) * words * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        if (regions_out && ntasks > 0)
+            visrt::ck(cudaMemcpyAsync(regions_out, d_reg, ntasks * sizeof(visrt_region), cudaMemcpyDeviceToHost, st), "D2H");
+        unsigned long long ctr[4] = {0, 0, 0, 0};
+        visrt::ck(cudaMemcpyAsync(ctr, d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st), "D2H");
+        visrt::ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (stats) {
+            *stats = visrt_stats{};
+            stats->pairs = ntasks;
+            stats->candidates = static_cast<int64_t>(ctr[2]);
+            stats->admitted = nsrc * nent;
+            stats->tests_exec = static_cast<int64_t>(ctr[1]);
+            stats->ms = ms;
+        }
+    });
+}
+
+extern "C" int visrt_segments_clear(visrt_scene* sc, int64_t nseg, const double* a_xyz, const double* b_xyz,
+                                    uint8_t* clear, visrt_stats* stats, void* stream) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const visrt::DevScene& ds = visrt::scene_dev(sc);
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        double* dA = visrt::dalloc<double>(static_cast<size_t>(nseg) * 3, tmp);
+        double* dB = visrt::dalloc<double>(static_cast<size_t>(nseg) * 3, tmp);
+        uint8_t* dC = visrt::dalloc<uint8_t>(static_cast<size_t>(nseg), tmp);
+        unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(2, tmp);
+        visrt::ck(cudaMemcpyAsync(dA, a_xyz, nseg * 24, cudaMemcpyHostToDevice, st), "H2D");
+        visrt::ck(cudaMemcpyAsync(dB, b_xyz, nseg * 24, cudaMemcpyHostToDevice, st), "H2D");
+        visrt::ck(cudaMemsetAsync(d_ctr, 0, 16, st), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        if (nseg > 0) {
+            if (ds.maxv <= 4) visrt::ck(visrt::launch_segments_t<4>(ds, nseg, dA, dB, dC, d_ctr, visrt::scene_device(sc), st), "k_segments_clear");
+            else visrt::ck(visrt::launch_segments_t<8>(ds, nseg, dA, dB, dC, d_ctr, visrt::scene_device(sc), st), "k_segments_clear");
+        }
+        cudaEventRecord(e1, st);
+        if (nseg > 0) visrt::ck(cudaMemcpyAsync(clear, dC, nseg, cudaMemcpyDeviceToHost, st), "D2H");
+        unsigned long long ctr[2] = {0, 0};
+        visrt::ck(cudaMemcpyAsync(ctr, d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st), "D2H");
+        visrt::ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (stats) {
+            *stats = visrt_stats{};
+            stats->pairs = nseg;
             stats->tests_exec = static_cast<int64_t>(ctr[1]);
             stats->ms = ms;
         }
