@@ -156,6 +156,55 @@ def cpu_baseline(soup, seconds: float = 10.0):
                       f"threads ({el:.1f} s)"}
 
 
+def secondary_measurements(stream: int):
+    """The other hot-path subsystems, timed with the library's CUDA events on
+    the same stream (outside the headline's timed region, rank 0, N = 1)."""
+    from paper_2501_02747_b200 import scenes
+    from paper_2501_02747_b200.core import Scene, Tracer, chain_triples, point_regions_array
+    out = {}
+    # (1) the other matrix configurations
+    for cfg in (1, 3):
+        with Scene(scenes.workload(cfg).scene) as sc:
+            sc.pair_visibility("all", copy_bits=False, stream=stream)
+            _, st = sc.pair_visibility("all", copy_bits=False, stream=stream)
+            _, sa = sc.pair_visibility("prefiltered", copy_bits=False, stream=stream)
+            out[f"matrix_config{cfg}"] = {"B_ms": st["ms"], "B_tests_per_s": st["tests_alg"] / (st["ms"] * 1e-3),
+                                          "A_ms": sa["ms"], "A_candidates": sa["candidates"],
+                                          "facets": sc.n}
+    # (2) per-snapshot Tx/Rx -> facet regions, config 3 (Tx and Rx snapshots)
+    wl = scenes.workload(3)
+    with Scene(wl.scene) as sc:
+        src = np.concatenate([wl.tx[::10], wl.rx[::10]])
+        point_regions_array(sc, src[:8])
+        arr, st = point_regions_array(sc, src)
+        out["regions_config3"] = {"snapshots": len(src), "facets": sc.n, "ms": st["ms"],
+                                  "regions_per_s": arr.size / (st["ms"] * 1e-3),
+                                  "ms_per_snapshot": st["ms"] / len(src),
+                                  "sightlines": st["candidates"], "exact_tests": st["tests_exec"]}
+        # (3) order-2 chains + image tree order 3, config 3
+        sc.pair_visibility("prefiltered", copy_bits=False)
+        tri, sch = chain_triples(sc)
+        out["chains_config3"] = {"candidate_triples": sch["candidates"], "feasible": sch["admitted"],
+                                 "ms": sch["ms"]}
+        tr = Tracer(sc, 3, triples=tri)
+        tr.trace_raw(wl.tx[:4], wl.rx[:4])
+        _, _, nodes, tst = tr.trace_raw(wl.tx[:50], wl.rx[:50])
+        out["tree_config3_order3"] = {"snapshots": 50, "nodes": tst["nodes"], "ms": tst["ms"],
+                                      "nodes_per_s": tst["nodes"] / (tst["ms"] * 1e-3),
+                                      "ms_per_snapshot": tst["ms"] / 50, "paths": tst["paths"]}
+        tr.close()
+    wl1 = scenes.workload(1)
+    with Scene(wl1.scene) as sc:
+        sc.pair_visibility("prefiltered", copy_bits=False)
+        tr = Tracer(sc, 2)
+        tr.trace_raw(wl1.tx[:4], wl1.rx)
+        _, _, nodes, tst = tr.trace_raw(wl1.tx, wl1.rx)
+        out["tree_config1_order2"] = {"snapshots": len(wl1.tx), "nodes": tst["nodes"], "ms": tst["ms"],
+                                      "ms_per_snapshot": tst["ms"] / len(wl1.tx), "paths": tst["paths"]}
+        tr.close()
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -300,6 +349,11 @@ def run_visrt(args, rank, world):
             "clocks": clocks,
             "wall_s_timed_loop": wall,
         }
+        if world == 1 and not args.no_secondary:
+            try:
+                line["subsystems"] = secondary_measurements(sh)
+            except Exception as e:   # noqa: BLE001
+                line["subsystems"] = {"error": str(e)}
         if world == 1:
             try:
                 line["cpu_baseline"] = cpu_baseline(soup, seconds=args.cpu_seconds)
@@ -321,6 +375,7 @@ def main():
     ap.add_argument("--impl", default="visrt", choices=["visrt", "reference"])
     ap.add_argument("--mode", default="all", choices=["all", "prefiltered"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-secondary", action="store_true", help="skip the other subsystems' timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "visrt" else args.warmup
     rank = _env_int("RANK", 0)

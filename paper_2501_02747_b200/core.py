@@ -227,6 +227,9 @@ class Tracer:
                  triples: Optional[np.ndarray] = None) -> None:
         self.scene = scene
         self.max_refl = max_refl
+        if max_refl >= 3 and triples is None:
+            # the ChainFilter needs the order-2 chains: grow them on the GPU
+            triples, _ = chain_triples(scene, admitted_bits)
         bits = None if admitted_bits is None else np.ascontiguousarray(admitted_bits, np.uint64)
         tri = None if triples is None else np.ascontiguousarray(np.asarray(triples, np.int32).reshape(-1, 3))
         h = C.c_void_p()
