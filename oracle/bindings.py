@@ -52,24 +52,39 @@ class vo_path(C.Structure):
 _u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 
 
-def chain_filter_arrays(n: int, admitted: np.ndarray, triples=None):
-    """Chain filter in the oracle's layout: admitted[n, n] (uint8) and the
-    order-2 continuations as CSR over directed admitted pairs (row-major rank).
-    `triples`: iterable of (p, t, a) order-2 chains (None: order <= 2 only)."""
-    adm = np.ascontiguousarray(admitted.astype(np.uint8).reshape(n, n))
-    pi, pj = np.nonzero(adm)
-    rank = {(int(p), int(t)): r for r, (p, t) in enumerate(zip(pi, pj))}
-    lists = [[] for _ in range(len(pi))]
-    if triples is not None:
-        for p, t, a in triples:
-            lists[rank[(int(p), int(t))]].append(int(a))
-    off = np.zeros(len(pi) + 1, np.int64)
-    idx = []
-    for r, l in enumerate(lists):
-        l = sorted(set(l))
-        idx.extend(l)
-        off[r + 1] = off[r] + len(l)
-    return adm, off, np.asarray(idx if idx else [0], np.int32)
+def chain_filter_arrays(n: int, admitted, triples=None):
+    """Chain filter in the oracle's layout: the admitted aims as CSR (off1,
+    idx1 ascending per face) and the order-2 continuations as CSR over the
+    directed admitted pairs in the same order. `admitted`: [n, n] bool matrix
+    or an (i, j) pair list of directed admitted pairs; `triples`: (p, t, a)
+    order-2 chains (None: order <= 2 only)."""
+    if isinstance(admitted, np.ndarray) and admitted.ndim == 2 and admitted.shape == (n, n):
+        pi, pj = np.nonzero(admitted)
+    else:
+        pi, pj = (np.asarray(x) for x in admitted)
+        o = np.lexsort((pj, pi))
+        pi, pj = pi[o], pj[o]
+    pi = pi.astype(np.int64)
+    pj = pj.astype(np.int32)
+    off1 = np.zeros(n + 1, np.int64)
+    np.add.at(off1, pi + 1, 1)
+    off1 = np.cumsum(off1)
+    idx1 = np.ascontiguousarray(pj if len(pj) else np.zeros(1, np.int32), np.int32)
+    off2 = np.zeros(len(pj) + 1, np.int64)
+    idx2 = np.zeros(1, np.int32)
+    if triples is not None and len(triples):
+        t = np.asarray(triples, np.int64).reshape(-1, 3)
+        key = pi * n + pj
+        rank = np.searchsorted(key, t[:, 0] * n + t[:, 1])
+        o = np.lexsort((t[:, 2], rank))
+        rank, aim = rank[o], t[o, 2]
+        keep = np.ones(len(rank), bool)
+        keep[1:] = (rank[1:] != rank[:-1]) | (aim[1:] != aim[:-1])
+        rank, aim = rank[keep], aim[keep]
+        np.add.at(off2, rank + 1, 1)
+        off2 = np.cumsum(off2)
+        idx2 = np.ascontiguousarray(aim.astype(np.int32))
+    return (np.ascontiguousarray(off1), idx1, np.ascontiguousarray(off2), idx2)
 
 
 class Oracle:
@@ -97,8 +112,10 @@ class Oracle:
             L.vo_occlusion_batch.argtypes = [C.c_void_p, C.c_int64, _i32p, _i32p, _i8p, C.c_int32]
             L.vo_sightline_count.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
             L.vo_illuminated_region.argtypes = [C.c_void_p, _f64p, C.c_int32, C.POINTER(vo_region)]
+            L.vo_prefilter_all.restype = C.c_int64
+            L.vo_prefilter_all.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]
             L.vo_trace.restype = C.c_int64
-            L.vo_trace.argtypes = [C.c_void_p, _u8p, _i64p, _i32p, C.c_int32, _f64p, _f64p,
+            L.vo_trace.argtypes = [C.c_void_p, _i64p, _i32p, _i64p, _i32p, C.c_int32, _f64p, _f64p,
                                    C.POINTER(vo_path), C.c_int64, _i64p]
             cls._lib = L
         return cls._lib
@@ -136,6 +153,16 @@ class Oracle:
     def required_planes(self, i: int, j: int) -> int:
         return int(self.lib().vo_required_planes(self.h, i, j))
 
+    def prefilter_all(self, threads: int = 0):
+        """(i, j) of every pair passing first_order_pair's gate, in order."""
+        L = self.lib()
+        th = threads or os.cpu_count() or 1
+        m = L.vo_prefilter_all(self.h, None, None, 0, th)
+        pi = np.zeros(m, np.int32)
+        pj = np.zeros(m, np.int32)
+        L.vo_prefilter_all(self.h, pi.ctypes.data, pj.ctypes.data, m, th)
+        return pi, pj
+
     def occlusion(self, i: int, j: int):
         buf = np.zeros(max(self.n, 1), np.int32)
         nb = C.c_int32()
@@ -161,11 +188,11 @@ class Oracle:
         """TraceAccelerator::trace (no diffraction) with the chain filter
         `filt` = chain_filter_arrays(...). Returns (paths, stats) with paths
         as dicts {faces, points, length}; stats = nodes, sequences, paths."""
-        adm, off, idx = filt
+        off1, idx1, off2, idx2 = filt
         cap = 1 << 16
         out = (vo_path * cap)()
         st = np.zeros(3, np.int64)
-        n = self.lib().vo_trace(self.h, adm.reshape(-1), off, idx, max_refl,
+        n = self.lib().vo_trace(self.h, off1, idx1, off2, idx2, max_refl,
                                 np.ascontiguousarray(tx, np.float64), np.ascontiguousarray(rx, np.float64),
                                 out, cap, st)
         if n < 0:
@@ -238,6 +265,7 @@ class RefOracle:
             L.vref_mutually_front.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
             L.vref_required_planes.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
             L.vref_plane_segment.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _f64p]
+            L.vref_triple_feasible.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]
             L.vref_segment_hits_face.argtypes = [C.c_void_p, _f64p, _f64p, C.c_int32]
             L.vref_build_matrix.restype = C.c_void_p
             L.vref_build_matrix.argtypes = [C.c_void_p, C.c_int32]
@@ -328,6 +356,13 @@ class RefOracle:
 
     def mutually_front(self, i, j) -> bool:
         return bool(self.lib().vref_mutually_front(self.h, i, j))
+
+    def triple_feasible(self, p: int, t: int, a: int) -> bool:
+        """build_matrix's triple_ext feasibility through the reference's public functions."""
+        r = self.lib().vref_triple_feasible(self.h, p, t, a)
+        if r < 0:
+            raise RuntimeError(self.lib().vref_last_error().decode())
+        return bool(r)
 
     def required_planes(self, i, j) -> int:
         return int(self.lib().vref_required_planes(self.h, i, j))

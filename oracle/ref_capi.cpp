@@ -255,6 +255,42 @@ int32_t vref_required_planes(void* h, int32_t i, int32_t j) {
     return m;
 }
 
+// build_matrix's triple_ext feasibility (proj/src/vismatrix.cpp:715-751) for one
+// triple p -> t -> a of admitted pairs, through the reference's public
+// chain_triple_feasible / required_planes / second_order_check. The matrix
+// second_order_check consults only needs the two order-1 legs, so a minimal
+// one with those entries stands in for the full build.
+int32_t vref_triple_feasible(void* h, int32_t p, int32_t t, int32_t a) {
+    try {
+        const R::Scene& s = static_cast<RefScene*>(h)->scene;
+        const R::Face& fp = s.face(p);
+        const R::Face& ft = s.face(t);
+        const R::Face& fa = s.face(a);
+        if (!R::chain_triple_feasible(fp, ft, fa)) return 0;
+        R::InterVisMatrix m;
+        auto add_leg = [&](const R::Face& x, const R::Face& y) {
+            for (R::PlaneTag pl : R::required_planes(x, y)) {
+                R::InterVisEntry e;
+                e.order = 1;
+                e.ref = x.id;
+                e.aim = y.id;
+                e.relation.plane = pl;
+                e.relation.chain = {x.id, y.id};
+                m.add(e);
+            }
+        };
+        add_leg(fp, ft);
+        add_leg(ft, fa);
+        for (R::PlaneTag pl : R::required_planes(ft, fa)) {
+            if (!m.find(1, fp.id, ft.id, pl)) continue;
+            if (R::second_order_check(fp, ft, fa, m, pl).verdict == R::ChainVerdict::None) return 0;
+        }
+        return 1;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
+
 // plane_segment (proj/src/scene.cpp:213-254): returns 1 and a,b,normal (6 doubles) if present.
 int32_t vref_plane_segment(void* h, int32_t i, int32_t plane, double* out6) {
     const R::Scene& s = static_cast<RefScene*>(h)->scene;

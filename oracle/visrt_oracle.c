@@ -246,6 +246,68 @@ int32_t vo_prefilter(const vo_scene* s, int32_t i, int32_t j) {
     return vo_required_planes(s, i, j) != 0;
 }
 
+typedef struct {
+    const vo_scene* s;
+    int32_t next;
+    pthread_mutex_t mu;
+    int64_t* row_count;      /* per row i: number of j > i passing */
+    int32_t* out_i;
+    int32_t* out_j;
+    const int64_t* row_off;  /* fill pass: output offset of row i */
+} pf_ctx;
+
+static void* pf_worker(void* arg) {
+    pf_ctx* c = (pf_ctx*)arg;
+    const int32_t n = c->s->n;
+    for (;;) {
+        pthread_mutex_lock(&c->mu);
+        int32_t i = c->next++;
+        pthread_mutex_unlock(&c->mu);
+        if (i >= n) break;
+        int64_t k = c->row_off ? c->row_off[i] : 0, cnt = 0;
+        for (int32_t j = i + 1; j < n; ++j) {
+            if (!vo_prefilter(c->s, i, j)) continue;
+            if (c->row_off) {
+                c->out_i[k] = i;
+                c->out_j[k] = j;
+                ++k;
+            }
+            ++cnt;
+        }
+        c->row_count[i] = cnt;
+    }
+    return NULL;
+}
+
+int64_t vo_prefilter_all(const vo_scene* s, int32_t* out_i, int32_t* out_j, int64_t cap, int32_t threads) {
+    if (threads < 1) threads = 1;
+    pf_ctx c = {s, 0, PTHREAD_MUTEX_INITIALIZER, (int64_t*)calloc((size_t)s->n + 1, sizeof(int64_t)), NULL,
+                NULL, NULL};
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, pf_worker, &c);
+    pf_worker(&c);
+    for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+    int64_t total = 0;
+    int64_t* off = (int64_t*)calloc((size_t)s->n + 1, sizeof(int64_t));
+    for (int32_t i = 0; i < s->n; ++i) {
+        off[i] = total;
+        total += c.row_count[i];
+    }
+    if (out_i && total <= cap) {
+        c.next = 0;
+        c.row_off = off;
+        c.out_i = out_i;
+        c.out_j = out_j;
+        for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, pf_worker, &c);
+        pf_worker(&c);
+        for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+    }
+    free(off);
+    free(c.row_count);
+    free(th);
+    return total;
+}
+
 /* centroid, src/geom.cpp:142-146 */
 static v3 centroid(const vo_face* f) {
     v3 c = {0, 0, 0};
@@ -531,10 +593,10 @@ static int segment_clear(const vo_scene* s, v3 a, v3 b) {
 
 typedef struct {
     const vo_scene* s;
-    const uint8_t* adm;
-    const int64_t* c2_off;
+    const int64_t* off1;      /* admitted aims of face p: idx1[off1[p] .. off1[p+1]) ascending */
+    const int32_t* idx1;
+    const int64_t* c2_off;    /* order-2 continuations of the pair at rank r (position in idx1) */
     const int32_t* c2_idx;
-    const int64_t* row_off;   /* admitted pairs before row p */
     int max_refl;
     v3 tx, rx;
     vo_path* out;
@@ -591,10 +653,13 @@ static void resolve(trace_ctx* c, const int* faces, int nf) {
 }
 
 static int64_t pair_rank(const trace_ctx* c, int p, int t) {
-    const int32_t n = c->s->n;
-    int64_t r = c->row_off[p];
-    for (int j = 0; j < t; ++j) r += c->adm[(size_t)p * n + j] != 0;
-    return r;
+    int64_t lo = c->off1[p], hi = c->off1[p + 1];
+    while (lo < hi) {   /* lower_bound in the ascending aim list */
+        int64_t mid = (lo + hi) / 2;
+        if (c->idx1[mid] < t) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
 static void expand(trace_ctx* c, int* seq, int depth, v3 image) {
@@ -607,6 +672,9 @@ static void expand(trace_ctx* c, int* seq, int depth, v3 image) {
     int row = -1;
     if (depth == 1) {
         row = seq[0];
+        lo = c->off1[row];
+        hi = c->off1[row + 1];
+        list = c->idx1;
     } else if (depth == 2) {
         int64_t r = pair_rank(c, seq[0], seq[1]);
         lo = c->c2_off[r];
@@ -618,10 +686,7 @@ static void expand(trace_ctx* c, int* seq, int depth, v3 image) {
     for (int64_t q = lo; q < hi; ++q) {
         int idx;
         if (depth == 0) idx = (int)q;
-        else if (depth == 1) {
-            if (!c->adm[(size_t)row * n + q]) continue;
-            idx = (int)q;
-        } else idx = list[q];
+        else idx = list[q];
         if (depth > 0 && idx == seq[depth - 1]) continue;
         if (sdist(&s->f[idx], image) <= VO_EPS) continue;
         seq[depth] = idx;
@@ -631,13 +696,14 @@ static void expand(trace_ctx* c, int* seq, int depth, v3 image) {
     }
 }
 
-int64_t vo_trace(const vo_scene* s, const uint8_t* adm, const int64_t* c2_off, const int32_t* c2_idx,
-                 int32_t max_refl, const double* tx, const double* rx, vo_path* out, int64_t cap,
-                 int64_t* stats) {
+int64_t vo_trace(const vo_scene* s, const int64_t* off1, const int32_t* idx1, const int64_t* c2_off,
+                 const int32_t* c2_idx, int32_t max_refl, const double* tx, const double* rx, vo_path* out,
+                 int64_t cap, int64_t* stats) {
     trace_ctx c;
     memset(&c, 0, sizeof(c));
     c.s = s;
-    c.adm = adm;
+    c.off1 = off1;
+    c.idx1 = idx1;
     c.c2_off = c2_off;
     c.c2_idx = c2_idx;
     c.max_refl = max_refl;
@@ -646,17 +712,9 @@ int64_t vo_trace(const vo_scene* s, const uint8_t* adm, const int64_t* c2_off, c
     c.out = out;
     c.cap = cap;
     if (norm3(sub3(c.tx, c.rx)) <= VO_EPS) return -1;   /* PlacementError */
-    int64_t* row_off = (int64_t*)calloc((size_t)s->n + 1, sizeof(int64_t));
-    for (int32_t p = 0; p < s->n; ++p) {
-        int64_t cnt = 0;
-        for (int32_t j = 0; j < s->n; ++j) cnt += adm[(size_t)p * s->n + j] != 0;
-        row_off[p + 1] = row_off[p] + cnt;
-    }
-    c.row_off = row_off;
     int seq[4];
     resolve(&c, seq, 0);   /* line of sight */
     if (max_refl > 0) expand(&c, seq, 0, c.tx);
-    free(row_off);
     if (stats) {
         stats[0] = c.nodes;
         stats[1] = c.seqs;

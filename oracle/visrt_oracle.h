@@ -31,6 +31,9 @@ int32_t vo_segment_hits_face(const vo_scene* s, const double* a, const double* b
 int32_t vo_mutually_front(const vo_scene* s, int32_t i, int32_t j);
 int32_t vo_required_planes(const vo_scene* s, int32_t i, int32_t j);   /* bitmask XY|YZ|XZ */
 int32_t vo_prefilter(const vo_scene* s, int32_t i, int32_t j);         /* first_order_pair gate */
+/* All i<j passing the gate, in (i, j) order, on `threads` pthreads. Two-call
+ * sizing: out == NULL returns the count. */
+int64_t vo_prefilter_all(const vo_scene* s, int32_t* out_i, int32_t* out_j, int64_t cap, int32_t threads);
 
 /* occlusion_judgment: kind 0 Visible / 1 Partial / 2 Occluded. Blockers as a
  * sorted face-index list (the reference sorts ids as strings; callers map). */
@@ -54,9 +57,10 @@ int32_t vo_illuminated_region(const vo_scene* s, const double* src, int32_t face
 
 /* (3) TraceAccelerator::trace, allow_diffraction = false, for a soup scene
  * (no buildings, no edges, no oblique faces needed). Chain filter: order-1
- * continuations = admitted rows (adm[i*n + j] != 0), order-2 continuations =
- * CSR over directed admitted pairs in row-major order (c2_off[npairs+1],
- * c2_idx), i.e. the key (p, t) is the rank of (p, t) among admitted pairs.
+ * continuations = admitted aims as CSR (off1[n+1], idx1 ascending per row),
+ * order-2 continuations = CSR over the directed admitted pairs in the same
+ * order (c2_off[npairs+1], c2_idx): the key (p, t) is the position of t in
+ * p's aim list.
  * Paths: nrefl, faces[4], points[3*(nrefl+2)], length. Returns path count,
  * or -1 (PlacementError: tx ~ rx). stats: nodes, sequences, paths. */
 typedef struct {
@@ -65,9 +69,9 @@ typedef struct {
     double points[18];
     double length;
 } vo_path;
-int64_t vo_trace(const vo_scene* s, const uint8_t* adm, const int64_t* c2_off, const int32_t* c2_idx,
-                 int32_t max_refl, const double* tx, const double* rx, vo_path* out, int64_t cap,
-                 int64_t* stats);
+int64_t vo_trace(const vo_scene* s, const int64_t* off1, const int32_t* idx1, const int64_t* c2_off,
+                 const int32_t* c2_idx, int32_t max_refl, const double* tx, const double* rx, vo_path* out,
+                 int64_t cap, int64_t* stats);
 
 #ifdef __cplusplus
 }
