@@ -43,6 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = [NVCC, "-std=c++17", "-O3", "-lineinfo", "--fmad=false",
               "-gencode", "arch=compute_100a,code=sm_100a",
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", INCLUDE, "-I", CSRC]
+    common += os.environ.get("VISRT_NVCC_FLAGS", "").split()   # tuning experiments (-DVISRT_K2_MINB=2 ...)
     if verbose:
         common += ["-Xptxas", "-v"]
     objs = []

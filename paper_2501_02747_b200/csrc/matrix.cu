@@ -77,9 +77,17 @@ __device__ __forceinline__ bool may_touch(const DevScene& s, int i, int j) {
     return !sep;
 }
 
+#ifndef VISRT_K2_MINB
+#define VISRT_K2_MINB 3   // CTAs per SM the register budget targets (80 regs at 3)
+#endif
+#ifndef VISRT_K2_BC
+#define VISRT_K2_BC 2     // blocker-cache entries per lane
+#endif
+
 template <int MAXV, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
+__global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    constexpr int BC = VISRT_K2_BC;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
     const DevScene& s = a.s;
@@ -90,7 +98,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
     bool active = false, exhausted = false;
     long long pidx = 0;
     int pi = 0, pj = 0, si = 0, sj = 0, nr = 0, na = 0, grid = 0, S = 0, ord = 0;
-    int bc0 = -1, bc1 = -1;   // blocker cache (Morton indices of the last blockers)
+    int bc[BC];               // blocker cache (Morton indices of the last blockers, most recent first)
+#pragma unroll
+    for (int q = 0; q < BC; ++q) bc[q] = -1;
     double ax = 0, ay = 0, az = 0, bx = 0, by = 0, bz = 0;
     Sweep sw{};
     unsigned long long tests = 0, sweeps = 0, batches = 0;
@@ -114,11 +124,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                 return;
             }
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
-            if (bc0 >= 0 && bc0 != si && bc0 != sj && exact(bc0)) continue;
-            if (bc1 >= 0 && bc1 != si && bc1 != sj && exact(bc1)) {
-                const int t = bc0;
-                bc0 = bc1;
-                bc1 = t;
+            int hitc = -1;
+#pragma unroll
+            for (int q = 0; q < BC; ++q)
+                if (hitc < 0 && bc[q] >= 0 && bc[q] != si && bc[q] != sj && exact(bc[q])) hitc = q;
+            if (hitc >= 0) {
+#pragma unroll
+                for (int q = 1; q < BC; ++q)
+                    if (q == hitc) {   // move to front
+                        const int t = bc[0];
+                        bc[0] = bc[q];
+                        bc[q] = t;
+                    }
                 continue;
             }
             sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
@@ -187,9 +204,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_pair_bits(PairArgs a) {
                 }
             }
             if (hk >= 0) {
-                if (hk != bc0) {
-                    bc1 = bc0;
-                    bc0 = hk;
+                if (hk != bc[0]) {
+#pragma unroll
+                    for (int q = BC - 1; q > 0; --q) bc[q] = bc[q - 1];
+                    bc[0] = hk;
                 }
                 advance();
             } else if (sw.done()) {
