@@ -81,7 +81,7 @@ __device__ __forceinline__ bool may_touch(const DevScene& s, int i, int j) {
 #define VISRT_K2_MINB 3   // CTAs per SM the register budget targets (80 regs at 3)
 #endif
 #ifndef VISRT_K2_BC
-#define VISRT_K2_BC 2     // blocker-cache entries per lane
+#define VISRT_K2_BC 4     // blocker-cache entries per lane (4 measured best: r01 k2sweep)
 #endif
 
 template <int MAXV, bool RESIDENT>
@@ -124,10 +124,13 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
                 return;
             }
             sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz);
+            const SegF g = make_segf(s, ax, ay, az, bx, by, bz);
             int hitc = -1;
 #pragma unroll
             for (int q = 0; q < BC; ++q)
-                if (hitc < 0 && bc[q] >= 0 && bc[q] != si && bc[q] != sj && exact(bc[q])) hitc = q;
+                if (hitc < 0 && bc[q] >= 0 && bc[q] != si && bc[q] != sj &&
+                    sat_maybe(ctx.mbox + static_cast<size_t>(bc[q]) * 8, g) && exact(bc[q]))
+                    hitc = q;
             if (hitc >= 0) {
 #pragma unroll
                 for (int q = 1; q < BC; ++q)
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
                     }
                 continue;
             }
-            sw.start(make_segf(s, ax, ay, az, bx, by, bz), si, sj, home_chunk(s, pi), ctx.nchunks);
+            sw.start(g, si, sj, home_chunk(s, pi), ctx.nchunks);
             ++sweeps;
             return;
         }
