@@ -142,6 +142,52 @@ int visrt_point_tables(visrt_scene* scene, int64_t nsrc, const double* src_xyz, 
 int visrt_segments_clear(visrt_scene* scene, int64_t nseg, const double* a_xyz, const double* b_xyz,
                          uint8_t* clear, visrt_stats* stats, void* stream);
 
+/* TableBuilder::reach for a query list (src/vistable.cpp:404-430, 432-467):
+ * query q = (source src_xyz[q], reflector chain chains[q].chain[0..order-1],
+ * order 1 or 2; chain[order] and plane name an entry whose plane decides
+ * full[q]). reach[q] = the beam reaches the last reflector (the row /
+ * MobileSampler::member test); full[q] (may be NULL) = Full in that plane. */
+int visrt_chain_reach(visrt_scene* scene, int64_t nq, const double* src_xyz, const visrt_entry* chains,
+                      uint8_t* reach, uint8_t* full, visrt_stats* stats, void* stream);
+
+/* (2) Trajectory visibility table: trajectory_vis_table(traj, matrix, scene,
+ * max_order) (include/rt/vistable.hpp:143-148, src/vistable.cpp:822-960) with
+ * MobileSampler (681-812). Inputs: the route waypoints, the matrix entries
+ * (order <= max_order used; max_order 1 or 2) in matrix order, and the string
+ * orders the reference sorts by, as integer ranks (any order-consistent
+ * integers; equal strings must get equal ranks):
+ *   key_rank[9n+1]   : face id of f at [f], corner node "<id>#k" at [n + 8f + k],
+ *                      "transmitter" at [9n]        (SigKey order, row node order)
+ *   parent_rank[n+1] : label(XY) of f at [f], "transmitter" at [n]   (row parent order)
+ *   building_rank[n] : building_of(f) ("ground" for faces without building)
+ * Rows come back in the reference's order; labels are integers: boundary i is
+ * "P<i>" (+ "'" when prime_*), 0 is "-". blockage is a building rank or -1 ("-").
+ * stats: pairs = samples, candidates = boundaries, admitted = rows,
+ * tests_exec = exact predicate tests, sweeps = kernel launches, ms = device time. */
+typedef struct {
+    const int32_t* key_rank;
+    const int32_t* parent_rank;
+    const int32_t* building_rank;
+} visrt_names;
+typedef struct {
+    int32_t order;
+    int32_t node;          /* face index */
+    int32_t vertex;        /* corner k of a "<id>#k" node, -1 = face node */
+    int32_t parent;        /* face index, -1 = "transmitter" */
+    double s_start, s_end;
+    int32_t label_start, label_end;
+    int32_t prime_start, prime_end;
+    int32_t blockage;
+    int32_t pad;
+} visrt_mobile_row;
+typedef struct visrt_mobile_table visrt_mobile_table;
+int visrt_trajectory_table(visrt_scene* scene, int32_t nwp, const double* waypoints, int64_t nent,
+                           const visrt_entry* entries, int32_t max_order, const visrt_names* names,
+                           visrt_mobile_table** out, visrt_stats* stats, void* stream);
+/* Copy up to cap rows (rows may be NULL); returns the row count. */
+int64_t visrt_mobile_table_rows(const visrt_mobile_table* table, visrt_mobile_row* rows, int64_t cap);
+void visrt_mobile_table_destroy(visrt_mobile_table* table);
+
 /* Order-2 chains of build_matrix(scene, 2) (src/vismatrix.cpp:715-797): every
  * triple p->t->a of admitted pairs that passes chain_triple_feasible and
  * second_order_check in each shared working plane. admitted_bits NULL = the

@@ -229,6 +229,12 @@ class vref_row(C.Structure):
                 ("parent_display", C.c_char * 32)]
 
 
+class vref_mobile_row(C.Structure):
+    _fields_ = [("order", C.c_int32), ("pad", C.c_int32), ("s_start", C.c_double), ("s_end", C.c_double),
+                ("node", C.c_char * 64), ("node_display", C.c_char * 64), ("label_start", C.c_char * 16),
+                ("label_end", C.c_char * 16), ("parent", C.c_char * 64), ("blockage", C.c_char * 64)]
+
+
 class vref_path(C.Structure):
     _fields_ = [("ninter", C.c_int32), ("face", C.c_int32 * 6), ("is_diff", C.c_int32 * 6),
                 ("points", C.c_double * 24), ("length", C.c_double), ("delay", C.c_double),
@@ -292,6 +298,12 @@ class RefOracle:
             L.vref_accel_trace_batch.restype = C.c_int64
             L.vref_accel_trace_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, _f64p, _f64p,
                                                  C.c_int32, C.c_int32, _i64p, _i64p]
+            L.vref_scene_from_shells.restype = C.c_void_p
+            L.vref_scene_from_shells.argtypes = [C.c_int32, _i32p, _f64p, C.c_char_p, _i32p, C.c_int32,
+                                                 C.c_char_p]
+            L.vref_trajectory_table.restype = C.c_int64
+            L.vref_trajectory_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _f64p, C.c_int32,
+                                                C.POINTER(vref_mobile_row), C.c_int64]
             L.vref_image_tree.restype = C.c_int64
             L.vref_image_tree.argtypes = [C.c_void_p, _f64p, C.c_int32, _i32p, _i32p, _i32p, _f64p,
                                           C.c_int64]
@@ -302,6 +314,14 @@ class RefOracle:
         L = self.lib()
         if path is not None:
             self.h = L.vref_scene_load(path.encode())
+        elif getattr(soup, "building", None) is not None and getattr(soup, "building_ids", None):
+            # closed shells through the reference's own Scene::finalize
+            ids = b"".join(s.encode() + b"\0" for s in soup.ids)
+            bids = b"".join(s.encode() + b"\0" for s in soup.building_ids)
+            self.h = L.vref_scene_from_shells(soup.nfaces, np.ascontiguousarray(soup.vert_off, np.int32),
+                                              np.ascontiguousarray(soup.verts, np.float64).reshape(-1), ids,
+                                              np.ascontiguousarray(soup.building, np.int32),
+                                              len(soup.building_ids), bids)
         else:
             ids = b"".join(s.encode() + b"\0" for s in soup.ids)
             self.h = L.vref_scene_from_soup(soup.nfaces, np.ascontiguousarray(soup.vert_off, np.int32),
@@ -415,6 +435,20 @@ class RefOracle:
         return [{"order": r.order, "chain": list(r.chain[: r.chain_len]), "aim": r.aim, "plane": r.plane,
                  "verdict": r.verdict, "ref_display": r.ref_display.decode(),
                  "aim_display": r.aim_display.decode(), "parent_display": r.parent_display.decode()}
+                for r in rows[:n]]
+
+    def trajectory_vis_table(self, m, waypoints, max_order: int) -> List[dict]:
+        """rt::trajectory_vis_table rows (proj/src/vistable.cpp:822-960)."""
+        L = self.lib()
+        cap = 1 << 16
+        rows = (vref_mobile_row * cap)()
+        wp = np.ascontiguousarray(np.asarray(waypoints, np.float64)[:, :3]).reshape(-1)
+        n = L.vref_trajectory_table(self.h, m, len(wp) // 3, wp, max_order, rows, cap)
+        if n < 0:
+            raise RuntimeError(L.vref_last_error().decode())
+        return [{"order": r.order, "node": r.node.decode(), "node_display": r.node_display.decode(),
+                 "s_start": r.s_start, "s_end": r.s_end, "label_start": r.label_start.decode(),
+                 "label_end": r.label_end.decode(), "parent": r.parent.decode(), "blockage": r.blockage.decode()}
                 for r in rows[:n]]
 
     # -- (3) ----------------------------------------------------------------

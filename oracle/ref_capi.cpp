@@ -600,4 +600,48 @@ int64_t vref_image_tree(void* h, const double* src, int32_t depth, int32_t* face
     return n;
 }
 
+// trajectory_vis_table (proj/src/vistable.cpp:822-960): rows flattened.
+// waypoints: [nwp][3]; speeds are irrelevant to the table (1 m/s).
+struct vref_mobile_row {
+    int32_t order;
+    int32_t pad;
+    double s_start;
+    double s_end;
+    char node[64];
+    char node_display[64];
+    char label_start[16];
+    char label_end[16];
+    char parent[64];
+    char blockage[64];
+};
+
+int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, int32_t max_order,
+                              vref_mobile_row* rows, int64_t cap) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    try {
+        R::Trajectory traj;
+        for (int32_t k = 0; k < nwp; ++k) traj.waypoints.push_back({wp[3 * k], wp[3 * k + 1], wp[3 * k + 2]});
+        traj.speeds.assign(static_cast<size_t>(nwp > 1 ? nwp - 1 : 1), 1.0);
+        const auto t = R::trajectory_vis_table(traj, *static_cast<R::InterVisMatrix*>(m), s, max_order);
+        const int64_t n = static_cast<int64_t>(t.size());
+        for (int64_t k = 0; k < n && k < cap; ++k) {
+            const R::MobileVisEntry& e = t[static_cast<size_t>(k)];
+            vref_mobile_row& r = rows[k];
+            std::memset(&r, 0, sizeof(r));
+            r.order = e.order;
+            r.s_start = e.s_start;
+            r.s_end = e.s_end;
+            std::snprintf(r.node, sizeof(r.node), "%s", e.node.c_str());
+            std::snprintf(r.node_display, sizeof(r.node_display), "%s", e.node_display.c_str());
+            std::snprintf(r.label_start, sizeof(r.label_start), "%s", e.label_start.c_str());
+            std::snprintf(r.label_end, sizeof(r.label_end), "%s", e.label_end.c_str());
+            std::snprintf(r.parent, sizeof(r.parent), "%s", e.parent.c_str());
+            std::snprintf(r.blockage, sizeof(r.blockage), "%s", e.blockage.c_str());
+        }
+        return n;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
+
 }  // extern "C"

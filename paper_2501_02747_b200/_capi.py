@@ -28,6 +28,7 @@ EXPORTS = [
     "visrt_scene_nfaces", "visrt_scene_ingest", "visrt_scene_upload_bytes", "visrt_measure_peaks",
     "visrt_pair_visibility", "visrt_matrix_bits_device",
     "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_point_tables", "visrt_segments_clear",
+    "visrt_chain_reach", "visrt_trajectory_table", "visrt_mobile_table_rows", "visrt_mobile_table_destroy",
     "visrt_chain_triples", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results",
 ]
@@ -50,6 +51,10 @@ class visrt_stats(C.Structure):
 class visrt_region(C.Structure):
     _fields_ = [("present", C.c_int8), ("has", C.c_int8 * 3), ("clipped", C.c_int8 * 3),
                 ("pad", C.c_int8), ("sub", C.c_double * 6)]
+
+
+class visrt_names(C.Structure):
+    _fields_ = [("key_rank", C.c_void_p), ("parent_rank", C.c_void_p), ("building_rank", C.c_void_p)]
 
 
 class visrt_path(C.Structure):
@@ -122,6 +127,14 @@ def lib():
                                      C.c_void_p, C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_segments_clear.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_void_p, C.POINTER(visrt_stats),
                                        C.c_void_p]
+    L.visrt_chain_reach.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.POINTER(visrt_stats), C.c_void_p]
+    L.visrt_trajectory_table.argtypes = [C.c_void_p, C.c_int32, _f64p, C.c_int64, C.c_void_p, C.c_int32,
+                                         C.POINTER(visrt_names), C.POINTER(C.c_void_p), C.POINTER(visrt_stats),
+                                         C.c_void_p]
+    L.visrt_mobile_table_rows.restype = C.c_int64
+    L.visrt_mobile_table_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    L.visrt_mobile_table_destroy.argtypes = [C.c_void_p]
     L.visrt_chain_triples.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                       C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_tracer_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,

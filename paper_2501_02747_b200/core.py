@@ -173,6 +173,89 @@ def segments_clear(scene: Scene, a: np.ndarray, b: np.ndarray):
     return out.astype(bool), _stats_dict(st)
 
 
+def chain_reach(scene: Scene, src: np.ndarray, chains: np.ndarray):
+    """TableBuilder::reach for a query list: (source q, reflector chain q) ->
+    (reach[q], full[q]) — MobileSampler::member for face nodes."""
+    src = np.ascontiguousarray(np.asarray(src, np.float64).reshape(-1, 3))
+    ch = np.ascontiguousarray(chains, ENTRY_DTYPE)
+    reach = np.zeros(len(src), np.uint8)
+    full = np.zeros(len(src), np.uint8)
+    st = _capi.visrt_stats()
+    check(lib().visrt_chain_reach(scene.h, len(src), src.reshape(-1), ch.ctypes.data, reach.ctypes.data,
+                                  full.ctypes.data, C.byref(st), None))
+    return reach.astype(bool), full.astype(bool), _stats_dict(st)
+
+
+MOBILE_ROW_DTYPE = np.dtype([("order", np.int32), ("node", np.int32), ("vertex", np.int32), ("parent", np.int32),
+                             ("s_start", np.float64), ("s_end", np.float64), ("label_start", np.int32),
+                             ("label_end", np.int32), ("prime_start", np.int32), ("prime_end", np.int32),
+                             ("blockage", np.int32), ("pad", np.int32)])
+
+
+def _ranks(strings: Sequence[str]) -> Dict[str, int]:
+    return {s: r for r, s in enumerate(sorted(set(strings)))}
+
+
+def trajectory_vis_table(scene: Scene, waypoints, entries: np.ndarray, max_order: int, ids: Sequence[str],
+                         labels_xy: Optional[Sequence[str]] = None, building: Optional[Sequence[int]] = None,
+                         building_names: Optional[Sequence[str]] = None, matrix_max_order: Optional[int] = None,
+                         return_stats: bool = False):
+    """rt::trajectory_vis_table (include/rt/vistable.hpp:143-148,
+    src/vistable.cpp:822-960) on the GPU: rows as dicts with the reference's
+    MobileVisEntry fields (order, node, node_display, s_start, s_end,
+    label_start, label_end, parent, blockage). ``entries`` are the matrix
+    entries (ENTRY_DTYPE) in matrix order; ``labels_xy`` the faces' XY labels
+    ("" = use the id); ``building``/``building_names`` give building_of()."""
+    n = scene.n
+    wp = np.ascontiguousarray(np.asarray(waypoints, np.float64)[:, :3]).reshape(-1)
+    if matrix_max_order is not None and matrix_max_order < max_order:
+        raise _capi.VisibilityError(f"matrix holds orders up to {matrix_max_order}, requested {max_order}")
+    nv = np.diff(scene.soup.vert_off)
+    corner = {(f, k): f"{ids[f]}#{k}" for f in range(n) for k in range(int(nv[f]))}
+    kr = _ranks(list(ids) + list(corner.values()) + ["transmitter"])
+    key_rank = np.zeros(9 * n + 1, np.int32)
+    key_rank[:n] = [kr[i] for i in ids]
+    for (f, k), s in corner.items():
+        key_rank[n + 8 * f + k] = kr[s]
+    key_rank[9 * n] = kr["transmitter"]
+    lab = [(labels_xy[f] if labels_xy is not None and labels_xy[f] else ids[f]) for f in range(n)]
+    pr = _ranks(lab + ["transmitter"])
+    parent_rank = np.array([pr[s] for s in lab] + [pr["transmitter"]], np.int32)
+    bname = [("ground" if building is None or building[f] < 0 or not building_names else building_names[building[f]])
+             for f in range(n)]
+    br = _ranks(bname)
+    building_rank = np.array([br[s] for s in bname], np.int32)
+    names = _capi.visrt_names(key_rank.ctypes.data, parent_rank.ctypes.data, building_rank.ctypes.data)
+    ent = np.ascontiguousarray(entries, ENTRY_DTYPE)
+    h = C.c_void_p()
+    st = _capi.visrt_stats()
+    L = lib()
+    check(L.visrt_trajectory_table(scene.h, len(wp) // 3, wp, len(ent), ent.ctypes.data, max_order, C.byref(names),
+                                   C.byref(h), C.byref(st), None))
+    try:
+        nrows = L.visrt_mobile_table_rows(h, None, 0)
+        rows = np.zeros(max(nrows, 1), MOBILE_ROW_DTYPE)
+        L.visrt_mobile_table_rows(h, rows.ctypes.data, nrows)
+    finally:
+        L.visrt_mobile_table_destroy(h)
+    inv_b = {r: s for s, r in br.items()}
+
+    def label(i, p):
+        return "-" if i == 0 else f"P{i}" + ("'" if p else "")
+
+    out = []
+    for r in rows[:nrows]:
+        f, v, p = int(r["node"]), int(r["vertex"]), int(r["parent"])
+        out.append({"order": int(r["order"]), "node": ids[f] if v < 0 else f"{ids[f]}#{v}",
+                    "node_display": lab[f] if v < 0 else f"{lab[f]}#{v}",
+                    "s_start": float(r["s_start"]), "s_end": float(r["s_end"]),
+                    "label_start": label(int(r["label_start"]), int(r["prime_start"])),
+                    "label_end": label(int(r["label_end"]), int(r["prime_end"])),
+                    "parent": "transmitter" if p < 0 else lab[p],
+                    "blockage": "-" if r["blockage"] < 0 else inv_b[int(r["blockage"])]})
+    return (out, _stats_dict(st)) if return_stats else out
+
+
 def point_vis_table(scene: Scene, src, entries: np.ndarray, ids: Sequence[str], labels=None):
     """rt::point_vis_table rows (src/vistable.cpp:478-521) for one source and
     the given matrix entries: (order, chain ids, aim id, plane, verdict,

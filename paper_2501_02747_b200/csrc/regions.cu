@@ -20,16 +20,10 @@
 
 #include "device.h"
 #include "sweep.h"
+#include "tables.h"
 
 namespace visrt {
 
-struct RegionArgs {
-    DevScene s;
-    long long ntasks;             // nsrc * n
-    const double* src;            // [nsrc][3]
-    visrt_region* out;            // [nsrc][n]
-    unsigned long long* counter;  // [0] cursor, [1] exact tests, [2] sightlines
-};
 
 __device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }
 __device__ __forceinline__ double dmax_std(double a, double b) { return (a < b) ? b : a; }
@@ -308,8 +302,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     };
     auto start_task = [&](long long t) {
         tid = t;
-        const long long k = t / n;
-        f = static_cast<int>(t - k * n);
+        long long k;
+        if (!a.task_face) {
+            k = t / n;
+            f = static_cast<int>(t - k * n);
+        } else if (a.paired) {
+            k = t;
+            f = a.task_face[t];
+        } else {
+            k = t / a.m;
+            f = a.task_face[t - k * a.m];
+        }
         sf = s.inv[f];
         sx = a.src[3 * k];
         sy = a.src[3 * k + 1];
@@ -432,81 +435,19 @@ cudaError_t launch_point_regions(const RegionArgs& a, int device, cudaStream_t s
 // K5: TableBuilder::reach for matrix entries of order 1 / 2 (beam cascade).
 // ---------------------------------------------------------------------------
 
-struct BeamArgs {
-    DevScene s;
-    long long nsrc, nent;
-    const double* src;
-    const visrt_region* regions;   // [nsrc][n]
-    const visrt_entry* ent;
-    uint32_t* row_bits;            // [nsrc][words]
-    uint32_t* full_bits;
-    int32_t words;
-};
-
-struct Cov {
-    int verdict;                   // 0 Full, 1 Partial, 2 None
-    double lo, hi;
-};
-
-// beam_coverage, src/vistable.cpp:225-272 (apex, window [wa, wb], outward; target qa->qb)
-__device__ Cov beam_coverage(double apx, double apy, double wax, double way, double wbx, double wby, double ox,
-                             double oy, double qax, double qay, double qbx, double qby) {
-    Cov r{2, 0.0, 0.0};
-    const double eax = dsub(wax, apx), eay = dsub(way, apy);
-    const double ebx = dsub(wbx, apx), eby = dsub(wby, apy);
-    const double inner = dsub(dmul(eax, eby), dmul(eay, ebx));
-    const double scale = dmul(__dsqrt_rn(dadd(dmul(eax, eax), dmul(eay, eay))),
-                              __dsqrt_rn(dadd(dmul(ebx, ebx), dmul(eby, eby))));
-    const double smax1 = scale < 1.0 ? 1.0 : scale;   // std::max(scale, 1.0)
-    if (fabs(inner) <= dmul(1e-14, smax1)) return r;
-    const double sgn = inner > 0.0 ? 1.0 : -1.0;
-    double lo = 0.0, hi = 1.0;
-    auto apply = [&](double c0, double c1) {
-        if (fabs(c1) <= dmul(1e-15, dadd(fabs(c0), 1.0))) {
-            if (c0 < 0.0) {
-                lo = 1.0;
-                hi = 0.0;
-            }
-            return;
-        }
-        const double t = __ddiv_rn(-c0, c1);
-        if (c1 > 0.0) lo = (lo < t) ? t : lo;     // std::max(lo, t)
-        else hi = (t < hi) ? t : hi;              // std::min(hi, t)
-    };
-    const double dqx = dsub(qbx, qax), dqy = dsub(qby, qay);
-    apply(dadd(dmul(dsub(qax, wax), ox), dmul(dsub(qay, way), oy)), dadd(dmul(dqx, ox), dmul(dqy, oy)));
-    const double rax = dsub(qax, apx), ray = dsub(qay, apy);
-    apply(dmul(sgn, dsub(dmul(eax, ray), dmul(eay, rax))), dmul(sgn, dsub(dmul(eax, dqy), dmul(eay, dqx))));
-    apply(dmul(-sgn, dsub(dmul(ebx, ray), dmul(eby, rax))), dmul(-sgn, dsub(dmul(ebx, dqy), dmul(eby, dqx))));
-    if (dsub(hi, lo) <= 1e-12) return r;
-    r.lo = lo;
-    r.hi = hi;
-    if (lo <= 1e-9 && hi >= 1.0 - 1e-9) {
-        r.verdict = 0;
-        r.lo = 0.0;
-        r.hi = 1.0;
-    } else {
-        r.verdict = 1;
-    }
-    return r;
-}
-
-__device__ __forceinline__ void proj(int pl, double x, double y, double z, double& u, double& v) {
-    if (pl == 0) { u = x; v = y; }
-    else if (pl == 1) { u = y; v = z; }
-    else { u = x; v = z; }
-}
-
 __global__ void __launch_bounds__(256) k_beam_rows(BeamArgs a) {
     const DevScene& s = a.s;
-    const long long total = a.nsrc * a.nent;
+    const long long total = a.paired ? a.nent : a.nsrc * a.nent;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long k = t / a.nent;
-        const int e = static_cast<int>(t - k * a.nent);
+        const long long k = a.paired ? t : t / a.nent;
+        const long long e = a.paired ? t : t - k * a.nent;
         const visrt_entry E = a.ent[e];
         const int head = E.chain[0];
-        const visrt_region& R = a.regions[static_cast<size_t>(k) * s.n + head];
+        const size_t ri = a.paired ? static_cast<size_t>(t)
+                        : a.slot ? static_cast<size_t>(k) * a.rstride + a.slot[head]
+                                 : static_cast<size_t>(k) * s.n + head;
+        const visrt_region& R = a.regions[ri];
         bool row = false, full = false;
         if (R.present == 1) {
             if (E.order == 1) {
@@ -560,7 +501,7 @@ __global__ void __launch_bounds__(256) k_beam_rows(BeamArgs a) {
                 full = row && has_pl && full_pl;
             }
         }
-        const size_t w = static_cast<size_t>(k) * a.words + (e >> 5);
+        const size_t w = (a.paired ? 0 : static_cast<size_t>(k) * a.words) + static_cast<size_t>(e >> 5);
         if (row) atomicOr(a.row_bits + w, 1u << (e & 31));
         if (full) atomicOr(a.full_bits + w, 1u << (e & 31));
     }
@@ -641,6 +582,20 @@ static cudaError_t launch_segments_t(const DevScene& s, long long nseg, const do
         return cudaGetLastError();
     };
     return res ? go(k_segments_clear<MAXV, true>) : go(k_segments_clear<MAXV, false>);
+}
+
+cudaError_t launch_segments_clear(const DevScene& s, long long nseg, const double* A, const double* B,
+                                  uint8_t* clear, unsigned long long* counter, int device, cudaStream_t st) {
+    return s.maxv <= 4 ? launch_segments_t<4>(s, nseg, A, B, clear, counter, device, st)
+                       : launch_segments_t<8>(s, nseg, A, B, clear, counter, device, st);
+}
+
+cudaError_t launch_beam_rows(const BeamArgs& a, cudaStream_t st) {
+    const long long work = a.paired ? a.nent : a.nsrc * a.nent;
+    if (work <= 0) return cudaSuccess;
+    const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 148 * 32));
+    k_beam_rows<<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace visrt

@@ -55,7 +55,7 @@ def test_sm100a_only_and_no_fma_in_predicate():
     # .rn.f64 and no fma.*.f64 (SASS DFMA appears only inside the correctly
     # rounded div.rn.f64 / sqrt.rn.f64 expansions).
     from paper_2501_02747_b200 import build
-    for src in ("matrix.cu", "tree.cu", "chains.cu"):
+    for src in ("matrix.cu", "tree.cu", "chains.cu", "regions.cu", "trajectory.cu"):
         ptx = subprocess.run([build.NVCC, "-std=c++17", "-ptx", "--fmad=false", "-gencode",
                               "arch=compute_100a,code=sm_100a", "-I", os.path.join(ROOT, "include"),
                               os.path.join(build.CSRC, src), "-o", "-"], capture_output=True, text=True, check=True).stdout

@@ -132,3 +132,47 @@ def test_two_buildings_trace_set():
     t3 = [t for t in d["traces"] if t["order"] == 3 and G.unhex(t["tx"]) == [3.0, 15.0, 2.0]][0]
     ids = {p["identity"] for p in t3["paths"]}
     assert {"LOS", "R:B1_n", "R:B2_s", "R:B1_n/R:B2_s", "R:B2_s/R:B1_n"} <= ids
+
+
+# ---- trajectory tables (tests/golden/trajectories.json) ---------------------
+def _traj_cases():
+    import json
+    import os
+    return json.load(open(os.path.join(G.GOLDEN, "trajectories.json")))
+
+
+def test_trajectory_golden_known_answers():
+    """The golden rows carry the reference's own known answers:
+    proj/tests/test_vistable.cpp:181-236 (drive-by: 18 rows, boundaries at
+    10/3, 4, 46, 140/3) and 286-319 (three primed W3_s rows ending at s = 4)."""
+    cases = _traj_cases()
+    drive = next(c for c in cases if c["scene"] == "screened_wall" and c["max_order"] == 2)
+    assert len(drive["rows"]) == 18
+    for r in drive["rows"]:
+        for lab, s in ((r["label_start"], r["s_start"]), (r["label_end"], r["s_end"])):
+            if lab != "-":
+                assert min(abs(float.fromhex(s) - x) for x in (10 / 3, 4.0, 46.0, 140 / 3)) <= 1e-3
+    primed = next(c for c in cases if c["scene"] == "primed")
+    assert len(primed["rows"]) == 3
+    assert all(r["label_end"].endswith("'") and abs(float.fromhex(r["s_end"]) - 4.0) <= 1e-3
+               for r in primed["rows"])
+
+
+def test_trajectory_golden_regenerates(oracle_built):
+    """Re-run the compiled reference on the small cases: identical rows."""
+    import numpy as np
+    if not oracle_built.have_ref():
+        pytest.skip("oracle/_ref not built")
+    for c in _traj_cases():
+        if c["scene"] not in ("screened_wall", "two_buildings", "street_canyon"):
+            continue
+        r = oracle_built.RefOracle(path=f"/root/reference/proj/data/fixtures/{c['scene']}.json") \
+            if __import__("os").path.exists("/root/reference") else None
+        if r is None:
+            pytest.skip("reference fixtures absent")
+        m = r.build_matrix(c["max_order"])
+        rows = r.trajectory_vis_table(m, np.asarray(c["waypoints"], np.float64), c["max_order"])
+        for row in rows:
+            row["s_start"] = float(row["s_start"]).hex()
+            row["s_end"] = float(row["s_end"]).hex()
+        assert rows == c["rows"]
