@@ -223,6 +223,24 @@ typedef struct {
 } visrt_trace_stats;
 int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const double* rx,
                 int rx_fixed, visrt_trace_stats* stats, void* stream);
+/* Unfiltered mirror hierarchy image_tree(scene, source, max_depth)
+ * (include/rt/raytracer.hpp:51-61, src/raytracer.cpp:458-486): nodes in the
+ * reference's depth-first order — face index, parent node (-1 at depth 1),
+ * depth, image[3]. Two-call sizing: all outputs NULL returns the count in
+ * *nnodes; otherwise cap must be >= the count. */
+int visrt_image_tree(visrt_scene* scene, const double* src, int32_t max_depth, int32_t* face, int32_t* parent,
+                     int32_t* depth, double* image, int64_t cap, int64_t* nnodes, visrt_stats* stats,
+                     void* stream);
+
+/* closest_diffraction_edge(receiver, scene) (include/rt/vistable.hpp:131-137,
+ * src/vistable.cpp:529-561) for nrx receivers over the scene's edges (edge e:
+ * a = edge_ab[6e..6e+2], b = edge_ab[6e+3..6e+5], in the scene's edge order;
+ * edge_rank[e] = order of its id string, for the tie-break). out_edge[r] =
+ * edge index, -1 = none visible. */
+int visrt_closest_edges(visrt_scene* scene, int64_t nrx, const double* rx_xyz, int32_t nedges,
+                        const double* edge_ab, const int32_t* edge_rank, int32_t* out_edge, visrt_stats* stats,
+                        void* stream);
+
 /* Fetch the last visrt_trace results: per-snapshot CSR (path_off[nsnap+1]),
  * paths grouped by snapshot, each group sorted by face sequence; nodes[nsnap]
  * per-snapshot node counts. Any pointer may be NULL; returns the path count. */

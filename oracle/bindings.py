@@ -301,6 +301,7 @@ class RefOracle:
             L.vref_scene_from_shells.restype = C.c_void_p
             L.vref_scene_from_shells.argtypes = [C.c_int32, _i32p, _f64p, C.c_char_p, _i32p, C.c_int32,
                                                  C.c_char_p]
+            L.vref_closest_edge.argtypes = [C.c_void_p, _f64p]
             L.vref_trajectory_table.restype = C.c_int64
             L.vref_trajectory_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _f64p, C.c_int32,
                                                 C.POINTER(vref_mobile_row), C.c_int64]
@@ -436,6 +437,18 @@ class RefOracle:
                  "verdict": r.verdict, "ref_display": r.ref_display.decode(),
                  "aim_display": r.aim_display.decode(), "parent_display": r.parent_display.decode()}
                 for r in rows[:n]]
+
+    def image_tree(self, src, depth: int):
+        L = self.lib()
+        src = np.ascontiguousarray(src, np.float64)
+        cap = 1 << 22
+        face, parent, dep = (np.zeros(cap, np.int32) for _ in range(3))
+        image = np.zeros(3 * cap, np.float64)
+        n = L.vref_image_tree(self.h, src, depth, face, parent, dep, image, cap)
+        return face[:n], parent[:n], dep[:n], image[:3 * n].reshape(n, 3)
+
+    def closest_edge(self, rx) -> int:
+        return int(self.lib().vref_closest_edge(self.h, np.ascontiguousarray(rx, np.float64)))
 
     def trajectory_vis_table(self, m, waypoints, max_order: int) -> List[dict]:
         """rt::trajectory_vis_table rows (proj/src/vistable.cpp:822-960)."""

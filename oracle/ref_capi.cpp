@@ -600,6 +600,17 @@ int64_t vref_image_tree(void* h, const double* src, int32_t depth, int32_t* face
     return n;
 }
 
+// closest_diffraction_edge (proj/src/vistable.cpp:545-561): edge index or -1.
+int32_t vref_closest_edge(void* h, const double* rx) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    const auto e = R::closest_diffraction_edge({rx[0], rx[1], rx[2]}, s);
+    if (!e) return -1;
+    const auto& edges = s.edges();
+    for (size_t k = 0; k < edges.size(); ++k)
+        if (edges[k].id == e->id) return static_cast<int32_t>(k);
+    return -2;
+}
+
 // trajectory_vis_table (proj/src/vistable.cpp:822-960): rows flattened.
 // waypoints: [nwp][3]; speeds are irrelevant to the table (1 m/s).
 struct vref_mobile_row {

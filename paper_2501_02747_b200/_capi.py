@@ -30,7 +30,7 @@ EXPORTS = [
     "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_point_tables", "visrt_segments_clear",
     "visrt_chain_reach", "visrt_trajectory_table", "visrt_mobile_table_rows", "visrt_mobile_table_destroy",
     "visrt_chain_triples", "visrt_tracer_create",
-    "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results",
+    "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results", "visrt_image_tree", "visrt_closest_edges",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -142,6 +142,10 @@ def lib():
     L.visrt_tracer_destroy.argtypes = [C.c_void_p]
     L.visrt_trace.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_int, C.POINTER(visrt_trace_stats),
                               C.c_void_p]
+    L.visrt_image_tree.argtypes = [C.c_void_p, _f64p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int64, C.POINTER(C.c_int64), C.POINTER(visrt_stats), C.c_void_p]
+    L.visrt_closest_edges.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_int32, C.c_void_p, C.c_void_p, _i32p,
+                                      C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_trace_results.restype = C.c_int64
     L.visrt_trace_results.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     _lib = L

@@ -363,6 +363,41 @@ class Tracer:
         return out, nodes, st
 
 
+def image_tree(scene: Scene, source, max_depth: int, ids: Optional[Sequence[str]] = None):
+    """rt::image_tree (include/rt/raytracer.hpp:51-61): the unfiltered
+    front-side mirror hierarchy in the reference's depth-first node order.
+    Returns a list of {face, image, parent, depth} (face = id when ``ids``)."""
+    src = np.ascontiguousarray(np.asarray(source, np.float64).reshape(3))
+    cnt = C.c_int64()
+    st = _capi.visrt_stats()
+    L = lib()
+    check(L.visrt_image_tree(scene.h, src, max_depth, None, None, None, None, 0, C.byref(cnt), C.byref(st), None))
+    n = cnt.value
+    face = np.zeros(max(n, 1), np.int32)
+    parent = np.zeros(max(n, 1), np.int32)
+    depth = np.zeros(max(n, 1), np.int32)
+    image = np.zeros((max(n, 1), 3), np.float64)
+    check(L.visrt_image_tree(scene.h, src, max_depth, face.ctypes.data, parent.ctypes.data, depth.ctypes.data,
+                             image.ctypes.data, n, C.byref(cnt), C.byref(st), None))
+    return [{"face": ids[face[k]] if ids is not None else int(face[k]), "image": image[k].tolist(),
+             "parent": int(parent[k]), "depth": int(depth[k])} for k in range(n)]
+
+
+def closest_diffraction_edges(scene: Scene, receivers, edges: Sequence[dict]):
+    """rt::closest_diffraction_edge (include/rt/vistable.hpp:131-137) for a batch
+    of receivers; ``edges`` = the scene's edges in order ({id, a, b}). Returns
+    per receiver the edge index or -1."""
+    rx = np.ascontiguousarray(np.asarray(receivers, np.float64).reshape(-1, 3))
+    ab = np.ascontiguousarray(np.array([list(e["a"]) + list(e["b"]) for e in edges], np.float64).reshape(-1))
+    rank = _ranks([e["id"] for e in edges])
+    er = np.ascontiguousarray(np.array([rank[e["id"]] for e in edges], np.int32))
+    out = np.full(len(rx), -1, np.int32)
+    st = _capi.visrt_stats()
+    check(lib().visrt_closest_edges(scene.h, len(rx), rx.reshape(-1), len(edges), ab.ctypes.data if len(edges) else None,
+                                    er.ctypes.data if len(edges) else None, out, C.byref(st), None))
+    return out
+
+
 def path_identity(ids: Sequence[str], faces: Sequence[int]) -> str:
     """Path::identity (src/raytracer.cpp:448-456) for a reflection-only path."""
     return "LOS" if not faces else "/".join("R:" + ids[f] for f in faces)

@@ -1,0 +1,58 @@
+"""Generate tests/golden/aux.json from the UNMODIFIED reference (oracle/_ref):
+image_tree(scene, source, depth) (proj/src/raytracer.cpp:458-486) node lists
+and closest_diffraction_edge(receiver, scene) (proj/src/vistable.cpp:545-561)
+answers on the reference's fixture scenes and the seeded config-1 soup.
+Run in the build container:  python tests/golden/make_golden_aux.py"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.dirname(HERE))
+
+from oracle import bindings  # noqa: E402
+from paper_2501_02747_b200 import scenes  # noqa: E402
+from make_golden import FIXTURES  # noqa: E402
+
+
+def main() -> None:
+    bindings.build(ref=True)
+    trees, edges = [], []
+    jobs = [("two_buildings", (5, -5, 2), 2), ("two_buildings", (5, 15, 2), 3), ("street_canyon", (5, 28, 11), 3),
+            ("screened_wall", (2, 2, 2), 3), ("manhattan", (12.5, 2.5, 1.5), 2), ("open_field", (0, 0, 2), 3)]
+    for name, src, depth in jobs:
+        r = bindings.RefOracle(path=os.path.join(FIXTURES, name + ".json"))
+        face, parent, dep, image = r.image_tree(np.asarray(src, np.float64), depth)
+        trees.append({"scene": name, "source": list(src), "depth": depth, "face": face.tolist(),
+                      "parent": parent.tolist(), "node_depth": dep.tolist(),
+                      "image": [[float(x).hex() for x in p] for p in image]})
+        print(name, depth, len(face), "nodes")
+    wl = scenes.workload(1)
+    r = bindings.RefOracle(wl.scene)
+    face, parent, dep, image = r.image_tree(wl.tx[3], 2)
+    trees.append({"scene": "config1", "source": wl.tx[3].tolist(), "depth": 2, "face": face.tolist(),
+                  "parent": parent.tolist(), "node_depth": dep.tolist(),
+                  "image": [[float(x).hex() for x in p] for p in image]})
+    print("config1", 2, len(face), "nodes")
+    rng = np.random.default_rng(7)
+    for name in ("two_buildings", "street_canyon", "screened_wall", "manhattan", "open_field"):
+        r = bindings.RefOracle(path=os.path.join(FIXTURES, name + ".json"))
+        _, es = r.export()
+        pts = [(5, 12, 1), (5, 5, 2), (5, -5, 2), (5, 28, 11), (12.5, 2.5, 1.5), (50, 50, 30)]
+        lo = np.min([e["a"] for e in es], axis=0) if es else np.zeros(3)
+        hi = np.max([e["a"] for e in es], axis=0) if es else np.ones(3)
+        pts += [tuple((lo + (hi - lo) * rng.random(3) * 1.2 - 0.1 * (hi - lo)).tolist()) for _ in range(24)]
+        edges.append({"scene": name, "receivers": [list(p) for p in pts],
+                      "edge": [r.closest_edge(np.asarray(p, np.float64)) for p in pts]})
+        print(name, len(es), "edges")
+    with open(os.path.join(HERE, "aux.json"), "w") as fh:
+        json.dump({"image_trees": trees, "closest_edges": edges}, fh, separators=(",", ":"))
+
+
+if __name__ == "__main__":
+    main()

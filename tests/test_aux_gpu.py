@@ -1,0 +1,54 @@
+"""(3) image_tree (proj/src/raytracer.cpp:458-486) and closest_diffraction_edge
+(proj/src/vistable.cpp:545-561) on the GPU vs the compiled reference's
+answers (tests/golden/aux.json, made by tests/golden/make_golden_aux.py) and
+the reference's known-answer test (proj/tests/test_raytracer.cpp:297-329)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import golden_util as G
+from paper_2501_02747_b200 import scenes
+from paper_2501_02747_b200.core import Scene, closest_diffraction_edges, image_tree
+
+pytestmark = pytest.mark.gpu
+AUX = json.load(open(os.path.join(G.GOLDEN, "aux.json")))
+
+
+def soup_of(name):
+    return scenes.workload(1).scene if name == "config1" else G.soup(G.load(name))
+
+
+@pytest.mark.parametrize("k", range(len(AUX["image_trees"])))
+def test_image_tree_vs_reference(k):
+    t = AUX["image_trees"][k]
+    with Scene(soup_of(t["scene"])) as sc:
+        nodes = image_tree(sc, t["source"], t["depth"])
+    assert [n["face"] for n in nodes] == t["face"]
+    assert [n["parent"] for n in nodes] == t["parent"]
+    assert [n["depth"] for n in nodes] == t["node_depth"]
+    assert [[float.fromhex(x) for x in p] for p in t["image"]] == [n["image"] for n in nodes]
+
+
+def test_image_tree_front_side_known_answer():
+    """proj/tests/test_raytracer.cpp:297-329: from (5,-5,2) at depth 2, two
+    depth-1 nodes (B1_s, B2_s) and three depth-2 nodes."""
+    s = soup_of("two_buildings")
+    with Scene(s) as sc:
+        nodes = image_tree(sc, [5, -5, 2], 2, ids=s.ids)
+    d1 = [n for n in nodes if n["depth"] == 1]
+    d2 = [n for n in nodes if n["depth"] == 2]
+    assert len(d1) == 2 and len(d2) == 3
+    assert {n["face"] for n in d1} == {"B1_s", "B2_s"}
+    for n in d2:
+        assert nodes[n["parent"]]["depth"] == 1 and nodes[n["parent"]]["face"] != n["face"]
+
+
+@pytest.mark.parametrize("k", range(len(AUX["closest_edges"])))
+def test_closest_edges_vs_reference(k):
+    c = AUX["closest_edges"][k]
+    d = G.load(c["scene"])
+    with Scene(G.soup(d)) as sc:
+        got = closest_diffraction_edges(sc, c["receivers"], d["edges"])
+    assert got.tolist() == c["edge"]
