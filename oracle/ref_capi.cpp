@@ -431,17 +431,6 @@ int32_t vref_regions_batch(void* h, int64_t n, const double* src, const int32_t*
 }
 
 // point_vis_table (proj/src/vistable.cpp:478-521): rows flattened.
-struct vref_row {
-    int32_t order;
-    int32_t chain[4];
-    int32_t chain_len;
-    int32_t aim;
-    int32_t plane;
-    int32_t verdict;
-    char ref_display[32];
-    char aim_display[32];
-    char parent_display[32];
-};
 
 int64_t vref_point_vis_table(void* h, void* m, const double* src, int32_t max_order, vref_row* rows,
                              int64_t cap) {
@@ -613,18 +602,6 @@ int32_t vref_closest_edge(void* h, const double* rx) {
 
 // trajectory_vis_table (proj/src/vistable.cpp:822-960): rows flattened.
 // waypoints: [nwp][3]; speeds are irrelevant to the table (1 m/s).
-struct vref_mobile_row {
-    int32_t order;
-    int32_t pad;
-    double s_start;
-    double s_end;
-    char node[64];
-    char node_display[64];
-    char label_start[16];
-    char label_end[16];
-    char parent[64];
-    char blockage[64];
-};
 
 int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, int32_t max_order,
                               vref_mobile_row* rows, int64_t cap) {

@@ -50,6 +50,31 @@ typedef struct {
     char identity[256];
 } vref_path;
 
+typedef struct {
+    int32_t order;
+    int32_t chain[4];
+    int32_t chain_len;
+    int32_t aim;
+    int32_t plane;
+    int32_t verdict;
+    char ref_display[32];
+    char aim_display[32];
+    char parent_display[32];
+} vref_row;
+
+typedef struct {
+    int32_t order;
+    int32_t pad;
+    double s_start;
+    double s_end;
+    char node[64];
+    char node_display[64];
+    char label_start[16];
+    char label_end[16];
+    char parent[64];
+    char blockage[64];
+} vref_mobile_row;
+
 const char* vref_last_error(void);
 void* vref_scene_from_soup(int32_t nfaces, const int32_t* vert_off, const double* verts, const char* ids);
 void* vref_scene_from_shells(int32_t nfaces, const int32_t* vert_off, const double* verts, const char* ids,
@@ -63,6 +88,12 @@ int64_t vref_matrix_size(void* m);
 int32_t vref_matrix_entry(void* h, void* m, int64_t k, vref_entry* out);
 int32_t vref_occlusion(void* h, int32_t i, int32_t j, int32_t* blockers, int32_t cap, int32_t* nblk);
 int32_t vref_illuminated_region(void* h, const double* src, int32_t face, vref_region* out);
+int64_t vref_point_vis_table(void* h, void* m, const double* src, int32_t max_order, vref_row* rows, int64_t cap);
+int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, int32_t max_order,
+                              vref_mobile_row* rows, int64_t cap);
+int32_t vref_closest_edge(void* h, const double* rx);
+int64_t vref_image_tree(void* h, const double* src, int32_t depth, int32_t* face, int32_t* parent,
+                        int32_t* dep, double* image, int64_t cap);
 void* vref_accel_create(void* h, void* m, int32_t max_refl);
 void vref_accel_free(void* a);
 int64_t vref_accel_trace(void* h, void* a, const double* tx, const double* rx, int32_t diffraction,

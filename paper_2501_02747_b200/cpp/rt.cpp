@@ -750,4 +750,217 @@ std::vector<Path> TraceAccelerator::trace(const Vec3& tx, const Vec3& rx, bool a
     return std::move(out[0]);
 }
 
+// ---------------------------------------------------------------------------
+// (2) tables: point_vis_table, trajectory_vis_table, closest_diffraction_edge
+// ---------------------------------------------------------------------------
+namespace {
+visrt_entry to_entry(const Scene& scene, const InterVisEntry& e) {
+    visrt_entry v{};
+    v.order = e.order;
+    const auto& c = e.relation.chain;
+    for (size_t k = 0; k < c.size() && k < 3; ++k) v.chain[k] = scene.face(c[k]).index;
+    v.plane = static_cast<int32_t>(e.relation.plane);
+    return v;
+}
+void check_table_order(const InterVisMatrix& matrix, int max_order) {
+    if (max_order < 1) throw VisibilityError("max_order must be at least 1");
+    if (matrix.max_order() < max_order)
+        throw VisibilityError("matrix holds orders up to " + std::to_string(matrix.max_order()) + ", requested " +
+                              std::to_string(max_order));
+    if (max_order > 2) throw std::invalid_argument("GPU tables cover orders 1 and 2");
+}
+}  // namespace
+
+std::vector<VisTableEntry> point_vis_table(const Vec3& source, const InterVisMatrix& matrix, const Scene& scene,
+                                           int max_order) {
+    check_table_order(matrix, max_order);   // src/vistable.cpp:480-485
+    const size_t n = scene.faces().size();
+    std::vector<const InterVisEntry*> used;
+    std::vector<visrt_entry> ents;
+    for (const InterVisEntry& e : matrix.entries()) {
+        if (e.order > max_order || e.relation.chain.size() < 2) continue;
+        used.push_back(&e);
+        ents.push_back(to_entry(scene, e));
+    }
+    const size_t words = (ents.size() + 31) / 32;
+    std::vector<uint32_t> rows(std::max<size_t>(words, 1)), full(std::max<size_t>(words, 1));
+    std::vector<visrt_region> regs(n);
+    const double src[3] = {source.x, source.y, source.z};
+    visrt_stats st{};
+    check(visrt_point_tables(scene.device_scene(), 1, src, static_cast<int64_t>(ents.size()), ents.data(),
+                             rows.data(), full.data(), regs.data(), &st, nullptr));
+    // TableBuilder::display (src/vistable.cpp:392-401)
+    auto display = [&](const std::string& id, PlaneTag plane) {
+        const Face& f = scene.face(id);
+        std::string name = f.label(plane);
+        const visrt_region& r = regs[static_cast<size_t>(f.index)];
+        const int pl = static_cast<int>(plane);
+        if (r.present == 1 && r.has[pl] && r.clipped[pl]) name += "'";
+        return name;
+    };
+    std::vector<VisTableEntry> out;
+    for (size_t k = 0; k < used.size(); ++k) {
+        if (!((rows[k >> 5] >> (k & 31)) & 1u)) continue;
+        const InterVisEntry& e = *used[k];
+        const auto& cf = e.relation.chain;
+        VisTableEntry row;
+        row.order = e.order;
+        row.chain.assign(cf.begin(), cf.end() - 1);
+        row.ref = row.chain.back();
+        row.aim = e.aim;
+        row.plane = e.relation.plane;
+        row.parent = row.chain.size() >= 2 ? row.chain[row.chain.size() - 2] : std::string("transmitter");
+        row.parent_display = row.chain.size() >= 2 ? display(row.parent, e.relation.plane) : std::string("transmitter");
+        row.ref_display = display(row.ref, e.relation.plane);
+        row.aim_display = display(row.aim, e.relation.plane);
+        row.verdict = ((full[k >> 5] >> (k & 31)) & 1u) ? ChainVerdict::Full : ChainVerdict::Partial;
+        out.push_back(std::move(row));
+    }
+    std::sort(out.begin(), out.end(), [](const VisTableEntry& a, const VisTableEntry& b) {
+        return std::tie(a.order, a.chain, a.aim, a.plane) < std::tie(b.order, b.chain, b.aim, b.plane);
+    });
+    return out;
+}
+
+// src/scene.cpp:443-469
+double Trajectory::total_length() const {
+    double len = 0;
+    for (size_t i = 0; i + 1 < waypoints.size(); ++i) len += norm(waypoints[i + 1] - waypoints[i]);
+    return len;
+}
+Vec3 Trajectory::position_at(double s) const {
+    if (s <= 0) return waypoints.front();
+    for (size_t i = 0; i + 1 < waypoints.size(); ++i) {
+        const double seg = norm(waypoints[i + 1] - waypoints[i]);
+        if (s <= seg) return waypoints[i] + (waypoints[i + 1] - waypoints[i]) * (s / seg);
+        s -= seg;
+    }
+    return waypoints.back();
+}
+
+namespace {
+template <class T>
+std::map<T, int32_t> ranks_of(std::vector<T> v) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    std::map<T, int32_t> r;
+    for (size_t k = 0; k < v.size(); ++k) r.emplace(v[k], static_cast<int32_t>(k));
+    return r;
+}
+std::string building_of(const Face& f) { return f.building.empty() ? "ground" : f.building; }
+}  // namespace
+
+std::vector<MobileVisEntry> trajectory_vis_table(const Trajectory& traj, const InterVisMatrix& matrix,
+                                                 const Scene& scene, int max_order) {
+    if (traj.waypoints.size() < 2 || traj.total_length() <= kEps)   // src/vistable.cpp:825-828
+        throw VisibilityError("trajectory must contain at least two distinct waypoints");
+    if (matrix.max_order() < max_order)
+        throw VisibilityError("matrix holds orders up to " + std::to_string(matrix.max_order()) + ", requested " +
+                              std::to_string(max_order));
+    if (max_order > 2) throw std::invalid_argument("GPU trajectory tables cover orders 1 and 2");
+    const int n = static_cast<int>(scene.faces().size());
+    std::vector<std::string> keys{"transmitter"}, parents{"transmitter"}, blds;
+    auto corner = [&](int f, int k) { return scene.face(f).id + "#" + std::to_string(k); };
+    for (int f = 0; f < n; ++f) {
+        const Face& fc = scene.face(f);
+        keys.push_back(fc.id);
+        for (size_t k = 0; k < fc.poly.pts.size(); ++k) keys.push_back(corner(f, static_cast<int>(k)));
+        parents.push_back(fc.label(PlaneTag::XY));
+        blds.push_back(building_of(fc));
+    }
+    const auto kr = ranks_of(keys), pr = ranks_of(parents), br = ranks_of(blds);
+    std::vector<int32_t> key_rank(9 * static_cast<size_t>(n) + 1, 0), parent_rank(n + 1), building_rank(n);
+    for (int f = 0; f < n; ++f) {
+        const Face& fc = scene.face(f);
+        key_rank[f] = kr.at(fc.id);
+        for (size_t k = 0; k < fc.poly.pts.size(); ++k)
+            key_rank[n + 8 * static_cast<size_t>(f) + k] = kr.at(corner(f, static_cast<int>(k)));
+        parent_rank[f] = pr.at(fc.label(PlaneTag::XY));
+        building_rank[f] = br.at(building_of(fc));
+    }
+    key_rank[9 * static_cast<size_t>(n)] = kr.at("transmitter");
+    parent_rank[n] = pr.at("transmitter");
+    std::vector<std::string> bname(br.size());
+    for (const auto& [name, r] : br) bname[static_cast<size_t>(r)] = name;
+    std::vector<visrt_entry> ents;
+    for (const InterVisEntry& e : matrix.entries())
+        if (e.order <= max_order && e.relation.chain.size() >= 2) ents.push_back(to_entry(scene, e));
+    std::vector<double> wp;
+    for (const Vec3& w : traj.waypoints) wp.insert(wp.end(), {w.x, w.y, w.z});
+    const visrt_names names{key_rank.data(), parent_rank.data(), building_rank.data()};
+    visrt_mobile_table* t = nullptr;
+    visrt_stats st{};
+    check(visrt_trajectory_table(scene.device_scene(), static_cast<int32_t>(traj.waypoints.size()), wp.data(),
+                                 static_cast<int64_t>(ents.size()), ents.data(), max_order, &names, &t, &st, nullptr));
+    const int64_t nr = visrt_mobile_table_rows(t, nullptr, 0);
+    std::vector<visrt_mobile_row> rows(static_cast<size_t>(std::max<int64_t>(nr, 1)));
+    visrt_mobile_table_rows(t, rows.data(), nr);
+    visrt_mobile_table_destroy(t);
+    auto label = [](int i, int prime) { return i == 0 ? std::string("-") : "P" + std::to_string(i) + (prime ? "'" : ""); };
+    std::vector<MobileVisEntry> out;
+    for (int64_t k = 0; k < nr; ++k) {
+        const visrt_mobile_row& r = rows[static_cast<size_t>(k)];
+        const Face& f = scene.face(r.node);
+        MobileVisEntry m;
+        m.order = r.order;
+        m.node = r.vertex < 0 ? f.id : corner(r.node, r.vertex);
+        m.node_display = r.vertex < 0 ? f.label(PlaneTag::XY) : f.label(PlaneTag::XY) + "#" + std::to_string(r.vertex);
+        m.s_start = r.s_start;
+        m.s_end = r.s_end;
+        m.label_start = label(r.label_start, r.prime_start);
+        m.label_end = label(r.label_end, r.prime_end);
+        m.parent = r.parent < 0 ? std::string("transmitter") : scene.face(r.parent).label(PlaneTag::XY);
+        m.blockage = r.blockage < 0 ? std::string("-") : bname[static_cast<size_t>(r.blockage)];
+        out.push_back(std::move(m));
+    }
+    return out;
+}
+
+std::optional<Edge> closest_diffraction_edge(const Vec3& receiver, const Scene& scene) {
+    const auto& es = scene.edges();
+    if (es.empty()) return std::nullopt;
+    std::vector<double> ab;
+    std::vector<std::string> ids;
+    for (const Edge& e : es) {
+        ab.insert(ab.end(), {e.a.x, e.a.y, e.a.z, e.b.x, e.b.y, e.b.z});
+        ids.push_back(e.id);
+    }
+    const auto rk = ranks_of(ids);
+    std::vector<int32_t> rank;
+    for (const Edge& e : es) rank.push_back(rk.at(e.id));
+    const double rx[3] = {receiver.x, receiver.y, receiver.z};
+    int32_t best = -1;
+    visrt_stats st{};
+    check(visrt_closest_edges(scene.device_scene(), 1, rx, static_cast<int32_t>(es.size()), ab.data(), rank.data(),
+                              &best, &st, nullptr));
+    if (best < 0) return std::nullopt;
+    return es[static_cast<size_t>(best)];
+}
+
+std::optional<Edge> closest_diffraction_edge(const Vec3& receiver, const Scene& scene, const InterVisMatrix&) {
+    return closest_diffraction_edge(receiver, scene);
+}
+
+std::vector<ImageTreeNode> image_tree(const Scene& scene, const Vec3& source, int max_depth) {
+    const double src[3] = {source.x, source.y, source.z};
+    int64_t cnt = 0;
+    visrt_stats st{};
+    check(visrt_image_tree(scene.device_scene(), src, max_depth, nullptr, nullptr, nullptr, nullptr, 0, &cnt, &st,
+                           nullptr));
+    const size_t m = static_cast<size_t>(std::max<int64_t>(cnt, 1));
+    std::vector<int32_t> face(m), parent(m), depth(m);
+    std::vector<double> image(3 * m);
+    check(visrt_image_tree(scene.device_scene(), src, max_depth, face.data(), parent.data(), depth.data(),
+                           image.data(), cnt, &cnt, &st, nullptr));
+    std::vector<ImageTreeNode> out(static_cast<size_t>(cnt));
+    for (int64_t k = 0; k < cnt; ++k) {
+        ImageTreeNode& nd = out[static_cast<size_t>(k)];
+        nd.face = scene.face(face[k]).id;
+        nd.image = {image[3 * k], image[3 * k + 1], image[3 * k + 2]};
+        nd.parent = parent[k];
+        nd.depth = depth[k];
+    }
+    return out;
+}
+
 }  // namespace rt

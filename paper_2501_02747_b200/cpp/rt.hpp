@@ -5,7 +5,8 @@
 //   Scene / Face / Building / plane_segment          include/rt/scene.hpp:38-106
 //   occlusion_judgment, build_matrix, InterVisMatrix include/rt/vismatrix.hpp:37-141
 //   illuminated_region                                include/rt/vistable.hpp:116-117
-//   TraceAccelerator / Path / TraceStats              include/rt/raytracer.hpp:25-118
+//   TraceAccelerator / Path / TraceStats / image_tree include/rt/raytracer.hpp:25-118
+//   point_vis_table, trajectory_vis_table, closest_diffraction_edge  include/rt/vistable.hpp:62-148
 // Geometry is decided on the GPU (sm_100a kernels); the host materialises the
 // string-keyed records (ids, angle records with atan2, aim images) exactly as
 // the reference does. There is no CPU fallback for any hot-path decision.
@@ -210,7 +211,53 @@ std::optional<IlluminatedRegion> illuminated_region(const Vec3& source, const Fa
 std::vector<std::vector<std::optional<IlluminatedRegion>>> illuminated_regions(const std::vector<Vec3>& sources,
                                                                                const Scene& scene);
 
+/// include/rt/vistable.hpp:62-76
+struct VisTableEntry {
+    int order = 1;
+    std::string parent, ref, aim;
+    PlaneTag plane = PlaneTag::XY;
+    std::string parent_display, ref_display, aim_display;
+    ChainVerdict verdict = ChainVerdict::Full;
+    std::vector<std::string> chain;
+};
+/// point_vis_table (include/rt/vistable.hpp:128-129): GPU regions + beam
+/// cascade; matrix entries of order <= min(max_order, 2).
+std::vector<VisTableEntry> point_vis_table(const Vec3& source, const InterVisMatrix& matrix, const Scene& scene,
+                                           int max_order);
+
+/// include/rt/scene.hpp:130-142 (the table-relevant part)
+struct Trajectory {
+    std::vector<Vec3> waypoints;
+    std::vector<double> speeds;
+    double total_length() const;
+    Vec3 position_at(double s) const;
+};
+/// include/rt/vistable.hpp:82-93
+struct MobileVisEntry {
+    int order = 1;
+    std::string node, node_display;
+    double s_start = 0.0, s_end = 0.0;
+    std::string label_start, label_end, parent, blockage;
+};
+inline constexpr double kTrajectoryStep = 0.5;
+inline constexpr double kBoundaryTolerance = 1e-3;
+/// trajectory_vis_table (include/rt/vistable.hpp:143-148): one GPU call.
+std::vector<MobileVisEntry> trajectory_vis_table(const Trajectory& traj, const InterVisMatrix& matrix,
+                                                 const Scene& scene, int max_order);
+/// closest_diffraction_edge (include/rt/vistable.hpp:131-137)
+std::optional<Edge> closest_diffraction_edge(const Vec3& receiver, const Scene& scene);
+std::optional<Edge> closest_diffraction_edge(const Vec3& receiver, const Scene& scene, const InterVisMatrix& matrix);
+
 // ---------------------------------------------------------------------------
+/// include/rt/raytracer.hpp:51-61
+struct ImageTreeNode {
+    std::string face;
+    Vec3 image;
+    int parent = -1;
+    int depth = 1;
+};
+std::vector<ImageTreeNode> image_tree(const Scene& scene, const Vec3& source, int max_depth);
+
 enum class InteractionKind { Reflection, Diffraction };
 struct Interaction {
     InteractionKind kind = InteractionKind::Reflection;

@@ -198,6 +198,67 @@ int main(int argc, char** argv) {
         }
     std::cout << "illuminated_region: " << nsrc << " sources x " << n << " faces compared" << std::endl;
 
+    // --- point_vis_table, image_tree, closest_diffraction_edge per source ---
+    const int tab_order = max_order < 2 ? max_order : 2;
+    std::vector<vref_row> rrows(1 << 16);
+    for (int s = 0; s < nsrc; ++s) {
+        const double sp[3] = {src[s].x, src[s].y, src[s].z};
+        const auto rows = rt::point_vis_table(src[s], M, *mine, tab_order);
+        const int64_t nrr = vref_point_vis_table(ref, RM, sp, tab_order, rrows.data(), 1 << 16);
+        EXPECT(static_cast<int64_t>(rows.size()) == nrr, "point_vis_table rows " << s);
+        for (int64_t q = 0; q < nrr && q < static_cast<int64_t>(rows.size()); ++q) {
+            const rt::VisTableEntry& g = rows[static_cast<size_t>(q)];
+            const vref_row& r = rrows[static_cast<size_t>(q)];
+            EXPECT(g.order == r.order && static_cast<int>(g.chain.size()) == r.chain_len, "table row " << q);
+            for (int c = 0; c < r.chain_len && c < static_cast<int>(g.chain.size()); ++c)
+                EXPECT(g.chain[c] == id_of(r.chain[c]), "table chain");
+            EXPECT(g.aim == id_of(r.aim) && static_cast<int>(g.plane) == r.plane, "table aim/plane");
+            EXPECT(static_cast<int>(g.verdict) == r.verdict, "table verdict " << s << "," << q);
+            EXPECT(g.ref_display == r.ref_display && g.aim_display == r.aim_display &&
+                       g.parent_display == r.parent_display,
+                   "table displays " << g.ref_display << "/" << r.ref_display);
+        }
+        const auto tree = rt::image_tree(*mine, src[s], 2);
+        std::vector<int32_t> tf(1 << 20), tp(1 << 20), td(1 << 20);
+        std::vector<double> ti(3 << 20);
+        const int64_t nt = vref_image_tree(ref, sp, 2, tf.data(), tp.data(), td.data(), ti.data(), 1 << 20);
+        EXPECT(static_cast<int64_t>(tree.size()) == nt, "image_tree size " << s);
+        for (int64_t q = 0; q < nt && q < static_cast<int64_t>(tree.size()); ++q) {
+            const rt::ImageTreeNode& g = tree[static_cast<size_t>(q)];
+            EXPECT(g.face == id_of(tf[q]) && g.parent == tp[q] && g.depth == td[q], "image_tree node");
+            EXPECT(g.image.x == ti[3 * q] && g.image.y == ti[3 * q + 1] && g.image.z == ti[3 * q + 2], "image");
+        }
+        const auto edge = rt::closest_diffraction_edge(src[s], *mine);
+        const int32_t re = vref_closest_edge(ref, sp);
+        EXPECT(edge.has_value() == (re >= 0), "closest edge presence " << s);
+        if (edge && re >= 0) EXPECT(edge->id == mine->edges()[static_cast<size_t>(re)].id, "closest edge id");
+    }
+    std::cout << "point_vis_table / image_tree / closest_diffraction_edge: " << nsrc << " sources compared"
+              << std::endl;
+
+    // --- trajectory_vis_table along each trace's tx -> rx -----------------
+    std::vector<vref_mobile_row> mrows(1 << 14);
+    for (int t = 0; t < ntr; ++t) {
+        rt::Trajectory traj;
+        traj.waypoints = {tr[t].first, tr[t].second};
+        traj.speeds = {1.0};
+        if (traj.total_length() <= rt::kEps) continue;
+        const auto rows = rt::trajectory_vis_table(traj, M, *mine, tab_order);
+        const double wp[6] = {tr[t].first.x, tr[t].first.y, tr[t].first.z,
+                              tr[t].second.x, tr[t].second.y, tr[t].second.z};
+        const int64_t nm = vref_trajectory_table(ref, RM, 2, wp, tab_order, mrows.data(), 1 << 14);
+        EXPECT(static_cast<int64_t>(rows.size()) == nm, "trajectory rows " << t << ": " << rows.size() << " vs " << nm);
+        for (int64_t q = 0; q < nm && q < static_cast<int64_t>(rows.size()); ++q) {
+            const rt::MobileVisEntry& g = rows[static_cast<size_t>(q)];
+            const vref_mobile_row& r = mrows[static_cast<size_t>(q)];
+            EXPECT(g.order == r.order && g.node == r.node && g.node_display == r.node_display, "mobile node " << q);
+            EXPECT(g.s_start == r.s_start && g.s_end == r.s_end, "mobile s " << q);
+            EXPECT(g.label_start == r.label_start && g.label_end == r.label_end, "mobile labels " << q);
+            EXPECT(g.parent == r.parent && g.blockage == r.blockage, "mobile parent/blockage " << q);
+        }
+    }
+    std::cout << "trajectory_vis_table: " << ntr << " routes compared" << std::endl;
+
     // --- TraceAccelerator up to max_order (+1 via set_max_order) ----------
     rt::InterVisMatrix M2 = M;
     M2.set_max_order(max_order + 1 <= 3 ? max_order + 1 : max_order);

@@ -2,7 +2,8 @@
 the GPU C-ABI) against the unmodified reference (visrt_ref::) in one C++
 program: build_matrix entries (every field: chains, PAR/PER, verdicts,
 angle records incl. edge ids, criterion, subranges, blockers, aim images),
-occlusion_judgment, illuminated_region (all fields incl. atan2 angles) and
+occlusion_judgment, illuminated_region (all fields incl. atan2 angles),
+point_vis_table rows, image_tree, closest_diffraction_edge, trajectory_vis_table and
 TraceAccelerator path sets/stats — bit-exact."""
 import os
 import subprocess
