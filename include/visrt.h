@@ -209,9 +209,10 @@ int visrt_tracer_create(visrt_scene* scene, int max_refl, const uint64_t* admitt
 void visrt_tracer_destroy(visrt_tracer* tracer);
 typedef struct {
     int32_t nrefl;
-    int32_t faces[4];
+    int32_t faces[3];      /* reflecting faces, source side first            */
+    int32_t edge;          /* diffraction edge index (last interaction), -1 none */
     int32_t snap;
-    double points[18];     /* tx, reflection points..., rx */
+    double points[18];     /* tx, reflection points..., [diffraction point], rx */
     double length;
 } visrt_path;
 typedef struct {
@@ -221,8 +222,19 @@ typedef struct {
     int64_t leg_tests;     /* exact segment-vs-face tests run on path legs            */
     float   ms;            /* device time of the whole batch                          */
 } visrt_trace_stats;
+/* flags: VISRT_TRACE_RX_FIXED — one receiver rx[0] for every snapshot;
+ * VISRT_TRACE_DIFFRACTION — allow_diffraction = true: per snapshot the
+ * closest diffraction edge of the receiver (closest_diffraction_edge over the
+ * edges of visrt_tracer_set_edges) adds Engine::attempt's second sequence
+ * per node, ending at the edge's Fermat point (src/raytracer.cpp:174-192,
+ * 367, 383-394). */
+#define VISRT_TRACE_RX_FIXED 0x1
+#define VISRT_TRACE_DIFFRACTION 0x2
 int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const double* rx,
-                int rx_fixed, visrt_trace_stats* stats, void* stream);
+                int flags, visrt_trace_stats* stats, void* stream);
+/* The scene's edges for diffraction (Scene::edges, include/rt/scene.hpp:85-95):
+ * edge e = (a, b) at edge_ab[6e..6e+5]; edge_rank[e] = order of its id string. */
+int visrt_tracer_set_edges(visrt_tracer* tracer, int32_t nedges, const double* edge_ab, const int32_t* edge_rank);
 /* Unfiltered mirror hierarchy image_tree(scene, source, max_depth)
  * (include/rt/raytracer.hpp:51-61, src/raytracer.cpp:458-486): nodes in the
  * reference's depth-first order — face index, parent node (-1 at depth 1),
@@ -246,6 +258,9 @@ int visrt_closest_edges(visrt_scene* scene, int64_t nrx, const double* rx_xyz, i
  * per-snapshot node counts. Any pointer may be NULL; returns the path count. */
 int64_t visrt_trace_results(const visrt_tracer* tracer, int64_t* path_off, visrt_path* paths,
                             int64_t path_cap, int64_t* nodes);
+/* Per snapshot of the last visrt_trace: the closest diffraction edge used
+ * (-1: none / diffraction off). Returns the snapshot count. */
+int64_t visrt_trace_snapshot_edges(const visrt_tracer* tracer, int32_t* snap_edge);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ EXPORTS = [
     "visrt_chain_reach", "visrt_trajectory_table", "visrt_mobile_table_rows", "visrt_mobile_table_destroy",
     "visrt_chain_triples", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results", "visrt_image_tree", "visrt_closest_edges",
+    "visrt_tracer_set_edges", "visrt_trace_snapshot_edges",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -58,7 +59,7 @@ class visrt_names(C.Structure):
 
 
 class visrt_path(C.Structure):
-    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("snap", C.c_int32),
+    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 3), ("edge", C.c_int32), ("snap", C.c_int32),
                 ("points", C.c_double * 18), ("length", C.c_double)]
 
 
@@ -146,6 +147,9 @@ def lib():
                                    C.c_int64, C.POINTER(C.c_int64), C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_closest_edges.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_int32, C.c_void_p, C.c_void_p, _i32p,
                                       C.POINTER(visrt_stats), C.c_void_p]
+    L.visrt_trace_snapshot_edges.restype = C.c_int64
+    L.visrt_trace_snapshot_edges.argtypes = [C.c_void_p, C.c_void_p]
+    L.visrt_tracer_set_edges.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
     L.visrt_trace_results.restype = C.c_int64
     L.visrt_trace_results.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     _lib = L

@@ -304,10 +304,13 @@ class Tracer:
     """rt::TraceAccelerator (include/rt/raytracer.hpp:96-118) over the GPU image
     tree: the chain filter is the admitted matrix (pair_admitted) plus the
     order-2 chains (p, t, a) for max_refl 3. ``trace`` runs a whole batch of
-    snapshots (allow_diffraction = false: the facet soups carry no edges)."""
+    snapshots. ``edges`` (the scene's edges in order, {id, a, b}) enable
+    ``allow_diffraction``: per snapshot the receiver's closest diffraction
+    edge adds the sequences ending at its Fermat point (facet soups carry no
+    edges)."""
 
     def __init__(self, scene: Scene, max_refl: int, admitted_bits: Optional[np.ndarray] = None,
-                 triples: Optional[np.ndarray] = None) -> None:
+                 triples: Optional[np.ndarray] = None, edges: Optional[Sequence[dict]] = None) -> None:
         self.scene = scene
         self.max_refl = max_refl
         if max_refl >= 3 and triples is None:
@@ -320,6 +323,12 @@ class Tracer:
                                         0 if tri is None else len(tri), None if tri is None else tri.ctypes.data,
                                         C.byref(h)))
         self.h = h
+        self.edges = list(edges) if edges else []
+        if self.edges:
+            ab = np.ascontiguousarray(np.array([list(e["a"]) + list(e["b"]) for e in self.edges], np.float64))
+            rank = _ranks([e["id"] for e in self.edges])
+            er = np.ascontiguousarray(np.array([rank[e["id"]] for e in self.edges], np.int32))
+            check(lib().visrt_tracer_set_edges(h, len(self.edges), ab.ctypes.data, er.ctypes.data))
 
     def close(self) -> None:
         if getattr(self, "h", None):
@@ -332,12 +341,14 @@ class Tracer:
         except Exception:
             pass
 
-    def trace_raw(self, tx: np.ndarray, rx: np.ndarray, stream: int = 0):
+    def trace_raw(self, tx: np.ndarray, rx: np.ndarray, stream: int = 0, allow_diffraction: bool = False):
         tx = np.ascontiguousarray(np.asarray(tx, np.float64).reshape(-1, 3))
         rx = np.ascontiguousarray(np.asarray(rx, np.float64).reshape(-1, 3))
-        fixed = 1 if len(rx) == 1 and len(tx) != 1 else 0
+        flags = 1 if len(rx) == 1 and len(tx) != 1 else 0
+        if allow_diffraction:
+            flags |= 2
         st = _capi.visrt_trace_stats()
-        check(lib().visrt_trace(self.h, len(tx), tx.reshape(-1), rx.reshape(-1), fixed, C.byref(st),
+        check(lib().visrt_trace(self.h, len(tx), tx.reshape(-1), rx.reshape(-1), flags, C.byref(st),
                                 C.c_void_p(stream) if stream else None))
         L = lib()
         npaths = L.visrt_trace_results(self.h, None, None, 0, None)
@@ -348,17 +359,18 @@ class Tracer:
         return off, paths, nodes, {"nodes": st.nodes, "sequences": st.sequences, "paths": st.paths,
                                    "leg_tests": st.leg_tests, "ms": st.ms}
 
-    def trace(self, tx: np.ndarray, rx: np.ndarray):
-        """Per snapshot: list of paths {faces, points, length} ordered by face
-        sequence, plus per-snapshot node counts and stats."""
-        off, paths, nodes, st = self.trace_raw(tx, rx)
+    def trace(self, tx: np.ndarray, rx: np.ndarray, allow_diffraction: bool = False):
+        """Per snapshot: list of paths {faces, edge (-1: none), points, length}
+        ordered by face sequence, plus per-snapshot node counts and stats."""
+        off, paths, nodes, st = self.trace_raw(tx, rx, allow_diffraction=allow_diffraction)
         out = []
         for k in range(len(off) - 1):
             row = []
             for q in range(off[k], off[k + 1]):
                 p = paths[q]
-                row.append({"faces": list(p.faces[: p.nrefl]), "points": list(p.points[: 3 * (p.nrefl + 2)]),
-                            "length": p.length})
+                npts = p.nrefl + 2 + (1 if p.edge >= 0 else 0)
+                row.append({"faces": list(p.faces[: p.nrefl]), "edge": int(p.edge),
+                            "points": list(p.points[: 3 * npts]), "length": p.length})
             out.append(row)
         return out, nodes, st
 
@@ -398,9 +410,10 @@ def closest_diffraction_edges(scene: Scene, receivers, edges: Sequence[dict]):
     return out
 
 
-def path_identity(ids: Sequence[str], faces: Sequence[int]) -> str:
-    """Path::identity (src/raytracer.cpp:448-456) for a reflection-only path."""
-    return "LOS" if not faces else "/".join("R:" + ids[f] for f in faces)
+def path_identity(ids: Sequence[str], faces: Sequence[int], edge_id: Optional[str] = None) -> str:
+    """Path::identity (src/raytracer.cpp:448-456): "LOS" or "R:<face>/.../D:<edge>"."""
+    parts = ["R:" + ids[f] for f in faces] + ([f"D:{edge_id}"] if edge_id is not None else [])
+    return "LOS" if not parts else "/".join(parts)
 
 
 def measure_peaks(device: int = 0) -> Tuple[float, float]:

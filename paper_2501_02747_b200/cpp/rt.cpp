@@ -26,6 +26,17 @@ void check(int rc) {
 }
 
 double dot(const Vec3& a, const Vec3& b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+
+// string order -> integer ranks (the C-ABI takes the reference's sort keys as ranks)
+template <class T>
+std::map<T, int32_t> ranks_of(std::vector<T> v) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    std::map<T, int32_t> r;
+    for (size_t k = 0; k < v.size(); ++k) r.emplace(v[k], static_cast<int32_t>(k));
+    return r;
+}
+std::string building_of(const Face& f) { return f.building.empty() ? "ground" : f.building; }
 double norm(const Vec3& a) { return std::sqrt(dot(a, a)); }
 double dot2(const Vec2& a, const Vec2& b) { return a.x * b.x + a.y * b.y; }
 double cross2(const Vec2& a, const Vec2& b) { return a.x * b.y - a.y * b.x; }
@@ -688,6 +699,18 @@ TraceAccelerator::TraceAccelerator(const Scene& scene, const InterVisMatrix& mat
     }
     check(visrt_tracer_create(scene.device_scene(), max_refl, bits.data(), static_cast<int64_t>(tri.size() / 3),
                               tri.empty() ? nullptr : tri.data(), &tracer_));
+    if (!scene.edges().empty()) {   // diffraction candidates (Scene::edges)
+        std::vector<double> ab;
+        std::vector<std::string> ids;
+        for (const Edge& e : scene.edges()) {
+            ab.insert(ab.end(), {e.a.x, e.a.y, e.a.z, e.b.x, e.b.y, e.b.z});
+            ids.push_back(e.id);
+        }
+        const auto rk = ranks_of(ids);
+        std::vector<int32_t> rank;
+        for (const Edge& e : scene.edges()) rank.push_back(rk.at(e.id));
+        check(visrt_tracer_set_edges(tracer_, static_cast<int32_t>(rank.size()), ab.data(), rank.data()));
+    }
 }
 
 TraceAccelerator::~TraceAccelerator() {
@@ -695,7 +718,8 @@ TraceAccelerator::~TraceAccelerator() {
 }
 
 std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<Vec3>& tx, const std::vector<Vec3>& rx,
-                                                             std::vector<TraceStats>* stats) const {
+                                                             std::vector<TraceStats>* stats,
+                                                             bool allow_diffraction) const {
     std::vector<double> t, r;
     for (const Vec3& p : tx) {
         t.push_back(p.x);
@@ -708,12 +732,14 @@ std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<V
         r.push_back(p.z);
     }
     visrt_trace_stats st{};
-    check(visrt_trace(tracer_, static_cast<int64_t>(tx.size()), t.data(), r.data(), rx.size() == 1 ? 1 : 0, &st,
-                      nullptr));
+    const int flags = (rx.size() == 1 ? VISRT_TRACE_RX_FIXED : 0) | (allow_diffraction ? VISRT_TRACE_DIFFRACTION : 0);
+    check(visrt_trace(tracer_, static_cast<int64_t>(tx.size()), t.data(), r.data(), flags, &st, nullptr));
     const int64_t np = visrt_trace_results(tracer_, nullptr, nullptr, 0, nullptr);
     std::vector<int64_t> off(tx.size() + 1), nodes(tx.size());
     std::vector<visrt_path> ps(static_cast<size_t>(np) + 1);
     visrt_trace_results(tracer_, off.data(), ps.data(), np, nodes.data());
+    std::vector<int32_t> sedge(tx.size(), -1);
+    visrt_trace_snapshot_edges(tracer_, sedge.data());
     std::vector<std::vector<Path>> out(tx.size());
     for (size_t k = 0; k < tx.size(); ++k) {
         for (int64_t q = off[k]; q < off[k + 1]; ++q) {
@@ -721,9 +747,13 @@ std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<V
             Path p;
             p.source = tx[k];
             p.receiver = rx.size() == 1 ? rx[0] : rx[k];
-            for (int i = 0; i < vp.nrefl + 2; ++i) p.points.push_back({vp.points[3 * i], vp.points[3 * i + 1], vp.points[3 * i + 2]});
+            const int npts = vp.nrefl + 2 + (vp.edge >= 0 ? 1 : 0);
+            for (int i = 0; i < npts; ++i) p.points.push_back({vp.points[3 * i], vp.points[3 * i + 1], vp.points[3 * i + 2]});
             for (int i = 0; i < vp.nrefl; ++i)
                 p.interactions.push_back({InteractionKind::Reflection, scene_->face(vp.faces[i]).id, p.points[1 + i]});
+            if (vp.edge >= 0)
+                p.interactions.push_back({InteractionKind::Diffraction, scene_->edges()[static_cast<size_t>(vp.edge)].id,
+                                          p.points[1 + vp.nrefl]});
             p.length = vp.length;
             p.delay = vp.length / kSpeedOfLight;
             out[k].push_back(std::move(p));
@@ -732,7 +762,7 @@ std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<V
         if (stats) {
             TraceStats ts;
             ts.nodes_expanded = nodes[k];
-            ts.sequences_checked = nodes[k] + 1;
+            ts.sequences_checked = (nodes[k] + 1) * (sedge[k] >= 0 ? 2 : 1);
             ts.paths_found = static_cast<long long>(out[k].size());
             stats->push_back(ts);
         }
@@ -742,10 +772,8 @@ std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<V
 
 std::vector<Path> TraceAccelerator::trace(const Vec3& tx, const Vec3& rx, bool allow_diffraction,
                                           TraceStats* stats) const {
-    if (allow_diffraction && !scene_->edges().empty())
-        throw std::invalid_argument("TraceAccelerator: the diffraction branch is not part of this build");
     std::vector<TraceStats> st;
-    auto out = trace_batch({tx}, {rx}, stats ? &st : nullptr);
+    auto out = trace_batch({tx}, {rx}, stats ? &st : nullptr, allow_diffraction);
     if (stats) *stats = st[0];
     return std::move(out[0]);
 }
@@ -838,17 +866,6 @@ Vec3 Trajectory::position_at(double s) const {
     return waypoints.back();
 }
 
-namespace {
-template <class T>
-std::map<T, int32_t> ranks_of(std::vector<T> v) {
-    std::sort(v.begin(), v.end());
-    v.erase(std::unique(v.begin(), v.end()), v.end());
-    std::map<T, int32_t> r;
-    for (size_t k = 0; k < v.size(); ++k) r.emplace(v[k], static_cast<int32_t>(k));
-    return r;
-}
-std::string building_of(const Face& f) { return f.building.empty() ? "ground" : f.building; }
-}  // namespace
 
 std::vector<MobileVisEntry> trajectory_vis_table(const Trajectory& traj, const InterVisMatrix& matrix,
                                                  const Scene& scene, int max_order) {

@@ -281,12 +281,14 @@ class TraceAccelerator {
     ~TraceAccelerator();
     TraceAccelerator(const TraceAccelerator&) = delete;
     TraceAccelerator& operator=(const TraceAccelerator&) = delete;
-    /// allow_diffraction must be false for scenes without edges (facet soups).
+    /// allow_diffraction: the receiver's closest diffraction edge adds the
+    /// sequences ending at its Fermat point (facet soups have no edges).
     std::vector<Path> trace(const Vec3& tx, const Vec3& rx, bool allow_diffraction,
                             TraceStats* stats = nullptr) const;
     /// Batched form: one GPU expansion over every snapshot (rx.size() == 1: fixed receiver).
     std::vector<std::vector<Path>> trace_batch(const std::vector<Vec3>& tx, const std::vector<Vec3>& rx,
-                                               std::vector<TraceStats>* stats = nullptr) const;
+                                               std::vector<TraceStats>* stats = nullptr,
+                                               bool allow_diffraction = false) const;
     int max_reflections() const { return max_refl_; }
 
   private:

@@ -186,89 +186,101 @@ extern "C" int visrt_image_tree(visrt_scene* sc, const double* src, int32_t max_
 // sightline, and the reference's sequential selection (distance with kEps
 // slack, ties to the lowest edge id) runs on the host over those answers —
 // the sweep result of an edge the loop skips is simply not read.
+namespace visrt {
+void closest_edges(const visrt_scene* sc, int64_t nrx, const double* rx_xyz, int32_t nedges, const double* edge_ab,
+                   const int32_t* edge_rank, int32_t* out_edge, float* ms_out, int64_t* tests_out, cudaStream_t st) {
+    const DevScene& ds = scene_dev(sc);
+    if (nedges > 0 && (!edge_ab || !edge_rank)) throw UsageError("null edge arrays");
+    const long long nseg = nrx * static_cast<long long>(nedges);
+    std::vector<double> A(3 * static_cast<size_t>(nseg)), B(3 * static_cast<size_t>(nseg)), D(static_cast<size_t>(nseg));
+    for (int64_t r = 0; r < nrx; ++r) {
+        const double* p = rx_xyz + 3 * r;
+        for (int32_t e = 0; e < nedges; ++e) {
+            const double* a = edge_ab + 6 * static_cast<size_t>(e);
+            const double* b = a + 3;
+            // closest_point_on_segment (src/vistable.cpp:529-535)
+            const double dx = b[0] - a[0], dy = b[1] - a[1], dz = b[2] - a[2];
+            const double len2 = dx * dx + dy * dy + dz * dz;
+            double c[3];
+            if (len2 <= kEps * kEps) {
+                c[0] = a[0]; c[1] = a[1]; c[2] = a[2];
+            } else {
+                const double t = std::clamp(((p[0] - a[0]) * dx + (p[1] - a[1]) * dy + (p[2] - a[2]) * dz) / len2,
+                                            0.0, 1.0);
+                c[0] = a[0] + dx * t; c[1] = a[1] + dy * t; c[2] = a[2] + dz * t;
+            }
+            const size_t q = static_cast<size_t>(r) * nedges + e;
+            const double ex = p[0] - c[0], ey = p[1] - c[1], ez = p[2] - c[2];
+            D[q] = std::sqrt(ex * ex + ey * ey + ez * ez);   // distance(receiver, cp)
+            for (int k = 0; k < 3; ++k) {
+                A[3 * q + k] = p[k];
+                B[3 * q + k] = c[k];
+            }
+        }
+    }
+    std::vector<uint8_t> clear(static_cast<size_t>(nseg), 0);
+    float ms = 0.f;
+    int64_t tests = 0;
+    if (nseg > 0) {
+        std::vector<void*> tmp;
+        FreeGuard guard{tmp};
+        double* dA = dalloc<double>(A.size(), tmp);
+        double* dB = dalloc<double>(B.size(), tmp);
+        uint8_t* dC = dalloc<uint8_t>(clear.size(), tmp);
+        unsigned long long* d_ctr = dalloc<unsigned long long>(2, tmp);
+        ck(cudaMemcpyAsync(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemsetAsync(d_ctr, 0, 16, st), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        ck(launch_segments_clear(ds, nseg, dA, dB, dC, d_ctr, scene_device(sc), st), "k_segments_clear");
+        cudaEventRecord(e1, st);
+        unsigned long long ctr[2];
+        ck(cudaMemcpyAsync(clear.data(), dC, clear.size(), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(ctr, d_ctr, 16, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        tests = static_cast<int64_t>(ctr[1]);
+    }
+    // the reference's sequential selection (src/vistable.cpp:548-558)
+    for (int64_t r = 0; r < nrx; ++r) {
+        int best = -1;
+        double best_dist = 0.0;
+        for (int32_t e = 0; e < nedges; ++e) {
+            const size_t q = static_cast<size_t>(r) * nedges + e;
+            const double d = D[q];
+            if (best >= 0 && d > best_dist + kEps) continue;
+            if (!clear[q]) continue;
+            if (best < 0 || d < best_dist - kEps ||
+                (std::abs(d - best_dist) <= kEps && edge_rank[e] < edge_rank[best])) {
+                best = e;
+                best_dist = d;
+            }
+        }
+        out_edge[r] = best;
+    }
+    if (ms_out) *ms_out = ms;
+    if (tests_out) *tests_out = tests;
+}
+}  // namespace visrt
+
 extern "C" int visrt_closest_edges(visrt_scene* sc, int64_t nrx, const double* rx_xyz, int32_t nedges,
                                    const double* edge_ab, const int32_t* edge_rank, int32_t* out_edge,
                                    visrt_stats* stats, void* stream) {
     using namespace visrt;
     return capi_guard([&] {
         ScopedDevice dev(sc);
-        const DevScene& ds = scene_dev(sc);
-        cudaStream_t st = static_cast<cudaStream_t>(stream);
-        if (nedges > 0 && (!edge_ab || !edge_rank)) throw UsageError("null edge arrays");
-        const long long nseg = nrx * static_cast<long long>(nedges);
-        std::vector<double> A(3 * static_cast<size_t>(nseg)), B(3 * static_cast<size_t>(nseg)), D(static_cast<size_t>(nseg));
-        for (int64_t r = 0; r < nrx; ++r) {
-            const double* p = rx_xyz + 3 * r;
-            for (int32_t e = 0; e < nedges; ++e) {
-                const double* a = edge_ab + 6 * static_cast<size_t>(e);
-                const double* b = a + 3;
-                // closest_point_on_segment (src/vistable.cpp:529-535)
-                const double dx = b[0] - a[0], dy = b[1] - a[1], dz = b[2] - a[2];
-                const double len2 = dx * dx + dy * dy + dz * dz;
-                double c[3];
-                if (len2 <= kEps * kEps) {
-                    c[0] = a[0]; c[1] = a[1]; c[2] = a[2];
-                } else {
-                    const double t = std::clamp(((p[0] - a[0]) * dx + (p[1] - a[1]) * dy + (p[2] - a[2]) * dz) / len2,
-                                                0.0, 1.0);
-                    c[0] = a[0] + dx * t; c[1] = a[1] + dy * t; c[2] = a[2] + dz * t;
-                }
-                const size_t q = static_cast<size_t>(r) * nedges + e;
-                const double ex = p[0] - c[0], ey = p[1] - c[1], ez = p[2] - c[2];
-                D[q] = std::sqrt(ex * ex + ey * ey + ez * ez);   // distance(receiver, cp)
-                for (int k = 0; k < 3; ++k) {
-                    A[3 * q + k] = p[k];
-                    B[3 * q + k] = c[k];
-                }
-            }
-        }
-        std::vector<uint8_t> clear(static_cast<size_t>(nseg), 0);
         float ms = 0.f;
         int64_t tests = 0;
-        if (nseg > 0) {
-            std::vector<void*> tmp;
-            FreeGuard guard{tmp};
-            double* dA = dalloc<double>(A.size(), tmp);
-            double* dB = dalloc<double>(B.size(), tmp);
-            uint8_t* dC = dalloc<uint8_t>(clear.size(), tmp);
-            unsigned long long* d_ctr = dalloc<unsigned long long>(2, tmp);
-            ck(cudaMemcpyAsync(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
-            ck(cudaMemcpyAsync(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
-            ck(cudaMemsetAsync(d_ctr, 0, 16, st), "memset");
-            cudaEvent_t e0, e1;
-            cudaEventCreate(&e0);
-            cudaEventCreate(&e1);
-            cudaEventRecord(e0, st);
-            ck(launch_segments_clear(ds, nseg, dA, dB, dC, d_ctr, scene_device(sc), st), "k_segments_clear");
-            cudaEventRecord(e1, st);
-            unsigned long long ctr[2];
-            ck(cudaMemcpyAsync(clear.data(), dC, clear.size(), cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemcpyAsync(ctr, d_ctr, 16, cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaStreamSynchronize(st), "sync");
-            cudaEventElapsedTime(&ms, e0, e1);
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-            tests = static_cast<int64_t>(ctr[1]);
-        }
-        for (int64_t r = 0; r < nrx; ++r) {
-            int best = -1;
-            double best_dist = 0.0;
-            for (int32_t e = 0; e < nedges; ++e) {
-                const size_t q = static_cast<size_t>(r) * nedges + e;
-                const double d = D[q];
-                if (best >= 0 && d > best_dist + kEps) continue;
-                if (!clear[q]) continue;
-                if (best < 0 || d < best_dist - kEps ||
-                    (std::abs(d - best_dist) <= kEps && edge_rank[e] < edge_rank[best])) {
-                    best = e;
-                    best_dist = d;
-                }
-            }
-            out_edge[r] = best;
-        }
+        closest_edges(sc, nrx, rx_xyz, nedges, edge_ab, edge_rank, out_edge, &ms, &tests,
+                      static_cast<cudaStream_t>(stream));
         if (stats) {
             *stats = visrt_stats{};
-            stats->pairs = nseg;
+            stats->pairs = nrx * static_cast<int64_t>(nedges);
             stats->tests_exec = tests;
             stats->ms = ms;
         }

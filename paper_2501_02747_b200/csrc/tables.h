@@ -102,4 +102,9 @@ cudaError_t launch_beam_rows(const BeamArgs& a, cudaStream_t st);
 cudaError_t launch_segments_clear(const DevScene& s, long long nseg, const double* A, const double* B,
                                   uint8_t* clear, unsigned long long* counter, int device, cudaStream_t st);
 
+// closest_diffraction_edge for a batch of receivers (imagetree.cu): out_edge[r]
+// = edge index or -1; ms / tests of the GPU sightline sweep.
+void closest_edges(const visrt_scene* sc, int64_t nrx, const double* rx_xyz, int32_t nedges, const double* edge_ab,
+                   const int32_t* edge_rank, int32_t* out_edge, float* ms, int64_t* tests, cudaStream_t st);
+
 }  // namespace visrt

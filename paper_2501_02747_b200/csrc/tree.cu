@@ -30,6 +30,7 @@
 #include "capi_internal.h"
 #include "device.h"
 #include "sweep.h"
+#include "tables.h"
 
 namespace visrt {
 
@@ -39,8 +40,8 @@ struct TreeNode {
 };
 
 struct Cand {
-    int32_t snap, depth, f[3], pad;
-    double pts[15];
+    int32_t snap, depth, f[3], edge;   // edge: diffraction edge index (-1: ends at the receiver)
+    double pts[18];                    // tx, reflections..., [diffraction point], rx
     double length;
 };
 
@@ -70,6 +71,8 @@ struct TreeArgs {
     unsigned long long* npaths;
     long long path_cap;
     unsigned long long* counter;          // [0] cursor, [1] leg tests
+    const int32_t* snap_edge;             // [total snapshots] closest diffraction edge or -1 (nullptr: none)
+    const double* edge_ab;                // [nedges][6]
 };
 
 __device__ __forceinline__ double sdist_face(const DevScene& s, int f, double x, double y, double z) {
@@ -187,8 +190,43 @@ __global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a) {
     }
 }
 
-// resolve_sequence up to the occlusion tests: one thread per node (or per
-// snapshot root for the line-of-sight sequence).
+// fermat_point_on_edge (src/raytracer.cpp:174-192)
+__device__ void fermat_point(const double* E, const double* from, const double* to, double* p) {
+    const double dx = dsub(E[3], E[0]), dy = dsub(E[4], E[1]), dz = dsub(E[5], E[2]);
+    const double len = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+    if (len <= kEps) {
+        p[0] = E[0]; p[1] = E[1]; p[2] = E[2];
+        return;
+    }
+    const double il = __ddiv_rn(1.0, len);
+    const double ux = dmul(dx, il), uy = dmul(dy, il), uz = dmul(dz, il);
+    const double fx = dsub(from[0], E[0]), fy = dsub(from[1], E[1]), fz = dsub(from[2], E[2]);
+    const double tx = dsub(to[0], E[0]), ty = dsub(to[1], E[1]), tz = dsub(to[2], E[2]);
+    const double A = dadd(dadd(dmul(fx, ux), dmul(fy, uy)), dmul(fz, uz));
+    const double B = dadd(dadd(dmul(tx, ux), dmul(ty, uy)), dmul(tz, uz));
+    const double ax = dsub(fx, dmul(ux, A)), ay = dsub(fy, dmul(uy, A)), az = dsub(fz, dmul(uz, A));
+    const double bx = dsub(tx, dmul(ux, B)), by = dsub(ty, dmul(uy, B)), bz = dsub(tz, dmul(uz, B));
+    const double ra = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
+    const double rb = __dsqrt_rn(dadd(dadd(dmul(bx, bx), dmul(by, by)), dmul(bz, bz)));
+    double t;
+    if (dadd(ra, rb) <= kEps) t = dmul(0.5, dadd(A, B));
+    else t = __ddiv_rn(dadd(dmul(A, rb), dmul(B, ra)), dadd(ra, rb));
+    double c = __ddiv_rn(t, len);
+    c = c < 0.0 ? 0.0 : (1.0 < c ? 1.0 : c);   // std::clamp(t / len, 0, 1)
+    p[0] = dadd(E[0], dmul(dx, c));
+    p[1] = dadd(E[1], dmul(dy, c));
+    p[2] = dadd(E[2], dmul(dz, c));
+}
+
+__device__ __forceinline__ double dist3(const double* a, const double* b) {
+    const double x = dsub(a[0], b[0]), y = dsub(a[1], b[1]), z = dsub(a[2], b[2]);
+    return __dsqrt_rn(dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z)));
+}
+
+// resolve_sequence up to the occlusion tests (src/raytracer.cpp:205-278): one
+// thread per node (or per snapshot root for the line-of-sight sequence); with
+// a diffraction edge for the snapshot, Engine::attempt's second sequence
+// (ending at the edge's Fermat point) is unfolded too (383-394).
 template <int MAXV>
 __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
@@ -215,10 +253,10 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
         img[0][0] = T[0];
         img[0][1] = T[1];
         img[0][2] = T[2];
-        bool ok = true;
-        for (int k = 0; k < d && ok; ++k) {
+        bool fwd = true;
+        for (int k = 0; k < d && fwd; ++k) {
             if (sdist_face(s, f[k], img[k][0], img[k][1], img[k][2]) <= kEps) {
-                ok = false;
+                fwd = false;
                 break;
             }
             img[k + 1][0] = img[k][0];
@@ -226,62 +264,80 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             img[k + 1][2] = img[k][2];
             mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
         }
-        double refl[3][3];
-        double cx = Rx[0], cy = Rx[1], cz = Rx[2];
-        for (int k = d - 1; k >= 0 && ok; --k) {
-            const double da = sdist_face(s, f[k], cx, cy, cz);
-            const double db = sdist_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
-            if (dmul(da, db) >= 0.0) {   // segment_plane_crossing, src/geom.cpp:182-189
-                ok = false;
-                break;
+        if (!fwd) continue;
+        const int edge = a.snap_edge ? a.snap_edge[snap] : -1;
+        for (int v = 0; v < (edge >= 0 ? 2 : 1); ++v) {
+            bool ok = true;
+            double target[3] = {Rx[0], Rx[1], Rx[2]};
+            if (v == 1) {
+                double p[3];
+                fermat_point(a.edge_ab + 6 * static_cast<size_t>(edge), img[d], Rx, p);
+                if (dist3(p, Rx) <= kEps || dist3(p, img[d]) <= kEps) continue;
+                target[0] = p[0];
+                target[1] = p[1];
+                target[2] = p[2];
             }
-            const double tt = __ddiv_rn(da, dsub(da, db));
-            const double px = dadd(cx, dmul(dsub(img[k + 1][0], cx), tt));
-            const double py = dadd(cy, dmul(dsub(img[k + 1][1], cy), tt));
-            const double pz = dadd(cz, dmul(dsub(img[k + 1][2], cz), tt));
-            if (!rec_contains<MAXV>(s.rec + static_cast<size_t>(f[k]) * STRIDE, px, py, pz)) {
-                ok = false;
-                break;
+            double refl[3][3];
+            double cx = target[0], cy = target[1], cz = target[2];
+            for (int k = d - 1; k >= 0 && ok; --k) {
+                const double da = sdist_face(s, f[k], cx, cy, cz);
+                const double db = sdist_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
+                if (dmul(da, db) >= 0.0) {   // segment_plane_crossing, src/geom.cpp:182-189
+                    ok = false;
+                    break;
+                }
+                const double tt = __ddiv_rn(da, dsub(da, db));
+                const double px = dadd(cx, dmul(dsub(img[k + 1][0], cx), tt));
+                const double py = dadd(cy, dmul(dsub(img[k + 1][1], cy), tt));
+                const double pz = dadd(cz, dmul(dsub(img[k + 1][2], cz), tt));
+                if (!rec_contains<MAXV>(s.rec + static_cast<size_t>(f[k]) * STRIDE, px, py, pz)) {
+                    ok = false;
+                    break;
+                }
+                refl[k][0] = px;
+                refl[k][1] = py;
+                refl[k][2] = pz;
+                cx = px;
+                cy = py;
+                cz = pz;
             }
-            refl[k][0] = px;
-            refl[k][1] = py;
-            refl[k][2] = pz;
-            cx = px;
-            cy = py;
-            cz = pz;
+            if (!ok) continue;
+            Cand c;
+            c.snap = snap;
+            c.depth = d;
+            c.f[0] = f[0];
+            c.f[1] = f[1];
+            c.f[2] = f[2];
+            c.edge = v ? edge : -1;
+            c.pts[0] = T[0];
+            c.pts[1] = T[1];
+            c.pts[2] = T[2];
+            for (int k = 0; k < d; ++k) {
+                c.pts[3 * (k + 1)] = refl[k][0];
+                c.pts[3 * (k + 1) + 1] = refl[k][1];
+                c.pts[3 * (k + 1) + 2] = refl[k][2];
+            }
+            int np = d + 1;
+            if (v) {
+                c.pts[3 * np] = target[0];
+                c.pts[3 * np + 1] = target[1];
+                c.pts[3 * np + 2] = target[2];
+                ++np;
+            }
+            c.pts[3 * np] = Rx[0];
+            c.pts[3 * np + 1] = Rx[1];
+            c.pts[3 * np + 2] = Rx[2];
+            double length = 0.0;
+            for (int i = 0; i < np && ok; ++i) {
+                const double seg = dist3(c.pts + 3 * i, c.pts + 3 * (i + 1));
+                if (seg <= kEps) ok = false;
+                length = dadd(length, seg);
+            }
+            if (!ok) continue;
+            c.length = length;
+            const unsigned long long slot = atomicAdd(a.ncand, 1ull);
+            if (static_cast<long long>(slot) < a.cand_cap) a.cand[slot] = c;
         }
-        if (!ok) continue;
-        Cand c;
-        c.snap = snap;
-        c.depth = d;
-        c.f[0] = f[0];
-        c.f[1] = f[1];
-        c.f[2] = f[2];
-        c.pad = 0;
-        c.pts[0] = T[0];
-        c.pts[1] = T[1];
-        c.pts[2] = T[2];
-        for (int k = 0; k < d; ++k) {
-            c.pts[3 * (k + 1)] = refl[k][0];
-            c.pts[3 * (k + 1) + 1] = refl[k][1];
-            c.pts[3 * (k + 1) + 2] = refl[k][2];
-        }
-        c.pts[3 * (d + 1)] = Rx[0];
-        c.pts[3 * (d + 1) + 1] = Rx[1];
-        c.pts[3 * (d + 1) + 2] = Rx[2];
-        double length = 0.0;
-        for (int i = 0; i <= d && ok; ++i) {
-            const double dx = dsub(c.pts[3 * i], c.pts[3 * (i + 1)]);
-            const double dy = dsub(c.pts[3 * i + 1], c.pts[3 * (i + 1) + 1]);
-            const double dz = dsub(c.pts[3 * i + 2], c.pts[3 * (i + 1) + 2]);
-            const double seg = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
-            if (seg <= kEps) ok = false;
-            length = dadd(length, seg);
-        }
-        if (!ok) continue;
-        c.length = length;
-        const unsigned long long slot = atomicAdd(a.ncand, 1ull);
-        if (static_cast<long long>(slot) < a.cand_cap) a.cand[slot] = c;
     }
 }
 
@@ -313,9 +369,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
             p.faces[0] = c.f[0];
             p.faces[1] = c.f[1];
             p.faces[2] = c.f[2];
-            p.faces[3] = -1;
+            p.edge = c.edge;
             p.snap = c.snap;
-            for (int i = 0; i < 18; ++i) p.points[i] = i < 3 * (c.depth + 2) ? c.pts[i] : 0.0;
+            const int npts = c.depth + 2 + (c.edge >= 0 ? 1 : 0);
+            for (int i = 0; i < 18; ++i) p.points[i] = i < 3 * npts ? c.pts[i] : 0.0;
             p.length = c.length;
             a.paths[slot] = p;
         }
@@ -345,7 +402,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
             }
             const Cand& c = a.cand[cid];
             sw.start(make_segf(s, ax, ay, az, bx, by, bz), -1, -1,
-                     home_chunk(s, leg == 0 ? (c.depth ? c.f[0] : -1) : c.f[leg - 1]), ctx.nchunks);
+                     home_chunk(s, leg == 0 ? (c.depth ? c.f[0] : -1) : (leg - 1 < c.depth ? c.f[leg - 1] : -1)),
+                     ctx.nchunks);
             return;
         }
     };
@@ -362,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
                     exhausted = true;
                 } else {
                     cid = my;
-                    legs = a.cand[my].depth + 1;
+                    legs = a.cand[my].depth + 1 + (a.cand[my].edge >= 0 ? 1 : 0);
                     leg = 0;
                     active = true;
                     start_leg();
@@ -443,6 +501,10 @@ struct visrt_tracer {
     int32_t* idx2 = nullptr;
     int32_t* obl = nullptr;
     int32_t nobl = 0;
+    // diffraction edges (visrt_tracer_set_edges)
+    std::vector<double> edge_ab;
+    std::vector<int32_t> edge_rank;
+    double* d_edge_ab = nullptr;
     // frontier / candidate / path buffers, allocated on the first trace
     visrt::TreeNode* lvl[2] = {nullptr, nullptr};
     visrt::Cand* cand = nullptr;
@@ -452,6 +514,7 @@ struct visrt_tracer {
     std::vector<visrt_path> paths;
     std::vector<int64_t> path_off;
     std::vector<int64_t> nodes;
+    std::vector<int32_t> snap_edge;   // per snapshot diffraction edge of the last trace (empty: none)
     ~visrt_tracer() {
         for (void* p : allocs) cudaFree(p);
     }
@@ -537,6 +600,20 @@ extern "C" int visrt_tracer_create(visrt_scene* sc, int max_refl, const uint64_t
 
 extern "C" void visrt_tracer_destroy(visrt_tracer* t) { delete t; }
 
+extern "C" int visrt_tracer_set_edges(visrt_tracer* tr, int32_t nedges, const double* edge_ab,
+                                      const int32_t* edge_rank) {
+    return visrt::capi_guard([&] {
+        if (!tr) throw visrt::UsageError("null tracer");
+        visrt::ScopedDevice dev(tr->scene);
+        if (nedges > 0 && (!edge_ab || !edge_rank)) throw visrt::UsageError("null edge arrays");
+        tr->edge_ab.assign(edge_ab, edge_ab + 6 * static_cast<size_t>(std::max(nedges, 0)));
+        tr->edge_rank.assign(edge_rank, edge_rank + std::max(nedges, 0));
+        tr->d_edge_ab = visrt::dalloc<double>(std::max<size_t>(tr->edge_ab.size(), 1), tr->allocs);
+        if (nedges > 0)
+            ck(cudaMemcpy(tr->d_edge_ab, tr->edge_ab.data(), tr->edge_ab.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    });
+}
+
 namespace {
 
 // Scene::inside_building (src/scene.cpp:199-211) for closed-shell scenes.
@@ -560,7 +637,7 @@ bool inside_building(const visrt::HostScene& hs, const double* p) {
 
 }  // namespace
 
-extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, const double* rx, int rx_fixed,
+extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, const double* rx, int flags,
                            visrt_trace_stats* stats, void* stream) {
     return visrt::capi_guard([&] {
         if (!tr) throw visrt::UsageError("null tracer");
@@ -569,6 +646,8 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         const visrt::HostScene& hs = visrt::scene_host(tr->scene);
         const visrt::DevScene& ds = visrt::scene_dev(tr->scene);
         const int device = visrt::scene_device(tr->scene);
+        const int rx_fixed = (flags & VISRT_TRACE_RX_FIXED) ? 1 : 0;
+        const bool diffraction = (flags & VISRT_TRACE_DIFFRACTION) != 0;
         // Engine ctor placement checks (src/raytracer.cpp:355-363)
         for (int64_t k = 0; k < nsnap; ++k) {
             const double* T = tx + 3 * k;
@@ -585,6 +664,19 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         double* d_rx = visrt::dalloc<double>(static_cast<size_t>(rx_fixed ? 1 : nsnap) * 3, tmp);
         ck(cudaMemcpyAsync(d_tx, tx, nsnap * 24, cudaMemcpyHostToDevice, st), "H2D tx");
         ck(cudaMemcpyAsync(d_rx, rx, (rx_fixed ? 1 : nsnap) * 24, cudaMemcpyHostToDevice, st), "H2D rx");
+        // Engine ctor: edge_ = closest_diffraction_edge(rx, scene) when allowed (src/raytracer.cpp:367)
+        std::vector<int32_t> snap_edge;
+        int32_t* d_snap_edge = nullptr;
+        if (diffraction && !tr->edge_rank.empty()) {
+            const int64_t nrx = rx_fixed ? 1 : nsnap;
+            std::vector<int32_t> e(static_cast<size_t>(std::max<int64_t>(nrx, 1)), -1);
+            visrt::closest_edges(tr->scene, nrx, rx, static_cast<int32_t>(tr->edge_rank.size()), tr->edge_ab.data(),
+                                 tr->edge_rank.data(), e.data(), nullptr, nullptr, st);
+            snap_edge.resize(static_cast<size_t>(nsnap));
+            for (int64_t k = 0; k < nsnap; ++k) snap_edge[k] = rx_fixed ? e[0] : e[k];
+            d_snap_edge = visrt::dalloc<int32_t>(snap_edge.size(), tmp);
+            ck(cudaMemcpyAsync(d_snap_edge, snap_edge.data(), snap_edge.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+        }
         unsigned long long* d_nodes = visrt::dalloc<unsigned long long>(std::max<int64_t>(nsnap, 1), tmp);
         ck(cudaMemsetAsync(d_nodes, 0, std::max<int64_t>(nsnap, 1) * 8, st), "memset");
         unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(8, tmp);   // nout, ncand, npaths, cursor, tests
@@ -623,6 +715,8 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         a.cand_cap = cand_cap;
         a.paths = d_paths;
         a.path_cap = path_cap;
+        a.snap_edge = d_snap_edge;
+        a.edge_ab = tr->d_edge_ab;
         std::vector<visrt_path> host_paths;
         int64_t total_nodes = 0, total_seq = 0, leg_tests = 0;
         unsigned long long* c_nout = d_ctr + 0;
@@ -718,7 +812,9 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         std::sort(host_paths.begin(), host_paths.end(), [](const visrt_path& x, const visrt_path& y) {
             if (x.snap != y.snap) return x.snap < y.snap;
             if (x.nrefl != y.nrefl) return x.nrefl < y.nrefl;
-            return std::lexicographical_compare(x.faces, x.faces + x.nrefl, y.faces, y.faces + y.nrefl);
+            if (!std::equal(x.faces, x.faces + x.nrefl, y.faces))
+                return std::lexicographical_compare(x.faces, x.faces + x.nrefl, y.faces, y.faces + y.nrefl);
+            return x.edge < y.edge;
         });
         tr->nsnap = nsnap;
         tr->paths = std::move(host_paths);
@@ -726,10 +822,13 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         for (const auto& p : tr->paths) tr->path_off[p.snap + 1]++;
         for (int64_t k = 0; k < nsnap; ++k) tr->path_off[k + 1] += tr->path_off[k];
         tr->nodes.assign(nsnap, 0);
+        total_seq = 0;   // resolve_sequence calls: (nodes + LOS) x (1 + diffraction attempt)
         for (int64_t k = 0; k < nsnap; ++k) {
             tr->nodes[k] = static_cast<int64_t>(nodes[k]);
             total_nodes += tr->nodes[k];
+            total_seq += (tr->nodes[k] + 1) * ((!snap_edge.empty() && snap_edge[k] >= 0) ? 2 : 1);
         }
+        tr->snap_edge = snap_edge;
         if (stats) {
             stats->nodes = total_nodes;
             stats->sequences = total_seq;
@@ -747,4 +846,11 @@ extern "C" int64_t visrt_trace_results(const visrt_tracer* tr, int64_t* path_off
     if (paths) std::copy_n(tr->paths.begin(), std::min<int64_t>(cap, tr->paths.size()), paths);
     if (nodes) std::copy(tr->nodes.begin(), tr->nodes.end(), nodes);
     return static_cast<int64_t>(tr->paths.size());
+}
+
+extern "C" int64_t visrt_trace_snapshot_edges(const visrt_tracer* tr, int32_t* snap_edge) {
+    if (!tr) return -1;
+    if (snap_edge)
+        for (int64_t k = 0; k < tr->nsnap; ++k) snap_edge[k] = tr->snap_edge.empty() ? -1 : tr->snap_edge[k];
+    return tr->nsnap;
 }

@@ -266,14 +266,17 @@ int main(int argc, char** argv) {
     for (int order = 1; order <= M2.max_order(); ++order) {
         rt::TraceAccelerator acc(*mine, M2, order);
         void* RA = vref_accel_create(ref, RM, order);
-        for (int t = 0; t < ntr; ++t) {
+        for (int t = 0; t < 2 * ntr; ++t) {
+            const bool diff = t >= ntr;   // second pass: allow_diffraction = true
+            if (diff && mine->edges().empty()) break;
+            const auto& trc = tr[t % ntr];
             rt::TraceStats st;
-            const auto paths = acc.trace(tr[t].first, tr[t].second, false, &st);
+            const auto paths = acc.trace(trc.first, trc.second, diff, &st);
             std::vector<vref_path> rp(16384);
             int64_t rst[4];
-            const double tx[3] = {tr[t].first.x, tr[t].first.y, tr[t].first.z};
-            const double rx[3] = {tr[t].second.x, tr[t].second.y, tr[t].second.z};
-            const int64_t np = vref_accel_trace(ref, RA, tx, rx, 0, rp.data(), 16384, rst);
+            const double tx[3] = {trc.first.x, trc.first.y, trc.first.z};
+            const double rx[3] = {trc.second.x, trc.second.y, trc.second.z};
+            const int64_t np = vref_accel_trace(ref, RA, tx, rx, diff ? 1 : 0, rp.data(), 16384, rst);
             EXPECT(static_cast<int64_t>(paths.size()) == np, "path count order " << order << " trace " << t);
             EXPECT(st.nodes_expanded == rst[0] && st.sequences_checked == rst[1], "trace stats " << order << "," << t);
             for (int64_t q = 0; q < np && q < static_cast<int64_t>(paths.size()); ++q) {
@@ -288,7 +291,8 @@ int main(int argc, char** argv) {
         }
         vref_accel_free(RA);
     }
-    std::cout << "TraceAccelerator: orders 1.." << M2.max_order() << " x " << ntr << " traces compared" << std::endl;
+    std::cout << "TraceAccelerator: orders 1.." << M2.max_order() << " x " << ntr
+              << " traces compared (+ allow_diffraction where the scene has edges)" << std::endl;
     vref_matrix_free(RM);
     vref_scene_free(ref);
     std::cout << (g_bad ? "FAIL " : "OK ") << g_bad << " mismatches" << std::endl;

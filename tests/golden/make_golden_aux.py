@@ -50,8 +50,34 @@ def main() -> None:
         edges.append({"scene": name, "receivers": [list(p) for p in pts],
                       "edge": [r.closest_edge(np.asarray(p, np.float64)) for p in pts]})
         print(name, len(es), "edges")
+    # TraceAccelerator::trace with allow_diffraction = true (proj/src/raytracer.cpp:342-444)
+    diff = []
+    djobs = {"two_buildings": [((3, 15, 2), (7, 16, 3)), ((5, -5, 2), (5, 15, 2)), ((-5, 5, 2), (35, 5, 2))],
+             "street_canyon": [((3, 15, 2), (7, 16, 3)), ((5, 15, 1.5), (5, 35, 1.5)), ((5, 5, 1.5), (5, 40, 8))],
+             "screened_wall": [((2, -3, 1.5), (20, 8, 1.5)), ((0, 10, 2), (50, 10, 2)), ((25, -5, 1.5), (5, 12, 1))],
+             "manhattan": [((2.5, 12.5, 1.5), (97.5, 62.5, 1.5)), ((30, 2.5, 2), (50, 97.5, 2))]}
+    for name, trs in djobs.items():
+        r = bindings.RefOracle(path=os.path.join(FIXTURES, name + ".json"))
+        m = r.build_matrix(2)
+        r.lib().vref_matrix_set_max_order(m, 3)
+        for order in (1, 2, 3):
+            acc = r.accel(m, order)
+            for tx, rx in trs:
+                try:
+                    paths, st = r.trace(acc, np.asarray(tx, np.float64), np.asarray(rx, np.float64), diffraction=True)
+                except RuntimeError as e:   # PlacementError: the GPU path must raise it too
+                    diff.append({"scene": name, "order": order, "tx": list(tx), "rx": list(rx), "error": str(e)})
+                    continue
+                diff.append({"scene": name, "order": order, "tx": list(tx), "rx": list(rx), "nodes": int(st[0]),
+                             "sequences": int(st[1]),
+                             "paths": sorted([{"identity": p["identity"], "points": [float(x).hex() for x in p["points"]],
+                                               "length": float(p["length"]).hex()} for p in paths],
+                                             key=lambda p: p["identity"])})
+            r.lib().vref_accel_free(acc)
+        print(name, "diffraction traces", sum(len(d.get("paths", [])) for d in diff if d["scene"] == name), "paths")
     with open(os.path.join(HERE, "aux.json"), "w") as fh:
-        json.dump({"image_trees": trees, "closest_edges": edges}, fh, separators=(",", ":"))
+        json.dump({"image_trees": trees, "closest_edges": edges, "diffraction_traces": diff}, fh,
+                  separators=(",", ":"))
 
 
 if __name__ == "__main__":

@@ -52,3 +52,33 @@ def test_closest_edges_vs_reference(k):
     with Scene(G.soup(d)) as sc:
         got = closest_diffraction_edges(sc, c["receivers"], d["edges"])
     assert got.tolist() == c["edge"]
+
+
+DIFF = AUX["diffraction_traces"]
+
+
+@pytest.mark.parametrize("k", range(len(DIFF)), ids=[f"{t['scene']}-o{t['order']}-{i}" for i, t in enumerate(DIFF)])
+def test_trace_with_diffraction_vs_reference(k):
+    """TraceAccelerator::trace(tx, rx, allow_diffraction=true): the receiver's
+    closest edge adds the Fermat-point sequences; path identities, points,
+    lengths and the node / sequence counters equal the reference's."""
+    from paper_2501_02747_b200._capi import PlacementError
+    from paper_2501_02747_b200.core import Tracer, chain_triples, path_identity
+    t = DIFF[k]
+    d = G.load(t["scene"])
+    s = G.soup(d)
+    with Scene(s) as sc:
+        bits, _ = sc.pair_visibility("prefiltered")
+        tri, _ = chain_triples(sc, bits)
+        tr = Tracer(sc, t["order"], admitted_bits=bits, triples=tri, edges=d["edges"])
+        if "error" in t:
+            with pytest.raises(PlacementError, match=t["error"]):
+                tr.trace([t["tx"]], [t["rx"]], allow_diffraction=True)
+            return
+        paths, nodes, st = tr.trace([t["tx"]], [t["rx"]], allow_diffraction=True)
+    got = sorted([{"identity": path_identity(s.ids, p["faces"], d["edges"][p["edge"]]["id"] if p["edge"] >= 0 else None),
+                   "points": [float(x).hex() for x in p["points"]], "length": float(p["length"]).hex()}
+                  for p in paths[0]], key=lambda p: p["identity"])
+    assert got == t["paths"]
+    assert int(nodes[0]) == t["nodes"]
+    assert st["sequences"] == t["sequences"]
