@@ -230,6 +230,10 @@ typedef struct {
  * 367, 383-394). */
 #define VISRT_TRACE_RX_FIXED 0x1
 #define VISRT_TRACE_DIFFRACTION 0x2
+/* VISRT_TRACE_BRUTE_FORCE — brute_force_trace (src/raytracer.cpp:488-493): the
+ * unaccelerated image method, every face but the immediate repeat at every
+ * level, no chain filter and no image prune (Engine with filter = nullptr). */
+#define VISRT_TRACE_BRUTE_FORCE 0x4
 int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const double* rx,
                 int flags, visrt_trace_stats* stats, void* stream);
 /* The scene's edges for diffraction (Scene::edges, include/rt/scene.hpp:85-95):

@@ -94,6 +94,8 @@ int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, i
 int32_t vref_closest_edge(void* h, const double* rx);
 int64_t vref_image_tree(void* h, const double* src, int32_t depth, int32_t* face, int32_t* parent,
                         int32_t* dep, double* image, int64_t cap);
+int64_t vref_brute_trace(void* h, const double* tx, const double* rx, int32_t max_refl, int32_t diffraction,
+                         vref_path* out, int64_t cap, int64_t* stats);
 void* vref_accel_create(void* h, void* m, int32_t max_refl);
 void vref_accel_free(void* a);
 int64_t vref_accel_trace(void* h, void* a, const double* tx, const double* rx, int32_t diffraction,

@@ -341,12 +341,15 @@ class Tracer:
         except Exception:
             pass
 
-    def trace_raw(self, tx: np.ndarray, rx: np.ndarray, stream: int = 0, allow_diffraction: bool = False):
+    def trace_raw(self, tx: np.ndarray, rx: np.ndarray, stream: int = 0, allow_diffraction: bool = False,
+                  brute_force: bool = False):
         tx = np.ascontiguousarray(np.asarray(tx, np.float64).reshape(-1, 3))
         rx = np.ascontiguousarray(np.asarray(rx, np.float64).reshape(-1, 3))
         flags = 1 if len(rx) == 1 and len(tx) != 1 else 0
         if allow_diffraction:
             flags |= 2
+        if brute_force:
+            flags |= 4
         st = _capi.visrt_trace_stats()
         check(lib().visrt_trace(self.h, len(tx), tx.reshape(-1), rx.reshape(-1), flags, C.byref(st),
                                 C.c_void_p(stream) if stream else None))
@@ -359,10 +362,10 @@ class Tracer:
         return off, paths, nodes, {"nodes": st.nodes, "sequences": st.sequences, "paths": st.paths,
                                    "leg_tests": st.leg_tests, "ms": st.ms}
 
-    def trace(self, tx: np.ndarray, rx: np.ndarray, allow_diffraction: bool = False):
+    def trace(self, tx: np.ndarray, rx: np.ndarray, allow_diffraction: bool = False, brute_force: bool = False):
         """Per snapshot: list of paths {faces, edge (-1: none), points, length}
         ordered by face sequence, plus per-snapshot node counts and stats."""
-        off, paths, nodes, st = self.trace_raw(tx, rx, allow_diffraction=allow_diffraction)
+        off, paths, nodes, st = self.trace_raw(tx, rx, allow_diffraction=allow_diffraction, brute_force=brute_force)
         out = []
         for k in range(len(off) - 1):
             row = []
@@ -373,6 +376,21 @@ class Tracer:
                             "points": list(p.points[: 3 * npts]), "length": p.length})
             out.append(row)
         return out, nodes, st
+
+
+def brute_force_trace(scene: Scene, tx, rx, max_refl: int, allow_diffraction: bool = False,
+                      edges: Optional[Sequence[dict]] = None):
+    """rt::brute_force_trace (include/rt/raytracer.hpp:78-83): the conventional
+    image method — every face but the immediate repeat at every level, no
+    chain filter, no image prune — batched over snapshots on the GPU."""
+    if max_refl < 0:
+        raise _capi.VisibilityError("reflection order must be non-negative")
+    zero = np.zeros((scene.n, scene.words), np.uint64)
+    tr = Tracer(scene, max_refl, admitted_bits=zero, triples=np.zeros((0, 3), np.int32), edges=edges)
+    try:
+        return tr.trace(tx, rx, allow_diffraction=allow_diffraction, brute_force=True)
+    finally:
+        tr.close()
 
 
 def image_tree(scene: Scene, source, max_depth: int, ids: Optional[Sequence[str]] = None):

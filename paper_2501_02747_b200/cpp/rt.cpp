@@ -699,6 +699,25 @@ TraceAccelerator::TraceAccelerator(const Scene& scene, const InterVisMatrix& mat
     }
     check(visrt_tracer_create(scene.device_scene(), max_refl, bits.data(), static_cast<int64_t>(tri.size() / 3),
                               tri.empty() ? nullptr : tri.data(), &tracer_));
+    set_edges(scene);
+}
+
+TraceAccelerator::TraceAccelerator(const Scene& scene, int max_refl)
+    : scene_(&scene), max_refl_(max_refl), brute_(true) {
+    if (max_refl < 0) throw VisibilityError("reflection order must be non-negative");
+    const size_t n = scene.faces().size();
+    std::vector<uint64_t> bits(n * ((n + 63) / 64) + 1, 0);
+    check(visrt_tracer_create(scene.device_scene(), max_refl, bits.data(), 0, nullptr, &tracer_));
+    set_edges(scene);
+}
+
+std::vector<Path> brute_force_trace(const Scene& scene, const Vec3& tx, const Vec3& rx, int max_refl,
+                                    bool allow_diffraction, TraceStats* stats) {
+    TraceAccelerator acc(scene, max_refl);
+    return acc.trace(tx, rx, allow_diffraction, stats);
+}
+
+void TraceAccelerator::set_edges(const Scene& scene) {
     if (!scene.edges().empty()) {   // diffraction candidates (Scene::edges)
         std::vector<double> ab;
         std::vector<std::string> ids;
@@ -732,7 +751,8 @@ std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<V
         r.push_back(p.z);
     }
     visrt_trace_stats st{};
-    const int flags = (rx.size() == 1 ? VISRT_TRACE_RX_FIXED : 0) | (allow_diffraction ? VISRT_TRACE_DIFFRACTION : 0);
+    const int flags = (rx.size() == 1 ? VISRT_TRACE_RX_FIXED : 0) | (allow_diffraction ? VISRT_TRACE_DIFFRACTION : 0) |
+                      (brute_ ? VISRT_TRACE_BRUTE_FORCE : 0);
     check(visrt_trace(tracer_, static_cast<int64_t>(tx.size()), t.data(), r.data(), flags, &st, nullptr));
     const int64_t np = visrt_trace_results(tracer_, nullptr, nullptr, 0, nullptr);
     std::vector<int64_t> off(tx.size() + 1), nodes(tx.size());

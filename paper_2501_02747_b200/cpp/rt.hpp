@@ -292,9 +292,18 @@ class TraceAccelerator {
     int max_reflections() const { return max_refl_; }
 
   private:
+    friend std::vector<Path> brute_force_trace(const Scene&, const Vec3&, const Vec3&, int, bool, TraceStats*);
+    TraceAccelerator(const Scene& scene, int max_refl);   // brute force: no filter, no prune
+    void set_edges(const Scene& scene);
     const Scene* scene_;
     int max_refl_;
+    bool brute_ = false;
     visrt_tracer* tracer_ = nullptr;
 };
+
+/// brute_force_trace (include/rt/raytracer.hpp:78-83): the unaccelerated image
+/// method on the GPU tree (every face but the immediate repeat, no prune).
+std::vector<Path> brute_force_trace(const Scene& scene, const Vec3& tx, const Vec3& rx, int max_refl,
+                                    bool allow_diffraction, TraceStats* stats = nullptr);
 
 }  // namespace rt

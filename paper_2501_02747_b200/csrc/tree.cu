@@ -73,6 +73,7 @@ struct TreeArgs {
     unsigned long long* counter;          // [0] cursor, [1] leg tests
     const int32_t* snap_edge;             // [total snapshots] closest diffraction edge or -1 (nullptr: none)
     const double* edge_ab;                // [nedges][6]
+    int32_t brute;                        // brute_force_trace: no chain filter, no image prune
 };
 
 __device__ __forceinline__ double sdist_face(const DevScene& s, int f, double x, double y, double z) {
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a) {
             par.depth = 0;
             par.f0 = par.f1 = par.f2 = -1;
             par.rank = -1;
-            par.filtered = 1;
+            par.filtered = a.brute ? 0 : 1;
             par.ix = a.tx[3 * static_cast<size_t>(par.snap)];
             par.iy = a.tx[3 * static_cast<size_t>(par.snap) + 1];
             par.iz = a.tx[3 * static_cast<size_t>(par.snap) + 2];
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a) {
                 } else {
                     c = a.obl[q - (hi - lo)];
                 }
-                ok = c != last && sdist_face(s, c, par.ix, par.iy, par.iz) > kEps;
+                ok = c != last && (a.brute || sdist_face(s, c, par.ix, par.iy, par.iz) > kEps);
             }
             const unsigned m = __ballot_sync(kFull, ok);
             if (!m) continue;
@@ -648,6 +649,7 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         const int device = visrt::scene_device(tr->scene);
         const int rx_fixed = (flags & VISRT_TRACE_RX_FIXED) ? 1 : 0;
         const bool diffraction = (flags & VISRT_TRACE_DIFFRACTION) != 0;
+        const bool brute = (flags & VISRT_TRACE_BRUTE_FORCE) != 0;
         // Engine ctor placement checks (src/raytracer.cpp:355-363)
         for (int64_t k = 0; k < nsnap; ++k) {
             const double* T = tx + 3 * k;
@@ -716,6 +718,7 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         a.paths = d_paths;
         a.path_cap = path_cap;
         a.snap_edge = d_snap_edge;
+        a.brute = brute ? 1 : 0;
         a.edge_ab = tr->d_edge_ab;
         std::vector<visrt_path> host_paths;
         int64_t total_nodes = 0, total_seq = 0, leg_tests = 0;

@@ -290,6 +290,22 @@ int main(int argc, char** argv) {
             }
         }
         vref_accel_free(RA);
+        // brute_force_trace on the first traces (the unpruned tree grows as N^order)
+        for (int t = 0; t < ntr && t < 2 && (order <= 2 || n <= 200); ++t) {
+            rt::TraceStats st;
+            const auto paths = rt::brute_force_trace(*mine, tr[t].first, tr[t].second, order, false, &st);
+            std::vector<vref_path> rp(16384);
+            int64_t rst[4];
+            const double tx[3] = {tr[t].first.x, tr[t].first.y, tr[t].first.z};
+            const double rx[3] = {tr[t].second.x, tr[t].second.y, tr[t].second.z};
+            const int64_t np = vref_brute_trace(ref, tx, rx, order, 0, rp.data(), 16384, rst);
+            EXPECT(static_cast<int64_t>(paths.size()) == np, "brute path count " << order << "," << t);
+            EXPECT(st.nodes_expanded == rst[0] && st.sequences_checked == rst[1], "brute stats " << order << "," << t);
+            for (int64_t q = 0; q < np && q < static_cast<int64_t>(paths.size()); ++q)
+                EXPECT(paths[static_cast<size_t>(q)].identity() == rp[q].identity &&
+                           paths[static_cast<size_t>(q)].length == rp[q].length,
+                       "brute path " << order << "," << t);
+        }
     }
     std::cout << "TraceAccelerator: orders 1.." << M2.max_order() << " x " << ntr
               << " traces compared (+ allow_diffraction where the scene has edges)" << std::endl;

@@ -75,9 +75,27 @@ def main() -> None:
                                              key=lambda p: p["identity"])})
             r.lib().vref_accel_free(acc)
         print(name, "diffraction traces", sum(len(d.get("paths", [])) for d in diff if d["scene"] == name), "paths")
+    # brute_force_trace (proj/src/raytracer.cpp:488-493)
+    brute = []
+    for name in ("two_buildings", "street_canyon", "screened_wall"):
+        r = bindings.RefOracle(path=os.path.join(FIXTURES, name + ".json"))
+        for order in (1, 2, 3):
+            for tx, rx in djobs[name]:
+                for dif in (False, True):
+                    try:
+                        paths, st = r.brute_trace(np.asarray(tx, np.float64), np.asarray(rx, np.float64), order, dif)
+                    except RuntimeError as e:
+                        continue
+                    brute.append({"scene": name, "order": order, "tx": list(tx), "rx": list(rx), "diffraction": dif,
+                                  "nodes": int(st[0]), "sequences": int(st[1]),
+                                  "paths": sorted([{"identity": p["identity"],
+                                                    "points": [float(x).hex() for x in p["points"]],
+                                                    "length": float(p["length"]).hex()} for p in paths],
+                                                  key=lambda p: p["identity"])})
+    print("brute traces", len(brute))
     with open(os.path.join(HERE, "aux.json"), "w") as fh:
-        json.dump({"image_trees": trees, "closest_edges": edges, "diffraction_traces": diff}, fh,
-                  separators=(",", ":"))
+        json.dump({"image_trees": trees, "closest_edges": edges, "diffraction_traces": diff, "brute_traces": brute},
+                  fh, separators=(",", ":"))
 
 
 if __name__ == "__main__":

@@ -82,3 +82,34 @@ def test_trace_with_diffraction_vs_reference(k):
     assert got == t["paths"]
     assert int(nodes[0]) == t["nodes"]
     assert st["sequences"] == t["sequences"]
+
+
+BRUTE = AUX["brute_traces"]
+
+
+@pytest.mark.parametrize("k", range(len(BRUTE)),
+                         ids=[f"{t['scene']}-o{t['order']}-d{int(t['diffraction'])}-{i}" for i, t in enumerate(BRUTE)])
+def test_brute_force_trace_vs_reference(k):
+    """brute_force_trace (proj/src/raytracer.cpp:488-493) on the GPU: the
+    unpruned, unfiltered tree (N(N-1)^(d-1) nodes) gives the reference's path
+    set and counters; and the accelerated trace finds the same path set
+    (proj/tests/test_raytracer.cpp:134-168, acceptance c1)."""
+    from paper_2501_02747_b200.core import Tracer, brute_force_trace, chain_triples, path_identity
+    t = BRUTE[k]
+    d = G.load(t["scene"])
+    s = G.soup(d)
+
+    def ident(p):
+        return path_identity(s.ids, p["faces"], d["edges"][p["edge"]]["id"] if p["edge"] >= 0 else None)
+
+    with Scene(s) as sc:
+        paths, nodes, st = brute_force_trace(sc, [t["tx"]], [t["rx"]], t["order"], t["diffraction"], d["edges"])
+        got = sorted([{"identity": ident(p), "points": [float(x).hex() for x in p["points"]],
+                       "length": float(p["length"]).hex()} for p in paths[0]], key=lambda p: p["identity"])
+        assert got == t["paths"]
+        assert int(nodes[0]) == t["nodes"] and st["sequences"] == t["sequences"]
+        bits, _ = sc.pair_visibility("prefiltered")
+        tri, _ = chain_triples(sc, bits)
+        acc = Tracer(sc, t["order"], admitted_bits=bits, triples=tri, edges=d["edges"])
+        apaths, _, _ = acc.trace([t["tx"]], [t["rx"]], allow_diffraction=t["diffraction"])
+        assert sorted(ident(p) for p in apaths[0]) == [p["identity"] for p in t["paths"]]
