@@ -160,7 +160,8 @@ def secondary_measurements(stream: int):
     """The other hot-path subsystems, timed with the library's CUDA events on
     the same stream (outside the headline's timed region, rank 0, N = 1)."""
     from paper_2501_02747_b200 import scenes
-    from paper_2501_02747_b200.core import Scene, Tracer, chain_triples, point_regions_array
+    from paper_2501_02747_b200.core import (ENTRY_DTYPE, Scene, Tracer, chain_triples, point_regions_array,
+                                            trajectory_vis_table, unpack_bits)
     out = {}
     # (1) the other matrix configurations
     for cfg in (1, 3):
@@ -202,6 +203,43 @@ def secondary_measurements(stream: int):
         out["tree_config1_order2"] = {"snapshots": len(wl1.tx), "nodes": tst["nodes"], "ms": tst["ms"],
                                       "ms_per_snapshot": tst["ms"] / len(wl1.tx), "paths": tst["paths"]}
         tr.close()
+        # (2) trajectory_vis_table along config 1's 100 m Tx line (MobileSampler
+        # keys depend only on the reflector chains: order-1 entries of the
+        # admitted pairs and order-2 entries of the GPU triples)
+        bits, _ = sc.pair_visibility("prefiltered")
+        tri, _ = chain_triples(sc, bits)
+        adm = unpack_bits(bits, sc.n)
+        ai, aj = np.nonzero(adm)
+        ent = np.zeros(len(ai) + len(tri), ENTRY_DTYPE)
+        ent["order"][: len(ai)] = 1
+        ent["chain"][: len(ai), 0] = ai
+        ent["chain"][: len(ai), 1] = aj
+        ent["order"][len(ai):] = 2
+        ent["chain"][len(ai):] = tri
+        wps = np.array([wl1.tx[0], wl1.tx[-1]])
+        for order in (1, 2):
+            sel = ent[ent["order"] <= order]
+            trajectory_vis_table(sc, wps, sel, order, wl1.scene.ids)
+            t0 = time.perf_counter()
+            rows, tst = trajectory_vis_table(sc, wps, sel, order, wl1.scene.ids, return_stats=True)
+            wall = (time.perf_counter() - t0) * 1e3
+            out[f"trajectory_config1_order{order}"] = {
+                "route_m": float(np.linalg.norm(wps[1] - wps[0])), "samples": tst["pairs"],
+                "boundaries": tst["candidates"], "rows": len(rows), "device_ms": tst["ms"], "wall_ms": wall,
+                "kernel_launches": tst["sweeps"]}
+        # the reference's trajectory_vis_table on the same route, host cores (order 1: ~2 s)
+        try:
+            from oracle import bindings
+            if bindings.have_ref():
+                r = bindings.RefOracle(wl1.scene)
+                m = r.build_matrix(1)
+                t0 = time.perf_counter()
+                rrows = r.trajectory_vis_table(m, wps, 1)
+                out["trajectory_config1_order1"]["reference_ms"] = (time.perf_counter() - t0) * 1e3
+                out["trajectory_config1_order1"]["reference_rows"] = len(rrows)
+                out["trajectory_config1_order1"]["reference_threads"] = _ncores()
+        except Exception as e:   # the reference build is optional on the box
+            out["trajectory_config1_order1"]["reference_error"] = str(e)[:120]
     return out
 
 

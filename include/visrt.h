@@ -15,8 +15,14 @@
  *                                (src/vismatrix.cpp:275-301)
  *   visrt_point_regions       <- illuminated_region for (snapshot, face) batches
  *                                (include/rt/vistable.hpp:116-117, src/vistable.cpp:287-334)
- *   visrt_image_tree          <- TraceAccelerator::trace / Engine::expand + resolve_sequence
- *                                (include/rt/raytracer.hpp:96-118, src/raytracer.cpp:205-444)
+ *   visrt_point_tables        <- point_vis_table (include/rt/vistable.hpp:128-129)
+ *   visrt_chain_reach         <- TableBuilder::reach / MobileSampler::member (src/vistable.cpp:404-467)
+ *   visrt_trajectory_table    <- trajectory_vis_table (include/rt/vistable.hpp:143-148)
+ *   visrt_closest_edges       <- closest_diffraction_edge (include/rt/vistable.hpp:131-137)
+ *   visrt_chain_triples       <- build_matrix chain growth (src/vismatrix.cpp:715-797)
+ *   visrt_tracer_* / visrt_trace <- TraceAccelerator::trace, brute_force_trace / Engine::expand +
+ *                                resolve_sequence (include/rt/raytracer.hpp:78-118, src/raytracer.cpp:174-493)
+ *   visrt_image_tree          <- image_tree (include/rt/raytracer.hpp:51-61)
  *
  * Conventions: plain pointers and sizes; caller-owned output buffers; every
  * call returns a status (0 ok) and never throws; the message of the last
