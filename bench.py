@@ -376,7 +376,7 @@ def run_visrt(args, rank, world):
                     "d2h_bytes_per_step": int(d2h),
                     "path": "Scene(soup) ingest+upload -> pair_visibility -> bits D2H -> free"},
             "gpu_launches": args.steps,
-            "roofline": {"bound": "fp64", "kernel": "k_pair_bits", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "fp64", "kernel": "k_pair_bits_warp", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "basis": "algorithmic: 17 FP64 ops x T_alg reference tests / kernel time; "
                                   "peak = in-run DADD/DMUL microbenchmark (MEASURED_PEAKS.json has no FP64); "

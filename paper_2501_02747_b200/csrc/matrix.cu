@@ -4,13 +4,16 @@
 //                    non-oblique, mutually_front 160-169, required_planes
 //                    171-181) over all i<j, ordered prefix-sum compaction
 //                    (cub::DeviceSelect) into a candidate list.
-//   K2 k_pair_bits   occlusion_judgment's Occluded verdict (253-302) with
-//                    early exit: one lane = one pair state machine walking its
-//                    sightlines; the block sweeps occluder tiles cyclically out
-//                    of shared memory (TMA bulk copies, double-buffered), every
-//                    lane testing the same occluder (smem broadcast) against its
-//                    own sightline. A sightline stops at its first hit; a pair
-//                    stops at its first clear (or degenerate) sightline.
+//   K2w k_pair_bits_warp (default) occlusion_judgment's Occluded verdict
+//                    (253-302) with early exit, one WARP per pair: warp blocker
+//                    cache tested on all sightlines at once, then one
+//                    warp-cooperative culled sweep (sweep.h hierarchy: tile
+//                    boxes, member boxes, exact survivors) per unresolved
+//                    sightline; a found blocker settles every other sightline
+//                    it blocks. A pair stops at its first clear (or degenerate)
+//                    sightline.
+//   K2 k_pair_bits   the same bit with one LANE per pair state machine
+//                    (VISRT_K2_WARP=0; kept for A/B).
 //   K2d k_pair_detail Visible / Partial / Occluded + blocker sets (no early exit).
 //
 // All geometry is the reference's FP64 predicate with explicit _rn intrinsics
@@ -232,6 +235,173 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
     }
 }
 
+// K2w: the same verdict bit with a WARP per pair. Lane l owns sightlines
+// l, l+32, l+64 (S <= 89). A warp-uniform cache of the last kWC blockers is
+// tested on every sightline at once; each still-unresolved sightline then gets
+// ONE warp-cooperative culled sweep (lanes split the 64 tile boxes of a chunk,
+// then the 64 member boxes of each candidate tile, then the survivors' exact
+// tests), and the blocker it finds is immediately tested on every other
+// unresolved sightline of the pair. The pair ends at the first clear sightline
+// (bit = 1) or when every sightline is blocked — the same bit as the lane
+// kernel, with converged SAT/exact work instead of 32 divergent state machines.
+#ifndef VISRT_K2W_MINB
+#define VISRT_K2W_MINB 3
+#endif
+#ifndef VISRT_K2W_WC
+#define VISRT_K2W_WC 1      // warp blocker-cache entries (r01 sweep 1/2/3/4/6/8/16: 1 best)
+#endif
+#ifndef VISRT_K2W_ROT
+#define VISRT_K2W_ROT 1     // candidate tiles of the home chunk start at the pair's own tile
+#endif
+constexpr int kWC = VISRT_K2W_WC;
+
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, VISRT_K2W_MINB) k_pair_bits_warp(PairArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    int wc = -1;        // lane q < kWC holds warp cache entry q (Morton index)
+    int wc_next = 0;    // warp-uniform insertion cursor
+    unsigned long long tests = 0, sweeps = 0, batches = 0;
+
+    for (;;) {
+        unsigned long long pw = 0;
+        if (lane == 0) pw = atomicAdd(&a.counter[0], 1ull);
+        const long long p = static_cast<long long>(__shfl_sync(kFull, pw, 0));
+        if (p >= a.npairs) break;
+        int pi, pj;
+        if (a.ci) {
+            pi = a.ci[p];
+            pj = a.cj[p];
+        } else {
+            pair_from_index(p, n, pi, pj);
+        }
+        const int si = s.inv[pi], sj = s.inv[pj];
+        const int nr = s.nv[pi], na = s.nv[pj];
+        const int grid = min(s.ns[pi] - nr - 1, s.ns[pj] - na - 1);
+        const int S = nr * na + 1 + grid;
+        unsigned unres = 0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            if (lane + 32 * r < S) unres |= 1u << r;
+        double ax, ay, az, bx, by, bz;
+        auto ends = [&](int ord) { sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz); };
+        auto exact = [&](int k) {
+            ++tests;
+            return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
+        };
+        // settle every unresolved sightline blocked by occluder k (Morton index)
+        auto resolve = [&](int k) {
+            const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
+            for (unsigned m = unres; m; m &= m - 1) {
+                const int r = __ffs(m) - 1;
+                ends(lane + 32 * r);
+                if (sat_maybe(B, make_segf(s, ax, ay, az, bx, by, bz)) && exact(k)) unres &= ~(1u << r);
+            }
+        };
+        bool clear = false;
+        if (may_touch(s, pi, pj)) {   // a degenerate sightline is never blocked
+            bool degen = false;
+            for (unsigned m = unres; m && !degen; m &= m - 1) {
+                ends(lane + 32 * (__ffs(m) - 1));
+                degen = degenerate(ax, ay, az, bx, by, bz);
+            }
+            clear = __any_sync(kFull, degen);
+        }
+        if (!clear) {
+            for (int i = 0; i < kWC; ++i) {   // most recent blocker first
+                const int q = (wc_next + kWC - 1 - i) % kWC;
+                const int k = __shfl_sync(kFull, wc, q);
+                if (k < 0 || k == si || k == sj) continue;
+                resolve(k);
+                if (!__any_sync(kFull, unres != 0)) break;
+            }
+        }
+        while (!clear) {
+            const unsigned who = __ballot_sync(kFull, unres != 0);
+            if (!who) break;   // every sightline blocked: Occluded
+            const int L = __ffs(who) - 1;
+            const int r0 = __ffs(__shfl_sync(kFull, unres, L)) - 1;
+            ends(L + 32 * r0);   // the swept sightline, uniform across the warp
+            const SegF g = make_segf(s, ax, ay, az, bx, by, bz);
+            ++sweeps;
+            int hit = -1;
+            const int home = home_chunk(s, pi);
+            for (int cc = 0; cc < ctx.nchunks && hit < 0; ++cc) {
+                const int c = home + cc < ctx.nchunks ? home + cc : home + cc - ctx.nchunks;
+                const int t0 = c * kTile;
+                const int tc = min(kTile, ctx.ntiles - t0);
+                const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
+                const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
+                unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
+                                          (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
+                unsigned long long later = 0;
+                if (VISRT_K2W_ROT && cc == 0) {   // the pair's own tile first, wrap around after
+                    const unsigned long long below = (1ull << ((si >> 6) - t0)) - 1ull;
+                    later = cand & below;
+                    cand &= ~below;
+                }
+                ++batches;
+                while ((cand | later) && hit < 0) {
+                    if (!cand) {
+                        cand = later;
+                        later = 0;
+                    }
+                    const int base = (t0 + __ffsll(static_cast<long long>(cand)) - 1) * kTile;
+                    cand &= cand - 1;
+                    const int mc = min(kTile, n - base);
+                    const int m0 = base + lane, m1 = base + lane + 32;
+                    const bool v0 = lane < mc && m0 != si && m0 != sj &&
+                                    sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g);
+                    const bool v1 = lane + 32 < mc && m1 != si && m1 != sj &&
+                                    sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g);
+                    unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
+                    ++batches;
+                    while ((lo | hi) && hit < 0) {
+                        // lane takes the lane-th surviving member
+                        const int clo = __popc(lo), chi = __popc(hi);
+                        int idx = -1;
+                        if (lane < clo) idx = __fns(lo, 0, lane + 1);
+                        else if (lane - clo < chi) idx = 32 + __fns(hi, 0, lane - clo + 1);
+                        const bool h = idx >= 0 && exact(base + idx);
+                        const unsigned hb = __ballot_sync(kFull, h);
+                        if (hb) hit = __shfl_sync(kFull, base + idx, __ffs(hb) - 1);
+                        // drop the (up to) 32 survivors just tested
+                        if (clo + chi <= 32) {
+                            lo = hi = 0;
+                        } else {
+                            const int drop_hi = 32 - clo;
+                            lo = 0;
+                            for (int q = 0; q < drop_hi; ++q) hi &= hi - 1;
+                        }
+                    }
+                }
+            }
+            if (hit < 0) {
+                clear = true;   // a sightline clear of every occluder
+                break;
+            }
+            if (lane == wc_next) wc = hit;
+            wc_next = wc_next + 1 == kWC ? 0 : wc_next + 1;
+            resolve(hit);
+        }
+        if (lane == 0) {
+            if (clear) set_pair_bit(a.bits, s.words, pi, pj);
+            if (a.cbit) a.cbit[p] = clear ? 1 : 0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) {
+        atomicAdd(&a.counter[1], tests);
+        atomicAdd(&a.counter[2], sweeps);
+        atomicAdd(&a.counter[3], batches);
+    }
+}
+
 // Detail sweep: per pair every sightline against every occluder (no early
 // exit), as occlusion_judgment does, recording the blocker set.
 template <int MAXV, bool RESIDENT>
@@ -408,10 +578,23 @@ static bool use_resident(int n) {
 
 static size_t sweep_smem(const DevScene& s, bool resident) { return sweep_smem_bytes(s.n, s.ntiles, resident); }
 
+// The warp-per-pair kernel is the default (r01: config 2 8.05 -> 6.31 ms,
+// config 3 40.8 -> 34.1 ms); VISRT_K2_WARP=0 selects the lane-per-pair kernel.
+static bool use_warp_k2() {
+    static const bool w = [] {
+        const char* e = std::getenv("VISRT_K2_WARP");
+        return !(e && e[0] == '0');
+    }();
+    return w;
+}
+
 template <int MAXV>
 static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
     const bool res = use_resident(a.s.n);
     const size_t smem = sweep_smem(a.s, res);
+    if (use_warp_k2())
+        return res ? launch_persistent(k_pair_bits_warp<MAXV, true>, smem, a, device, st)
+                   : launch_persistent(k_pair_bits_warp<MAXV, false>, smem, a, device, st);
     return res ? launch_persistent(k_pair_bits<MAXV, true>, smem, a, device, st)
                : launch_persistent(k_pair_bits<MAXV, false>, smem, a, device, st);
 }

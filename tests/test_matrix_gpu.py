@@ -120,3 +120,23 @@ def test_matrix_stream_path_config1(oracle_built, cfg1, monkeypatch):
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
         out[force] = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["0"] == out["1"]
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_matrix_lane_and_warp_kernels_agree(cfg):
+    """K2w (warp per pair, default) and K2 (lane per pair, VISRT_K2_WARP=0)
+    give identical (A) and (B) bits; both resident and global box paths."""
+    import subprocess, sys, os, json
+    code = ("import sys, json, hashlib; sys.path.insert(0, %r);"
+            "from paper_2501_02747_b200 import scenes;"
+            "from paper_2501_02747_b200.core import Scene;"
+            "sc = Scene(scenes.workload(%d).scene); b, _ = sc.pair_visibility('all');"
+            "a, _ = sc.pair_visibility('prefiltered');"
+            "print(json.dumps([hashlib.sha256(b.tobytes()).hexdigest(), hashlib.sha256(a.tobytes()).hexdigest()]))"
+            ) % (os.path.dirname(os.path.dirname(__file__)), cfg)
+    out = {}
+    for warp, force in (("0", "0"), ("1", "0"), ("1", "1")):
+        env = dict(os.environ, VISRT_K2_WARP=warp, VISRT_FORCE_STREAM=force)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+        out[warp + force] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["00"] == out["10"] == out["11"]
