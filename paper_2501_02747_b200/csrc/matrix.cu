@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #endif
 constexpr int kWC = VISRT_K2W_WC;
 
-template <int MAXV, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads, VISRT_K2W_MINB) k_pair_bits_warp(PairArgs a) {
+template <int MAXV, bool RESIDENT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
@@ -267,6 +267,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2W_MINB) k_pair_bits_warp(Pai
     int wc = -1;        // lane q < kWC holds warp cache entry q (Morton index)
     int wc_next = 0;    // warp-uniform insertion cursor
     unsigned long long tests = 0, sweeps = 0, batches = 0;
+    __shared__ unsigned char surv_buf[kThreads / 32][64];   // per warp: surviving members of a tile, in order
+    unsigned char* sv = surv_buf[threadIdx.x >> 5];
+    const unsigned lt = (1u << lane) - 1u;
 
     for (;;) {
         unsigned long long pw = 0;
@@ -289,7 +292,26 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2W_MINB) k_pair_bits_warp(Pai
         for (int r = 0; r < 3; ++r)
             if (lane + 32 * r < S) unres |= 1u << r;
         double ax, ay, az, bx, by, bz;
-        auto ends = [&](int ord) { sightline_endpoints(s, pi, pj, nr, na, grid, ord, ax, ay, az, bx, by, bz); };
+        // sightline_endpoints without the integer division: v / na = (v * mg) >> 16 for v < 64
+        const unsigned mg = (65536u + na - 1) / na;
+        auto ends = [&](int ord) {
+            int ri, ai;
+            if (ord == 0) {
+                ri = nr;
+                ai = na;
+            } else if (ord <= grid) {
+                ri = nr + ord;
+                ai = na + ord;
+            } else {
+                const unsigned v = static_cast<unsigned>(ord - 1 - grid);
+                ri = static_cast<int>((v * mg) >> 16);
+                ai = static_cast<int>(v) - ri * na;
+            }
+            const double* P = s.samples + (static_cast<size_t>(pi) * kMaxSamples + ri) * 3;
+            const double* Q = s.samples + (static_cast<size_t>(pj) * kMaxSamples + ai) * 3;
+            ax = P[0]; ay = P[1]; az = P[2];
+            bx = Q[0]; by = Q[1]; bz = Q[2];
+        };
         auto exact = [&](int k) {
             ++tests;
             return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
@@ -359,26 +381,21 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2W_MINB) k_pair_bits_warp(Pai
                                     sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g);
                     const bool v1 = lane + 32 < mc && m1 != si && m1 != sj &&
                                     sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g);
-                    unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
+                    const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
                     ++batches;
-                    while ((lo | hi) && hit < 0) {
-                        // lane takes the lane-th surviving member
-                        const int clo = __popc(lo), chi = __popc(hi);
-                        int idx = -1;
-                        if (lane < clo) idx = __fns(lo, 0, lane + 1);
-                        else if (lane - clo < chi) idx = 32 + __fns(hi, 0, lane - clo + 1);
+                    const int clo = __popc(lo), tot = clo + __popc(hi);
+                    if (tot == 0) continue;
+                    // compact the survivors (member order) through shared memory
+                    if (v0) sv[__popc(lo & lt)] = static_cast<unsigned char>(lane);
+                    if (v1) sv[clo + __popc(hi & lt)] = static_cast<unsigned char>(32 + lane);
+                    __syncwarp();
+                    for (int r = 0; r < tot && hit < 0; r += 32) {
+                        const int idx = r + lane < tot ? sv[r + lane] : -1;
                         const bool h = idx >= 0 && exact(base + idx);
                         const unsigned hb = __ballot_sync(kFull, h);
                         if (hb) hit = __shfl_sync(kFull, base + idx, __ffs(hb) - 1);
-                        // drop the (up to) 32 survivors just tested
-                        if (clo + chi <= 32) {
-                            lo = hi = 0;
-                        } else {
-                            const int drop_hi = 32 - clo;
-                            lo = 0;
-                            for (int q = 0; q < drop_hi; ++q) hi &= hi - 1;
-                        }
                     }
+                    __syncwarp();
                 }
             }
             if (hit < 0) {
@@ -592,9 +609,18 @@ template <int MAXV>
 static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
     const bool res = use_resident(a.s.n);
     const size_t smem = sweep_smem(a.s, res);
-    if (use_warp_k2())
-        return res ? launch_persistent(k_pair_bits_warp<MAXV, true>, smem, a, device, st)
-                   : launch_persistent(k_pair_bits_warp<MAXV, false>, smem, a, device, st);
+    if (use_warp_k2()) {
+        // register budget by occupancy: when shared memory already limits the
+        // SM to <= 2 CTAs (large resident scenes), take the 2-CTA register budget
+        int smem_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        const bool two = smem + 1024 > static_cast<size_t>(smem_sm) / 3;
+        if (two)
+            return res ? launch_persistent(k_pair_bits_warp<MAXV, true, 2>, smem, a, device, st)
+                       : launch_persistent(k_pair_bits_warp<MAXV, false, 2>, smem, a, device, st);
+        return res ? launch_persistent(k_pair_bits_warp<MAXV, true, VISRT_K2W_MINB>, smem, a, device, st)
+                   : launch_persistent(k_pair_bits_warp<MAXV, false, VISRT_K2W_MINB>, smem, a, device, st);
+    }
     return res ? launch_persistent(k_pair_bits<MAXV, true>, smem, a, device, st)
                : launch_persistent(k_pair_bits<MAXV, false>, smem, a, device, st);
 }
