@@ -75,6 +75,37 @@ __device__ bool column_span(const DevScene& s, int f, int pl, double ax, double 
     return any;
 }
 
+// column_span on the face's (u, s) ring precomputed once per plane (the
+// reference's FaceParam::poly_us, src/vistable.cpp:84-98): same values, no
+// per-call divisions.
+__device__ bool column_span_us(const double* us, int nv, double u, double& lo_o, double& hi_o) {
+    double lo = 0.0, hi = 0.0;
+    bool any = false;
+    double ua = us[0], sa = us[1];
+    for (int i = 0; i < nv; ++i) {
+        const double ub = i + 1 < nv ? us[2 * i + 2] : us[0];
+        const double sb = i + 1 < nv ? us[2 * i + 3] : us[1];
+        const double da = dsub(ua, u), db = dsub(ub, u);
+        if (fabs(da) <= 1e-12) {
+            if (!any) { lo = hi = sa; any = true; }
+            else { lo = dmin_std(lo, sa); hi = dmax_std(hi, sa); }
+        }
+        if ((da < 0.0) != (db < 0.0) && fabs(dsub(da, db)) > 1e-15) {
+            const double sv = dadd(sa, dmul(dsub(sb, sa), __ddiv_rn(da, dsub(da, db))));
+            if (!any) { lo = hi = sv; any = true; }
+            else { lo = dmin_std(lo, sv); hi = dmax_std(hi, sv); }
+        }
+        ua = ub;
+        sa = sb;
+    }
+    lo_o = lo;
+    hi_o = hi;
+    return any;
+}
+
+// double(j) / (kTransverse - 1), j = 0..6 (correctly rounded, as the reference)
+__constant__ double kSampFrac[7] = {0.0 / 6.0, 1.0 / 6.0, 2.0 / 6.0, 3.0 / 6.0, 4.0 / 6.0, 5.0 / 6.0, 6.0 / 6.0};
+
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
@@ -91,6 +122,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     int f = 0, pl = 0;
     double sx = 0, sy = 0, sz = 0;      // source
     double ax = 0, ay = 0, dx = 0, dy = 0, len2 = 0;   // face_param of plane pl
+    double us[2 * MAXV];                // face_param poly_us of plane pl
+    auto load_us = [&]() {
+        const int nv = s.nv[f];
+        for (int k = 0; k < nv; ++k) face_us(s, f, pl, k, ax, ay, dx, dy, len2, us[2 * k], us[2 * k + 1]);
+    };
     // SCAN / REFINE
     int phase = 0;                      // 0 scan, 1 refine
     int col = 0;                        // scan column
@@ -137,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     // already blocks are settled here.
     auto next_sample = [&]() -> bool {
         for (; samp < 7; ++samp) {
-            const double fj = __ddiv_rn(static_cast<double>(samp), 6.0);
+            const double fj = kSampFrac[samp];
             const double sv = dmin_std(dsub(cs1, inset), dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), fj))));
             const double px = dadd(ax, dmul(dx, cu));
             const double py = dadd(ay, dmul(dy, cu));
@@ -161,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     // column was decided without one (result in `res`).
     auto begin_col = [&](double u, bool& res) -> bool {
         cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
-        if (!column_span(s, f, pl, ax, ay, dx, dy, len2, cu, cs0, cs1)) {
+        if (!column_span_us(us, s.nv[f], cu, cs0, cs1)) {
             res = false;
             return false;
         }
@@ -294,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
                 if (len2 <= kEps * kEps) continue;
                 break;
             }
+            load_us();
             phase = 0;
             col = 0;
             vis = 0;
@@ -338,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
             if (len2 <= kEps * kEps) continue;
             break;
         }
+        load_us();
         phase = 0;
         col = 0;
         vis = 0;
