@@ -440,6 +440,163 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
     }
 }
 
+// K4w: illuminated_region with a WARP per (source, face) task. The region
+// algorithm runs warp-uniformly as straight-line code that mirrors the
+// reference (planes -> 65 col_vis columns -> run refinement -> first largest
+// interval), and every sightline_clear is ONE warp-cooperative culled sweep
+// (sweep.h coop_any_hit) after a one-entry warp blocker cache. Same
+// arithmetic, same call order, so every output is bit-identical to K4 — with
+// converged lanes and a short per-region critical path (small batches and
+// trajectory probes are latency-bound on K4's lane state machines).
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 2) k_point_regions_warp(RegionArgs a) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
+    __shared__ unsigned char surv_buf[kThreads / 32][64];
+    const DevScene& s = a.s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31;
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    unsigned char* sv = surv_buf[threadIdx.x >> 5];
+    unsigned long long tests = 0, queries = 0, batches = 0;
+    int cache = -1;   // warp-uniform: Morton index of the last blocker
+    for (;;) {
+        unsigned long long tw = 0;
+        if (lane == 0) tw = atomicAdd(&a.counter[0], 1ull);
+        const long long t = static_cast<long long>(__shfl_sync(kFull, tw, 0));
+        if (t >= a.ntasks) break;
+        long long k;
+        int f;
+        if (!a.task_face) {
+            k = t / n;
+            f = static_cast<int>(t - k * n);
+        } else if (a.paired) {
+            k = t;
+            f = a.task_face[t];
+        } else {
+            k = t / a.m;
+            f = a.task_face[t - k * a.m];
+        }
+        const int sf = s.inv[f];
+        const int nv = s.nv[f];
+        const double sx = a.src[3 * k], sy = a.src[3 * k + 1], sz = a.src[3 * k + 2];
+        int8_t present = 1;
+        int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
+        double sub[6] = {0, 0, 0, 0, 0, 0};
+        // back-face test (src/vistable.cpp:289-294)
+        {
+            const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
+            const double* N = s.normal + 3 * static_cast<size_t>(f);
+            const double dist = dot_rel(sx, sy, sz, P[0], P[1], P[2], N[0], N[1], N[2]);
+            if (fabs(dist) <= kEps) present = -1;
+            else if (dist < 0.0) present = 0;
+        }
+        for (int pl = 0; pl < 3 && present == 1; ++pl) {
+            if (!s.seg_ok[3 * f + pl]) continue;
+            const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;
+            const double ax = sg[0], ay = sg[1];
+            const double dx = dsub(sg[2], sg[0]), dy = dsub(sg[3], sg[1]);
+            const double len2 = dadd(dmul(dx, dx), dmul(dy, dy));
+            if (len2 <= kEps * kEps) continue;   // no face_param in this plane
+            double us[2 * MAXV];
+            for (int q = 0; q < nv; ++q) face_us(s, f, pl, q, ax, ay, dx, dy, len2, us[2 * q], us[2 * q + 1]);
+            // col_vis (src/vistable.cpp:146-159)
+            auto col_vis = [&](double u) -> bool {
+                const double cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
+                double cs0, cs1;
+                if (!column_span_us(us, nv, cu, cs0, cs1)) return false;
+                const double inset = dmul(dsub(cs1, cs0), 1e-6);
+                const double px = dadd(ax, dmul(dx, cu));
+                const double py = dadd(ay, dmul(dy, cu));
+                for (int j = 0; j < 7; ++j) {
+                    const double sv_ = dmin_std(dsub(cs1, inset),
+                                                dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
+                    double qx, qy, qz;
+                    if (pl == 0) { qx = px; qy = py; qz = sv_; }
+                    else if (pl == 1) { qx = sv_; qy = px; qz = py; }
+                    else { qx = px; qy = sv_; qz = py; }
+                    ++queries;
+                    if (cache >= 0 && cache != sf) {
+                        ++tests;
+                        if (seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * STRIDE, sx, sy, sz, qx, qy, qz))
+                            continue;
+                    }
+                    const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz,
+                                                     qx, qy, qz, sf, -1, sf, sv, tests, batches);
+                    if (h < 0) return true;
+                    cache = h;
+                }
+                return false;
+            };
+            unsigned long long vis = 0;
+            bool vis64 = false;
+            for (int i = 0; i < 65; ++i) {
+                const bool v = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
+                if (i < 64) vis |= static_cast<unsigned long long>(v) << i;
+                else vis64 = v;
+            }
+            auto V = [&](int i) { return i == 64 ? vis64 : ((vis >> i) & 1ull) != 0; };
+            // refine (src/vistable.cpp:163-172)
+            auto refine = [&](double lo, double hi, bool lo_vis) {
+                for (int it = 0; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
+                    const double mid = dmul(0.5, dadd(lo, hi));
+                    if (col_vis(mid) == lo_vis) lo = mid;
+                    else hi = mid;
+                }
+                return dmul(0.5, dadd(lo, hi));
+            };
+            const double step = __ddiv_rn(1.0, 64.0);
+            bool have = false;
+            double b0 = 0, b1 = 0;
+            int i = 0;
+            while (i < 65) {   // runs (src/vistable.cpp:175-192)
+                if (!V(i)) {
+                    ++i;
+                    continue;
+                }
+                double start = __ddiv_rn(static_cast<double>(i), 64.0);
+                if (i > 0) start = refine(dsub(start, step), start, false);
+                int j = i;
+                while (j + 1 < 65 && V(j + 1)) ++j;
+                double end = __ddiv_rn(static_cast<double>(j), 64.0);
+                if (j + 1 < 65) end = refine(end, dadd(end, step), true);
+                if (!have || dsub(b1, b0) < dsub(end, start)) {   // std::max_element: first largest
+                    b0 = start;
+                    b1 = end;
+                    have = true;
+                }
+                i = j + 1;
+            }
+            if (!have) {
+                present = 0;   // fully hidden in this plane: no region
+                break;
+            }
+            has[pl] = 1;
+            sub[2 * pl] = b0;
+            sub[2 * pl + 1] = b1;
+            clp[pl] = (b0 > 1e-9 || b1 < 1.0 - 1e-9) ? 1 : 0;
+        }
+        if (present == 1 && !(has[0] | has[1] | has[2])) present = 0;
+        if (lane == 0) {
+            visrt_region r;
+            r.present = present;
+            r.pad = 0;
+            for (int q = 0; q < 3; ++q) {
+                r.has[q] = present == 1 ? has[q] : 0;
+                r.clipped[q] = present == 1 ? clp[q] : 0;
+            }
+            for (int q = 0; q < 6; ++q) r.sub[q] = present == 1 ? sub[q] : 0.0;
+            a.out[t] = r;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) {
+        atomicAdd(&a.counter[1], tests);
+        atomicAdd(&a.counter[2], queries);
+    }
+}
+
 static int persistent_grid_r(const void* fn, size_t smem, int device) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -461,6 +618,19 @@ static cudaError_t launch_regions_t(const RegionArgs& a, int device, cudaStream_
     const char* e = std::getenv("VISRT_FORCE_STREAM");
     const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
     const size_t smem = sweep_smem_bytes(a.s.n, a.s.ntiles, res);
+    // K4w for latency-bound launches (fewer tasks than ~2x the resident lanes:
+    // small snapshot batches, trajectory probes), K4 lanes for throughput.
+    // VISRT_K4_WARP=0/1 forces either kernel.
+    static const int force = [] {
+        const char* w = std::getenv("VISRT_K4_WARP");
+        return w ? (w[0] == '1' ? 1 : 0) : -1;
+    }();
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const bool warp = force >= 0 ? force == 1 : a.ntasks < 2ll * sms * 2 * kThreads;
+    if (warp)
+        return res ? launch_r(k_point_regions_warp<MAXV, true>, smem, a, device, st)
+                   : launch_r(k_point_regions_warp<MAXV, false>, smem, a, device, st);
     return res ? launch_r(k_point_regions<MAXV, true>, smem, a, device, st)
                : launch_r(k_point_regions<MAXV, false>, smem, a, device, st);
 }

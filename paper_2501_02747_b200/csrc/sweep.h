@@ -155,6 +155,76 @@ __device__ __forceinline__ int coop_exact(const double* __restrict__ srec, unsig
     return h == 0x7fffffff ? -1 : h;
 }
 
+// Warp-cooperative any-hit sweep of ONE segment (warp-uniform g / a->b):
+// lanes split the 64 tile boxes of a chunk, then the 64 member boxes of each
+// candidate tile; the survivors are compacted through the per-warp byte
+// buffer `sv` (64 entries) and run the exact predicate 32 at a time. The
+// sweep starts at the tile holding Morton face `home` (its neighbourhood is
+// the likeliest blocker) and wraps around. Returns the Morton index of a
+// blocking face (skip0 / skip1 never tested) or -1 when the segment is clear.
+// Must be called by all 32 lanes with identical arguments.
+template <int MAXV>
+__device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* __restrict__ srec, const SegF& g,
+                                            double ax, double ay, double az, double bx, double by, double bz,
+                                            int skip0, int skip1, int home, unsigned char* sv,
+                                            unsigned long long& tests, unsigned long long& batches) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int home_tile = home < 0 ? 0 : home / kTile;
+    const int hc = home_tile / kTile;
+    int hit = -1;
+    for (int cc = 0; cc < ctx.nchunks && hit < 0; ++cc) {
+        const int c = hc + cc < ctx.nchunks ? hc + cc : hc + cc - ctx.nchunks;
+        const int t0 = c * kTile;
+        const int tc = min(kTile, ctx.ntiles - t0);
+        const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
+        const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
+        unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
+                                  (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
+        unsigned long long later = 0;
+        if (cc == 0) {   // the home tile first, wrap around after
+            const unsigned long long below = (1ull << (home_tile - t0)) - 1ull;
+            later = cand & below;
+            cand &= ~below;
+        }
+        ++batches;
+        while ((cand | later) && hit < 0) {
+            if (!cand) {
+                cand = later;
+                later = 0;
+            }
+            const int base = (t0 + __ffsll(static_cast<long long>(cand)) - 1) * kTile;
+            cand &= cand - 1;
+            const int mc = min(kTile, ctx.n - base);
+            const int m0 = base + lane, m1 = base + lane + 32;
+            const bool v0 = lane < mc && m0 != skip0 && m0 != skip1 &&
+                            sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g);
+            const bool v1 = lane + 32 < mc && m1 != skip0 && m1 != skip1 &&
+                            sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g);
+            const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
+            ++batches;
+            const int clo = __popc(lo), tot = clo + __popc(hi);
+            if (tot == 0) continue;
+            if (v0) sv[__popc(lo & lt)] = static_cast<unsigned char>(lane);
+            if (v1) sv[clo + __popc(hi & lt)] = static_cast<unsigned char>(32 + lane);
+            __syncwarp();
+            for (int r = 0; r < tot && hit < 0; r += 32) {
+                const int idx = r + lane < tot ? sv[r + lane] : -1;
+                bool h = false;
+                if (idx >= 0) {
+                    ++tests;
+                    h = seg_hits<MAXV>(srec + static_cast<size_t>(base + idx) * STRIDE, ax, ay, az, bx, by, bz);
+                }
+                const unsigned hb = __ballot_sync(kFull, h);
+                if (hb) hit = __shfl_sync(kFull, base + idx, __ffs(hb) - 1);
+            }
+            __syncwarp();
+        }
+    }
+    return hit;
+}
+
 // Block setup: stage the tile boxes (and the member boxes when RESIDENT) in
 // shared memory with TMA bulk copies (cp.async.bulk, one mbarrier).
 template <bool RESIDENT>
