@@ -518,11 +518,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions_warp(RegionArgs a
                     else { qx = px; qy = sv_; qz = py; }
                     ++queries;
                     if (cache >= 0 && cache != sf) {
-                        ++tests;
+                        tests += lane == 0;   // warp-uniform test: count it once
                         if (seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * STRIDE, sx, sy, sz, qx, qy, qz))
                             continue;
                     }
-                    const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz,
+#ifndef VISRT_K4W_FIRST
+#define VISRT_K4W_FIRST 0
+#endif
+                    const int h = coop_any_hit<MAXV, VISRT_K4W_FIRST>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz,
                                                      qx, qy, qz, sf, -1, sf, sv, tests, batches);
                     if (h < 0) return true;
                     cache = h;

@@ -163,7 +163,7 @@ __device__ __forceinline__ int coop_exact(const double* __restrict__ srec, unsig
 // the likeliest blocker) and wraps around. Returns the Morton index of a
 // blocking face (skip0 / skip1 never tested) or -1 when the segment is clear.
 // Must be called by all 32 lanes with identical arguments.
-template <int MAXV>
+template <int MAXV, int FIRST = 0>
 __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* __restrict__ srec, const SegF& g,
                                             double ax, double ay, double az, double bx, double by, double bz,
                                             int skip0, int skip1, int home, unsigned char* sv,
@@ -209,8 +209,11 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
             if (v0) sv[__popc(lo & lt)] = static_cast<unsigned char>(lane);
             if (v1) sv[clo + __popc(hi & lt)] = static_cast<unsigned char>(32 + lane);
             __syncwarp();
-            for (int r = 0; r < tot && hit < 0; r += 32) {
-                const int idx = r + lane < tot ? sv[r + lane] : -1;
+            // FIRST > 0: a narrow first round (the home-ordered first survivors
+            // are the likeliest blockers), then rounds of 32
+            for (int r = 0; r < tot && hit < 0; r += (FIRST > 0 && r == 0) ? FIRST : 32) {
+                const int width = (FIRST > 0 && r == 0) ? FIRST : 32;
+                const int idx = (lane < width && r + lane < tot) ? sv[r + lane] : -1;
                 bool h = false;
                 if (idx >= 0) {
                     ++tests;
