@@ -27,6 +27,8 @@
 #include <numeric>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "capi_internal.h"
 #include "device.h"
 #include "sweep.h"
@@ -104,89 +106,147 @@ __device__ __forceinline__ bool rec_contains(const double* __restrict__ R, doubl
     return true;
 }
 
-__global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a) {
+// Candidate pool of a parent node (Engine::expand, src/raytracer.cpp:400-430):
+// all faces at the root or under an unfiltered prefix; else the chain
+// continuations of the prefix, then the obliques.
+struct Pool {
+    const int32_t* list;
+    long long lo, hi, npool;
+    bool all;
+    int d, last;
+};
+
+__device__ __forceinline__ TreeNode tree_parent(const TreeArgs& a, long long p) {
+    if (a.in) return a.in[p];
+    TreeNode par{};
+    par.snap = a.snap0 + static_cast<int>(p);
+    par.depth = 0;
+    par.f0 = par.f1 = par.f2 = -1;
+    par.rank = -1;
+    par.filtered = a.brute ? 0 : 1;
+    par.ix = a.tx[3 * static_cast<size_t>(par.snap)];
+    par.iy = a.tx[3 * static_cast<size_t>(par.snap) + 1];
+    par.iz = a.tx[3 * static_cast<size_t>(par.snap) + 2];
+    return par;
+}
+
+__device__ __forceinline__ Pool tree_pool(const TreeArgs& a, const TreeNode& par, int n) {
+    Pool q;
+    q.d = par.depth;
+    q.last = q.d == 0 ? -1 : (q.d == 1 ? par.f0 : (q.d == 2 ? par.f1 : par.f2));
+    q.list = nullptr;
+    q.lo = 0;
+    q.hi = n;
+    q.all = q.d == 0 || !par.filtered;
+    if (!q.all) {
+        if (q.d == 1) {
+            q.lo = a.off1[par.f0];
+            q.hi = a.off1[par.f0 + 1];
+            q.list = a.idx1;
+        } else if (q.d == 2 && par.rank >= 0) {
+            q.lo = a.off2[par.rank];
+            q.hi = a.off2[par.rank + 1];
+            q.list = a.idx2;
+        } else {
+            q.lo = q.hi = 0;
+        }
+    }
+    q.npool = (q.hi - q.lo) + (q.all ? 0 : a.nobl);
+    return q;
+}
+
+// candidate q of the pool: face c (+ its continuation rank at depth 1); ok =
+// not the immediate repeat and the parent image strictly in front
+__device__ __forceinline__ bool tree_child(const TreeArgs& a, const TreeNode& par, const Pool& P, long long q, int& c,
+                                           int& rank) {
+    rank = -1;
+    if (q < P.hi - P.lo) {
+        c = P.list ? P.list[P.lo + q] : static_cast<int>(P.lo + q);
+        if (!P.all && P.d == 1) rank = static_cast<int>(P.lo + q);
+    } else {
+        c = a.obl[q - (P.hi - P.lo)];
+    }
+    return c != P.last && (a.brute || sdist_face(a.s, c, par.ix, par.iy, par.iz) > kEps);
+}
+
+// K6 level expansion, pass 1: children per parent (warp per parent).
+__global__ void __launch_bounds__(256) k_tree_count(TreeArgs a, unsigned long long* cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const long long nparents = a.in ? a.nin : a.nsnap;
+    for (long long p = warp; p < nparents; p += nwarps) {
+        const TreeNode par = tree_parent(a, p);
+        const Pool P = tree_pool(a, par, a.s.n);
+        unsigned long long c_all = 0;
+        for (long long q0 = 0; q0 < P.npool; q0 += 32) {
+            const long long q = q0 + lane;
+            int c, rank;
+            const bool ok = q < P.npool && tree_child(a, par, P, q, c, rank);
+            c_all += __popc(__ballot_sync(kFull, ok));
+        }
+        if (lane == 0) cnt[p] = c_all;
+    }
+}
+
+// Per-snapshot node counts of one level: the level is ordered by snapshot
+// (children are written in parent order, roots in snapshot order), so each
+// snapshot's count is an upper_bound - lower_bound over the level.
+__global__ void k_tree_snapcount(const TreeNode* lvl, long long nn, int snap0, int ns,
+                                 unsigned long long* nodes_per_snap) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= ns) return;
+    const int sn = snap0 + q;
+    long long lo = 0, hi = nn;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (lvl[mid].snap < sn) lo = mid + 1;
+        else hi = mid;
+    }
+    long long lo2 = lo, hi2 = nn;
+    while (lo2 < hi2) {
+        const long long mid = (lo2 + hi2) >> 1;
+        if (lvl[mid].snap <= sn) lo2 = mid + 1;
+        else hi2 = mid;
+    }
+    nodes_per_snap[sn] += static_cast<unsigned long long>(lo2 - lo);
+}
+
+// Pass 2 (after an exclusive scan of the counts): each parent's children are
+// written contiguously at off[p], in pool order — coalesced rows, no global
+// append atomics, and a deterministic frontier order.
+__global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a, const unsigned long long* off) {
     const DevScene& s = a.s;
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const long long nparents = a.in ? a.nin : a.nsnap;
     for (long long p = warp; p < nparents; p += nwarps) {
-        TreeNode par;
-        if (a.in) {
-            par = a.in[p];
-        } else {
-            par = TreeNode{};
-            par.snap = a.snap0 + static_cast<int>(p);
-            par.depth = 0;
-            par.f0 = par.f1 = par.f2 = -1;
-            par.rank = -1;
-            par.filtered = a.brute ? 0 : 1;
-            par.ix = a.tx[3 * static_cast<size_t>(par.snap)];
-            par.iy = a.tx[3 * static_cast<size_t>(par.snap) + 1];
-            par.iz = a.tx[3 * static_cast<size_t>(par.snap) + 2];
-        }
-        const int d = par.depth;
-        const int last = d == 0 ? -1 : (d == 1 ? par.f0 : (d == 2 ? par.f1 : par.f2));
-        // candidate pool: all faces at the root or for an unfiltered prefix;
-        // else the chain continuations of the prefix, then the obliques
-        const int32_t* list = nullptr;
-        long long lo = 0, hi = s.n;
-        bool all = d == 0 || !par.filtered;
-        if (!all) {
-            if (d == 1) {
-                lo = a.off1[par.f0];
-                hi = a.off1[par.f0 + 1];
-                list = a.idx1;
-            } else if (d == 2 && par.rank >= 0) {
-                lo = a.off2[par.rank];
-                hi = a.off2[par.rank + 1];
-                list = a.idx2;
-            } else {
-                lo = hi = 0;
-            }
-        }
-        const long long npool = (hi - lo) + (all ? 0 : a.nobl);
-        for (long long q0 = 0; q0 < npool; q0 += 32) {
+        const TreeNode par = tree_parent(a, p);
+        const Pool P = tree_pool(a, par, s.n);
+        unsigned long long w = off[p];
+        for (long long q0 = 0; q0 < P.npool; q0 += 32) {
             const long long q = q0 + lane;
-            bool ok = false;
-            int c = -1;
-            int rank = -1;
-            if (q < npool) {
-                if (q < hi - lo) {
-                    c = list ? list[lo + q] : static_cast<int>(lo + q);
-                    if (!all && d == 1) rank = static_cast<int>(lo + q);
-                } else {
-                    c = a.obl[q - (hi - lo)];
-                }
-                ok = c != last && (a.brute || sdist_face(s, c, par.ix, par.iy, par.iz) > kEps);
-            }
+            int c = -1, rank = -1;
+            const bool ok = q < P.npool && tree_child(a, par, P, q, c, rank);
             const unsigned m = __ballot_sync(kFull, ok);
-            if (!m) continue;
-            unsigned long long base = 0;
-            if (lane == 0) {
-                base = atomicAdd(a.nout, static_cast<unsigned long long>(__popc(m)));
-                atomicAdd(a.nodes_per_snap + par.snap, static_cast<unsigned long long>(__popc(m)));
-            }
-            base = __shfl_sync(kFull, base, 0);
             if (ok) {
-                const long long slot = static_cast<long long>(base) + __popc(m & ((1u << lane) - 1u));
-                if (slot < a.cap) {
-                    TreeNode ch;
-                    ch.snap = par.snap;
-                    ch.depth = d + 1;
-                    ch.f0 = d == 0 ? c : par.f0;
-                    ch.f1 = d == 1 ? c : par.f1;
-                    ch.f2 = d == 2 ? c : par.f2;
-                    ch.rank = d == 1 ? rank : -1;
-                    ch.filtered = par.filtered && s.orient[c] != 2;
-                    ch.pad = 0;
-                    ch.ix = par.ix;
-                    ch.iy = par.iy;
-                    ch.iz = par.iz;
-                    mirror_face(s, c, ch.ix, ch.iy, ch.iz);
-                    a.out[slot] = ch;
-                }
+                TreeNode ch;
+                ch.snap = par.snap;
+                ch.depth = P.d + 1;
+                ch.f0 = P.d == 0 ? c : par.f0;
+                ch.f1 = P.d == 1 ? c : par.f1;
+                ch.f2 = P.d == 2 ? c : par.f2;
+                ch.rank = P.d == 1 ? rank : -1;
+                ch.filtered = par.filtered && s.orient[c] != 2;
+                ch.pad = 0;
+                ch.ix = par.ix;
+                ch.iy = par.iy;
+                ch.iz = par.iz;
+                mirror_face(s, c, ch.ix, ch.iy, ch.iz);
+                a.out[w + __popc(m & ((1u << lane) - 1u))] = ch;
             }
+            w += __popc(m);
         }
     }
 }
@@ -508,6 +568,10 @@ struct visrt_tracer {
     double* d_edge_ab = nullptr;
     // frontier / candidate / path buffers, allocated on the first trace
     visrt::TreeNode* lvl[2] = {nullptr, nullptr};
+    unsigned long long* cnt = nullptr;   // per parent child counts (+1 for the scan total)
+    unsigned long long* off = nullptr;
+    void* scan_tmp = nullptr;
+    size_t scan_bytes = 0;
     visrt::Cand* cand = nullptr;
     visrt_path* dpaths = nullptr;
     // results of the last trace
@@ -683,10 +747,14 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
         ck(cudaMemsetAsync(d_nodes, 0, std::max<int64_t>(nsnap, 1) * 8, st), "memset");
         unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(8, tmp);   // nout, ncand, npaths, cursor, tests
         // frontier / candidate / path buffers (capacity-bounded; batches adapt)
-        const long long node_cap = 1ll << 24;   // 16.7M nodes per level per batch (0.9 GB)
+        const long long node_cap = 1ll << 25;   // 33.5M nodes per level per batch (1.9 GB per level buffer)
         const long long cand_cap = 1ll << 22;
         const long long path_cap = 1ll << 22;
         if (!tr->lvl[0]) {
+            tr->cnt = visrt::dalloc<unsigned long long>(node_cap + 1, tr->allocs);
+            tr->off = visrt::dalloc<unsigned long long>(node_cap + 1, tr->allocs);
+            cub::DeviceScan::ExclusiveSum(nullptr, tr->scan_bytes, tr->cnt, tr->off, node_cap + 1);
+            tr->scan_tmp = visrt::dalloc<char>(tr->scan_bytes, tr->allocs);
             tr->lvl[0] = visrt::dalloc<visrt::TreeNode>(node_cap, tr->allocs);
             tr->lvl[1] = visrt::dalloc<visrt::TreeNode>(node_cap, tr->allocs);
             tr->cand = visrt::dalloc<visrt::Cand>(cand_cap, tr->allocs);
@@ -762,15 +830,23 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
                 a.in = in;
                 a.nin = nin;
                 a.out = lvl[depth & 1];
-                a.nout = c_nout;
                 a.cap = node_cap;
-                ck(cudaMemsetAsync(c_nout, 0, 8, st), "memset");
-                visrt::k_tree_expand<<<eb, 256, 0, st>>>(a);
-                ck(cudaGetLastError(), "k_tree_expand");
+                // count -> exclusive scan -> fill (src/raytracer.cpp:400-430 per parent)
+                const long long np = in ? nin : ns;
+                visrt::k_tree_count<<<eb, 256, 0, st>>>(a, tr->cnt);
+                ck(cudaGetLastError(), "k_tree_count");
+                ck(cub::DeviceScan::ExclusiveSum(tr->scan_tmp, tr->scan_bytes, tr->cnt, tr->off, np + 1, st), "scan");
                 unsigned long long no = 0;
-                ck(cudaMemcpyAsync(&no, c_nout, 8, cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaMemcpyAsync(&no, tr->off + np, 8, cudaMemcpyDeviceToHost, st), "D2H");
                 ck(cudaStreamSynchronize(st), "sync");
                 if (static_cast<long long>(no) > node_cap) return false;
+                if (no) {
+                    visrt::k_tree_expand<<<eb, 256, 0, st>>>(a, tr->off);
+                    ck(cudaGetLastError(), "k_tree_expand");
+                    visrt::k_tree_snapcount<<<(ns + 255) / 256, 256, 0, st>>>(lvl[depth & 1], static_cast<long long>(no),
+                                                                             s0, ns, d_nodes);
+                    ck(cudaGetLastError(), "k_tree_snapcount");
+                }
                 seqs += static_cast<long long>(no);
                 if (no == 0) break;
                 if (!resolve_level(lvl[depth & 1], static_cast<long long>(no))) return false;
