@@ -242,6 +242,22 @@ typedef struct {
 #define VISRT_TRACE_BRUTE_FORCE 0x4
 int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const double* rx,
                 int flags, visrt_trace_stats* stats, void* stream);
+/* One fixed interaction sequence (SequenceKey, src/raytracer.cpp:528-552):
+ * reflecting faces (source side first) + optional final diffraction edge. */
+typedef struct {
+    int32_t nrefl;         /* 0..3 */
+    int32_t faces[3];
+    int32_t edge;          /* -1: the path ends at the receiver */
+} visrt_seqkey;
+/* resolve_keys (src/raytracer.cpp:554-570), the dynamic-run re-solve: for
+ * every sample k (tx[k], rx[k] or rx[0] with VISRT_TRACE_RX_FIXED) and every
+ * key q in key_off[k]..key_off[k+1]-1, resolve_sequence(keys[q]) at the new
+ * endpoints: ok[q] = a valid path exists (unfolding + every leg clear), and
+ * paths[q] (may be NULL) = that path (snap = k). edge_ab: the scene's edges. */
+int visrt_resolve_keys(visrt_scene* scene, int64_t nsamp, const double* tx, const double* rx, int flags,
+                       const int64_t* key_off, const visrt_seqkey* keys, int32_t nedges, const double* edge_ab,
+                       uint8_t* ok, visrt_path* paths, visrt_stats* stats, void* stream);
+
 /* The scene's edges for diffraction (Scene::edges, include/rt/scene.hpp:85-95):
  * edge e = (a, b) at edge_ab[6e..6e+5]; edge_rank[e] = order of its id string. */
 int visrt_tracer_set_edges(visrt_tracer* tracer, int32_t nedges, const double* edge_ab, const int32_t* edge_rank);

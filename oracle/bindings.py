@@ -235,6 +235,11 @@ class vref_mobile_row(C.Structure):
                 ("label_end", C.c_char * 16), ("parent", C.c_char * 64), ("blockage", C.c_char * 64)]
 
 
+class vref_dyn_sample(C.Structure):
+    _fields_ = [("s", C.c_double), ("segment", C.c_int32), ("retraced", C.c_int32), ("npaths", C.c_int32),
+                ("first", C.c_int32)]
+
+
 class vref_path(C.Structure):
     _fields_ = [("ninter", C.c_int32), ("face", C.c_int32 * 6), ("is_diff", C.c_int32 * 6),
                 ("points", C.c_double * 24), ("length", C.c_double), ("delay", C.c_double),
@@ -302,6 +307,10 @@ class RefOracle:
             L.vref_scene_from_shells.argtypes = [C.c_int32, _i32p, _f64p, C.c_char_p, _i32p, C.c_int32,
                                                  C.c_char_p]
             L.vref_closest_edge.argtypes = [C.c_void_p, _f64p]
+            L.vref_dynamic_trace.restype = C.c_int64
+            L.vref_dynamic_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _f64p, _f64p, C.c_int32, C.c_int32,
+                                             C.c_double, C.POINTER(vref_dyn_sample), C.c_int64, C.POINTER(vref_path),
+                                             C.c_int64, C.POINTER(C.c_int64)]
             L.vref_trajectory_table.restype = C.c_int64
             L.vref_trajectory_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _f64p, C.c_int32,
                                                 C.POINTER(vref_mobile_row), C.c_int64]
@@ -446,6 +455,27 @@ class RefOracle:
         image = np.zeros(3 * cap, np.float64)
         n = L.vref_image_tree(self.h, src, depth, face, parent, dep, image, cap)
         return face[:n], parent[:n], dep[:n], image[:3 * n].reshape(n, 3)
+
+    def dynamic_trace(self, m, waypoints, rx, max_refl: int, diffraction: bool, step: float):
+        """rt::dynamic_trace (fixed receiver): samples with their paths."""
+        L = self.lib()
+        scap, pcap = 1 << 14, 1 << 18
+        smp = (vref_dyn_sample * scap)()
+        pth = (vref_path * pcap)()
+        npth = C.c_int64()
+        wp = np.ascontiguousarray(np.asarray(waypoints, np.float64)[:, :3]).reshape(-1)
+        ns = L.vref_dynamic_trace(self.h, m, len(wp) // 3, wp, np.ascontiguousarray(rx, np.float64), max_refl,
+                                  int(diffraction), step, smp, scap, pth, pcap, C.byref(npth))
+        if ns < 0:
+            raise RuntimeError(L.vref_last_error().decode())
+        out = []
+        for k in range(ns):
+            d = smp[k]
+            ps = [pth[d.first + q] for q in range(d.npaths)]
+            out.append({"s": d.s, "segment": d.segment, "retraced": bool(d.retraced),
+                        "paths": [{"identity": p.identity.decode(), "points": list(p.points[: 3 * (p.ninter + 2)]),
+                                   "length": p.length} for p in ps]})
+        return out
 
     def closest_edge(self, rx) -> int:
         return int(self.lib().vref_closest_edge(self.h, np.ascontiguousarray(rx, np.float64)))

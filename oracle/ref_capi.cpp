@@ -589,6 +589,62 @@ int64_t vref_image_tree(void* h, const double* src, int32_t depth, int32_t* face
     return n;
 }
 
+// dynamic_trace against a fixed receiver (proj/src/raytracer.cpp:590-643):
+// per sample s, segment, retraced flag and the paths (identity, points, length)
+// flattened; waypoints [nwp][3] with speed 1 m/s.
+typedef struct {
+    double s;
+    int32_t segment;
+    int32_t retraced;
+    int32_t npaths;
+    int32_t first;   // index of its first path in the path array
+} vref_dyn_sample;
+
+int64_t vref_dynamic_trace(void* h, void* m, int32_t nwp, const double* wp, const double* rx, int32_t max_refl,
+                           int32_t diffraction, double step, vref_dyn_sample* samples, int64_t scap,
+                           vref_path* paths, int64_t pcap, int64_t* npaths_out) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    try {
+        R::Trajectory traj;
+        for (int32_t k = 0; k < nwp; ++k) traj.waypoints.push_back({wp[3 * k], wp[3 * k + 1], wp[3 * k + 2]});
+        traj.speeds.assign(static_cast<size_t>(nwp > 1 ? nwp - 1 : 1), 1.0);
+        const auto res = R::dynamic_trace(s, *static_cast<R::InterVisMatrix*>(m), traj, {rx[0], rx[1], rx[2]},
+                                          max_refl, diffraction != 0, step);
+        int64_t np = 0;
+        const int64_t ns = static_cast<int64_t>(res.samples.size());
+        for (int64_t k = 0; k < ns; ++k) {
+            const auto& smp = res.samples[static_cast<size_t>(k)];
+            if (k < scap) {
+                samples[k].s = smp.s;
+                samples[k].segment = smp.segment;
+                samples[k].retraced = smp.retraced ? 1 : 0;
+                samples[k].npaths = static_cast<int32_t>(smp.paths.size());
+                samples[k].first = static_cast<int32_t>(np);
+            }
+            for (const auto& p : smp.paths) {
+                if (np < pcap) {
+                    vref_path& o = paths[np];
+                    std::memset(&o, 0, sizeof(o));
+                    o.ninter = static_cast<int32_t>(p.interactions.size());
+                    for (size_t q = 0; q < p.points.size() && q < 8; ++q) {
+                        o.points[3 * q] = p.points[q].x;
+                        o.points[3 * q + 1] = p.points[q].y;
+                        o.points[3 * q + 2] = p.points[q].z;
+                    }
+                    o.length = p.length;
+                    o.delay = p.delay;
+                    std::snprintf(o.identity, sizeof(o.identity), "%s", p.identity().c_str());
+                }
+                ++np;
+            }
+        }
+        *npaths_out = np;
+        return ns;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
+
 // closest_diffraction_edge (proj/src/vistable.cpp:545-561): edge index or -1.
 int32_t vref_closest_edge(void* h, const double* rx) {
     const R::Scene& s = static_cast<RefScene*>(h)->scene;

@@ -31,7 +31,7 @@ EXPORTS = [
     "visrt_chain_reach", "visrt_trajectory_table", "visrt_mobile_table_rows", "visrt_mobile_table_destroy",
     "visrt_chain_triples", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results", "visrt_image_tree", "visrt_closest_edges",
-    "visrt_tracer_set_edges", "visrt_trace_snapshot_edges",
+    "visrt_tracer_set_edges", "visrt_trace_snapshot_edges", "visrt_resolve_keys",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -61,6 +61,10 @@ class visrt_names(C.Structure):
 class visrt_path(C.Structure):
     _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 3), ("edge", C.c_int32), ("snap", C.c_int32),
                 ("points", C.c_double * 18), ("length", C.c_double)]
+
+
+class visrt_seqkey(C.Structure):
+    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 3), ("edge", C.c_int32)]
 
 
 class visrt_trace_stats(C.Structure):
@@ -147,6 +151,9 @@ def lib():
                                    C.c_int64, C.POINTER(C.c_int64), C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_closest_edges.argtypes = [C.c_void_p, C.c_int64, _f64p, C.c_int32, C.c_void_p, C.c_void_p, _i32p,
                                       C.POINTER(visrt_stats), C.c_void_p]
+    L.visrt_resolve_keys.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(visrt_stats),
+                                     C.c_void_p]
     L.visrt_trace_snapshot_edges.restype = C.c_int64
     L.visrt_trace_snapshot_edges.argtypes = [C.c_void_p, C.c_void_p]
     L.visrt_tracer_set_edges.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]

@@ -378,6 +378,49 @@ class Tracer:
         return out, nodes, st
 
 
+def resolve_keys(scene: Scene, tx, rx, keys: Sequence[Sequence[Tuple[Sequence[int], int]]],
+                 edges: Optional[Sequence[dict]] = None):
+    """resolve_keys (src/raytracer.cpp:554-570) batched: keys[k] = the fixed
+    sequences (faces, edge index or -1) to re-solve at sample k (tx[k], rx[k];
+    one rx = fixed receiver). Returns per sample the valid paths
+    {faces, edge, points, length} in key order, and the stats."""
+    tx = np.ascontiguousarray(np.asarray(tx, np.float64).reshape(-1, 3))
+    rx = np.ascontiguousarray(np.asarray(rx, np.float64).reshape(-1, 3))
+    ns = len(tx)
+    flags = 1 if len(rx) == 1 and ns != 1 else 0
+    off = np.zeros(ns + 1, np.int64)
+    off[1:] = np.cumsum([len(kk) for kk in keys])
+    nk = int(off[-1])
+    karr = (_capi.visrt_seqkey * max(nk, 1))()
+    q = 0
+    for kk in keys:
+        for faces, edge in kk:
+            karr[q].nrefl = len(faces)
+            for i, f in enumerate(faces):
+                karr[q].faces[i] = int(f)
+            karr[q].edge = int(edge)
+            q += 1
+    ab = np.ascontiguousarray(np.array([list(e["a"]) + list(e["b"]) for e in (edges or [])], np.float64).reshape(-1))
+    ok = np.zeros(max(nk, 1), np.uint8)
+    paths = (_capi.visrt_path * max(nk, 1))()
+    st = _capi.visrt_stats()
+    check(lib().visrt_resolve_keys(scene.h, ns, tx.reshape(-1), rx.reshape(-1), flags, off.ctypes.data,
+                                   C.cast(karr, C.c_void_p), len(edges or []), ab.ctypes.data if len(ab) else None,
+                                   ok.ctypes.data, C.cast(paths, C.c_void_p), C.byref(st), None))
+    out = []
+    for k in range(ns):
+        row = []
+        for q in range(off[k], off[k + 1]):
+            if not ok[q]:
+                continue
+            p = paths[q]
+            npts = p.nrefl + 2 + (1 if p.edge >= 0 else 0)
+            row.append({"faces": list(p.faces[: p.nrefl]), "edge": int(p.edge), "points": list(p.points[: 3 * npts]),
+                        "length": p.length})
+        out.append(row)
+    return out, _stats_dict(st)
+
+
 def brute_force_trace(scene: Scene, tx, rx, max_refl: int, allow_diffraction: bool = False,
                       edges: Optional[Sequence[dict]] = None):
     """rt::brute_force_trace (include/rt/raytracer.hpp:78-83): the conventional

@@ -43,6 +43,7 @@ struct TreeNode {
 
 struct Cand {
     int32_t snap, depth, f[3], edge;   // edge: diffraction edge index (-1: ends at the receiver)
+    int32_t node, pad;                 // keyed mode: index of the source node (result slot)
     double pts[18];                    // tx, reflections..., [diffraction point], rx
     double length;
 };
@@ -76,6 +77,11 @@ struct TreeArgs {
     const int32_t* snap_edge;             // [total snapshots] closest diffraction edge or -1 (nullptr: none)
     const double* edge_ab;                // [nedges][6]
     int32_t brute;                        // brute_force_trace: no chain filter, no image prune
+    // keyed mode (resolve_keys): every node is one fixed sequence; node.rank
+    // holds its edge (-1: ends at the receiver); results go to per-node slots
+    int32_t keyed;
+    uint8_t* slot_ok;
+    visrt_path* slot_paths;
 };
 
 __device__ __forceinline__ double sdist_face(const DevScene& s, int f, double x, double y, double z) {
@@ -326,8 +332,9 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
         }
         if (!fwd) continue;
-        const int edge = a.snap_edge ? a.snap_edge[snap] : -1;
-        for (int v = 0; v < (edge >= 0 ? 2 : 1); ++v) {
+        const int kedge = a.keyed ? a.in[t].rank : -1;
+        const int edge = a.keyed ? kedge : (a.snap_edge ? a.snap_edge[snap] : -1);
+        for (int v = (a.keyed && kedge >= 0) ? 1 : 0; v < (edge >= 0 ? 2 : 1); ++v) {
             bool ok = true;
             double target[3] = {Rx[0], Rx[1], Rx[2]};
             if (v == 1) {
@@ -370,6 +377,8 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             c.f[1] = f[1];
             c.f[2] = f[2];
             c.edge = v ? edge : -1;
+            c.node = static_cast<int32_t>(t);
+            c.pad = 0;
             c.pts[0] = T[0];
             c.pts[1] = T[1];
             c.pts[2] = T[2];
@@ -423,8 +432,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
 
     auto emit = [&]() {
         const Cand& c = a.cand[cid];
-        const unsigned long long slot = atomicAdd(a.npaths, 1ull);
-        if (static_cast<long long>(slot) < a.path_cap) {
+        const unsigned long long slot = a.keyed ? static_cast<unsigned long long>(c.node) : atomicAdd(a.npaths, 1ull);
+        if (a.keyed || static_cast<long long>(slot) < a.path_cap) {
             visrt_path p;
             p.nrefl = c.depth;
             p.faces[0] = c.f[0];
@@ -435,7 +444,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
             const int npts = c.depth + 2 + (c.edge >= 0 ? 1 : 0);
             for (int i = 0; i < 18; ++i) p.points[i] = i < 3 * npts ? c.pts[i] : 0.0;
             p.length = c.length;
-            a.paths[slot] = p;
+            if (a.keyed) {
+                a.slot_paths[slot] = p;
+                a.slot_ok[slot] = 1;
+            } else {
+                a.paths[slot] = p;
+            }
         }
         active = false;
     };
@@ -932,4 +946,114 @@ extern "C" int64_t visrt_trace_snapshot_edges(const visrt_tracer* tr, int32_t* s
     if (snap_edge)
         for (int64_t k = 0; k < tr->nsnap; ++k) snap_edge[k] = tr->snap_edge.empty() ? -1 : tr->snap_edge[k];
     return tr->nsnap;
+}
+
+// resolve_keys (src/raytracer.cpp:554-570): re-solve fixed interaction
+// sequences at new endpoints — the dynamic-run inner loop — as ONE batched
+// pass: every (sample, key) is a keyed node of the unfold kernel (forward
+// images, backward unfolding, Fermat point for a diffraction key) and its legs
+// are swept by the leg kernel; results land in per-(sample, key) slots.
+extern "C" int visrt_resolve_keys(visrt_scene* sc, int64_t nsamp, const double* tx, const double* rx, int flags,
+                                  const int64_t* key_off, const visrt_seqkey* keys, int32_t nedges,
+                                  const double* edge_ab, uint8_t* ok, visrt_path* paths, visrt_stats* stats,
+                                  void* stream) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        if (nsamp < 0 || (nsamp > 0 && (!tx || !rx || !key_off))) throw visrt::UsageError("null argument");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const visrt::DevScene& ds = visrt::scene_dev(sc);
+        const int device = visrt::scene_device(sc);
+        const int rx_fixed = (flags & VISRT_TRACE_RX_FIXED) ? 1 : 0;
+        const int64_t nk = nsamp > 0 ? key_off[nsamp] : 0;
+        std::vector<visrt::TreeNode> nodes(static_cast<size_t>(nk));
+        for (int64_t k = 0; k < nsamp; ++k) {
+            for (int64_t q = key_off[k]; q < key_off[k + 1]; ++q) {
+                const visrt_seqkey& K = keys[q];
+                if (K.nrefl < 0 || K.nrefl > 3) throw visrt::UsageError("keys hold 0..3 reflections");
+                for (int i = 0; i < K.nrefl; ++i)
+                    if (K.faces[i] < 0 || K.faces[i] >= ds.n) throw visrt::UsageError("bad face index");
+                if (K.edge < -1 || K.edge >= nedges) throw visrt::UsageError("bad edge index");
+                visrt::TreeNode& nd = nodes[static_cast<size_t>(q)];
+                nd = visrt::TreeNode{};
+                nd.snap = static_cast<int32_t>(k);
+                nd.depth = K.nrefl;
+                nd.f0 = K.nrefl > 0 ? K.faces[0] : -1;
+                nd.f1 = K.nrefl > 1 ? K.faces[1] : -1;
+                nd.f2 = K.nrefl > 2 ? K.faces[2] : -1;
+                nd.rank = K.edge;
+            }
+        }
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        auto up = [&](const void* src, size_t bytes) {
+            void* d = visrt::dalloc<char>(std::max<size_t>(bytes, 16), tmp);
+            if (bytes) ck(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
+            return d;
+        };
+        double* d_tx = static_cast<double*>(up(tx, nsamp * 24));
+        double* d_rx = static_cast<double*>(up(rx, (rx_fixed ? 1 : nsamp) * 24));
+        visrt::TreeNode* d_nodes = static_cast<visrt::TreeNode*>(up(nodes.data(), nodes.size() * sizeof(visrt::TreeNode)));
+        double* d_edges = static_cast<double*>(up(edge_ab, std::max(nedges, 0) * 48));
+        uint8_t* d_ok = visrt::dalloc<uint8_t>(std::max<int64_t>(nk, 1), tmp);
+        visrt_path* d_paths = visrt::dalloc<visrt_path>(std::max<int64_t>(nk, 1), tmp);
+        const long long cand_cap = std::min<long long>(std::max<int64_t>(nk, 1), 1ll << 22);
+        visrt::Cand* d_cand = visrt::dalloc<visrt::Cand>(cand_cap, tmp);
+        unsigned long long* d_ctr = visrt::dalloc<unsigned long long>(4, tmp);   // ncand, cursor, tests
+        ck(cudaMemsetAsync(d_ok, 0, std::max<int64_t>(nk, 1), st), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        visrt::TreeArgs a{};
+        a.s = ds;
+        a.tx = d_tx;
+        a.rx = d_rx;
+        a.rx_fixed = rx_fixed;
+        a.edge_ab = d_edges;
+        a.keyed = 1;
+        a.cand = d_cand;
+        a.cand_cap = cand_cap;
+        a.ncand = d_ctr;
+        a.counter = d_ctr + 1;
+        unsigned long long tests = 0;
+        const int ub = visrt::grid_of(reinterpret_cast<const void*>(ds.maxv <= 4 ? visrt::k_tree_unfold<4>
+                                                                                  : visrt::k_tree_unfold<8>),
+                                      256, 0, device);
+        for (long long b0 = 0; b0 < nk; b0 += cand_cap) {
+            const long long nb = std::min<long long>(cand_cap, nk - b0);
+            a.in = d_nodes + b0;
+            a.nin = nb;
+            a.slot_ok = d_ok + b0;
+            a.slot_paths = d_paths + b0;
+            ck(cudaMemsetAsync(d_ctr, 0, 32, st), "memset");
+            if (ds.maxv <= 4) visrt::k_tree_unfold<4><<<ub, 256, 0, st>>>(a);
+            else visrt::k_tree_unfold<8><<<ub, 256, 0, st>>>(a);
+            ck(cudaGetLastError(), "k_tree_unfold");
+            if (ds.maxv <= 4) visrt::launch_legs_t<4>(a, device, st);
+            else visrt::launch_legs_t<8>(a, device, st);
+            unsigned long long t2 = 0;
+            ck(cudaMemcpyAsync(&t2, d_ctr + 2, 8, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            tests += t2;
+        }
+        cudaEventRecord(e1, st);
+        if (nk > 0) {
+            ck(cudaMemcpyAsync(ok, d_ok, nk, cudaMemcpyDeviceToHost, st), "D2H");
+            if (paths) ck(cudaMemcpyAsync(paths, d_paths, nk * sizeof(visrt_path), cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        int64_t found = 0;
+        for (int64_t q = 0; q < nk; ++q) found += ok[q] != 0;
+        if (stats) {
+            *stats = visrt_stats{};
+            stats->pairs = nk;
+            stats->admitted = found;
+            stats->tests_exec = static_cast<int64_t>(tests);
+            stats->ms = ms;
+        }
+    });
 }

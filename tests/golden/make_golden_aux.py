@@ -93,8 +93,31 @@ def main() -> None:
                                                     "length": float(p["length"]).hex()} for p in paths],
                                                   key=lambda p: p["identity"])})
     print("brute traces", len(brute))
+    # dynamic_trace against a fixed receiver (proj/src/raytracer.cpp:590-643): the
+    # non-retraced samples are resolve_keys of their segment's first trace
+    dyn = []
+    djobs2 = [("screened_wall", "route_drive_by", (25, -5, 1.5)), ("street_canyon", "route_corridor", (5, 35, 1.5)),
+              ("two_buildings", "route_drive_by", (35, 5, 2))]
+    for name, route_name, rx in djobs2:
+        r = bindings.RefOracle(path=os.path.join(FIXTURES, name + ".json"))
+        m = r.build_matrix(2)
+        with open(os.path.join(FIXTURES, route_name + ".json")) as fh:
+            wps = [w[:3] for w in json.load(fh)["waypoints"]]
+        for dif in (False, True):
+            try:
+                smp = r.dynamic_trace(m, np.asarray(wps, np.float64), np.asarray(rx, np.float64), 2, dif, 0.5)
+            except RuntimeError as e:
+                print(name, "dynamic", e)
+                continue
+            dyn.append({"scene": name, "waypoints": wps, "rx": list(rx), "diffraction": dif,
+                        "samples": [{"s": float(q["s"]).hex(), "segment": q["segment"], "retraced": q["retraced"],
+                                     "paths": [{"identity": p["identity"], "points": [float(x).hex() for x in p["points"]],
+                                                "length": float(p["length"]).hex()} for p in q["paths"]]}
+                                    for q in smp]})
+            print(name, "dynamic", dif, len(smp), "samples")
     with open(os.path.join(HERE, "aux.json"), "w") as fh:
-        json.dump({"image_trees": trees, "closest_edges": edges, "diffraction_traces": diff, "brute_traces": brute},
+        json.dump({"image_trees": trees, "closest_edges": edges, "diffraction_traces": diff, "brute_traces": brute,
+                   "dynamic": dyn},
                   fh, separators=(",", ":"))
 
 

@@ -113,3 +113,61 @@ def test_brute_force_trace_vs_reference(k):
         acc = Tracer(sc, t["order"], admitted_bits=bits, triples=tri, edges=d["edges"])
         apaths, _, _ = acc.trace([t["tx"]], [t["rx"]], allow_diffraction=t["diffraction"])
         assert sorted(ident(p) for p in apaths[0]) == [p["identity"] for p in t["paths"]]
+
+
+def _route_position(wps, s):
+    """Trajectory::position_at (proj/src/scene.cpp:459-469) in float64."""
+    w = np.asarray(wps, np.float64)
+    if s <= 0:
+        return w[0]
+    for i in range(len(w) - 1):
+        d = w[i + 1] - w[i]
+        seg = np.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+        if s <= seg:
+            return w[i] + (w[i + 1] - w[i]) * (s / seg)
+        s -= seg
+    return w[-1]
+
+
+@pytest.mark.parametrize("k", range(len(AUX["dynamic"])),
+                         ids=[f"{t['scene']}-d{int(t['diffraction'])}" for t in AUX["dynamic"]])
+def test_resolve_keys_vs_reference_dynamic_trace(k):
+    """dynamic_trace's re-solve (proj/src/raytracer.cpp:554-570, 590-643): the
+    keys of each coherence segment's retraced sample, re-solved on the GPU at
+    every later sample of the segment in ONE batched call, give the
+    reference's paths (identity, points, length) bit for bit."""
+    from paper_2501_02747_b200.core import resolve_keys, path_identity
+    t = AUX["dynamic"][k]
+    d = G.load(t["scene"])
+    s = G.soup(d)
+    fid = {f: i for i, f in enumerate(s.ids)}
+    eid = {e["id"]: i for i, e in enumerate(d["edges"])}
+
+    def key_of(ident):
+        if ident == "LOS":
+            return [], -1
+        import re
+        faces, edge = [], -1
+        for kind, name in re.findall(r"(R|D):(.*?)(?=/(?:R|D):|$)", ident):   # edge ids contain '/'
+            if kind == "R":
+                faces.append(fid[name])
+            else:
+                edge = eid[name]
+        return faces, edge
+
+    seg_keys, tx, keys, expect = {}, [], [], []
+    for smp in t["samples"]:
+        if smp["retraced"]:
+            seg_keys[smp["segment"]] = [key_of(p["identity"]) for p in smp["paths"]]
+            continue
+        tx.append(_route_position(t["waypoints"], float.fromhex(smp["s"])))
+        keys.append(seg_keys[smp["segment"]])
+        expect.append(smp["paths"])
+    assert tx, "no re-solved samples"
+    with Scene(s) as sc:
+        got, st = resolve_keys(sc, np.array(tx), [t["rx"]], keys, d["edges"])
+    for g, e in zip(got, expect):
+        gp = sorted([{"identity": path_identity(s.ids, p["faces"], d["edges"][p["edge"]]["id"] if p["edge"] >= 0 else None),
+                      "points": [float(x).hex() for x in p["points"]], "length": float(p["length"]).hex()} for p in g],
+                    key=lambda p: p["identity"])
+        assert gp == e
