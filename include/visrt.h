@@ -194,6 +194,17 @@ int visrt_trajectory_table(visrt_scene* scene, int32_t nwp, const double* waypoi
 int64_t visrt_mobile_table_rows(const visrt_mobile_table* table, visrt_mobile_row* rows, int64_t cap);
 void visrt_mobile_table_destroy(visrt_mobile_table* table);
 
+/* Binary matrix / pair-graph cache (replaces the text
+ * format of save_matrix / load_matrix, src/vismatrix.cpp:805-968): the
+ * admitted order-1 bits + the feasible order-2 triples, tied to the scene by a
+ * fingerprint (load on another scene -> status 3 SceneError). Host-only
+ * handles (device < 0) are accepted. load: bits and triples NULL = header
+ * only (max_order, ntriples); else cap must hold the cached triples. */
+int visrt_cache_save(const char* path, const visrt_scene* scene, int32_t max_order, const uint64_t* admitted_bits,
+                     int64_t ntriples, const int32_t* triples);
+int visrt_cache_load(const char* path, const visrt_scene* scene, int32_t* max_order, uint64_t* admitted_bits,
+                     int32_t* triples, int64_t cap, int64_t* ntriples);
+
 /* Order-2 chains of build_matrix(scene, 2) (src/vismatrix.cpp:715-797): every
  * triple p->t->a of admitted pairs that passes chain_triple_feasible and
  * second_order_check in each shared working plane. admitted_bits NULL = the

@@ -32,6 +32,7 @@ EXPORTS = [
     "visrt_chain_triples", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results", "visrt_image_tree", "visrt_closest_edges",
     "visrt_tracer_set_edges", "visrt_trace_snapshot_edges", "visrt_resolve_keys",
+    "visrt_cache_save", "visrt_cache_load",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -154,6 +155,9 @@ def lib():
     L.visrt_resolve_keys.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_int, C.c_void_p, C.c_void_p,
                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(visrt_stats),
                                      C.c_void_p]
+    L.visrt_cache_save.argtypes = [C.c_char_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]
+    L.visrt_cache_load.argtypes = [C.c_char_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_int64,
+                                   C.POINTER(C.c_int64)]
     L.visrt_trace_snapshot_edges.restype = C.c_int64
     L.visrt_trace_snapshot_edges.argtypes = [C.c_void_p, C.c_void_p]
     L.visrt_tracer_set_edges.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]

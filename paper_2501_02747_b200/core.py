@@ -421,6 +421,30 @@ def resolve_keys(scene: Scene, tx, rx, keys: Sequence[Sequence[Tuple[Sequence[in
     return out, _stats_dict(st)
 
 
+def save_matrix_cache(scene: Scene, path: str, admitted_bits: np.ndarray, triples: Optional[np.ndarray] = None,
+                      max_order: int = 2) -> None:
+    """Binary matrix / pair-graph cache (replaces the text save_matrix,
+    src/vismatrix.cpp:849-894): admitted bits + feasible order-2 triples."""
+    bits = np.ascontiguousarray(admitted_bits, np.uint64)
+    tri = np.ascontiguousarray(np.zeros((0, 3), np.int32) if triples is None else triples, np.int32).reshape(-1, 3)
+    check(lib().visrt_cache_save(path.encode(), scene.h, max_order, bits.ctypes.data, len(tri),
+                                 tri.ctypes.data if len(tri) else None))
+
+
+def load_matrix_cache(scene: Scene, path: str):
+    """-> (admitted bits [N, words] uint64, triples [T, 3] int32, max_order);
+    SceneError if the cache was built for another scene."""
+    mo = C.c_int32()
+    nt = C.c_int64()
+    L = lib()
+    check(L.visrt_cache_load(path.encode(), scene.h, C.byref(mo), None, None, 0, C.byref(nt)))
+    bits = np.zeros((scene.n, scene.words), np.uint64)
+    tri = np.zeros((max(nt.value, 1), 3), np.int32)
+    check(L.visrt_cache_load(path.encode(), scene.h, C.byref(mo), bits.ctypes.data, tri.ctypes.data, nt.value,
+                             C.byref(nt)))
+    return bits, tri[: nt.value], mo.value
+
+
 def brute_force_trace(scene: Scene, tx, rx, max_refl: int, allow_diffraction: bool = False,
                       edges: Optional[Sequence[dict]] = None):
     """rt::brute_force_trace (include/rt/raytracer.hpp:78-83): the conventional

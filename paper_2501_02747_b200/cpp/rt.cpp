@@ -471,12 +471,16 @@ OcclusionVerdict occlusion_judgment(const Face& ref, const Face& aim, const Scen
     return v;
 }
 
+namespace {
+// The host half of build_matrix: InterVisEntry records for the admitted pairs
+// (pair order) and the Markov-2 chain growth over the feasible triples.
+InterVisMatrix materialize(const Scene& scene, int max_order, const std::vector<int32_t>& ai,
+                           const std::vector<int32_t>& aj, const std::vector<int32_t>& tri);
+}  // namespace
+
 InterVisMatrix build_matrix(const Scene& scene, int max_order) {
     if (max_order < 1 || max_order > 4) throw VisibilityError("max reflection order must be between 1 and 4");
     visrt_scene* dev = scene.device_scene();
-    const int n = static_cast<int>(scene.faces().size());
-    InterVisMatrix matrix;
-    matrix.set_max_order(max_order);
     visrt_stats st{};
     check(visrt_pair_visibility(dev, VISRT_PAIRS_PREFILTERED, nullptr, &st, nullptr));
     const int64_t m = visrt_candidates(dev, nullptr, nullptr, nullptr);
@@ -489,6 +493,69 @@ InterVisMatrix build_matrix(const Scene& scene, int max_order) {
             ai.push_back(ci[k]);
             aj.push_back(cj[k]);
         }
+    std::vector<int32_t> tri;
+    if (max_order >= 2) {
+        int64_t nt = 0;
+        check(visrt_chain_triples(dev, nullptr, nullptr, 0, &nt, &st, nullptr));
+        tri.resize(static_cast<size_t>(nt) * 3 + 3);
+        check(visrt_chain_triples(dev, nullptr, tri.data(), nt, &nt, &st, nullptr));
+        tri.resize(static_cast<size_t>(nt) * 3);
+    }
+    return materialize(scene, max_order, ai, aj, tri);
+}
+
+void save_matrix_cache(const InterVisMatrix& matrix, const Scene& scene, const std::string& path) {
+    const size_t n = scene.faces().size(), words = (n + 63) / 64;
+    std::vector<uint64_t> bits(n * words + 1, 0);
+    std::vector<int32_t> tri;
+    for (const InterVisEntry& e : matrix.entries()) {
+        const auto& c = e.relation.chain;
+        if (e.order == 1 && c.size() == 2) {
+            const size_t r = static_cast<size_t>(scene.face(c[0]).index), a = static_cast<size_t>(scene.face(c[1]).index);
+            bits[r * words + a / 64] |= 1ull << (a % 64);
+        } else if (e.order == 2 && c.size() == 3) {
+            for (const auto& id : c) tri.push_back(scene.face(id).index);
+        }
+    }
+    // one copy per triple (an order-2 chain has one entry per shared plane at most)
+    std::vector<std::array<int32_t, 3>> t3;
+    for (size_t k = 0; k + 2 < tri.size(); k += 3) t3.push_back({tri[k], tri[k + 1], tri[k + 2]});
+    std::sort(t3.begin(), t3.end());
+    t3.erase(std::unique(t3.begin(), t3.end()), t3.end());
+    std::vector<int32_t> flat;
+    for (const auto& t : t3) flat.insert(flat.end(), t.begin(), t.end());
+    check(visrt_cache_save(path.c_str(), scene.device_scene(), matrix.max_order(), bits.data(),
+                           static_cast<int64_t>(t3.size()), flat.empty() ? nullptr : flat.data()));
+}
+
+InterVisMatrix load_matrix_cache(const Scene& scene, const std::string& path) {
+    visrt_scene* dev = scene.device_scene();
+    int32_t mo = 1;
+    int64_t nt = 0;
+    check(visrt_cache_load(path.c_str(), dev, &mo, nullptr, nullptr, 0, &nt));
+    const size_t n = scene.faces().size(), words = (n + 63) / 64;
+    std::vector<uint64_t> bits(n * words + 1);
+    std::vector<int32_t> tri(static_cast<size_t>(nt) * 3 + 3);
+    check(visrt_cache_load(path.c_str(), dev, &mo, bits.data(), tri.data(), nt, &nt));
+    tri.resize(static_cast<size_t>(nt) * 3);
+    std::vector<int32_t> ai, aj;
+    for (size_t i = 0; i < n; ++i)
+        for (size_t j = i + 1; j < n; ++j)
+            if ((bits[i * words + j / 64] >> (j % 64)) & 1ull) {
+                ai.push_back(static_cast<int32_t>(i));
+                aj.push_back(static_cast<int32_t>(j));
+            }
+    return materialize(scene, mo, ai, aj, tri);
+}
+
+namespace {
+InterVisMatrix materialize(const Scene& scene, int max_order, const std::vector<int32_t>& ai,
+                           const std::vector<int32_t>& aj, const std::vector<int32_t>& tri) {
+    visrt_scene* dev = scene.device_scene();
+    const int n = static_cast<int>(scene.faces().size());
+    InterVisMatrix matrix;
+    matrix.set_max_order(max_order);
+    visrt_stats st{};
     // verdict kinds + blockers of the admitted pairs (Partial pairs record them)
     std::vector<int8_t> kind(ai.size());
     std::vector<int64_t> boff(ai.size() + 1);
@@ -524,10 +591,7 @@ InterVisMatrix build_matrix(const Scene& scene, int max_order) {
     if (max_order < 2) return matrix;
     // chains: the GPU decides every feasible triple; the frontier growth and
     // the record fields follow src/vismatrix.cpp:682-797
-    int64_t nt = 0;
-    check(visrt_chain_triples(dev, nullptr, nullptr, 0, &nt, &st, nullptr));
-    std::vector<int32_t> tri(static_cast<size_t>(nt) * 3 + 3);
-    check(visrt_chain_triples(dev, nullptr, tri.data(), nt, &nt, &st, nullptr));
+    const int64_t nt = static_cast<int64_t>(tri.size() / 3);
     std::unordered_set<uint64_t> feasible;
     auto key3 = [n](int a, int b, int c) {
         return (static_cast<uint64_t>(a) * n + static_cast<uint64_t>(b)) * n + static_cast<uint64_t>(c);
@@ -590,6 +654,7 @@ InterVisMatrix build_matrix(const Scene& scene, int max_order) {
     }
     return matrix;
 }
+}  // namespace
 
 // ---------------------------------------------------------------------------
 namespace {

@@ -184,6 +184,11 @@ class InterVisMatrix {
 
 OcclusionVerdict occlusion_judgment(const Face& ref, const Face& aim, const Scene& scene);
 InterVisMatrix build_matrix(const Scene& scene, int max_order);
+/// Binary matrix / pair-graph cache (replaces the text save_matrix /
+/// load_matrix of include/rt/vismatrix.hpp:143-144): admitted pairs + order-2
+/// chains; load re-derives every entry exactly as build_matrix does.
+void save_matrix_cache(const InterVisMatrix& matrix, const Scene& scene, const std::string& path);
+InterVisMatrix load_matrix_cache(const Scene& scene, const std::string& path);
 
 // ---------------------------------------------------------------------------
 struct PlaneIllumination {

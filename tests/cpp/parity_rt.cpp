@@ -155,6 +155,25 @@ int main(int argc, char** argv) {
     }
     std::cout << "build_matrix(" << max_order << "): " << ne << " entries compared" << std::endl;
 
+    // --- binary matrix cache round trip: every entry re-derived identically ---
+    {
+        const std::string cpath = std::string(argv[1]) + ".cache";
+        rt::save_matrix_cache(M, *mine, cpath);
+        const rt::InterVisMatrix MC = rt::load_matrix_cache(*mine, cpath);
+        EXPECT(MC.max_order() == M.max_order() && MC.entries().size() == M.entries().size(), "cache entry count");
+        for (size_t k = 0; k < M.entries().size() && k < MC.entries().size(); ++k) {
+            const rt::InterVisEntry& x = M.entries()[k];
+            const rt::InterVisEntry& y = MC.entries()[k];
+            EXPECT(x.order == y.order && x.relation.chain == y.relation.chain && x.relation.plane == y.relation.plane &&
+                       x.relation.kind == y.relation.kind && x.verdict == y.verdict && x.blockers == y.blockers &&
+                       x.subranges == y.subranges && x.ranges.at_a.low == y.ranges.at_a.low &&
+                       x.ranges.at_b.high == y.ranges.at_b.high && x.aim_image.size() == y.aim_image.size() &&
+                       x.criterion.has_value() == y.criterion.has_value(),
+                   "cache entry " << k);
+        }
+        std::cout << "matrix cache: " << MC.entries().size() << " entries re-derived" << std::endl;
+    }
+
     // --- occlusion_judgment (every 5th pair) -------------------------------
     int npj = 0;
     for (int i = 0; i < n; ++i)

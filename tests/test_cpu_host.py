@@ -122,3 +122,35 @@ def test_generated_normals_point_outward(oracle_built):
         idx = [k for k, x in enumerate(s.ids) if x.split("_")[0] == b]
         centre = np.concatenate([s.face_points(k) for k in idx]).mean(axis=0)
         assert np.dot(nrm, pts.mean(axis=0) - centre) > 0
+
+
+def test_matrix_cache_roundtrip_cpu(tmp_path):
+    """Binary matrix / pair-graph cache, host-only:
+    the reference's admitted pairs + order-2 chains of config 1 round-trip
+    exactly; another scene is refused (SceneError); a corrupt file is a
+    VisibilityError."""
+    from paper_2501_02747_b200.core import load_matrix_cache, save_matrix_cache
+    d = G.load("config1")
+    s = G.soup(d)
+    n = s.nfaces
+    words = (n + 63) // 64
+    bits = np.zeros((n, words), np.uint64)
+    for e in d["matrix1"]:
+        i, j = e["ref"], e["aim"]
+        bits[i, j // 64] |= np.uint64(1) << np.uint64(j % 64)
+    tri = np.array(d["triples"], np.int32)
+    path = str(tmp_path / "m.bin")
+    with Scene(s, device=-1) as sc:
+        save_matrix_cache(sc, path, bits, tri, max_order=2)
+        b2, t2, mo = load_matrix_cache(sc, path)
+    assert mo == 2 and np.array_equal(b2, bits) and np.array_equal(t2, tri)
+    other = G.soup(G.load("street_canyon"))
+    with Scene(other, device=-1) as sc2:
+        with pytest.raises(_capi.SceneError, match="different scene"):
+            load_matrix_cache(sc2, path)
+    raw = bytearray(open(path, "rb").read())
+    raw[100] ^= 0xFF
+    open(path, "wb").write(bytes(raw))
+    with Scene(s, device=-1) as sc:
+        with pytest.raises(_capi.VisibilityError, match="corrupt"):
+            load_matrix_cache(sc, path)
