@@ -253,6 +253,12 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_ROT
 #define VISRT_K2W_ROT 1     // candidate tiles of the home chunk start at the pair's own tile
 #endif
+#ifndef VISRT_K2W_MULTI
+#define VISRT_K2W_MULTI 2     // extra blockers of the swept sightline used to settle its siblings (1 or 2)
+#endif
+#ifndef VISRT_K2W_MORTON
+#define VISRT_K2W_MORTON 0
+#endif
 constexpr int kWC = VISRT_K2W_WC;
 
 template <int MAXV, bool RESIDENT, int MINB>
@@ -282,6 +288,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             pj = a.cj[p];
         } else {
             pair_from_index(p, n, pi, pj);
+#if VISRT_K2W_MORTON
+            // walk the pair space in Morton order (spatially coherent pairs keep
+            // the warp blocker cache warm); the verdict keeps the reference's
+            // lower-index orientation
+            {
+                const int oi = s.perm[pi], oj = s.perm[pj];
+                pi = oi < oj ? oi : oj;
+                pj = oi < oj ? oj : oi;
+            }
+#endif
         }
         const int si = s.inv[pi], sj = s.inv[pj];
         const int nr = s.nv[pi], na = s.nv[pj];
@@ -352,6 +368,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             const SegF g = make_segf(s, ax, ay, az, bx, by, bz);
             ++sweeps;
             int hit = -1;
+#if VISRT_K2W_MULTI
+            int hit2 = -1, hit3 = -1;
+#endif
             const int home = home_chunk(s, pi);
             for (int cc = 0; cc < ctx.nchunks && hit < 0; ++cc) {
                 const int c = home + cc < ctx.nchunks ? home + cc : home + cc - ctx.nchunks;
@@ -393,7 +412,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                         const int idx = r + lane < tot ? sv[r + lane] : -1;
                         const bool h = idx >= 0 && exact(base + idx);
                         const unsigned hb = __ballot_sync(kFull, h);
-                        if (hb) hit = __shfl_sync(kFull, base + idx, __ffs(hb) - 1);
+                        if (hb) {
+                            hit = __shfl_sync(kFull, base + idx, __ffs(hb) - 1);
+#if VISRT_K2W_MULTI
+                            // the round's other blockers of this sightline are likely
+                            // blockers of its siblings too: settle with them as well
+                            const unsigned rest = hb & (hb - 1);
+                            hit2 = rest ? __shfl_sync(kFull, base + idx, __ffs(rest) - 1) : -1;
+                            const unsigned rest2 = rest & (rest - 1);
+                            hit3 = (VISRT_K2W_MULTI > 1 && rest2) ? __shfl_sync(kFull, base + idx, __ffs(rest2) - 1) : -1;
+#endif
+                        }
                     }
                     __syncwarp();
                 }
@@ -405,6 +434,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             if (lane == wc_next) wc = hit;
             wc_next = wc_next + 1 == kWC ? 0 : wc_next + 1;
             resolve(hit);
+#if VISRT_K2W_MULTI
+            if (hit2 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit2);
+            if (hit3 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit3);
+#endif
         }
         if (lane == 0) {
             if (clear) set_pair_bit(a.bits, s.words, pi, pj);
