@@ -225,11 +225,12 @@ int visrt_tracer_create(visrt_scene* scene, int max_refl, const uint64_t* admitt
                         int64_t ntriples, const int32_t* triples, visrt_tracer** out);
 void visrt_tracer_destroy(visrt_tracer* tracer);
 typedef struct {
-    int32_t nrefl;
-    int32_t faces[3];      /* reflecting faces, source side first            */
+    int32_t nrefl;         /* 0..4 */
+    int32_t faces[4];      /* reflecting faces, source side first            */
     int32_t edge;          /* diffraction edge index (last interaction), -1 none */
     int32_t snap;
-    double points[18];     /* tx, reflection points..., [diffraction point], rx */
+    int32_t pad;
+    double points[21];     /* tx, reflection points..., [diffraction point], rx */
     double length;
 } visrt_path;
 typedef struct {
@@ -256,8 +257,8 @@ int visrt_trace(visrt_tracer* tracer, int64_t nsnap, const double* tx, const dou
 /* One fixed interaction sequence (SequenceKey, src/raytracer.cpp:528-552):
  * reflecting faces (source side first) + optional final diffraction edge. */
 typedef struct {
-    int32_t nrefl;         /* 0..3 */
-    int32_t faces[3];
+    int32_t nrefl;         /* 0..4 */
+    int32_t faces[4];
     int32_t edge;          /* -1: the path ends at the receiver */
 } visrt_seqkey;
 /* resolve_keys (src/raytracer.cpp:554-570), the dynamic-run re-solve: for

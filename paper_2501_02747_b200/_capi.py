@@ -60,12 +60,12 @@ class visrt_names(C.Structure):
 
 
 class visrt_path(C.Structure):
-    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 3), ("edge", C.c_int32), ("snap", C.c_int32),
-                ("points", C.c_double * 18), ("length", C.c_double)]
+    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("edge", C.c_int32), ("snap", C.c_int32),
+                ("pad", C.c_int32), ("points", C.c_double * 21), ("length", C.c_double)]
 
 
 class visrt_seqkey(C.Structure):
-    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 3), ("edge", C.c_int32)]
+    _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("edge", C.c_int32)]
 
 
 class visrt_trace_stats(C.Structure):

@@ -37,14 +37,14 @@
 namespace visrt {
 
 struct TreeNode {
-    int32_t snap, depth, f0, f1, f2, rank, filtered, pad;
+    int32_t snap, depth, f0, f1, f2, f3, rank, filtered;   // rank: continuation row of the last pair
     double ix, iy, iz;
 };
 
 struct Cand {
-    int32_t snap, depth, f[3], edge;   // edge: diffraction edge index (-1: ends at the receiver)
-    int32_t node, pad;                 // keyed mode: index of the source node (result slot)
-    double pts[18];                    // tx, reflections..., [diffraction point], rx
+    int32_t snap, depth, f[4], edge;   // edge: diffraction edge index (-1: ends at the receiver)
+    int32_t node;                      // keyed mode: index of the source node (result slot)
+    double pts[21];                    // tx, reflections..., [diffraction point], rx
     double length;
 };
 
@@ -127,7 +127,7 @@ __device__ __forceinline__ TreeNode tree_parent(const TreeArgs& a, long long p) 
     TreeNode par{};
     par.snap = a.snap0 + static_cast<int>(p);
     par.depth = 0;
-    par.f0 = par.f1 = par.f2 = -1;
+    par.f0 = par.f1 = par.f2 = par.f3 = -1;
     par.rank = -1;
     par.filtered = a.brute ? 0 : 1;
     par.ix = a.tx[3 * static_cast<size_t>(par.snap)];
@@ -139,7 +139,7 @@ __device__ __forceinline__ TreeNode tree_parent(const TreeArgs& a, long long p) 
 __device__ __forceinline__ Pool tree_pool(const TreeArgs& a, const TreeNode& par, int n) {
     Pool q;
     q.d = par.depth;
-    q.last = q.d == 0 ? -1 : (q.d == 1 ? par.f0 : (q.d == 2 ? par.f1 : par.f2));
+    q.last = q.d == 0 ? -1 : (q.d == 1 ? par.f0 : (q.d == 2 ? par.f1 : (q.d == 3 ? par.f2 : par.f3)));
     q.list = nullptr;
     q.lo = 0;
     q.hi = n;
@@ -149,7 +149,9 @@ __device__ __forceinline__ Pool tree_pool(const TreeArgs& a, const TreeNode& par
             q.lo = a.off1[par.f0];
             q.hi = a.off1[par.f0 + 1];
             q.list = a.idx1;
-        } else if (q.d == 2 && par.rank >= 0) {
+        } else if ((q.d == 2 || q.d == 3) && par.rank >= 0) {
+            // Markov-2 chains: the continuations of (..., p, t) are those of the
+            // pair (p, t) (build_matrix growth, src/vismatrix.cpp:760-797)
             q.lo = a.off2[par.rank];
             q.hi = a.off2[par.rank + 1];
             q.list = a.idx2;
@@ -243,9 +245,22 @@ __global__ void __launch_bounds__(256) k_tree_expand(TreeArgs a, const unsigned 
                 ch.f0 = P.d == 0 ? c : par.f0;
                 ch.f1 = P.d == 1 ? c : par.f1;
                 ch.f2 = P.d == 2 ? c : par.f2;
-                ch.rank = P.d == 1 ? rank : -1;
+                ch.f3 = P.d == 3 ? c : par.f3;
+                if (P.d == 1) {
+                    ch.rank = rank;
+                } else if (P.d == 2 && a.max_refl > 3) {
+                    // rank of the admitted pair (f1, c): its row in idx1
+                    int lo = a.off1[par.f1], hi = a.off1[par.f1 + 1];
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (a.idx1[mid] < c) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    ch.rank = (lo < a.off1[par.f1 + 1] && a.idx1[lo] == c) ? lo : -1;
+                } else {
+                    ch.rank = -1;
+                }
                 ch.filtered = par.filtered && s.orient[c] != 2;
-                ch.pad = 0;
                 ch.ix = par.ix;
                 ch.iy = par.iy;
                 ch.iz = par.iz;
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < nt; t += stride) {
         int snap, d;
-        int f[3] = {-1, -1, -1};
+        int f[4] = {-1, -1, -1, -1};
         if (a.in) {
             const TreeNode& nd = a.in[t];
             snap = nd.snap;
@@ -310,13 +325,14 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             f[0] = nd.f0;
             f[1] = nd.f1;
             f[2] = nd.f2;
+            f[3] = nd.f3;
         } else {
             snap = a.snap0 + static_cast<int>(t);
             d = 0;
         }
         const double* T = a.tx + 3 * static_cast<size_t>(snap);
         const double* Rx = a.rx_fixed ? a.rx : a.rx + 3 * static_cast<size_t>(snap);
-        double img[4][3];
+        double img[5][3];
         img[0][0] = T[0];
         img[0][1] = T[1];
         img[0][2] = T[2];
@@ -345,7 +361,7 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
                 target[1] = p[1];
                 target[2] = p[2];
             }
-            double refl[3][3];
+            double refl[4][3];
             double cx = target[0], cy = target[1], cz = target[2];
             for (int k = d - 1; k >= 0 && ok; --k) {
                 const double da = sdist_face(s, f[k], cx, cy, cz);
@@ -376,9 +392,9 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             c.f[0] = f[0];
             c.f[1] = f[1];
             c.f[2] = f[2];
+            c.f[3] = f[3];
             c.edge = v ? edge : -1;
             c.node = static_cast<int32_t>(t);
-            c.pad = 0;
             c.pts[0] = T[0];
             c.pts[1] = T[1];
             c.pts[2] = T[2];
@@ -439,10 +455,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_tree_legs(TreeArgs a) {
             p.faces[0] = c.f[0];
             p.faces[1] = c.f[1];
             p.faces[2] = c.f[2];
+            p.faces[3] = c.f[3];
             p.edge = c.edge;
             p.snap = c.snap;
+            p.pad = 0;
             const int npts = c.depth + 2 + (c.edge >= 0 ? 1 : 0);
-            for (int i = 0; i < 18; ++i) p.points[i] = i < 3 * npts ? c.pts[i] : 0.0;
+            for (int i = 0; i < 21; ++i) p.points[i] = i < 3 * npts ? c.pts[i] : 0.0;
             p.length = c.length;
             if (a.keyed) {
                 a.slot_paths[slot] = p;
@@ -606,9 +624,8 @@ extern "C" int visrt_tracer_create(visrt_scene* sc, int max_refl, const uint64_t
         if (!out) throw visrt::UsageError("null out");
         *out = nullptr;
         if (max_refl < 0) throw visrt::VisError("reflection order must be non-negative");
-        if (max_refl > 3)
-            throw visrt::UsageError("max_refl > 3 needs order-3 chains, which this build does not represent");
-        if (max_refl == 3 && !triples && ntriples > 0) throw visrt::UsageError("triples required");
+        if (max_refl > 4) throw visrt::VisError("max reflection order must be between 1 and 4");
+        if (max_refl >= 3 && !triples && ntriples > 0) throw visrt::UsageError("triples required");
         const visrt::HostScene& hs = visrt::scene_host(sc);
         const int n = hs.n;
         const int words = (n + 63) / 64;
@@ -969,7 +986,7 @@ extern "C" int visrt_resolve_keys(visrt_scene* sc, int64_t nsamp, const double* 
         for (int64_t k = 0; k < nsamp; ++k) {
             for (int64_t q = key_off[k]; q < key_off[k + 1]; ++q) {
                 const visrt_seqkey& K = keys[q];
-                if (K.nrefl < 0 || K.nrefl > 3) throw visrt::UsageError("keys hold 0..3 reflections");
+                if (K.nrefl < 0 || K.nrefl > 4) throw visrt::UsageError("keys hold 0..4 reflections");
                 for (int i = 0; i < K.nrefl; ++i)
                     if (K.faces[i] < 0 || K.faces[i] >= ds.n) throw visrt::UsageError("bad face index");
                 if (K.edge < -1 || K.edge >= nedges) throw visrt::UsageError("bad edge index");
@@ -980,6 +997,7 @@ extern "C" int visrt_resolve_keys(visrt_scene* sc, int64_t nsamp, const double* 
                 nd.f0 = K.nrefl > 0 ? K.faces[0] : -1;
                 nd.f1 = K.nrefl > 1 ? K.faces[1] : -1;
                 nd.f2 = K.nrefl > 2 ? K.faces[2] : -1;
+                nd.f3 = K.nrefl > 3 ? K.faces[3] : -1;
                 nd.rank = K.edge;
             }
         }

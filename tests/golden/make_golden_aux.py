@@ -93,6 +93,42 @@ def main() -> None:
                                                     "length": float(p["length"]).hex()} for p in paths],
                                                   key=lambda p: p["identity"])})
     print("brute traces", len(brute))
+    # TraceAccelerator(max_refl = 4): the order-3 chains of build_matrix(scene, 3)
+    # restrict depth-4 continuations (proj/src/raytracer.cpp:319-340)
+    order4 = []
+    o4jobs = [("two_buildings", djobs["two_buildings"][:2]), ("street_canyon", djobs["street_canyon"][:2]),
+              ("screened_wall", djobs["screened_wall"][:2])]
+    for name, trs in o4jobs:
+        r = bindings.RefOracle(path=os.path.join(FIXTURES, name + ".json"))
+        m = r.build_matrix(3)
+        r.lib().vref_matrix_set_max_order(m, 4)
+        acc = r.accel(m, 4)
+        for tx, rx in trs:
+            for dif in (False, True):
+                try:
+                    paths, st = r.trace(acc, np.asarray(tx, np.float64), np.asarray(rx, np.float64), diffraction=dif)
+                except RuntimeError:
+                    continue
+                order4.append({"scene": name, "tx": list(tx), "rx": list(rx), "diffraction": dif, "nodes": int(st[0]),
+                               "sequences": int(st[1]),
+                               "paths": sorted([{"identity": p["identity"], "points": [float(x).hex() for x in p["points"]],
+                                                 "length": float(p["length"]).hex()} for p in paths],
+                                               key=lambda p: p["identity"])})
+        r.lib().vref_accel_free(acc)
+    wl = scenes.workload(1)
+    r = bindings.RefOracle(wl.scene)
+    m = r.build_matrix(3)
+    r.lib().vref_matrix_set_max_order(m, 4)
+    acc = r.accel(m, 4)
+    for k in (0, 50):
+        paths, st = r.trace(acc, wl.tx[k], wl.rx[0])
+        order4.append({"scene": "config1", "tx": wl.tx[k].tolist(), "rx": wl.rx[0].tolist(), "diffraction": False,
+                       "nodes": int(st[0]), "sequences": int(st[1]),
+                       "paths": sorted([{"identity": p["identity"], "points": [float(x).hex() for x in p["points"]],
+                                         "length": float(p["length"]).hex()} for p in paths],
+                                       key=lambda p: p["identity"])})
+    r.lib().vref_accel_free(acc)
+    print("order-4 traces", len(order4), [t["nodes"] for t in order4])
     # dynamic_trace against a fixed receiver (proj/src/raytracer.cpp:590-643): the
     # non-retraced samples are resolve_keys of their segment's first trace
     dyn = []
@@ -117,7 +153,7 @@ def main() -> None:
             print(name, "dynamic", dif, len(smp), "samples")
     with open(os.path.join(HERE, "aux.json"), "w") as fh:
         json.dump({"image_trees": trees, "closest_edges": edges, "diffraction_traces": diff, "brute_traces": brute,
-                   "dynamic": dyn},
+                   "dynamic": dyn, "order4_traces": order4},
                   fh, separators=(",", ":"))
 
 

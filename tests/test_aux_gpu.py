@@ -171,3 +171,30 @@ def test_resolve_keys_vs_reference_dynamic_trace(k):
                       "points": [float(x).hex() for x in p["points"]], "length": float(p["length"]).hex()} for p in g],
                     key=lambda p: p["identity"])
         assert gp == e
+
+
+O4 = AUX["order4_traces"]
+
+
+@pytest.mark.parametrize("k", range(len(O4)), ids=[f"{t['scene']}-d{int(t['diffraction'])}-{i}" for i, t in enumerate(O4)])
+def test_trace_order4_vs_reference(k):
+    """TraceAccelerator(max_refl = 4) (proj/include/rt/raytracer.hpp:96-118):
+    depth-4 continuations follow the order-3 chains (Markov-2 growth of the
+    order-2 triples); path sets and counters equal the reference's."""
+    from paper_2501_02747_b200.core import Tracer, chain_triples, path_identity
+    t = O4[k]
+    if t["scene"] == "config1":
+        s, edges = scenes.workload(1).scene, []
+    else:
+        d = G.load(t["scene"])
+        s, edges = G.soup(d), d["edges"]
+    with Scene(s) as sc:
+        bits, _ = sc.pair_visibility("prefiltered")
+        tri, _ = chain_triples(sc, bits)
+        tr = Tracer(sc, 4, admitted_bits=bits, triples=tri, edges=edges)
+        paths, nodes, st = tr.trace([t["tx"]], [t["rx"]], allow_diffraction=t["diffraction"])
+    got = sorted([{"identity": path_identity(s.ids, p["faces"], edges[p["edge"]]["id"] if p["edge"] >= 0 else None),
+                   "points": [float(x).hex() for x in p["points"]], "length": float(p["length"]).hex()}
+                  for p in paths[0]], key=lambda p: p["identity"])
+    assert got == t["paths"]
+    assert int(nodes[0]) == t["nodes"] and st["sequences"] == t["sequences"]
