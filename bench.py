@@ -215,7 +215,7 @@ def secondary_measurements(stream: int):
         ent["chain"][: len(ai), 0] = ai
         ent["chain"][: len(ai), 1] = aj
         ent["order"][len(ai):] = 2
-        ent["chain"][len(ai):] = tri
+        ent["chain"][len(ai):, :3] = tri
         wps = np.array([wl1.tx[0], wl1.tx[-1]])
         for order in (1, 2):
             sel = ent[ent["order"] <= order]

@@ -125,7 +125,7 @@ int visrt_point_regions(visrt_scene* scene, int64_t nsrc, const double* src_xyz,
                         visrt_region* out, visrt_stats* stats, void* stream);
 
 /* (2) Per-snapshot point tables (point_vis_table rows, src/vistable.cpp:478-521)
- * for a list of matrix entries of order 1 or 2: entry e = (order, chain[0..2],
+ * for a list of matrix entries of order 1..4: entry e = (order, chain[0..2],
  * plane) with chain = reflectors..., aim. For every (source k, entry e) the
  * kernels decide whether TableBuilder::reach(reflectors) succeeds (the row
  * exists) and whether the beam is Full in the entry's plane, from the GPU
@@ -134,8 +134,8 @@ int visrt_point_regions(visrt_scene* scene, int64_t nsrc, const double* src_xyz,
  * [nsrc][ceil(nent/32)] uint32 (bit e of source k). regions_out (optional):
  * the regions as visrt_point_regions would return them. */
 typedef struct {
-    int32_t order;        /* 1 or 2 */
-    int32_t chain[3];     /* reflectors..., aim (order 1: chain[0], chain[1]) */
+    int32_t order;        /* 1..4 */
+    int32_t chain[5];     /* reflectors chain[0..order-1], aim chain[order] */
     int32_t plane;        /* the entry's working plane (PlaneTag) */
 } visrt_entry;
 int visrt_point_tables(visrt_scene* scene, int64_t nsrc, const double* src_xyz, int64_t nent,
@@ -150,7 +150,7 @@ int visrt_segments_clear(visrt_scene* scene, int64_t nseg, const double* a_xyz, 
 
 /* TableBuilder::reach for a query list (src/vistable.cpp:404-430, 432-467):
  * query q = (source src_xyz[q], reflector chain chains[q].chain[0..order-1],
- * order 1 or 2; chain[order] and plane name an entry whose plane decides
+ * order 1..4; chain[order] and plane name an entry whose plane decides
  * full[q]). reach[q] = the beam reaches the last reflector (the row /
  * MobileSampler::member test); full[q] (may be NULL) = Full in that plane. */
 int visrt_chain_reach(visrt_scene* scene, int64_t nq, const double* src_xyz, const visrt_entry* chains,
@@ -159,7 +159,7 @@ int visrt_chain_reach(visrt_scene* scene, int64_t nq, const double* src_xyz, con
 /* (2) Trajectory visibility table: trajectory_vis_table(traj, matrix, scene,
  * max_order) (include/rt/vistable.hpp:143-148, src/vistable.cpp:822-960) with
  * MobileSampler (681-812). Inputs: the route waypoints, the matrix entries
- * (order <= max_order used; max_order 1 or 2) in matrix order, and the string
+ * (order <= max_order used; max_order 1..4) in matrix order, and the string
  * orders the reference sorts by, as integer ranks (any order-consistent
  * integers; equal strings must get equal ranks):
  *   key_rank[9n+1]   : face id of f at [f], corner node "<id>#k" at [n + 8f + k],

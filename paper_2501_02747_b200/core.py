@@ -140,7 +140,7 @@ def point_regions(scene: Scene, src: np.ndarray) -> List[List[dict]]:
              for r in row] for row in arr]
 
 
-ENTRY_DTYPE = np.dtype([("order", np.int32), ("chain", np.int32, 3), ("plane", np.int32)])
+ENTRY_DTYPE = np.dtype([("order", np.int32), ("chain", np.int32, 5), ("plane", np.int32)])
 
 
 def point_tables(scene: Scene, src: np.ndarray, entries: np.ndarray, want_regions: bool = False):

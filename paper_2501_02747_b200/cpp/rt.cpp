@@ -871,7 +871,7 @@ visrt_entry to_entry(const Scene& scene, const InterVisEntry& e) {
     visrt_entry v{};
     v.order = e.order;
     const auto& c = e.relation.chain;
-    for (size_t k = 0; k < c.size() && k < 3; ++k) v.chain[k] = scene.face(c[k]).index;
+    for (size_t k = 0; k < c.size() && k < 5; ++k) v.chain[k] = scene.face(c[k]).index;
     v.plane = static_cast<int32_t>(e.relation.plane);
     return v;
 }
@@ -880,7 +880,7 @@ void check_table_order(const InterVisMatrix& matrix, int max_order) {
     if (matrix.max_order() < max_order)
         throw VisibilityError("matrix holds orders up to " + std::to_string(matrix.max_order()) + ", requested " +
                               std::to_string(max_order));
-    if (max_order > 2) throw std::invalid_argument("GPU tables cover orders 1 and 2");
+
 }
 }  // namespace
 
@@ -959,7 +959,7 @@ std::vector<MobileVisEntry> trajectory_vis_table(const Trajectory& traj, const I
     if (matrix.max_order() < max_order)
         throw VisibilityError("matrix holds orders up to " + std::to_string(matrix.max_order()) + ", requested " +
                               std::to_string(max_order));
-    if (max_order > 2) throw std::invalid_argument("GPU trajectory tables cover orders 1 and 2");
+
     const int n = static_cast<int>(scene.faces().size());
     std::vector<std::string> keys{"transmitter"}, parents{"transmitter"}, blds;
     auto corner = [&](int f, int k) { return scene.face(f).id + "#" + std::to_string(k); };

@@ -661,56 +661,89 @@ __global__ void __launch_bounds__(256) k_beam_rows(BeamArgs a) {
         const visrt_region& R = a.regions[ri];
         bool row = false, full = false;
         if (R.present == 1) {
-            if (E.order == 1) {
-                row = true;   // reach({head}) = region(head)
-                full = R.has[E.plane] && !R.clipped[E.plane];
-            } else {
-                // step(reach({head}), head, mid), src/vistable.cpp:432-467
-                const int mid = E.chain[1];
+            // BeamState after the head (src/vistable.cpp:409-421): per plane the
+            // region's window and Full flag; image = source mirrored by the head
+            double wx0[3], wy0[3], wx1[3], wy1[3];
+            bool hw[3], fl[3];
+            for (int pl = 0; pl < 3; ++pl) {
+                hw[pl] = R.has[pl] != 0;
+                fl[pl] = hw[pl] && !R.clipped[pl];
+                wx0[pl] = wy0[pl] = wx1[pl] = wy1[pl] = 0.0;
+                if (hw[pl]) {
+                    const double* fs = s.seg + (static_cast<size_t>(head) * 3 + pl) * 6;
+                    const double dx = dsub(fs[2], fs[0]), dy = dsub(fs[3], fs[1]);
+                    wx0[pl] = dadd(fs[0], dmul(dx, R.sub[2 * pl]));
+                    wy0[pl] = dadd(fs[1], dmul(dy, R.sub[2 * pl]));
+                    wx1[pl] = dadd(fs[0], dmul(dx, R.sub[2 * pl + 1]));
+                    wy1[pl] = dadd(fs[1], dmul(dy, R.sub[2 * pl + 1]));
+                }
+            }
+            double ix, iy, iz;
+            {
                 const double* P = s.pts + static_cast<size_t>(head) * VISRT_MAX_VERTS * 3;
                 const double* N = s.normal + 3 * static_cast<size_t>(head);
                 const double sx = a.src[3 * k], sy = a.src[3 * k + 1], sz = a.src[3 * k + 2];
                 const double d2 = dmul(2.0, dot_rel(sx, sy, sz, P[0], P[1], P[2], N[0], N[1], N[2]));
-                const double ix = dsub(sx, dmul(N[0], d2)), iy = dsub(sy, dmul(N[1], d2)),
-                             iz = dsub(sz, dmul(N[2], d2));   // mirror_point
-                bool any = false, ok = true, full_pl = false, has_pl = false;
-                for (int pl = 0; pl < 3 && ok; ++pl) {
-                    if (!s.seg_ok[3 * head + pl] || !s.seg_ok[3 * mid + pl]) continue;
-                    const double* fs = s.seg + (static_cast<size_t>(head) * 3 + pl) * 6;
-                    const double* gs = s.seg + (static_cast<size_t>(mid) * 3 + pl) * 6;
+                ix = dsub(sx, dmul(N[0], d2));   // mirror_point
+                iy = dsub(sy, dmul(N[1], d2));
+                iz = dsub(sz, dmul(N[2], d2));
+            }
+            bool ok = true;
+            // TableBuilder::step along the reflector chain (src/vistable.cpp:432-467)
+            for (int c = 1; c < E.order && ok; ++c) {
+                const int from = E.chain[c - 1], to = E.chain[c];
+                double nx0[3], ny0[3], nx1[3], ny1[3];
+                bool nh[3] = {false, false, false}, nf[3] = {false, false, false};
+                bool any = false;
+                for (int pl = 0; pl < 3; ++pl) {
+                    nx0[pl] = ny0[pl] = nx1[pl] = ny1[pl] = 0.0;
+                    if (!s.seg_ok[3 * from + pl] || !s.seg_ok[3 * to + pl]) continue;
+                    const double* fs = s.seg + (static_cast<size_t>(from) * 3 + pl) * 6;
+                    const double* gs = s.seg + (static_cast<size_t>(to) * 3 + pl) * 6;
                     const double dd = fabs(dadd(dmul(fs[4], gs[4]), dmul(fs[5], gs[5])));
-                    if (!(dd >= 1.0 - 1e-9 || dd <= 1e-9)) continue;   // required_planes(f, g)
-                    double w0x, w0y, w1x, w1y;
-                    bool was_full = true;
-                    if (R.has[pl]) {
-                        const double dx = dsub(fs[2], fs[0]), dy = dsub(fs[3], fs[1]);
-                        w0x = dadd(fs[0], dmul(dx, R.sub[2 * pl]));
-                        w0y = dadd(fs[1], dmul(dy, R.sub[2 * pl]));
-                        w1x = dadd(fs[0], dmul(dx, R.sub[2 * pl + 1]));
-                        w1y = dadd(fs[1], dmul(dy, R.sub[2 * pl + 1]));
-                        was_full = !R.clipped[pl];
-                    } else {
-                        w0x = fs[0];
-                        w0y = fs[1];
-                        w1x = fs[2];
-                        w1y = fs[3];
-                    }
+                    if (!(dd >= 1.0 - 1e-9 || dd <= 1e-9)) continue;   // required_planes(from, to)
+                    // the window in this plane, or the whole face when never constrained
+                    const double w0x = hw[pl] ? wx0[pl] : fs[0], w0y = hw[pl] ? wy0[pl] : fs[1];
+                    const double w1x = hw[pl] ? wx1[pl] : fs[2], w1y = hw[pl] ? wy1[pl] : fs[3];
+                    const bool was_full = hw[pl] ? fl[pl] : true;
                     double apx, apy;
                     proj(pl, ix, iy, iz, apx, apy);
-                    const Cov c = beam_coverage(apx, apy, w0x, w0y, w1x, w1y, fs[4], fs[5], gs[0], gs[1], gs[2], gs[3]);
-                    if (c.verdict == 2) {
+                    const Cov cv = beam_coverage(apx, apy, w0x, w0y, w1x, w1y, fs[4], fs[5], gs[0], gs[1], gs[2], gs[3]);
+                    if (cv.verdict == 2) {
                         ok = false;
                         break;
                     }
+                    const double qx = dsub(gs[2], gs[0]), qy = dsub(gs[3], gs[1]);
+                    nx0[pl] = dadd(gs[0], dmul(qx, cv.lo));
+                    ny0[pl] = dadd(gs[1], dmul(qy, cv.lo));
+                    nx1[pl] = dadd(gs[0], dmul(qx, cv.hi));
+                    ny1[pl] = dadd(gs[1], dmul(qy, cv.hi));
+                    nh[pl] = true;
+                    nf[pl] = was_full && cv.verdict == 0;
                     any = true;
-                    if (pl == E.plane) {
-                        has_pl = true;
-                        full_pl = was_full && c.verdict == 0;
-                    }
                 }
-                row = ok && any;
-                full = row && has_pl && full_pl;
+                if (!ok || !any) {
+                    ok = false;
+                    break;
+                }
+                for (int pl = 0; pl < 3; ++pl) {
+                    hw[pl] = nh[pl];
+                    fl[pl] = nf[pl];
+                    wx0[pl] = nx0[pl];
+                    wy0[pl] = ny0[pl];
+                    wx1[pl] = nx1[pl];
+                    wy1[pl] = ny1[pl];
+                }
+                // image3 mirrored through the new tail face
+                const double* P = s.pts + static_cast<size_t>(to) * VISRT_MAX_VERTS * 3;
+                const double* N = s.normal + 3 * static_cast<size_t>(to);
+                const double d2 = dmul(2.0, dot_rel(ix, iy, iz, P[0], P[1], P[2], N[0], N[1], N[2]));
+                ix = dsub(ix, dmul(N[0], d2));
+                iy = dsub(iy, dmul(N[1], d2));
+                iz = dsub(iz, dmul(N[2], d2));
             }
+            row = ok;
+            full = ok && hw[E.plane] && fl[E.plane];
         }
         const size_t w = (a.paired ? 0 : static_cast<size_t>(k) * a.words) + static_cast<size_t>(e >> 5);
         if (row) atomicOr(a.row_bits + w, 1u << (e & 31));
@@ -865,8 +898,8 @@ extern "C" int visrt_point_tables(visrt_scene* sc, int64_t nsrc, const double* s
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const visrt::DevScene& ds = visrt::scene_dev(sc);
         for (int64_t e = 0; e < nent; ++e) {
-            if (entries[e].order < 1 || entries[e].order > 2)
-                throw visrt::UsageError("point tables cover matrix entries of order 1 and 2");
+            if (entries[e].order < 1 || entries[e].order > 4)
+                throw visrt::UsageError("point tables cover matrix entries of order 1..4");
             for (int c = 0; c <= entries[e].order; ++c)
                 if (entries[e].chain[c] < 0 || entries[e].chain[c] >= ds.n) throw visrt::UsageError("bad face index");
             if (entries[e].plane < 0 || entries[e].plane > 2) throw visrt::UsageError("bad plane tag");

@@ -21,6 +21,7 @@
 //     string orders of the reference's SigKey / row sorts supplied as ranks
 //     (visrt_names), so tie-breaking matches std::set / std::sort exactly.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <iterator>
 #include <map>
@@ -97,13 +98,13 @@ __global__ void __launch_bounds__(256) k_plan_clear(DevScene s, int nq, const do
 }
 
 // plan_member_chain (src/vistable.cpp:635-669) with plan_visible_intervals
-// (594-633) inlined: query q = (source xy, reflector chain[2], -1 padded).
+// (594-633) inlined: query q = (source xy, reflector chain[4], -1 padded).
 __global__ void __launch_bounds__(256) k_plan_member(DevScene s, int nq, const double* S2, const int32_t* chain,
                                                      uint8_t* out) {
     const int lane = threadIdx.x & 31;
     for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += (gridDim.x * blockDim.x) >> 5) {
         const double sx = S2[2 * q], sy = S2[2 * q + 1];
-        const int head = chain[2 * q];
+        const int head = chain[4 * q];
         bool member = false;
         do {
             if (!s.seg_ok[3 * head]) break;
@@ -161,8 +162,8 @@ __global__ void __launch_bounds__(256) k_plan_member(DevScene s, int nq, const d
             mirror2(sx, sy, ax, ay, bx, by, apx, apy);
             double ox = nx, oy = ny;
             bool ok = true;
-            for (int c = 1; c < 2 && ok; ++c) {
-                const int g = chain[2 * q + c];
+            for (int c = 1; c < 4 && ok; ++c) {
+                const int g = chain[4 * q + c];
                 if (g < 0) break;
                 if (!s.seg_ok[3 * g]) {
                     ok = false;
@@ -495,30 +496,28 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
     };
 
     // ---- MobileSampler ctor (src/vistable.cpp:699-716): keys and chains ----
-    std::map<std::pair<int, int>, int> chain_id;   // reflectors (f0, f1 or -1) -> id
+    std::map<std::array<int, 4>, int> chain_id;   // reflectors (-1 padded) -> id
     std::vector<visrt_entry> chains;              // as K5 entries (order = #reflectors)
     std::vector<KeyDef> keys;
     std::map<std::tuple<int, int, int>, int> face_key;   // (order, parent, node) -> keys index
     std::vector<std::vector<int>> key_chains;
     for (const visrt_entry& e : entries) {
         if (e.order > max_order) continue;
-        const int f0 = e.chain[0], f1 = e.order >= 2 ? e.chain[1] : -1;
-        auto ci = chain_id.find({f0, f1});
+        const int L = e.order;   // reflectors chain[0..L-1]
+        std::array<int, 4> refl{-1, -1, -1, -1};
+        for (int q = 0; q < L; ++q) refl[q] = e.chain[q];
+        auto ci = chain_id.find(refl);
         int c;
         if (ci == chain_id.end()) {
             c = static_cast<int>(chains.size());
-            chain_id[{f0, f1}] = c;
-            visrt_entry ce{};
-            ce.order = e.order;
-            ce.chain[0] = f0;
-            ce.chain[1] = e.order >= 2 ? f1 : e.chain[1];
-            ce.chain[2] = e.order >= 2 ? e.chain[2] : 0;
+            chain_id[refl] = c;
+            visrt_entry ce = e;   // the K5 query: same reflectors (the aim and plane are not read for reach)
             ce.plane = 0;
             chains.push_back(ce);
         } else {
             c = ci->second;
         }
-        const KeyDef kd{e.order, e.order >= 2 ? f0 : -1, e.order >= 2 ? f1 : f0, -1};
+        const KeyDef kd{L, L >= 2 ? refl[L - 2] : -1, refl[L - 1], -1};
         auto it = face_key.find({kd.order, kd.parent, kd.node});
         int k;
         if (it == face_key.end()) {
@@ -730,11 +729,12 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
                 }
             const visrt_entry& ch = chains[flipped];
             plan0[e] = static_cast<int>(MS.size() / 2);
-            const int32_t c2[2] = {ch.chain[0], ch.order >= 2 ? ch.chain[1] : -1};
+            int32_t c4[4] = {-1, -1, -1, -1};
+            for (int q = 0; q < ch.order && q < 4; ++q) c4[q] = ch.chain[q];
             MS.insert(MS.end(), m2, m2 + 2);
-            MC.insert(MC.end(), c2, c2 + 2);
+            MC.insert(MC.end(), c4, c4 + 4);
             MS.insert(MS.end(), o2, o2 + 2);
-            MC.insert(MC.end(), c2, c2 + 2);
+            MC.insert(MC.end(), c4, c4 + 4);
             // probe_blockers(p, head): head vertices + centroid, head skipped
             const int head = ch.chain[0];
             const int nv = hs.nv[head];
@@ -873,8 +873,8 @@ extern "C" int visrt_chain_reach(visrt_scene* sc, int64_t nq, const double* src_
         visrt::ScopedDevice dev(sc);
         const visrt::DevScene& ds = visrt::scene_dev(sc);
         for (int64_t q = 0; q < nq; ++q) {
-            if (chains[q].order < 1 || chains[q].order > 2)
-                throw visrt::UsageError("chain reach covers reflector chains of length 1 and 2");
+            if (chains[q].order < 1 || chains[q].order > 4)
+                throw visrt::UsageError("chain reach covers reflector chains of length 1..4");
             for (int c = 0; c <= chains[q].order; ++c)
                 if (chains[q].chain[c] < 0 || chains[q].chain[c] >= ds.n) throw visrt::UsageError("bad face index");
             if (chains[q].plane < 0 || chains[q].plane > 2) throw visrt::UsageError("bad plane tag");
@@ -905,10 +905,10 @@ extern "C" int visrt_trajectory_table(visrt_scene* sc, int32_t nwp, const double
         const visrt::DevScene& ds = visrt::scene_dev(sc);
         if (!names || !names->key_rank || !names->parent_rank || !names->building_rank)
             throw visrt::UsageError("visrt_names: every rank array is required");
-        if (max_order < 1 || max_order > 2)
-            throw visrt::UsageError("trajectory tables cover max_order 1 and 2 on the GPU path");
+        if (max_order < 1 || max_order > 4)
+            throw visrt::UsageError("trajectory tables cover max_order 1..4");
         for (int64_t e = 0; e < nent; ++e) {
-            if (entries[e].order < 1 || entries[e].order > 2) continue;   // higher orders are never sampled
+            if (entries[e].order < 1 || entries[e].order > 4) continue;
             for (int c = 0; c <= entries[e].order; ++c)
                 if (entries[e].chain[c] < 0 || entries[e].chain[c] >= ds.n) throw visrt::UsageError("bad face index");
         }

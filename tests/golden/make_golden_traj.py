@@ -8,8 +8,8 @@ Run in the build container (needs /root/reference):
     python tests/golden/make_golden_traj.py
 
 Per case: the scene (a golden fixture name, or inline faces), building names,
-waypoints, max_order, the matrix entries of order <= 2 in matrix order
-(order, chain[3], plane — the input a caller hands the GPU path) and the
+waypoints, max_order, the matrix entries of order <= max_order in matrix order
+([order, chain ids..., plane] — the input a caller hands the GPU path) and the
 reference's rows, doubles as float.hex() for bit-exact comparison.
 """
 from __future__ import annotations
@@ -52,7 +52,7 @@ def entries(r, m, max_order):
         if e["order"] > max_order:
             continue
         ch = list(e["chain"]) + [0] * (3 - len(e["chain"]))
-        out.append([e["order"], ch[0], ch[1], ch[2], e["plane"]])
+        out.append([e["order"]] + ch + [e["plane"]])   # [order, chain (>= 3 ids), plane]
     return out
 
 
@@ -75,7 +75,9 @@ def main() -> None:
     cases = []
     jobs = [("screened_wall", "route_drive_by", 2), ("screened_wall", "route_drive_by", 1),
             ("screened_wall", "route_corridor", 1), ("manhattan", "route_manhattan", 2),
-            ("street_canyon", "route_corridor", 2), ("two_buildings", "route_drive_by", 2)]
+            ("street_canyon", "route_corridor", 2), ("two_buildings", "route_drive_by", 2),
+            ("screened_wall", "route_drive_by", 3), ("street_canyon", "route_corridor", 3),
+            ("two_buildings", "route_drive_by", 4)]
     for scene, rt_name, order in jobs:
         r = bindings.RefOracle(path=os.path.join(FIXTURES, scene + ".json"))
         soup = soup_from_ref(r, scene)

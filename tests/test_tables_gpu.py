@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 def entries_of(ents, max_order):
-    out = [(e["order"], e["chain"] + [0] * (3 - len(e["chain"])), e["plane"]) for e in ents
+    out = [(e["order"], e["chain"] + [0] * (5 - len(e["chain"])), e["plane"]) for e in ents
            if e["order"] <= max_order]
     return np.array(out, dtype=ENTRY_DTYPE)
 
@@ -45,7 +45,7 @@ def test_street_canyon_published_rows():
     {AB->EF, AC'->EG, AC'->EI, AC'->CG, EI->AC'} from (5, 28, 11)."""
     d = G.load("street_canyon")
     s = G.soup(d)
-    E = np.array([(1, [e["ref"], e["aim"], 0], e["plane"]) for e in d["matrix1"]], dtype=ENTRY_DTYPE)
+    E = np.array([(1, [e["ref"], e["aim"], 0, 0, 0], e["plane"]) for e in d["matrix1"]], dtype=ENTRY_DTYPE)
     labels = [(f["label_xy"], f["label_vert"]) for f in d["faces"]]
     with Scene(s) as sc:
         rows = point_vis_table(sc, [5.0, 28.0, 11.0], E, s.ids, labels)
@@ -80,7 +80,7 @@ def test_point_tables_full_bits_consistent():
     exactly where that region is unclipped in the entry's plane."""
     wl = scenes.workload(1)
     d = G.load("config1")
-    E = np.array([(1, [e["ref"], e["aim"], 0], e["plane"]) for e in d["matrix1"]], dtype=ENTRY_DTYPE)
+    E = np.array([(1, [e["ref"], e["aim"], 0, 0, 0], e["plane"]) for e in d["matrix1"]], dtype=ENTRY_DTYPE)
     with Scene(wl.scene) as sc:
         rows, full, regs, _ = point_tables(sc, wl.tx[:5], E, want_regions=True)
     for k in range(5):
@@ -88,3 +88,26 @@ def test_point_tables_full_bits_consistent():
             r = regs[k, ent["chain"][0]]
             assert rows[k, e] == (r["present"] == 1)
             assert full[k, e] == (r["present"] == 1 and bool(r["has"][ent["plane"]]) and not r["clipped"][ent["plane"]])
+
+
+@pytest.mark.parametrize("name,order", [("two_buildings", 3), ("street_canyon", 3), ("screened_wall", 4)])
+def test_point_vis_table_higher_orders_vs_reference(oracle_built, name, order):
+    """point_vis_table of orders 3 and 4 (the beam cascade through 3-4
+    reflectors, src/vistable.cpp:404-467) vs the compiled reference."""
+    if not oracle_built.have_ref():
+        pytest.skip("oracle/_ref not built")
+    d = G.load(name)
+    soup = G.soup(d, with_buildings=False)
+    r = oracle_built.RefOracle(soup)
+    m = r.build_matrix(order)
+    E = entries_of(r.matrix_entries(m), order)
+    ids = soup.ids
+    srcs = [G.unhex(x["source"]) for x in d["regions"]]
+    with Scene(soup) as sc:
+        for src in srcs:
+            got = point_vis_table(sc, src, E, ids)
+            exp = r.point_vis_table(m, np.asarray(src), order)
+            exp_rows = [{"order": x["order"], "chain": [ids[f] for f in x["chain"]], "aim": ids[x["aim"]],
+                         "plane": x["plane"], "verdict": "Full" if x["verdict"] == 0 else "Partial",
+                         "ref_display": x["ref_display"], "aim_display": x["aim_display"]} for x in exp]
+            assert got == exp_rows, src

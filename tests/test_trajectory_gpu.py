@@ -36,8 +36,9 @@ def case_scene(c):
 
 def entries_of(c):
     e = np.zeros(len(c["entries"]), ENTRY_DTYPE)
-    for k, (o, a, b, cc, p) in enumerate(c["entries"]):
-        e[k] = (o, [a, b, cc], p)
+    for k, row in enumerate(c["entries"]):   # [order, chain..., plane]
+        ch = list(row[1:-1]) + [0] * 5
+        e[k] = (row[0], ch[:5], row[-1])
     return e
 
 
@@ -128,7 +129,7 @@ def test_trajectory_errors():
         with pytest.raises(VisibilityError, match="matrix holds orders up to 1, requested 2"):
             trajectory_vis_table(sc, c["waypoints"], entries_of(c), 2, soup.ids, labels, matrix_max_order=1)
         with pytest.raises(UsageError):
-            trajectory_vis_table(sc, c["waypoints"], entries_of(c), 3, soup.ids, labels)
+            trajectory_vis_table(sc, c["waypoints"], entries_of(c), 5, soup.ids, labels)
 
 
 @pytest.mark.gpu
