@@ -82,17 +82,57 @@ inline int required_planes(const HostScene& hs, int i, int j) {
     return m;
 }
 
+// Conservative screen (no atan2): true when the angle record at `at` is
+// certainly NOT degenerate — both aim endpoints clearly in front of the ref
+// line (angles strictly inside (0, 180), never clamped) at clearly different
+// angles, or one clearly in front and the other clearly behind (clamped to 0).
+// The 1e-6 relative margins dwarf every rounding of the exact path, whose
+// threshold is 1e-12 degrees; anything near a boundary goes to the exact check.
+inline bool record_clearly_open(double atx, double aty, double otx, double oty, double ox, double oy,
+                                const double* aim_seg) {
+    constexpr double kM = 1e-6;
+    const double dx = otx - atx, dy = oty - aty;
+    const double dl = std::sqrt(dx * dx + dy * dy);
+    if (!(dl > 0.0)) return false;
+    const double ux = dx / dl, uy = dy / dl;
+    const double sg = (ux * oy - uy * ox) >= 0.0 ? 1.0 : -1.0;
+    double y[2], r[2], vx[2], vy[2];
+    for (int q = 0; q < 2; ++q) {
+        vx[q] = aim_seg[2 * q] - atx;
+        vy[q] = aim_seg[2 * q + 1] - aty;
+        r[q] = std::sqrt(vx[q] * vx[q] + vy[q] * vy[q]);
+        if (!(r[q] > 1e-6)) return false;   // near-coincident endpoint: exact path
+        y[q] = sg * (ux * vy[q] - uy * vx[q]);
+    }
+    const bool f0 = y[0] > kM * r[0], f1 = y[1] > kM * r[1];
+    const bool b0 = y[0] < -kM * r[0], b1 = y[1] < -kM * r[1];
+    if (f0 && f1) return std::fabs(vx[0] * vy[1] - vy[0] * vx[1]) > kM * r[0] * r[1];
+    return (f0 && b1) || (b0 && f1);
+}
+
+inline bool range_clearly_open(const HostScene& hs, int ref, int aim, int plane) {
+    const double* sr = &hs.seg[(static_cast<size_t>(ref) * 3 + plane) * 6];
+    const double* sa = &hs.seg[(static_cast<size_t>(aim) * 3 + plane) * 6];
+    return record_clearly_open(sr[0], sr[1], sr[2], sr[3], sr[4], sr[5], sa) ||
+           record_clearly_open(sr[2], sr[3], sr[0], sr[1], sr[4], sr[5], sa);
+}
+
 // first_order_pair drops the pair when any (plane, direction) range is
-// degenerate (src/vismatrix.cpp:614-624).
+// degenerate (src/vismatrix.cpp:614-624). The screen settles almost every
+// range without atan2; the rest run the reference's exact records.
 inline bool pair_range_degenerate(const HostScene& hs, int i, int j) {
     const int planes = required_planes(hs, i, j);
     for (int pl = 0; pl < 3; ++pl) {
         if (!(planes >> pl & 1)) continue;
         AngleRec a, b;
-        first_order_ranges(hs, i, j, pl, a, b);
-        if (range_is_degenerate(a, b)) return true;
-        first_order_ranges(hs, j, i, pl, a, b);
-        if (range_is_degenerate(a, b)) return true;
+        if (!range_clearly_open(hs, i, j, pl)) {
+            first_order_ranges(hs, i, j, pl, a, b);
+            if (range_is_degenerate(a, b)) return true;
+        }
+        if (!range_clearly_open(hs, j, i, pl)) {
+            first_order_ranges(hs, j, i, pl, a, b);
+            if (range_is_degenerate(a, b)) return true;
+        }
     }
     return false;
 }
