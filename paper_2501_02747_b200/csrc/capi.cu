@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <mutex>
+
 #include "capi_internal.h"
 #include "device.h"
 #include "host_geom.h"
@@ -56,6 +58,43 @@ T* dev_alloc(size_t count, std::vector<void*>& allocs) {
     return visrt::dalloc<T>(count, allocs);
 }
 
+// Scene state lives in ONE device arena from the device's stream-ordered
+// memory pool (kept resident: release threshold = max), filled by ONE copy
+// from a process-wide pinned staging buffer — scene creation/destruction stay
+// at O(10 us) of driver work instead of ~20 cudaMalloc/cudaFree/pageable
+// copies (the e2e path creates a scene per step).
+struct Arena {
+    struct Part {
+        const void* src;
+        size_t bytes, off;
+    };
+    std::vector<Part> parts;
+    size_t total = 0;
+    size_t add(const void* src, size_t bytes) {
+        const size_t off = total;
+        parts.push_back({src, bytes, off});
+        total += (std::max<size_t>(bytes, 16) + 255) & ~size_t(255);
+        return off;
+    }
+};
+
+std::mutex g_stage_mu;
+void* g_stage = nullptr;
+size_t g_stage_bytes = 0;
+
+void pool_setup(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.push_back(device);
+}
+
 }  // namespace
 
 struct visrt_scene {
@@ -63,6 +102,7 @@ struct visrt_scene {
     visrt::DevScene ds;
     int device = 0;
     std::vector<void*> allocs;
+    void* arena = nullptr;   // pooled device arena holding every scene array
     int64_t upload_bytes = 0;
     unsigned long long* d_bits = nullptr;
     unsigned long long* d_counter = nullptr;
@@ -86,6 +126,10 @@ struct visrt_scene {
         cudaGetDevice(&cur);
         cudaSetDevice(device);
         for (void* p : allocs) cudaFree(p);
+        if (arena) {
+            cudaFreeAsync(arena, 0);
+            cudaStreamSynchronize(0);
+        }
         if (d_sel) cudaFree(d_sel);
         if (d_ci) cudaFree(d_ci);
         if (d_cj) cudaFree(d_cj);
@@ -174,28 +218,55 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.n = hs.n;
         ds.maxv = hs.maxv;
         ds.words = (hs.n + 63) / 64;
-        if (hs.maxv <= 4) {
-            ds.rec = dev_upload(hs.rec4, sc->allocs);
-            ds.rec_stride = visrt::RecLayout<4>::kStride;
-        } else {
-            ds.rec = dev_upload(hs.rec8, sc->allocs);
-            ds.rec_stride = visrt::RecLayout<8>::kStride;
+        Arena ar;
+        auto add = [&](const auto& v) { return ar.add(v.data(), v.size() * sizeof(v[0])); };
+        const auto& rec = hs.maxv <= 4 ? hs.rec4 : hs.rec8;
+        ds.rec_stride = hs.maxv <= 4 ? visrt::RecLayout<4>::kStride : visrt::RecLayout<8>::kStride;
+        const size_t o_rec = add(rec), o_samples = add(hs.samples), o_pts = add(hs.pts), o_normal = add(hs.normal),
+                     o_seg = add(hs.seg), o_aabb = add(hs.aabb), o_nv = add(hs.nv), o_ns = add(hs.ns),
+                     o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_box = add(hs.box), o_sbox = add(hs.sbox),
+                     o_tbox = add(hs.tbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
+        const size_t o_bits = ar.add(nullptr, static_cast<size_t>(hs.n) * ds.words * 8);
+        const size_t o_counter = ar.add(nullptr, 4 * 8);
+        const size_t o_count = ar.add(nullptr, 2 * 8);
+        pool_setup(device);
+        ck(cudaMallocAsync(&sc->arena, ar.total, 0), "cudaMallocAsync arena");
+        {
+            std::lock_guard<std::mutex> lk(g_stage_mu);
+            if (g_stage_bytes < ar.total) {
+                if (g_stage) cudaFreeHost(g_stage);
+                g_stage = nullptr;
+                g_stage_bytes = 0;
+                ck(cudaHostAlloc(&g_stage, ar.total, cudaHostAllocDefault), "cudaHostAlloc staging");
+                g_stage_bytes = ar.total;
+            }
+            char* st = static_cast<char*>(g_stage);
+            for (const auto& pt : ar.parts)
+                if (pt.src && pt.bytes) std::memcpy(st + pt.off, pt.src, pt.bytes);
+            ck(cudaMemcpyAsync(sc->arena, g_stage, ar.total, cudaMemcpyHostToDevice, 0), "H2D scene");
+            ck(cudaStreamSynchronize(0), "sync");
         }
-        ds.samples = dev_upload(hs.samples, sc->allocs);
-        ds.pts = dev_upload(hs.pts, sc->allocs);
-        ds.normal = dev_upload(hs.normal, sc->allocs);
-        ds.seg = dev_upload(hs.seg, sc->allocs);
-        ds.aabb = dev_upload(hs.aabb, sc->allocs);
-        ds.nv = dev_upload(hs.nv, sc->allocs);
-        ds.ns = dev_upload(hs.ns, sc->allocs);
-        ds.orient = dev_upload(hs.orient, sc->allocs);
-        ds.seg_ok = dev_upload(hs.seg_ok, sc->allocs);
-        ds.box = dev_upload(hs.box, sc->allocs);
-        ds.sbox = dev_upload(hs.sbox, sc->allocs);
-        ds.tbox = dev_upload(hs.tbox, sc->allocs);
-        ds.srec = dev_upload(hs.srec, sc->allocs);
-        ds.perm = dev_upload(hs.perm, sc->allocs);
-        ds.inv = dev_upload(hs.inv, sc->allocs);
+        char* base = static_cast<char*>(sc->arena);
+        auto at = [&](size_t off) { return static_cast<void*>(base + off); };
+        ds.rec = static_cast<const double*>(at(o_rec));
+        ds.samples = static_cast<const double*>(at(o_samples));
+        ds.pts = static_cast<const double*>(at(o_pts));
+        ds.normal = static_cast<const double*>(at(o_normal));
+        ds.seg = static_cast<const double*>(at(o_seg));
+        ds.aabb = static_cast<const double*>(at(o_aabb));
+        ds.nv = static_cast<const int32_t*>(at(o_nv));
+        ds.ns = static_cast<const int32_t*>(at(o_ns));
+        ds.orient = static_cast<const int32_t*>(at(o_orient));
+        ds.seg_ok = static_cast<const int32_t*>(at(o_seg_ok));
+        ds.box = static_cast<const float*>(at(o_box));
+        ds.sbox = static_cast<const float*>(at(o_sbox));
+        ds.tbox = static_cast<const float*>(at(o_tbox));
+        ds.srec = static_cast<const double*>(at(o_srec));
+        ds.perm = static_cast<const int32_t*>(at(o_perm));
+        ds.inv = static_cast<const int32_t*>(at(o_inv));
+        sc->d_bits = static_cast<unsigned long long*>(at(o_bits));
+        sc->d_counter = static_cast<unsigned long long*>(at(o_counter));
+        sc->d_count = static_cast<long long*>(at(o_count));
         ds.ntiles = hs.ntiles;
         ds.nchunks = hs.nchunks;
         sc->upload_bytes = static_cast<int64_t>(
@@ -205,9 +276,6 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.ox = hs.origin[0];
         ds.oy = hs.origin[1];
         ds.oz = hs.origin[2];
-        sc->d_bits = dev_alloc<unsigned long long>(static_cast<size_t>(hs.n) * ds.words, sc->allocs);
-        sc->d_counter = dev_alloc<unsigned long long>(4, sc->allocs);
-        sc->d_count = dev_alloc<long long>(2, sc->allocs);
         ck(cudaEventCreate(&sc->ev0), "event");
         ck(cudaEventCreate(&sc->ev1), "event");
         *out = sc.release();
