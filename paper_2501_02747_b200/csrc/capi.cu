@@ -125,7 +125,7 @@ struct visrt_scene {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(device);
-        for (void* p : allocs) cudaFree(p);
+        for (void* p : allocs) visrt::BlockCache::get().release(p);
         if (arena) {
             cudaFreeAsync(arena, 0);
             cudaStreamSynchronize(0);
@@ -431,12 +431,7 @@ int visrt_pair_detail(visrt_scene* sc, int64_t npairs, const int32_t* ci, const 
         }
         const int words32 = (n + 31) / 32;
         std::vector<void*> tmp;
-        struct Free {
-            std::vector<void*>& v;
-            ~Free() {
-                for (void* p : v) cudaFree(p);
-            }
-        } guard{tmp};
+        visrt::FreeGuard guard{tmp};
         int32_t* d_ci = dev_alloc<int32_t>(npairs, tmp);
         int32_t* d_cj = dev_alloc<int32_t>(npairs, tmp);
         int8_t* d_kind = dev_alloc<int8_t>(npairs, tmp);

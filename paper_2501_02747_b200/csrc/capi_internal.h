@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -67,10 +69,62 @@ struct ScopedDevice {
     }
 };
 
+// Caching allocator for the per-call scratch buffers (power-of-two buckets
+// per device, blocks returned by FreeGuard are reused, never released): every
+// C-ABI call synchronises its stream before returning, so a returned block is
+// idle. Repeated calls (trajectory bisection rounds, e2e steps) then pay no
+// cudaMalloc/cudaFree. Blocks above 1 GiB bypass the cache.
+struct BlockCache {
+    std::mutex mu;
+    std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;
+    std::map<void*, std::pair<int, size_t>> owner;
+    static BlockCache& get() {
+        static BlockCache c;
+        return c;
+    }
+    static size_t bucket(size_t bytes) {
+        size_t b = 256;
+        while (b < bytes) b <<= 1;
+        return b;
+    }
+    void* alloc(size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (bytes > (size_t(1) << 30)) {
+            void* p = nullptr;
+            ck(cudaMalloc(&p, bytes), "cudaMalloc");
+            return p;
+        }
+        const size_t b = bucket(bytes);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto& fl = free_blocks[{dev, b}];
+            if (!fl.empty()) {
+                void* p = fl.back();
+                fl.pop_back();
+                return p;
+            }
+        }
+        void* p = nullptr;
+        ck(cudaMalloc(&p, b), "cudaMalloc");
+        std::lock_guard<std::mutex> lk(mu);
+        owner[p] = {dev, b};
+        return p;
+    }
+    void release(void* p) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = owner.find(p);
+        if (it == owner.end()) {
+            cudaFree(p);   // uncached (large) block
+            return;
+        }
+        free_blocks[it->second].push_back(p);
+    }
+};
+
 template <class T>
 T* dalloc(size_t count, std::vector<void*>& allocs) {
-    T* p = nullptr;
-    ck(cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)), "cudaMalloc");
+    T* p = static_cast<T*>(BlockCache::get().alloc(std::max<size_t>(count * sizeof(T), 16)));
     allocs.push_back(p);
     return p;
 }
@@ -78,7 +132,7 @@ T* dalloc(size_t count, std::vector<void*>& allocs) {
 struct FreeGuard {
     std::vector<void*>& v;
     ~FreeGuard() {
-        for (void* p : v) cudaFree(p);
+        for (void* p : v) BlockCache::get().release(p);
     }
 };
 

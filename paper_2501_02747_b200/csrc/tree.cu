@@ -613,7 +613,7 @@ struct visrt_tracer {
     std::vector<int64_t> nodes;
     std::vector<int32_t> snap_edge;   // per snapshot diffraction edge of the last trace (empty: none)
     ~visrt_tracer() {
-        for (void* p : allocs) cudaFree(p);
+        for (void* p : allocs) visrt::BlockCache::get().release(p);
     }
 };
 
