@@ -310,26 +310,10 @@ __device__ __forceinline__ double dist3(const double* a, const double* b) {
 // a diffraction edge for the snapshot, Engine::attempt's second sequence
 // (ending at the edge's Fermat point) is unfolded too (383-394).
 template <int MAXV>
-__global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
+__device__ void unfold_one(const TreeArgs& a, int snap, int d, const int* f, long long t, int kedge) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const DevScene& s = a.s;
-    const long long nt = a.in ? a.nin : a.nsnap;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < nt; t += stride) {
-        int snap, d;
-        int f[4] = {-1, -1, -1, -1};
-        if (a.in) {
-            const TreeNode& nd = a.in[t];
-            snap = nd.snap;
-            d = nd.depth;
-            f[0] = nd.f0;
-            f[1] = nd.f1;
-            f[2] = nd.f2;
-            f[3] = nd.f3;
-        } else {
-            snap = a.snap0 + static_cast<int>(t);
-            d = 0;
-        }
+    {
         const double* T = a.tx + 3 * static_cast<size_t>(snap);
         const double* Rx = a.rx_fixed ? a.rx : a.rx + 3 * static_cast<size_t>(snap);
         double img[5][3];
@@ -347,8 +331,7 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             img[k + 1][2] = img[k][2];
             mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
         }
-        if (!fwd) continue;
-        const int kedge = a.keyed ? a.in[t].rank : -1;
+        if (!fwd) return;
         const int edge = a.keyed ? kedge : (a.snap_edge ? a.snap_edge[snap] : -1);
         for (int v = (a.keyed && kedge >= 0) ? 1 : 0; v < (edge >= 0 ? 2 : 1); ++v) {
             bool ok = true;
@@ -425,6 +408,89 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
             if (static_cast<long long>(slot) < a.cand_cap) a.cand[slot] = c;
         }
     }
+}
+
+template <int MAXV>
+__global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
+    const long long nt = a.in ? a.nin : a.nsnap;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < nt; t += stride) {
+        int snap, d;
+        int f[4] = {-1, -1, -1, -1};
+        if (a.in) {
+            const TreeNode& nd = a.in[t];
+            snap = nd.snap;
+            d = nd.depth;
+            f[0] = nd.f0;
+            f[1] = nd.f1;
+            f[2] = nd.f2;
+            f[3] = nd.f3;
+        } else {
+            snap = a.snap0 + static_cast<int>(t);
+            d = 0;
+        }
+        unfold_one<MAXV>(a, snap, d, f, t, a.keyed ? a.in[t].rank : -1);
+    }
+}
+
+// The LAST level fused: per parent (warp) the children are counted (cnt[p])
+// and unfolded on the spot instead of being written as a frontier level and
+// read back — the deepest level is most of the tree (config 3 order 3: 4.3M of
+// 4.3M nodes per snapshot), so this removes its node rows from HBM entirely.
+template <int MAXV>
+__global__ void __launch_bounds__(256) k_tree_last(TreeArgs a, unsigned long long* cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const long long nparents = a.in ? a.nin : a.nsnap;
+    for (long long p = warp; p < nparents; p += nwarps) {
+        const TreeNode par = tree_parent(a, p);
+        const Pool P = tree_pool(a, par, a.s.n);
+        const int fp[4] = {par.f0, par.f1, par.f2, par.f3};
+        unsigned long long c_all = 0;
+        for (long long q0 = 0; q0 < P.npool; q0 += 32) {
+            const long long q = q0 + lane;
+            int c = -1, rank;
+            const bool ok = q < P.npool && tree_child(a, par, P, q, c, rank);
+            c_all += __popc(__ballot_sync(kFull, ok));
+            if (ok) {
+                int f[4] = {fp[0], fp[1], fp[2], fp[3]};
+                f[P.d] = c;
+                unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1);
+            }
+        }
+        if (lane == 0) cnt[p] = c_all;
+    }
+}
+
+// Per-snapshot node counts of a fused last level: the parents are in snapshot
+// order, so snapshot sn's children are off[hi] - off[lo] over its parent range.
+__global__ void k_tree_snapcount_parents(const TreeNode* par, long long np, const unsigned long long* off, int snap0,
+                                         int ns, unsigned long long* nodes_per_snap) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= ns) return;
+    const int sn = snap0 + q;
+    long long lo = 0, hi = np;
+    if (par) {
+        long long l = 0, h = np;
+        while (l < h) {
+            const long long mid = (l + h) >> 1;
+            if (par[mid].snap < sn) l = mid + 1;
+            else h = mid;
+        }
+        lo = l;
+        h = np;
+        while (l < h) {
+            const long long mid = (l + h) >> 1;
+            if (par[mid].snap <= sn) l = mid + 1;
+            else h = mid;
+        }
+        hi = l;
+    } else {   // roots: parent q is snapshot snap0 + q
+        lo = q;
+        hi = q + 1;
+    }
+    nodes_per_snap[sn] += off[hi] - off[lo];
 }
 
 // Occluder::clear on every leg of every candidate (lane per candidate).
@@ -862,6 +928,30 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
                 a.nin = nin;
                 a.out = lvl[depth & 1];
                 a.cap = node_cap;
+                if (depth == tr->max_refl - 1) {
+                    // deepest level: count + unfold fused, no frontier rows
+                    const long long np = in ? nin : ns;
+                    ck(cudaMemsetAsync(c_ncand, 0, 8, st), "memset");
+                    ck(cudaMemsetAsync(d_ctr + 3, 0, 8, st), "memset");
+                    if (ds.maxv <= 4) visrt::k_tree_last<4><<<eb, 256, 0, st>>>(a, tr->cnt);
+                    else visrt::k_tree_last<8><<<eb, 256, 0, st>>>(a, tr->cnt);
+                    ck(cudaGetLastError(), "k_tree_last");
+                    ck(cub::DeviceScan::ExclusiveSum(tr->scan_tmp, tr->scan_bytes, tr->cnt, tr->off, np + 1, st), "scan");
+                    visrt::k_tree_snapcount_parents<<<(ns + 255) / 256, 256, 0, st>>>(in, np, tr->off, s0, ns, d_nodes);
+                    ck(cudaGetLastError(), "k_tree_snapcount_parents");
+                    a.ncand = c_ncand;
+                    a.npaths = c_npath;
+                    a.counter = d_ctr + 3;
+                    if (ds.maxv <= 4) visrt::launch_legs_t<4>(a, device, st);
+                    else visrt::launch_legs_t<8>(a, device, st);
+                    unsigned long long no = 0, nc = 0;
+                    ck(cudaMemcpyAsync(&no, tr->off + np, 8, cudaMemcpyDeviceToHost, st), "D2H");
+                    ck(cudaMemcpyAsync(&nc, c_ncand, 8, cudaMemcpyDeviceToHost, st), "D2H");
+                    ck(cudaStreamSynchronize(st), "sync");
+                    if (static_cast<long long>(nc) > cand_cap) return false;
+                    seqs += static_cast<long long>(no);
+                    break;
+                }
                 // count -> exclusive scan -> fill (src/raytracer.cpp:400-430 per parent)
                 const long long np = in ? nin : ns;
                 visrt::k_tree_count<<<eb, 256, 0, st>>>(a, tr->cnt);
