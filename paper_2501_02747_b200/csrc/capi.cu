@@ -103,6 +103,7 @@ struct visrt_scene {
     int device = 0;
     std::vector<void*> allocs;
     void* arena = nullptr;   // pooled device arena holding every scene array
+    visrt::ChainCache chain_cache;
     int64_t upload_bytes = 0;
     unsigned long long* d_bits = nullptr;
     unsigned long long* d_counter = nullptr;
@@ -156,6 +157,7 @@ struct visrt_scene {
 
 namespace visrt {
 void set_last_error(const std::string& msg) { g_err = msg; }
+ChainCache& scene_chain_cache(visrt_scene* s) { return s->chain_cache; }
 const DevScene& scene_dev(const visrt_scene* s) { return s->ds; }
 const HostScene& scene_host(const visrt_scene* s) { return s->hs; }
 int scene_device(const visrt_scene* s) { return s->device; }

@@ -57,6 +57,17 @@ int capi_guard(F&& f) {
     }
 }
 
+// Result cache of visrt_chain_triples (the two-call sizing pattern would
+// otherwise run the kernel twice): keyed by a hash of the admitted bits.
+struct ChainCache {
+    bool valid = false;
+    uint64_t key = 0;
+    std::vector<int32_t> tri;   // sorted (p, t, a)
+    int64_t pairs = 0, candidates = 0;
+    float ms = 0.f;
+};
+ChainCache& scene_chain_cache(visrt_scene* s);
+
 const DevScene& scene_dev(const visrt_scene* s);
 const HostScene& scene_host(const visrt_scene* s);
 int scene_device(const visrt_scene* s);
