@@ -66,7 +66,7 @@ __device__ __forceinline__ V3 face_pt(const DevScene& s, int f, int k) {
 
 // clip_polygon_halfspace, src/geom.cpp:191-207
 template <int MAXV>
-__device__ int clip_halfspace(const DevScene& s, int f, const PlaneD& pl, V3* out) {
+__device__ __noinline__ int clip_halfspace(const DevScene& s, int f, const PlaneD& pl, V3* out) {
     const int n = s.nv[f];
     int c = 0;
     for (int i = 0; i < n; ++i) {
@@ -148,7 +148,7 @@ __device__ bool has_finite_edge(const V2* p, int n) {
 
 // chain_triple_feasible, src/vismatrix.cpp:457-476
 template <int MAXV>
-__device__ bool triple_feasible(const DevScene& s, int a, int b, int c) {
+__device__ __noinline__ bool triple_feasible(const DevScene& s, int a, int b, int c) {
     const double* N = s.normal + 3 * static_cast<size_t>(b);
     const PlaneD pl{face_pt(s, b, 0), {N[0], N[1], N[2]}};
     V3 pts[Caps<MAXV>::kPts];
