@@ -270,6 +270,31 @@ int visrt_resolve_keys(visrt_scene* scene, int64_t nsamp, const double* tx, cons
                        const int64_t* key_off, const visrt_seqkey* keys, int32_t nedges, const double* edge_ab,
                        uint8_t* ok, visrt_path* paths, visrt_stats* stats, void* stream);
 
+/* EM consumer of the path sets: ray_gains and
+ * channel_stats (include/rt/em.hpp:92-103, src/em.cpp:194-235). Per path
+ * (visrt_path as returned by the tracer): complex amplitude amp[2q..2q+1]
+ * (re, im; relative to unit transmit power and the antenna gains) and delay.
+ * face_material: [nfaces][2] relative permittivity, conductivity (S/m);
+ * edges as for the tracer plus their two adjacent faces (edge_faces[2e], the
+ * 0-face first). Transcendentals are CUDA's: parity is tolerance-based.
+ * Errors (the reference's EmError) map to status 1. */
+typedef struct {
+    double frequency;      /* Hz */
+    double tx_gain_dbi;
+    double rx_gain_dbi;
+    int32_t polarization;  /* 0 TE, 1 TM */
+    int32_t pad;
+} visrt_em_config;
+int visrt_ray_gains(visrt_scene* scene, int64_t npaths, const visrt_path* paths, const double* face_material,
+                    int32_t nedges, const double* edge_ab, const int32_t* edge_faces, const visrt_em_config* config,
+                    double* amp, double* delay, visrt_stats* stats, void* stream);
+/* channel_stats per snapshot over its rays path_off[k]..path_off[k+1]: outage,
+ * path loss -10 log10(sum |a|^2) (inf on outage) and the power-weighted RMS
+ * delay spread. */
+int visrt_channel_stats(visrt_scene* scene, int64_t nsnap, const int64_t* path_off, const double* amp,
+                        const double* delay, int8_t* outage, double* path_loss_db, double* rms_delay_spread,
+                        void* stream);
+
 /* The scene's edges for diffraction (Scene::edges, include/rt/scene.hpp:85-95):
  * edge e = (a, b) at edge_ab[6e..6e+5]; edge_rank[e] = order of its id string. */
 int visrt_tracer_set_edges(visrt_tracer* tracer, int32_t nedges, const double* edge_ab, const int32_t* edge_rank);

@@ -307,6 +307,11 @@ class RefOracle:
             L.vref_scene_from_shells.argtypes = [C.c_int32, _i32p, _f64p, C.c_char_p, _i32p, C.c_int32,
                                                  C.c_char_p]
             L.vref_closest_edge.argtypes = [C.c_void_p, _f64p]
+            L.vref_face_material.argtypes = [C.c_void_p, C.c_int32, _f64p]
+            L.vref_edge_faces.argtypes = [C.c_void_p, C.c_int32, _i32p]
+            L.vref_trace_em.restype = C.c_int64
+            L.vref_trace_em.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p, C.c_int32, C.c_double, C.c_double,
+                                        C.c_double, C.c_int32, _f64p, _f64p, _f64p, C.c_int64]
             L.vref_dynamic_trace.restype = C.c_int64
             L.vref_dynamic_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _f64p, _f64p, C.c_int32, C.c_int32,
                                              C.c_double, C.POINTER(vref_dyn_sample), C.c_int64, C.POINTER(vref_path),
@@ -476,6 +481,35 @@ class RefOracle:
                         "paths": [{"identity": p.identity.decode(), "points": list(p.points[: 3 * (p.ninter + 2)]),
                                    "length": p.length} for p in ps]})
         return out
+
+    def face_materials(self):
+        out = np.zeros((self.n, 2), np.float64)
+        for i in range(self.n):
+            v = np.zeros(2, np.float64)
+            self.lib().vref_face_material(self.h, i, v)
+            out[i] = v
+        return out
+
+    def edge_faces(self):
+        L = self.lib()
+        out = []
+        for e in range(L.vref_nedges(self.h)):
+            f2 = np.zeros(2, np.int32)
+            L.vref_edge_faces(self.h, e, f2)
+            out.append(f2.tolist())
+        return out
+
+    def trace_em(self, accel, tx, rx, diffraction, freq, tx_gain, rx_gain, tm):
+        cap = 1 << 14
+        amp = np.zeros(2 * cap, np.float64)
+        dl = np.zeros(cap, np.float64)
+        st = np.zeros(3, np.float64)
+        n = self.lib().vref_trace_em(self.h, accel, np.ascontiguousarray(tx, np.float64),
+                                     np.ascontiguousarray(rx, np.float64), int(diffraction), freq, tx_gain, rx_gain,
+                                     int(tm), amp, dl, st, cap)
+        if n < 0:
+            raise RuntimeError(self.lib().vref_last_error().decode())
+        return amp[: 2 * n].reshape(n, 2), dl[:n], st
 
     def closest_edge(self, rx) -> int:
         return int(self.lib().vref_closest_edge(self.h, np.ascontiguousarray(rx, np.float64)))

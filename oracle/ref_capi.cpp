@@ -38,6 +38,7 @@
 #include "rt/raytracer.hpp"
 #include "rt/vismatrix.hpp"
 #include "rt/vistable.hpp"
+#include "rt/em.hpp"
 
 #include "ref_capi.h"
 
@@ -642,6 +643,60 @@ int64_t vref_dynamic_trace(void* h, void* m, int32_t nwp, const double* wp, cons
         return ns;
     } catch (const std::exception& e) {
         return fail(e, -1);
+    }
+}
+
+// Face material parameters (permittivity, conductivity) and edge faces, for
+// the EM consumer (proj/src/em.cpp).
+int32_t vref_face_material(void* h, int32_t idx, double* eps_sigma) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    try {
+        const R::Material& m = s.material(s.face(idx).material);
+        eps_sigma[0] = m.permittivity;
+        eps_sigma[1] = m.conductivity;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
+
+int32_t vref_edge_faces(void* h, int32_t idx, int32_t* faces) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    const R::Edge& e = s.edges().at(static_cast<size_t>(idx));
+    faces[0] = s.face(e.faces[0]).index;
+    faces[1] = s.face(e.faces[1]).index;
+    return 0;
+}
+
+// ray_gains + channel_stats (proj/src/em.cpp:194-277) of an accelerated trace:
+// per path amplitude (re, im) and delay (path order = the trace's), plus
+// [outage, path_loss_db, rms_delay_spread].
+int64_t vref_trace_em(void* h, void* a, const double* tx, const double* rx, int32_t diffraction, double freq,
+                      double tx_gain, double rx_gain, int32_t tm, double* amp, double* delay, double* stats3,
+                      int64_t cap) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    try {
+        const auto paths = static_cast<R::TraceAccelerator*>(a)->trace({tx[0], tx[1], tx[2]}, {rx[0], rx[1], rx[2]},
+                                                                       diffraction != 0, nullptr);
+        R::EmConfig cfg;
+        cfg.frequency = freq;
+        cfg.tx_gain_dbi = tx_gain;
+        cfg.rx_gain_dbi = rx_gain;
+        cfg.polarization = tm ? R::Polarization::TM : R::Polarization::TE;
+        const auto rays = R::ray_gains(s, paths, cfg);
+        const auto st = R::channel_stats(rays);
+        const int64_t n = static_cast<int64_t>(rays.size());
+        for (int64_t k = 0; k < n && k < cap; ++k) {
+            amp[2 * k] = rays[static_cast<size_t>(k)].amplitude.real();
+            amp[2 * k + 1] = rays[static_cast<size_t>(k)].amplitude.imag();
+            delay[k] = rays[static_cast<size_t>(k)].delay;
+        }
+        stats3[0] = st.outage ? 1.0 : 0.0;
+        stats3[1] = st.path_loss_db;
+        stats3[2] = st.rms_delay_spread;
+        return n;
+    } catch (const std::exception& e) {
+        return fail(e, -1 - error_code(e));
     }
 }
 

@@ -92,6 +92,9 @@ int64_t vref_point_vis_table(void* h, void* m, const double* src, int32_t max_or
 int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, int32_t max_order,
                               vref_mobile_row* rows, int64_t cap);
 int32_t vref_closest_edge(void* h, const double* rx);
+int64_t vref_trace_em(void* h, void* a, const double* tx, const double* rx, int32_t diffraction, double freq,
+                      double tx_gain, double rx_gain, int32_t tm, double* amp, double* delay, double* stats3,
+                      int64_t cap);
 int64_t vref_image_tree(void* h, const double* src, int32_t depth, int32_t* face, int32_t* parent,
                         int32_t* dep, double* image, int64_t cap);
 int64_t vref_brute_trace(void* h, const double* tx, const double* rx, int32_t max_refl, int32_t diffraction,

@@ -32,7 +32,7 @@ EXPORTS = [
     "visrt_chain_triples", "visrt_tracer_create",
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results", "visrt_image_tree", "visrt_closest_edges",
     "visrt_tracer_set_edges", "visrt_trace_snapshot_edges", "visrt_resolve_keys",
-    "visrt_cache_save", "visrt_cache_load",
+    "visrt_cache_save", "visrt_cache_load", "visrt_ray_gains", "visrt_channel_stats",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -66,6 +66,11 @@ class visrt_path(C.Structure):
 
 class visrt_seqkey(C.Structure):
     _fields_ = [("nrefl", C.c_int32), ("faces", C.c_int32 * 4), ("edge", C.c_int32)]
+
+
+class visrt_em_config(C.Structure):
+    _fields_ = [("frequency", C.c_double), ("tx_gain_dbi", C.c_double), ("rx_gain_dbi", C.c_double),
+                ("polarization", C.c_int32), ("pad", C.c_int32)]
 
 
 class visrt_trace_stats(C.Structure):
@@ -155,6 +160,11 @@ def lib():
     L.visrt_resolve_keys.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, C.c_int, C.c_void_p, C.c_void_p,
                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(visrt_stats),
                                      C.c_void_p]
+    L.visrt_ray_gains.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, _f64p, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.POINTER(visrt_em_config), C.c_void_p, C.c_void_p, C.POINTER(visrt_stats),
+                                  C.c_void_p]
+    L.visrt_channel_stats.argtypes = [C.c_void_p, C.c_int64, _i64p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]
     L.visrt_cache_save.argtypes = [C.c_char_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]
     L.visrt_cache_load.argtypes = [C.c_char_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_int64,
                                    C.POINTER(C.c_int64)]

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvisrt_cuda.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["ingest.cpp", "matrix.cu", "regions.cu", "trajectory.cu", "imagetree.cu", "chains.cu", "tree.cu", "peaks.cu", "capi.cu", "cache.cu"]
+SOURCES = ["ingest.cpp", "matrix.cu", "regions.cu", "trajectory.cu", "imagetree.cu", "chains.cu", "tree.cu", "peaks.cu", "capi.cu", "cache.cu", "em.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

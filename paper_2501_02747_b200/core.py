@@ -445,6 +445,52 @@ def load_matrix_cache(scene: Scene, path: str):
     return bits, tri[: nt.value], mo.value
 
 
+def ray_gains(scene: Scene, paths: Sequence[dict], materials, edges: Sequence[dict] = (),
+              edge_faces: Sequence[Sequence[int]] = (), frequency: float = 5.5e9, tx_gain_dbi: float = 0.0,
+              rx_gain_dbi: float = 0.0, polarization: str = "TE"):
+    """rt::ray_gains (include/rt/em.hpp:92-96) on the GPU for a list of paths
+    (the dicts Tracer.trace returns). materials: [nfaces][2] (permittivity,
+    conductivity). Returns (complex amplitudes, delays)."""
+    n = len(paths)
+    arr = (_capi.visrt_path * max(n, 1))()
+    for q, p in enumerate(paths):
+        arr[q].nrefl = len(p["faces"])
+        for i, f in enumerate(p["faces"]):
+            arr[q].faces[i] = int(f)
+        arr[q].edge = int(p.get("edge", -1))
+        for i, v in enumerate(p["points"]):
+            arr[q].points[i] = float(v)
+        arr[q].length = float(p["length"])
+    mat = np.ascontiguousarray(np.asarray(materials, np.float64).reshape(-1, 2))
+    ab = np.ascontiguousarray(np.array([list(e["a"]) + list(e["b"]) for e in edges], np.float64).reshape(-1))
+    ef = np.ascontiguousarray(np.asarray(edge_faces, np.int32).reshape(-1))
+    cfg = _capi.visrt_em_config(frequency, tx_gain_dbi, rx_gain_dbi, 1 if polarization == "TM" else 0, 0)
+    amp = np.zeros(2 * max(n, 1), np.float64)
+    dl = np.zeros(max(n, 1), np.float64)
+    st = _capi.visrt_stats()
+    check(lib().visrt_ray_gains(scene.h, n, C.cast(arr, C.c_void_p), mat.reshape(-1), len(edges),
+                                ab.ctypes.data if len(ab) else None, ef.ctypes.data if len(ef) else None,
+                                C.byref(cfg), amp.ctypes.data, dl.ctypes.data, C.byref(st), None))
+    return amp[: 2 * n].view(np.complex128), dl[:n]
+
+
+def channel_stats(scene: Scene, amps: Sequence[np.ndarray], delays: Sequence[np.ndarray]):
+    """rt::channel_stats (include/rt/em.hpp:98-101) per snapshot on the GPU:
+    (outage, path_loss_db, rms_delay_spread) arrays."""
+    ns = len(amps)
+    off = np.zeros(ns + 1, np.int64)
+    off[1:] = np.cumsum([len(a) for a in amps])
+    amp = np.ascontiguousarray(np.concatenate([np.asarray(a, np.complex128) for a in amps]) if ns else np.zeros(0, np.complex128))
+    dl = np.ascontiguousarray(np.concatenate([np.asarray(d, np.float64) for d in delays]) if ns else np.zeros(0))
+    outage = np.zeros(max(ns, 1), np.int8)
+    loss = np.zeros(max(ns, 1), np.float64)
+    rms = np.zeros(max(ns, 1), np.float64)
+    check(lib().visrt_channel_stats(scene.h, ns, off, amp.ctypes.data if len(amp) else None,
+                                    dl.ctypes.data if len(dl) else None, outage.ctypes.data, loss.ctypes.data,
+                                    rms.ctypes.data, None))
+    return outage[:ns].astype(bool), loss[:ns], rms[:ns]
+
+
 def brute_force_trace(scene: Scene, tx, rx, max_refl: int, allow_diffraction: bool = False,
                       edges: Optional[Sequence[dict]] = None):
     """rt::brute_force_trace (include/rt/raytracer.hpp:78-83): the conventional

@@ -341,10 +341,12 @@ void Scene::finalize() {
 std::unique_ptr<Scene> Scene::from_facets(const std::vector<std::string>& ids,
                                           const std::vector<std::vector<Vec3>>& rings) {
     auto s = std::make_unique<Scene>();
+    s->materials.push_back({"concrete", 5.31, 0.139});   // the facet-soup convention (one wall material)
     s->soup_.reserve(ids.size());
     for (size_t i = 0; i < ids.size(); ++i) {
         Face f;
         f.id = ids[i];
+        f.material = "concrete";
         f.poly = ConvexPolygon::from_points(rings[i]);
         f.orientation = classify(f.poly.normal);
         f.index = static_cast<int>(i);
@@ -355,6 +357,12 @@ std::unique_ptr<Scene> Scene::from_facets(const std::vector<std::string>& ids,
         s->face_ptrs_.push_back(&f);
     }
     return s;
+}
+
+const Material& Scene::material(const std::string& name) const {   // src/scene.cpp:192-197
+    for (const Material& m : materials)
+        if (m.name == name) return m;
+    throw SceneError("unknown material '" + name + "'");
 }
 
 const Face& Scene::face(const std::string& id) const {
@@ -1063,6 +1071,90 @@ std::vector<ImageTreeNode> image_tree(const Scene& scene, const Vec3& source, in
         nd.depth = depth[k];
     }
     return out;
+}
+
+// ---------------------------------------------------------------------------
+// EM consumer (src/em.cpp:194-235) over the GPU kernels
+// ---------------------------------------------------------------------------
+std::vector<RayGain> ray_gains(const Scene& scene, const std::vector<Path>& paths, const EmConfig& config) {
+    if (config.frequency <= 0) throw EmError("frequency must be positive");
+    const size_t n = scene.faces().size();
+    std::vector<double> mat(2 * n);
+    for (size_t f = 0; f < n; ++f) {
+        const Material& m = scene.material(scene.face(static_cast<int>(f)).material);
+        mat[2 * f] = m.permittivity;
+        mat[2 * f + 1] = m.conductivity;
+    }
+    std::map<std::string, int> edge_index;
+    std::vector<double> ab;
+    std::vector<int32_t> ef;
+    for (const Edge& e : scene.edges()) {
+        edge_index.emplace(e.id, static_cast<int>(edge_index.size()));
+        ab.insert(ab.end(), {e.a.x, e.a.y, e.a.z, e.b.x, e.b.y, e.b.z});
+        ef.push_back(scene.face(e.faces[0]).index);
+        ef.push_back(scene.face(e.faces[1]).index);
+    }
+    std::vector<visrt_path> vp(paths.size());
+    for (size_t q = 0; q < paths.size(); ++q) {
+        const Path& p = paths[q];
+        visrt_path& o = vp[q];
+        std::memset(&o, 0, sizeof(o));
+        o.edge = -1;
+        for (const Interaction& ia : p.interactions) {
+            if (ia.kind == InteractionKind::Reflection) {
+                if (o.nrefl >= 4) throw EmError("paths carry at most four reflections");
+                o.faces[o.nrefl++] = scene.face(ia.id).index;
+            } else {
+                auto it = edge_index.find(ia.id);
+                if (it == edge_index.end()) throw EmError("path references unknown edge '" + ia.id + "'");
+                o.edge = it->second;
+            }
+        }
+        for (size_t i = 0; i < p.points.size() && i < 7; ++i) {
+            o.points[3 * i] = p.points[i].x;
+            o.points[3 * i + 1] = p.points[i].y;
+            o.points[3 * i + 2] = p.points[i].z;
+        }
+        o.length = p.length;
+    }
+    const visrt_em_config cfg{config.frequency, config.tx_gain_dbi, config.rx_gain_dbi,
+                              config.polarization == Polarization::TM ? 1 : 0, 0};
+    std::vector<double> amp(2 * paths.size() + 2), delay(paths.size() + 1);
+    visrt_stats st{};
+    const int rc = visrt_ray_gains(scene.device_scene(), static_cast<int64_t>(paths.size()), vp.data(), mat.data(),
+                                   static_cast<int32_t>(ef.size() / 2), ab.empty() ? nullptr : ab.data(),
+                                   ef.empty() ? nullptr : ef.data(), &cfg, amp.data(), delay.data(), &st, nullptr);
+    if (rc == VISRT_E_VISIBILITY) throw EmError(visrt_last_error());
+    check(rc);
+    std::vector<RayGain> rays;
+    for (size_t q = 0; q < paths.size(); ++q)
+        rays.push_back({{amp[2 * q], amp[2 * q + 1]}, delay[q], paths[q].identity()});
+    return rays;
+}
+
+ChannelStats channel_stats(const std::vector<RayGain>& rays) {   // src/em.cpp:209-235
+    ChannelStats stats;
+    stats.rays = rays;
+    if (rays.empty()) {
+        stats.outage = true;
+        return stats;
+    }
+    double power = 0.0, m1 = 0.0, m2 = 0.0;
+    for (const RayGain& r : rays) {
+        const double p = std::norm(r.amplitude);
+        power += p;
+        m1 += p * r.delay;
+        m2 += p * r.delay * r.delay;
+    }
+    if (power <= 0) {
+        stats.outage = true;
+        return stats;
+    }
+    stats.path_loss_db = -10.0 * std::log10(power);
+    m1 /= power;
+    m2 /= power;
+    stats.rms_delay_spread = std::sqrt(std::max(0.0, m2 - m1 * m1));
+    return stats;
 }
 
 }  // namespace rt

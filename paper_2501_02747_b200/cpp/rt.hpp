@@ -14,6 +14,8 @@
 
 #include <array>
 #include <cmath>
+#include <complex>
+#include <limits>
 #include <map>
 #include <memory>
 #include <optional>
@@ -95,10 +97,19 @@ struct PlaneSegment {
     Vec2 a, b, normal;
 };
 
+/// include/rt/scene.hpp:21-25
+struct Material {
+    std::string name;
+    double permittivity = 1.0;
+    double conductivity = 0.0;
+};
+
 class Scene {
   public:
+    std::vector<Material> materials;
     std::vector<Building> buildings;
     std::optional<Face> ground;
+    const Material& material(const std::string& name) const;
 
     Scene() = default;
     Scene(const Scene&) = delete;             // faces() holds pointers into the scene
@@ -310,5 +321,33 @@ class TraceAccelerator {
 /// method on the GPU tree (every face but the immediate repeat, no prune).
 std::vector<Path> brute_force_trace(const Scene& scene, const Vec3& tx, const Vec3& rx, int max_refl,
                                     bool allow_diffraction, TraceStats* stats = nullptr);
+
+// ---------------------------------------------------------------------------
+/// EM consumer (include/rt/em.hpp:14-103), GPU kernels with CUDA's
+/// transcendentals (tolerance-level agreement with the reference).
+class EmError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+enum class Polarization { TE, TM };
+struct EmConfig {
+    double frequency = 5.5e9;
+    double tx_gain_dbi = 0.0;
+    double rx_gain_dbi = 0.0;
+    Polarization polarization = Polarization::TE;
+};
+struct RayGain {
+    std::complex<double> amplitude;
+    double delay = 0.0;
+    std::string path_id;
+};
+struct ChannelStats {
+    bool outage = false;
+    double path_loss_db = std::numeric_limits<double>::infinity();
+    double rms_delay_spread = 0.0;
+    std::vector<RayGain> rays;
+};
+std::vector<RayGain> ray_gains(const Scene& scene, const std::vector<Path>& paths, const EmConfig& config);
+ChannelStats channel_stats(const std::vector<RayGain>& rays);
 
 }  // namespace rt

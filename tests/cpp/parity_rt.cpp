@@ -5,6 +5,7 @@
 //
 // Scene file:  nfaces nbuildings / building ids / per face: id b nv x y z ... /
 //              nsrc / sources / ntrace / tx ty tz rx ry rz / max_order
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -87,11 +88,13 @@ int main(int argc, char** argv) {
     void* ref = nullptr;
     if (nb > 0) {
         owned = std::make_unique<rt::Scene>();
+        owned->materials.push_back({"concrete", 5.31, 0.139});   // as vref_scene_from_shells
         owned->buildings.resize(nb);
         for (int b = 0; b < nb; ++b) owned->buildings[b].id = bids[b];
         for (int i = 0; i < n; ++i) {
             rt::Face f;
             f.id = ids[i];
+            f.material = "concrete";
             f.poly = rt::ConvexPolygon::from_points(rings[i]);
             if (bidx[i] >= 0) owned->buildings[bidx[i]].faces.push_back(std::move(f));
             else owned->ground = std::move(f);
@@ -297,6 +300,25 @@ int main(int argc, char** argv) {
             const double rx[3] = {trc.second.x, trc.second.y, trc.second.z};
             const int64_t np = vref_accel_trace(ref, RA, tx, rx, diff ? 1 : 0, rp.data(), 16384, rst);
             EXPECT(static_cast<int64_t>(paths.size()) == np, "path count order " << order << " trace " << t);
+            if (order <= 2 && static_cast<int64_t>(paths.size()) == np && np > 0) {
+                // EM consumer: GPU ray_gains vs the reference's, relative 1e-9
+                rt::EmConfig cfg;
+                cfg.frequency = 5.5e9;
+                cfg.polarization = (t % 2) ? rt::Polarization::TM : rt::Polarization::TE;
+                const auto rays = rt::ray_gains(*mine, paths, cfg);
+                std::vector<double> ramp(2 * np), rdl(np), rst3(3);
+                vref_trace_em(ref, RA, tx, rx, diff ? 1 : 0, cfg.frequency, 0.0, 0.0, (t % 2) ? 1 : 0, ramp.data(),
+                              rdl.data(), rst3.data(), np);
+                for (int64_t q = 0; q < np; ++q) {
+                    const std::complex<double> rr(ramp[2 * q], ramp[2 * q + 1]);
+                    EXPECT(std::abs(rays[static_cast<size_t>(q)].amplitude - rr) <= 1e-9 * std::abs(rr),
+                           "ray gain " << q << " " << rays[static_cast<size_t>(q)].path_id);
+                    EXPECT(rays[static_cast<size_t>(q)].delay == rdl[static_cast<size_t>(q)], "ray delay");
+                }
+                const rt::ChannelStats cs = rt::channel_stats(rays);
+                EXPECT(cs.outage == (rst3[0] != 0.0), "channel outage");
+                if (!cs.outage) EXPECT(std::abs(cs.path_loss_db - rst3[1]) <= 1e-9 * std::abs(rst3[1]), "path loss");
+            }
             EXPECT(st.nodes_expanded == rst[0] && st.sequences_checked == rst[1], "trace stats " << order << "," << t);
             for (int64_t q = 0; q < np && q < static_cast<int64_t>(paths.size()); ++q) {
                 const rt::Path& p = paths[static_cast<size_t>(q)];
