@@ -448,8 +448,49 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // arithmetic, same call order, so every output is bit-identical to K4 — with
 // converged lanes and a short per-region critical path (small batches and
 // trajectory probes are latency-bound on K4's lane state machines).
+// col_vis (src/vistable.cpp:146-159) for the warp kernel: warp-uniform
+// arithmetic, one warp-cooperative sweep per transverse sample. Out of line:
+// it has three call sites (scan, both refine directions) and inlining them
+// blew the instruction cache (ncu: stall_no_inst dominated).
+template <int MAXV>
+__device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx, const double* us, int nv, int pl,
+                                          double ax, double ay, double dx, double dy, double u, double sx,
+                                          double sy, double sz, int sf, unsigned char* sv, int& cache,
+                                          unsigned long long& tests, unsigned long long& queries,
+                                          unsigned long long& batches) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    const int lane = threadIdx.x & 31;
+    const double cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
+    double cs0, cs1;
+    if (!column_span_us(us, nv, cu, cs0, cs1)) return false;
+    const double inset = dmul(dsub(cs1, cs0), 1e-6);
+    const double px = dadd(ax, dmul(dx, cu));
+    const double py = dadd(ay, dmul(dy, cu));
+    for (int j = 0; j < 7; ++j) {
+        const double sv_ = dmin_std(dsub(cs1, inset),
+                                    dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
+        double qx, qy, qz;
+        if (pl == 0) { qx = px; qy = py; qz = sv_; }
+        else if (pl == 1) { qx = sv_; qy = px; qz = py; }
+        else { qx = px; qy = sv_; qz = py; }
+        ++queries;
+        if (cache >= 0 && cache != sf) {
+            tests += lane == 0;   // warp-uniform test: count it once
+            if (seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * STRIDE, sx, sy, sz, qx, qy, qz)) continue;
+        }
+        const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz, qx, qy, qz, sf,
+                                         -1, sf, sv, tests, batches);
+        if (h < 0) return true;
+        cache = h;
+    }
+    return false;
+}
+
+#ifndef VISRT_K4W_MINB
+#define VISRT_K4W_MINB 2
+#endif
 template <int MAXV, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads, 2) k_point_regions_warp(RegionArgs a) {
+__global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp(RegionArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
@@ -503,34 +544,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions_warp(RegionArgs a
             for (int q = 0; q < nv; ++q) face_us(s, f, pl, q, ax, ay, dx, dy, len2, us[2 * q], us[2 * q + 1]);
             // col_vis (src/vistable.cpp:146-159)
             auto col_vis = [&](double u) -> bool {
-                const double cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
-                double cs0, cs1;
-                if (!column_span_us(us, nv, cu, cs0, cs1)) return false;
-                const double inset = dmul(dsub(cs1, cs0), 1e-6);
-                const double px = dadd(ax, dmul(dx, cu));
-                const double py = dadd(ay, dmul(dy, cu));
-                for (int j = 0; j < 7; ++j) {
-                    const double sv_ = dmin_std(dsub(cs1, inset),
-                                                dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
-                    double qx, qy, qz;
-                    if (pl == 0) { qx = px; qy = py; qz = sv_; }
-                    else if (pl == 1) { qx = sv_; qy = px; qz = py; }
-                    else { qx = px; qy = sv_; qz = py; }
-                    ++queries;
-                    if (cache >= 0 && cache != sf) {
-                        tests += lane == 0;   // warp-uniform test: count it once
-                        if (seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * STRIDE, sx, sy, sz, qx, qy, qz))
-                            continue;
-                    }
-#ifndef VISRT_K4W_FIRST
-#define VISRT_K4W_FIRST 0
-#endif
-                    const int h = coop_any_hit<MAXV, VISRT_K4W_FIRST>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz,
-                                                     qx, qy, qz, sf, -1, sf, sv, tests, batches);
-                    if (h < 0) return true;
-                    cache = h;
-                }
-                return false;
+                return col_vis_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, u, sx, sy, sz, sf, sv, cache, tests,
+                                          queries, batches);
             };
             unsigned long long vis = 0;
             bool vis64 = false;
@@ -630,7 +645,7 @@ static cudaError_t launch_regions_t(const RegionArgs& a, int device, cudaStream_
     }();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const bool warp = force >= 0 ? force == 1 : a.ntasks < 2ll * sms * 2 * kThreads;
+    const bool warp = force >= 0 ? force == 1 : true;   // K4w measured faster at every size since r01
     if (warp)
         return res ? launch_r(k_point_regions_warp<MAXV, true>, smem, a, device, st)
                    : launch_r(k_point_regions_warp<MAXV, false>, smem, a, device, st);
