@@ -21,11 +21,15 @@
 //     string orders of the reference's SigKey / row sorts supplied as ranks
 //     (visrt_names), so tie-breaking matches std::set / std::sort exactly.
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <iterator>
 #include <map>
 #include <tuple>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -484,6 +488,19 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
                                                const std::vector<visrt_entry>& entries, int max_order,
                                                const visrt_names& nm, visrt_stats& stats) {
     const int n = hs.n;
+    // VISRT_TRAJ_PROFILE=1: host wall time per phase on stderr (development aid)
+    static const bool prof = [] {
+        const char* e = std::getenv("VISRT_TRAJ_PROFILE");
+        return e && e[0] == '1';
+    }();
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+        if (!prof) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[traj] %-10s %8.2f ms\n", name,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     const double length = route.total_length();
     auto pos = [&](double s, std::vector<double>& out) {
         double p[3];
@@ -496,37 +513,49 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
     };
 
     // ---- MobileSampler ctor (src/vistable.cpp:699-716): keys and chains ----
-    std::map<std::array<int, 4>, int> chain_id;   // reflectors (-1 padded) -> id
+    // hash maps on packed 16-bit face slots (faces < 65536 is checked by the caller)
+    std::unordered_map<uint64_t, int> chain_id;   // reflectors (-1 padded) -> id
     std::vector<visrt_entry> chains;              // as K5 entries (order = #reflectors)
     std::vector<KeyDef> keys;
-    std::map<std::tuple<int, int, int>, int> face_key;   // (order, parent, node) -> keys index
+    std::unordered_map<uint64_t, int> face_key;   // (order, parent, node) -> keys index
     std::vector<std::vector<int>> key_chains;
+    auto slot16 = [](int f) { return static_cast<uint64_t>(static_cast<uint16_t>(f)); };   // -1 -> 0xFFFF
+    uint64_t last_refl = ~0ull;
+    int last_c = -1, last_k = -1;
     for (const visrt_entry& e : entries) {
         if (e.order > max_order) continue;
         const int L = e.order;   // reflectors chain[0..L-1]
-        std::array<int, 4> refl{-1, -1, -1, -1};
-        for (int q = 0; q < L; ++q) refl[q] = e.chain[q];
-        auto ci = chain_id.find(refl);
-        int c;
-        if (ci == chain_id.end()) {
-            c = static_cast<int>(chains.size());
-            chain_id[refl] = c;
-            visrt_entry ce = e;   // the K5 query: same reflectors (the aim and plane are not read for reach)
-            ce.plane = 0;
-            chains.push_back(ce);
+        uint64_t rk = 0;
+        for (int q = 0; q < 4; ++q) rk = (rk << 16) | slot16(q < L ? e.chain[q] : -1);
+        int c, k;
+        if (rk == last_refl) {   // consecutive entries of one chain (planes, aims): no lookups
+            c = last_c;
+            k = last_k;
         } else {
-            c = ci->second;
-        }
-        const KeyDef kd{L, L >= 2 ? refl[L - 2] : -1, refl[L - 1], -1};
-        auto it = face_key.find({kd.order, kd.parent, kd.node});
-        int k;
-        if (it == face_key.end()) {
-            k = static_cast<int>(keys.size());
-            face_key[{kd.order, kd.parent, kd.node}] = k;
-            keys.push_back(kd);
-            key_chains.emplace_back();
-        } else {
-            k = it->second;
+            auto ci = chain_id.find(rk);
+            if (ci == chain_id.end()) {
+                c = static_cast<int>(chains.size());
+                chain_id.emplace(rk, c);
+                visrt_entry ce = e;   // the K5 query: same reflectors (the aim and plane are not read for reach)
+                ce.plane = 0;
+                chains.push_back(ce);
+            } else {
+                c = ci->second;
+            }
+            const KeyDef kd{L, L >= 2 ? e.chain[L - 2] : -1, e.chain[L - 1], -1};
+            const uint64_t kk = (static_cast<uint64_t>(L) << 32) | (slot16(kd.parent) << 16) | slot16(kd.node);
+            auto it = face_key.find(kk);
+            if (it == face_key.end()) {
+                k = static_cast<int>(keys.size());
+                face_key.emplace(kk, k);
+                keys.push_back(kd);
+                key_chains.emplace_back();
+            } else {
+                k = it->second;
+            }
+            last_refl = rk;
+            last_c = c;
+            last_k = k;
         }
         if (std::find(key_chains[k].begin(), key_chains[k].end(), c) == key_chains[k].end())
             key_chains[k].push_back(c);
@@ -558,6 +587,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
     std::stable_sort(by_rank.begin(), by_rank.end(), [&](int a, int b) { return key_less(keys[a], keys[b]); });
     for (int r = 0; r < nk; ++r) order_of[by_rank[r]] = r;   // key -> position in SigKey order
 
+    phase("keys");
     // ---- sampling pass (src/vistable.cpp:846-866) --------------------------
     std::vector<double> samples;
     for (double s = 0.0; s < length; s += kStep) samples.push_back(s);
@@ -568,15 +598,21 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
     for (double s : samples) pos(s, P);
     int words = 0;
     const std::vector<uint32_t> rbits = gpu.reach_dense(P, chains, words);
-    auto reached = [&](int i, int c) { return (rbits[static_cast<size_t>(i) * words + (c >> 5)] >> (c & 31)) & 1u; };
     std::vector<std::vector<int>> snaps(ns);   // SigKey-ordered positions
     std::vector<double> VA, VB;
     std::vector<std::pair<int, int>> vseg;     // (sample, key)
+    std::vector<int> key_of_chain(chains.size(), -1);   // a chain's reflectors fix its key
+    for (int k = 0; k < nface_keys; ++k)
+        for (int c : key_chains[k]) key_of_chain[c] = k;
+    std::vector<int> ks;
     for (int i = 0; i < ns; ++i) {
-        for (int k = 0; k < nface_keys; ++k) {
-            bool in = false;
-            for (int c : key_chains[k]) in = in || reached(i, c);
-            if (!in) continue;
+        ks.clear();
+        for (int w = 0; w < words; ++w)
+            for (uint32_t b = rbits[static_cast<size_t>(i) * words + w]; b; b &= b - 1)
+                ks.push_back(key_of_chain[32 * w + __builtin_ctz(b)]);
+        std::sort(ks.begin(), ks.end());
+        ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+        for (int k : ks) {
             snaps[i].push_back(order_of[k]);
             if (keys[k].order == 1)
                 for (int v = 0; v < hs.nv[keys[k].node]; ++v) {
@@ -591,6 +627,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
         if (vclear[q]) snaps[vseg[q].first].push_back(order_of[vseg[q].second]);
     for (auto& sn : snaps) std::sort(sn.begin(), sn.end());
 
+    phase("sampling");
     // ---- boundaries: lockstep bisection (src/vistable.cpp:868-885) -------
     std::vector<Event> events;
     for (int i = 0; i + 1 < ns; ++i) {
@@ -660,6 +697,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
         }
     }
 
+    phase("bisection");
     // ---- classify (src/vistable.cpp:770-812), batched ----------------------
     const size_t ne = events.size();
     std::vector<double> pm(3 * ne), po(3 * ne);   // p_member, p_other
@@ -775,6 +813,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
         ev.blockage = fresh.empty() ? -1 : fresh.front();
     }
 
+    phase("classify");
     // ---- labels (src/vistable.cpp:887-898) --------------------------------
     std::stable_sort(events.begin(), events.end(), [](const Event& a, const Event& b) {
         if (a.vertical != b.vertical) return a.vertical > b.vertical;
@@ -785,11 +824,21 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
     std::sort(events.begin(), events.end(), [](const Event& a, const Event& b) { return a.s < b.s; });
 
     // ---- per-node ranges (900-940) ------------------------------------------
-    std::vector<int> all;   // SigKey positions
-    for (const auto& sn : snaps) all.insert(all.end(), sn.begin(), sn.end());
-    for (const Event& ev : events) all.push_back(order_of[ev.key]);
-    std::sort(all.begin(), all.end());
-    all.erase(std::unique(all.begin(), all.end()), all.end());
+    std::vector<char> seen(static_cast<size_t>(nk), 0);   // all_keys as a mark per SigKey position
+    for (const auto& sn : snaps)
+        for (int r : sn) seen[r] = 1;
+    for (const Event& ev : events) seen[order_of[ev.key]] = 1;
+    std::vector<int> all;   // SigKey positions, ascending
+    for (int r = 0; r < nk; ++r)
+        if (seen[r]) all.push_back(r);
+    // each key's events in s order (the reference scans all events per key)
+    std::vector<int> ev_first(keys.size() + 1, 0), ev_list(events.size());
+    for (const Event& ev : events) ++ev_first[ev.key + 1];
+    for (size_t k = 0; k < keys.size(); ++k) ev_first[k + 1] += ev_first[k];
+    {
+        std::vector<int> fill(ev_first.begin(), ev_first.end() - 1);
+        for (int e = 0; e < static_cast<int>(events.size()); ++e) ev_list[fill[events[e].key]++] = e;
+    }
     std::vector<visrt_mobile_row> table;
     for (int r : all) {
         const int k = by_rank[r];
@@ -812,8 +861,8 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
             row.blockage = open_block != -1 ? open_block : end_block;
             table.push_back(row);
         };
-        for (const Event& ev : events) {
-            if (ev.key != k) continue;
+        for (int qi = ev_first[k]; qi < ev_first[k + 1]; ++qi) {
+            const Event& ev = events[ev_list[qi]];
             if (ev.appearing) {
                 if (!open) {
                     open = true;
@@ -830,6 +879,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
         if (open) close_range(length, 0, 0, -1);
     }
 
+    phase("ranges");
     // ---- merge touching ranges (942-960) ------------------------------------
     auto par = [&](const visrt_mobile_row& r) { return r.parent < 0 ? nm.parent_rank[n] : nm.parent_rank[r.parent]; };
     auto nod = [&](const visrt_mobile_row& r) {
@@ -855,6 +905,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
         }
         merged.push_back(row);
     }
+    phase("merge");
     stats.pairs = ns;
     stats.candidates = static_cast<int64_t>(events.size());
     stats.admitted = static_cast<int64_t>(merged.size());
@@ -907,6 +958,7 @@ extern "C" int visrt_trajectory_table(visrt_scene* sc, int32_t nwp, const double
             throw visrt::UsageError("visrt_names: every rank array is required");
         if (max_order < 1 || max_order > 4)
             throw visrt::UsageError("trajectory tables cover max_order 1..4");
+        if (ds.n >= 65535) throw visrt::UsageError("trajectory tables index faces in 16 bits");
         for (int64_t e = 0; e < nent; ++e) {
             if (entries[e].order < 1 || entries[e].order > 4) continue;
             for (int c = 0; c <= entries[e].order; ++c)
