@@ -256,6 +256,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_MULTI
 #define VISRT_K2W_MULTI 2     // extra blockers of the swept sightline used to settle its siblings (1 or 2)
 #endif
+#ifndef VISRT_K2W_NOSAT
+#define VISRT_K2W_NOSAT 0   // 1: member boxes not culled, every member of a candidate tile runs the exact test
+#endif
 #ifndef VISRT_K2W_MORTON
 #define VISRT_K2W_MORTON 0
 #endif
@@ -397,9 +400,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                     const int mc = min(kTile, n - base);
                     const int m0 = base + lane, m1 = base + lane + 32;
                     const bool v0 = lane < mc && m0 != si && m0 != sj &&
-                                    sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g);
+                                    (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g));
                     const bool v1 = lane + 32 < mc && m1 != si && m1 != sj &&
-                                    sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g);
+                                    (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g));
                     const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
                     ++batches;
                     const int clo = __popc(lo), tot = clo + __popc(hi);
