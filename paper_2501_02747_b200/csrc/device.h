@@ -83,13 +83,6 @@ struct PairArgs {
     int8_t* kind;                    // detail: per pair 0/1/2
     uint32_t* blk_mask;              // detail: per pair ceil(N/32) words
     int32_t blk_words;
-    // two-phase bits: phase 1 sweeps the centroid sightline only and writes
-    // first_blk[pair] = its blocker (Morton index) or -1 when the pair is decided
-    int32_t* first_blk;
-    // phase 2: pending pairs (indices into the pair space) + their phase-1 blocker
-    const long long* pend;
-    const int32_t* pend_blk;
-    long long npend;
 };
 
 // ---------------------------------------------------------------------------

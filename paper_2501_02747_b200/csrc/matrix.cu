@@ -12,8 +12,8 @@
 //                    sightline; a found blocker settles every other sightline
 //                    it blocks. A pair stops at its first clear (or degenerate)
 //                    sightline.
-//   K2 k_pair_bits   the same bit with one LANE per pair state machine
-//                    (VISRT_K2_WARP=0; kept for A/B).
+//   K2 k_pair_bits   the same bit with one LANE per pair state machine and
+//                    per-lane culled sweeps (VISRT_K2_WARP=0; kept for A/B).
 //   K2d k_pair_detail Visible / Partial / Occluded + blocker sets (no early exit).
 //
 // All geometry is the reference's FP64 predicate with explicit _rn intrinsics
