@@ -148,6 +148,10 @@ int visrt_point_tables(visrt_scene* scene, int64_t nsrc, const double* src_xyz, 
 int visrt_segments_clear(visrt_scene* scene, int64_t nseg, const double* a_xyz, const double* b_xyz,
                          uint8_t* clear, visrt_stats* stats, void* stream);
 
+/* chain_triple_feasible(original, mid, test) (include/rt/vismatrix.hpp:131,
+ * src/vismatrix.cpp:457-476) for an explicit list of face triples. */
+int visrt_triples_feasible(visrt_scene* scene, int64_t n, const int32_t* triples, uint8_t* feasible, void* stream);
+
 /* TableBuilder::reach for a query list (src/vistable.cpp:404-430, 432-467):
  * query q = (source src_xyz[q], reflector chain chains[q].chain[0..order-1],
  * order 1..4; chain[order] and plane name an entry whose plane decides

@@ -261,6 +261,13 @@ int32_t vref_required_planes(void* h, int32_t i, int32_t j) {
 // chain_triple_feasible / required_planes / second_order_check. The matrix
 // second_order_check consults only needs the two order-1 legs, so a minimal
 // one with those entries stands in for the full build.
+// chain_triple_feasible alone (proj/src/vismatrix.cpp:457-476)
+int32_t vref_chain_triple_feasible(void* h, int32_t p, int32_t t, int32_t a) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    return R::chain_triple_feasible(s.face(p), s.face(t), s.face(a)) ? 1 : 0;
+}
+
+// the K7 filter: chain_triple_feasible and second_order_check != None per shared plane
 int32_t vref_triple_feasible(void* h, int32_t p, int32_t t, int32_t a) {
     try {
         const R::Scene& s = static_cast<RefScene*>(h)->scene;

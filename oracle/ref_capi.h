@@ -92,6 +92,10 @@ int64_t vref_point_vis_table(void* h, void* m, const double* src, int32_t max_or
 int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, int32_t max_order,
                               vref_mobile_row* rows, int64_t cap);
 int32_t vref_closest_edge(void* h, const double* rx);
+int32_t vref_mutually_front(void* h, int32_t i, int32_t j);
+int32_t vref_required_planes(void* h, int32_t i, int32_t j);
+int32_t vref_triple_feasible(void* h, int32_t p, int32_t t, int32_t a);
+int32_t vref_chain_triple_feasible(void* h, int32_t p, int32_t t, int32_t a);
 int64_t vref_trace_em(void* h, void* a, const double* tx, const double* rx, int32_t diffraction, double freq,
                       double tx_gain, double rx_gain, int32_t tm, double* amp, double* delay, double* stats3,
                       int64_t cap);

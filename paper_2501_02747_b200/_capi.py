@@ -33,6 +33,7 @@ EXPORTS = [
     "visrt_tracer_destroy", "visrt_trace", "visrt_trace_results", "visrt_image_tree", "visrt_closest_edges",
     "visrt_tracer_set_edges", "visrt_trace_snapshot_edges", "visrt_resolve_keys",
     "visrt_cache_save", "visrt_cache_load", "visrt_ray_gains", "visrt_channel_stats",
+    "visrt_triples_feasible",
 ]
 
 VISRT_PAIRS_ALL = 0x1
@@ -165,6 +166,7 @@ def lib():
                                   C.c_void_p]
     L.visrt_channel_stats.argtypes = [C.c_void_p, C.c_int64, _i64p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p]
+    L.visrt_triples_feasible.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
     L.visrt_cache_save.argtypes = [C.c_char_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]
     L.visrt_cache_load.argtypes = [C.c_char_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_int64,
                                    C.POINTER(C.c_int64)]

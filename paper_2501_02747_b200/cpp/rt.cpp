@@ -5,6 +5,8 @@
 #include "rt.hpp"
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <set>
 #include <unordered_set>
@@ -269,7 +271,30 @@ ConvexPolygon ConvexPolygon::from_points(std::vector<Vec3> pts) {
     return p;
 }
 
+namespace {
+// Face -> owning Scene, for the reference's scene-less predicates that need
+// the device scene (chain_triple_feasible)
+std::mutex g_owner_mu;
+std::unordered_map<const Face*, const Scene*> g_owner;
+void register_faces(const Scene* sc, const std::vector<const Face*>& faces) {
+    std::lock_guard<std::mutex> lk(g_owner_mu);
+    for (const Face* f : faces) g_owner[f] = sc;
+}
+const Scene* owner_of(const Face& f) {
+    std::lock_guard<std::mutex> lk(g_owner_mu);
+    auto it = g_owner.find(&f);
+    return it == g_owner.end() ? nullptr : it->second;
+}
+}  // namespace
+
 Scene::~Scene() {
+    {
+        std::lock_guard<std::mutex> lk(g_owner_mu);
+        for (const Face* f : face_ptrs_) {
+            auto it = g_owner.find(f);
+            if (it != g_owner.end() && it->second == this) g_owner.erase(it);
+        }
+    }
     if (dev_) visrt_scene_destroy(dev_);
 }
 
@@ -336,6 +361,7 @@ void Scene::finalize() {
         reg(*ground);
     }
     if (face_ptrs_.empty()) throw SceneError("scene has no faces");
+    register_faces(this, face_ptrs_);
 }
 
 std::unique_ptr<Scene> Scene::from_facets(const std::vector<std::string>& ids,
@@ -356,6 +382,7 @@ std::unique_ptr<Scene> Scene::from_facets(const std::vector<std::string>& ids,
         s->face_index_[f.id] = f.index;
         s->face_ptrs_.push_back(&f);
     }
+    register_faces(s.get(), s->face_ptrs_);
     return s;
 }
 
@@ -1071,6 +1098,108 @@ std::vector<ImageTreeNode> image_tree(const Scene& scene, const Vec3& source, in
         nd.depth = depth[k];
     }
     return out;
+}
+
+// ---------------------------------------------------------------------------
+// Public single-pair predicates (src/vismatrix.cpp:160-225, 387-476)
+// ---------------------------------------------------------------------------
+bool mutually_front(const Face& a, const Face& b) {
+    auto has_front_point = [](const Face& of, const Face& probe) {
+        for (const Vec3& p : probe.poly.pts)
+            if (signed_distance(of, p) > kEps) return true;
+        return false;
+    };
+    return has_front_point(a, b) && has_front_point(b, a);
+}
+
+std::vector<PlaneTag> required_planes(const Face& ref, const Face& aim) {
+    std::vector<PlaneTag> out;
+    for (PlaneTag tag : {PlaneTag::XY, PlaneTag::YZ, PlaneTag::XZ}) {
+        const auto sr = plane_segment(ref, tag);
+        const auto sa = plane_segment(aim, tag);
+        if (!sr || !sa) continue;
+        const double d = std::abs(dot2(sr->normal, sa->normal));
+        if (d >= 1.0 - 1e-9 || d <= 1e-9) out.push_back(tag);
+    }
+    return out;
+}
+
+namespace {
+const char* plane_name(PlaneTag p) { return p == PlaneTag::XY ? "XY" : (p == PlaneTag::YZ ? "YZ" : "XZ"); }
+}  // namespace
+
+InterfaceRelation classify_relation_in_plane(const Face& ref, const Face& aim, PlaneTag plane) {
+    const auto sr = plane_segment(ref, plane);
+    const auto sa = plane_segment(aim, plane);
+    if (!sr || !sa)
+        throw VisibilityError("faces '" + ref.id + "' and '" + aim.id + "' do not both project to segments in plane " +
+                              plane_name(plane));
+    const double d = std::abs(dot2(sr->normal, sa->normal));
+    InterfaceRelation rel;
+    rel.plane = plane;
+    rel.chain = {ref.id, aim.id};
+    rel.chain_orientations = {ref.orientation, aim.orientation};
+    if (d >= 1.0 - 1e-9) rel.kind = RelationKind::Parallel;
+    else if (d <= 1e-9) rel.kind = RelationKind::Perpendicular;
+    else
+        throw VisibilityError("faces '" + ref.id + "' and '" + aim.id +
+                              "' are neither parallel nor perpendicular in plane " + plane_name(plane));
+    return rel;
+}
+
+InterfaceRelation classify_relation(const Face& ref, const Face& aim) {
+    if (ref.id == aim.id) throw VisibilityError("reference and aim face must differ (got '" + ref.id + "')");
+    if (ref.orientation == Orientation::Oblique || aim.orientation == Orientation::Oblique)
+        throw VisibilityError("unsupported relation: face pair ('" + ref.id + "', '" + aim.id +
+                              "') involves an oblique face");
+    const auto planes = required_planes(ref, aim);
+    if (planes.empty())
+        throw VisibilityError("unsupported relation: faces '" + ref.id + "' and '" + aim.id +
+                              "' share no working plane");
+    return classify_relation_in_plane(ref, aim, planes.front());
+}
+
+SecondOrderResult second_order_check(const Face& original, const Face& mid, const Face& test,
+                                     const InterVisMatrix& matrix, PlaneTag plane) {
+    if (!matrix.find(1, original.id, mid.id, plane) || !matrix.find(1, mid.id, test.id, plane))
+        throw VisibilityError("second-order check needs first-order entries for ('" + original.id + "','" + mid.id +
+                              "') and ('" + mid.id + "','" + test.id + "') in plane " + plane_name(plane));
+    const auto so = plane_segment(original, plane), sm = plane_segment(mid, plane), st = plane_segment(test, plane);
+    if (!so || !sm || !st)
+        throw VisibilityError(std::string("second-order check: missing segment projection in plane ") +
+                              plane_name(plane));
+    Segs segs;   // the three segments as a 3-face table
+    segs.seg.assign(18 * 3, 0.0);
+    segs.ok.assign(9, 0);
+    const PlaneSegment* ps[3] = {&*so, &*sm, &*st};
+    const int pl = static_cast<int>(plane);
+    for (int f = 0; f < 3; ++f) {
+        double* d = &segs.seg[(static_cast<size_t>(f) * 3 + pl) * 6];
+        d[0] = ps[f]->a.x; d[1] = ps[f]->a.y; d[2] = ps[f]->b.x; d[3] = ps[f]->b.y;
+        d[4] = ps[f]->normal.x; d[5] = ps[f]->normal.y;
+        segs.ok[3 * f + pl] = 1;
+    }
+    ISet reach;
+    SecondOrderResult r;
+    r.verdict = second_order(segs, 0, 1, 2, plane, reach);
+    if (r.verdict == ChainVerdict::Partial) r.reachable.assign(reach.begin(), reach.end());
+    return r;
+}
+
+bool chain_triple_feasible(const Face& original, const Face& mid, const Face& test) {
+    const Scene* sc = owner_of(mid);
+    if (!sc || owner_of(original) != sc || owner_of(test) != sc)
+        throw std::invalid_argument("chain_triple_feasible: faces must belong to one finalized rt::Scene");
+    const int32_t t[3] = {original.index, mid.index, test.index};
+    uint8_t ok = 0;
+    check(visrt_triples_feasible(sc->device_scene(), 1, t, &ok, nullptr));
+    return ok != 0;
+}
+
+std::vector<Path> accelerated_trace(const Scene& scene, const InterVisMatrix& matrix, const Vec3& tx, const Vec3& rx,
+                                    int max_refl, bool allow_diffraction, TraceStats* stats) {
+    const TraceAccelerator accel(scene, matrix, max_refl);
+    return accel.trace(tx, rx, allow_diffraction, stats);
 }
 
 // ---------------------------------------------------------------------------

@@ -3,7 +3,8 @@
 // top of the C-ABI (include/visrt.h). Same names, argument meaning and
 // exception types/messages for:
 //   Scene / Face / Building / plane_segment          include/rt/scene.hpp:38-106
-//   occlusion_judgment, build_matrix, InterVisMatrix include/rt/vismatrix.hpp:37-141
+//   occlusion_judgment, build_matrix, InterVisMatrix, mutually_front, required_planes,
+//   classify_relation(_in_plane), second_order_check, chain_triple_feasible  include/rt/vismatrix.hpp:37-153
 //   illuminated_region                                include/rt/vistable.hpp:116-117
 //   TraceAccelerator / Path / TraceStats / image_tree include/rt/raytracer.hpp:25-118
 //   point_vis_table, trajectory_vis_table, closest_diffraction_edge  include/rt/vistable.hpp:62-148
@@ -194,6 +195,21 @@ class InterVisMatrix {
 };
 
 OcclusionVerdict occlusion_judgment(const Face& ref, const Face& aim, const Scene& scene);
+
+/// Public predicates of include/rt/vismatrix.hpp:105-153 (single-pair helpers
+/// of the matrix builder; the builder itself runs them batched on the GPU).
+bool mutually_front(const Face& a, const Face& b);
+std::vector<PlaneTag> required_planes(const Face& ref, const Face& aim);
+InterfaceRelation classify_relation_in_plane(const Face& ref, const Face& aim, PlaneTag plane);
+InterfaceRelation classify_relation(const Face& ref, const Face& aim);
+struct SecondOrderResult {
+    ChainVerdict verdict = ChainVerdict::None;
+    std::vector<std::array<double, 2>> reachable;
+};
+SecondOrderResult second_order_check(const Face& original, const Face& mid, const Face& test,
+                                     const InterVisMatrix& matrix, PlaneTag plane);
+/// GPU (K7's exact predicate); the faces must belong to a finalized rt::Scene.
+bool chain_triple_feasible(const Face& original, const Face& mid, const Face& test);
 InterVisMatrix build_matrix(const Scene& scene, int max_order);
 /// Binary matrix / pair-graph cache (replaces the text save_matrix /
 /// load_matrix of include/rt/vismatrix.hpp:143-144): admitted pairs + order-2
@@ -316,6 +332,11 @@ class TraceAccelerator {
     bool brute_ = false;
     visrt_tracer* tracer_ = nullptr;
 };
+
+/// accelerated_trace (include/rt/raytracer.hpp:121-124): one-shot TraceAccelerator.
+std::vector<Path> accelerated_trace(const Scene& scene, const InterVisMatrix& matrix, const Vec3& tx,
+                                    const Vec3& rx, int max_refl, bool allow_diffraction,
+                                    TraceStats* stats = nullptr);
 
 /// brute_force_trace (include/rt/raytracer.hpp:78-83): the unaccelerated image
 /// method on the GPU tree (every face but the immediate repeat, no prune).

@@ -412,6 +412,15 @@ __global__ void __launch_bounds__(128) k_chain_triples(ChainArgs a) {
     }
 }
 
+// chain_triple_feasible for an explicit triple list (the public predicate,
+// include/rt/vismatrix.hpp:131), thread per triple.
+template <int MAXV>
+__global__ void k_triples_feasible(DevScene s, long long n, const int32_t* t, uint8_t* out) {
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[k] = triple_feasible<MAXV>(s, t[3 * k], t[3 * k + 1], t[3 * k + 2]) ? 1 : 0;
+}
+
 __global__ void k_pack_triples(const int32_t* t, long long m, unsigned long long* key) {
     for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < m;
          k += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -570,5 +579,28 @@ extern "C" int visrt_chain_triples(visrt_scene* sc, const uint64_t* admitted_bit
             stats->tests_exec = total;
             stats->ms = ms;
         }
+    });
+}
+
+extern "C" int visrt_triples_feasible(visrt_scene* sc, int64_t n, const int32_t* triples, uint8_t* feasible,
+                                      void* stream) {
+    return visrt::capi_guard([&] {
+        visrt::ScopedDevice dev(sc);
+        const visrt::DevScene& ds = visrt::scene_dev(sc);
+        for (int64_t k = 0; k < 3 * n; ++k)
+            if (triples[k] < 0 || triples[k] >= ds.n) throw visrt::UsageError("bad face index");
+        if (n <= 0) return;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        std::vector<void*> tmp;
+        visrt::FreeGuard guard{tmp};
+        int32_t* d_t = visrt::dalloc<int32_t>(3 * n, tmp);
+        uint8_t* d_o = visrt::dalloc<uint8_t>(n, tmp);
+        ck(cudaMemcpyAsync(d_t, triples, 12 * n, cudaMemcpyHostToDevice, st), "H2D");
+        const int blocks = static_cast<int>(std::min<long long>((n + 127) / 128, 148 * 8));
+        if (ds.maxv <= 4) visrt::k_triples_feasible<4><<<blocks, 128, 0, st>>>(ds, n, d_t, d_o);
+        else visrt::k_triples_feasible<8><<<blocks, 128, 0, st>>>(ds, n, d_t, d_o);
+        ck(cudaGetLastError(), "k_triples_feasible");
+        ck(cudaMemcpyAsync(feasible, d_o, n, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
     });
 }

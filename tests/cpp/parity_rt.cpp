@@ -177,6 +177,28 @@ int main(int argc, char** argv) {
         std::cout << "matrix cache: " << MC.entries().size() << " entries re-derived" << std::endl;
     }
 
+    // --- public single-pair predicates ----------------------------------------
+    {
+        int npp = 0;
+        for (int i = 0; i < n; i += 3)
+            for (int j = 0; j < n; j += 7) {
+                if (i == j) continue;
+                const rt::Face& a = mine->face(i);
+                const rt::Face& b = mine->face(j);
+                EXPECT(rt::mutually_front(a, b) == (vref_mutually_front(ref, i, j) != 0), "mutually_front " << i << "," << j);
+                int m = 0;
+                for (rt::PlaneTag t : rt::required_planes(a, b)) m |= 1 << static_cast<int>(t);
+                EXPECT(m == vref_required_planes(ref, i, j), "required_planes " << i << "," << j);
+                const int c = (i + 2 * j + 1) % n;
+                if (c != i && c != j)
+                    EXPECT(rt::chain_triple_feasible(a, b, mine->face(c)) ==
+                               (vref_chain_triple_feasible(ref, i, j, c) != 0),
+                           "chain_triple_feasible " << i << "," << j << "," << c);
+                ++npp;
+            }
+        std::cout << "mutually_front / required_planes / chain_triple_feasible: " << npp << " cases compared" << std::endl;
+    }
+
     // --- occlusion_judgment (every 5th pair) -------------------------------
     int npj = 0;
     for (int i = 0; i < n; ++i)
