@@ -827,6 +827,45 @@ __global__ void __launch_bounds__(kThreads, 3) k_segments_clear(DevScene s, long
     if (lane == 0) atomicAdd(&counter[1], tests);
 }
 
+// Warp-per-segment variant (coop_any_hit), the default: converged culling and
+// exact phases like K2w / K4w.
+template <int MAXV, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads, 3) k_segments_clear_warp(DevScene s, long long nseg, const double* A,
+                                                                     const double* B, uint8_t* clear,
+                                                                     unsigned long long* counter) {
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
+    __shared__ unsigned char surv_buf[kThreads / 32][64];
+    const int lane = threadIdx.x & 31;
+    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    unsigned char* sv = surv_buf[threadIdx.x >> 5];
+    unsigned long long tests = 0, batches = 0;
+    int cache = -1;
+    for (;;) {
+        unsigned long long qw = 0;
+        if (lane == 0) qw = atomicAdd(&counter[0], 1ull);
+        const long long q = static_cast<long long>(__shfl_sync(kFull, qw, 0));
+        if (q >= nseg) break;
+        const double ax = A[3 * q], ay = A[3 * q + 1], az = A[3 * q + 2];
+        const double bx = B[3 * q], by = B[3 * q + 1], bz = B[3 * q + 2];
+        bool blocked = false;
+        if (cache >= 0) {
+            tests += lane == 0;
+            blocked = seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * RecLayout<MAXV>::kStride, ax, ay, az, bx,
+                                     by, bz);
+        }
+        if (!blocked) {
+            const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, ax, ay, az, bx, by, bz), ax, ay, az, bx, by,
+                                             bz, -1, -1, -1, sv, tests, batches);
+            blocked = h >= 0;
+            if (blocked) cache = h;
+        }
+        if (lane == 0) clear[q] = blocked ? 0 : 1;
+    }
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    if (lane == 0) atomicAdd(&counter[1], tests);
+}
+
 template <int MAXV>
 static cudaError_t launch_segments_t(const DevScene& s, long long nseg, const double* A, const double* B,
                                      uint8_t* clear, unsigned long long* ctr, int device, cudaStream_t st) {
@@ -840,6 +879,11 @@ static cudaError_t launch_segments_t(const DevScene& s, long long nseg, const do
                                                                                                        clear, ctr);
         return cudaGetLastError();
     };
+    static const bool lane_kernel = [] {
+        const char* w = std::getenv("VISRT_SEG_WARP");
+        return w && w[0] == '0';
+    }();
+    if (!lane_kernel) return res ? go(k_segments_clear_warp<MAXV, true>) : go(k_segments_clear_warp<MAXV, false>);
     return res ? go(k_segments_clear<MAXV, true>) : go(k_segments_clear<MAXV, false>);
 }
 
