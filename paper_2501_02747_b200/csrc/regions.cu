@@ -522,6 +522,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
         const int sf = s.inv[f];
         const int nv = s.nv[f];
         const double sx = a.src[3 * k], sy = a.src[3 * k + 1], sz = a.src[3 * k + 2];
+        const bool presence = a.presence_only ||
+                              (a.presence_of && a.task_face &&
+                               a.presence_of[a.paired ? t : t - k * static_cast<long long>(a.m)]);
         int8_t present = 1;
         int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
         double sub[6] = {0, 0, 0, 0, 0, 0};
@@ -547,6 +550,16 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
                 return col_vis_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, u, sx, sy, sz, sf, sv, cache, tests,
                                           queries, batches);
             };
+            if (presence) {   // a visible column <=> a non-empty interval list
+                bool any = false;
+                for (int i = 0; i < 65 && !any; ++i) any = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
+                if (!any) {
+                    present = 0;
+                    break;
+                }
+                has[pl] = 1;
+                continue;
+            }
             unsigned long long vis = 0;
             bool vis64 = false;
             for (int i = 0; i < 65; ++i) {
@@ -645,7 +658,7 @@ static cudaError_t launch_regions_t(const RegionArgs& a, int device, cudaStream_
     }();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const bool warp = force >= 0 ? force == 1 : true;   // K4w measured faster at every size since r01
+    const bool warp = a.presence_only || a.presence_of || (force >= 0 ? force == 1 : true);   // K4w: faster at every size
     if (warp)
         return res ? launch_r(k_point_regions_warp<MAXV, true>, smem, a, device, st)
                    : launch_r(k_point_regions_warp<MAXV, false>, smem, a, device, st);

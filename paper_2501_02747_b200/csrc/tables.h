@@ -22,6 +22,11 @@ struct RegionArgs {
     const int32_t* task_face = nullptr;
     int m = 0;
     int paired = 0;
+    // presence only (K4w): present = every plane with a face_param has a
+    // visible column (the scan stops at the first one; no refinement, no sub)
+    // — exactly whether illuminated_region returns a region
+    int presence_only = 0;
+    const uint8_t* presence_of = nullptr;   // per face-list entry (list mode) / per task (paired)
 };
 
 // K5 (TableBuilder::reach for order 1/2 chains). Dense: every (source k,

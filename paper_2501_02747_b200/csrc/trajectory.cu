@@ -262,8 +262,10 @@ struct Gpu {
 
     // TableBuilder::reach(chain) != nullopt for query list (src[q], chain q):
     // K4 region of the chain head (paired task mode) + K5 cascade.
+    // presence: order-1 queries only need whether the head has a region (K4w
+    // presence mode: the scan stops at the first visible column)
     std::vector<uint8_t> reach_paired(const std::vector<double>& src, const std::vector<visrt_entry>& q,
-                                      std::vector<uint8_t>* full = nullptr) {
+                                      std::vector<uint8_t>* full = nullptr, bool presence = false) {
         const long long nq = static_cast<long long>(q.size());
         std::vector<uint8_t> out(q.size(), 0);
         if (full) full->assign(q.size(), 0);
@@ -285,6 +287,11 @@ struct Gpu {
         ck(cudaMemsetAsync(d_ctr, 0, 32, st), "memset");
         Timed t(*this);
         RegionArgs ra{ds, nq, d_src, d_reg, d_ctr, d_face, 0, 1};
+        if (presence) {
+            std::vector<uint8_t> pres(q.size());
+            for (size_t k = 0; k < q.size(); ++k) pres[k] = q[k].order == 1 ? 1 : 0;
+            ra.presence_of = up(pres, tmp);
+        }
         ck(launch_point_regions(ra, device, st), "k_point_regions");
         BeamArgs ba{ds, 1, nq, d_src, d_reg, d_ent, d_rows, d_full, words, nullptr, 0, 1};
         ck(launch_beam_rows(ba, st), "k_beam_rows");
@@ -319,10 +326,15 @@ struct Gpu {
                 heads.push_back(e.chain[0]);
             }
         const long long m = static_cast<long long>(heads.size());
+        // heads whose chains are all single reflectors only need presence
+        std::vector<uint8_t> pres(heads.size(), 1);
+        for (const visrt_entry& e : chains)
+            if (e.order >= 2) pres[slot[e.chain[0]]] = 0;
         const long long batch = std::max<long long>(1, (1ll << 24) / m);   // <= 16.8 M regions (0.9 GB) per batch
         std::vector<void*> tmp;
         FreeGuard guard{tmp};
         int32_t* d_heads = up(heads, tmp);
+        uint8_t* d_pres = up(pres, tmp);
         int32_t* d_slot = up(slot, tmp);
         visrt_entry* d_ent = up(chains, tmp);
         const long long bs = std::min(batch, ns);
@@ -339,6 +351,7 @@ struct Gpu {
             ck(cudaMemsetAsync(d_ctr, 0, 32, st), "memset");
             Timed t(*this);
             RegionArgs ra{ds, nb * m, d_src, d_reg, d_ctr, d_heads, static_cast<int>(m), 0};
+            ra.presence_of = d_pres;
             ck(launch_point_regions(ra, device, st), "k_point_regions");
             BeamArgs ba{ds, nb, nc, d_src, d_reg, d_ent, d_rows, d_full, words, d_slot, static_cast<int>(m), 0};
             ck(launch_beam_rows(ba, st), "k_beam_rows");
@@ -664,7 +677,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
             }
         }
         const std::vector<uint8_t> sc = gpu.segs_clear(SA, SB);
-        const std::vector<uint8_t> rc = gpu.reach_paired(RS, RQ);
+        const std::vector<uint8_t> rc = gpu.reach_paired(RS, RQ, nullptr, true);
         std::vector<uint8_t> out(probes.size(), 0);
         for (size_t q = 0; q < probes.size(); ++q) {
             if (seg_of[q] >= 0) {
@@ -731,7 +744,7 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
             RS.insert(RS.end(), &po[3 * e], &po[3 * e] + 3);
         }
     }
-    const std::vector<uint8_t> rc = gpu.reach_paired(RS, RQ);
+    const std::vector<uint8_t> rc = gpu.reach_paired(RS, RQ, nullptr, true);
     // (b) plan-view membership + blocker segments
     std::vector<double> CP, CQ, MS;
     std::vector<int32_t> MC, skip;
