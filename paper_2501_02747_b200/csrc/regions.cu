@@ -16,6 +16,13 @@
 // Every sightline is one culled any-hit sweep (sweep.h) over all faces but
 // the target, with the 2-entry blocker cache. The lane's arithmetic follows
 // the reference operation by operation, so sub[] is bit-identical.
+//
+// K4w (k_point_regions_warp, the default since r01) runs the same algorithm
+// with a WARP per region as uniform straight-line code and one
+// warp-cooperative sweep (coop_any_hit) per sightline; it also has a
+// presence-only mode (scan until the first visible column) for callers that
+// only need whether a region exists (trajectory keys of order 1).
+// K5 (k_beam_rows): TableBuilder::reach through 1..4 reflectors.
 #include <cstdlib>
 
 #include "device.h"

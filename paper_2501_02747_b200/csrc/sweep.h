@@ -8,12 +8,14 @@
 //   * level 2: the 64 member boxes of each candidate tile -> survivor mask;
 //   * survivors run the exact FP64 predicate (device.h seg_hits) on records
 //     stored in the same Morton order.
-// Every lane runs its own sweep, but each warp iteration is ONE 64-box fp32
-// SAT batch for every active lane (level-1 chunk or level-2 tile, selected by
-// a per-lane pointer), so the hot loop stays converged; the short exact-test
-// tail is the only divergent part. Tile boxes always live in shared memory;
-// member boxes too when they fit (RESIDENT, N <= kResidentMaxBoxes), else they
-// are read through L1/L2. No block barrier after the one-time TMA staging.
+// Two traversals: per LANE (sweep_batch: every lane runs its own sweep, each
+// warp iteration one 64-box fp32 SAT batch for every active lane) and per
+// WARP (coop_any_hit: the 32 lanes split one segment's tile boxes, member
+// boxes and exact survivors — used by K2w, K4w and the segment kernels,
+// converged and with a short per-segment critical path). Tile boxes always
+// live in shared memory; member boxes too when they fit (RESIDENT,
+// N <= kResidentMaxBoxes), else they are read through L1/L2. No block barrier
+// after the one-time TMA staging.
 #pragma once
 
 #include "device.h"
