@@ -172,6 +172,25 @@ def secondary_measurements(stream: int):
             out[f"matrix_config{cfg}"] = {"B_ms": st["ms"], "B_tests_per_s": st["tests_alg"] / (st["ms"] * 1e-3),
                                           "A_ms": sa["ms"], "A_candidates": sa["candidates"],
                                           "facets": sc.n}
+    # config 4 / 5 geometry (22k facets): (B) matrix once, regions + order-3 trees of config-5 snapshots
+    wl5 = scenes.workload(5)
+    with Scene(wl5.scene) as sc:
+        _, st = sc.pair_visibility("all", copy_bits=False, stream=stream)
+        _, sa = sc.pair_visibility("prefiltered", copy_bits=False, stream=stream)
+        out["matrix_config4"] = {"B_ms": st["ms"], "B_tests_per_s": st["tests_alg"] / (st["ms"] * 1e-3),
+                                 "A_ms": sa["ms"], "A_candidates": sa["candidates"], "facets": sc.n,
+                                 "pairs": st["pairs"]}
+        src = np.concatenate([wl5.tx[:10], wl5.rx[:10]])
+        arr, st = point_regions_array(sc, src)
+        out["regions_config5"] = {"snapshots": len(src), "facets": sc.n, "ms": st["ms"],
+                                  "regions_per_s": arr.size / (st["ms"] * 1e-3), "ms_per_snapshot": st["ms"] / len(src)}
+        tri, _ = chain_triples(sc)
+        tr = Tracer(sc, 3, triples=tri)
+        tr.trace_raw(wl5.tx[:4], wl5.rx[:4])
+        _, _, nodes, tst = tr.trace_raw(wl5.tx[:200], wl5.rx[:200])
+        out["tree_config5_order3"] = {"snapshots": 200, "nodes": tst["nodes"], "ms": tst["ms"],
+                                      "ms_per_snapshot": tst["ms"] / 200, "paths": tst["paths"]}
+        tr.close()
     # (2) per-snapshot Tx/Rx -> facet regions, config 3 (Tx and Rx snapshots)
     wl = scenes.workload(3)
     with Scene(wl.scene) as sc:
