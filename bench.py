@@ -373,11 +373,12 @@ def run_visrt(args, rank, world):
         execd = sum(tests_exec) / len(tests_exec)
         achieved = FLOPS_PER_TEST * tests_alg / (kern * 1e-3) / 1e12
         peak = fp64_peak / 1e12
-        traffic = None
+        traffic, ncu_sol = None, None
         tp = os.path.join(ROOT, "profiles", "k_pair_bits_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+                prof = json.load(open(tp))
+                traffic, ncu_sol = prof.get("dram_bytes_per_launch"), prof.get("ncu_sol")
             except Exception:
                 traffic = None
         line = {
@@ -402,7 +403,8 @@ def run_visrt(args, rank, world):
                                   "frac > 1 means conservative culling + early exit skip reference work",
                          "executed_exact_tests": execd,
                          "executed_exact_tests_per_s": execd / (kern * 1e-3),
-                         "fp32_peak_tflops": fp32_peak / 1e12},
+                         "fp32_peak_tflops": fp32_peak / 1e12,
+                         "ncu_sol": ncu_sol},
             "clocks": clocks,
             "wall_s_timed_loop": wall,
         }
