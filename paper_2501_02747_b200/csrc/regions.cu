@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // arithmetic, same call order, so every output is bit-identical to K4 — with
 // converged lanes and a short per-region critical path (small batches and
 // trajectory probes are latency-bound on K4's lane state machines).
+#ifndef VISRT_K4W_PCOL
+#define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
+#endif
 // col_vis (src/vistable.cpp:146-159) for the warp kernel: warp-uniform
 // arithmetic, one warp-cooperative sweep per transverse sample. Out of line:
 // it has three call sites (scan, both refine directions) and inlining them
@@ -473,6 +476,40 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
     const double inset = dmul(dsub(cs1, cs0), 1e-6);
     const double px = dadd(ax, dmul(dx, cu));
     const double py = dadd(ay, dmul(dy, cu));
+#if VISRT_K4W_PCOL
+    {   // the 7 transverse samples on lanes 0..6: col_vis is their OR, so the
+        // order they are decided in does not change the verdict
+        const int j = lane;
+        bool pending = j < 7;
+        double qx = 0, qy = 0, qz = 0;
+        if (pending) {
+            const double sv_ = dmin_std(dsub(cs1, inset),
+                                        dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
+            if (pl == 0) { qx = px; qy = py; qz = sv_; }
+            else if (pl == 1) { qx = sv_; qy = px; qz = py; }
+            else { qx = px; qy = sv_; qz = py; }
+            queries += lane == 0 ? 7 : 0;
+        }
+        auto blocked_by = [&](int k) {
+            return sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, sx, sy, sz, qx, qy, qz)) &&
+                   (++tests, seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz));
+        };
+        if (pending && cache >= 0 && cache != sf && blocked_by(cache)) pending = false;
+        for (;;) {
+            const unsigned who = __ballot_sync(kFull, pending);
+            if (!who) return false;   // every sample blocked
+            const int L = __ffs(who) - 1;
+            const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
+                         bz = __shfl_sync(kFull, qz, L);
+            const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
+                                             sf, -1, sf, sv, tests, batches);
+            if (h < 0) return true;
+            cache = h;
+            if (lane == L) pending = false;
+            else if (pending && blocked_by(h)) pending = false;
+        }
+    }
+#endif
     for (int j = 0; j < 7; ++j) {
         const double sv_ = dmin_std(dsub(cs1, inset),
                                     dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
@@ -493,8 +530,98 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
     return false;
 }
 
+// The SCAN of visible_intervals (src/vistable.cpp:175-176: col_vis(i / 64) for
+// the 65 columns) with the columns spread over the lanes: lane l owns column
+// 32 * pass + l. col_vis is an OR over its <= 7 transverse samples, so the
+// per-column verdict does not depend on the order the samples are decided in:
+// every lane first drops the samples the warp's last blocker already blocks
+// (fp32 SAT + exact test), then the warp sweeps ONE pending sample at a time
+// (coop_any_hit) — a clear sample makes its column visible, a blocker found is
+// immediately tested on every lane's pending sample (a hidden face's columns
+// are mostly blocked by the same few faces). Same arithmetic per sightline as
+// col_vis_warp, so the 65 verdicts are identical. stop_at_first: return after
+// the first visible column (presence mode).
+template <int MAXV>
+__device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, const SweepCtx& ctx, const double* us,
+                                                          int nv, int pl, double ax, double ay, double dx, double dy,
+                                                          double sx, double sy, double sz, int sf, unsigned char* sv,
+                                                          int& cache, bool stop_at_first, bool& vis64,
+                                                          unsigned long long& tests, unsigned long long& queries,
+                                                          unsigned long long& batches) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    const int lane = threadIdx.x & 31;
+    unsigned long long vis = 0;
+    vis64 = false;
+    for (int pass = 0; pass < 3; ++pass) {
+        const int col = 32 * pass + lane;
+        double cs0 = 0, cs1 = 0, inset = 0, px = 0, py = 0;
+        bool pending = col < 65 && column_span_us(us, nv, __ddiv_rn(static_cast<double>(col), 64.0), cs0, cs1);
+        if (pending) {
+            const double cu = __ddiv_rn(static_cast<double>(col), 64.0);   // in [0, 1]: std::clamp is the identity
+            inset = dmul(dsub(cs1, cs0), 1e-6);
+            px = dadd(ax, dmul(dx, cu));
+            py = dadd(ay, dmul(dy, cu));
+        }
+        int j = 0;
+        double qx = 0, qy = 0, qz = 0;
+        auto point = [&]() {
+            const double v = dmin_std(dsub(cs1, inset),
+                                      dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
+            if (pl == 0) { qx = px; qy = py; qz = v; }
+            else if (pl == 1) { qx = v; qy = px; qz = py; }
+            else { qx = px; qy = v; qz = py; }
+            ++queries;
+        };
+        if (pending) point();
+        // advance this lane's column over the samples occluder k (Morton index) blocks
+        auto settle = [&](int k) {
+            const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
+            const double* R = s.srec + static_cast<size_t>(k) * STRIDE;
+            while (pending && sat_maybe(B, make_segf(s, sx, sy, sz, qx, qy, qz))) {
+                ++tests;
+                if (!seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz)) break;
+                if (++j == 7) pending = false;   // every sample blocked: column hidden
+                else point();
+            }
+        };
+        if (cache >= 0 && cache != sf) settle(cache);
+        bool visible = false;
+        for (;;) {
+            const unsigned who = __ballot_sync(kFull, pending);
+            if (!who) break;
+            const int L = __ffs(who) - 1;
+            const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
+                         bz = __shfl_sync(kFull, qz, L);
+            const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
+                                             sf, -1, sf, sv, tests, batches);
+            if (h < 0) {   // a clear sample: column L is visible
+                if (lane == L) {
+                    visible = true;
+                    pending = false;
+                }
+                if (stop_at_first) break;
+            } else {
+                cache = h;
+                if (lane == L) {   // the sweep proved this sample blocked
+                    if (++j == 7) pending = false;
+                    else point();
+                }
+                settle(h);
+            }
+        }
+        const unsigned vb = __ballot_sync(kFull, visible);
+        if (pass < 2) vis |= static_cast<unsigned long long>(vb) << (32 * pass);
+        else vis64 = (vb & 1u) != 0;
+        if (stop_at_first && (vis || vis64)) break;
+    }
+    return vis;
+}
+
 #ifndef VISRT_K4W_MINB
 #define VISRT_K4W_MINB 2
+#endif
+#ifndef VISRT_K4W_PSCAN
+#define VISRT_K4W_PSCAN 1   // 1: lane-parallel column scan (scan_cols_warp); 0: 65 serial col_vis calls
 #endif
 template <int MAXV, bool RESIDENT>
 __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp(RegionArgs a) {
@@ -559,7 +686,13 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             };
             if (presence) {   // a visible column <=> a non-empty interval list
                 bool any = false;
-                for (int i = 0; i < 65 && !any; ++i) any = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
+                if (VISRT_K4W_PSCAN) {
+                    bool v64;
+                    any = scan_cols_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, true,
+                                               v64, tests, queries, batches) != 0ull || v64;
+                } else {
+                    for (int i = 0; i < 65 && !any; ++i) any = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
+                }
                 if (!any) {
                     present = 0;
                     break;
@@ -569,10 +702,15 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             }
             unsigned long long vis = 0;
             bool vis64 = false;
-            for (int i = 0; i < 65; ++i) {
-                const bool v = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
-                if (i < 64) vis |= static_cast<unsigned long long>(v) << i;
-                else vis64 = v;
+            if (VISRT_K4W_PSCAN) {
+                vis = scan_cols_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, false, vis64,
+                                           tests, queries, batches);
+            } else {
+                for (int i = 0; i < 65; ++i) {
+                    const bool v = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
+                    if (i < 64) vis |= static_cast<unsigned long long>(v) << i;
+                    else vis64 = v;
+                }
             }
             auto V = [&](int i) { return i == 64 ? vis64 : ((vis >> i) & 1ull) != 0; };
             // refine (src/vistable.cpp:163-172)

@@ -1,5 +1,5 @@
 """Quick per-snapshot region timing (development aid)."""
-import sys, time
+import hashlib, sys, time
 import numpy as np
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2501_02747_b200 import scenes
@@ -16,4 +16,4 @@ for arg in sys.argv[1:] or ["1:101", "3:200"]:
         pres = (arr["present"] == 1).sum()
         print(f"cfg{cfg} N={wl.scene.nfaces} nsrc={len(src)}: kernel {st['ms']:.2f} ms wall {1e3*(t1-t0):.1f} ms "
               f"regions {arr.size} present {pres} sightlines {st['candidates']:.3e} exact {st['tests_exec']:.3e} "
-              f"-> {arr.size/st['ms']*1e3:.3e} regions/s", flush=True)
+              f"-> {arr.size/st['ms']*1e3:.3e} regions/s sha {hashlib.sha256(arr.tobytes()).hexdigest()[:16]}", flush=True)
