@@ -455,6 +455,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // arithmetic, same call order, so every output is bit-identical to K4 — with
 // converged lanes and a short per-region critical path (small batches and
 // trajectory probes are latency-bound on K4's lane state machines).
+#ifndef VISRT_K4W_NI
+#define VISRT_K4W_NI 1   // 1: one out-of-line copy of the sweep / blocker test for the K4w helpers
+#endif
+// The warp sweep and the fp32-SAT + exact blocker test as single out-of-line
+// copies: inlined at each call site of the lane-parallel scan and col_vis
+// they overflowed the instruction cache (ncu: stall_no_inst).
+template <int MAXV>
+__device__ __noinline__ int k4w_sweep(const DevScene& s, const SweepCtx& ctx, double sx, double sy, double sz,
+                                      double bx, double by, double bz, int sf, unsigned char* sv,
+                                      unsigned long long& tests, unsigned long long& batches) {
+    return coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz, sf, -1, sf,
+                              sv, tests, batches);
+}
+template <int MAXV>
+__device__ __noinline__ bool k4w_blocked(const DevScene& s, const SweepCtx& ctx, int k, double sx, double sy,
+                                         double sz, double qx, double qy, double qz, unsigned long long& tests) {
+    if (!sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, sx, sy, sz, qx, qy, qz))) return false;
+    ++tests;
+    return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
+}
+
 #ifndef VISRT_K4W_PCOL
 #define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
 #endif
@@ -491,8 +512,12 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             queries += lane == 0 ? 7 : 0;
         }
         auto blocked_by = [&](int k) {
+#if VISRT_K4W_NI
+            return k4w_blocked<MAXV>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests);
+#else
             return sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, sx, sy, sz, qx, qy, qz)) &&
                    (++tests, seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz));
+#endif
         };
         if (pending && cache >= 0 && cache != sf && blocked_by(cache)) pending = false;
         for (;;) {
@@ -501,8 +526,12 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             const int L = __ffs(who) - 1;
             const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
                          bz = __shfl_sync(kFull, qz, L);
+#if VISRT_K4W_NI
+            const int h = k4w_sweep<MAXV>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
+#else
             const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
+#endif
             if (h < 0) return true;
             cache = h;
             if (lane == L) pending = false;
@@ -517,7 +546,7 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
         if (pl == 0) { qx = px; qy = py; qz = sv_; }
         else if (pl == 1) { qx = sv_; qy = px; qz = py; }
         else { qx = px; qy = sv_; qz = py; }
-        ++queries;
+        queries += lane == 0;   // warp-uniform sample
         if (cache >= 0 && cache != sf) {
             tests += lane == 0;   // warp-uniform test: count it once
             if (seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * STRIDE, sx, sy, sz, qx, qy, qz)) continue;
@@ -577,9 +606,15 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
         auto settle = [&](int k) {
             const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
             const double* R = s.srec + static_cast<size_t>(k) * STRIDE;
+#if VISRT_K4W_NI
+            (void)B;
+            (void)R;
+            while (pending && k4w_blocked<MAXV>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests)) {
+#else
             while (pending && sat_maybe(B, make_segf(s, sx, sy, sz, qx, qy, qz))) {
                 ++tests;
                 if (!seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz)) break;
+#endif
                 if (++j == 7) pending = false;   // every sample blocked: column hidden
                 else point();
             }
@@ -592,8 +627,12 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             const int L = __ffs(who) - 1;
             const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
                          bz = __shfl_sync(kFull, qz, L);
+#if VISRT_K4W_NI
+            const int h = k4w_sweep<MAXV>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
+#else
             const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
+#endif
             if (h < 0) {   // a clear sample: column L is visible
                 if (lane == L) {
                     visible = true;
@@ -766,7 +805,10 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             a.out[t] = r;
         }
     }
-    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(kFull, tests, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        tests += __shfl_down_sync(kFull, tests, o);
+        queries += __shfl_down_sync(kFull, queries, o);
+    }
     if (lane == 0) {
         atomicAdd(&a.counter[1], tests);
         atomicAdd(&a.counter[2], queries);
