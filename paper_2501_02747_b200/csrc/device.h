@@ -101,26 +101,36 @@ __device__ __forceinline__ double dot_rel(double px, double py, double pz, doubl
 
 // segment_face_intersection (src/geom.cpp:169-180) + ConvexPolygon::contains
 // (src/geom.cpp:155-167) on one occluder record R (see RecLayout).
+#ifdef VISRT_SEG_STATS
+// development aid: where the exact predicate decides (total, |d| <= eps, same
+// side, off-plane, first edge, later edge, hit) — per translation unit
+__device__ unsigned long long g_seg_stats[8];
+#define SEG_STAT(k) atomicAdd(&g_seg_stats[k], 1ull)
+#else
+#define SEG_STAT(k) ((void)0)
+#endif
 template <int MAXV>
 __device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax, double ay,
                                          double az, double bx, double by, double bz) {
+    SEG_STAT(0);
     const double Px = R[0], Py = R[1], Pz = R[2];
     const double nx = R[3], ny = R[4], nz = R[5];
     const double da = dot_rel(ax, ay, az, Px, Py, Pz, nx, ny, nz);
     const double db = dot_rel(bx, by, bz, Px, Py, Pz, nx, ny, nz);
-    if (fabs(da) <= kEps || fabs(db) <= kEps) return false;
-    if (dmul(da, db) > 0.0) return false;
+    if (fabs(da) <= kEps || fabs(db) <= kEps) return SEG_STAT(1), false;
+    if (dmul(da, db) > 0.0) return SEG_STAT(2), false;
     const double t = __ddiv_rn(da, dsub(da, db));
     const double px = dadd(ax, dmul(dsub(bx, ax), t));
     const double py = dadd(ay, dmul(dsub(by, ay), t));
     const double pz = dadd(az, dmul(dsub(bz, az), t));
-    if (fabs(dot_rel(px, py, pz, Px, Py, Pz, nx, ny, nz)) > kEps) return false;
-    if (dot_rel(px, py, pz, Px, Py, Pz, R[6], R[7], R[8]) < -kEps) return false;
+    if (fabs(dot_rel(px, py, pz, Px, Py, Pz, nx, ny, nz)) > kEps) return SEG_STAT(3), false;
+    if (dot_rel(px, py, pz, Px, Py, Pz, R[6], R[7], R[8]) < -kEps) return SEG_STAT(4), false;
 #pragma unroll
     for (int k = 1; k < MAXV; ++k) {
         const double* E = R + 9 + (k - 1) * 6;
-        if (dot_rel(px, py, pz, E[0], E[1], E[2], E[3], E[4], E[5]) < -kEps) return false;
+        if (dot_rel(px, py, pz, E[0], E[1], E[2], E[3], E[4], E[5]) < -kEps) return SEG_STAT(5), false;
     }
+    SEG_STAT(6);
     return true;
 }
 

@@ -711,3 +711,10 @@ cudaError_t launch_clear_pairs(unsigned long long* bits, int words, const int32_
 }
 
 }  // namespace visrt
+
+#ifdef VISRT_SEG_STATS
+extern "C" int visrt_debug_seg_stats(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    return static_cast<int>(cudaMemcpyFromSymbol(out, visrt::g_seg_stats, sizeof(visrt::g_seg_stats)));
+}
+#endif

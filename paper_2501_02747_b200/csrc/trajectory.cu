@@ -498,7 +498,7 @@ struct Event {
 };
 
 std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, const Route& route,
-                                               const std::vector<visrt_entry>& entries, int max_order,
+                                               const visrt_entry* entries, int64_t nent, int max_order,
                                                const visrt_names& nm, visrt_stats& stats) {
     const int n = hs.n;
     // VISRT_TRAJ_PROFILE=1: host wall time per phase on stderr (development aid)
@@ -535,11 +535,12 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
     auto slot16 = [](int f) { return static_cast<uint64_t>(static_cast<uint16_t>(f)); };   // -1 -> 0xFFFF
     uint64_t last_refl = ~0ull;
     int last_c = -1, last_k = -1;
-    for (const visrt_entry& e : entries) {
-        if (e.order > max_order) continue;
+    for (int64_t q = 0; q < nent; ++q) {   // the caller's matrix entries, read in place
+        const visrt_entry& e = entries[q];
+        if (e.order < 1 || e.order > max_order) continue;
         const int L = e.order;   // reflectors chain[0..L-1]
         uint64_t rk = 0;
-        for (int q = 0; q < 4; ++q) rk = (rk << 16) | slot16(q < L ? e.chain[q] : -1);
+        for (int w = 0; w < 4; ++w) rk = (rk << 16) | slot16(w < L ? e.chain[w] : -1);
         int c, k;
         if (rk == last_refl) {   // consecutive entries of one chain (planes, aims): no lookups
             c = last_c;
@@ -569,9 +570,9 @@ std::vector<visrt_mobile_row> trajectory_table(Gpu& gpu, const HostScene& hs, co
             last_refl = rk;
             last_c = c;
             last_k = k;
+            if (std::find(key_chains[k].begin(), key_chains[k].end(), c) == key_chains[k].end())
+                key_chains[k].push_back(c);
         }
-        if (std::find(key_chains[k].begin(), key_chains[k].end(), c) == key_chains[k].end())
-            key_chains[k].push_back(c);
     }
     const int nface_keys = static_cast<int>(keys.size());
     std::vector<int> vkey_base(nface_keys, -1);   // order-1 face key -> first vertex key
@@ -983,14 +984,11 @@ extern "C" int visrt_trajectory_table(visrt_scene* sc, int32_t nwp, const double
         // src/vistable.cpp:825-828
         if (nwp < 2 || route.total_length() <= visrt::kEps)
             throw visrt::VisError("trajectory must contain at least two distinct waypoints");
-        std::vector<visrt_entry> ents;
-        for (int64_t e = 0; e < nent; ++e)
-            if (entries[e].order >= 1 && entries[e].order <= max_order) ents.push_back(entries[e]);
         visrt::Gpu gpu{sc, ds, visrt::scene_device(sc), static_cast<cudaStream_t>(stream)};
         visrt_stats st{};
         auto* t = new visrt_mobile_table;
         try {
-            t->rows = visrt::trajectory_table(gpu, visrt::scene_host(sc), route, ents, max_order, *names, st);
+            t->rows = visrt::trajectory_table(gpu, visrt::scene_host(sc), route, entries, nent, max_order, *names, st);
         } catch (...) {
             delete t;
             throw;
