@@ -227,7 +227,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         const size_t o_rec = add(rec), o_samples = add(hs.samples), o_pts = add(hs.pts), o_normal = add(hs.normal),
                      o_seg = add(hs.seg), o_aabb = add(hs.aabb), o_nv = add(hs.nv), o_ns = add(hs.ns),
                      o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_box = add(hs.box), o_sbox = add(hs.sbox),
-                     o_tbox = add(hs.tbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
+                     o_tbox = add(hs.tbox), o_gbox = add(hs.gbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
         const size_t o_bits = ar.add(nullptr, static_cast<size_t>(hs.n) * ds.words * 8);
         const size_t o_counter = ar.add(nullptr, 4 * 8);
         const size_t o_count = ar.add(nullptr, 2 * 8);
@@ -263,6 +263,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.box = static_cast<const float*>(at(o_box));
         ds.sbox = static_cast<const float*>(at(o_sbox));
         ds.tbox = static_cast<const float*>(at(o_tbox));
+        ds.gbox = static_cast<const float*>(at(o_gbox));
         ds.srec = static_cast<const double*>(at(o_srec));
         ds.perm = static_cast<const int32_t*>(at(o_perm));
         ds.inv = static_cast<const int32_t*>(at(o_inv));
@@ -271,6 +272,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         sc->d_count = static_cast<long long*>(at(o_count));
         ds.ntiles = hs.ntiles;
         ds.nchunks = hs.nchunks;
+        ds.ngroups = hs.ngroups;
         sc->upload_bytes = static_cast<int64_t>(
             (hs.maxv <= 4 ? hs.rec4.size() : hs.rec8.size()) * 8 + hs.samples.size() * 8 + hs.pts.size() * 8 +
             hs.normal.size() * 8 + hs.seg.size() * 8 + hs.aabb.size() * 8 + hs.nv.size() * 4 + hs.ns.size() * 4 +

@@ -32,7 +32,8 @@ struct DevScene {
     const double* srec = nullptr;  // occluder records, Morton order
     const int32_t* perm = nullptr; // Morton position -> face index
     const int32_t* inv = nullptr;  // face index -> Morton position
-    int32_t ntiles = 0, nchunks = 0;
+    const float* gbox = nullptr;   // [ngroups][8] group union boxes (kGroup faces)
+    int32_t ntiles = 0, nchunks = 0, ngroups = 0;
 };
 
 // A sightline in the fp32 culling frame: midpoint (relative to the scene

@@ -305,24 +305,30 @@ void build_hierarchy(HostScene& hs) {
     }
     hs.ntiles = (n + 63) / 64;
     hs.nchunks = (hs.ntiles + 63) / 64;
-    hs.tbox.assign(static_cast<size_t>(hs.ntiles) * 8, 0.0f);
-    for (int t = 0; t < hs.ntiles; ++t) {
-        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-        for (int k = t * 64; k < std::min(n, t * 64 + 64); ++k) {
-            const float* b = &hs.sbox[static_cast<size_t>(k) * 8];
+    hs.ngroups = (n + kGroup - 1) / kGroup;
+    // union boxes of `size` consecutive member boxes (tiles of 64, groups of 16)
+    auto unions = [&](int size, int count, std::vector<float>& out) {
+        out.assign(static_cast<size_t>(count) * 8, 0.0f);
+        for (int t = 0; t < count; ++t) {
+            double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+            for (int k = t * size; k < std::min(n, t * size + size); ++k) {
+                const float* b = &hs.sbox[static_cast<size_t>(k) * 8];
+                for (int d = 0; d < 3; ++d) {
+                    lo[d] = std::min(lo[d], static_cast<double>(b[d]) - static_cast<double>(b[4 + d]));
+                    hi[d] = std::max(hi[d], static_cast<double>(b[d]) + static_cast<double>(b[4 + d]));
+                }
+            }
+            float* o = &out[static_cast<size_t>(t) * 8];
             for (int d = 0; d < 3; ++d) {
-                lo[d] = std::min(lo[d], static_cast<double>(b[d]) - static_cast<double>(b[4 + d]));
-                hi[d] = std::max(hi[d], static_cast<double>(b[d]) + static_cast<double>(b[4 + d]));
+                // a member box lies inside [lo, hi]; the fp32 centre/half of the
+                // union are padded by a few ulps of the extent so it still does
+                o[d] = static_cast<float>(0.5 * (lo[d] + hi[d]));
+                o[4 + d] = static_cast<float>(0.5 * (hi[d] - lo[d]) + 1e-4 + 8.0 * ext * 1.1920928955078125e-7);
             }
         }
-        float* o = &hs.tbox[static_cast<size_t>(t) * 8];
-        for (int d = 0; d < 3; ++d) {
-            // a member box lies inside [lo, hi]; the fp32 centre/half of the
-            // union are padded by a few ulps of the extent so it still does
-            o[d] = static_cast<float>(0.5 * (lo[d] + hi[d]));
-            o[4 + d] = static_cast<float>(0.5 * (hi[d] - lo[d]) + 1e-4 + 8.0 * ext * 1.1920928955078125e-7);
-        }
-    }
+    };
+    unions(64, hs.ntiles, hs.tbox);
+    unions(kGroup, hs.ngroups, hs.gbox);
 }
 
 }  // namespace visrt

@@ -36,10 +36,15 @@ __device__ __forceinline__ unsigned long long sat64(const float* __restrict__ B,
     return mask;
 }
 
+#ifndef VISRT_GROUPS
+#define VISRT_GROUPS 1   // 1: non-resident sweeps cull 16-face groups (boxes in shared memory) before member boxes
+#endif
+
 struct SweepCtx {
     const float* tbox;   // [ntiles][8] (shared memory)
     const float* mbox;   // [n][8] member boxes (shared or global)
-    int n, ntiles, nchunks;
+    const float* gbox;   // [ngroups][8] group boxes (shared memory; non-resident path only, else nullptr)
+    int n, ntiles, nchunks, ngroups;
 };
 
 // Per-lane state of one segment sweep.
@@ -165,11 +170,84 @@ __device__ __forceinline__ int coop_exact(const double* __restrict__ srec, unsig
 // the likeliest blocker) and wraps around. Returns the Morton index of a
 // blocking face (skip0 / skip1 never tested) or -1 when the segment is clear.
 // Must be called by all 32 lanes with identical arguments.
+// Non-resident any-hit sweep with the group level: per chunk the 64 tile
+// boxes (2 per lane), then up to 8 candidate tiles at once — lane = (tile
+// slot, group) tests one of the tile's 4 group boxes (shared memory) — then 2
+// candidate groups at a time, a lane per member box (L1/L2) whose survivors
+// run the exact test in place (at most 32 per round: no compaction needed).
+// Same contract as coop_any_hit; which blocker is found first may differ.
+template <int MAXV>
+__device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const double* __restrict__ srec,
+                                                    const SegF& g, double ax, double ay, double az, double bx,
+                                                    double by, double bz, int skip0, int skip1, int home,
+                                                    unsigned long long& tests, unsigned long long& batches) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    constexpr int GPT = kTile / kGroup;   // groups per tile (4)
+    const int lane = threadIdx.x & 31;
+    const int home_tile = home < 0 ? 0 : home / kTile;
+    const int hc = home_tile / kTile;
+    for (int cc = 0; cc < ctx.nchunks; ++cc) {
+        const int c = hc + cc < ctx.nchunks ? hc + cc : hc + cc - ctx.nchunks;
+        const int t0 = c * kTile;
+        const int tc = min(kTile, ctx.ntiles - t0);
+        const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
+        const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
+        unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
+                                  (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
+        if (cc == 0) {   // the home tile first: rotate the mask so it starts there
+            const int r = home_tile - t0;
+            cand = r ? ((cand >> r) | (cand << (64 - r))) : cand;
+        }
+        const int rot = cc == 0 ? home_tile - t0 : 0;
+        ++batches;
+        while (cand) {
+            // up to 8 candidate tiles -> lane (slot = lane / 4, group = lane % 4)
+            int my_tile = -1;
+#pragma unroll
+            for (int q = 0; q < 32 / GPT; ++q) {
+                if (!cand) break;
+                const int b = __ffsll(static_cast<long long>(cand)) - 1;
+                cand &= cand - 1;
+                int t = b + rot;
+                if (t >= 64) t -= 64;
+                if (q == lane / GPT) my_tile = t0 + t;
+            }
+            const int grp = my_tile * GPT + (lane % GPT);
+            const bool gv = my_tile >= 0 && grp < ctx.ngroups && sat_maybe(ctx.gbox + static_cast<size_t>(grp) * 8, g);
+            unsigned gm = __ballot_sync(kFull, gv);
+            ++batches;
+            while (gm) {
+                // two candidate groups per round: lanes 0-15 / 16-31
+                const int la = __ffs(gm) - 1;
+                gm &= gm - 1;
+                const int lb = gm ? __ffs(gm) - 1 : -1;
+                if (lb >= 0) gm &= gm - 1;
+                const int ga = __shfl_sync(kFull, grp, la);
+                const int gb = __shfl_sync(kFull, grp, lb < 0 ? la : lb);
+                const int mg = lane < kGroup ? ga : (lb < 0 ? -1 : gb);
+                const int m = mg * kGroup + (lane & (kGroup - 1));
+                bool v = mg >= 0 && m < ctx.n && m != skip0 && m != skip1 &&
+                         sat_maybe(ctx.mbox + static_cast<size_t>(m) * 8, g);
+                if (v) {
+                    ++tests;
+                    v = seg_hits<MAXV>(srec + static_cast<size_t>(m) * STRIDE, ax, ay, az, bx, by, bz);
+                }
+                const unsigned hb = __ballot_sync(kFull, v);
+                ++batches;
+                if (hb) return __shfl_sync(kFull, m, __ffs(hb) - 1);
+            }
+        }
+    }
+    return -1;
+}
+
 template <int MAXV, int FIRST = 0>
 __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* __restrict__ srec, const SegF& g,
                                             double ax, double ay, double az, double bx, double by, double bz,
                                             int skip0, int skip1, int home, unsigned char* sv,
                                             unsigned long long& tests, unsigned long long& batches) {
+    if (ctx.gbox) return coop_any_hit_grouped<MAXV>(ctx, srec, g, ax, ay, az, bx, by, bz, skip0, skip1, home, tests,
+                                                   batches);
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -239,7 +317,9 @@ __device__ __forceinline__ SweepCtx sweep_setup(const DevScene& s, float* smem, 
     c.ntiles = s.ntiles;
     c.nchunks = s.nchunks;
     float* st = smem;
-    float* sm = smem + static_cast<size_t>(s.ntiles) * 8;
+    float* sm = smem + static_cast<size_t>(s.ntiles) * 8;   // member boxes (RESIDENT) or group boxes
+    constexpr bool kGroups = !RESIDENT && VISRT_GROUPS;
+    c.ngroups = s.ngroups;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -247,23 +327,26 @@ __device__ __forceinline__ SweepCtx sweep_setup(const DevScene& s, float* smem, 
     __syncthreads();
     if (threadIdx.x == 0) {
         const uint32_t tb = static_cast<uint32_t>(s.ntiles) * 32u;
-        const uint32_t mb = RESIDENT ? static_cast<uint32_t>(s.n) * 32u : 0u;
+        const uint32_t mb = RESIDENT ? static_cast<uint32_t>(s.n) * 32u
+                                     : (kGroups ? static_cast<uint32_t>(s.ngroups) * 32u : 0u);
+        const char* msrc = reinterpret_cast<const char*>(RESIDENT ? s.sbox : s.gbox);
         mbar_expect_tx(bar, tb + mb);
         for (uint32_t off = 0; off < tb; off += 32768u)
             bulk_g2s(reinterpret_cast<char*>(st) + off, reinterpret_cast<const char*>(s.tbox) + off,
                      min(32768u, tb - off), bar);
         for (uint32_t off = 0; off < mb; off += 32768u)
-            bulk_g2s(reinterpret_cast<char*>(sm) + off, reinterpret_cast<const char*>(s.sbox) + off,
-                     min(32768u, mb - off), bar);
+            bulk_g2s(reinterpret_cast<char*>(sm) + off, msrc + off, min(32768u, mb - off), bar);
     }
     mbar_wait(bar, 0);
     c.tbox = st;
     c.mbox = RESIDENT ? sm : s.sbox;
+    c.gbox = kGroups ? sm : nullptr;
     return c;
 }
 
 inline size_t sweep_smem_bytes(int n, int ntiles, bool resident) {
-    return (static_cast<size_t>(ntiles) + (resident ? static_cast<size_t>(n) : 0)) * 32 + 128;
+    const size_t groups = VISRT_GROUPS ? static_cast<size_t>((n + kGroup - 1) / kGroup) : 0;
+    return (static_cast<size_t>(ntiles) + (resident ? static_cast<size_t>(n) : groups)) * 32 + 128;
 }
 
 // Morton chunk holding original face f (a sweep starting there meets the

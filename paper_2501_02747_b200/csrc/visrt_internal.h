@@ -26,6 +26,8 @@ struct RecLayout {
     static constexpr int kStride = (kDoubles + 1) / 2 * 2;  // 16-B multiple
 };
 
+constexpr int kGroup = 16;   // faces per culling group (the mid level of the non-resident sweep)
+
 // Samples (face_samples, src/vismatrix.cpp:226-249): vertices, centroid,
 // then the grid (quads: 16 bilinear points; k-gons: 3 per vertex).
 constexpr int kMaxSamples = VISRT_MAX_VERTS + 1 + 3 * VISRT_MAX_VERTS;
@@ -53,9 +55,9 @@ struct HostScene {
     // two-level culling hierarchy: Morton order of the xy AABB centres,
     // tiles of 64 consecutive faces with union boxes (sweep.h)
     std::vector<int32_t> perm, inv;
-    std::vector<float> sbox, tbox;
+    std::vector<float> sbox, tbox, gbox;   // member / tile (64) / group (16) boxes, Morton order
     std::vector<double> srec;         // records in Morton order (layout of rec4/rec8)
-    int32_t ntiles = 0, nchunks = 0;
+    int32_t ntiles = 0, nchunks = 0, ngroups = 0;
 };
 
 // Dilation of the fp32 culling boxes. A true hit of segment_face_intersection

@@ -79,3 +79,30 @@ def test_regions_match_reference_region(oracle_built):
                 assert [int(x) for x in g["has"]] == e["has"]
                 assert [int(x) for x in g["clipped"]] == e["clipped"]
                 assert [float(x) for x in g["sub"]] == e["sub"]
+
+
+def test_streamed_sweep_paths_agree():
+    """The non-resident sweep (group boxes in shared memory, member boxes
+    through L1/L2 — what config 4/5 scenes use) and the resident sweep give
+    identical regions, segment verdicts and trees on config 3
+    (VISRT_FORCE_STREAM=1 forces the non-resident path)."""
+    import hashlib, json, os, subprocess, sys
+    code = ("import sys, json, hashlib; import numpy as np; sys.path.insert(0, %r);"
+            "from paper_2501_02747_b200 import scenes;"
+            "from paper_2501_02747_b200.core import Scene, point_regions_array, segments_clear, Tracer;"
+            "wl = scenes.workload(3); sc = Scene(wl.scene);"
+            "src = np.concatenate([wl.tx[:6], wl.rx[:6]]);"
+            "arr, _ = point_regions_array(sc, src);"
+            "rng = np.random.default_rng(5); a = src[rng.integers(0, len(src), 4000)];"
+            "b = wl.rx[rng.integers(0, len(wl.rx), 4000)] + rng.normal(0, 30, (4000, 3));"
+            "clr = segments_clear(sc, a, b)[0];"
+            "tr = Tracer(sc, 2); raw = tr.trace_raw(wl.tx[:4], wl.rx[:4]);"
+            "h = lambda x: hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest();"
+            "print(json.dumps([h(arr), h(np.asarray(clr)), h(raw[0]), h(raw[1])]))") % os.path.dirname(os.path.dirname(__file__))
+    out = {}
+    for force in ("0", "1"):
+        env = dict(os.environ, VISRT_FORCE_STREAM=force)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[force] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["0"] == out["1"]
