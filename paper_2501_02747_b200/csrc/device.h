@@ -84,6 +84,9 @@ struct PairArgs {
     int8_t* kind;                    // detail: per pair 0/1/2
     uint32_t* blk_mask;              // detail: per pair ceil(N/32) words
     int32_t blk_words;
+    int32_t flat;                    // K2w: 1 = non-resident sweep without the group level (A/B knob)
+    int32_t chunk;                   // K2w: consecutive pairs per warp grab
+    int32_t stride;                  // K2w profiling aid: decide every stride-th pair only (VISRT_K2_STRIDE, default 1)
 };
 
 // ---------------------------------------------------------------------------

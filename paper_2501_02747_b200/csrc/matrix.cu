@@ -18,6 +18,7 @@
 //
 // All geometry is the reference's FP64 predicate with explicit _rn intrinsics
 // (device.h), so every decision is bit-identical to the CPU oracle.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cub/cub.cuh>
@@ -248,7 +249,19 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #define VISRT_K2W_MINB 3
 #endif
 #ifndef VISRT_K2W_WC
-#define VISRT_K2W_WC 1      // warp blocker-cache entries (r01 sweep 1/2/3/4/6/8/16: 1 best)
+#define VISRT_K2W_WC 4      // warp blocker-cache entries (with 16-pair grabs; 2/3/4/5/6/8 swept: 4 best)
+#endif
+#ifndef VISRT_K2W_SETTLE
+#define VISRT_K2W_SETTLE 0  // 1: lane-balanced (sightline x blocker) settling rounds (measured slower)
+#endif
+#ifndef VISRT_K2W_RSAT
+#define VISRT_K2W_RSAT 1    // fp32 SAT before the exact test when settling sightlines with a known blocker
+#endif
+#ifndef VISRT_K2W_CHUNK
+#define VISRT_K2W_CHUNK 16  // consecutive pairs per warp grab (r01 sweep 1/4/8/12/16/32: 16 best)
+#endif
+#ifndef VISRT_K2W_CHUNK_CAND
+#define VISRT_K2W_CHUNK_CAND 2
 #endif
 #ifndef VISRT_K2W_ROT
 #define VISRT_K2W_ROT 1     // candidate tiles of the home chunk start at the pair's own tile
@@ -279,18 +292,34 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
     __shared__ unsigned char surv_buf[kThreads / 32][64];   // per warp: surviving members of a tile, in order
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     const unsigned lt = (1u << lane) - 1u;
+#if VISRT_K2W_SETTLE
+    __shared__ unsigned char ul_buf[kThreads / 32][96];   // per warp: compacted unresolved sightlines
+    __shared__ unsigned char fl_buf[kThreads / 32][96];   // per warp: sightline blocked flags
+    unsigned char* ul = ul_buf[threadIdx.x >> 5];
+    unsigned char* fl = fl_buf[threadIdx.x >> 5];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) fl[lane + 32 * r] = 0;
+    __syncwarp();
+#endif
 
+    long long pnext = 0, pend = 0;
     for (;;) {
-        unsigned long long pw = 0;
-        if (lane == 0) pw = atomicAdd(&a.counter[0], 1ull);
-        const long long p = static_cast<long long>(__shfl_sync(kFull, pw, 0));
-        if (p >= a.npairs) break;
+        // a warp takes VISRT_K2W_CHUNK consecutive pairs at a time: row-major
+        // neighbours share the reference face (and its blockers: warp cache)
+        if (pnext == pend) {
+            unsigned long long pw = 0;
+            if (lane == 0) pw = atomicAdd(&a.counter[0], static_cast<unsigned long long>(a.chunk));
+            pnext = static_cast<long long>(__shfl_sync(kFull, pw, 0));
+            if (pnext >= a.npairs) break;
+            pend = min(pnext + a.chunk, a.npairs);
+        }
+        const long long p = pnext++;
         int pi, pj;
         if (a.ci) {
             pi = a.ci[p];
             pj = a.cj[p];
         } else {
-            pair_from_index(p, n, pi, pj);
+            pair_from_index(p * a.stride, n, pi, pj);
 #if VISRT_K2W_MORTON
             // walk the pair space in Morton order (spatially coherent pairs keep
             // the warp blocker cache warm); the verdict keeps the reference's
@@ -341,9 +370,57 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             for (unsigned m = unres; m; m &= m - 1) {
                 const int r = __ffs(m) - 1;
                 ends(lane + 32 * r);
-                if (sat_maybe(B, make_segf(s, ax, ay, az, bx, by, bz)) && exact(k)) unres &= ~(1u << r);
+                if ((!VISRT_K2W_RSAT || sat_maybe(B, make_segf(s, ax, ay, az, bx, by, bz))) && exact(k))
+                    unres &= ~(1u << r);
             }
         };
+#if VISRT_K2W_SETTLE
+        // Lane-balanced settling: lanes q < m hold candidate blockers (Morton
+        // indices; -1 / the pair's own faces are skipped). The unresolved
+        // sightlines are compacted and every lane tests one (sightline,
+        // blocker) item per round — blocker-major, so a round covers all
+        // unresolved sightlines with the first floor(32 / #unresolved)
+        // blockers — instead of each lane walking its own sightline slots
+        // (1 of 32 lanes busy on the 33rd sightline of a quad pair).
+        auto settle = [&](int kreg, int m) {
+            for (int kstart = 0; kstart < m;) {
+                int cu = 0;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const bool b = (unres >> r) & 1u;
+                    const unsigned bb = __ballot_sync(kFull, b);
+                    if (b) ul[cu + __popc(bb & lt)] = static_cast<unsigned char>(lane + 32 * r);
+                    cu += __popc(bb);
+                }
+                if (cu == 0) return;
+                const int nb = min(cu >= 32 ? 1 : 32 / cu, m - kstart);
+                const int items = cu * nb;
+                const unsigned mgu = (65536u + cu - 1) / cu;   // w / cu = (w * mgu) >> 16 for w < 96
+                __syncwarp();
+                for (int b0 = 0; b0 < items; b0 += 32) {
+                    const int w = b0 + lane;
+                    const int q = static_cast<int>((static_cast<unsigned>(w) * mgu) >> 16);
+                    const int k = __shfl_sync(kFull, kreg, min(kstart + q, 31));
+                    if (w < items && k >= 0 && k != si && k != sj) {
+                        const int ord = ul[w - q * cu];
+                        ends(ord);
+                        if (sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, ax, ay, az, bx, by, bz)) &&
+                            exact(k))
+                            fl[ord] = 1;
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+                    if (((unres >> r) & 1u) && fl[lane + 32 * r]) {
+                        unres &= ~(1u << r);
+                        fl[lane + 32 * r] = 0;
+                    }
+                __syncwarp();
+                kstart += nb;
+            }
+        };
+#endif
         bool clear = false;
         if (may_touch(s, pi, pj)) {   // a degenerate sightline is never blocked
             bool degen = false;
@@ -353,6 +430,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             }
             clear = __any_sync(kFull, degen);
         }
+#if VISRT_K2W_SETTLE
+        if (!clear) {   // the warp cache, most recent blocker first
+            const int q = (wc_next + 2 * kWC - 1 - lane) % kWC;
+            settle(__shfl_sync(kFull, wc, q), kWC);
+        }
+#else
         if (!clear) {
             for (int i = 0; i < kWC; ++i) {   // most recent blocker first
                 const int q = (wc_next + kWC - 1 - i) % kWC;
@@ -362,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                 if (!__any_sync(kFull, unres != 0)) break;
             }
         }
+#endif
         while (!clear) {
             const unsigned who = __ballot_sync(kFull, unres != 0);
             if (!who) break;   // every sightline blocked: Occluded
@@ -375,7 +459,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             int hit2 = -1, hit3 = -1;
 #endif
             const int home = home_chunk(s, pi);
-            for (int cc = 0; cc < ctx.nchunks && hit < 0; ++cc) {
+            if (!RESIDENT && ctx.gbox && !a.flat) {
+                // non-resident scenes (config 4/5): tile -> group (shared memory) -> member (L1/L2)
+                int more[2];
+                hit = coop_any_hit_grouped<MAXV>(ctx, s.srec, g, ax, ay, az, bx, by, bz, si, sj, si, tests, batches,
+                                                 more);
+#if VISRT_K2W_MULTI
+                if (hit >= 0) {
+                    hit2 = more[0];
+                    hit3 = VISRT_K2W_MULTI > 1 ? more[1] : -1;
+                }
+#endif
+            }
+            for (int cc = 0; cc < ctx.nchunks && hit < 0 && (RESIDENT || !ctx.gbox || a.flat); ++cc) {
                 const int c = home + cc < ctx.nchunks ? home + cc : home + cc - ctx.nchunks;
                 const int t0 = c * kTile;
                 const int tc = min(kTile, ctx.ntiles - t0);
@@ -436,10 +532,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             }
             if (lane == wc_next) wc = hit;
             wc_next = wc_next + 1 == kWC ? 0 : wc_next + 1;
+#if VISRT_K2W_SETTLE
+#if VISRT_K2W_MULTI
+            settle(lane == 0 ? hit : lane == 1 ? hit2 : hit3, 3);
+#else
+            settle(hit, 1);
+#endif
+#else
             resolve(hit);
 #if VISRT_K2W_MULTI
             if (hit2 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit2);
             if (hit3 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit3);
+#endif
 #endif
         }
         if (lane == 0) {
@@ -642,7 +746,22 @@ static bool use_warp_k2() {
 }
 
 template <int MAXV>
-static cudaError_t launch_bits_t(const PairArgs& a, int device, cudaStream_t st) {
+static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st) {
+    static const int flat = [] {
+        const char* e = std::getenv("VISRT_K2W_GROUPED");
+        return e && e[0] == '0' ? 1 : 0;
+    }();
+    static const int stride = [] {
+        const char* e = std::getenv("VISRT_K2_STRIDE");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    PairArgs a = a0;
+    a.flat = flat;
+    a.stride = a.ci ? 1 : stride;
+    // all-pairs rows share the reference face over long runs; candidate lists are
+    // short and sparse, where big grabs only unbalance the tail
+    a.chunk = a.ci ? VISRT_K2W_CHUNK_CAND : VISRT_K2W_CHUNK;
+    if (a.stride > 1) a.npairs = (a.npairs + a.stride - 1) / a.stride;
     const bool res = use_resident(a.s.n);
     const size_t smem = sweep_smem(a.s, res);
     if (use_warp_k2()) {

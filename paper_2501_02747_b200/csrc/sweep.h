@@ -176,11 +176,14 @@ __device__ __forceinline__ int coop_exact(const double* __restrict__ srec, unsig
 // candidate groups at a time, a lane per member box (L1/L2) whose survivors
 // run the exact test in place (at most 32 per round: no compaction needed).
 // Same contract as coop_any_hit; which blocker is found first may differ.
+// With `more` (2 ints), the round's second and third blockers of the segment
+// come back too (-1 when none): K2w settles sibling sightlines with them.
 template <int MAXV>
 __device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const double* __restrict__ srec,
                                                     const SegF& g, double ax, double ay, double az, double bx,
                                                     double by, double bz, int skip0, int skip1, int home,
-                                                    unsigned long long& tests, unsigned long long& batches) {
+                                                    unsigned long long& tests, unsigned long long& batches,
+                                                    int* more = nullptr) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     constexpr int GPT = kTile / kGroup;   // groups per tile (4)
     const int lane = threadIdx.x & 31;
@@ -234,7 +237,14 @@ __device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const d
                 }
                 const unsigned hb = __ballot_sync(kFull, v);
                 ++batches;
-                if (hb) return __shfl_sync(kFull, m, __ffs(hb) - 1);
+                if (hb) {
+                    if (more) {
+                        const unsigned r1 = hb & (hb - 1), r2 = r1 & (r1 - 1);
+                        more[0] = r1 ? __shfl_sync(kFull, m, __ffs(r1) - 1) : -1;
+                        more[1] = r2 ? __shfl_sync(kFull, m, __ffs(r2) - 1) : -1;
+                    }
+                    return __shfl_sync(kFull, m, __ffs(hb) - 1);
+                }
             }
         }
     }
