@@ -227,7 +227,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         const size_t o_rec = add(rec), o_samples = add(hs.samples), o_pts = add(hs.pts), o_normal = add(hs.normal),
                      o_seg = add(hs.seg), o_aabb = add(hs.aabb), o_nv = add(hs.nv), o_ns = add(hs.ns),
                      o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_box = add(hs.box), o_sbox = add(hs.sbox),
-                     o_tbox = add(hs.tbox), o_gbox = add(hs.gbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
+                     o_tbox = add(hs.tbox), o_gbox = add(hs.gbox), o_cbox = add(hs.cbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
         const size_t o_bits = ar.add(nullptr, static_cast<size_t>(hs.n) * ds.words * 8);
         const size_t o_counter = ar.add(nullptr, 4 * 8);
         const size_t o_count = ar.add(nullptr, 2 * 8);
@@ -264,6 +264,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.sbox = static_cast<const float*>(at(o_sbox));
         ds.tbox = static_cast<const float*>(at(o_tbox));
         ds.gbox = static_cast<const float*>(at(o_gbox));
+        ds.cbox = static_cast<const float*>(at(o_cbox));
         ds.srec = static_cast<const double*>(at(o_srec));
         ds.perm = static_cast<const int32_t*>(at(o_perm));
         ds.inv = static_cast<const int32_t*>(at(o_inv));

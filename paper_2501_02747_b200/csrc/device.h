@@ -33,6 +33,7 @@ struct DevScene {
     const int32_t* perm = nullptr; // Morton position -> face index
     const int32_t* inv = nullptr;  // face index -> Morton position
     const float* gbox = nullptr;   // [ngroups][8] group union boxes (kGroup faces)
+    const float* cbox = nullptr;   // [nchunks][8] chunk union boxes (64 tiles)
     int32_t ntiles = 0, nchunks = 0, ngroups = 0;
 };
 

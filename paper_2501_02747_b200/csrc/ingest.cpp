@@ -329,6 +329,7 @@ void build_hierarchy(HostScene& hs) {
     };
     unions(64, hs.ntiles, hs.tbox);
     unions(kGroup, hs.ngroups, hs.gbox);
+    unions(64 * 64, hs.nchunks, hs.cbox);
 }
 
 }  // namespace visrt

@@ -475,6 +475,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                 const int c = home + cc < ctx.nchunks ? home + cc : home + cc - ctx.nchunks;
                 const int t0 = c * kTile;
                 const int tc = min(kTile, ctx.ntiles - t0);
+                if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !sat_maybe(ctx.cbox + static_cast<size_t>(c) * 8, g))
+                    continue;
                 const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
                 const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
                 unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
@@ -761,6 +763,12 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
     // all-pairs rows share the reference face over long runs; candidate lists are
     // short and sparse, where big grabs only unbalance the tail
     a.chunk = a.ci ? VISRT_K2W_CHUNK_CAND : VISRT_K2W_CHUNK;
+    {   // keep >= 8 grabs per resident warp (small scenes: config 1 has 6,670 pairs)
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const long long warps = static_cast<long long>(sms) * 3 * (kThreads / 32);
+        a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(a.chunk, a.npairs / (8 * warps))));
+    }
     if (a.stride > 1) a.npairs = (a.npairs + a.stride - 1) / a.stride;
     const bool res = use_resident(a.s.n);
     const size_t smem = sweep_smem(a.s, res);

@@ -36,6 +36,9 @@ __device__ __forceinline__ unsigned long long sat64(const float* __restrict__ B,
     return mask;
 }
 
+#ifndef VISRT_CHUNK_BOXES
+#define VISRT_CHUNK_BOXES 1   // 1: warp sweeps skip 4096-face chunks whose union box the segment misses
+#endif
 #ifndef VISRT_GROUPS
 #define VISRT_GROUPS 1   // 1: non-resident sweeps cull 16-face groups (boxes in shared memory) before member boxes
 #endif
@@ -44,6 +47,7 @@ struct SweepCtx {
     const float* tbox;   // [ntiles][8] (shared memory)
     const float* mbox;   // [n][8] member boxes (shared or global)
     const float* gbox;   // [ngroups][8] group boxes (shared memory; non-resident path only, else nullptr)
+    const float* cbox;   // [nchunks][8] chunk boxes (shared memory): a chunk whose box the segment misses is skipped
     int n, ntiles, nchunks, ngroups;
 };
 
@@ -193,6 +197,7 @@ __device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const d
         const int c = hc + cc < ctx.nchunks ? hc + cc : hc + cc - ctx.nchunks;
         const int t0 = c * kTile;
         const int tc = min(kTile, ctx.ntiles - t0);
+        if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !sat_maybe(ctx.cbox + static_cast<size_t>(c) * 8, g)) continue;
         const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
         const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
         unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
@@ -268,6 +273,7 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
         const int c = hc + cc < ctx.nchunks ? hc + cc : hc + cc - ctx.nchunks;
         const int t0 = c * kTile;
         const int tc = min(kTile, ctx.ntiles - t0);
+        if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !sat_maybe(ctx.cbox + static_cast<size_t>(c) * 8, g)) continue;
         const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
         const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
         unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
@@ -340,23 +346,27 @@ __device__ __forceinline__ SweepCtx sweep_setup(const DevScene& s, float* smem, 
         const uint32_t mb = RESIDENT ? static_cast<uint32_t>(s.n) * 32u
                                      : (kGroups ? static_cast<uint32_t>(s.ngroups) * 32u : 0u);
         const char* msrc = reinterpret_cast<const char*>(RESIDENT ? s.sbox : s.gbox);
-        mbar_expect_tx(bar, tb + mb);
+        const uint32_t cb = static_cast<uint32_t>(s.nchunks) * 32u;
+        mbar_expect_tx(bar, tb + mb + cb);
         for (uint32_t off = 0; off < tb; off += 32768u)
             bulk_g2s(reinterpret_cast<char*>(st) + off, reinterpret_cast<const char*>(s.tbox) + off,
                      min(32768u, tb - off), bar);
         for (uint32_t off = 0; off < mb; off += 32768u)
             bulk_g2s(reinterpret_cast<char*>(sm) + off, msrc + off, min(32768u, mb - off), bar);
+        bulk_g2s(reinterpret_cast<char*>(sm) + mb, reinterpret_cast<const char*>(s.cbox), cb, bar);
     }
     mbar_wait(bar, 0);
     c.tbox = st;
     c.mbox = RESIDENT ? sm : s.sbox;
     c.gbox = kGroups ? sm : nullptr;
+    c.cbox = sm + (RESIDENT ? static_cast<size_t>(s.n) * 8 : (kGroups ? static_cast<size_t>(s.ngroups) * 8 : 0));
     return c;
 }
 
 inline size_t sweep_smem_bytes(int n, int ntiles, bool resident) {
     const size_t groups = VISRT_GROUPS ? static_cast<size_t>((n + kGroup - 1) / kGroup) : 0;
-    return (static_cast<size_t>(ntiles) + (resident ? static_cast<size_t>(n) : groups)) * 32 + 128;
+    const size_t chunks = (static_cast<size_t>(ntiles) + kTile - 1) / kTile;
+    return (static_cast<size_t>(ntiles) + (resident ? static_cast<size_t>(n) : groups) + chunks) * 32 + 128;
 }
 
 // Morton chunk holding original face f (a sweep starting there meets the

@@ -55,7 +55,7 @@ struct HostScene {
     // two-level culling hierarchy: Morton order of the xy AABB centres,
     // tiles of 64 consecutive faces with union boxes (sweep.h)
     std::vector<int32_t> perm, inv;
-    std::vector<float> sbox, tbox, gbox;   // member / tile (64) / group (16) boxes, Morton order
+    std::vector<float> sbox, tbox, gbox, cbox;   // member / tile (64) / group (16) / chunk (4096) boxes, Morton order
     std::vector<double> srec;         // records in Morton order (layout of rec4/rec8)
     int32_t ntiles = 0, nchunks = 0, ngroups = 0;
 };

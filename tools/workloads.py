@@ -1,0 +1,162 @@
+"""Every BASELINE config's WHOLE workload on one GPU (BASELINE.json configs[0..4]):
+matrix (A) and (B), per-snapshot Tx/Rx tables over ALL snapshots, order-2
+chains and the matrix-pruned image tree for ALL snapshots. Device times are
+the library's CUDA events (sum over batches); wall times include host
+orchestration and the D2H of every result. Outputs are reduced to counts and
+a SHA-256 over the result bytes (determinism across runs / builds); parity is
+the tests' job (tests/test_fullsize_gpu.py re-decides seeded samples with the
+CPU oracle).
+
+usage: python tools/workloads.py [cfg ...] > workloads.json"""
+import hashlib
+import json
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2501_02747_b200 import scenes  # noqa: E402
+from paper_2501_02747_b200.core import (ENTRY_DTYPE, Scene, Tracer, chain_triples, point_regions_array,  # noqa: E402
+                                        point_tables, unpack_bits)
+
+
+def order1_entries(sc: Scene, bits: np.ndarray) -> np.ndarray:
+    """Order-1 InterVisEntry list of build_matrix(scene, 1): per admitted pair,
+    both directions x required_planes (src/vismatrix.cpp:171-206, 597-634;
+    plane segments and their unit normals from the library's ingest)."""
+    _, _, seg, ok = sc.ingest()
+    adm = unpack_bits(bits, sc.n)
+    ai, aj = np.nonzero(np.triu(adm, 1))
+    rows = []
+    for pl in range(3):
+        both = (ok[ai, pl] != 0) & (ok[aj, pl] != 0)
+        d = np.abs(seg[ai, pl, 4] * seg[aj, pl, 4] + seg[ai, pl, 5] * seg[aj, pl, 5])
+        sel = both & ((d >= 1.0 - 1e-9) | (d <= 1e-9))
+        for r, a in ((ai[sel], aj[sel]), (aj[sel], ai[sel])):
+            e = np.zeros(len(r), ENTRY_DTYPE)
+            e["order"] = 1
+            e["chain"][:, 0] = r
+            e["chain"][:, 1] = a
+            e["plane"] = pl
+            rows.append(e)
+    return np.concatenate(rows) if rows else np.zeros(0, ENTRY_DTYPE)
+
+
+class Stage:
+    def __init__(self):
+        self.ms = 0.0
+        self.t0 = time.perf_counter()
+        self.h = hashlib.sha256()
+        self.extra = {}
+
+    def add(self, ms, *arrays):
+        self.ms += float(ms)
+        for a in arrays:
+            self.h.update(np.ascontiguousarray(a).tobytes())
+
+    def done(self, **kw):
+        d = {"device_ms": round(self.ms, 3), "wall_ms": round((time.perf_counter() - self.t0) * 1e3, 1),
+             "sha": self.h.hexdigest()[:16]}
+        d.update(kw)
+        return d
+
+
+def matrices(sc: Scene, out: dict):
+    sc.pair_visibility("all", copy_bits=False)           # warm-up (allocation, module load)
+    s = Stage()
+    bits_b, st = sc.pair_visibility("all")
+    s.add(st["ms"], bits_b)
+    out["matrix_B"] = s.done(pairs=int(st["pairs"]), tests_alg=st["tests_alg"],
+                             tests_per_s=st["tests_alg"] / (st["ms"] * 1e-3),
+                             visible_pairs=int(np.unpackbits(bits_b.view(np.uint8)).sum() // 2))
+    sc.pair_visibility("prefiltered", copy_bits=False)
+    s = Stage()
+    bits_a, st = sc.pair_visibility("prefiltered")
+    s.add(st["ms"], bits_a)
+    out["matrix_A"] = s.done(candidates=int(st["candidates"]), admitted=int(st["admitted"]))
+    return bits_a
+
+
+def regions(sc: Scene, src: np.ndarray, batch: int, out: dict, key: str):
+    point_regions_array(sc, src[:2])
+    s = Stage()
+    present = 0
+    for b in range(0, len(src), batch):
+        arr, st = point_regions_array(sc, src[b:b + batch])
+        # present / has / clipped bytes + an xor of the sub bit patterns (cheap on 1e8+ regions)
+        s.add(st["ms"], arr.view(np.uint8).reshape(-1, arr.dtype.itemsize)[:, :8],
+              np.bitwise_xor.reduce(arr["sub"].reshape(-1).view(np.uint64)))
+        present += int((arr["present"] == 1).sum())
+    out[key] = s.done(sources=len(src), facets=sc.n, regions=len(src) * sc.n, present=present,
+                      regions_per_s=len(src) * sc.n / max(s.ms * 1e-3, 1e-12))
+
+
+def tables(sc: Scene, src: np.ndarray, ent: np.ndarray, batch: int, out: dict, key: str):
+    point_tables(sc, src[:2], ent)
+    s = Stage()
+    nrows = 0
+    for b in range(0, len(src), batch):
+        rows, full, _, st = point_tables(sc, src[b:b + batch], ent)
+        s.add(st["ms"], rows, full)
+        nrows += int(rows.sum())
+    out[key] = s.done(sources=len(src), entries=len(ent), rows=nrows)
+
+
+def trees(sc: Scene, tx, rx, max_refl: int, tri, batch: int, out: dict, key: str):
+    tr = Tracer(sc, max_refl, triples=tri)
+    tr.trace_raw(tx[:2], rx[:2] if len(rx) > 1 else rx)
+    s = Stage()
+    nodes = paths = 0
+    for b in range(0, len(tx), batch):
+        r = rx[b:b + batch] if len(rx) > 1 else rx
+        off, p, nd, st = tr.trace_raw(tx[b:b + batch], r)
+        s.add(st["ms"], off, nd, np.frombuffer(bytes(p), np.uint8))
+        nodes += int(st["nodes"])
+        paths += int(st["paths"])
+    tr.close()
+    out[key] = s.done(snapshots=len(tx), max_refl=max_refl, nodes=nodes, paths=paths,
+                      nodes_per_s=nodes / max(s.ms * 1e-3, 1e-12))
+
+
+def run(cfg: int) -> dict:
+    wl = scenes.workload(cfg)
+    out = {"config": cfg, "facets": wl.scene.nfaces, "tx": 0 if wl.tx is None else len(wl.tx),
+           "rx": 0 if wl.rx is None else len(wl.rx)}
+    t0 = time.perf_counter()
+    with Scene(wl.scene) as sc:
+        bits_a = matrices(sc, out)
+        if cfg in (1, 3):
+            ent = order1_entries(sc, bits_a)
+            if cfg == 1:   # the entry list equals the compiled reference's build_matrix(scene, 1)
+                try:
+                    from oracle import bindings
+                    r = bindings.RefOracle(wl.scene)
+                    exp = sorted((e["chain"][0], e["chain"][1], e["plane"])
+                                 for e in r.matrix_entries(r.build_matrix(1)) if e["order"] == 1)
+                    got = sorted(zip(ent["chain"][:, 0].tolist(), ent["chain"][:, 1].tolist(),
+                                     ent["plane"].tolist()))
+                    out["entries_match_reference"] = got == exp
+                except Exception as e:   # oracle/_ref not built
+                    out["entries_match_reference"] = f"unchecked: {e}"
+            src = np.concatenate([wl.tx, wl.rx])
+            tables(sc, src, ent, 256, out, "tables_order1")
+            regions(sc, src, 512, out, "regions")
+        if cfg == 5:
+            regions(sc, np.concatenate([wl.tx, wl.rx]), 500, out, "regions")
+        if cfg in (1, 3, 5):
+            s = Stage()
+            tri, st = chain_triples(sc, bits_a)
+            s.add(st["ms"], tri)
+            out["chains_order2"] = s.done(candidate_triples=int(st["candidates"]), feasible=len(tri))
+            order = 2 if cfg == 1 else 3
+            trees(sc, wl.tx, wl.rx, order, tri if order >= 3 else None, 50 if cfg == 3 else 500, out,
+                  f"trees_order{order}")
+    out["total_wall_s"] = round(time.perf_counter() - t0, 2)
+    out["total_device_ms"] = round(sum(v["device_ms"] for v in out.values() if isinstance(v, dict)), 2)
+    return out
+
+
+if __name__ == "__main__":
+    for c in [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]:
+        print(json.dumps(run(c)), flush=True)
