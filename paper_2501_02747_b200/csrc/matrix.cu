@@ -759,6 +759,8 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
     }();
     PairArgs a = a0;
     a.flat = flat;
+    int smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     a.stride = a.ci ? 1 : stride;
     // all-pairs rows share the reference face over long runs; candidate lists are
     // short and sparse, where big grabs only unbalance the tail
@@ -770,13 +772,15 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(a.chunk, a.npairs / (8 * warps))));
     }
     if (a.stride > 1) a.npairs = (a.npairs + a.stride - 1) / a.stride;
-    const bool res = use_resident(a.s.n);
+    // K2w keeps the member boxes resident only while 3 CTAs still fit per SM:
+    // occupancy beats residency (r01: config 3 resident 14.8 ms at 2 CTAs,
+    // streamed with the group level 12.9 ms at 3 CTAs)
+    bool res = use_resident(a.s.n);
+    if (res && use_warp_k2() && 3 * (sweep_smem(a.s, true) + 3 * 1024) > static_cast<size_t>(smem_sm)) res = false;
     const size_t smem = sweep_smem(a.s, res);
     if (use_warp_k2()) {
         // register budget by occupancy: when shared memory already limits the
-        // SM to <= 2 CTAs (large resident scenes), take the 2-CTA register budget
-        int smem_sm = 0;
-        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        // SM to <= 2 CTAs, take the 2-CTA register budget
         const bool two = smem + 1024 > static_cast<size_t>(smem_sm) / 3;
         if (two)
             return res ? launch_persistent(k_pair_bits_warp<MAXV, true, 2>, smem, a, device, st)

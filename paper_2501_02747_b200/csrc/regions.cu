@@ -23,6 +23,7 @@
 // presence-only mode (scan until the first visible column) for callers that
 // only need whether a region exists (trajectory keys of order 1).
 // K5 (k_beam_rows): TableBuilder::reach through 1..4 reflectors.
+#include <algorithm>
 #include <cstdlib>
 
 #include "device.h"
@@ -461,10 +462,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // The warp sweep and the fp32-SAT + exact blocker test as single out-of-line
 // copies: inlined at each call site of the lane-parallel scan and col_vis
 // they overflowed the instruction cache (ncu: stall_no_inst).
+#ifndef VISRT_K4W_FAN
+#define VISRT_K4W_FAN 0     // 1: per region, collect the faces that may block ANY sightline of the source->face fan
+                            //    (bit-identical; r01 measured no gain: the sweeps are latency-bound on L2 loads, not traversal)
+#endif
+#ifndef VISRT_K4W_FANCAP
+#define VISRT_K4W_FANCAP 255   // candidate-list capacity per warp (overflow: hierarchical sweeps)
+#endif
+#if VISRT_K4W_FAN
+// Per warp: [0] = candidate count of the current region's fan (-1: none), then the list.
+__shared__ int k4w_fan[kThreads / 32][VISRT_K4W_FANCAP + 1];
+#endif
 template <int MAXV>
 __device__ __noinline__ int k4w_sweep(const DevScene& s, const SweepCtx& ctx, double sx, double sy, double sz,
                                       double bx, double by, double bz, int sf, unsigned char* sv,
                                       unsigned long long& tests, unsigned long long& batches) {
+#if VISRT_K4W_FAN
+    const int* fan = k4w_fan[threadIdx.x >> 5];
+    if (fan[0] >= 0)
+        return list_any_hit<MAXV>(ctx, s.srec, fan + 1, fan[0], make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx,
+                                  by, bz, tests);
+#endif
     return coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz, sf, -1, sf,
                               sv, tests, batches);
 }
@@ -476,6 +494,44 @@ __device__ __noinline__ bool k4w_blocked(const DevScene& s, const SweepCtx& ctx,
     return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
 }
 
+// Development aid (-DVISRT_K4W_PROF): per-phase cycle and sweep counters of K4w.
+#ifdef VISRT_K4W_PROF
+__shared__ unsigned long long k4w_sprof[16];
+__device__ unsigned long long g_k4w_prof[16];
+#define K4P(i, v)                                                                                     \
+    do {                                                                                              \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&k4w_sprof[i], static_cast<unsigned long long>(v));     \
+    } while (0)
+#define K4CLK() clock64()
+#else
+#define K4P(i, v) \
+    do {          \
+    } while (0)
+#define K4CLK() 0ll
+#endif
+
+#ifndef VISRT_K4W_WC
+#define VISRT_K4W_WC 1   // warp blocker-cache entries, most recent first (r01: 1/2/4/8 swept; 4 helps config-5 Tx, hurts config 3)
+#endif
+#ifndef VISRT_K4W_CHUNK
+#define VISRT_K4W_CHUNK 1   // consecutive (source, face) tasks per warp grab (r01: 8/16 measured slower: heavy faces cluster)
+#endif
+// Warp blocker cache: lane q < VISRT_K4W_WC holds entry q (Morton index or
+// -1); `next` is the warp-uniform insertion slot. Entries are distinct.
+struct WCache {
+    int v = -1;
+    int next = 0;
+    __device__ __forceinline__ int entry(int i) const {   // i-th most recent (call with all lanes)
+        return __shfl_sync(kFull, v, (next + 2 * VISRT_K4W_WC - 1 - i) % VISRT_K4W_WC);
+    }
+    __device__ __forceinline__ void put(int h) {   // all lanes, warp-uniform h
+        const int lane = threadIdx.x & 31;
+        if (__any_sync(kFull, lane < VISRT_K4W_WC && v == h)) return;
+        if (lane == next) v = h;
+        next = next + 1 == VISRT_K4W_WC ? 0 : next + 1;
+    }
+};
+
 #ifndef VISRT_K4W_PCOL
 #define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
 #endif
@@ -486,7 +542,7 @@ __device__ __noinline__ bool k4w_blocked(const DevScene& s, const SweepCtx& ctx,
 template <int MAXV>
 __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx, const double* us, int nv, int pl,
                                           double ax, double ay, double dx, double dy, double u, double sx,
-                                          double sy, double sz, int sf, unsigned char* sv, int& cache,
+                                          double sy, double sz, int sf, unsigned char* sv, WCache& cache,
                                           unsigned long long& tests, unsigned long long& queries,
                                           unsigned long long& batches) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
@@ -519,7 +575,10 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
                    (++tests, seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz));
 #endif
         };
-        if (pending && cache >= 0 && cache != sf && blocked_by(cache)) pending = false;
+        for (int i = 0; i < VISRT_K4W_WC; ++i) {
+            const int k = cache.entry(i);
+            if (pending && k >= 0 && k != sf && blocked_by(k)) pending = false;
+        }
         for (;;) {
             const unsigned who = __ballot_sync(kFull, pending);
             if (!who) return false;   // every sample blocked
@@ -532,8 +591,12 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
 #endif
-            if (h < 0) return true;
-            cache = h;
+            K4P(4, 1);
+            if (h < 0) {
+                K4P(5, 1);
+                return true;
+            }
+            cache.put(h);
             if (lane == L) pending = false;
             else if (pending && blocked_by(h)) pending = false;
         }
@@ -547,14 +610,15 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
         else if (pl == 1) { qx = sv_; qy = px; qz = py; }
         else { qx = px; qy = sv_; qz = py; }
         queries += lane == 0;   // warp-uniform sample
-        if (cache >= 0 && cache != sf) {
+        const int c0 = cache.entry(0);
+        if (c0 >= 0 && c0 != sf) {
             tests += lane == 0;   // warp-uniform test: count it once
-            if (seg_hits<MAXV>(s.srec + static_cast<size_t>(cache) * STRIDE, sx, sy, sz, qx, qy, qz)) continue;
+            if (seg_hits<MAXV>(s.srec + static_cast<size_t>(c0) * STRIDE, sx, sy, sz, qx, qy, qz)) continue;
         }
         const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz, qx, qy, qz, sf,
                                          -1, sf, sv, tests, batches);
         if (h < 0) return true;
-        cache = h;
+        cache.put(h);
     }
     return false;
 }
@@ -574,7 +638,7 @@ template <int MAXV>
 __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, const SweepCtx& ctx, const double* us,
                                                           int nv, int pl, double ax, double ay, double dx, double dy,
                                                           double sx, double sy, double sz, int sf, unsigned char* sv,
-                                                          int& cache, bool stop_at_first, bool& vis64,
+                                                          WCache& cache, bool stop_at_first, bool& vis64,
                                                           unsigned long long& tests, unsigned long long& queries,
                                                           unsigned long long& batches) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
@@ -619,7 +683,10 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                 else point();
             }
         };
-        if (cache >= 0 && cache != sf) settle(cache);
+        for (int i = 0; i < VISRT_K4W_WC; ++i) {   // the warp cache, most recent first
+            const int k = cache.entry(i);
+            if (k >= 0 && k != sf) settle(k);
+        }
         bool visible = false;
         for (;;) {
             const unsigned who = __ballot_sync(kFull, pending);
@@ -633,6 +700,8 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
 #endif
+            K4P(2, 1);
+            if (h < 0) K4P(3, 1);
             if (h < 0) {   // a clear sample: column L is visible
                 if (lane == L) {
                     visible = true;
@@ -640,7 +709,7 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                 }
                 if (stop_at_first) break;
             } else {
-                cache = h;
+                cache.put(h);
                 if (lane == L) {   // the sweep proved this sample blocked
                     if (++j == 7) pending = false;
                     else point();
@@ -674,12 +743,24 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
     const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     unsigned long long tests = 0, queries = 0, batches = 0;
-    int cache = -1;   // warp-uniform: Morton index of the last blocker
+    WCache cache;   // the last blockers (Morton indices)
+#if VISRT_K4W_FAN
+    int* fan = k4w_fan[threadIdx.x >> 5];
+#endif
+#ifdef VISRT_K4W_PROF
+    if (threadIdx.x < 16) k4w_sprof[threadIdx.x] = 0;
+    __syncthreads();
+#endif
+    long long tnext = 0, tend = 0;
     for (;;) {
-        unsigned long long tw = 0;
-        if (lane == 0) tw = atomicAdd(&a.counter[0], 1ull);
-        const long long t = static_cast<long long>(__shfl_sync(kFull, tw, 0));
-        if (t >= a.ntasks) break;
+        if (tnext == tend) {   // a.chunk consecutive tasks: the same source, neighbouring faces
+            unsigned long long tw = 0;
+            if (lane == 0) tw = atomicAdd(&a.counter[0], static_cast<unsigned long long>(a.chunk));
+            tnext = static_cast<long long>(__shfl_sync(kFull, tw, 0));
+            if (tnext >= a.ntasks) break;
+            tend = min(tnext + a.chunk, a.ntasks);
+        }
+        const long long t = tnext++;
         long long k;
         int f;
         if (!a.task_face) {
@@ -698,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
         const bool presence = a.presence_only ||
                               (a.presence_of && a.task_face &&
                                a.presence_of[a.paired ? t : t - k * static_cast<long long>(a.m)]);
+        const long long tclk0 = K4CLK();
         int8_t present = 1;
         int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
         double sub[6] = {0, 0, 0, 0, 0, 0};
@@ -709,6 +791,32 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             if (fabs(dist) <= kEps) present = -1;
             else if (dist < 0.0) present = 0;
         }
+        if (present == 1) K4P(9, 1);
+#if VISRT_K4W_FAN
+        if (lane == 0) fan[0] = -1;
+        if (present == 1) {
+            // every sightline of this region runs from the source to a point of
+            // the face, i.e. within r (circumradius about the centroid) of the
+            // source -> centroid segment: collect the faces that may block any
+            // of them once, then each sightline scans that list
+            const double* C0 = s.samples + (static_cast<size_t>(f) * kMaxSamples + nv) * 3;
+            const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
+            double r2 = 0.0;
+            for (int q = 0; q < nv; ++q) {
+                const double ex = P[3 * q] - C0[0], ey = P[3 * q + 1] - C0[1], ez = P[3 * q + 2] - C0[2];
+                r2 = fmax(r2, ex * ex + ey * ey + ez * ez);
+            }
+            const float r = static_cast<float>(sqrt(r2) * (1.0 + 1e-6)) + 0.01f;
+            __syncwarp();
+            const int c = coop_collect(ctx, make_segf(s, sx, sy, sz, C0[0], C0[1], C0[2]), r, sf, fan + 1,
+                                       VISRT_K4W_FANCAP);
+            if (lane == 0) fan[0] = c;
+            K4P(12, 1);
+            K4P(13, c < 0 ? 0 : c);
+            K4P(14, c < 0 ? 1 : 0);
+        }
+        __syncwarp();
+#endif
         for (int pl = 0; pl < 3 && present == 1; ++pl) {
             if (!s.seg_ok[3 * f + pl]) continue;
             const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;
@@ -741,6 +849,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             }
             unsigned long long vis = 0;
             bool vis64 = false;
+            const long long sclk0 = K4CLK();
             if (VISRT_K4W_PSCAN) {
                 vis = scan_cols_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, false, vis64,
                                            tests, queries, batches);
@@ -751,14 +860,20 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
                     else vis64 = v;
                 }
             }
+            K4P(0, K4CLK() - sclk0);
             auto V = [&](int i) { return i == 64 ? vis64 : ((vis >> i) & 1ull) != 0; };
             // refine (src/vistable.cpp:163-172)
             auto refine = [&](double lo, double hi, bool lo_vis) {
-                for (int it = 0; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
+                const long long rclk0 = K4CLK();
+                int it = 0;
+                for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
                     const double mid = dmul(0.5, dadd(lo, hi));
                     if (col_vis(mid) == lo_vis) lo = mid;
                     else hi = mid;
                 }
+                K4P(1, K4CLK() - rclk0);
+                K4P(6, 1);
+                K4P(7, it);
                 return dmul(0.5, dadd(lo, hi));
             };
             const double step = __ddiv_rn(1.0, 64.0);
@@ -793,6 +908,11 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             clp[pl] = (b0 > 1e-9 || b1 < 1.0 - 1e-9) ? 1 : 0;
         }
         if (present == 1 && !(has[0] | has[1] | has[2])) present = 0;
+        K4P(8, K4CLK() - tclk0);
+        if (present == 1) {
+            K4P(10, K4CLK() - tclk0);
+            K4P(11, 1);
+        }
         if (lane == 0) {
             visrt_region r;
             r.present = present;
@@ -813,7 +933,22 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
         atomicAdd(&a.counter[1], tests);
         atomicAdd(&a.counter[2], queries);
     }
+#ifdef VISRT_K4W_PROF
+    __syncthreads();
+    if (threadIdx.x < 16) atomicAdd(&g_k4w_prof[threadIdx.x], k4w_sprof[threadIdx.x]);
+#endif
 }
+
+#ifdef VISRT_K4W_PROF
+}  // namespace visrt
+extern "C" int visrt_debug_k4w_prof(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, visrt::g_k4w_prof, sizeof(visrt::g_k4w_prof));
+    static const unsigned long long zero[16] = {};
+    return static_cast<int>(cudaMemcpyToSymbol(visrt::g_k4w_prof, zero, sizeof(zero)));
+}
+namespace visrt {
+#endif
 
 static int persistent_grid_r(const void* fn, size_t smem, int device) {
     int sms = 0, per = 0;
@@ -832,7 +967,14 @@ static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a, int device, 
 }
 
 template <int MAXV>
-static cudaError_t launch_regions_t(const RegionArgs& a, int device, cudaStream_t st) {
+static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream_t st) {
+    RegionArgs a = a0;
+    {   // K4w task grabs: VISRT_K4W_CHUNK consecutive tasks, fewer when that leaves < 8 grabs per warp
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const long long warps = static_cast<long long>(sms) * 2 * (kThreads / 32);
+        a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(VISRT_K4W_CHUNK, a.ntasks / (8 * warps))));
+    }
     const char* e = std::getenv("VISRT_FORCE_STREAM");
     const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
     const size_t smem = sweep_smem_bytes(a.s.n, a.s.ntiles, res);

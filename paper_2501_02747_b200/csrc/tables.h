@@ -27,6 +27,7 @@ struct RegionArgs {
     // — exactly whether illuminated_region returns a region
     int presence_only = 0;
     const uint8_t* presence_of = nullptr;   // per face-list entry (list mode) / per task (paired)
+    int chunk = 1;                          // K4w: consecutive tasks per warp grab (set by the launcher)
 };
 
 // K5 (TableBuilder::reach for order 1/2 chains). Dense: every (source k,
