@@ -464,10 +464,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // they overflowed the instruction cache (ncu: stall_no_inst).
 #ifndef VISRT_K4W_FAN
 #define VISRT_K4W_FAN 0     // 1: per region, collect the faces that may block ANY sightline of the source->face fan
-                            //    (bit-identical; r01 measured no gain: the sweeps are latency-bound on L2 loads, not traversal)
+                            //    and scan that list lane-parallel (lane = column / sample). Bit-identical, but r01
+                            //    measured 3-5x SLOWER (fans hold ~130-200 candidates; the hierarchical sweep
+                            //    tests a handful of member boxes per sightline), so off
 #endif
 #ifndef VISRT_K4W_FANCAP
-#define VISRT_K4W_FANCAP 255   // candidate-list capacity per warp (overflow: hierarchical sweeps)
+#define VISRT_K4W_FANCAP 511   // candidate-list capacity per warp (overflow: hierarchical sweeps)
 #endif
 #if VISRT_K4W_FAN
 // Per warp: [0] = candidate count of the current region's fan (-1: none), then the list.
@@ -532,6 +534,16 @@ struct WCache {
     }
 };
 
+// Lane-level blocker test against a precomputed fp32 sightline (list scans).
+template <int MAXV>
+__device__ __noinline__ bool k4w_blocked_g(const DevScene& s, const SweepCtx& ctx, int k, const SegF& g, double sx,
+                                           double sy, double sz, double qx, double qy, double qz,
+                                           unsigned long long& tests) {
+    if (!sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, g)) return false;
+    ++tests;
+    return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
+}
+
 #ifndef VISRT_K4W_PCOL
 #define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
 #endif
@@ -579,6 +591,29 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             const int k = cache.entry(i);
             if (pending && k >= 0 && k != sf && blocked_by(k)) pending = false;
         }
+#if VISRT_K4W_FAN
+        {   // the region's fan list: every lane scans it with its own sample
+            // (same face k on every lane: broadcast loads); a sample is clear
+            // after all fcnt candidates failed to block it
+            const int* fan = k4w_fan[threadIdx.x >> 5];
+            const int fcnt = fan[0];
+            if (fcnt >= 0) {
+                if (fcnt == 0) return __any_sync(kFull, pending);
+                const SegF g = make_segf(s, sx, sy, sz, qx, qy, qz);
+                int scanned = 0;
+                for (int i = 0; __any_sync(kFull, pending); i = i + 1 == fcnt ? 0 : i + 1) {
+                    const int k = fan[1 + i];
+                    bool vis = false;
+                    if (pending) {
+                        if (k4w_blocked_g<MAXV>(s, ctx, k, g, sx, sy, sz, qx, qy, qz, tests)) pending = false;
+                        else if (++scanned == fcnt) vis = true;
+                    }
+                    if (__any_sync(kFull, vis)) return true;
+                }
+                return false;
+            }
+        }
+#endif
         for (;;) {
             const unsigned who = __ballot_sync(kFull, pending);
             if (!who) return false;   // every sample blocked
@@ -688,6 +723,40 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             if (k >= 0 && k != sf) settle(k);
         }
         bool visible = false;
+#if VISRT_K4W_FAN
+        {   // the region's fan list, lane-parallel: lane = column, all lanes test
+            // the same candidate k per step (broadcast loads); a blocked sample
+            // moves the lane to its next sample, re-tested against k first; a
+            // sample is clear after fcnt consecutive candidates (cyclic) failed
+            const int* fan = k4w_fan[threadIdx.x >> 5];
+            const int fcnt = fan[0];
+            if (fcnt == 0) {
+                visible = pending;
+                pending = false;
+            } else if (fcnt > 0) {
+                SegF g = make_segf(s, sx, sy, sz, qx, qy, qz);
+                int scanned = 0;
+                for (int i = 0; __any_sync(kFull, pending); i = i + 1 == fcnt ? 0 : i + 1) {
+                    const int k = fan[1 + i];
+                    while (pending && k4w_blocked_g<MAXV>(s, ctx, k, g, sx, sy, sz, qx, qy, qz, tests)) {
+                        scanned = 0;
+                        if (++j == 7) {
+                            pending = false;   // every sample blocked: column hidden
+                        } else {
+                            point();
+                            g = make_segf(s, sx, sy, sz, qx, qy, qz);
+                        }
+                    }
+                    if (pending && ++scanned == fcnt) {
+                        visible = true;
+                        pending = false;
+                    }
+                    if (stop_at_first && __any_sync(kFull, visible)) break;
+                }
+                pending = false;
+            }
+        }
+#endif
         for (;;) {
             const unsigned who = __ballot_sync(kFull, pending);
             if (!who) break;
