@@ -187,7 +187,7 @@ __device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const d
                                                     const SegF& g, double ax, double ay, double az, double bx,
                                                     double by, double bz, int skip0, int skip1, int home,
                                                     unsigned long long& tests, unsigned long long& batches,
-                                                    int* more = nullptr) {
+                                                    int* more = nullptr, int prio = -1) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     constexpr int GPT = kTile / kGroup;   // groups per tile (4)
     const int lane = threadIdx.x & 31;
@@ -207,18 +207,38 @@ __device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const d
             cand = r ? ((cand >> r) | (cand << (64 - r))) : cand;
         }
         const int rot = cc == 0 ? home_tile - t0 : 0;
+        // `prio`'s tile joins the first batch (second slot)
+        int ptile = -1;
+        if (prio >= 0) {
+            const int pt = prio / kTile - t0;
+            if (pt >= 0 && pt < 64 && pt != home_tile - t0) {
+                int pb = pt - rot;
+                if (pb < 0) pb += 64;
+                if ((cand >> pb) & 1ull) {
+                    cand &= ~(1ull << pb);
+                    ptile = t0 + pt;
+                }
+            }
+        }
         ++batches;
-        while (cand) {
+        while (cand || ptile >= 0) {
             // up to 8 candidate tiles -> lane (slot = lane / 4, group = lane % 4)
             int my_tile = -1;
 #pragma unroll
             for (int q = 0; q < 32 / GPT; ++q) {
-                if (!cand) break;
-                const int b = __ffsll(static_cast<long long>(cand)) - 1;
-                cand &= cand - 1;
-                int t = b + rot;
-                if (t >= 64) t -= 64;
-                if (q == lane / GPT) my_tile = t0 + t;
+                int t_abs;
+                if (ptile >= 0 && (q == 1 || !cand)) {
+                    t_abs = ptile;
+                    ptile = -1;
+                } else {
+                    if (!cand) break;
+                    const int b = __ffsll(static_cast<long long>(cand)) - 1;
+                    cand &= cand - 1;
+                    int t = b + rot;
+                    if (t >= 64) t -= 64;
+                    t_abs = t0 + t;
+                }
+                if (q == lane / GPT) my_tile = t_abs;
             }
             const int grp = my_tile * GPT + (lane % GPT);
             const bool gv = my_tile >= 0 && grp < ctx.ngroups && sat_maybe(ctx.gbox + static_cast<size_t>(grp) * 8, g);
