@@ -222,12 +222,16 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.words = (hs.n + 63) / 64;
         Arena ar;
         auto add = [&](const auto& v) { return ar.add(v.data(), v.size() * sizeof(v[0])); };
-        const auto& rec = hs.maxv <= 4 ? hs.rec4 : hs.rec8;
         ds.rec_stride = hs.maxv <= 4 ? visrt::RecLayout<4>::kStride : visrt::RecLayout<8>::kStride;
+        // device copies: the sweeps read the occluder records and culling boxes
+        // in Morton order (srec / sbox); the tree's unfolding reads the records
+        // by face index (rec: no inv[] indirection on its dependent chain)
+        const auto& rec = hs.maxv <= 4 ? hs.rec4 : hs.rec8;
         const size_t o_rec = add(rec), o_samples = add(hs.samples), o_pts = add(hs.pts), o_normal = add(hs.normal),
                      o_seg = add(hs.seg), o_aabb = add(hs.aabb), o_nv = add(hs.nv), o_ns = add(hs.ns),
-                     o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_box = add(hs.box), o_sbox = add(hs.sbox),
+                     o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_sbox = add(hs.sbox),
                      o_tbox = add(hs.tbox), o_gbox = add(hs.gbox), o_cbox = add(hs.cbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
+        const size_t data_bytes = ar.total;   // the scene data; the buffers below are device-only
         const size_t o_bits = ar.add(nullptr, static_cast<size_t>(hs.n) * ds.words * 8);
         const size_t o_counter = ar.add(nullptr, 4 * 8);
         const size_t o_count = ar.add(nullptr, 2 * 8);
@@ -245,7 +249,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
             char* st = static_cast<char*>(g_stage);
             for (const auto& pt : ar.parts)
                 if (pt.src && pt.bytes) std::memcpy(st + pt.off, pt.src, pt.bytes);
-            ck(cudaMemcpyAsync(sc->arena, g_stage, ar.total, cudaMemcpyHostToDevice, 0), "H2D scene");
+            ck(cudaMemcpyAsync(sc->arena, g_stage, data_bytes, cudaMemcpyHostToDevice, 0), "H2D scene");
             ck(cudaStreamSynchronize(0), "sync");
         }
         char* base = static_cast<char*>(sc->arena);
@@ -260,7 +264,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.ns = static_cast<const int32_t*>(at(o_ns));
         ds.orient = static_cast<const int32_t*>(at(o_orient));
         ds.seg_ok = static_cast<const int32_t*>(at(o_seg_ok));
-        ds.box = static_cast<const float*>(at(o_box));
+        ds.box = nullptr;
         ds.sbox = static_cast<const float*>(at(o_sbox));
         ds.tbox = static_cast<const float*>(at(o_tbox));
         ds.gbox = static_cast<const float*>(at(o_gbox));
@@ -274,10 +278,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.ntiles = hs.ntiles;
         ds.nchunks = hs.nchunks;
         ds.ngroups = hs.ngroups;
-        sc->upload_bytes = static_cast<int64_t>(
-            (hs.maxv <= 4 ? hs.rec4.size() : hs.rec8.size()) * 8 + hs.samples.size() * 8 + hs.pts.size() * 8 +
-            hs.normal.size() * 8 + hs.seg.size() * 8 + hs.aabb.size() * 8 + hs.nv.size() * 4 + hs.ns.size() * 4 +
-            hs.orient.size() * 4 + hs.seg_ok.size() * 4 + hs.box.size() * 4);
+        sc->upload_bytes = static_cast<int64_t>(data_bytes);   // the one H2D copy of the scene
         ds.ox = hs.origin[0];
         ds.oy = hs.origin[1];
         ds.oz = hs.origin[2];

@@ -221,8 +221,10 @@ void ingest(const visrt_facets_v1& f, HostScene& hs) {
                 const double nu = norm(u), nvv = norm(v);
                 if (nu < kEps || nvv < kEps) { miter = 1.0; continue; }   // degenerate edge: be generous
                 const double c = std::max(-1.0, std::min(1.0, dot(u, v) / (nu * nvv)));
-                const double s = std::sin(0.5 * std::acos(c));
-                miter = std::max(miter, s > 1e-12 ? 2e-9 / s : 1.0);
+                // sin(theta / 2) = sqrt((1 - cos theta) / 2), trig-free; the 1 %
+                // slack covers its rounding (a conservative margin only)
+                const double s = std::sqrt(0.5 * (1.0 - c));
+                miter = std::max(miter, s > 1e-12 ? 2.02e-9 / s : 1.0);
             }
             const double m = box_margin(hs.extent, miter);
             const double* bb = &hs.aabb[static_cast<size_t>(i) * 6];
@@ -246,8 +248,8 @@ void ingest(const visrt_facets_v1& f, HostScene& hs) {
                             &hs.rec4[static_cast<size_t>(i) * RecLayout<4>::kStride]);
         }
     }
-    hs.rec8.assign(static_cast<size_t>(n) * RecLayout<8>::kStride, 0.0);
-    for (int i = 0; i < n; ++i) {
+    if (hs.maxv > 4) hs.rec8.assign(static_cast<size_t>(n) * RecLayout<8>::kStride, 0.0);
+    for (int i = 0; i < n && hs.maxv > 4; ++i) {
         V3 pts[VISRT_MAX_VERTS];
         for (int k = 0; k < hs.nv[i]; ++k) {
             const double* p = &hs.pts[(static_cast<size_t>(i) * VISRT_MAX_VERTS + k) * 3];
