@@ -263,6 +263,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_CHUNK_CAND
 #define VISRT_K2W_CHUNK_CAND 2
 #endif
+#ifndef VISRT_K2W_SEGC
+#define VISRT_K2W_SEGC 0    // 1: the lane's first sightline's fp32 segment kept in registers per pair
+#endif
 #ifndef VISRT_K2W_PRI
 #define VISRT_K2W_PRI 0     // 1: the aim face's tile is swept second (r01: more sweeps, 4-9% slower)
 #endif
@@ -383,10 +386,27 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
         };
         // settle every unresolved sightline blocked by occluder k (Morton index)
+#if VISRT_K2W_SEGC
+        // the lane's first sightline in the fp32 culling frame, once per pair
+        SegF g0{};
+        if (unres & 1u) {
+            ends(lane);
+            g0 = make_segf(s, ax, ay, az, bx, by, bz);
+        }
+#endif
         auto resolve = [&](int k) {
             const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
             for (unsigned m = unres; m; m &= m - 1) {
                 const int r = __ffs(m) - 1;
+#if VISRT_K2W_SEGC
+                if (r == 0) {
+                    if (sat_maybe(B, g0)) {
+                        ends(lane);
+                        if (exact(k)) unres &= ~1u;
+                    }
+                    continue;
+                }
+#endif
                 ends(lane + 32 * r);
                 if ((!VISRT_K2W_RSAT || sat_maybe(B, make_segf(s, ax, ay, az, bx, by, bz))) && exact(k))
                     unres &= ~(1u << r);

@@ -544,6 +544,50 @@ __device__ __noinline__ bool k4w_blocked_g(const DevScene& s, const SweepCtx& ct
     return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
 }
 
+#ifndef VISRT_K4W_SHADOW
+#define VISRT_K4W_SHADOW 0   // 1: a face wholly in one blocker's shadow (proved with a margin) skips its scan
+                             //    (bit-identical; r01: shadows 30-45 % of hidden faces but hidden faces are cheap —
+                             //    visible faces carry ~90 % of the cycles — so no gain; off)
+#endif
+constexpr double kShadowMargin = 1e-6;   // metres; >> every fp64 rounding of the samples and predicate
+// Does occluder record R block the sightline from s to face vertex v with a
+// margin? Both ends strictly on opposite sides of R's plane by more than
+// kEps + margin, and the crossing point inside every (non-skipped) edge of R
+// by more than the margin. If this holds for EVERY vertex of a convex face,
+// it holds for every point q of the face: the signed distance of q is a
+// convex combination of the vertices' (same sign, same bound) and the
+// crossing points of s->q are the central projection of the face from s,
+// which maps the face into the convex hull of the vertices' crossing points,
+// inside the margin-inset polygon. The reference's fp64 predicate on any
+// sample sightline s->q (q on the face up to ~1e-11 m of rounding) therefore
+// returns "hit": every column of every plane is hidden and
+// illuminated_region has no region (src/vistable.cpp:287-334).
+template <int MAXV>
+__device__ __noinline__ bool shadow_blocks(const double* __restrict__ R, double sx, double sy, double sz, double vx,
+                                           double vy, double vz) {
+    constexpr double T = kEps + kShadowMargin;
+    const double Px = R[0], Py = R[1], Pz = R[2];
+    const double nx = R[3], ny = R[4], nz = R[5];
+    const double ds = dot_rel(sx, sy, sz, Px, Py, Pz, nx, ny, nz);
+    const double dv = dot_rel(vx, vy, vz, Px, Py, Pz, nx, ny, nz);
+    if (!(fabs(ds) > T && fabs(dv) > T) || dmul(ds, dv) >= 0.0) return false;
+    const double t = __ddiv_rn(ds, dsub(ds, dv));
+    const double px = dadd(sx, dmul(dsub(vx, sx), t));
+    const double py = dadd(sy, dmul(dsub(vy, sy), t));
+    const double pz = dadd(sz, dmul(dsub(vz, sz), t));
+    auto inside = [&](double ax, double ay, double az, double ix, double iy, double iz) {
+        if (ix == 0.0 && iy == 0.0 && iz == 0.0) return true;   // a skipped (too short) edge
+        return dot_rel(px, py, pz, ax, ay, az, ix, iy, iz) >= kShadowMargin;
+    };
+    if (!inside(Px, Py, Pz, R[6], R[7], R[8])) return false;
+#pragma unroll
+    for (int k = 1; k < MAXV; ++k) {
+        const double* E = R + 9 + (k - 1) * 6;
+        if (!inside(E[0], E[1], E[2], E[3], E[4], E[5])) return false;
+    }
+    return true;
+}
+
 #ifndef VISRT_K4W_PCOL
 #define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
 #endif
@@ -861,6 +905,30 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             else if (dist < 0.0) present = 0;
         }
         if (present == 1) K4P(9, 1);
+#if VISRT_K4W_SHADOW
+        if (present == 1 && !presence) {
+            // one sweep of the source -> centroid sightline; its blocker (or the
+            // warp's last one) is tested for shadowing the whole face
+            const double* C0 = s.samples + (static_cast<size_t>(f) * kMaxSamples + nv) * 3;
+            const int h = k4w_sweep<MAXV>(s, ctx, sx, sy, sz, C0[0], C0[1], C0[2], sf, sv, tests, batches);
+            const int c0 = cache.entry(0);
+            if (h >= 0) cache.put(h);
+            for (int q = 0; q < 2 && present == 1; ++q) {
+                const int k = q == 0 ? h : c0;
+                if (k < 0 || k == sf || (q == 1 && k == h)) continue;
+                const double* R = s.srec + static_cast<size_t>(k) * STRIDE;
+                bool ok = true;
+                if (lane < nv) {
+                    const double* V = s.pts + (static_cast<size_t>(f) * VISRT_MAX_VERTS + lane) * 3;
+                    ok = shadow_blocks<MAXV>(R, sx, sy, sz, V[0], V[1], V[2]);
+                }
+                if (__all_sync(kFull, ok)) {
+                    present = 0;   // wholly in k's shadow: no region
+                    K4P(15, 1);
+                }
+            }
+        }
+#endif
 #if VISRT_K4W_FAN
         if (lane == 0) fan[0] = -1;
         if (present == 1) {

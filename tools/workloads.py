@@ -10,8 +10,13 @@ CPU oracle).
 usage: python tools/workloads.py [cfg ...] > workloads.json"""
 import hashlib
 import json
+import os
 import sys
 import time
+
+# load every kernel up front: lazy module loading would charge the first launch
+# of each kernel (tens of ms) to the stage that happens to use it first
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 import numpy as np
 
