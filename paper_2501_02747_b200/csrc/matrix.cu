@@ -251,9 +251,6 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_WC
 #define VISRT_K2W_WC 4      // warp blocker-cache entries (with 16-pair grabs; 2/3/4/5/6/8 swept: 4 best)
 #endif
-#ifndef VISRT_K2W_SETTLE
-#define VISRT_K2W_SETTLE 0  // 1: lane-balanced (sightline x blocker) settling rounds (measured slower)
-#endif
 #ifndef VISRT_K2W_RSAT
 #define VISRT_K2W_RSAT 1    // fp32 SAT before the exact test when settling sightlines with a known blocker
 #endif
@@ -262,9 +259,6 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #endif
 #ifndef VISRT_K2W_CHUNK_CAND
 #define VISRT_K2W_CHUNK_CAND 2
-#endif
-#ifndef VISRT_K2W_SEGC
-#define VISRT_K2W_SEGC 0    // 1: the lane's first sightline's fp32 segment kept in registers per pair
 #endif
 #ifndef VISRT_K2W_PRI
 #define VISRT_K2W_PRI 0     // 1: the aim face's tile is swept second (r01: more sweeps, 4-9% slower)
@@ -313,15 +307,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
     __shared__ unsigned char surv_buf[kThreads / 32][64];   // per warp: surviving members of a tile, in order
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     const unsigned lt = (1u << lane) - 1u;
-#if VISRT_K2W_SETTLE
-    __shared__ unsigned char ul_buf[kThreads / 32][96];   // per warp: compacted unresolved sightlines
-    __shared__ unsigned char fl_buf[kThreads / 32][96];   // per warp: sightline blocked flags
-    unsigned char* ul = ul_buf[threadIdx.x >> 5];
-    unsigned char* fl = fl_buf[threadIdx.x >> 5];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) fl[lane + 32 * r] = 0;
-    __syncwarp();
-#endif
 
     long long pnext = 0, pend = 0;
     for (;;) {
@@ -386,79 +371,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
         };
         // settle every unresolved sightline blocked by occluder k (Morton index)
-#if VISRT_K2W_SEGC
-        // the lane's first sightline in the fp32 culling frame, once per pair
-        SegF g0{};
-        if (unres & 1u) {
-            ends(lane);
-            g0 = make_segf(s, ax, ay, az, bx, by, bz);
-        }
-#endif
         auto resolve = [&](int k) {
             const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
             for (unsigned m = unres; m; m &= m - 1) {
                 const int r = __ffs(m) - 1;
-#if VISRT_K2W_SEGC
-                if (r == 0) {
-                    if (sat_maybe(B, g0)) {
-                        ends(lane);
-                        if (exact(k)) unres &= ~1u;
-                    }
-                    continue;
-                }
-#endif
                 ends(lane + 32 * r);
                 if ((!VISRT_K2W_RSAT || sat_maybe(B, make_segf(s, ax, ay, az, bx, by, bz))) && exact(k))
                     unres &= ~(1u << r);
             }
         };
-#if VISRT_K2W_SETTLE
-        // Lane-balanced settling: lanes q < m hold candidate blockers (Morton
-        // indices; -1 / the pair's own faces are skipped). The unresolved
-        // sightlines are compacted and every lane tests one (sightline,
-        // blocker) item per round — blocker-major, so a round covers all
-        // unresolved sightlines with the first floor(32 / #unresolved)
-        // blockers — instead of each lane walking its own sightline slots
-        // (1 of 32 lanes busy on the 33rd sightline of a quad pair).
-        auto settle = [&](int kreg, int m) {
-            for (int kstart = 0; kstart < m;) {
-                int cu = 0;
-#pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    const bool b = (unres >> r) & 1u;
-                    const unsigned bb = __ballot_sync(kFull, b);
-                    if (b) ul[cu + __popc(bb & lt)] = static_cast<unsigned char>(lane + 32 * r);
-                    cu += __popc(bb);
-                }
-                if (cu == 0) return;
-                const int nb = min(cu >= 32 ? 1 : 32 / cu, m - kstart);
-                const int items = cu * nb;
-                const unsigned mgu = (65536u + cu - 1) / cu;   // w / cu = (w * mgu) >> 16 for w < 96
-                __syncwarp();
-                for (int b0 = 0; b0 < items; b0 += 32) {
-                    const int w = b0 + lane;
-                    const int q = static_cast<int>((static_cast<unsigned>(w) * mgu) >> 16);
-                    const int k = __shfl_sync(kFull, kreg, min(kstart + q, 31));
-                    if (w < items && k >= 0 && k != si && k != sj) {
-                        const int ord = ul[w - q * cu];
-                        ends(ord);
-                        if (sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, ax, ay, az, bx, by, bz)) &&
-                            exact(k))
-                            fl[ord] = 1;
-                    }
-                }
-                __syncwarp();
-#pragma unroll
-                for (int r = 0; r < 3; ++r)
-                    if (((unres >> r) & 1u) && fl[lane + 32 * r]) {
-                        unres &= ~(1u << r);
-                        fl[lane + 32 * r] = 0;
-                    }
-                __syncwarp();
-                kstart += nb;
-            }
-        };
-#endif
         bool clear = false;
         const long long pclk0 = K2CLK();
         if (may_touch(s, pi, pj)) {   // a degenerate sightline is never blocked
@@ -469,12 +390,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             }
             clear = __any_sync(kFull, degen);
         }
-#if VISRT_K2W_SETTLE
-        if (!clear) {   // the warp cache, most recent blocker first
-            const int q = (wc_next + 2 * kWC - 1 - lane) % kWC;
-            settle(__shfl_sync(kFull, wc, q), kWC);
-        }
-#else
         const long long cclk0 = K2CLK();
         if (!clear) {
             for (int i = 0; i < kWC; ++i) {   // most recent blocker first
@@ -491,7 +406,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             K2P(9, left ? 0 : 1);   // pairs settled by the cache alone
             (void)left;
         }
-#endif
         while (!clear) {
             const unsigned who = __ballot_sync(kFull, unres != 0);
             if (!who) break;   // every sightline blocked: Occluded
@@ -607,18 +521,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             const long long rclk0 = K2CLK();
             if (lane == wc_next) wc = hit;
             wc_next = wc_next + 1 == kWC ? 0 : wc_next + 1;
-#if VISRT_K2W_SETTLE
-#if VISRT_K2W_MULTI
-            settle(lane == 0 ? hit : lane == 1 ? hit2 : hit3, 3);
-#else
-            settle(hit, 1);
-#endif
-#else
             resolve(hit);
 #if VISRT_K2W_MULTI
             if (hit2 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit2);
             if (hit3 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit3);
-#endif
 #endif
             K2P(6, K2CLK() - rclk0);
         }

@@ -462,29 +462,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // The warp sweep and the fp32-SAT + exact blocker test as single out-of-line
 // copies: inlined at each call site of the lane-parallel scan and col_vis
 // they overflowed the instruction cache (ncu: stall_no_inst).
-#ifndef VISRT_K4W_FAN
-#define VISRT_K4W_FAN 0     // 1: per region, collect the faces that may block ANY sightline of the source->face fan
-                            //    and scan that list lane-parallel (lane = column / sample). Bit-identical, but r01
-                            //    measured 3-5x SLOWER (fans hold ~130-200 candidates; the hierarchical sweep
-                            //    tests a handful of member boxes per sightline), so off
-#endif
-#ifndef VISRT_K4W_FANCAP
-#define VISRT_K4W_FANCAP 511   // candidate-list capacity per warp (overflow: hierarchical sweeps)
-#endif
-#if VISRT_K4W_FAN
-// Per warp: [0] = candidate count of the current region's fan (-1: none), then the list.
-__shared__ int k4w_fan[kThreads / 32][VISRT_K4W_FANCAP + 1];
-#endif
 template <int MAXV>
 __device__ __noinline__ int k4w_sweep(const DevScene& s, const SweepCtx& ctx, double sx, double sy, double sz,
                                       double bx, double by, double bz, int sf, unsigned char* sv,
                                       unsigned long long& tests, unsigned long long& batches) {
-#if VISRT_K4W_FAN
-    const int* fan = k4w_fan[threadIdx.x >> 5];
-    if (fan[0] >= 0)
-        return list_any_hit<MAXV>(ctx, s.srec, fan + 1, fan[0], make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx,
-                                  by, bz, tests);
-#endif
     return coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz, sf, -1, sf,
                               sv, tests, batches);
 }
@@ -534,60 +515,6 @@ struct WCache {
     }
 };
 
-// Lane-level blocker test against a precomputed fp32 sightline (list scans).
-template <int MAXV>
-__device__ __noinline__ bool k4w_blocked_g(const DevScene& s, const SweepCtx& ctx, int k, const SegF& g, double sx,
-                                           double sy, double sz, double qx, double qy, double qz,
-                                           unsigned long long& tests) {
-    if (!sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, g)) return false;
-    ++tests;
-    return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
-}
-
-#ifndef VISRT_K4W_SHADOW
-#define VISRT_K4W_SHADOW 0   // 1: a face wholly in one blocker's shadow (proved with a margin) skips its scan
-                             //    (bit-identical; r01: shadows 30-45 % of hidden faces but hidden faces are cheap —
-                             //    visible faces carry ~90 % of the cycles — so no gain; off)
-#endif
-constexpr double kShadowMargin = 1e-6;   // metres; >> every fp64 rounding of the samples and predicate
-// Does occluder record R block the sightline from s to face vertex v with a
-// margin? Both ends strictly on opposite sides of R's plane by more than
-// kEps + margin, and the crossing point inside every (non-skipped) edge of R
-// by more than the margin. If this holds for EVERY vertex of a convex face,
-// it holds for every point q of the face: the signed distance of q is a
-// convex combination of the vertices' (same sign, same bound) and the
-// crossing points of s->q are the central projection of the face from s,
-// which maps the face into the convex hull of the vertices' crossing points,
-// inside the margin-inset polygon. The reference's fp64 predicate on any
-// sample sightline s->q (q on the face up to ~1e-11 m of rounding) therefore
-// returns "hit": every column of every plane is hidden and
-// illuminated_region has no region (src/vistable.cpp:287-334).
-template <int MAXV>
-__device__ __noinline__ bool shadow_blocks(const double* __restrict__ R, double sx, double sy, double sz, double vx,
-                                           double vy, double vz) {
-    constexpr double T = kEps + kShadowMargin;
-    const double Px = R[0], Py = R[1], Pz = R[2];
-    const double nx = R[3], ny = R[4], nz = R[5];
-    const double ds = dot_rel(sx, sy, sz, Px, Py, Pz, nx, ny, nz);
-    const double dv = dot_rel(vx, vy, vz, Px, Py, Pz, nx, ny, nz);
-    if (!(fabs(ds) > T && fabs(dv) > T) || dmul(ds, dv) >= 0.0) return false;
-    const double t = __ddiv_rn(ds, dsub(ds, dv));
-    const double px = dadd(sx, dmul(dsub(vx, sx), t));
-    const double py = dadd(sy, dmul(dsub(vy, sy), t));
-    const double pz = dadd(sz, dmul(dsub(vz, sz), t));
-    auto inside = [&](double ax, double ay, double az, double ix, double iy, double iz) {
-        if (ix == 0.0 && iy == 0.0 && iz == 0.0) return true;   // a skipped (too short) edge
-        return dot_rel(px, py, pz, ax, ay, az, ix, iy, iz) >= kShadowMargin;
-    };
-    if (!inside(Px, Py, Pz, R[6], R[7], R[8])) return false;
-#pragma unroll
-    for (int k = 1; k < MAXV; ++k) {
-        const double* E = R + 9 + (k - 1) * 6;
-        if (!inside(E[0], E[1], E[2], E[3], E[4], E[5])) return false;
-    }
-    return true;
-}
-
 #ifndef VISRT_K4W_PCOL
 #define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
 #endif
@@ -635,29 +562,6 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             const int k = cache.entry(i);
             if (pending && k >= 0 && k != sf && blocked_by(k)) pending = false;
         }
-#if VISRT_K4W_FAN
-        {   // the region's fan list: every lane scans it with its own sample
-            // (same face k on every lane: broadcast loads); a sample is clear
-            // after all fcnt candidates failed to block it
-            const int* fan = k4w_fan[threadIdx.x >> 5];
-            const int fcnt = fan[0];
-            if (fcnt >= 0) {
-                if (fcnt == 0) return __any_sync(kFull, pending);
-                const SegF g = make_segf(s, sx, sy, sz, qx, qy, qz);
-                int scanned = 0;
-                for (int i = 0; __any_sync(kFull, pending); i = i + 1 == fcnt ? 0 : i + 1) {
-                    const int k = fan[1 + i];
-                    bool vis = false;
-                    if (pending) {
-                        if (k4w_blocked_g<MAXV>(s, ctx, k, g, sx, sy, sz, qx, qy, qz, tests)) pending = false;
-                        else if (++scanned == fcnt) vis = true;
-                    }
-                    if (__any_sync(kFull, vis)) return true;
-                }
-                return false;
-            }
-        }
-#endif
         for (;;) {
             const unsigned who = __ballot_sync(kFull, pending);
             if (!who) return false;   // every sample blocked
@@ -767,40 +671,6 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             if (k >= 0 && k != sf) settle(k);
         }
         bool visible = false;
-#if VISRT_K4W_FAN
-        {   // the region's fan list, lane-parallel: lane = column, all lanes test
-            // the same candidate k per step (broadcast loads); a blocked sample
-            // moves the lane to its next sample, re-tested against k first; a
-            // sample is clear after fcnt consecutive candidates (cyclic) failed
-            const int* fan = k4w_fan[threadIdx.x >> 5];
-            const int fcnt = fan[0];
-            if (fcnt == 0) {
-                visible = pending;
-                pending = false;
-            } else if (fcnt > 0) {
-                SegF g = make_segf(s, sx, sy, sz, qx, qy, qz);
-                int scanned = 0;
-                for (int i = 0; __any_sync(kFull, pending); i = i + 1 == fcnt ? 0 : i + 1) {
-                    const int k = fan[1 + i];
-                    while (pending && k4w_blocked_g<MAXV>(s, ctx, k, g, sx, sy, sz, qx, qy, qz, tests)) {
-                        scanned = 0;
-                        if (++j == 7) {
-                            pending = false;   // every sample blocked: column hidden
-                        } else {
-                            point();
-                            g = make_segf(s, sx, sy, sz, qx, qy, qz);
-                        }
-                    }
-                    if (pending && ++scanned == fcnt) {
-                        visible = true;
-                        pending = false;
-                    }
-                    if (stop_at_first && __any_sync(kFull, visible)) break;
-                }
-                pending = false;
-            }
-        }
-#endif
         for (;;) {
             const unsigned who = __ballot_sync(kFull, pending);
             if (!who) break;
@@ -857,9 +727,6 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     unsigned long long tests = 0, queries = 0, batches = 0;
     WCache cache;   // the last blockers (Morton indices)
-#if VISRT_K4W_FAN
-    int* fan = k4w_fan[threadIdx.x >> 5];
-#endif
 #ifdef VISRT_K4W_PROF
     if (threadIdx.x < 16) k4w_sprof[threadIdx.x] = 0;
     __syncthreads();
@@ -905,55 +772,6 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             else if (dist < 0.0) present = 0;
         }
         if (present == 1) K4P(9, 1);
-#if VISRT_K4W_SHADOW
-        if (present == 1 && !presence) {
-            // one sweep of the source -> centroid sightline; its blocker (or the
-            // warp's last one) is tested for shadowing the whole face
-            const double* C0 = s.samples + (static_cast<size_t>(f) * kMaxSamples + nv) * 3;
-            const int h = k4w_sweep<MAXV>(s, ctx, sx, sy, sz, C0[0], C0[1], C0[2], sf, sv, tests, batches);
-            const int c0 = cache.entry(0);
-            if (h >= 0) cache.put(h);
-            for (int q = 0; q < 2 && present == 1; ++q) {
-                const int k = q == 0 ? h : c0;
-                if (k < 0 || k == sf || (q == 1 && k == h)) continue;
-                const double* R = s.srec + static_cast<size_t>(k) * STRIDE;
-                bool ok = true;
-                if (lane < nv) {
-                    const double* V = s.pts + (static_cast<size_t>(f) * VISRT_MAX_VERTS + lane) * 3;
-                    ok = shadow_blocks<MAXV>(R, sx, sy, sz, V[0], V[1], V[2]);
-                }
-                if (__all_sync(kFull, ok)) {
-                    present = 0;   // wholly in k's shadow: no region
-                    K4P(15, 1);
-                }
-            }
-        }
-#endif
-#if VISRT_K4W_FAN
-        if (lane == 0) fan[0] = -1;
-        if (present == 1) {
-            // every sightline of this region runs from the source to a point of
-            // the face, i.e. within r (circumradius about the centroid) of the
-            // source -> centroid segment: collect the faces that may block any
-            // of them once, then each sightline scans that list
-            const double* C0 = s.samples + (static_cast<size_t>(f) * kMaxSamples + nv) * 3;
-            const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
-            double r2 = 0.0;
-            for (int q = 0; q < nv; ++q) {
-                const double ex = P[3 * q] - C0[0], ey = P[3 * q + 1] - C0[1], ez = P[3 * q + 2] - C0[2];
-                r2 = fmax(r2, ex * ex + ey * ey + ez * ez);
-            }
-            const float r = static_cast<float>(sqrt(r2) * (1.0 + 1e-6)) + 0.01f;
-            __syncwarp();
-            const int c = coop_collect(ctx, make_segf(s, sx, sy, sz, C0[0], C0[1], C0[2]), r, sf, fan + 1,
-                                       VISRT_K4W_FANCAP);
-            if (lane == 0) fan[0] = c;
-            K4P(12, 1);
-            K4P(13, c < 0 ? 0 : c);
-            K4P(14, c < 0 ? 1 : 0);
-        }
-        __syncwarp();
-#endif
         for (int pl = 0; pl < 3 && present == 1; ++pl) {
             if (!s.seg_ok[3 * f + pl]) continue;
             const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;

@@ -344,99 +344,6 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
     return hit;
 }
 
-// SAT of a segment against a box dilated by r on every axis (the Minkowski sum
-// with a cube of half-size r contains the one with a ball of radius r): true
-// whenever the box may meet ANY segment whose points lie within r of the
-// corresponding points of g (a fan of sightlines from one source to the
-// points of a face of circumradius r around its centroid).
-__device__ __forceinline__ bool sat_maybe_r(const float* __restrict__ B, const SegF& g, float r) {
-    const float dx = g.mx - B[0], dy = g.my - B[1], dz = g.mz - B[2];
-    const float hx = B[4] + r, hy = B[5] + r, hz = B[6] + r;
-    bool ok = fabsf(dx) <= hx + g.ax;
-    ok &= fabsf(dy) <= hy + g.ay;
-    ok &= fabsf(dz) <= hz + g.az;
-    ok &= fabsf(__fmaf_rn(dy, g.ez, -dz * g.ey)) <= __fmaf_rn(hy, g.az, hz * g.ay);
-    ok &= fabsf(__fmaf_rn(dz, g.ex, -dx * g.ez)) <= __fmaf_rn(hx, g.az, hz * g.ax);
-    ok &= fabsf(__fmaf_rn(dx, g.ey, -dy * g.ex)) <= __fmaf_rn(hx, g.ay, hy * g.ax);
-    return ok;
-}
-
-// Candidate collection for a fan of sightlines (warp-cooperative, all lanes):
-// every face (Morton index, `skip` excluded) whose member box may meet a
-// segment within r of g, through the same chunk -> tile -> (group) -> member
-// hierarchy with every box dilated by r. Writes them to out[0..cnt) in Morton
-// order and returns cnt, or -1 when more than `cap` faces qualify.
-__device__ __forceinline__ int coop_collect(const SweepCtx& ctx, const SegF& g, float r, int skip, int* out,
-                                            int cap) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    int cnt = 0;
-    for (int c = 0; c < ctx.nchunks; ++c) {
-        if (ctx.nchunks > 1 && !sat_maybe_r(ctx.cbox + static_cast<size_t>(c) * 8, g, r)) continue;
-        const int t0 = c * kTile;
-        const int tc = min(kTile, ctx.ntiles - t0);
-        const bool h0 = lane < tc && sat_maybe_r(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g, r);
-        const bool h1 = lane + 32 < tc && sat_maybe_r(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g, r);
-        unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
-                                  (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
-        while (cand) {
-            const int base = (t0 + __ffsll(static_cast<long long>(cand)) - 1) * kTile;
-            cand &= cand - 1;
-            unsigned long long gm = ~0ull;   // 16-face groups of the tile worth testing (bit per member)
-            if (ctx.gbox) {
-                const int grp = base / kGroup + (lane & 3);
-                const bool gv = lane < 4 && grp < ctx.ngroups && sat_maybe_r(ctx.gbox + static_cast<size_t>(grp) * 8, g, r);
-                const unsigned gb = __ballot_sync(kFull, gv) & 0xfu;
-                if (!gb) continue;
-                gm = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (gb & (1u << q)) gm |= 0xffffull << (16 * q);
-            }
-            const int mc = min(kTile, ctx.n - base);
-            const int m0 = base + lane, m1 = base + lane + 32;
-            const bool v0 = lane < mc && ((gm >> lane) & 1ull) && m0 != skip &&
-                            sat_maybe_r(ctx.mbox + static_cast<size_t>(m0) * 8, g, r);
-            const bool v1 = lane + 32 < mc && ((gm >> (lane + 32)) & 1ull) && m1 != skip &&
-                            sat_maybe_r(ctx.mbox + static_cast<size_t>(m1) * 8, g, r);
-            const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
-            const int clo = __popc(lo), tot = clo + __popc(hi);
-            if (cnt + tot > cap) return -1;
-            if (v0) out[cnt + __popc(lo & lt)] = m0;
-            if (v1) out[cnt + clo + __popc(hi & lt)] = m1;
-            cnt += tot;
-        }
-    }
-    __syncwarp();
-    return cnt;
-}
-
-// Any-hit of ONE segment over a collected candidate list (all lanes): the
-// lanes take 32 candidates at a time (thin fp32 SAT, then the exact
-// predicate). Returns the Morton index of a blocking face or -1.
-template <int MAXV>
-__device__ __forceinline__ int list_any_hit(const SweepCtx& ctx, const double* __restrict__ srec, const int* lst,
-                                            int cnt, const SegF& g, double ax, double ay, double az, double bx,
-                                            double by, double bz, unsigned long long& tests) {
-    constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    const int lane = threadIdx.x & 31;
-    for (int b0 = 0; b0 < cnt; b0 += 32) {
-        const int idx = b0 + lane;
-        int k = -1;
-        bool h = false;
-        if (idx < cnt) {
-            k = lst[idx];
-            if (sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, g)) {
-                ++tests;
-                h = seg_hits<MAXV>(srec + static_cast<size_t>(k) * STRIDE, ax, ay, az, bx, by, bz);
-            }
-        }
-        const unsigned hb = __ballot_sync(kFull, h);
-        if (hb) return __shfl_sync(kFull, k, __ffs(hb) - 1);
-    }
-    return -1;
-}
-
 // Block setup: stage the tile boxes (and the member boxes when RESIDENT) in
 // shared memory with TMA bulk copies (cp.async.bulk, one mbarrier).
 template <bool RESIDENT>

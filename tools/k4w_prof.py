@@ -21,5 +21,4 @@ for arg in sys.argv[1:] or ["5:20:rx", "5:20:tx", "3:200:mix"]:
     print(f"cfg{cfg}/{which} nsrc={nsrc}: {st['ms']:.1f} ms; task cycles {o[8]:.3e}: scan {100*o[0]/tot:.1f}% "
           f"refine {100*o[1]/tot:.1f}% present-tasks {100*o[10]/tot:.1f}% ({o[11]} of {o[9]} front-facing); "
           f"scan sweeps {o[2]} clear {o[3]}; refine calls {o[6]} iters {o[7]} sweeps {o[4]} clear {o[5]}; "
-          f"cycles/sweep scan {o[0]/max(o[2],1):.0f} refine {o[1]/max(o[4],1):.0f}; fans {o[12]} "
-          f"avg list {o[13]/max(o[12]-o[14],1):.1f} overflow {o[14]}; shadowed faces {o[15]}", flush=True)
+          f"cycles/sweep scan {o[0]/max(o[2],1):.0f} refine {o[1]/max(o[4],1):.0f}", flush=True)
