@@ -135,8 +135,9 @@ def test_matrix_lane_and_warp_kernels_agree(cfg):
             "print(json.dumps([hashlib.sha256(b.tobytes()).hexdigest(), hashlib.sha256(a.tobytes()).hexdigest()]))"
             ) % (os.path.dirname(os.path.dirname(__file__)), cfg)
     out = {}
-    for warp, force in (("0", "0"), ("1", "0"), ("1", "1")):
-        env = dict(os.environ, VISRT_K2_WARP=warp, VISRT_FORCE_STREAM=force)
+    # lane kernel; warp kernel resident; streamed with the group level; streamed flat
+    for warp, force, grouped in (("0", "0", "1"), ("1", "0", "1"), ("1", "1", "1"), ("1", "1", "0")):
+        env = dict(os.environ, VISRT_K2_WARP=warp, VISRT_FORCE_STREAM=force, VISRT_K2W_GROUPED=grouped)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
-        out[warp + force] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert out["00"] == out["10"] == out["11"]
+        out[warp + force + grouped] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["001"] == out["101"] == out["111"] == out["110"]
