@@ -156,6 +156,24 @@ def cpu_baseline(soup, seconds: float = 10.0):
                       f"threads ({el:.1f} s)"}
 
 
+def _hbm_peak_gbs() -> tuple:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except Exception:
+        return 6536.0, "fallback (B200_PROFILING.md)"
+
+
+def _hbm_roofline(alg_bytes: float, ms: float, basis: str) -> dict:
+    """Algorithmic bytes of a table / frontier launch against the HBM peak
+    (regions = the scene state read once + the region records
+    written; image tree = 80 B per node)."""
+    peak, src = _hbm_peak_gbs()
+    gbs = alg_bytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "alg_bytes": alg_bytes, "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "frac": gbs / peak, "basis": basis, "peak_source": src}
+
+
 def secondary_measurements(stream: int):
     """The other hot-path subsystems, timed with the library's CUDA events on
     the same stream (outside the headline's timed region, rank 0, N = 1)."""
@@ -183,13 +201,16 @@ def secondary_measurements(stream: int):
         src = np.concatenate([wl5.tx[:10], wl5.rx[:10]])
         arr, st = point_regions_array(sc, src)
         out["regions_config5"] = {"snapshots": len(src), "facets": sc.n, "ms": st["ms"],
-                                  "regions_per_s": arr.size / (st["ms"] * 1e-3), "ms_per_snapshot": st["ms"] / len(src)}
+                                  "regions_per_s": arr.size / (st["ms"] * 1e-3), "ms_per_snapshot": st["ms"] / len(src),
+                                  "roofline": _hbm_roofline(arr.nbytes + sc.upload_bytes, st["ms"],
+                                                            "region records written + scene state read once")}
         tri, _ = chain_triples(sc)
         tr = Tracer(sc, 3, triples=tri)
         tr.trace_raw(wl5.tx[:4], wl5.rx[:4])
         _, _, nodes, tst = tr.trace_raw(wl5.tx[:200], wl5.rx[:200])
         out["tree_config5_order3"] = {"snapshots": 200, "nodes": tst["nodes"], "ms": tst["ms"],
-                                      "ms_per_snapshot": tst["ms"] / 200, "paths": tst["paths"]}
+                                      "ms_per_snapshot": tst["ms"] / 200, "paths": tst["paths"],
+                                      "roofline": _hbm_roofline(80.0 * tst["nodes"], tst["ms"], "80 B per node")}
         tr.close()
     # (2) per-snapshot Tx/Rx -> facet regions, config 3 (Tx and Rx snapshots)
     wl = scenes.workload(3)
@@ -200,7 +221,9 @@ def secondary_measurements(stream: int):
         out["regions_config3"] = {"snapshots": len(src), "facets": sc.n, "ms": st["ms"],
                                   "regions_per_s": arr.size / (st["ms"] * 1e-3),
                                   "ms_per_snapshot": st["ms"] / len(src),
-                                  "sightlines": st["candidates"], "exact_tests": st["tests_exec"]}
+                                  "sightlines": st["candidates"], "exact_tests": st["tests_exec"],
+                                  "roofline": _hbm_roofline(arr.nbytes + sc.upload_bytes, st["ms"],
+                                                            "region records written + scene state read once")}
         # (3) order-2 chains + image tree order 3, config 3
         sc.pair_visibility("prefiltered", copy_bits=False)
         tri, sch = chain_triples(sc)
@@ -211,7 +234,8 @@ def secondary_measurements(stream: int):
         _, _, nodes, tst = tr.trace_raw(wl.tx[:50], wl.rx[:50])
         out["tree_config3_order3"] = {"snapshots": 50, "nodes": tst["nodes"], "ms": tst["ms"],
                                       "nodes_per_s": tst["nodes"] / (tst["ms"] * 1e-3),
-                                      "ms_per_snapshot": tst["ms"] / 50, "paths": tst["paths"]}
+                                      "ms_per_snapshot": tst["ms"] / 50, "paths": tst["paths"],
+                                      "roofline": _hbm_roofline(80.0 * tst["nodes"], tst["ms"], "80 B per node")}
         tr.close()
     wl1 = scenes.workload(1)
     with Scene(wl1.scene) as sc:
