@@ -210,21 +210,32 @@ def trajectory_vis_table(scene: Scene, waypoints, entries: np.ndarray, max_order
     wp = np.ascontiguousarray(np.asarray(waypoints, np.float64)[:, :3]).reshape(-1)
     if matrix_max_order is not None and matrix_max_order < max_order:
         raise _capi.VisibilityError(f"matrix holds orders up to {matrix_max_order}, requested {max_order}")
-    nv = np.diff(scene.soup.vert_off)
-    corner = {(f, k): f"{ids[f]}#{k}" for f in range(n) for k in range(int(nv[f]))}
-    kr = _ranks(list(ids) + list(corner.values()) + ["transmitter"])
-    key_rank = np.zeros(9 * n + 1, np.int32)
-    key_rank[:n] = [kr[i] for i in ids]
-    for (f, k), s in corner.items():
-        key_rank[n + 8 * f + k] = kr[s]
-    key_rank[9 * n] = kr["transmitter"]
-    lab = [(labels_xy[f] if labels_xy is not None and labels_xy[f] else ids[f]) for f in range(n)]
-    pr = _ranks(lab + ["transmitter"])
-    parent_rank = np.array([pr[s] for s in lab] + [pr["transmitter"]], np.int32)
-    bname = [("ground" if building is None or building[f] < 0 or not building_names else building_names[building[f]])
-             for f in range(n)]
-    br = _ranks(bname)
-    building_rank = np.array([br[s] for s in bname], np.int32)
+    # the reference's string orders as integer ranks (SigKey / row sorts);
+    # cached per scene and naming, since they cost more than the GPU work on
+    # 20k-facet scenes
+    nkey = (tuple(ids), None if labels_xy is None else tuple(labels_xy),
+            None if building is None else tuple(int(b) for b in building),
+            None if building_names is None else tuple(building_names))
+    cache = scene.__dict__.setdefault("_traj_names", {})
+    if nkey not in cache:
+        nv = np.diff(scene.soup.vert_off)
+        corner = {(f, k): f"{ids[f]}#{k}" for f in range(n) for k in range(int(nv[f]))}
+        kr = _ranks(list(ids) + list(corner.values()) + ["transmitter"])
+        key_rank = np.zeros(9 * n + 1, np.int32)
+        key_rank[:n] = [kr[i] for i in ids]
+        for (f, k), s in corner.items():
+            key_rank[n + 8 * f + k] = kr[s]
+        key_rank[9 * n] = kr["transmitter"]
+        lab = [(labels_xy[f] if labels_xy is not None and labels_xy[f] else ids[f]) for f in range(n)]
+        pr = _ranks(lab + ["transmitter"])
+        parent_rank = np.array([pr[s] for s in lab] + [pr["transmitter"]], np.int32)
+        bname = [("ground" if building is None or building[f] < 0 or not building_names
+                  else building_names[building[f]]) for f in range(n)]
+        br = _ranks(bname)
+        building_rank = np.array([br[s] for s in bname], np.int32)
+        cache.clear()
+        cache[nkey] = (key_rank, parent_rank, building_rank, lab, br)
+    key_rank, parent_rank, building_rank, lab, br = cache[nkey]
     names = _capi.visrt_names(key_rank.ctypes.data, parent_rank.ctypes.data, building_rank.ctypes.data)
     ent = np.ascontiguousarray(entries, ENTRY_DTYPE)
     h = C.c_void_p()

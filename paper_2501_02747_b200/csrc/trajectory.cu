@@ -66,17 +66,59 @@ __device__ __forceinline__ bool plan_blocks(double px, double py, double qx, dou
     return t > 1e-9 && t < 1.0 - 1e-9 && u > 1e-9 && u < 1.0 - 1e-9;
 }
 
-// plan_sightline_clear (584-592): every lane tests faces lane, lane+32, ...
+// Conservative fp32 test of a plan-view (xy) segment against the xy footprint
+// of a culling box (2 box axes + the segment normal). A plan blocker's xy
+// segment crosses the query strictly inside both, so its face's box (dilated
+// by box_margin(), which bounds the fp32 rounding) passes: one-sided culling.
+struct Seg2F {
+    float mx, my, ex, ey, ax, ay;
+};
+__device__ __forceinline__ Seg2F make_seg2f(const DevScene& s, double px, double py, double qx, double qy) {
+    Seg2F g;
+    g.mx = static_cast<float>(0.5 * (px + qx) - s.ox);
+    g.my = static_cast<float>(0.5 * (py + qy) - s.oy);
+    g.ex = static_cast<float>(0.5 * (qx - px));
+    g.ey = static_cast<float>(0.5 * (qy - py));
+    g.ax = fabsf(g.ex);
+    g.ay = fabsf(g.ey);
+    return g;
+}
+__device__ __forceinline__ bool sat2_maybe(const float* __restrict__ B, const Seg2F& g) {
+    const float dx = g.mx - B[0], dy = g.my - B[1];
+    const float hx = B[4], hy = B[5];
+    bool ok = fabsf(dx) <= hx + g.ax;
+    ok &= fabsf(dy) <= hy + g.ay;
+    ok &= fabsf(__fmaf_rn(dx, g.ey, -dy * g.ex)) <= __fmaf_rn(hx, g.ay, hy * g.ax);
+    return ok;
+}
+
+// plan_sightline_clear (584-592): any face's xy segment strictly crossing p->q
+// blocks. Culled over the Morton hierarchy: lanes test tile footprints, then
+// the members of each candidate tile (2 per lane), exact plan_blocks on the
+// survivors (face index perm[m]).
 __device__ bool plan_clear_warp(const DevScene& s, double px, double py, double qx, double qy, int skip) {
     const int lane = threadIdx.x & 31;
-    for (int base = 0; base < s.n; base += 32) {
-        const int f = base + lane;
-        bool hit = false;
-        if (f < s.n && f != skip && s.seg_ok[3 * f]) {
-            const double* g = s.seg + static_cast<size_t>(f) * 18;
-            hit = plan_blocks(px, py, qx, qy, g[0], g[1], g[2], g[3]);
+    const Seg2F g = make_seg2f(s, px, py, qx, qy);
+    for (int t0 = 0; t0 < s.ntiles; t0 += 32) {
+        const int t = t0 + lane;
+        unsigned cand = __ballot_sync(kFull, t < s.ntiles && sat2_maybe(s.tbox + static_cast<size_t>(t) * 8, g));
+        while (cand) {
+            const int base = (t0 + __ffs(cand) - 1) * 64;
+            cand &= cand - 1;
+            bool hit = false;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int m = base + lane + 32 * h;
+                if (m < s.n && sat2_maybe(s.sbox + static_cast<size_t>(m) * 8, g)) {
+                    const int f = s.perm[m];
+                    if (f != skip && s.seg_ok[3 * f]) {
+                        const double* sg = s.seg + static_cast<size_t>(f) * 18;
+                        hit |= plan_blocks(px, py, qx, qy, sg[0], sg[1], sg[2], sg[3]);
+                    }
+                }
+            }
+            if (__any_sync(kFull, hit)) return false;
         }
-        if (__any_sync(kFull, hit)) return false;
     }
     return true;
 }
@@ -208,10 +250,25 @@ __global__ void __launch_bounds__(256) k_seg_hits(DevScene s, int nseg, const do
     for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nseg; q += (gridDim.x * blockDim.x) >> 5) {
         const double ax = A[3 * q], ay = A[3 * q + 1], az = A[3 * q + 2];
         const double bx = B[3 * q], by = B[3 * q + 1], bz = B[3 * q + 2];
-        for (int f = lane; f < s.n; f += 32) {
-            if (f == skip[q]) continue;
-            if (seg_hits<MAXV>(s.srec + static_cast<size_t>(s.inv[f]) * STRIDE, ax, ay, az, bx, by, bz))
-                atomicOr(hits + static_cast<size_t>(q) * words + (f >> 5), 1u << (f & 31));
+        // every hit, culled: tile boxes, then the members of candidate tiles
+        // (a true hit lies in its face's dilated box: sweep.h)
+        const SegF g = make_segf(s, ax, ay, az, bx, by, bz);
+        for (int t0 = 0; t0 < s.ntiles; t0 += 32) {
+            const int t = t0 + lane;
+            unsigned cand = __ballot_sync(kFull, t < s.ntiles && sat_maybe(s.tbox + static_cast<size_t>(t) * 8, g));
+            while (cand) {
+                const int base = (t0 + __ffs(cand) - 1) * 64;
+                cand &= cand - 1;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = base + lane + 32 * h;
+                    if (m >= s.n || !sat_maybe(s.sbox + static_cast<size_t>(m) * 8, g)) continue;
+                    const int f = s.perm[m];
+                    if (f == skip[q]) continue;
+                    if (seg_hits<MAXV>(s.srec + static_cast<size_t>(m) * STRIDE, ax, ay, az, bx, by, bz))
+                        atomicOr(hits + static_cast<size_t>(q) * words + (f >> 5), 1u << (f & 31));
+                }
+            }
         }
     }
 }
