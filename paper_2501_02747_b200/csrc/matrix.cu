@@ -257,6 +257,12 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_CHUNK
 #define VISRT_K2W_CHUNK 16  // consecutive pairs per warp grab (r01 sweep 1/4/8/12/16/32: 16 best)
 #endif
+#ifndef VISRT_K2W_TR
+#define VISRT_K2W_TR 2      // large all-pairs launches grab TR x TC tiles of the pair matrix
+#endif
+#ifndef VISRT_K2W_TC
+#define VISRT_K2W_TC 16
+#endif
 #ifndef VISRT_K2W_CHUNK_CAND
 #define VISRT_K2W_CHUNK_CAND 2
 #endif
@@ -309,7 +315,39 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
     const unsigned lt = (1u << lane) - 1u;
 
     long long pnext = 0, pend = 0;
+    int tI = 0, tJ = 0, tl = 0, tl_end = 0;   // tiled grabs: current tile origin and cursor
+    const bool tiled = a.tiled != 0;
+    const int ntc = (n + VISRT_K2W_TC - 1) / VISRT_K2W_TC;
+    const long long ntiles_all = static_cast<long long>((n + VISRT_K2W_TR - 1) / VISRT_K2W_TR) * ntc;
     for (;;) {
+        long long p = 0;
+        int pi = 0, pj = 0;
+        if (tiled) {
+            // a warp takes a VISRT_K2W_TR x VISRT_K2W_TC tile of the pair matrix
+            // (neighbouring reference AND aim faces: the warp cache stays warm)
+            bool got = false, done = false;
+            while (!got) {
+                if (tl == tl_end) {
+                    unsigned long long tw = 0;
+                    if (lane == 0) tw = atomicAdd(&a.counter[0], 1ull);
+                    const long long T = static_cast<long long>(__shfl_sync(kFull, tw, 0));
+                    if (T >= ntiles_all) {
+                        done = true;
+                        break;
+                    }
+                    tI = static_cast<int>(T / ntc) * VISRT_K2W_TR;
+                    tJ = static_cast<int>(T % ntc) * VISRT_K2W_TC;
+                    tl = 0;
+                    tl_end = tJ + VISRT_K2W_TC - 1 > tI ? VISRT_K2W_TR * VISRT_K2W_TC : 0;   // skip tiles below the diagonal
+                    continue;
+                }
+                const int l = tl++;
+                pi = tI + l / VISRT_K2W_TC;
+                pj = tJ + l % VISRT_K2W_TC;
+                got = pi < n && pj < n && pj > pi;
+            }
+            if (done) break;
+        } else {
         // a warp takes VISRT_K2W_CHUNK consecutive pairs at a time: row-major
         // neighbours share the reference face (and its blockers: warp cache)
         if (pnext == pend) {
@@ -319,8 +357,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             if (pnext >= a.npairs) break;
             pend = min(pnext + a.chunk, a.npairs);
         }
-        const long long p = pnext++;
-        int pi, pj;
+        p = pnext++;
         if (a.ci) {
             pi = a.ci[p];
             pj = a.cj[p];
@@ -336,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                 pj = oi < oj ? oj : oi;
             }
 #endif
+        }
         }
         const int si = s.inv[pi], sj = s.inv[pj];
         const int nr = s.nv[pi], na = s.nv[pj];
@@ -751,11 +789,16 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
     // all-pairs rows share the reference face over long runs; candidate lists are
     // short and sparse, where big grabs only unbalance the tail
     a.chunk = a.ci ? VISRT_K2W_CHUNK_CAND : VISRT_K2W_CHUNK;
+    // all-pairs launches with >= 512 pairs per resident warp (configs 3-5) grab
+    // 2 x 16 tiles of the pair matrix (r01: config 4 915 -> 831 ms, config 3
+    // 12.9 -> 12.3 ms); smaller ones keep 16-pair rows (config 2: tiles of 32
+    // pairs unbalance the tail)
     {   // keep >= 8 grabs per resident warp (small scenes: config 1 has 6,670 pairs)
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const long long warps = static_cast<long long>(sms) * 3 * (kThreads / 32);
         a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(a.chunk, a.npairs / (8 * warps))));
+        a.tiled = (VISRT_K2W_TR > 1 && !a.ci && a.stride == 1 && a.npairs >= 512 * warps) ? 1 : 0;
     }
     if (a.stride > 1) a.npairs = (a.npairs + a.stride - 1) / a.stride;
     // K2w keeps the member boxes resident only while 3 CTAs still fit per SM:
