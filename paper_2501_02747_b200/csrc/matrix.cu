@@ -257,6 +257,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_CHUNK
 #define VISRT_K2W_CHUNK 16  // consecutive pairs per warp grab (r01 sweep 1/4/8/12/16/32: 16 best)
 #endif
+#ifndef VISRT_K2W_HISLOT
+#define VISRT_K2W_HISLOT 0  // 1: sweep the highest-slot unresolved sightline first (r01: -1 % config 2, +4 % config 3)
+#endif
 #ifndef VISRT_K2W_TR
 #define VISRT_K2W_TR 2      // large all-pairs launches grab TR x TC tiles of the pair matrix
 #endif
@@ -447,8 +450,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
         while (!clear) {
             const unsigned who = __ballot_sync(kFull, unres != 0);
             if (!who) break;   // every sightline blocked: Occluded
-            const int L = __ffs(who) - 1;
-            const int r0 = __ffs(__shfl_sync(kFull, unres, L)) - 1;
+            int L = __ffs(who) - 1;
+            int r0 = __ffs(__shfl_sync(kFull, unres, L)) - 1;
+#if VISRT_K2W_HISLOT
+            // sweep a sightline of the highest occupied slot first (lane 0's
+            // 33rd sightline of a quad pair): once it is settled, every resolve
+            // pass over the pair is a single lane iteration
+            for (int r = 2; r > 0; --r) {
+                const unsigned wr = __ballot_sync(kFull, (unres >> r) & 1u);
+                if (wr) {
+                    L = __ffs(wr) - 1;
+                    r0 = r;
+                    break;
+                }
+            }
+#endif
             ends(L + 32 * r0);   // the swept sightline, uniform across the warp
             const SegF g = make_segf(s, ax, ay, az, bx, by, bz);
             ++sweeps;
@@ -557,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                 break;
             }
             const long long rclk0 = K2CLK();
+            if (lane == L) unres &= ~(1u << r0);   // the swept sightline: its sweep found `hit` blocking it
             if (lane == wc_next) wc = hit;
             wc_next = wc_next + 1 == kWC ? 0 : wc_next + 1;
             resolve(hit);
