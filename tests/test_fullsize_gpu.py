@@ -114,3 +114,26 @@ def test_trace_order3_sampled(oracle_built, cfg, nsnap):
         key = lambda p: (len(p["faces"]), tuple(p["faces"]), tuple(p["points"]), p["length"])
         assert sorted(map(key, paths[q])) == sorted(map(key, exp))
         assert nodes[q] == est[0]
+
+
+def test_matrix_config2_full_vs_reference(oracle_built):
+    """The WHOLE config-2 matrix against the unmodified reference (oracle/_ref,
+    all host threads): (B) occlusion_judgment on all 788,140 pairs and (A)
+    build_matrix(scene, 1).pair_admitted — bit-identical, no sampling."""
+    if not oracle_built.have_ref():
+        pytest.skip("oracle/_ref not built")
+    soup = scenes.workload(2).scene
+    n = soup.nfaces
+    with Scene(soup) as sc:
+        bits_b, _ = sc.pair_visibility("all")
+        bits_a, _ = sc.pair_visibility("prefiltered")
+    r = oracle_built.RefOracle(soup)
+    pi, pj = np.triu_indices(n, 1)
+    kinds = r.occlusion_batch(pi.astype(np.int32), pj.astype(np.int32))
+    M = unpack_bits(bits_b, n)
+    np.testing.assert_array_equal(M[pi, pj], kinds != 2)
+    adm = np.zeros((n, n), bool)
+    for e in r.matrix_entries(r.build_matrix(1)):
+        if e["order"] == 1:
+            adm[e["chain"][0], e["chain"][1]] = True
+    np.testing.assert_array_equal(unpack_bits(bits_a, n), adm)
