@@ -437,8 +437,11 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
 // and unfolded on the spot instead of being written as a frontier level and
 // read back — the deepest level is most of the tree (config 3 order 3: 4.3M of
 // 4.3M nodes per snapshot), so this removes its node rows from HBM entirely.
+#ifndef VISRT_K6L_MINB
+#define VISRT_K6L_MINB 3   // CTAs per SM the fused last level's register budget targets (r01: 1/3/4 -> 3 best, -2 %)
+#endif
 template <int MAXV>
-__global__ void __launch_bounds__(256) k_tree_last(TreeArgs a, unsigned long long* cnt) {
+__global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, unsigned long long* cnt) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -933,8 +936,16 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
                     const long long np = in ? nin : ns;
                     ck(cudaMemsetAsync(c_ncand, 0, 8, st), "memset");
                     ck(cudaMemsetAsync(d_ctr + 3, 0, 8, st), "memset");
-                    if (ds.maxv <= 4) visrt::k_tree_last<4><<<eb, 256, 0, st>>>(a, tr->cnt);
-                    else visrt::k_tree_last<8><<<eb, 256, 0, st>>>(a, tr->cnt);
+                    // grid = the fused kernel's own residency (one wave)
+                    if (ds.maxv <= 4) {
+                        static const int lb4 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<4>),
+                                                              256, 0, device);
+                        visrt::k_tree_last<4><<<lb4, 256, 0, st>>>(a, tr->cnt);
+                    } else {
+                        static const int lb8 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<8>),
+                                                              256, 0, device);
+                        visrt::k_tree_last<8><<<lb8, 256, 0, st>>>(a, tr->cnt);
+                    }
                     ck(cudaGetLastError(), "k_tree_last");
                     ck(cub::DeviceScan::ExclusiveSum(tr->scan_tmp, tr->scan_bytes, tr->cnt, tr->off, np + 1, st), "scan");
                     visrt::k_tree_snapcount_parents<<<(ns + 255) / 256, 256, 0, st>>>(in, np, tr->off, s0, ns, d_nodes);
