@@ -441,12 +441,16 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
 #define VISRT_K6L_MINB 3   // CTAs per SM the fused last level's register budget targets (r01: 1/3/4 -> 3 best, -2 %)
 #endif
 template <int MAXV>
-__global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, unsigned long long* cnt) {
+__global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, unsigned long long* cnt,
+                                                                   unsigned long long* pcur) {
     const int lane = threadIdx.x & 31;
-    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
-    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const long long nparents = a.in ? a.nin : a.nsnap;
-    for (long long p = warp; p < nparents; p += nwarps) {
+    for (;;) {
+        // parents grabbed dynamically: pool sizes vary widely between parents
+        unsigned long long pw = 0;
+        if (lane == 0) pw = atomicAdd(pcur, 1ull);
+        const long long p = static_cast<long long>(__shfl_sync(kFull, pw, 0));
+        if (p >= nparents) break;
         const TreeNode par = tree_parent(a, p);
         const Pool P = tree_pool(a, par, a.s.n);
         const int fp[4] = {par.f0, par.f1, par.f2, par.f3};
@@ -935,16 +939,17 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
                     // deepest level: count + unfold fused, no frontier rows
                     const long long np = in ? nin : ns;
                     ck(cudaMemsetAsync(c_ncand, 0, 8, st), "memset");
-                    ck(cudaMemsetAsync(d_ctr + 3, 0, 8, st), "memset");
+                    ck(cudaMemsetAsync(d_ctr + 3, 0, 8, st), "memset");   // legs cursor
+                    ck(cudaMemsetAsync(d_ctr + 5, 0, 8, st), "memset");   // k_tree_last parent cursor
                     // grid = the fused kernel's own residency (one wave)
                     if (ds.maxv <= 4) {
                         static const int lb4 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<4>),
                                                               256, 0, device);
-                        visrt::k_tree_last<4><<<lb4, 256, 0, st>>>(a, tr->cnt);
+                        visrt::k_tree_last<4><<<lb4, 256, 0, st>>>(a, tr->cnt, d_ctr + 5);
                     } else {
                         static const int lb8 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<8>),
                                                               256, 0, device);
-                        visrt::k_tree_last<8><<<lb8, 256, 0, st>>>(a, tr->cnt);
+                        visrt::k_tree_last<8><<<lb8, 256, 0, st>>>(a, tr->cnt, d_ctr + 5);
                     }
                     ck(cudaGetLastError(), "k_tree_last");
                     ck(cub::DeviceScan::ExclusiveSum(tr->scan_tmp, tr->scan_bytes, tr->cnt, tr->off, np + 1, st), "scan");
