@@ -437,6 +437,12 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
 // and unfolded on the spot instead of being written as a frontier level and
 // read back — the deepest level is most of the tree (config 3 order 3: 4.3M of
 // 4.3M nodes per snapshot), so this removes its node rows from HBM entirely.
+#ifndef VISRT_K6L_COMPACT
+#define VISRT_K6L_COMPACT 1   // 1: pruned-in children compacted before the unfold
+#endif
+#if VISRT_K6L_COMPACT
+__shared__ int k6l_buf[8][64];   // per warp (256 threads): pending children of the current parent
+#endif
 #ifndef VISRT_K6L_MINB
 #define VISRT_K6L_MINB 3   // CTAs per SM the fused last level's register budget targets (r01: 1/3/4 -> 3 best, -2 %)
 #endif
@@ -455,6 +461,39 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
         const Pool P = tree_pool(a, par, a.s.n);
         const int fp[4] = {par.f0, par.f1, par.f2, par.f3};
         unsigned long long c_all = 0;
+#if VISRT_K6L_COMPACT
+        // the children that pass the prune are compacted through shared memory
+        // and unfolded 32 at a time (full lanes on the heavy unfold)
+        int* buf = k6l_buf[threadIdx.x >> 5];
+        int pend = 0;
+        auto unfold_batch = [&](int m) {
+            const int c = lane < m ? buf[lane] : -1;
+            __syncwarp();
+            if (c >= 0) {
+                int f[4] = {fp[0], fp[1], fp[2], fp[3]};
+                f[P.d] = c;
+                unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1);
+            }
+        };
+        for (long long q0 = 0; q0 < P.npool; q0 += 32) {
+            const long long q = q0 + lane;
+            int c = -1, rank;
+            const bool ok = q < P.npool && tree_child(a, par, P, q, c, rank);
+            const unsigned ob = __ballot_sync(kFull, ok);
+            c_all += __popc(ob);
+            if (ok) buf[pend + __popc(ob & ((1u << lane) - 1u))] = c;
+            pend += __popc(ob);
+            __syncwarp();
+            if (pend >= 32) {
+                unfold_batch(32);
+                pend -= 32;
+                if (lane < pend) buf[lane] = buf[32 + lane];
+                __syncwarp();
+            }
+        }
+        if (pend > 0) unfold_batch(pend);
+        __syncwarp();
+#else
         for (long long q0 = 0; q0 < P.npool; q0 += 32) {
             const long long q = q0 + lane;
             int c = -1, rank;
@@ -466,6 +505,7 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
                 unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1);
             }
         }
+#endif
         if (lane == 0) cnt[p] = c_all;
     }
 }
