@@ -493,6 +493,9 @@ __device__ unsigned long long g_k4w_prof[16];
 #define K4CLK() 0ll
 #endif
 
+#ifndef VISRT_K4W_FACEMAJOR
+#define VISRT_K4W_FACEMAJOR 1   // all-pairs tasks walk face-major: neighbouring warps take one face for consecutive snapshots (r01: config 3 -12 %, config-5 Tx -9 %, Rx -2.5 %)
+#endif
 #ifndef VISRT_K4W_WC
 #define VISRT_K4W_WC 1   // warp blocker-cache entries, most recent first (r01: 1/2/4/8 swept; 4 helps config-5 Tx, hurts config 3)
 #endif
@@ -744,8 +747,14 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
         long long k;
         int f;
         if (!a.task_face) {
+            if (VISRT_K4W_FACEMAJOR) {   // consecutive tasks: one face, consecutive snapshot sources
+                const long long nsrc = a.ntasks / n;
+                f = static_cast<int>(t / nsrc);
+                k = t - static_cast<long long>(f) * nsrc;
+            } else {
             k = t / n;
             f = static_cast<int>(t - k * n);
+            }
         } else if (a.paired) {
             k = t;
             f = a.task_face[t];
@@ -877,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
                 r.clipped[q] = present == 1 ? clp[q] : 0;
             }
             for (int q = 0; q < 6; ++q) r.sub[q] = present == 1 ? sub[q] : 0.0;
-            a.out[t] = r;
+            a.out[a.task_face ? t : k * n + f] = r;
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
