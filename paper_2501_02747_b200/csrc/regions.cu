@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             tend = min(tnext + a.chunk, a.ntasks);
         }
         const long long t = tnext++;
-        long long k;
+        long long k, li = 0;   // li: entry of the per-source face list (list mode)
         int f;
         if (!a.task_face) {
             if (VISRT_K4W_FACEMAJOR) {   // consecutive tasks: one face, consecutive snapshot sources
@@ -758,16 +758,22 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
         } else if (a.paired) {
             k = t;
             f = a.task_face[t];
+        } else if (VISRT_K4W_FACEMAJOR) {   // face list per source, walked list-entry-major
+            const long long nsrc = a.ntasks / a.m;
+            li = t / nsrc;
+            k = t - li * nsrc;
+            f = a.task_face[li];
         } else {
             k = t / a.m;
-            f = a.task_face[t - k * a.m];
+            li = t - k * a.m;
+            f = a.task_face[li];
         }
         const int sf = s.inv[f];
         const int nv = s.nv[f];
         const double sx = a.src[3 * k], sy = a.src[3 * k + 1], sz = a.src[3 * k + 2];
         const bool presence = a.presence_only ||
                               (a.presence_of && a.task_face &&
-                               a.presence_of[a.paired ? t : t - k * static_cast<long long>(a.m)]);
+                               a.presence_of[a.paired ? t : li]);
         const long long tclk0 = K4CLK();
         int8_t present = 1;
         int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
@@ -886,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
                 r.clipped[q] = present == 1 ? clp[q] : 0;
             }
             for (int q = 0; q < 6; ++q) r.sub[q] = present == 1 ? sub[q] : 0.0;
-            a.out[a.task_face ? t : k * n + f] = r;
+            a.out[a.paired ? t : (a.task_face ? k * a.m + li : k * n + f)] = r;
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
