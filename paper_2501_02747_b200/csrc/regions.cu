@@ -497,7 +497,7 @@ __device__ unsigned long long g_k4w_prof[16];
 #define VISRT_K4W_FACEMAJOR 1   // all-pairs tasks walk face-major: neighbouring warps take one face for consecutive snapshots (r01: config 3 -12 %, config-5 Tx -9 %, Rx -2.5 %)
 #endif
 #ifndef VISRT_K4W_WC
-#define VISRT_K4W_WC 2   // warp blocker-cache entries, most recent first (r01, face-major walk: 2 beats 1 — config-5 Tx -13 %, config 1 -11 %)
+#define VISRT_K4W_WC 3   // warp blocker-cache entries, most recent first (r01, face-major walk, 1/2/3/4 swept: 3 best overall)
 #endif
 #ifndef VISRT_K4W_CHUNK
 #define VISRT_K4W_CHUNK 1   // consecutive (source, face) tasks per warp grab (r01: 8/16 measured slower: heavy faces cluster)
