@@ -1,11 +1,13 @@
 #!/usr/bin/env python
 """bench.py — headline benchmark (driver contract).
 
-Workload (BASELINE.json configs[1], "medium city grid, matrix only"): the full
-N x N bit-packed inter-visibility matrix of a seeded 1 km city of 200 boxes on
-16x16 ground tiles (N = 1,256 facets, 788,140 unordered pairs), (B) semantics:
-bit(i,j) = occlusion_judgment(F_i, F_j).kind != Occluded, every pair tested
-against every other facet as occluder.
+Workload (BASELINE.json configs[3], "large irregular city" — the largest
+configuration that runs on one GPU): the full N x N bit-packed
+inter-visibility matrix of a seeded 4 km city of 2,000 convex prisms on 32x32
+ground tiles (N = 22,096 facets, 244,105,560 unordered pairs), (B)
+semantics: bit(i,j) = occlusion_judgment(F_i, F_j).kind != Occluded, every
+pair tested against every other facet as occluder.
+``--config 2`` runs the round-1 headline (config 2, N = 1,256) instead.
 
 metric: facet-pair occlusion tests/s = T_alg / t, T_alg = sum_{i<j} S(i,j)(N-2)
 (the segment-vs-facet tests the reference's occlusion_judgment performs),
@@ -125,7 +127,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(soup, seconds: float = 10.0):
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for l in f:
+                if l.startswith("model name"):
+                    return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _pairs_per_core(cfg: int) -> int:
+    """Pairs per host thread per reference step: ~0.5-1 s of occlusion_judgment
+    (a config-4 pair costs ~22 ms on one core: 33 sightlines x 22k occluders)."""
+    return {1: 4000, 2: 250, 3: 100, 4: 40}.get(cfg, 40)
+
+
+def cpu_baseline(soup, seconds: float = 10.0, cfg: int = 4):
     """The compiled reference (oracle/_ref) — or the C restatement when the
     reference could not be built — timed on the host cores over a bounded
     sample of the same workload's pairs."""
@@ -137,7 +156,7 @@ def cpu_baseline(soup, seconds: float = 10.0):
     except Exception:
         kind = "port"
         o = bindings.Oracle(soup)
-    batch = max(2000, cores * 100)
+    batch = cores * _pairs_per_core(cfg)
     tests = 0.0
     npairs = 0
     t0 = time.perf_counter()
@@ -151,9 +170,10 @@ def cpu_baseline(soup, seconds: float = 10.0):
         el = time.perf_counter() - t0
         if el >= seconds or b >= 200:
             break
-    return {"value": tests / el, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{npairs} seeded random pairs of the config-2 matrix, occlusion_judgment on {cores} "
-                      f"threads ({el:.1f} s)"}
+    return {"value": tests / el, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": _cpu_model(),
+            "sample": f"{npairs} seeded random pairs of the config-{cfg} matrix, occlusion_judgment on {cores} "
+                      f"threads ({el:.1f} s)",
+            "pairs_per_s": npairs / el}
 
 
 def _hbm_peak_gbs() -> tuple:
@@ -174,7 +194,31 @@ def _hbm_roofline(alg_bytes: float, ms: float, basis: str) -> dict:
             "frac": gbs / peak, "basis": basis, "peak_source": src}
 
 
-def secondary_measurements(stream: int):
+def _committed_ncu(cfg: int) -> dict:
+    """The ncu capture of the headline kernel committed under profiles/ for
+    this workload (NOT measured in this run: labelled with its source)."""
+    p = os.path.join(ROOT, "profiles", f"k2w_config{cfg}_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "committed ncu " + os.path.relpath(p, ROOT)
+        return d
+    except Exception:
+        return {"source": "none committed for this workload"}
+
+
+def _committed_kernel_ncu(name: str) -> dict:
+    p = os.path.join(ROOT, "profiles", f"{name}_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "committed ncu " + os.path.relpath(p, ROOT)
+        return d
+    except Exception:
+        return {"source": "none committed"}
+
+
+def secondary_measurements(stream: int, headline_cfg: int = 4):
     """The other hot-path subsystems, timed with the library's CUDA events on
     the same stream (outside the headline's timed region, rank 0, N = 1)."""
     from paper_2501_02747_b200 import scenes
@@ -182,7 +226,7 @@ def secondary_measurements(stream: int):
                                             trajectory_vis_table, unpack_bits)
     out = {}
     # (1) the other matrix configurations
-    for cfg in (1, 3):
+    for cfg in [c for c in (1, 2, 3) if c != headline_cfg]:
         with Scene(scenes.workload(cfg).scene) as sc:
             sc.pair_visibility("all", copy_bits=False, stream=stream)
             _, st = sc.pair_visibility("all", copy_bits=False, stream=stream)
@@ -193,17 +237,22 @@ def secondary_measurements(stream: int):
     # config 4 / 5 geometry (22k facets): (B) matrix once, regions + order-3 trees of config-5 snapshots
     wl5 = scenes.workload(5)
     with Scene(wl5.scene) as sc:
-        _, st = sc.pair_visibility("all", copy_bits=False, stream=stream)
+        if headline_cfg != 4:
+            _, st = sc.pair_visibility("all", copy_bits=False, stream=stream)
+            out["matrix_config4"] = {"B_ms": st["ms"], "B_tests_per_s": st["tests_alg"] / (st["ms"] * 1e-3),
+                                     "facets": sc.n, "pairs": st["pairs"]}
         _, sa = sc.pair_visibility("prefiltered", copy_bits=False, stream=stream)
-        out["matrix_config4"] = {"B_ms": st["ms"], "B_tests_per_s": st["tests_alg"] / (st["ms"] * 1e-3),
-                                 "A_ms": sa["ms"], "A_candidates": sa["candidates"], "facets": sc.n,
-                                 "pairs": st["pairs"]}
+        out.setdefault("matrix_config4", {}).update({"A_ms": sa["ms"], "A_candidates": sa["candidates"],
+                                                      "facets": sc.n})
         src = np.concatenate([wl5.tx[:10], wl5.rx[:10]])
+        point_regions_array(sc, src[:2])
         arr, st = point_regions_array(sc, src)
         out["regions_config5"] = {"snapshots": len(src), "facets": sc.n, "ms": st["ms"],
                                   "regions_per_s": arr.size / (st["ms"] * 1e-3), "ms_per_snapshot": st["ms"] / len(src),
+                                  "sightlines": st["candidates"], "exact_tests": st["tests_exec"],
                                   "roofline": _hbm_roofline(arr.nbytes + sc.upload_bytes, st["ms"],
-                                                            "region records written + scene state read once")}
+                                                            "region records written + scene state read once"),
+                                  "ncu": _committed_kernel_ncu("k4w_config5")}
         tri, _ = chain_triples(sc)
         tr = Tracer(sc, 3, triples=tri)
         tr.trace_raw(wl5.tx[:4], wl5.rx[:4])
@@ -235,7 +284,8 @@ def secondary_measurements(stream: int):
         out["tree_config3_order3"] = {"snapshots": 50, "nodes": tst["nodes"], "ms": tst["ms"],
                                       "nodes_per_s": tst["nodes"] / (tst["ms"] * 1e-3),
                                       "ms_per_snapshot": tst["ms"] / 50, "paths": tst["paths"],
-                                      "roofline": _hbm_roofline(80.0 * tst["nodes"], tst["ms"], "80 B per node")}
+                                      "roofline": _hbm_roofline(80.0 * tst["nodes"], tst["ms"], "80 B per node"),
+                                      "ncu": _committed_kernel_ncu("k6_config3")}
         tr.close()
     wl1 = scenes.workload(1)
     with Scene(wl1.scene) as sc:
@@ -291,7 +341,7 @@ def run_reference(args, rank, world):
         return 0
     from paper_2501_02747_b200 import scenes
     from oracle import bindings
-    soup = scenes.workload(2).scene
+    soup = scenes.workload(args.config).scene
     cores = _ncores()
     kind = "reference"
     try:
@@ -299,7 +349,7 @@ def run_reference(args, rank, world):
     except Exception:
         kind = "port"
         o = bindings.Oracle(soup)
-    per_step = max(4000, cores * 500)
+    per_step = cores * _pairs_per_core(args.config)
     times, tests = [], []
     for step in range(args.warmup + args.steps):
         pi, pj = _sample_pairs(soup.nfaces, per_step, 5000 + step)
@@ -313,11 +363,12 @@ def run_reference(args, rank, world):
     ms = 1e3 * sum(times) / len(times)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 city)",
-            "config": {"workload": "config2 matrix (B): reference occlusion_judgment on a bounded pair sample per step",
-                       "pairs_per_step": per_step, "facets": soup.nfaces},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{per_step} seeded pairs per step on {cores} threads"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded config-{args.config} city)",
+            "config": {"workload": f"config{args.config} matrix (B): reference occlusion_judgment on a bounded "
+                                   f"pair sample per step", "pairs_per_step": per_step, "facets": soup.nfaces},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": _cpu_model(),
+                             "sample": f"{per_step} seeded pairs of the config-{args.config} matrix per step on "
+                                       f"{cores} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -334,7 +385,7 @@ def run_visrt(args, rank, world):
     from paper_2501_02747_b200 import scenes
     from paper_2501_02747_b200.core import Scene, measure_peaks
 
-    wl = scenes.workload(2, seed=scenes.SEED_BASE + 2 + 7919 * rank)
+    wl = scenes.workload(args.config, seed=scenes.SEED_BASE + args.config + 7919 * rank)
     soup = wl.scene
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -395,51 +446,55 @@ def run_visrt(args, rank, world):
         fp64_peak, fp32_peak = measure_peaks(local)
         kern = sum(kern_ms) / len(kern_ms)
         execd = sum(tests_exec) / len(tests_exec)
-        achieved = FLOPS_PER_TEST * tests_alg / (kern * 1e-3) / 1e12
         peak = fp64_peak / 1e12
-        traffic, ncu_sol = None, None
-        tp = os.path.join(ROOT, "profiles", "k_pair_bits_traffic.json")
-        if os.path.exists(tp):
-            try:
-                prof = json.load(open(tp))
-                traffic, ncu_sol = prof.get("dram_bytes_per_launch"), prof.get("ncu_sol")
-            except Exception:
-                traffic = None
+        ref_equiv = FLOPS_PER_TEST * tests_alg / (kern * 1e-3) / 1e12
+        ncu = _committed_ncu(args.config)
+        ops_per_test = ncu.get("fp64_thread_ops_per_exact_test") or FLOPS_PER_TEST
+        achieved = ops_per_test * execd / (kern * 1e-3) / 1e12
+        wl_desc = {2: "config2: 1 km city, 200 boxes + 16x16 tiles, N=1256 facets",
+                   3: "config3: 2 km Manhattan grid, 500 boxes + 16x16 tiles, N=2756 facets",
+                   4: "config4: 4 km city, 2000 convex prisms + 32x32 tiles, N=22096 facets"}.get(
+                       args.config, f"config{args.config}")
         line = {
             "metric": METRIC, "value": total_tests / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "matrix_build_ms": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded config-2 generator, one city per rank)",
-            "config": {"workload": "config2: 1 km city, 200 boxes + 16x16 tiles, N=1256 facets; full NxN "
-                                   "bit-packed occlusion matrix (B: every i<j vs all N-2 occluders)",
+            "data": f"synthetic (seeded config-{args.config} generator, one city per rank)",
+            "config": {"workload": wl_desc + "; full NxN bit-packed occlusion matrix (B: every i<j vs all N-2 "
+                                             "occluders)",
                        "facets": soup.nfaces, "pairs": int(st["pairs"]), "mode": args.mode,
                        "candidates": int(cand), "tests_alg_per_gpu": tests_alg,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"dp{world} (independent cities)"},
             "e2e": {"value": total_tests / e2e_max, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h),
+                    "d2h_bytes_per_step": int(d2h), "s_per_step": e2e_max,
                     "path": "Scene(soup) ingest+upload -> pair_visibility -> bits D2H -> free"},
             "gpu_launches": args.steps,
             "roofline": {"bound": "fp64", "kernel": "k_pair_bits_warp", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "basis": "algorithmic: 17 FP64 ops x T_alg reference tests / kernel time; "
-                                  "peak = in-run DADD/DMUL microbenchmark (MEASURED_PEAKS.json has no FP64); "
-                                  "frac > 1 means conservative culling + early exit skip reference work",
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": ncu.get("dram_bytes_per_launch"),
+                         "basis": "EXECUTED work: in-run exact-test count x FP64 thread ops per exact test "
+                                  "(calibrated by ncu on this kernel, see ncu.source) / kernel time; peak = in-run "
+                                  "DADD/DMUL microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
                          "executed_exact_tests": execd,
                          "executed_exact_tests_per_s": execd / (kern * 1e-3),
+                         "reference_equivalent": {"achieved": ref_equiv, "frac": ref_equiv / peak,
+                                                  "basis": "17 FP64 ops x T_alg reference tests / kernel time: "
+                                                           "culling + early exit skip the reference's work, "
+                                                           "so this exceeds 1; not a roofline"},
                          "fp32_peak_tflops": fp32_peak / 1e12,
-                         "ncu_sol": ncu_sol},
+                         "ncu": ncu},
             "clocks": clocks,
             "wall_s_timed_loop": wall,
         }
         if world == 1 and not args.no_secondary:
             try:
-                line["subsystems"] = secondary_measurements(sh)
+                line["subsystems"] = secondary_measurements(sh, args.config)
             except Exception as e:   # noqa: BLE001
                 line["subsystems"] = {"error": str(e)}
         if world == 1:
             try:
-                line["cpu_baseline"] = cpu_baseline(soup, seconds=args.cpu_seconds)
+                line["cpu_baseline"] = cpu_baseline(soup, seconds=args.cpu_seconds, cfg=args.config)
             except Exception as e:   # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": _ncores(), "kind": "unavailable",
                                         "sample": f"failed: {e}"}
@@ -457,6 +512,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="visrt", choices=["visrt", "reference"])
     ap.add_argument("--mode", default="all", choices=["all", "prefiltered"])
+    ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4],
+                    help="matrix workload (default: config 4, the largest single-GPU configuration)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-secondary", action="store_true", help="skip the other subsystems' timings")
     args = ap.parse_args()

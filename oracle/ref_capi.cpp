@@ -162,6 +162,17 @@ void* vref_scene_load(const char* path) {
 
 void vref_scene_free(void* h) { delete static_cast<RefScene*>(h); }
 
+// save_scene (proj/src/scene.cpp:327-375) of a loaded scene; 0 ok, -1 error.
+int32_t vref_scene_save(void* h, const char* path) {
+    try {
+        R::save_scene(static_cast<RefScene*>(h)->scene, path);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 int32_t vref_nfaces(void* h) {
     return static_cast<int32_t>(static_cast<RefScene*>(h)->scene.faces().size());
 }

@@ -80,7 +80,13 @@ void* vref_scene_from_soup(int32_t nfaces, const int32_t* vert_off, const double
 void* vref_scene_from_shells(int32_t nfaces, const int32_t* vert_off, const double* verts, const char* ids,
                              const int32_t* building, int32_t nbuildings, const char* building_ids);
 void vref_scene_free(void* h);
+int32_t vref_scene_save(void* h, const char* path);
 int32_t vref_nfaces(void* h);
+int32_t vref_nedges(void* h);
+void* vref_scene_load(const char* path);
+int32_t vref_face_export(void* h, int32_t idx, char* id, int32_t idcap, char* bld, int32_t bldcap, char* lab_xy,
+                         char* lab_vert, int32_t labcap, double* pts, int32_t ptcap, double* normal);
+int32_t vref_edge_export(void* h, int32_t idx, char* id, int32_t idcap, double* ab);
 void* vref_build_matrix(void* h, int32_t order);
 void vref_matrix_free(void* m);
 void vref_matrix_set_max_order(void* m, int32_t order);

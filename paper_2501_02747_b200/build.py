@@ -32,6 +32,7 @@ def needs_build() -> bool:
     t = os.path.getmtime(LIB)
     deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
     deps.append(os.path.join(INCLUDE, "visrt.h"))
+    deps += [os.path.join(HERE, "cpp", f) for f in ("rt.cpp", "rt.hpp")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -69,11 +70,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
 RT_LIB = os.path.join(HERE, "librt_b200.so")
 
 
+def json_include() -> str:
+    """nlohmann json.hpp for rt::load_scene / save_scene: the copy vendored in the
+    image's site-packages (cudnn_frontend); VISRT_JSON_INCLUDE overrides."""
+    if os.environ.get("VISRT_JSON_INCLUDE"):
+        return os.environ["VISRT_JSON_INCLUDE"]
+    import sysconfig
+    return os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty", "nlohmann")
+
+
 def build_rt() -> str:
     """The C++ drop-in layer (namespace rt over the C-ABI), host code only."""
     src = os.path.join(HERE, "cpp", "rt.cpp")
     subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-shared", "-o", RT_LIB, src,
-                    "-I", os.path.join(HERE, "cpp"), "-L", HERE, "-lvisrt_cuda", "-Wl,-rpath,$ORIGIN"], check=True)
+                    "-I", os.path.join(HERE, "cpp"), "-I", json_include(), "-L", HERE, "-lvisrt_cuda",
+                    "-Wl,-rpath,$ORIGIN"], check=True)
     return RT_LIB
 
 

@@ -13,6 +13,10 @@
 
 #include "../../include/visrt.h"
 
+#include <fstream>
+
+#include <json.hpp>   // nlohmann 3.11 (the image's vendored copy; host I/O only)
+
 namespace rt {
 namespace {
 
@@ -298,11 +302,65 @@ Scene::~Scene() {
     if (dev_) visrt_scene_destroy(dev_);
 }
 
+namespace {
+Vec3 cross3(const Vec3& a, const Vec3& b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+
+// validate_face (src/scene.cpp:26-49): >= 3 vertices, planar within 1e-9 of
+// the Newell plane through pts[0], convex with the stored winding, area > kEps
+void validate_face(const Face& face) {
+    const auto& pts = face.poly.pts;
+    if (pts.size() < 3) throw SceneError("face '" + face.id + "' has fewer than 3 vertices");
+    for (const Vec3& p : pts)
+        if (std::abs(signed_distance(face, p)) > 1e-9) throw SceneError("face '" + face.id + "' is not planar");
+    const size_t n = pts.size();
+    for (size_t i = 0; i < n; ++i) {
+        const Vec3 e0 = pts[(i + 1) % n] - pts[i];
+        const Vec3 e1 = pts[(i + 2) % n] - pts[(i + 1) % n];
+        if (dot(cross3(e0, e1), face.poly.normal) < -kEps) throw SceneError("face '" + face.id + "' is not convex");
+    }
+    Vec3 acc{0, 0, 0};   // ConvexPolygon::area (src/geom.cpp:148-153): fan of cross products
+    for (size_t i = 1; i + 1 < n; ++i) acc = acc + cross3(pts[i] - pts[0], pts[i + 1] - pts[0]);
+    if (0.5 * norm(acc) <= kEps) throw SceneError("face '" + face.id + "' is degenerate");
+}
+}  // namespace
+
+Scene::Scene(Scene&& o)
+    : materials(std::move(o.materials)), buildings(std::move(o.buildings)), ground(std::move(o.ground)),
+      soup_(std::move(o.soup_)), dev_(o.dev_) {
+    // building faces keep their addresses (vector moves keep the buffers);
+    // the ground face lives in the optional, so the index is rebuilt
+    o.dev_ = nullptr;
+    const bool finalized = !o.face_ptrs_.empty();
+    o.face_ptrs_.clear();
+    o.face_index_.clear();
+    o.edges_.clear();
+    if (!finalized) return;
+    if (!soup_.empty()) {
+        for (Face& f : soup_) {
+            face_index_[f.id] = f.index;
+            face_ptrs_.push_back(&f);
+        }
+        register_faces(this, face_ptrs_);
+    } else {
+        finalize();
+    }
+}
+
 void Scene::finalize() {
+    // materials (src/scene.cpp:66-78)
+    std::set<std::string> material_names;
+    for (const Material& m : materials) {
+        if (!material_names.insert(m.name).second) throw SceneError("duplicate material '" + m.name + "'");
+        if (m.permittivity < 1.0) throw SceneError("material '" + m.name + "' has relative permittivity < 1");
+        if (m.conductivity < 0.0) throw SceneError("material '" + m.name + "' has negative conductivity");
+    }
     face_ptrs_.clear();
     face_index_.clear();
     edges_.clear();
     auto reg = [&](Face& f) {
+        validate_face(f);
+        if (!material_names.count(f.material))
+            throw SceneError("face '" + f.id + "' references unknown material '" + f.material + "'");
         if (face_index_.count(f.id)) throw SceneError("duplicate face id '" + f.id + "'");
         f.orientation = classify(f.poly.normal);
         f.index = static_cast<int>(face_ptrs_.size());
@@ -310,7 +368,9 @@ void Scene::finalize() {
         face_ptrs_.push_back(&f);
     };
     using Key = std::tuple<double, double, double>;
+    std::set<std::string> building_ids;
     for (Building& b : buildings) {
+        if (!building_ids.insert(b.id).second) throw SceneError("duplicate building id '" + b.id + "'");
         if (b.faces.empty()) throw SceneError("building '" + b.id + "' has no faces");
         Vec3 c{0, 0, 0};
         double cnt = 0;
@@ -384,6 +444,110 @@ std::unique_ptr<Scene> Scene::from_facets(const std::vector<std::string>& ids,
     }
     register_faces(s.get(), s->face_ptrs_);
     return s;
+}
+
+// ---------------------------------------------------------------------------
+// JSON scene I/O (src/scene.cpp:258-375)
+// ---------------------------------------------------------------------------
+namespace {
+Face face_of_json(const nlohmann::json& jf, const std::vector<Vec3>& verts) {
+    Face f;
+    f.id = jf.at("id").get<std::string>();
+    f.material = jf.at("material").get<std::string>();
+    std::vector<Vec3> ring;
+    for (const auto& jv : jf.at("vertices")) {
+        const size_t v = jv.get<size_t>();
+        if (v >= verts.size())
+            throw SceneError("face '" + f.id + "' references vertex " + std::to_string(v) + " out of range");
+        ring.push_back(verts[v]);
+    }
+    try {
+        f.poly = ConvexPolygon::from_points(std::move(ring));
+    } catch (const std::exception& e) {
+        throw SceneError("face '" + f.id + "': " + e.what());
+    }
+    if (jf.contains("labels")) {
+        const auto& jl = jf.at("labels");
+        if (jl.contains("xy")) f.labels.xy = jl.at("xy").get<std::string>();
+        if (jl.contains("vert")) f.labels.vert = jl.at("vert").get<std::string>();
+    }
+    return f;
+}
+}  // namespace
+
+Scene load_scene(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw SceneError("cannot open scene file '" + path + "'");
+    nlohmann::json j;
+    try {
+        in >> j;
+    } catch (const std::exception& e) {
+        throw SceneError("scene file '" + path + "' is not valid JSON: " + e.what());
+    }
+    Scene sc;
+    for (const auto& jm : j.value("materials", nlohmann::json::array()))
+        sc.materials.push_back({jm.at("name").get<std::string>(), jm.at("permittivity").get<double>(),
+                                jm.at("conductivity").get<double>()});
+    std::vector<Vec3> verts;
+    for (const auto& jv : j.value("vertices", nlohmann::json::array()))
+        verts.push_back({jv.at(0).get<double>(), jv.at(1).get<double>(), jv.at(2).get<double>()});
+    for (const auto& jb : j.value("buildings", nlohmann::json::array())) {
+        Building b;
+        b.id = jb.at("id").get<std::string>();
+        for (const auto& jf : jb.at("faces")) b.faces.push_back(face_of_json(jf, verts));
+        sc.buildings.push_back(std::move(b));
+    }
+    if (j.contains("ground")) sc.ground = face_of_json(j.at("ground"), verts);
+    sc.finalize();
+    return sc;
+}
+
+void save_scene(const Scene& scene, const std::string& path) {
+    if (scene.buildings.empty() && !scene.ground && !scene.faces().empty())
+        throw SceneError("a facet soup has no scene-file form");
+    nlohmann::json j;
+    j["materials"] = nlohmann::json::array();
+    for (const Material& m : scene.materials)
+        j["materials"].push_back({{"name", m.name}, {"permittivity", m.permittivity}, {"conductivity", m.conductivity}});
+    std::vector<Vec3> verts;
+    std::map<std::tuple<double, double, double>, size_t> index;   // exact-coordinate interning
+    auto face_json = [&](const Face& f) {
+        nlohmann::json jf;
+        jf["id"] = f.id;
+        jf["material"] = f.material;
+        nlohmann::json idx = nlohmann::json::array();
+        for (const Vec3& p : f.poly.pts) {
+            const auto key = std::make_tuple(p.x, p.y, p.z);
+            auto it = index.find(key);
+            if (it == index.end()) {
+                verts.push_back(p);
+                it = index.emplace(key, verts.size() - 1).first;
+            }
+            idx.push_back(it->second);
+        }
+        jf["vertices"] = idx;
+        if (!f.labels.xy.empty() || !f.labels.vert.empty()) {
+            nlohmann::json jl;
+            if (!f.labels.xy.empty()) jl["xy"] = f.labels.xy;
+            if (!f.labels.vert.empty()) jl["vert"] = f.labels.vert;
+            jf["labels"] = jl;
+        }
+        return jf;
+    };
+    j["buildings"] = nlohmann::json::array();
+    for (const Building& b : scene.buildings) {
+        nlohmann::json jb;
+        jb["id"] = b.id;
+        jb["faces"] = nlohmann::json::array();
+        for (const Face& f : b.faces) jb["faces"].push_back(face_json(f));
+        j["buildings"].push_back(jb);
+    }
+    if (scene.ground) j["ground"] = face_json(*scene.ground);
+    j["vertices"] = nlohmann::json::array();
+    for (const Vec3& v : verts) j["vertices"].push_back({v.x, v.y, v.z});
+    std::ofstream out(path);
+    if (!out) throw SceneError("cannot write scene file '" + path + "'");
+    out << j.dump(2) << "\n";
 }
 
 const Material& Scene::material(const std::string& name) const {   // src/scene.cpp:192-197

@@ -115,6 +115,7 @@ class Scene {
     Scene() = default;
     Scene(const Scene&) = delete;             // faces() holds pointers into the scene
     Scene& operator=(const Scene&) = delete;
+    Scene(Scene&& other);                     // re-indexes the moved faces (load_scene returns by value)
     ~Scene();
 
     /// Closed-shell scenes (reference semantics: indices, orientations, edges).
@@ -141,6 +142,15 @@ class Scene {
 };
 
 std::optional<PlaneSegment> plane_segment(const Face& face, PlaneTag plane);
+
+/// The reference's JSON scene files (include/rt/scene.hpp:108-109,
+/// src/scene.cpp:288-375): materials, shared vertex list, buildings of faces
+/// (id, material, vertex indices, optional labels), optional ground face.
+/// load_scene finalizes (same validation and SceneError messages);
+/// save_scene interns vertices by exact coordinates in face order. A facet
+/// soup (Scene::from_facets) has no JSON form: SceneError.
+Scene load_scene(const std::string& path);
+void save_scene(const Scene& scene, const std::string& path);
 
 // ---------------------------------------------------------------------------
 enum class RelationKind { Parallel, Perpendicular };

@@ -230,7 +230,8 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         const size_t o_rec = add(rec), o_samples = add(hs.samples), o_pts = add(hs.pts), o_normal = add(hs.normal),
                      o_seg = add(hs.seg), o_aabb = add(hs.aabb), o_nv = add(hs.nv), o_ns = add(hs.ns),
                      o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_sbox = add(hs.sbox),
-                     o_tbox = add(hs.tbox), o_gbox = add(hs.gbox), o_cbox = add(hs.cbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv);
+                     o_tbox = add(hs.tbox), o_gbox = add(hs.gbox), o_cbox = add(hs.cbox), o_srec = add(hs.srec), o_perm = add(hs.perm), o_inv = add(hs.inv),
+                     o_tframe = add(hs.tframe), o_qbox = add(hs.qbox);
         const size_t data_bytes = ar.total;   // the scene data; the buffers below are device-only
         const size_t o_bits = ar.add(nullptr, static_cast<size_t>(hs.n) * ds.words * 8);
         const size_t o_counter = ar.add(nullptr, 4 * 8);
@@ -270,6 +271,8 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.gbox = static_cast<const float*>(at(o_gbox));
         ds.cbox = static_cast<const float*>(at(o_cbox));
         ds.srec = static_cast<const double*>(at(o_srec));
+        ds.tframe = static_cast<const float*>(at(o_tframe));
+        ds.qbox = static_cast<const uint32_t*>(at(o_qbox));
         ds.perm = static_cast<const int32_t*>(at(o_perm));
         ds.inv = static_cast<const int32_t*>(at(o_inv));
         sc->d_bits = static_cast<unsigned long long*>(at(o_bits));
@@ -374,17 +377,16 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
                 }
             }
             if (!drop_i.empty()) {
-                int32_t* di = nullptr;
-                int32_t* dj = nullptr;
-                ck(cudaMalloc(&di, drop_i.size() * 4), "cudaMalloc");
-                ck(cudaMalloc(&dj, drop_j.size() * 4), "cudaMalloc");
-                ck(cudaMemcpy(di, drop_i.data(), drop_i.size() * 4, cudaMemcpyHostToDevice), "H2D");
-                ck(cudaMemcpy(dj, drop_j.data(), drop_j.size() * 4, cudaMemcpyHostToDevice), "H2D");
+                // the selection buffer (npairs x 8 B, consumed by the split
+                // above) holds the drop lists: no allocation, and the copies
+                // are ordered on the caller's stream before the clear kernel
+                int32_t* di = reinterpret_cast<int32_t*>(sc->d_sel);
+                int32_t* dj = di + drop_i.size();
+                ck(cudaMemcpyAsync(di, drop_i.data(), drop_i.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+                ck(cudaMemcpyAsync(dj, drop_j.data(), drop_j.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
                 ck(visrt::launch_clear_pairs(sc->d_bits, sc->ds.words, di, dj,
                                              static_cast<long long>(drop_i.size()), st), "clear");
                 ck(cudaStreamSynchronize(st), "sync");
-                cudaFree(di);
-                cudaFree(dj);
             }
         }
         if (bits_host) {

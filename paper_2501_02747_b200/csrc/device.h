@@ -34,6 +34,8 @@ struct DevScene {
     const int32_t* inv = nullptr;  // face index -> Morton position
     const float* gbox = nullptr;   // [ngroups][8] group union boxes (kGroup faces)
     const float* cbox = nullptr;   // [nchunks][8] chunk union boxes (64 tiles)
+    const float* tframe = nullptr; // [ntiles][8] quantisation frame of each tile (sweep.h qsat)
+    const uint32_t* qbox = nullptr;// [n even][2] 8-bit member boxes in their tile's frame
     int32_t ntiles = 0, nchunks = 0, ngroups = 0;
 };
 

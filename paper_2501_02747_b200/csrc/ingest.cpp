@@ -266,6 +266,8 @@ void ingest(const visrt_facets_v1& f, HostScene& hs) {
 // consecutive faces, tile box = union of the member boxes rounded outward.
 // Only the ORDER in which occluders are examined changes; every verdict is
 // still the exact predicate's.
+void quantise_members(HostScene& hs);
+
 void build_hierarchy(HostScene& hs) {
     const int n = hs.n;
     const double ext = std::max(hs.extent, 1.0);
@@ -332,6 +334,52 @@ void build_hierarchy(HostScene& hs) {
     unions(64, hs.ntiles, hs.tbox);
     unions(kGroup, hs.ngroups, hs.gbox);
     unions(64 * 64, hs.nchunks, hs.cbox);
+    quantise_members(hs);
+}
+
+// 8-bit member boxes in their tile's frame (sweep.h qsat). Frame of tile t:
+// step s_d = max(size_d / 251, extent * 2^-14) and origin o_d = lo_d - 2 s_d,
+// so every member box maps into [2, 253]; it is stored rounded outward plus
+// ONE more step on each side. That step absorbs the device's fp32 transform
+// of the segment into the frame and the SAT's rounding there: with
+// |coordinates| <= 2 extent / s_min + 510 = 2^15 + 510 frame units the fp32
+// products err by < 2^-8 units, far inside the extra step. The float boxes
+// quantised here already carry box_margin(), so the culling stays one-sided:
+// the quantised box contains the float box contains every true hit.
+void quantise_members(HostScene& hs) {
+    const int n = hs.n;
+    const double ext = std::max(hs.extent, 1.0);
+    const double smin = ext * 6.103515625e-05;   // 2^-14
+    hs.tframe.assign(static_cast<size_t>(hs.ntiles) * 8, 0.0f);
+    hs.qbox.assign(static_cast<size_t>((n + 1) / 2 * 2) * 2, 0u);
+    for (int t = 0; t < hs.ntiles; ++t) {
+        const float* tb = &hs.tbox[static_cast<size_t>(t) * 8];
+        float* F = &hs.tframe[static_cast<size_t>(t) * 8];
+        double o[3], inv[3];
+        for (int d = 0; d < 3; ++d) {
+            const double lo = static_cast<double>(tb[d]) - static_cast<double>(tb[4 + d]);
+            const double hi = static_cast<double>(tb[d]) + static_cast<double>(tb[4 + d]);
+            const double st = std::max((hi - lo) / 251.0, smin);
+            F[d] = static_cast<float>(lo - 2.0 * st);
+            F[4 + d] = static_cast<float>(1.0 / st);
+            o[d] = F[d];
+            inv[d] = F[4 + d];
+        }
+        for (int k = t * 64; k < std::min(n, t * 64 + 64); ++k) {
+            const float* b = &hs.sbox[static_cast<size_t>(k) * 8];
+            uint32_t q[6];
+            for (int d = 0; d < 3; ++d) {
+                const double lo = (static_cast<double>(b[d]) - static_cast<double>(b[4 + d]) - o[d]) * inv[d];
+                const double hi = (static_cast<double>(b[d]) + static_cast<double>(b[4 + d]) - o[d]) * inv[d];
+                const double ql = std::floor(lo) - 1.0, qh = std::ceil(hi) + 1.0;
+                if (ql < 0.0 || qh > 255.0) throw std::runtime_error("quantised member box out of its tile frame");
+                q[d] = static_cast<uint32_t>(ql);
+                q[3 + d] = static_cast<uint32_t>(qh);
+            }
+            hs.qbox[2 * static_cast<size_t>(k)] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+            hs.qbox[2 * static_cast<size_t>(k) + 1] = q[4] | (q[5] << 8);
+        }
+    }
 }
 
 }  // namespace visrt

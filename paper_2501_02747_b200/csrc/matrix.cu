@@ -301,19 +301,19 @@ __device__ unsigned long long g_k2w_prof[16];
 #define K2CLK() 0ll
 #endif
 
-template <int MAXV, bool RESIDENT, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
+template <int MAXV, int RES, int MINB, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
     int wc = -1;        // lane q < kWC holds warp cache entry q (Morton index)
     int wc_next = 0;    // warp-uniform insertion cursor
     unsigned long long tests = 0, sweeps = 0, batches = 0;
-    __shared__ unsigned char surv_buf[kThreads / 32][64];   // per warp: surviving members of a tile, in order
+    __shared__ unsigned char surv_buf[NT / 32][64];   // per warp: surviving members of a tile, in order
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     const unsigned lt = (1u << lane) - 1u;
 
@@ -413,11 +413,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
         };
         // settle every unresolved sightline blocked by occluder k (Morton index)
         auto resolve = [&](int k) {
-            const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
             for (unsigned m = unres; m; m &= m - 1) {
                 const int r = __ffs(m) - 1;
                 ends(lane + 32 * r);
-                if ((!VISRT_K2W_RSAT || sat_maybe(B, make_segf(s, ax, ay, az, bx, by, bz))) && exact(k))
+                if ((!VISRT_K2W_RSAT || member_maybe(ctx, k, make_segf(s, ax, ay, az, bx, by, bz))) && exact(k))
                     unres &= ~(1u << r);
             }
         };
@@ -474,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
             int hit2 = -1, hit3 = -1;
 #endif
             const int home = home_chunk(s, pi);
-            if (!RESIDENT && ctx.gbox && !a.flat) {
+            if (RES == kStreamed && ctx.gbox && !a.flat) {
                 // non-resident scenes (config 4/5): tile -> group (shared memory) -> member (L1/L2)
                 int more[2];
                 hit = coop_any_hit_grouped<MAXV>(ctx, s.srec, g, ax, ay, az, bx, by, bz, si, sj, si, tests, batches,
@@ -486,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                 }
 #endif
             }
-            for (int cc = 0; cc < ctx.nchunks && hit < 0 && (RESIDENT || !ctx.gbox || a.flat); ++cc) {
+            for (int cc = 0; cc < ctx.nchunks && hit < 0 && (RES != kStreamed || !ctx.gbox || a.flat); ++cc) {
                 const int c = home + cc < ctx.nchunks ? home + cc : home + cc - ctx.nchunks;
                 const int t0 = c * kTile;
                 const int tc = min(kTile, ctx.ntiles - t0);
@@ -533,10 +532,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pair_bits_warp(PairArgs a) {
                     const int base = (t0 + tb) * kTile;
                     const int mc = min(kTile, n - base);
                     const int m0 = base + lane, m1 = base + lane + 32;
-                    const bool v0 = lane < mc && m0 != si && m0 != sj &&
-                                    (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g));
-                    const bool v1 = lane + 32 < mc && m1 != si && m1 != sj &&
-                                    (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g));
+                    bool v0, v1;
+                    if (RES == kQuantised) {
+                        const QSeg qs = make_qseg(g, ctx.tframe + static_cast<size_t>(t0 + tb) * 8);
+                        v0 = lane < mc && m0 != si && m0 != sj && (VISRT_K2W_NOSAT || qsat(ctx.qbox[m0], qs));
+                        v1 = lane + 32 < mc && m1 != si && m1 != sj && (VISRT_K2W_NOSAT || qsat(ctx.qbox[m1], qs));
+                    } else {
+                        v0 = lane < mc && m0 != si && m0 != sj &&
+                             (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g));
+                        v1 = lane + 32 < mc && m1 != si && m1 != sj &&
+                             (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g));
+                    }
                     const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
                     ++batches;
                     const int clo = __popc(lo), tot = clo + __popc(hi);
@@ -749,20 +755,21 @@ __global__ void k_clear_pairs(unsigned long long* bits, int words, const int32_t
 // Host launchers
 // ---------------------------------------------------------------------------
 
-static int persistent_grid(const void* fn, size_t smem, int device) {
+static int persistent_grid(const void* fn, size_t smem, int device, int threads = kThreads) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
     if (per < 1) per = 1;
     return sms * per;
 }
 
 template <class K>
-static cudaError_t launch_persistent(K fn, size_t smem, const PairArgs& a, int device, cudaStream_t st) {
+static cudaError_t launch_persistent(K fn, size_t smem, const PairArgs& a, int device, cudaStream_t st,
+                                     int threads = kThreads) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device);
-    fn<<<grid, kThreads, smem, st>>>(a);
+    const int grid = persistent_grid(reinterpret_cast<const void*>(fn), smem, device, threads);
+    fn<<<grid, threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -776,7 +783,24 @@ static bool use_resident(int n) {
     return !force_stream && n <= kResidentMaxBoxes;
 }
 
-static size_t sweep_smem(const DevScene& s, bool resident) { return sweep_smem_bytes(s.n, s.ntiles, resident); }
+static size_t sweep_smem(const DevScene& s, int res) { return sweep_smem_bytes(s.n, s.ntiles, res); }
+
+// Scenes too large for fp32 resident member boxes but within kQuantisedMaxBoxes
+// keep 8-byte quantised boxes in shared memory (one CTA of kQThreads per SM).
+// VISRT_QUANT=0: streamed path instead; VISRT_QUANT=2: quantised even where
+// the fp32 boxes would fit (A/B and tests on small scenes).
+static int quant_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("VISRT_QUANT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return m;
+}
+
+static bool use_quantised(int n, bool resident_ok) {
+    const int m = quant_mode();
+    return m != 0 && n <= kQuantisedMaxBoxes && (m == 2 || !resident_ok);
+}
 
 // The warp-per-pair kernel is the default (r01: config 2 8.05 -> 6.31 ms,
 // config 3 40.8 -> 34.1 ms); VISRT_K2_WARP=0 selects the lane-per-pair kernel.
@@ -815,14 +839,26 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const long long warps = static_cast<long long>(sms) * 3 * (kThreads / 32);
         a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(a.chunk, a.npairs / (8 * warps))));
-        a.tiled = (VISRT_K2W_TR > 1 && !a.ci && a.stride == 1 && a.npairs >= 512 * warps) ? 1 : 0;
+        // VISRT_K2W_TILED=0/1 forces the grab shape (tests run the tiled walk on small scenes)
+        static const int tiled_env = [] {
+            const char* e = std::getenv("VISRT_K2W_TILED");
+            return e ? std::atoi(e) : -1;
+        }();
+        const bool big = tiled_env >= 0 ? tiled_env == 1 : a.npairs >= 512 * warps;
+        a.tiled = (VISRT_K2W_TR > 1 && !a.ci && a.stride == 1 && big) ? 1 : 0;
     }
     if (a.stride > 1) a.npairs = (a.npairs + a.stride - 1) / a.stride;
     // K2w keeps the member boxes resident only while 3 CTAs still fit per SM:
     // occupancy beats residency (r01: config 3 resident 14.8 ms at 2 CTAs,
     // streamed with the group level 12.9 ms at 3 CTAs)
     bool res = use_resident(a.s.n);
-    if (res && use_warp_k2() && 3 * (sweep_smem(a.s, true) + 3 * 1024) > static_cast<size_t>(smem_sm)) res = false;
+    if (res && use_warp_k2() && 3 * (sweep_smem(a.s, kResident) + 3 * 1024) > static_cast<size_t>(smem_sm)) res = false;
+    if (use_warp_k2() && use_quantised(a.s.n, res)) {
+        // one CTA of kQThreads per SM holds the quantised member boxes
+        const size_t qsm = sweep_smem(a.s, kQuantised);
+        if (qsm + (kQThreads / 32) * 64 + 1024 <= static_cast<size_t>(smem_sm))
+            return launch_persistent(k_pair_bits_warp<MAXV, kQuantised, 1, kQThreads>, qsm, a, device, st, kQThreads);
+    }
     const size_t smem = sweep_smem(a.s, res);
     if (use_warp_k2()) {
         // register budget by occupancy: when shared memory already limits the

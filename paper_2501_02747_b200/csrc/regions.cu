@@ -346,18 +346,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
         }
     };
     auto start_task = [&](long long t) {
-        tid = t;
-        long long k;
-        if (!a.task_face) {
-            k = t / n;
-            f = static_cast<int>(t - k * n);
-        } else if (a.paired) {
-            k = t;
-            f = a.task_face[t];
-        } else {
-            k = t / a.m;
-            f = a.task_face[t - k * a.m];
-        }
+        const RegionTask rt = region_task(a, t, n);   // a.face_major == 0 for this kernel
+        tid = rt.out;
+        const long long k = rt.k;
+        f = rt.f;
         sf = s.inv[f];
         sx = a.src[3 * k];
         sy = a.src[3 * k + 1];
@@ -472,7 +464,7 @@ __device__ __noinline__ int k4w_sweep(const DevScene& s, const SweepCtx& ctx, do
 template <int MAXV>
 __device__ __noinline__ bool k4w_blocked(const DevScene& s, const SweepCtx& ctx, int k, double sx, double sy,
                                          double sz, double qx, double qy, double qz, unsigned long long& tests) {
-    if (!sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, sx, sy, sz, qx, qy, qz))) return false;
+    if (!member_maybe(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) return false;
     ++tests;
     return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
 }
@@ -493,9 +485,9 @@ __device__ unsigned long long g_k4w_prof[16];
 #define K4CLK() 0ll
 #endif
 
-#ifndef VISRT_K4W_FACEMAJOR
-#define VISRT_K4W_FACEMAJOR 1   // all-pairs tasks walk face-major: neighbouring warps take one face for consecutive snapshots (r01: config 3 -12 %, config-5 Tx -9 %, Rx -2.5 %)
-#endif
+// K4w walks its tasks face-major by default (RegionArgs::face_major: neighbouring
+// warps take one face for consecutive snapshots; r01: config 3 -12 %, config-5
+// Tx -9 %, Rx -2.5 %); VISRT_K4W_FACEMAJOR=0 selects the source-major walk.
 #ifndef VISRT_K4W_WC
 #define VISRT_K4W_WC 3   // warp blocker-cache entries, most recent first (r01, face-major walk, 1/2/3/4 swept: 3 best overall)
 #endif
@@ -557,7 +549,7 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
 #if VISRT_K4W_NI
             return k4w_blocked<MAXV>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests);
 #else
-            return sat_maybe(ctx.mbox + static_cast<size_t>(k) * 8, make_segf(s, sx, sy, sz, qx, qy, qz)) &&
+            return member_maybe(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz)) &&
                    (++tests, seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz));
 #endif
         };
@@ -661,7 +653,7 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             (void)R;
             while (pending && k4w_blocked<MAXV>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests)) {
 #else
-            while (pending && sat_maybe(B, make_segf(s, sx, sy, sz, qx, qy, qz))) {
+            while (pending && member_maybe(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) {
                 ++tests;
                 if (!seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz)) break;
 #endif
@@ -717,16 +709,16 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
 #ifndef VISRT_K4W_PSCAN
 #define VISRT_K4W_PSCAN 1   // 1: lane-parallel column scan (scan_cols_warp); 0: 65 serial col_vis calls
 #endif
-template <int MAXV, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp(RegionArgs a) {
+template <int MAXV, int RES, int NT = kThreads, int MINB = VISRT_K4W_MINB>
+__global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
-    __shared__ unsigned char surv_buf[kThreads / 32][64];
+    __shared__ unsigned char surv_buf[NT / 32][64];
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
-    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     unsigned long long tests = 0, queries = 0, batches = 0;
     WCache cache;   // the last blockers (Morton indices)
@@ -736,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
 #endif
     long long tnext = 0, tend = 0;
     for (;;) {
-        if (tnext == tend) {   // a.chunk consecutive tasks: the same source, neighbouring faces
+        if (tnext == tend) {   // a.chunk consecutive tasks (region_task: walk order a.face_major)
             unsigned long long tw = 0;
             if (lane == 0) tw = atomicAdd(&a.counter[0], static_cast<unsigned long long>(a.chunk));
             tnext = static_cast<long long>(__shfl_sync(kFull, tw, 0));
@@ -744,30 +736,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
             tend = min(tnext + a.chunk, a.ntasks);
         }
         const long long t = tnext++;
-        long long k, li = 0;   // li: entry of the per-source face list (list mode)
-        int f;
-        if (!a.task_face) {
-            if (VISRT_K4W_FACEMAJOR) {   // consecutive tasks: one face, consecutive snapshot sources
-                const long long nsrc = a.ntasks / n;
-                f = static_cast<int>(t / nsrc);
-                k = t - static_cast<long long>(f) * nsrc;
-            } else {
-            k = t / n;
-            f = static_cast<int>(t - k * n);
-            }
-        } else if (a.paired) {
-            k = t;
-            f = a.task_face[t];
-        } else if (VISRT_K4W_FACEMAJOR) {   // face list per source, walked list-entry-major
-            const long long nsrc = a.ntasks / a.m;
-            li = t / nsrc;
-            k = t - li * nsrc;
-            f = a.task_face[li];
-        } else {
-            k = t / a.m;
-            li = t - k * a.m;
-            f = a.task_face[li];
-        }
+        const RegionTask rt = region_task(a, t, n);
+        const long long k = rt.k, li = rt.li;
+        const int f = rt.f;
         const int sf = s.inv[f];
         const int nv = s.nv[f];
         const double sx = a.src[3 * k], sy = a.src[3 * k + 1], sz = a.src[3 * k + 2];
@@ -892,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, VISRT_K4W_MINB) k_point_regions_warp
                 r.clipped[q] = present == 1 ? clp[q] : 0;
             }
             for (int q = 0; q < 6; ++q) r.sub[q] = present == 1 ? sub[q] : 0.0;
-            a.out[a.paired ? t : (a.task_face ? k * a.m + li : k * n + f)] = r;
+            a.out[rt.out] = r;
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -920,20 +891,32 @@ extern "C" int visrt_debug_k4w_prof(unsigned long long* out) {
 namespace visrt {
 #endif
 
-static int persistent_grid_r(const void* fn, size_t smem, int device) {
+static int persistent_grid_r(const void* fn, size_t smem, int device, int threads = kThreads) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
     if (per < 1) per = 1;
     return sms * per;
 }
 
 template <class K>
-static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a, int device, cudaStream_t st) {
+static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a, int device, cudaStream_t st,
+                            int threads = kThreads) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device), kThreads, smem, st>>>(a);
+    fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads), threads, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+// K4w threads per QUANTISED CTA (one CTA per SM: 16 warps at 128 registers)
+constexpr int kQThreadsK4 = 512;
+
+static int quant_mode_r() {
+    static const int m = [] {
+        const char* e = std::getenv("VISRT_QUANT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return m;
 }
 
 template <int MAXV>
@@ -958,9 +941,21 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const bool warp = a.presence_only || a.presence_of || (force >= 0 ? force == 1 : true);   // K4w: faster at every size
+    static const int face_major = [] {
+        const char* e = std::getenv("VISRT_K4W_FACEMAJOR");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    a.face_major = warp ? face_major : 0;   // the lane kernel K4 walks source-major
+    if (warp && quant_mode_r() != 0 && a.s.n <= kQuantisedMaxBoxes && (quant_mode_r() == 2 || !res)) {
+        int smem_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        const size_t qsm = sweep_smem_bytes(a.s.n, a.s.ntiles, kQuantised);
+        if (qsm + (kQThreadsK4 / 32) * 64 + 1024 <= static_cast<size_t>(smem_sm))
+            return launch_r(k_point_regions_warp<MAXV, kQuantised, kQThreadsK4, 1>, qsm, a, device, st, kQThreadsK4);
+    }
     if (warp)
-        return res ? launch_r(k_point_regions_warp<MAXV, true>, smem, a, device, st)
-                   : launch_r(k_point_regions_warp<MAXV, false>, smem, a, device, st);
+        return res ? launch_r(k_point_regions_warp<MAXV, kResident>, smem, a, device, st)
+                   : launch_r(k_point_regions_warp<MAXV, kStreamed>, smem, a, device, st);
     return res ? launch_r(k_point_regions<MAXV, true>, smem, a, device, st)
                : launch_r(k_point_regions<MAXV, false>, smem, a, device, st);
 }

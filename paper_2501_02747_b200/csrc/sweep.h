@@ -48,8 +48,63 @@ struct SweepCtx {
     const float* mbox;   // [n][8] member boxes (shared or global)
     const float* gbox;   // [ngroups][8] group boxes (shared memory; non-resident path only, else nullptr)
     const float* cbox;   // [nchunks][8] chunk boxes (shared memory): a chunk whose box the segment misses is skipped
+    const float* tframe; // QRES: [ntiles][8] tile quantisation frames (shared memory), else nullptr
+    const uint2* qbox;   // QRES: [n] 8-bit member boxes (shared memory), else nullptr
     int n, ntiles, nchunks, ngroups;
 };
+
+// Residency modes of the member boxes (template argument RES of the sweeping kernels).
+constexpr int kStreamed = 0;   // member boxes read through L1/L2 (group level in shared memory)
+constexpr int kResident = 1;   // fp32 member boxes in shared memory (N <= kResidentMaxBoxes)
+constexpr int kQuantised = 2;  // 8-byte quantised member boxes + tile frames in shared memory
+constexpr int kQuantisedMaxBoxes = 24576;   // 8 B/box + 64 B/tile: <= 200 KB, one CTA per SM
+constexpr int kQThreads = 768;              // threads of a QUANTISED CTA (24 warps: the SM's only CTA)
+
+// A segment in one tile's quantisation frame, coordinates doubled: M = 2 (m - o) inv,
+// E = 2 e inv (ingest.cpp quantise_members). Against a quantised member box
+// (lo, hi) the SAT reads D = M - (lo + hi), H = hi - lo: the same six axes as
+// sat_maybe, all quantities scaled by 2 inv per axis (an affine map preserves
+// intersection, so separating axes map to separating axes).
+struct QSeg {
+    float mx, my, mz, ex, ey, ez, ax, ay, az;
+};
+
+__device__ __forceinline__ QSeg make_qseg(const SegF& g, const float* __restrict__ F) {
+    QSeg q;
+    const float ix = 2.0f * F[4], iy = 2.0f * F[5], iz = 2.0f * F[6];
+    q.mx = (g.mx - F[0]) * ix;
+    q.my = (g.my - F[1]) * iy;
+    q.mz = (g.mz - F[2]) * iz;
+    q.ex = g.ex * ix;
+    q.ey = g.ey * iy;
+    q.ez = g.ez * iz;
+    q.ax = fabsf(q.ex);
+    q.ay = fabsf(q.ey);
+    q.az = fabsf(q.ez);
+    return q;
+}
+
+__device__ __forceinline__ bool qsat(uint2 b, const QSeg& g) {
+    const float lx = static_cast<float>(b.x & 255u), ly = static_cast<float>((b.x >> 8) & 255u),
+                lz = static_cast<float>((b.x >> 16) & 255u);
+    const float ux = static_cast<float>(b.x >> 24), uy = static_cast<float>(b.y & 255u),
+                uz = static_cast<float>((b.y >> 8) & 255u);
+    const float dx = g.mx - (lx + ux), dy = g.my - (ly + uy), dz = g.mz - (lz + uz);
+    const float hx = ux - lx, hy = uy - ly, hz = uz - lz;
+    bool ok = fabsf(dx) <= hx + g.ax;
+    ok &= fabsf(dy) <= hy + g.ay;
+    ok &= fabsf(dz) <= hz + g.az;
+    ok &= fabsf(__fmaf_rn(dy, g.ez, -dz * g.ey)) <= __fmaf_rn(hy, g.az, hz * g.ay);
+    ok &= fabsf(__fmaf_rn(dz, g.ex, -dx * g.ez)) <= __fmaf_rn(hx, g.az, hz * g.ax);
+    ok &= fabsf(__fmaf_rn(dx, g.ey, -dy * g.ex)) <= __fmaf_rn(hx, g.ay, hy * g.ax);
+    return ok;
+}
+
+// Member box k (Morton index) may meet segment g — any residency mode.
+__device__ __forceinline__ bool member_maybe(const SweepCtx& c, int k, const SegF& g) {
+    if (c.qbox) return qsat(c.qbox[k], make_qseg(g, c.tframe + static_cast<size_t>(k >> 6) * 8));
+    return sat_maybe(c.mbox + static_cast<size_t>(k) * 8, g);
+}
 
 // Per-lane state of one segment sweep.
 struct Sweep {
@@ -314,10 +369,16 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
             cand &= cand - 1;
             const int mc = min(kTile, ctx.n - base);
             const int m0 = base + lane, m1 = base + lane + 32;
-            const bool v0 = lane < mc && m0 != skip0 && m0 != skip1 &&
-                            sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g);
-            const bool v1 = lane + 32 < mc && m1 != skip0 && m1 != skip1 &&
-                            sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g);
+            bool v0, v1;
+            if (ctx.qbox) {
+                const QSeg qs = make_qseg(g, ctx.tframe + static_cast<size_t>(base >> 6) * 8);
+                v0 = lane < mc && m0 != skip0 && m0 != skip1 && qsat(ctx.qbox[m0], qs);
+                v1 = lane + 32 < mc && m1 != skip0 && m1 != skip1 && qsat(ctx.qbox[m1], qs);
+            } else {
+                v0 = lane < mc && m0 != skip0 && m0 != skip1 && sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g);
+                v1 = lane + 32 < mc && m1 != skip0 && m1 != skip1 &&
+                     sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g);
+            }
             const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
             ++batches;
             const int clo = __popc(lo), tot = clo + __popc(hi);
@@ -344,9 +405,11 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
     return hit;
 }
 
-// Block setup: stage the tile boxes (and the member boxes when RESIDENT) in
-// shared memory with TMA bulk copies (cp.async.bulk, one mbarrier).
-template <bool RESIDENT>
+// Block setup: stage the tile boxes (and the member boxes when resident,
+// fp32 or quantised) in shared memory with TMA bulk copies (cp.async.bulk,
+// one mbarrier). Shared layout: tile boxes | members (fp32 [n][8] RESIDENT,
+// group boxes STREAMED, tile frames + quantised boxes QUANTISED) | chunk boxes.
+template <int RES>
 __device__ __forceinline__ SweepCtx sweep_setup(const DevScene& s, float* smem, uint64_t* bar) {
     SweepCtx c;
     c.n = s.n;
@@ -354,39 +417,55 @@ __device__ __forceinline__ SweepCtx sweep_setup(const DevScene& s, float* smem, 
     c.nchunks = s.nchunks;
     float* st = smem;
     float* sm = smem + static_cast<size_t>(s.ntiles) * 8;   // member boxes (RESIDENT) or group boxes
-    constexpr bool kGroups = !RESIDENT && VISRT_GROUPS;
+    constexpr bool kGroups = RES == kStreamed && VISRT_GROUPS;
     c.ngroups = s.ngroups;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
+    const uint32_t tb = static_cast<uint32_t>(s.ntiles) * 32u;
+    const uint32_t qb = static_cast<uint32_t>((s.n + 1) / 2) * 16u;
+    const uint32_t mb = RES == kResident ? static_cast<uint32_t>(s.n) * 32u
+                      : RES == kQuantised ? tb + qb
+                                         : (kGroups ? static_cast<uint32_t>(s.ngroups) * 32u : 0u);
     if (threadIdx.x == 0) {
-        const uint32_t tb = static_cast<uint32_t>(s.ntiles) * 32u;
-        const uint32_t mb = RESIDENT ? static_cast<uint32_t>(s.n) * 32u
-                                     : (kGroups ? static_cast<uint32_t>(s.ngroups) * 32u : 0u);
-        const char* msrc = reinterpret_cast<const char*>(RESIDENT ? s.sbox : s.gbox);
         const uint32_t cb = static_cast<uint32_t>(s.nchunks) * 32u;
         mbar_expect_tx(bar, tb + mb + cb);
         for (uint32_t off = 0; off < tb; off += 32768u)
             bulk_g2s(reinterpret_cast<char*>(st) + off, reinterpret_cast<const char*>(s.tbox) + off,
                      min(32768u, tb - off), bar);
-        for (uint32_t off = 0; off < mb; off += 32768u)
-            bulk_g2s(reinterpret_cast<char*>(sm) + off, msrc + off, min(32768u, mb - off), bar);
+        if (RES == kQuantised) {
+            for (uint32_t off = 0; off < tb; off += 32768u)
+                bulk_g2s(reinterpret_cast<char*>(sm) + off, reinterpret_cast<const char*>(s.tframe) + off,
+                         min(32768u, tb - off), bar);
+            for (uint32_t off = 0; off < qb; off += 32768u)
+                bulk_g2s(reinterpret_cast<char*>(sm) + tb + off, reinterpret_cast<const char*>(s.qbox) + off,
+                         min(32768u, qb - off), bar);
+        } else {
+            const char* msrc = reinterpret_cast<const char*>(RES == kResident ? s.sbox : s.gbox);
+            for (uint32_t off = 0; off < mb; off += 32768u)
+                bulk_g2s(reinterpret_cast<char*>(sm) + off, msrc + off, min(32768u, mb - off), bar);
+        }
         bulk_g2s(reinterpret_cast<char*>(sm) + mb, reinterpret_cast<const char*>(s.cbox), cb, bar);
     }
     mbar_wait(bar, 0);
     c.tbox = st;
-    c.mbox = RESIDENT ? sm : s.sbox;
+    c.mbox = RES == kResident ? sm : s.sbox;
     c.gbox = kGroups ? sm : nullptr;
-    c.cbox = sm + (RESIDENT ? static_cast<size_t>(s.n) * 8 : (kGroups ? static_cast<size_t>(s.ngroups) * 8 : 0));
+    c.tframe = RES == kQuantised ? sm : nullptr;
+    c.qbox = RES == kQuantised ? reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(sm) + tb) : nullptr;
+    c.cbox = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sm) + mb);
     return c;
 }
 
-inline size_t sweep_smem_bytes(int n, int ntiles, bool resident) {
+inline size_t sweep_smem_bytes(int n, int ntiles, int res) {
     const size_t groups = VISRT_GROUPS ? static_cast<size_t>((n + kGroup - 1) / kGroup) : 0;
     const size_t chunks = (static_cast<size_t>(ntiles) + kTile - 1) / kTile;
-    return (static_cast<size_t>(ntiles) + (resident ? static_cast<size_t>(n) : groups) + chunks) * 32 + 128;
+    const size_t members = res == kResident ? static_cast<size_t>(n) * 32
+                         : res == kQuantised ? static_cast<size_t>(ntiles) * 32 + static_cast<size_t>((n + 1) / 2) * 16
+                                            : groups * 32;
+    return static_cast<size_t>(ntiles) * 32 + members + chunks * 32 + 128;
 }
 
 // Morton chunk holding original face f (a sweep starting there meets the

@@ -8,11 +8,15 @@
 
 namespace visrt {
 
-// K4 task list. Task t of the launch is one (source, face) region:
-//   task_face == nullptr : source t / n, face t % n           (all faces)
-//   paired == 0          : source t / m, face task_face[t % m] (face list)
-//   paired == 1          : source t,     face task_face[t]     (query list)
-// The region of task t is written to out[t].
+// K4 task list. A launch decides `ntasks` (source k, face f) regions in one of
+// three modes; region_task() below is the ONE mapping task t -> (k, f, list
+// entry li, output slot) both region kernels use:
+//   task_face == nullptr : all faces of every source, out[k * n + f]
+//   paired == 0          : face list task_face[0..m) per source, out[k * m + li]
+//   paired == 1          : query list, source t, face task_face[t], out[t]
+// The walk order of the first two modes is `face_major`: 1 = consecutive tasks
+// take one face (list entry) for consecutive sources (K4w's default: warps
+// share blockers and cached lines), 0 = one source for consecutive faces.
 struct RegionArgs {
     DevScene s;
     long long ntasks;
@@ -28,7 +32,37 @@ struct RegionArgs {
     int presence_only = 0;
     const uint8_t* presence_of = nullptr;   // per face-list entry (list mode) / per task (paired)
     int chunk = 1;                          // K4w: consecutive tasks per warp grab (set by the launcher)
+    int face_major = 1;                     // walk order of the all-faces / face-list modes (see above)
 };
+
+struct RegionTask {
+    long long k, li, out;   // source, face-list entry (list mode, else 0), output slot
+    int f;                  // face
+};
+
+__device__ __forceinline__ RegionTask region_task(const RegionArgs& a, long long t, int n) {
+    RegionTask r;
+    r.li = 0;
+    if (a.paired) {
+        r.k = t;
+        r.f = a.task_face[t];
+        r.out = t;
+        return r;
+    }
+    const long long per = a.task_face ? a.m : n;   // faces per source
+    if (a.face_major) {
+        const long long nsrc = a.ntasks / per;
+        r.li = t / nsrc;
+        r.k = t - r.li * nsrc;
+    } else {
+        r.k = t / per;
+        r.li = t - r.k * per;
+    }
+    r.f = a.task_face ? a.task_face[r.li] : static_cast<int>(r.li);
+    r.out = r.k * per + r.li;
+    if (!a.task_face) r.li = 0;
+    return r;
+}
 
 // K5 (TableBuilder::reach for order 1/2 chains). Dense: every (source k,
 // entry e), region of face f at regions[k * rstride + slot[f]] (slot NULL:

@@ -57,6 +57,11 @@ struct HostScene {
     std::vector<int32_t> perm, inv;
     std::vector<float> sbox, tbox, gbox, cbox;   // member / tile (64) / group (16) / chunk (4096) boxes, Morton order
     std::vector<double> srec;         // records in Morton order (layout of rec4/rec8)
+    // quantised member boxes (sweep.h QRES): per tile a frame [o.xyz 0 inv.xyz 0]
+    // (fp32 origin and inverse step of an 8-bit grid), per member 8 bytes
+    // (lo.x lo.y lo.z hi.x | hi.y hi.z 0 0), rounded outward plus one step
+    std::vector<float> tframe;
+    std::vector<uint32_t> qbox;       // [n rounded up to even][2]
     int32_t ntiles = 0, nchunks = 0, ngroups = 0;
 };
 

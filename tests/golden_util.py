@@ -54,3 +54,22 @@ def admitted_matrix(d: dict) -> np.ndarray:
 def region_tuple(row):
     present, has, clipped, sub = row
     return (int(present), list(has), list(clipped), unhex(sub))
+
+
+def region_canonical(P, H, Cl, S):
+    """Canonical bytes of one source's regions over all faces (present int8
+    [n], has/clipped int8 [n,3], sub float64 [n,6]): fields that the present /
+    has flags make meaningless are zeroed, so the reference's and the GPU's
+    arrays hash alike exactly when every bit-exact field agrees."""
+    P = np.ascontiguousarray(P, np.int8)
+    pres = (P == 1)[:, None]
+    H2 = np.where(pres, np.asarray(H, np.int8), 0).astype(np.int8)
+    hb = H2.astype(bool)
+    Cl2 = np.where(hb, np.asarray(Cl, np.int8), 0).astype(np.int8)
+    S2 = np.where(np.repeat(hb, 2, axis=1), np.asarray(S, np.float64), 0.0)
+    return P.tobytes() + H2.tobytes() + Cl2.tobytes() + np.ascontiguousarray(S2, np.float64).tobytes()
+
+
+def region_digest(P, H, Cl, S) -> str:
+    import hashlib
+    return hashlib.sha256(region_canonical(P, H, Cl, S)).hexdigest()

@@ -1,0 +1,95 @@
+"""Every traversal variant of the sweeping kernels gives bit-identical outputs
+on FULL matrices / region tables (sha-256 of the whole output):
+
+  * K2w member boxes: fp32 resident (N <= 6,144), streamed with the group
+    level, and 8-bit quantised in shared memory (sweep.h qsat; the default
+    for 6,144 < N <= 24,576, forced on small scenes with VISRT_QUANT=2);
+  * K2w grabs: 16-pair rows vs 2 x 16 pair-matrix tiles (VISRT_K2W_TILED);
+  * K4w task walk: face-major (default) vs source-major
+    (VISRT_K4W_FACEMAJOR=0), and the same three member-box residencies.
+
+Each variant runs in its own process (the knobs are read once per process).
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+MATRIX = ("import sys, json, hashlib; sys.path.insert(0, %r);"
+          "from paper_2501_02747_b200 import scenes;"
+          "from paper_2501_02747_b200.core import Scene;"
+          "sc = Scene(scenes.workload(%d).scene); b, st = sc.pair_visibility('all');"
+          "a, _ = sc.pair_visibility('prefiltered');"
+          "print(json.dumps([hashlib.sha256(b.tobytes()).hexdigest(), hashlib.sha256(a.tobytes()).hexdigest(),"
+          " st['tests_exec']]))")
+
+REGIONS = ("import sys, json, hashlib; import numpy as np; sys.path.insert(0, %r);"
+           "from paper_2501_02747_b200 import scenes;"
+           "from paper_2501_02747_b200.core import Scene, point_regions_array;"
+           "wl = scenes.workload(%d); src = np.concatenate([wl.tx[::%d], wl.rx[::%d]]);"
+           "sc = Scene(wl.scene); arr, st = point_regions_array(sc, src);"
+           "print(json.dumps([hashlib.sha256(arr.tobytes()).hexdigest(), int((arr['present'] == 1).sum())]))")
+
+
+def run(code, **env):
+    e = dict(os.environ)
+    e.update({k: str(v) for k, v in env.items()})
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+MATRIX_VARIANTS = [
+    {},
+    {"VISRT_QUANT": 2},
+    {"VISRT_QUANT": 0, "VISRT_FORCE_STREAM": 1},
+    {"VISRT_K2W_TILED": 1},
+    {"VISRT_K2W_TILED": 1, "VISRT_QUANT": 2},
+    {"VISRT_K2W_TILED": 0, "VISRT_QUANT": 0, "VISRT_FORCE_STREAM": 1},
+]
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_matrix_variants_agree(cfg):
+    code = MATRIX % (ROOT, cfg)
+    out = [run(code, **v) for v in MATRIX_VARIANTS]
+    for v, o in zip(MATRIX_VARIANTS[1:], out[1:]):
+        assert o[:2] == out[0][:2], (v, o, out[0])
+
+
+@pytest.mark.slow
+def test_matrix_config4_quantised_vs_streamed():
+    """Config 4 (22,096 facets): the quantised shared-memory sweep (default)
+    and the streamed sweep give the same full (A) and (B) matrices."""
+    code = MATRIX % (ROOT, 4)
+    q = run(code)
+    st = run(code, VISRT_QUANT=0)
+    assert q[:2] == st[:2]
+
+
+REGION_VARIANTS = [
+    {},
+    {"VISRT_QUANT": 2},
+    {"VISRT_QUANT": 0, "VISRT_FORCE_STREAM": 1},
+    {"VISRT_K4W_FACEMAJOR": 0},
+    {"VISRT_K4W_FACEMAJOR": 0, "VISRT_QUANT": 2},
+]
+
+
+@pytest.mark.parametrize("cfg,step", [(1, 7), (3, 50)])
+def test_region_variants_agree(cfg, step):
+    code = REGIONS % (ROOT, cfg, step, step)
+    out = [run(code, **v) for v in REGION_VARIANTS]
+    for v, o in zip(REGION_VARIANTS[1:], out[1:]):
+        assert o == out[0], (v, o, out[0])
+
+
+@pytest.mark.slow
+def test_region_config5_quantised_vs_streamed():
+    code = REGIONS % (ROOT, 5, 2500, 2500)
+    assert run(code) == run(code, VISRT_QUANT=0)
