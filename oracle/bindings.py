@@ -278,6 +278,7 @@ class RefOracle:
             L.vref_plane_segment.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _f64p]
             L.vref_triple_feasible.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]
             L.vref_segment_hits_face.argtypes = [C.c_void_p, _f64p, _f64p, C.c_int32]
+            L.vref_segments_blocked.argtypes = [C.c_void_p, C.c_int64, _f64p, _f64p, _u8p, C.c_int32]
             L.vref_build_matrix.restype = C.c_void_p
             L.vref_build_matrix.argtypes = [C.c_void_p, C.c_int32]
             L.vref_matrix_free.argtypes = [C.c_void_p]
@@ -388,6 +389,15 @@ class RefOracle:
         out = np.zeros(len(pi), np.int8)
         self.lib().vref_occlusion_batch(self.h, len(pi), pi, pj, out, threads or os.cpu_count() or 1)
         return out
+
+    def segments_blocked(self, a, b, threads: int = 0) -> np.ndarray:
+        """sightline_clear's negation for a batch of segments (any face hits)."""
+        a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1, 3))
+        b = np.ascontiguousarray(np.asarray(b, np.float64).reshape(-1, 3))
+        out = np.zeros(len(a), np.uint8)
+        self.lib().vref_segments_blocked(self.h, len(a), a.reshape(-1), b.reshape(-1), out,
+                                         threads or os.cpu_count() or 1)
+        return out.astype(bool)
 
     def mutually_front(self, i, j) -> bool:
         return bool(self.lib().vref_mutually_front(self.h, i, j))

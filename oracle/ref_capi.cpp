@@ -328,6 +328,32 @@ int32_t vref_segment_hits_face(void* h, const double* a, const double* b, int32_
                : 0;
 }
 
+// sightline_clear semantics (proj/src/vistable.cpp:38-44, skip = none) for a
+// batch of segments: blocked[k] = some face's segment_face_intersection hits
+// (a_k, b_k). Host thread pool.
+int32_t vref_segments_blocked(void* h, int64_t n, const double* a, const double* b, uint8_t* blocked,
+                              int32_t threads) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    std::atomic<int64_t> next{0};
+    auto work = [&]() {
+        for (int64_t k = next.fetch_add(1); k < n; k = next.fetch_add(1)) {
+            const R::Vec3 pa{a[3 * k], a[3 * k + 1], a[3 * k + 2]}, pb{b[3 * k], b[3 * k + 1], b[3 * k + 2]};
+            uint8_t hit = 0;
+            for (const R::Face* f : s.faces())
+                if (R::segment_face_intersection(pa, pb, f->poly)) {
+                    hit = 1;
+                    break;
+                }
+            blocked[k] = hit;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    return 0;
+}
+
 // ---------------------------------------------------------------------------
 // build_matrix (proj/src/vismatrix.cpp:638-799) — entries exported flat
 // ---------------------------------------------------------------------------

@@ -99,6 +99,8 @@ int64_t vref_trajectory_table(void* h, void* m, int32_t nwp, const double* wp, i
                               vref_mobile_row* rows, int64_t cap);
 int32_t vref_closest_edge(void* h, const double* rx);
 int32_t vref_mutually_front(void* h, int32_t i, int32_t j);
+int32_t vref_segments_blocked(void* h, int64_t n, const double* a, const double* b, uint8_t* blocked,
+                              int32_t threads);
 int32_t vref_required_planes(void* h, int32_t i, int32_t j);
 int32_t vref_triple_feasible(void* h, int32_t p, int32_t t, int32_t a);
 int32_t vref_chain_triple_feasible(void* h, int32_t p, int32_t t, int32_t a);

@@ -91,6 +91,7 @@ struct PairArgs {
     int32_t chunk;                   // K2w: consecutive pairs per warp grab
     int32_t tiled;                   // K2w: 1 = grabs are VISRT_K2W_TR x VISRT_K2W_TC tiles (all pairs)
     int32_t stride;                  // K2w profiling aid: decide every stride-th pair only (VISRT_K2_STRIDE, default 1)
+    int32_t nocull;                  // K2w: 1 = no fp32 culling, every occluder tested exactly (VISRT_NOCULL)
 };
 
 // ---------------------------------------------------------------------------

@@ -416,7 +416,8 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
             for (unsigned m = unres; m; m &= m - 1) {
                 const int r = __ffs(m) - 1;
                 ends(lane + 32 * r);
-                if ((!VISRT_K2W_RSAT || member_maybe(ctx, k, make_segf(s, ax, ay, az, bx, by, bz))) && exact(k))
+                if ((!VISRT_K2W_RSAT || a.nocull || member_maybe(ctx, k, make_segf(s, ax, ay, az, bx, by, bz))) &&
+                    exact(k))
                     unres &= ~(1u << r);
             }
         };
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
             int hit2 = -1, hit3 = -1;
 #endif
             const int home = home_chunk(s, pi);
-            if (RES == kStreamed && ctx.gbox && !a.flat) {
+            if (RES == kStreamed && ctx.gbox && !a.flat && !a.nocull) {
                 // non-resident scenes (config 4/5): tile -> group (shared memory) -> member (L1/L2)
                 int more[2];
                 hit = coop_any_hit_grouped<MAXV>(ctx, s.srec, g, ax, ay, az, bx, by, bz, si, sj, si, tests, batches,
@@ -485,14 +486,16 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
                 }
 #endif
             }
-            for (int cc = 0; cc < ctx.nchunks && hit < 0 && (RES != kStreamed || !ctx.gbox || a.flat); ++cc) {
+            for (int cc = 0; cc < ctx.nchunks && hit < 0 && (RES != kStreamed || !ctx.gbox || a.flat || a.nocull); ++cc) {
                 const int c = home + cc < ctx.nchunks ? home + cc : home + cc - ctx.nchunks;
                 const int t0 = c * kTile;
                 const int tc = min(kTile, ctx.ntiles - t0);
-                if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !sat_maybe(ctx.cbox + static_cast<size_t>(c) * 8, g))
+                if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !a.nocull &&
+                    !sat_maybe(ctx.cbox + static_cast<size_t>(c) * 8, g))
                     continue;
-                const bool h0 = lane < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g);
-                const bool h1 = lane + 32 < tc && sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g);
+                const bool h0 = lane < tc && (a.nocull || sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g));
+                const bool h1 = lane + 32 < tc &&
+                                (a.nocull || sat_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g));
                 unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
                                           (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
                 unsigned long long later = 0;
@@ -535,13 +538,14 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
                     bool v0, v1;
                     if (RES == kQuantised) {
                         const QSeg qs = make_qseg(g, ctx.tframe + static_cast<size_t>(t0 + tb) * 8);
-                        v0 = lane < mc && m0 != si && m0 != sj && (VISRT_K2W_NOSAT || qsat(ctx.qbox[m0], qs));
-                        v1 = lane + 32 < mc && m1 != si && m1 != sj && (VISRT_K2W_NOSAT || qsat(ctx.qbox[m1], qs));
+                        v0 = lane < mc && m0 != si && m0 != sj && (VISRT_K2W_NOSAT || a.nocull || qsat(ctx.qbox[m0], qs));
+                        v1 = lane + 32 < mc && m1 != si && m1 != sj &&
+                             (VISRT_K2W_NOSAT || a.nocull || qsat(ctx.qbox[m1], qs));
                     } else {
                         v0 = lane < mc && m0 != si && m0 != sj &&
-                             (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g));
+                             (VISRT_K2W_NOSAT || a.nocull || sat_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, g));
                         v1 = lane + 32 < mc && m1 != si && m1 != sj &&
-                             (VISRT_K2W_NOSAT || sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g));
+                             (VISRT_K2W_NOSAT || a.nocull || sat_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, g));
                     }
                     const unsigned lo = __ballot_sync(kFull, v0), hi = __ballot_sync(kFull, v1);
                     ++batches;
@@ -785,14 +789,16 @@ static bool use_resident(int n) {
 
 static size_t sweep_smem(const DevScene& s, int res) { return sweep_smem_bytes(s.n, s.ntiles, res); }
 
-// Scenes too large for fp32 resident member boxes but within kQuantisedMaxBoxes
-// keep 8-byte quantised boxes in shared memory (one CTA of kQThreads per SM).
-// VISRT_QUANT=0: streamed path instead; VISRT_QUANT=2: quantised even where
-// the fp32 boxes would fit (A/B and tests on small scenes).
+// Quantised shared-memory member boxes (sweep.h QSeg/qsat, one CTA of
+// kQThreads per SM) are an opt-in residency: VISRT_QUANT=1 uses them where the
+// fp32 boxes do not fit (6,144 < N <= 24,576), VISRT_QUANT=2 everywhere (tests).
+// Off by default — measured r02 on config 4 (B): 982 ms quantised vs 822 ms
+// streamed; the 200 KB of shared memory leave L1 too small for the occluder
+// records and the 8-bit boxes pass 18 % more exact tests.
 static int quant_mode() {
     static const int m = [] {
         const char* e = std::getenv("VISRT_QUANT");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 0;   // off by default: measured slower
     }();
     return m;
 }
@@ -824,6 +830,14 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
     }();
     PairArgs a = a0;
     a.flat = flat;
+    // VISRT_NOCULL=1: every fp32 culling test (chunk, tile, member boxes, cache
+    // pre-checks) passes, so every occluder runs the exact predicate — the
+    // brute-force reference for the culled builds (tools/nocull_check.py)
+    static const int nocull = [] {
+        const char* e = std::getenv("VISRT_NOCULL");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    a.nocull = nocull;
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     a.stride = a.ci ? 1 : stride;

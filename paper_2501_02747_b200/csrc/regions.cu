@@ -601,6 +601,104 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
     return false;
 }
 
+// REFINE with fan candidate lists (src/vistable.cpp:163-172). Every sightline
+// the bisection of one run boundary can ask about for transverse sample j runs
+// from the source S to q_j(u), u in [lo, hi]; q_j is piecewise linear in u
+// (breakpoints at the face's vertices), so those end points lie in the box
+// spanned by q_j at lo, hi and the breakpoints between, and every such sightline
+// stays within R_j (the box's half-diagonal) of the axis S -> c_j (its centre).
+// One collecting sweep per sample (coop_collect: culling boxes dilated by R_j)
+// lists every face that could block any of them; the <= 50 bisection steps then
+// decide col_vis(mid) by exact tests against those lists alone — the same
+// verdicts as sweeping every sightline, since no other face can block one.
+// Returns false (nothing decided) when a list overflows kFanCap.
+#ifndef VISRT_K4W_FAN
+#define VISRT_K4W_FAN 1
+#endif
+constexpr int kFanCap = 32;
+
+template <int MAXV>
+__device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, const double* us, int nv, int pl,
+                                        double ax, double ay, double dx, double dy, double& lo_io, double& hi_io,
+                                        bool lo_vis, double sx, double sy, double sz, int sf, int* fl,
+                                        unsigned long long& tests, unsigned long long& queries,
+                                        unsigned long long& batches, int& iters) {
+    constexpr int STRIDE = RecLayout<MAXV>::kStride;
+    const int lane = threadIdx.x & 31;
+    double lo = lo_io, hi = hi_io;
+    // per-sample end-point boxes (lane j < 7)
+    auto sample = [&](double u, int j, double& qx, double& qy, double& qz) -> bool {
+        const double cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
+        double cs0, cs1;
+        if (!column_span_us(us, nv, cu, cs0, cs1)) return false;
+        const double inset = dmul(dsub(cs1, cs0), 1e-6);
+        const double px = dadd(ax, dmul(dx, cu));
+        const double py = dadd(ay, dmul(dy, cu));
+        const double v = dmin_std(dsub(cs1, inset), dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
+        if (pl == 0) { qx = px; qy = py; qz = v; }
+        else if (pl == 1) { qx = v; qy = px; qz = py; }
+        else { qx = px; qy = v; qz = py; }
+        return true;
+    };
+    double bl[3] = {1e300, 1e300, 1e300}, bh[3] = {-1e300, -1e300, -1e300};
+    if (lane < 7) {
+        auto grow = [&](double u) {
+            double q[3];
+            if (!sample(u, lane, q[0], q[1], q[2])) return;
+            for (int d = 0; d < 3; ++d) {
+                bl[d] = fmin(bl[d], q[d]);
+                bh[d] = fmax(bh[d], q[d]);
+            }
+        };
+        grow(lo);
+        grow(hi);
+        for (int q = 0; q < nv; ++q)
+            if (us[2 * q] > lo && us[2 * q] < hi) grow(us[2 * q]);
+    }
+    int cnt[7];
+    for (int j = 0; j < 7; ++j) {
+        const double c0 = __shfl_sync(kFull, 0.5 * (bl[0] + bh[0]), j), c1 = __shfl_sync(kFull, 0.5 * (bl[1] + bh[1]), j),
+                     c2 = __shfl_sync(kFull, 0.5 * (bl[2] + bh[2]), j);
+        const double e0 = __shfl_sync(kFull, bh[0] - bl[0], j), e1 = __shfl_sync(kFull, bh[1] - bl[1], j),
+                     e2 = __shfl_sync(kFull, bh[2] - bl[2], j);
+        if (!(e0 >= 0.0)) {   // no column span anywhere in [lo, hi]: col_vis is false throughout
+            cnt[j] = 0;
+            continue;
+        }
+        // half-diagonal, rounded up generously (fp32 box test)
+        const float R = static_cast<float>(0.5 * sqrt(e0 * e0 + e1 * e1 + e2 * e2) * 1.0001 + 1e-6);
+        cnt[j] = coop_collect(ctx, make_segf(s, sx, sy, sz, c0, c1, c2), R, sf, fl + j * kFanCap, kFanCap, batches);
+        if (cnt[j] < 0) return false;
+    }
+    __syncwarp();
+    const int my_cnt = lane < 7 ? cnt[lane] : 0;
+    int it = 0;
+    for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
+        const double mid = dmul(0.5, dadd(lo, hi));
+        bool clear = false;
+        if (lane < 7) {
+            double qx, qy, qz;
+            if (sample(mid, lane, qx, qy, qz)) {
+                clear = true;
+                for (int q = 0; q < my_cnt && clear; ++q) {
+                    ++tests;
+                    if (seg_hits<MAXV>(s.srec + static_cast<size_t>(fl[lane * kFanCap + q]) * STRIDE, sx, sy, sz, qx,
+                                       qy, qz))
+                        clear = false;
+                }
+            }
+        }
+        queries += lane == 0 ? 7 : 0;
+        const bool vis = __any_sync(kFull, clear);
+        if (vis == lo_vis) lo = mid;
+        else hi = mid;
+    }
+    iters = it;
+    lo_io = lo;
+    hi_io = hi;
+    return true;
+}
+
 // The SCAN of visible_intervals (src/vistable.cpp:175-176: col_vis(i / 64) for
 // the 65 columns) with the columns spread over the lanes: lane l owns column
 // 32 * pass + l. col_vis is an OR over its <= 7 transverse samples, so the
@@ -715,10 +813,12 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
     __shared__ unsigned char surv_buf[NT / 32][64];
+    __shared__ int fan_buf[NT / 32][7 * kFanCap];   // per warp: refine_fan candidate lists
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
     const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
+    int* fan = fan_buf[threadIdx.x >> 5];
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     unsigned long long tests = 0, queries = 0, batches = 0;
     WCache cache;   // the last blockers (Morton indices)
@@ -807,6 +907,14 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             auto refine = [&](double lo, double hi, bool lo_vis) {
                 const long long rclk0 = K4CLK();
                 int it = 0;
+                if (VISRT_K4W_FAN && a.fan &&
+                    refine_fan<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, lo, hi, lo_vis, sx, sy, sz, sf, fan,
+                                     tests, queries, batches, it)) {
+                    K4P(1, K4CLK() - rclk0);
+                    K4P(6, 1);
+                    K4P(7, it);
+                    return dmul(0.5, dadd(lo, hi));
+                }
                 for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
                     const double mid = dmul(0.5, dadd(lo, hi));
                     if (col_vis(mid) == lo_vis) lo = mid;
@@ -914,7 +1022,7 @@ constexpr int kQThreadsK4 = 512;
 static int quant_mode_r() {
     static const int m = [] {
         const char* e = std::getenv("VISRT_QUANT");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 0;   // off by default: measured slower
     }();
     return m;
 }
@@ -946,6 +1054,11 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
         return e && e[0] == '0' ? 0 : 1;
     }();
     a.face_major = warp ? face_major : 0;   // the lane kernel K4 walks source-major
+    static const int fan = [] {   // VISRT_K4W_FAN=0: refine by per-sightline sweeps (A/B and tests)
+        const char* e = std::getenv("VISRT_K4W_FAN");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    a.fan = fan;
     if (warp && quant_mode_r() != 0 && a.s.n <= kQuantisedMaxBoxes && (quant_mode_r() == 2 || !res)) {
         int smem_sm = 0;
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
@@ -1136,15 +1249,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_segments_clear(DevScene s, long
 
 // Warp-per-segment variant (coop_any_hit), the default: converged culling and
 // exact phases like K2w / K4w.
-template <int MAXV, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads, 3) k_segments_clear_warp(DevScene s, long long nseg, const double* A,
-                                                                     const double* B, uint8_t* clear,
-                                                                     unsigned long long* counter) {
+template <int MAXV, int RES, int NT = kThreads, int MINB = 3>
+__global__ void __launch_bounds__(NT, MINB) k_segments_clear_warp(DevScene s, long long nseg, const double* A,
+                                                                  const double* B, uint8_t* clear,
+                                                                  unsigned long long* counter) {
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
-    __shared__ unsigned char surv_buf[kThreads / 32][64];
+    __shared__ unsigned char surv_buf[NT / 32][64];
     const int lane = threadIdx.x & 31;
-    const SweepCtx ctx = sweep_setup<RESIDENT>(s, smem, bar);
+    const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     unsigned long long tests = 0, batches = 0;
     int cache = -1;
@@ -1178,19 +1291,31 @@ static cudaError_t launch_segments_t(const DevScene& s, long long nseg, const do
                                      uint8_t* clear, unsigned long long* ctr, int device, cudaStream_t st) {
     const char* e = std::getenv("VISRT_FORCE_STREAM");
     const bool res = !(e && e[0] == '1') && s.n <= kResidentMaxBoxes;
-    const size_t smem = sweep_smem_bytes(s.n, s.ntiles, res);
+    size_t smem = sweep_smem_bytes(s.n, s.ntiles, res);
+    int threads = kThreads;
     auto go = [&](auto fn) {
         cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (err != cudaSuccess) return err;
-        fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device), kThreads, smem, st>>>(s, nseg, A, B,
-                                                                                                       clear, ctr);
+        fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads), threads, smem, st>>>(
+            s, nseg, A, B, clear, ctr);
         return cudaGetLastError();
     };
     static const bool lane_kernel = [] {
         const char* w = std::getenv("VISRT_SEG_WARP");
         return w && w[0] == '0';
     }();
-    if (!lane_kernel) return res ? go(k_segments_clear_warp<MAXV, true>) : go(k_segments_clear_warp<MAXV, false>);
+    if (!lane_kernel && quant_mode_r() != 0 && s.n <= kQuantisedMaxBoxes && (quant_mode_r() == 2 || !res)) {
+        int smem_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        const size_t qsm = sweep_smem_bytes(s.n, s.ntiles, kQuantised);
+        if (qsm + (kQThreads / 32) * 64 + 1024 <= static_cast<size_t>(smem_sm)) {
+            smem = qsm;
+            threads = kQThreads;
+            return go(k_segments_clear_warp<MAXV, kQuantised, kQThreads, 1>);
+        }
+    }
+    if (!lane_kernel)
+        return res ? go(k_segments_clear_warp<MAXV, kResident>) : go(k_segments_clear_warp<MAXV, kStreamed>);
     return res ? go(k_segments_clear<MAXV, true>) : go(k_segments_clear<MAXV, false>);
 }
 

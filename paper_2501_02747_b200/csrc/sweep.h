@@ -405,6 +405,98 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
     return hit;
 }
 
+// sat_maybe against the box dilated by R on every axis (conservative for any
+// segment within distance R of g: the box grown by R contains the box's
+// Minkowski sum with the R-ball).
+__device__ __forceinline__ bool sat_maybe_dil(const float* __restrict__ B, const SegF& g, float R) {
+    const float dx = g.mx - B[0], dy = g.my - B[1], dz = g.mz - B[2];
+    const float hx = B[4] + R, hy = B[5] + R, hz = B[6] + R;
+    bool ok = fabsf(dx) <= hx + g.ax;
+    ok &= fabsf(dy) <= hy + g.ay;
+    ok &= fabsf(dz) <= hz + g.az;
+    ok &= fabsf(__fmaf_rn(dy, g.ez, -dz * g.ey)) <= __fmaf_rn(hy, g.az, hz * g.ay);
+    ok &= fabsf(__fmaf_rn(dz, g.ex, -dx * g.ez)) <= __fmaf_rn(hx, g.az, hz * g.ax);
+    ok &= fabsf(__fmaf_rn(dx, g.ey, -dy * g.ex)) <= __fmaf_rn(hx, g.ay, hy * g.ax);
+    return ok;
+}
+
+// Collecting sweep of a FAN: every face (Morton index, `skip` excluded) whose
+// culling box, dilated by R, meets the axis segment g — i.e. every face that
+// could meet ANY segment within distance R of g. No exact tests, no early
+// exit. The indices go to `list` (per-warp shared memory, `cap` entries) in
+// traversal order; returns their count, or -1 when more than `cap` faces
+// qualify or the member boxes are quantised (the caller falls back to
+// per-sightline sweeps). Warp-uniform arguments; all 32 lanes.
+__device__ __forceinline__ int coop_collect(const SweepCtx& ctx, const SegF& g, float R, int skip, int* list,
+                                            int cap, unsigned long long& batches) {
+    if (ctx.qbox) return -1;
+    constexpr int GPT = kTile / kGroup;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int cnt = 0;
+    auto append = [&](bool v, int m) -> bool {   // false: overflow
+        const unsigned b = __ballot_sync(kFull, v);
+        if (v && cnt + __popc(b & lt) < cap) list[cnt + __popc(b & lt)] = m;
+        cnt += __popc(b);
+        return cnt <= cap;
+    };
+    for (int c = 0; c < ctx.nchunks; ++c) {
+        const int t0 = c * kTile;
+        const int tc = min(kTile, ctx.ntiles - t0);
+        if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !sat_maybe_dil(ctx.cbox + static_cast<size_t>(c) * 8, g, R))
+            continue;
+        const bool h0 = lane < tc && sat_maybe_dil(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, g, R);
+        const bool h1 = lane + 32 < tc && sat_maybe_dil(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, g, R);
+        unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
+                                  (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
+        ++batches;
+        if (ctx.gbox) {   // streamed: 8 candidate tiles x 4 groups per round, then 2 groups of members
+            while (cand) {
+                int my_tile = -1;
+#pragma unroll
+                for (int q = 0; q < 32 / GPT; ++q) {
+                    if (!cand) break;
+                    const int t = t0 + __ffsll(static_cast<long long>(cand)) - 1;
+                    cand &= cand - 1;
+                    if (q == lane / GPT) my_tile = t;
+                }
+                const int grp = my_tile * GPT + (lane % GPT);
+                const bool gv = my_tile >= 0 && grp < ctx.ngroups &&
+                                sat_maybe_dil(ctx.gbox + static_cast<size_t>(grp) * 8, g, R);
+                unsigned gm = __ballot_sync(kFull, gv);
+                ++batches;
+                while (gm) {
+                    const int la = __ffs(gm) - 1;
+                    gm &= gm - 1;
+                    const int lb = gm ? __ffs(gm) - 1 : -1;
+                    if (lb >= 0) gm &= gm - 1;
+                    const int ga = __shfl_sync(kFull, grp, la);
+                    const int gb = __shfl_sync(kFull, grp, lb < 0 ? la : lb);
+                    const int mg = lane < kGroup ? ga : (lb < 0 ? -1 : gb);
+                    const int m = mg * kGroup + (lane & (kGroup - 1));
+                    const bool v = mg >= 0 && m < ctx.n && m != skip &&
+                                   sat_maybe_dil(ctx.mbox + static_cast<size_t>(m) * 8, g, R);
+                    ++batches;
+                    if (!append(v, m)) return -1;
+                }
+            }
+        } else {   // member boxes in shared memory: 64 per candidate tile
+            while (cand) {
+                const int base = (t0 + __ffsll(static_cast<long long>(cand)) - 1) * kTile;
+                cand &= cand - 1;
+                const int mc = min(kTile, ctx.n - base);
+                const int m0 = base + lane, m1 = base + lane + 32;
+                const bool v0 = lane < mc && m0 != skip && sat_maybe_dil(ctx.mbox + static_cast<size_t>(m0) * 8, g, R);
+                const bool v1 =
+                    lane + 32 < mc && m1 != skip && sat_maybe_dil(ctx.mbox + static_cast<size_t>(m1) * 8, g, R);
+                ++batches;
+                if (!append(v0, m0) || !append(v1, m1)) return -1;
+            }
+        }
+    }
+    return cnt;
+}
+
 // Block setup: stage the tile boxes (and the member boxes when resident,
 // fp32 or quantised) in shared memory with TMA bulk copies (cp.async.bulk,
 // one mbarrier). Shared layout: tile boxes | members (fp32 [n][8] RESIDENT,

@@ -33,6 +33,7 @@ struct RegionArgs {
     const uint8_t* presence_of = nullptr;   // per face-list entry (list mode) / per task (paired)
     int chunk = 1;                          // K4w: consecutive tasks per warp grab (set by the launcher)
     int face_major = 1;                     // walk order of the all-faces / face-list modes (see above)
+    int fan = 1;                            // K4w: refine run boundaries with fan candidate lists
 };
 
 struct RegionTask {

@@ -200,16 +200,24 @@ def stage_tables(cfg: int, k: int):
     off = [0]
     ent, full, rp, ap = [], [], [], []
     for q, rs in enumerate(rows):
+        recs = []
         for x in rs:
             key = (x["chain"][0], x["aim"], x["plane"])
-            ent.append(index[key])
-            full.append(x["verdict"] == 0)
-            rp.append(x["ref_display"] == ids[x["chain"][0]] + "'")
-            ap.append(x["aim_display"] == ids[x["aim"]] + "'")
             assert x["ref_display"] in (ids[x["chain"][0]], ids[x["chain"][0]] + "'")
+            recs.append((index[key], x["verdict"] == 0, x["ref_display"] == ids[x["chain"][0]] + "'",
+                         x["aim_display"] == ids[x["aim"]] + "'"))
+        recs.sort()   # by entry index (the rows' own order is the reference's name sort)
+        prev = 0
+        for e, fu, r_, a_ in recs:
+            ent.append(e - prev)   # delta-coded per source (first = absolute)
+            prev = e
+            full.append(fu)
+            rp.append(r_)
+            ap.append(a_)
         off.append(len(ent))
-    save(f"c{cfg}tables", scene_sha=np.array(scene_sha(wl.scene)), src=src, tag=tag, entries=E,
-         off=np.array(off, np.int64), entry=np.array(ent, np.int32), full=np.array(full, bool),
+    # the entry list itself is c{cfg}A.npz's (the same build_matrix(scene, 1))
+    save(f"c{cfg}tables", scene_sha=np.array(scene_sha(wl.scene)), src=src, tag=tag,
+         off=np.array(off, np.int64), entry_delta=np.array(ent, np.int32), full=np.array(full, bool),
          ref_primed=np.array(rp, bool), aim_primed=np.array(ap, bool))
 
 
@@ -222,8 +230,8 @@ def stage_traj(cfg: int, length: int):
     keys = ["order", "node", "node_display", "s_start", "s_end", "label_start", "label_end", "parent", "blockage"]
     strs = "\n".join("\t".join(str(x[k]) if k not in ("s_start", "s_end") else float(x[k]).hex() for k in keys)
                      for x in rows)
-    save(f"c{cfg}traj", scene_sha=np.array(scene_sha(wl.scene)), waypoints=wps, entries=E,
-         rows=np.frombuffer(strs.encode(), np.uint8))
+    save(f"c{cfg}traj", scene_sha=np.array(scene_sha(wl.scene)), waypoints=wps,
+         rows=np.frombuffer(strs.encode(), np.uint8))   # entries: c{cfg}A.npz
     print(f"  {len(rows)} rows", flush=True)
 
 

@@ -150,17 +150,16 @@ def test_config5_regions_all_faces():
 def test_config3_point_vis_table():
     d = fixture("c3tables")
     wl = workload(3, d)
-    E = entries_dtype(d["entries"])
+    E = entries_dtype(fixture("c3A")["entries"])
     src = d["src"]
     with Scene(wl.scene) as sc:
         rows, full, regs, _ = point_tables(sc, src, E, want_regions=True)
     off = d["off"]
     for q in range(len(src)):
-        exp_e = d["entry"][off[q]:off[q + 1]]
+        ee = np.cumsum(d["entry_delta"][off[q]:off[q + 1]])   # ascending entry indices of the rows
         got_e = np.nonzero(rows[q])[0]
-        np.testing.assert_array_equal(np.sort(got_e), np.sort(exp_e))
-        o = np.argsort(exp_e)
-        ee = exp_e[o]
+        np.testing.assert_array_equal(got_e, ee)
+        o = np.arange(len(ee))
         np.testing.assert_array_equal(full[q, ee], d["full"][off[q]:off[q + 1]][o])
         # display primes: clipped region of the named face in the entry's plane
         pl = E["plane"][ee]
@@ -175,7 +174,7 @@ def test_config3_point_vis_table():
 def test_config3_trajectory_table():
     d = fixture("c3traj")
     wl = workload(3, d)
-    E = entries_dtype(d["entries"])
+    E = entries_dtype(fixture("c3A")["entries"])
     with Scene(wl.scene) as sc:
         rows = trajectory_vis_table(sc, d["waypoints"], E, 1, wl.scene.ids)
     keys = ["order", "node", "node_display", "s_start", "s_end", "label_start", "label_end", "parent", "blockage"]

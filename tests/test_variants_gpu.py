@@ -6,7 +6,9 @@ on FULL matrices / region tables (sha-256 of the whole output):
     for 6,144 < N <= 24,576, forced on small scenes with VISRT_QUANT=2);
   * K2w grabs: 16-pair rows vs 2 x 16 pair-matrix tiles (VISRT_K2W_TILED);
   * K4w task walk: face-major (default) vs source-major
-    (VISRT_K4W_FACEMAJOR=0), and the same three member-box residencies.
+    (VISRT_K4W_FACEMAJOR=0), and the same three member-box residencies;
+  * K4w refinement: fan candidate lists (default) vs one sweep per sightline
+    (VISRT_K4W_FAN=0).
 
 Each variant runs in its own process (the knobs are read once per process).
 """
@@ -64,16 +66,17 @@ def test_matrix_variants_agree(cfg):
 
 @pytest.mark.slow
 def test_matrix_config4_quantised_vs_streamed():
-    """Config 4 (22,096 facets): the quantised shared-memory sweep (default)
-    and the streamed sweep give the same full (A) and (B) matrices."""
+    """Config 4 (22,096 facets): the quantised shared-memory sweep and the
+    streamed sweep (default) give the same full (A) and (B) matrices."""
     code = MATRIX % (ROOT, 4)
-    q = run(code)
-    st = run(code, VISRT_QUANT=0)
+    q = run(code, VISRT_QUANT=1)
+    st = run(code)
     assert q[:2] == st[:2]
 
 
 REGION_VARIANTS = [
     {},
+    {"VISRT_K4W_FAN": 0},
     {"VISRT_QUANT": 2},
     {"VISRT_QUANT": 0, "VISRT_FORCE_STREAM": 1},
     {"VISRT_K4W_FACEMAJOR": 0},
@@ -92,4 +95,4 @@ def test_region_variants_agree(cfg, step):
 @pytest.mark.slow
 def test_region_config5_quantised_vs_streamed():
     code = REGIONS % (ROOT, 5, 2500, 2500)
-    assert run(code) == run(code, VISRT_QUANT=0)
+    assert run(code, VISRT_QUANT=1) == run(code)
