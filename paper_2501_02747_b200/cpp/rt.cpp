@@ -1048,6 +1048,9 @@ std::vector<std::vector<Path>> TraceAccelerator::trace_batch(const std::vector<V
             ts.nodes_expanded = nodes[k];
             ts.sequences_checked = (nodes[k] + 1) * (sedge[k] >= 0 ? 2 : 1);
             ts.paths_found = static_cast<long long>(out[k].size());
+            // the GPU's exact leg tests of the batch, split evenly (INTEGRATION.md:
+            // the reference's grid-filtered count has no counterpart)
+            ts.occlusion_tests = tx.empty() ? 0 : st.leg_tests / static_cast<long long>(tx.size());
             stats->push_back(ts);
         }
     }

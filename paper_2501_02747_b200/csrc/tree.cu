@@ -981,13 +981,13 @@ extern "C" int visrt_trace(visrt_tracer* tr, int64_t nsnap, const double* tx, co
                     ck(cudaMemsetAsync(c_ncand, 0, 8, st), "memset");
                     ck(cudaMemsetAsync(d_ctr + 3, 0, 8, st), "memset");   // legs cursor
                     ck(cudaMemsetAsync(d_ctr + 5, 0, 8, st), "memset");   // k_tree_last parent cursor
-                    // grid = the fused kernel's own residency (one wave)
+                    // grid = the fused kernel's own residency on THIS device (one wave; per call, cheap)
                     if (ds.maxv <= 4) {
-                        static const int lb4 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<4>),
+                        const int lb4 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<4>),
                                                               256, 0, device);
                         visrt::k_tree_last<4><<<lb4, 256, 0, st>>>(a, tr->cnt, d_ctr + 5);
                     } else {
-                        static const int lb8 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<8>),
+                        const int lb8 = visrt::grid_of(reinterpret_cast<const void*>(visrt::k_tree_last<8>),
                                                               256, 0, device);
                         visrt::k_tree_last<8><<<lb8, 256, 0, st>>>(a, tr->cnt, d_ctr + 5);
                     }
