@@ -90,6 +90,7 @@ __device__ bool column_span_us(const double* us, int nv, double u, double& lo_o,
     double lo = 0.0, hi = 0.0;
     bool any = false;
     double ua = us[0], sa = us[1];
+#pragma unroll 1
     for (int i = 0; i < nv; ++i) {
         const double ub = i + 1 < nv ? us[2 * i + 2] : us[0];
         const double sb = i + 1 < nv ? us[2 * i + 3] : us[1];
@@ -454,25 +455,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_point_regions(RegionArgs a) {
 // The warp sweep and the fp32-SAT + exact blocker test as single out-of-line
 // copies: inlined at each call site of the lane-parallel scan and col_vis
 // they overflowed the instruction cache (ncu: stall_no_inst).
-template <int MAXV>
+template <int MAXV, int RES>
 __device__ __noinline__ int k4w_sweep(const DevScene& s, const SweepCtx& ctx, double sx, double sy, double sz,
                                       double bx, double by, double bz, int sf, unsigned char* sv,
                                       unsigned long long& tests, unsigned long long& batches) {
-    return coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz, sf, -1, sf,
+    return coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz, sf, -1, sf,
                               sv, tests, batches);
 }
-template <int MAXV>
+template <int MAXV, int RES>
 __device__ __noinline__ bool k4w_blocked(const DevScene& s, const SweepCtx& ctx, int k, double sx, double sy,
                                          double sz, double qx, double qy, double qz, unsigned long long& tests) {
-    if (!member_maybe(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) return false;
+    if (!member_maybe<RES>(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) return false;
     ++tests;
     return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
 }
 
 // Development aid (-DVISRT_K4W_PROF): per-phase cycle and sweep counters of K4w.
 #ifdef VISRT_K4W_PROF
-__shared__ unsigned long long k4w_sprof[16];
-__device__ unsigned long long g_k4w_prof[16];
+__shared__ unsigned long long k4w_sprof[24];
+__device__ unsigned long long g_k4w_prof[24];
 #define K4P(i, v)                                                                                     \
     do {                                                                                              \
         if ((threadIdx.x & 31) == 0) atomicAdd(&k4w_sprof[i], static_cast<unsigned long long>(v));     \
@@ -517,7 +518,7 @@ struct WCache {
 // arithmetic, one warp-cooperative sweep per transverse sample. Out of line:
 // it has three call sites (scan, both refine directions) and inlining them
 // blew the instruction cache (ncu: stall_no_inst dominated).
-template <int MAXV>
+template <int MAXV, int RES>
 __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx, const double* us, int nv, int pl,
                                           double ax, double ay, double dx, double dy, double u, double sx,
                                           double sy, double sz, int sf, unsigned char* sv, WCache& cache,
@@ -547,9 +548,9 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
         }
         auto blocked_by = [&](int k) {
 #if VISRT_K4W_NI
-            return k4w_blocked<MAXV>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests);
+            return k4w_blocked<MAXV, RES>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests);
 #else
-            return member_maybe(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz)) &&
+            return member_maybe<RES>(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz)) &&
                    (++tests, seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * STRIDE, sx, sy, sz, qx, qy, qz));
 #endif
         };
@@ -564,9 +565,9 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
                          bz = __shfl_sync(kFull, qz, L);
 #if VISRT_K4W_NI
-            const int h = k4w_sweep<MAXV>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
+            const int h = k4w_sweep<MAXV, RES>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
 #else
-            const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
+            const int h = coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
 #endif
             K4P(4, 1);
@@ -593,7 +594,7 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
             tests += lane == 0;   // warp-uniform test: count it once
             if (seg_hits<MAXV>(s.srec + static_cast<size_t>(c0) * STRIDE, sx, sy, sz, qx, qy, qz)) continue;
         }
-        const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz, qx, qy, qz, sf,
+        const int h = coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, sx, sy, sz, qx, qy, qz), sx, sy, sz, qx, qy, qz, sf,
                                          -1, sf, sv, tests, batches);
         if (h < 0) return true;
         cache.put(h);
@@ -617,12 +618,40 @@ __device__ __noinline__ bool col_vis_warp(const DevScene& s, const SweepCtx& ctx
 #endif
 constexpr int kFanCap = 32;
 
-template <int MAXV>
+// The entries of a cone list whose box, dilated by R, meets g (in list order)
+// -> fl; returns their count or -1 when more than cap qualify.
+__device__ __forceinline__ int cone_filter(const float4* cbuf, int L, const SegF& g, float R, int* fl, int cap) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int cnt = 0;
+    for (int e0 = 0; e0 < L; e0 += 32) {
+        const int e = e0 + lane;
+        bool v = false;
+        int m = 0;
+        if (e < L) {
+            float4 c = cbuf[2 * e];
+            float4 h = cbuf[2 * e + 1];
+            m = __float_as_int(c.w);
+            h.x += R;
+            h.y += R;
+            h.z += R;
+            v = sat_maybe4(c, h, g);
+        }
+        const unsigned b = __ballot_sync(kFull, v);
+        const int at = cnt + __popc(b & lt);
+        if (v && at < cap) fl[at] = m;
+        cnt += __popc(b);
+        if (cnt > cap) return -1;
+    }
+    return cnt;
+}
+
+template <int MAXV, int RES>
 __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, const double* us, int nv, int pl,
                                         double ax, double ay, double dx, double dy, double& lo_io, double& hi_io,
                                         bool lo_vis, double sx, double sy, double sz, int sf, int* fl,
                                         unsigned long long& tests, unsigned long long& queries,
-                                        unsigned long long& batches, int& iters) {
+                                        unsigned long long& batches, int& iters, const float4* cbuf, int coneL) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
     double lo = lo_io, hi = hi_io;
@@ -640,6 +669,7 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
         else { qx = px; qy = v; qz = py; }
         return true;
     };
+    const long long fclk0 = K4CLK();
     double bl[3] = {1e300, 1e300, 1e300}, bh[3] = {-1e300, -1e300, -1e300};
     if (lane < 7) {
         auto grow = [&](double u) {
@@ -650,46 +680,71 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
                 bh[d] = fmax(bh[d], q[d]);
             }
         };
-        grow(lo);
-        grow(hi);
-        for (int q = 0; q < nv; ++q)
-            if (us[2 * q] > lo && us[2 * q] < hi) grow(us[2 * q]);
+        // lo, hi and every vertex column strictly between (one call site: i-cache)
+#pragma unroll 1
+        for (int q = -2; q < nv; ++q) {
+            const double u = q == -2 ? lo : (q == -1 ? hi : us[2 * q]);
+            if (q < 0 || (u > lo && u < hi)) grow(u);
+        }
     }
-    int cnt[7];
+    int my_cnt = 0;   // lane j < 7: the length of sample j's fan list
+#pragma unroll 1
     for (int j = 0; j < 7; ++j) {
         const double c0 = __shfl_sync(kFull, 0.5 * (bl[0] + bh[0]), j), c1 = __shfl_sync(kFull, 0.5 * (bl[1] + bh[1]), j),
                      c2 = __shfl_sync(kFull, 0.5 * (bl[2] + bh[2]), j);
         const double e0 = __shfl_sync(kFull, bh[0] - bl[0], j), e1 = __shfl_sync(kFull, bh[1] - bl[1], j),
                      e2 = __shfl_sync(kFull, bh[2] - bl[2], j);
-        if (!(e0 >= 0.0)) {   // no column span anywhere in [lo, hi]: col_vis is false throughout
-            cnt[j] = 0;
-            continue;
+        int cj = 0;   // no column span anywhere in [lo, hi]: col_vis is false throughout
+        if (e0 >= 0.0) {
+            // half-diagonal, rounded up generously (fp32 box test)
+            const float R = static_cast<float>(0.5 * sqrt(e0 * e0 + e1 * e1 + e2 * e2) * 1.0001 + 1e-6);
+            const SegF gj = make_segf(s, sx, sy, sz, c0, c1, c2);
+            // the task's cone list holds every face that can block a sightline to
+            // the face: filter it (no hierarchy walk) when it has been built
+            cj = coneL >= 0 ? cone_filter(cbuf, coneL, gj, R, fl + j * kFanCap, kFanCap)
+                            : coop_collect<RES>(ctx, gj, R, sf, fl + j * kFanCap, kFanCap, batches);
+            if (cj < 0) return false;
         }
-        // half-diagonal, rounded up generously (fp32 box test)
-        const float R = static_cast<float>(0.5 * sqrt(e0 * e0 + e1 * e1 + e2 * e2) * 1.0001 + 1e-6);
-        cnt[j] = coop_collect(ctx, make_segf(s, sx, sy, sz, c0, c1, c2), R, sf, fl + j * kFanCap, kFanCap, batches);
-        if (cnt[j] < 0) return false;
+        if (lane == j) my_cnt = cj;
     }
     __syncwarp();
-    const int my_cnt = lane < 7 ? cnt[lane] : 0;
+    K4P(16, K4CLK() - fclk0);
+    int excl = my_cnt;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, excl, o);
+        if (lane >= o) excl += v;
+    }
+    const int T = __shfl_sync(kFull, excl, 6);
+    excl -= my_cnt;
+    K4P(17, T);
+    K4P(18, 1);
     int it = 0;
     for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
         const double mid = dmul(0.5, dadd(lo, hi));
-        bool clear = false;
-        if (lane < 7) {
-            double qx, qy, qz;
-            if (sample(mid, lane, qx, qy, qz)) {
-                clear = true;
-                for (int q = 0; q < my_cnt && clear; ++q) {
-                    ++tests;
-                    if (seg_hits<MAXV>(s.srec + static_cast<size_t>(fl[lane * kFanCap + q]) * STRIDE, sx, sy, sz, qx,
-                                       qy, qz))
-                        clear = false;
-                }
+        double qx = 0, qy = 0, qz = 0;
+        const bool valid = lane < 7 && sample(mid, lane, qx, qy, qz);
+        unsigned blocked = 0;
+        for (int r = 0; r < T; r += 32) {
+            const int g = r + lane;
+            int j = 0;
+#pragma unroll
+            for (int k = 1; k < 7; ++k)
+                if (__shfl_sync(kFull, excl, k) <= g) j = k;
+            const int ej = __shfl_sync(kFull, excl, j);
+            const double ox = __shfl_sync(kFull, qx, j), oy = __shfl_sync(kFull, qy, j),
+                         oz = __shfl_sync(kFull, qz, j);
+            const bool ov = __shfl_sync(kFull, valid, j);
+            bool hit = false;
+            if (g < T && ov && !((blocked >> j) & 1u)) {
+                ++tests;
+                hit = seg_hits<MAXV>(s.srec + static_cast<size_t>(fl[j * kFanCap + g - ej]) * STRIDE, sx, sy, sz, ox,
+                                     oy, oz);
             }
+            blocked |= __reduce_or_sync(kFull, hit ? 1u << j : 0u);
         }
         queries += lane == 0 ? 7 : 0;
-        const bool vis = __any_sync(kFull, clear);
+        const bool vis = __any_sync(kFull, valid && !((blocked >> lane) & 1u));
         if (vis == lo_vis) lo = mid;
         else hi = mid;
     }
@@ -699,7 +754,34 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
     return true;
 }
 
-// The SCAN of visible_intervals (src/vistable.cpp:175-176: col_vis(i / 64) for
+// The cone list of task (source S, face f): every face but f whose culling
+// box may meet hull(S, f) (sweep.h ConeF / coop_collect_cone), written to the
+// warp's slice of the launch's cone buffer. Every sightline of
+// visible_intervals runs from S to a point of f, so a face outside the list
+// blocks none of them. Returns the count, or -1 (overflow / quantised boxes).
+constexpr int kConeUnbuilt = -2;
+template <int MAXV, int RES>
+__device__ __noinline__ int build_cone(const DevScene& s, const SweepCtx& ctx, int f, double sx, double sy, double sz,
+                                       int sf, const float4* cbuf, int ccap, unsigned long long& batches) {
+    const double* bb = s.aabb + static_cast<size_t>(f) * 6;
+    const double cx = 0.5 * (bb[0] + bb[3]), cy = 0.5 * (bb[1] + bb[4]), cz = 0.5 * (bb[2] + bb[5]);
+    const double ex = bb[3] - bb[0], ey = bb[4] - bb[1], ez = bb[5] - bb[2];
+    const double r = 0.5 * sqrt(ex * ex + ey * ey + ez * ez) * 1.0001 + 1e-6;
+    ConeF cone;
+    const double tk[4] = {0.0, 0.5, 0.75, 1.0};
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        const double t0 = tk[p], t1 = tk[p + 1];
+        cone.g[p] = make_segf(s, sx + t0 * (cx - sx), sy + t0 * (cy - sy), sz + t0 * (cz - sz), sx + t1 * (cx - sx),
+                              sy + t1 * (cy - sy), sz + t1 * (cz - sz));
+        cone.R[p] = static_cast<float>(t1 * r * 1.0001 + 1e-6);
+    }
+    const int L = coop_collect_cone<RES>(ctx, cone, sf, const_cast<float4*>(cbuf), ccap, batches);
+    __syncwarp();   // the list's stores are read back by every lane
+    return L;
+}
+
+// The SCAN of visible_intervals// The SCAN of visible_intervals (src/vistable.cpp:175-176: col_vis(i / 64) for
 // the 65 columns) with the columns spread over the lanes: lane l owns column
 // 32 * pass + l. col_vis is an OR over its <= 7 transverse samples, so the
 // per-column verdict does not depend on the order the samples are decided in:
@@ -710,13 +792,14 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
 // are mostly blocked by the same few faces). Same arithmetic per sightline as
 // col_vis_warp, so the 65 verdicts are identical. stop_at_first: return after
 // the first visible column (presence mode).
-template <int MAXV>
+template <int MAXV, int RES>
 __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, const SweepCtx& ctx, const double* us,
                                                           int nv, int pl, double ax, double ay, double dx, double dy,
                                                           double sx, double sy, double sz, int sf, unsigned char* sv,
                                                           WCache& cache, bool stop_at_first, bool& vis64,
                                                           unsigned long long& tests, unsigned long long& queries,
-                                                          unsigned long long& batches) {
+                                                          unsigned long long& batches, int f, const float4* cbuf,
+                                                          int ccap, int& coneL) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
     unsigned long long vis = 0;
@@ -749,9 +832,9 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
 #if VISRT_K4W_NI
             (void)B;
             (void)R;
-            while (pending && k4w_blocked<MAXV>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests)) {
+            while (pending && k4w_blocked<MAXV, RES>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests)) {
 #else
-            while (pending && member_maybe(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) {
+            while (pending && member_maybe<RES>(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) {
                 ++tests;
                 if (!seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz)) break;
 #endif
@@ -764,16 +847,66 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             if (k >= 0 && k != sf) settle(k);
         }
         bool visible = false;
+        // cone mode: every pending sample of the pass against the task's cone
+        // list (build_cone) — the same verdicts as sweeping the whole scene
+        auto cone_scan = [&]() {
+            const int Lc = coneL;
+            if (Lc == 0) {
+                if (pending) visible = true;
+                pending = false;
+                return;
+            }
+            SegF g{};
+            if (pending) g = make_segf(s, sx, sy, sz, qx, qy, qz);
+            int left = Lc, c = 0;
+            float4 n0 = cbuf[0], n1 = cbuf[1];   // entry c, loaded one iteration ahead
+            while (__any_sync(kFull, pending)) {
+                if (stop_at_first && __any_sync(kFull, visible)) break;
+                K4P(15, 1);
+                const float4 b0 = n0, b1 = n1;
+                const int cn = c + 1 == Lc ? 0 : c + 1;
+                n0 = cbuf[2 * cn];
+                n1 = cbuf[2 * cn + 1];
+                if (pending) {
+                    // entry c against this lane's sample, and against the next
+                    // samples of the column while it blocks them (a blocker of
+                    // one sample mostly blocks its neighbours)
+                    bool blk_any = false;
+                    const double* R = s.srec + static_cast<size_t>(__float_as_int(b0.w)) * STRIDE;
+                    while (pending && sat_maybe4(b0, b1, g) && (++tests, seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz))) {
+                        blk_any = true;
+                        if (++j == 7) {
+                            pending = false;   // every sample blocked: column hidden
+                        } else {
+                            point();
+                            g = make_segf(s, sx, sy, sz, qx, qy, qz);
+                        }
+                    }
+                    if (pending) {
+                        left = blk_any ? Lc - 1 : left - 1;   // a new sample has passed entry c already
+                        if (left == 0) {   // clear of every face of the cone
+                            visible = true;
+                            pending = false;
+                        }
+                    }
+                }
+                c = cn;
+            }
+        };
         for (;;) {
+            if (coneL >= 0) {
+                cone_scan();
+                break;
+            }
             const unsigned who = __ballot_sync(kFull, pending);
             if (!who) break;
             const int L = __ffs(who) - 1;
             const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
                          bz = __shfl_sync(kFull, qz, L);
 #if VISRT_K4W_NI
-            const int h = k4w_sweep<MAXV>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
+            const int h = k4w_sweep<MAXV, RES>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
 #else
-            const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
+            const int h = coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
 #endif
             K4P(2, 1);
@@ -784,6 +917,15 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                     pending = false;
                 }
                 if (stop_at_first) break;
+                // a (partly) visible face: its remaining samples are mostly clear
+                // and a clear sweep visits every candidate along the segment —
+                // decide them against the face's cone list instead
+                if (coneL == kConeUnbuilt && cbuf) {
+                    coneL = build_cone<MAXV, RES>(s, ctx, f, sx, sy, sz, sf, cbuf, ccap, batches);
+                    K4P(12, 1);
+                    K4P(13, coneL < 0 ? 1 : 0);
+                    K4P(14, coneL < 0 ? 0 : coneL);
+                }
             } else {
                 cache.put(h);
                 if (lane == L) {   // the sweep proved this sample blocked
@@ -820,10 +962,13 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
     const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
     int* fan = fan_buf[threadIdx.x >> 5];
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
+    const float4* cbuf = a.cone_buf ? a.cone_buf + static_cast<size_t>((blockIdx.x * NT + threadIdx.x) >> 5) * 2 *
+                                                       a.cone_cap
+                                    : nullptr;
     unsigned long long tests = 0, queries = 0, batches = 0;
     WCache cache;   // the last blockers (Morton indices)
 #ifdef VISRT_K4W_PROF
-    if (threadIdx.x < 16) k4w_sprof[threadIdx.x] = 0;
+    if (threadIdx.x < 24) k4w_sprof[threadIdx.x] = 0;
     __syncthreads();
 #endif
     long long tnext = 0, tend = 0;
@@ -849,6 +994,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
         int8_t present = 1;
         int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
         double sub[6] = {0, 0, 0, 0, 0, 0};
+        int coneL = kConeUnbuilt;   // this task's cone list: built at its first clear sample
         // back-face test (src/vistable.cpp:289-294)
         {
             const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
@@ -866,18 +1012,20 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             const double len2 = dadd(dmul(dx, dx), dmul(dy, dy));
             if (len2 <= kEps * kEps) continue;   // no face_param in this plane
             double us[2 * MAXV];
+#pragma unroll 1
             for (int q = 0; q < nv; ++q) face_us(s, f, pl, q, ax, ay, dx, dy, len2, us[2 * q], us[2 * q + 1]);
             // col_vis (src/vistable.cpp:146-159)
             auto col_vis = [&](double u) -> bool {
-                return col_vis_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, u, sx, sy, sz, sf, sv, cache, tests,
+                return col_vis_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, u, sx, sy, sz, sf, sv, cache, tests,
                                           queries, batches);
             };
             if (presence) {   // a visible column <=> a non-empty interval list
                 bool any = false;
                 if (VISRT_K4W_PSCAN) {
                     bool v64;
-                    any = scan_cols_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, true,
-                                               v64, tests, queries, batches) != 0ull || v64;
+                    any = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, true,
+                                               v64, tests, queries, batches, f, cbuf, a.cone_cap, coneL) != 0ull ||
+                          v64;
                 } else {
                     for (int i = 0; i < 65 && !any; ++i) any = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
                 }
@@ -892,8 +1040,8 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             bool vis64 = false;
             const long long sclk0 = K4CLK();
             if (VISRT_K4W_PSCAN) {
-                vis = scan_cols_warp<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, false, vis64,
-                                           tests, queries, batches);
+                vis = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, false, vis64,
+                                           tests, queries, batches, f, cbuf, a.cone_cap, coneL);
             } else {
                 for (int i = 0; i < 65; ++i) {
                     const bool v = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
@@ -908,8 +1056,8 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
                 const long long rclk0 = K4CLK();
                 int it = 0;
                 if (VISRT_K4W_FAN && a.fan &&
-                    refine_fan<MAXV>(s, ctx, us, nv, pl, ax, ay, dx, dy, lo, hi, lo_vis, sx, sy, sz, sf, fan,
-                                     tests, queries, batches, it)) {
+                    refine_fan<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, lo, hi, lo_vis, sx, sy, sz, sf, fan,
+                                     tests, queries, batches, it, cbuf, coneL)) {
                     K4P(1, K4CLK() - rclk0);
                     K4P(6, 1);
                     K4P(7, it);
@@ -935,11 +1083,18 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
                     continue;
                 }
                 double start = __ddiv_rn(static_cast<double>(i), 64.0);
-                if (i > 0) start = refine(dsub(start, step), start, false);
                 int j = i;
                 while (j + 1 < 65 && V(j + 1)) ++j;
                 double end = __ddiv_rn(static_cast<double>(j), 64.0);
-                if (j + 1 < 65) end = refine(end, dadd(end, step), true);
+                // the run's interior boundaries, start then end (one refine call site: i-cache)
+#pragma unroll 1
+                for (int side = 0; side < 2; ++side) {
+                    if (side == 0 ? i == 0 : j + 1 == 65) continue;
+                    const double r = refine(side == 0 ? dsub(start, step) : end, side == 0 ? start : dadd(end, step),
+                                            side == 1);
+                    if (side == 0) start = r;
+                    else end = r;
+                }
                 if (!have || dsub(b1, b0) < dsub(end, start)) {   // std::max_element: first largest
                     b0 = start;
                     b1 = end;
@@ -984,7 +1139,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
     }
 #ifdef VISRT_K4W_PROF
     __syncthreads();
-    if (threadIdx.x < 16) atomicAdd(&g_k4w_prof[threadIdx.x], k4w_sprof[threadIdx.x]);
+    if (threadIdx.x < 24) atomicAdd(&g_k4w_prof[threadIdx.x], k4w_sprof[threadIdx.x]);
 #endif
 }
 
@@ -993,7 +1148,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
 extern "C" int visrt_debug_k4w_prof(unsigned long long* out) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, visrt::g_k4w_prof, sizeof(visrt::g_k4w_prof));
-    static const unsigned long long zero[16] = {};
+    static const unsigned long long zero[24] = {};
     return static_cast<int>(cudaMemcpyToSymbol(visrt::g_k4w_prof, zero, sizeof(zero)));
 }
 namespace visrt {
@@ -1007,13 +1162,34 @@ static int persistent_grid_r(const void* fn, size_t smem, int device, int thread
     return sms * per;
 }
 
+// K4w cone-list capacity per warp (VISRT_K4W_CONE, entries of 32 B; 0 = no cone lists)
+static int cone_cap_r() {
+    static const int c = [] {
+        const char* e = std::getenv("VISRT_K4W_CONE");
+        return e ? std::max(0, std::atoi(e)) : 1024;
+    }();
+    return c;
+}
+void* region_scratch_alloc(size_t bytes);                 // BlockCache (below)
+void region_scratch_release(void* p, cudaStream_t st);    // after the stream's queued work
+
 template <class K>
-static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a, int device, cudaStream_t st,
-                            int threads = kThreads) {
+static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a0, int device, cudaStream_t st,
+                            int threads = kThreads, bool cone = false) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    fn<<<persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads), threads, smem, st>>>(a);
-    return cudaGetLastError();
+    const int grid = persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads);
+    RegionArgs a = a0;
+    void* cb = nullptr;
+    if (cone && cone_cap_r() > 0 && !a.presence_only) {
+        a.cone_cap = cone_cap_r();
+        cb = region_scratch_alloc(static_cast<size_t>(grid) * (threads / 32) * a.cone_cap * 32);
+        a.cone_buf = static_cast<float4*>(cb);
+    }
+    fn<<<grid, threads, smem, st>>>(a);
+    e = cudaGetLastError();
+    if (cb) region_scratch_release(cb, st);
+    return e;
 }
 
 // K4w threads per QUANTISED CTA (one CTA per SM: 16 warps at 128 registers)
@@ -1067,8 +1243,8 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
             return launch_r(k_point_regions_warp<MAXV, kQuantised, kQThreadsK4, 1>, qsm, a, device, st, kQThreadsK4);
     }
     if (warp)
-        return res ? launch_r(k_point_regions_warp<MAXV, kResident>, smem, a, device, st)
-                   : launch_r(k_point_regions_warp<MAXV, kStreamed>, smem, a, device, st);
+        return res ? launch_r(k_point_regions_warp<MAXV, kResident>, smem, a, device, st, kThreads, true)
+                   : launch_r(k_point_regions_warp<MAXV, kStreamed>, smem, a, device, st, kThreads, true);
     return res ? launch_r(k_point_regions<MAXV, true>, smem, a, device, st)
                : launch_r(k_point_regions<MAXV, false>, smem, a, device, st);
 }
@@ -1275,7 +1451,7 @@ __global__ void __launch_bounds__(NT, MINB) k_segments_clear_warp(DevScene s, lo
                                      by, bz);
         }
         if (!blocked) {
-            const int h = coop_any_hit<MAXV>(ctx, s.srec, make_segf(s, ax, ay, az, bx, by, bz), ax, ay, az, bx, by,
+            const int h = coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, ax, ay, az, bx, by, bz), ax, ay, az, bx, by,
                                              bz, -1, -1, -1, sv, tests, batches);
             blocked = h >= 0;
             if (blocked) cache = h;
@@ -1339,6 +1515,17 @@ cudaError_t launch_beam_rows(const BeamArgs& a, cudaStream_t st) {
 // C-ABI entry (include/visrt.h)
 // ---------------------------------------------------------------------------
 #include "capi_internal.h"
+
+namespace visrt {
+void* region_scratch_alloc(size_t bytes) { return BlockCache::get().alloc(bytes); }
+// the block goes back to the cache once the stream has run everything queued so far
+void region_scratch_release(void* p, cudaStream_t st) {
+    if (cudaLaunchHostFunc(st, [](void* q) { BlockCache::get().release(q); }, p) != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        BlockCache::get().release(p);
+    }
+}
+}  // namespace visrt
 
 extern "C" int visrt_point_regions(visrt_scene* sc, int64_t nsrc, const double* src_xyz, visrt_region* out,
                                    visrt_stats* stats, void* stream) {

@@ -100,9 +100,22 @@ __device__ __forceinline__ bool qsat(uint2 b, const QSeg& g) {
     return ok;
 }
 
+// Residency of a sweep: compile-time (RES >= 0, the kernel's template
+// argument: dead paths drop out and the code stays i-cache sized) or read
+// from the context (RES = -1).
+template <int RES>
+__device__ __forceinline__ bool use_groups(const SweepCtx& c) {
+    return RES == kStreamed ? VISRT_GROUPS != 0 : (RES < 0 ? c.gbox != nullptr : false);
+}
+template <int RES>
+__device__ __forceinline__ bool use_qbox(const SweepCtx& c) {
+    return RES == kQuantised ? true : (RES < 0 ? c.qbox != nullptr : false);
+}
+
 // Member box k (Morton index) may meet segment g — any residency mode.
+template <int RES = -1>
 __device__ __forceinline__ bool member_maybe(const SweepCtx& c, int k, const SegF& g) {
-    if (c.qbox) return qsat(c.qbox[k], make_qseg(g, c.tframe + static_cast<size_t>(k >> 6) * 8));
+    if (use_qbox<RES>(c)) return qsat(c.qbox[k], make_qseg(g, c.tframe + static_cast<size_t>(k >> 6) * 8));
     return sat_maybe(c.mbox + static_cast<size_t>(k) * 8, g);
 }
 
@@ -331,12 +344,12 @@ __device__ __forceinline__ int coop_any_hit_grouped(const SweepCtx& ctx, const d
     return -1;
 }
 
-template <int MAXV, int FIRST = 0>
+template <int MAXV, int FIRST = 0, int RES = -1>
 __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* __restrict__ srec, const SegF& g,
                                             double ax, double ay, double az, double bx, double by, double bz,
                                             int skip0, int skip1, int home, unsigned char* sv,
                                             unsigned long long& tests, unsigned long long& batches) {
-    if (ctx.gbox) return coop_any_hit_grouped<MAXV>(ctx, srec, g, ax, ay, az, bx, by, bz, skip0, skip1, home, tests,
+    if (use_groups<RES>(ctx)) return coop_any_hit_grouped<MAXV>(ctx, srec, g, ax, ay, az, bx, by, bz, skip0, skip1, home, tests,
                                                    batches);
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
@@ -370,7 +383,7 @@ __device__ __forceinline__ int coop_any_hit(const SweepCtx& ctx, const double* _
             const int mc = min(kTile, ctx.n - base);
             const int m0 = base + lane, m1 = base + lane + 32;
             bool v0, v1;
-            if (ctx.qbox) {
+            if (use_qbox<RES>(ctx)) {
                 const QSeg qs = make_qseg(g, ctx.tframe + static_cast<size_t>(base >> 6) * 8);
                 v0 = lane < mc && m0 != skip0 && m0 != skip1 && qsat(ctx.qbox[m0], qs);
                 v1 = lane + 32 < mc && m1 != skip0 && m1 != skip1 && qsat(ctx.qbox[m1], qs);
@@ -427,9 +440,10 @@ __device__ __forceinline__ bool sat_maybe_dil(const float* __restrict__ B, const
 // traversal order; returns their count, or -1 when more than `cap` faces
 // qualify or the member boxes are quantised (the caller falls back to
 // per-sightline sweeps). Warp-uniform arguments; all 32 lanes.
+template <int RES = -1>
 __device__ __forceinline__ int coop_collect(const SweepCtx& ctx, const SegF& g, float R, int skip, int* list,
                                             int cap, unsigned long long& batches) {
-    if (ctx.qbox) return -1;
+    if (use_qbox<RES>(ctx)) return -1;
     constexpr int GPT = kTile / kGroup;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -450,7 +464,7 @@ __device__ __forceinline__ int coop_collect(const SweepCtx& ctx, const SegF& g, 
         unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
                                   (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
         ++batches;
-        if (ctx.gbox) {   // streamed: 8 candidate tiles x 4 groups per round, then 2 groups of members
+        if (use_groups<RES>(ctx)) {   // streamed: 8 candidate tiles x 4 groups per round, then 2 groups of members
             while (cand) {
                 int my_tile = -1;
 #pragma unroll
@@ -495,6 +509,116 @@ __device__ __forceinline__ int coop_collect(const SweepCtx& ctx, const SegF& g, 
         }
     }
     return cnt;
+}
+
+// A CONE: every segment from the apex S to a point of a target face F lies in
+// the pyramid hull(S, F). A point at parameter t of such a segment is within
+// t * r of the axis point S + t (c - S) (c the centre of F's box, r its
+// half-diagonal), so the pyramid lies inside the union of three tapered
+// pieces: axis t in [0, 1/2] dilated by r/2, [1/2, 3/4] by 3r/4, [3/4, 1] by r.
+// A box that misses all three pieces (sat_maybe_dil) cannot meet any segment
+// S -> F: its face can block none of them.
+struct ConeF {
+    SegF g[3];
+    float R[3];
+};
+
+__device__ __forceinline__ bool cone_maybe(const float* __restrict__ B, const ConeF& c) {
+    return sat_maybe_dil(B, c.g[0], c.R[0]) | sat_maybe_dil(B, c.g[1], c.R[1]) | sat_maybe_dil(B, c.g[2], c.R[2]);
+}
+
+// Collecting sweep of a cone: every face (Morton index, `skip` excluded) whose
+// culling box may meet the cone, written to `out` (global, per warp: entry e =
+// out[2e] {cx, cy, cz, index as int bits}, out[2e + 1] {hx, hy, hz, 0} — the
+// member box with its face) in traversal order. Returns the count, or -1 when
+// more than `cap` faces qualify or the member boxes are quantised. No exact
+// tests, no early exit. Warp-uniform arguments; all 32 lanes.
+template <int RES = -1>
+__device__ __forceinline__ int coop_collect_cone(const SweepCtx& ctx, const ConeF& cone, int skip, float4* out,
+                                                 int cap, unsigned long long& batches) {
+    if (use_qbox<RES>(ctx)) return -1;
+    constexpr int GPT = kTile / kGroup;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int cnt = 0;
+    auto append = [&](bool v, int m) -> bool {   // false: overflow
+        const unsigned b = __ballot_sync(kFull, v);
+        const int at = cnt + __popc(b & lt);
+        if (v && at < cap) {
+            const float4* B = reinterpret_cast<const float4*>(ctx.mbox + static_cast<size_t>(m) * 8);
+            float4 b0 = B[0];
+            b0.w = __int_as_float(m);
+            out[2 * at] = b0;
+            out[2 * at + 1] = B[1];
+        }
+        cnt += __popc(b);
+        return cnt <= cap;
+    };
+    for (int c = 0; c < ctx.nchunks; ++c) {
+        const int t0 = c * kTile;
+        const int tc = min(kTile, ctx.ntiles - t0);
+        if (VISRT_CHUNK_BOXES && ctx.nchunks > 1 && !cone_maybe(ctx.cbox + static_cast<size_t>(c) * 8, cone)) continue;
+        const bool h0 = lane < tc && cone_maybe(ctx.tbox + static_cast<size_t>(t0 + lane) * 8, cone);
+        const bool h1 = lane + 32 < tc && cone_maybe(ctx.tbox + static_cast<size_t>(t0 + lane + 32) * 8, cone);
+        unsigned long long cand = static_cast<unsigned long long>(__ballot_sync(kFull, h0)) |
+                                  (static_cast<unsigned long long>(__ballot_sync(kFull, h1)) << 32);
+        ++batches;
+        if (use_groups<RES>(ctx)) {   // streamed: 8 candidate tiles x 4 groups per round, then 2 groups of members
+            while (cand) {
+                int my_tile = -1;
+#pragma unroll
+                for (int q = 0; q < 32 / GPT; ++q) {
+                    if (!cand) break;
+                    const int t = t0 + __ffsll(static_cast<long long>(cand)) - 1;
+                    cand &= cand - 1;
+                    if (q == lane / GPT) my_tile = t;
+                }
+                const int grp = my_tile * GPT + (lane % GPT);
+                const bool gv = my_tile >= 0 && grp < ctx.ngroups &&
+                                cone_maybe(ctx.gbox + static_cast<size_t>(grp) * 8, cone);
+                unsigned gm = __ballot_sync(kFull, gv);
+                ++batches;
+                while (gm) {
+                    const int la = __ffs(gm) - 1;
+                    gm &= gm - 1;
+                    const int lb = gm ? __ffs(gm) - 1 : -1;
+                    if (lb >= 0) gm &= gm - 1;
+                    const int ga = __shfl_sync(kFull, grp, la);
+                    const int gb = __shfl_sync(kFull, grp, lb < 0 ? la : lb);
+                    const int mg = lane < kGroup ? ga : (lb < 0 ? -1 : gb);
+                    const int m = mg * kGroup + (lane & (kGroup - 1));
+                    const bool v = mg >= 0 && m < ctx.n && m != skip &&
+                                   cone_maybe(ctx.mbox + static_cast<size_t>(m) * 8, cone);
+                    ++batches;
+                    if (!append(v, m)) return -1;
+                }
+            }
+        } else {   // member boxes in shared memory: 64 per candidate tile
+            while (cand) {
+                const int base = (t0 + __ffsll(static_cast<long long>(cand)) - 1) * kTile;
+                cand &= cand - 1;
+                const int mc = min(kTile, ctx.n - base);
+                const int m0 = base + lane, m1 = base + lane + 32;
+                const bool v0 = lane < mc && m0 != skip && cone_maybe(ctx.mbox + static_cast<size_t>(m0) * 8, cone);
+                const bool v1 = lane + 32 < mc && m1 != skip && cone_maybe(ctx.mbox + static_cast<size_t>(m1) * 8, cone);
+                ++batches;
+                if (!append(v0, m0) || !append(v1, m1)) return -1;
+            }
+        }
+    }
+    return cnt;
+}
+
+// sat_maybe on a cone-list entry (two float4: centre, half extent)
+__device__ __forceinline__ bool sat_maybe4(const float4& c, const float4& h, const SegF& g) {
+    const float dx = g.mx - c.x, dy = g.my - c.y, dz = g.mz - c.z;
+    bool ok = fabsf(dx) <= h.x + g.ax;
+    ok &= fabsf(dy) <= h.y + g.ay;
+    ok &= fabsf(dz) <= h.z + g.az;
+    ok &= fabsf(__fmaf_rn(dy, g.ez, -dz * g.ey)) <= __fmaf_rn(h.y, g.az, h.z * g.ay);
+    ok &= fabsf(__fmaf_rn(dz, g.ex, -dx * g.ez)) <= __fmaf_rn(h.x, g.az, h.z * g.ax);
+    ok &= fabsf(__fmaf_rn(dx, g.ey, -dy * g.ex)) <= __fmaf_rn(h.x, g.ay, h.y * g.ax);
+    return ok;
 }
 
 // Block setup: stage the tile boxes (and the member boxes when resident,

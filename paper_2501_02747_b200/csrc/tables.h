@@ -34,6 +34,8 @@ struct RegionArgs {
     int chunk = 1;                          // K4w: consecutive tasks per warp grab (set by the launcher)
     int face_major = 1;                     // walk order of the all-faces / face-list modes (see above)
     int fan = 1;                            // K4w: refine run boundaries with fan candidate lists
+    float4* cone_buf = nullptr;             // K4w: per-warp cone lists (cone_cap entries of 2 float4), set by the launcher
+    int cone_cap = 0;
 };
 
 struct RegionTask {

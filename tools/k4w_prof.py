@@ -12,7 +12,7 @@ for arg in sys.argv[1:] or ["5:20:rx", "5:20:tx", "3:200:mix"]:
     wl = scenes.workload(cfg)
     src = {"tx": wl.tx, "rx": wl.rx, "mix": np.concatenate([wl.tx[:nsrc // 2], wl.rx[:nsrc - nsrc // 2]])}[which][:nsrc]
     with Scene(wl.scene) as sc:
-        out = (C.c_ulonglong * 16)()
+        out = (C.c_ulonglong * 24)()
         lib().visrt_debug_k4w_prof(out)   # reset
         arr, st = point_regions_array(sc, src)
         lib().visrt_debug_k4w_prof(out)
@@ -21,4 +21,6 @@ for arg in sys.argv[1:] or ["5:20:rx", "5:20:tx", "3:200:mix"]:
     print(f"cfg{cfg}/{which} nsrc={nsrc}: {st['ms']:.1f} ms; task cycles {o[8]:.3e}: scan {100*o[0]/tot:.1f}% "
           f"refine {100*o[1]/tot:.1f}% present-tasks {100*o[10]/tot:.1f}% ({o[11]} of {o[9]} front-facing); "
           f"scan sweeps {o[2]} clear {o[3]}; refine calls {o[6]} iters {o[7]} sweeps {o[4]} clear {o[5]}; "
-          f"cycles/sweep scan {o[0]/max(o[2],1):.0f} refine {o[1]/max(o[4],1):.0f}", flush=True)
+          f"cycles/sweep scan {o[0]/max(o[2],1):.0f} refine {o[1]/max(o[4],1):.0f}; "
+          f"cone lists {o[12]} overflow {o[13]} mean length {o[14]/max(o[12]-o[13],1):.0f} scan iterations {o[15]:.3e}; "
+          f"refine fan build {100*o[16]/tot:.1f}% fans {o[18]} mean T {o[17]/max(o[18],1):.1f}", flush=True)
