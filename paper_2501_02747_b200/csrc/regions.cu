@@ -112,6 +112,42 @@ __device__ bool column_span_us(const double* us, int nv, double u, double& lo_o,
     return any;
 }
 
+// column_span_us for one warp-uniform u with the polygon edges on lanes
+// 0..nv-1: each lane forms its edge's taken values in the reference's order,
+// then an order-preserving tree reduction (std::min / std::max keep the
+// earlier of equal values, and "leftmost extremum" is associative) gives the
+// sequential fold's lo / hi. All lanes; uniform result.
+__device__ bool column_span_warp(const double* us, int nv, double u, double& lo_o, double& hi_o) {
+    const int lane = threadIdx.x & 31;
+    double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;   // +inf / -inf: nothing taken
+    if (lane < nv) {
+        const double ua = us[2 * lane], sa = us[2 * lane + 1];
+        const double ub = lane + 1 < nv ? us[2 * lane + 2] : us[0];
+        const double sb = lane + 1 < nv ? us[2 * lane + 3] : us[1];
+        const double da = dsub(ua, u), db = dsub(ub, u);
+        if (fabs(da) <= 1e-12) {
+            lo = sa;
+            hi = sa;
+        }
+        if ((da < 0.0) != (db < 0.0) && fabs(dsub(da, db)) > 1e-15) {
+            const double sv = dadd(sa, dmul(dsub(sb, sa), __ddiv_rn(da, dsub(da, db))));
+            lo = dmin_std(lo, sv);
+            hi = dmax_std(hi, sv);
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {   // lane l combines with lane l + o (its right neighbour run)
+        const double rl = __shfl_down_sync(kFull, lo, o), rh = __shfl_down_sync(kFull, hi, o);
+        lo = dmin_std(lo, rl);
+        hi = dmax_std(hi, rh);
+    }
+    lo = __shfl_sync(kFull, lo, 0);
+    hi = __shfl_sync(kFull, hi, 0);
+    lo_o = lo;
+    hi_o = hi;
+    return lo <= hi;
+}
+
 // double(j) / (kTransverse - 1), j = 0..6 (correctly rounded, as the reference)
 __constant__ double kSampFrac[7] = {0.0 / 6.0, 1.0 / 6.0, 2.0 / 6.0, 3.0 / 6.0, 4.0 / 6.0, 5.0 / 6.0, 6.0 / 6.0};
 
@@ -620,7 +656,7 @@ constexpr int kFanCap = 32;
 
 // The entries of a cone list whose box, dilated by R, meets g (in list order)
 // -> fl; returns their count or -1 when more than cap qualify.
-__device__ __forceinline__ int cone_filter(const float4* cbuf, int L, const SegF& g, float R, int* fl, int cap) {
+__device__ __forceinline__ int cone_filter(ConeBuf cbuf, int L, const SegF& g, float R, int* fl, int cap) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     int cnt = 0;
@@ -629,8 +665,9 @@ __device__ __forceinline__ int cone_filter(const float4* cbuf, int L, const SegF
         bool v = false;
         int m = 0;
         if (e < L) {
-            float4 c = cbuf[2 * e];
-            float4 h = cbuf[2 * e + 1];
+            const float4* E = cbuf.at(e);
+            float4 c = E[0];
+            float4 h = E[1];
             m = __float_as_int(c.w);
             h.x += R;
             h.y += R;
@@ -651,11 +688,21 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
                                         double ax, double ay, double dx, double dy, double& lo_io, double& hi_io,
                                         bool lo_vis, double sx, double sy, double sz, int sf, int* fl,
                                         unsigned long long& tests, unsigned long long& queries,
-                                        unsigned long long& batches, int& iters, const float4* cbuf, int coneL) {
+                                        unsigned long long& batches, int& iters, ConeBuf cbuf, int coneL) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
     double lo = lo_io, hi = hi_io;
     // per-sample end-point boxes (lane j < 7)
+    // sample j of column u from its span [cs0, cs1] (col_vis, src/vistable.cpp:150-156)
+    auto point_at = [&](double cu, double cs0, double cs1, int j, double& qx, double& qy, double& qz) {
+        const double inset = dmul(dsub(cs1, cs0), 1e-6);
+        const double px = dadd(ax, dmul(dx, cu));
+        const double py = dadd(ay, dmul(dy, cu));
+        const double v = dmin_std(dsub(cs1, inset), dmax_std(dadd(cs0, inset), dadd(cs0, dmul(dsub(cs1, cs0), kSampFrac[j]))));
+        if (pl == 0) { qx = px; qy = py; qz = v; }
+        else if (pl == 1) { qx = v; qy = px; qz = py; }
+        else { qx = px; qy = v; qz = py; }
+    };
     auto sample = [&](double u, int j, double& qx, double& qy, double& qz) -> bool {
         const double cu = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);   // std::clamp
         double cs0, cs1;
@@ -709,44 +756,84 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
     }
     __syncwarp();
     K4P(16, K4CLK() - fclk0);
-    int excl = my_cnt;
+    int T = my_cnt;   // every sample's fan: the pairs of one step
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, excl, o);
-        if (lane >= o) excl += v;
-    }
-    const int T = __shfl_sync(kFull, excl, 6);
-    excl -= my_cnt;
+    for (int o = 1; o < 8; o <<= 1) T += __shfl_xor_sync(kFull, T, o) * (lane < 8 ? 1 : 0);
+    T = __shfl_sync(kFull, T, 0);
     K4P(17, T);
     K4P(18, 1);
+    // Lane l < 7 evaluates sample jl = (l + rot) mod 7: the sample found clear
+    // by the previous step leads (neighbouring midpoints mostly share the
+    // verdict), and the step stops as soon as its verdict is known — a valid
+    // sample whose pairs are all tested without a hit (visible), or every
+    // valid sample blocked (hidden).
+    int rot = 0, jl = lane, cl = my_cnt, excl = 0;
+    auto order = [&]() {
+        jl = lane < 7 ? (lane + rot >= 7 ? lane + rot - 7 : lane + rot) : lane;
+        cl = __shfl_sync(kFull, my_cnt, jl & 31);
+        if (lane >= 7) cl = 0;
+        excl = cl;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, excl, o);
+            if (lane >= o) excl += v;
+        }
+        excl -= cl;
+    };
+    order();
     int it = 0;
     for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
         const double mid = dmul(0.5, dadd(lo, hi));
         double qx = 0, qy = 0, qz = 0;
-        const bool valid = lane < 7 && sample(mid, lane, qx, qy, qz);
-        unsigned blocked = 0;
-        for (int r = 0; r < T; r += 32) {
+        const long long sc0_ = K4CLK();
+        // the step's column span once, its edges on lanes (column_span_warp)
+        const double cu = mid < 0.0 ? 0.0 : (1.0 < mid ? 1.0 : mid);   // std::clamp
+        double cs0, cs1;
+        const bool span = column_span_warp(us, nv, cu, cs0, cs1);
+        const bool valid = lane < 7 && span;
+        if (valid) point_at(cu, cs0, cs1, jl, qx, qy, qz);
+        K4P(22, K4CLK() - sc0_);
+        unsigned blocked = 0;   // bit l: lane l's sample is blocked
+        bool vis = __any_sync(kFull, valid && cl == 0);   // an empty fan: clear
+        int clear_lane = vis ? __ffs(__ballot_sync(kFull, valid && cl == 0)) - 1 : -1;
+        for (int r = 0; r < T && !vis; r += 32) {
             const int g = r + lane;
-            int j = 0;
+            int l = 0;
 #pragma unroll
             for (int k = 1; k < 7; ++k)
-                if (__shfl_sync(kFull, excl, k) <= g) j = k;
-            const int ej = __shfl_sync(kFull, excl, j);
-            const double ox = __shfl_sync(kFull, qx, j), oy = __shfl_sync(kFull, qy, j),
-                         oz = __shfl_sync(kFull, qz, j);
-            const bool ov = __shfl_sync(kFull, valid, j);
+                if (__shfl_sync(kFull, excl, k) <= g) l = k;
+            const int el = __shfl_sync(kFull, excl, l);
+            const int jj = __shfl_sync(kFull, jl, l);
+            const double ox = __shfl_sync(kFull, qx, l), oy = __shfl_sync(kFull, qy, l),
+                         oz = __shfl_sync(kFull, qz, l);
+            const bool ov = __shfl_sync(kFull, valid, l);
             bool hit = false;
-            if (g < T && ov && !((blocked >> j) & 1u)) {
+            if (g < T && ov && !((blocked >> l) & 1u)) {
                 ++tests;
-                hit = seg_hits<MAXV>(s.srec + static_cast<size_t>(fl[j * kFanCap + g - ej]) * STRIDE, sx, sy, sz, ox,
+                hit = seg_hits<MAXV>(s.srec + static_cast<size_t>(fl[jj * kFanCap + g - el]) * STRIDE, sx, sy, sz, ox,
                                      oy, oz);
             }
-            blocked |= __reduce_or_sync(kFull, hit ? 1u << j : 0u);
+            blocked |= __reduce_or_sync(kFull, hit ? 1u << l : 0u);
+            const bool open = valid && !((blocked >> lane) & 1u);
+            const unsigned done = __ballot_sync(kFull, open && excl + cl <= r + 32);
+            if (done) {   // a sample clear of its whole fan
+                vis = true;
+                clear_lane = __ffs(done) - 1;
+            } else if (!__any_sync(kFull, open)) {
+                break;   // every sample blocked
+            }
         }
+        K4P(23, K4CLK() - sc0_);
         queries += lane == 0 ? 7 : 0;
-        const bool vis = __any_sync(kFull, valid && !((blocked >> lane) & 1u));
         if (vis == lo_vis) lo = mid;
         else hi = mid;
+        if (vis) {
+            const int nr = __shfl_sync(kFull, jl, clear_lane);
+            if (nr != rot) {
+                rot = nr;
+                order();
+            }
+        }
     }
     iters = it;
     lo_io = lo;
@@ -762,7 +849,7 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
 constexpr int kConeUnbuilt = -2;
 template <int MAXV, int RES>
 __device__ __noinline__ int build_cone(const DevScene& s, const SweepCtx& ctx, int f, double sx, double sy, double sz,
-                                       int sf, const float4* cbuf, int ccap, unsigned long long& batches) {
+                                       int sf, ConeBuf cbuf, unsigned long long& batches) {
     const double* bb = s.aabb + static_cast<size_t>(f) * 6;
     const double cx = 0.5 * (bb[0] + bb[3]), cy = 0.5 * (bb[1] + bb[4]), cz = 0.5 * (bb[2] + bb[5]);
     const double ex = bb[3] - bb[0], ey = bb[4] - bb[1], ez = bb[5] - bb[2];
@@ -776,7 +863,7 @@ __device__ __noinline__ int build_cone(const DevScene& s, const SweepCtx& ctx, i
                               sy + t1 * (cy - sy), sz + t1 * (cz - sz));
         cone.R[p] = static_cast<float>(t1 * r * 1.0001 + 1e-6);
     }
-    const int L = coop_collect_cone<RES>(ctx, cone, sf, const_cast<float4*>(cbuf), ccap, batches);
+    const int L = coop_collect_cone<RES>(ctx, cone, sf, cbuf, batches);
     __syncwarp();   // the list's stores are read back by every lane
     return L;
 }
@@ -798,8 +885,8 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                                                           double sx, double sy, double sz, int sf, unsigned char* sv,
                                                           WCache& cache, bool stop_at_first, bool& vis64,
                                                           unsigned long long& tests, unsigned long long& queries,
-                                                          unsigned long long& batches, int f, const float4* cbuf,
-                                                          int ccap, int& coneL) {
+                                                          unsigned long long& batches, int f, ConeBuf cbuf,
+                                                          int& coneL) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
     unsigned long long vis = 0;
@@ -825,19 +912,11 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             ++queries;
         };
         if (pending) point();
-        // advance this lane's column over the samples occluder k (Morton index) blocks
+        // advance this lane's column over the samples occluder k (Morton index)
+        // blocks (warp-uniform k: the lanes test one record in lockstep — a
+        // per-lane walk over the whole cache was measured slower, divergent)
         auto settle = [&](int k) {
-            const float* B = ctx.mbox + static_cast<size_t>(k) * 8;
-            const double* R = s.srec + static_cast<size_t>(k) * STRIDE;
-#if VISRT_K4W_NI
-            (void)B;
-            (void)R;
             while (pending && k4w_blocked<MAXV, RES>(s, ctx, k, sx, sy, sz, qx, qy, qz, tests)) {
-#else
-            while (pending && member_maybe<RES>(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) {
-                ++tests;
-                if (!seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz)) break;
-#endif
                 if (++j == 7) pending = false;   // every sample blocked: column hidden
                 else point();
             }
@@ -859,14 +938,15 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             SegF g{};
             if (pending) g = make_segf(s, sx, sy, sz, qx, qy, qz);
             int left = Lc, c = 0;
-            float4 n0 = cbuf[0], n1 = cbuf[1];   // entry c, loaded one iteration ahead
+            float4 n0 = cbuf.at(0)[0], n1 = cbuf.at(0)[1];   // entry c, loaded one iteration ahead
             while (__any_sync(kFull, pending)) {
                 if (stop_at_first && __any_sync(kFull, visible)) break;
                 K4P(15, 1);
                 const float4 b0 = n0, b1 = n1;
                 const int cn = c + 1 == Lc ? 0 : c + 1;
-                n0 = cbuf[2 * cn];
-                n1 = cbuf[2 * cn + 1];
+                const float4* E = cbuf.at(cn);
+                n0 = E[0];
+                n1 = E[1];
                 if (pending) {
                     // entry c against this lane's sample, and against the next
                     // samples of the column while it blocks them (a blocker of
@@ -895,7 +975,7 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
         };
         for (;;) {
             if (coneL >= 0) {
-                cone_scan();
+                { const long long c0_ = K4CLK(); cone_scan(); K4P(20, K4CLK() - c0_); }
                 break;
             }
             const unsigned who = __ballot_sync(kFull, pending);
@@ -904,12 +984,14 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
             const double bx = __shfl_sync(kFull, qx, L), by = __shfl_sync(kFull, qy, L),
                          bz = __shfl_sync(kFull, qz, L);
 #if VISRT_K4W_NI
+            const long long w0_ = K4CLK();
             const int h = k4w_sweep<MAXV, RES>(s, ctx, sx, sy, sz, bx, by, bz, sf, sv, tests, batches);
 #else
             const int h = coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz,
                                              sf, -1, sf, sv, tests, batches);
 #endif
             K4P(2, 1);
+            K4P(21, K4CLK() - w0_);
             if (h < 0) K4P(3, 1);
             if (h < 0) {   // a clear sample: column L is visible
                 if (lane == L) {
@@ -920,8 +1002,10 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                 // a (partly) visible face: its remaining samples are mostly clear
                 // and a clear sweep visits every candidate along the segment —
                 // decide them against the face's cone list instead
-                if (coneL == kConeUnbuilt && cbuf) {
-                    coneL = build_cone<MAXV, RES>(s, ctx, f, sx, sy, sz, sf, cbuf, ccap, batches);
+                if (coneL == kConeUnbuilt && cbuf.cap > 0) {
+                    const long long b0_ = K4CLK();
+                    coneL = build_cone<MAXV, RES>(s, ctx, f, sx, sy, sz, sf, cbuf, batches);
+                    K4P(19, K4CLK() - b0_);
                     K4P(12, 1);
                     K4P(13, coneL < 0 ? 1 : 0);
                     K4P(14, coneL < 0 ? 0 : coneL);
@@ -962,9 +1046,10 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
     const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
     int* fan = fan_buf[threadIdx.x >> 5];
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
-    const float4* cbuf = a.cone_buf ? a.cone_buf + static_cast<size_t>((blockIdx.x * NT + threadIdx.x) >> 5) * 2 *
-                                                       a.cone_cap
-                                    : nullptr;
+    ConeBuf cbuf;   // this warp's cone list
+    cbuf.cap = a.cone_buf ? a.cone_cap : 0;
+    cbuf.g = a.cone_buf ? a.cone_buf + static_cast<size_t>((blockIdx.x * NT + threadIdx.x) >> 5) * 2 * a.cone_cap
+                        : nullptr;
     unsigned long long tests = 0, queries = 0, batches = 0;
     WCache cache;   // the last blockers (Morton indices)
 #ifdef VISRT_K4W_PROF
@@ -1024,7 +1109,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
                 if (VISRT_K4W_PSCAN) {
                     bool v64;
                     any = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, true,
-                                               v64, tests, queries, batches, f, cbuf, a.cone_cap, coneL) != 0ull ||
+                                               v64, tests, queries, batches, f, cbuf, coneL) != 0ull ||
                           v64;
                 } else {
                     for (int i = 0; i < 65 && !any; ++i) any = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
@@ -1041,7 +1126,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             const long long sclk0 = K4CLK();
             if (VISRT_K4W_PSCAN) {
                 vis = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, false, vis64,
-                                           tests, queries, batches, f, cbuf, a.cone_cap, coneL);
+                                           tests, queries, batches, f, cbuf, coneL);
             } else {
                 for (int i = 0; i < 65; ++i) {
                     const bool v = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
@@ -1178,11 +1263,11 @@ static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a0, int device,
                             int threads = kThreads, bool cone = false) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int grid = persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads);
     RegionArgs a = a0;
+    if (cone && cone_cap_r() > 0 && !a.presence_only) a.cone_cap = cone_cap_r();
+    const int grid = persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads);
     void* cb = nullptr;
-    if (cone && cone_cap_r() > 0 && !a.presence_only) {
-        a.cone_cap = cone_cap_r();
+    if (a.cone_cap > 0) {
         cb = region_scratch_alloc(static_cast<size_t>(grid) * (threads / 32) * a.cone_cap * 32);
         a.cone_buf = static_cast<float4*>(cb);
     }

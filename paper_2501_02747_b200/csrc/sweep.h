@@ -527,6 +527,15 @@ __device__ __forceinline__ bool cone_maybe(const float* __restrict__ B, const Co
     return sat_maybe_dil(B, c.g[0], c.R[0]) | sat_maybe_dil(B, c.g[1], c.R[1]) | sat_maybe_dil(B, c.g[2], c.R[2]);
 }
 
+// A warp's cone list: up to cap entries in its slice of a global buffer (L1
+// resident while the warp scans it; a shared-memory head was measured slower:
+// it shrinks the L1 the streamed member boxes live in).
+struct ConeBuf {
+    float4* g;
+    int cap;
+    __device__ __forceinline__ float4* at(int c) const { return g + 2 * c; }
+};
+
 // Collecting sweep of a cone: every face (Morton index, `skip` excluded) whose
 // culling box may meet the cone, written to `out` (global, per warp: entry e =
 // out[2e] {cx, cy, cz, index as int bits}, out[2e + 1] {hx, hy, hz, 0} — the
@@ -534,8 +543,9 @@ __device__ __forceinline__ bool cone_maybe(const float* __restrict__ B, const Co
 // more than `cap` faces qualify or the member boxes are quantised. No exact
 // tests, no early exit. Warp-uniform arguments; all 32 lanes.
 template <int RES = -1>
-__device__ __forceinline__ int coop_collect_cone(const SweepCtx& ctx, const ConeF& cone, int skip, float4* out,
-                                                 int cap, unsigned long long& batches) {
+__device__ __forceinline__ int coop_collect_cone(const SweepCtx& ctx, const ConeF& cone, int skip, ConeBuf out,
+                                                 unsigned long long& batches) {
+    const int cap = out.cap;
     if (use_qbox<RES>(ctx)) return -1;
     constexpr int GPT = kTile / kGroup;
     const int lane = threadIdx.x & 31;
@@ -548,8 +558,9 @@ __device__ __forceinline__ int coop_collect_cone(const SweepCtx& ctx, const Cone
             const float4* B = reinterpret_cast<const float4*>(ctx.mbox + static_cast<size_t>(m) * 8);
             float4 b0 = B[0];
             b0.w = __int_as_float(m);
-            out[2 * at] = b0;
-            out[2 * at + 1] = B[1];
+            float4* e = out.at(at);
+            e[0] = b0;
+            e[1] = B[1];
         }
         cnt += __popc(b);
         return cnt <= cap;

@@ -23,4 +23,6 @@ for arg in sys.argv[1:] or ["5:20:rx", "5:20:tx", "3:200:mix"]:
           f"scan sweeps {o[2]} clear {o[3]}; refine calls {o[6]} iters {o[7]} sweeps {o[4]} clear {o[5]}; "
           f"cycles/sweep scan {o[0]/max(o[2],1):.0f} refine {o[1]/max(o[4],1):.0f}; "
           f"cone lists {o[12]} overflow {o[13]} mean length {o[14]/max(o[12]-o[13],1):.0f} scan iterations {o[15]:.3e}; "
-          f"refine fan build {100*o[16]/tot:.1f}% fans {o[18]} mean T {o[17]/max(o[18],1):.1f}", flush=True)
+          f"refine fan build {100*o[16]/tot:.1f}% fans {o[18]} mean T {o[17]/max(o[18],1):.1f}; "
+          f"scan split: cone build {100*o[19]/tot:.1f}% cone scan {100*o[20]/tot:.1f}% sweeps {100*o[21]/tot:.1f}%; "
+          f"refine steps: sample {100*o[22]/tot:.1f}% whole steps {100*o[23]/tot:.1f}%", flush=True)
