@@ -143,11 +143,15 @@ def point_regions(scene: Scene, src: np.ndarray) -> List[List[dict]]:
 ENTRY_DTYPE = np.dtype([("order", np.int32), ("chain", np.int32, 5), ("plane", np.int32)])
 
 
-def point_tables(scene: Scene, src: np.ndarray, entries: np.ndarray, want_regions: bool = False):
+def point_tables(scene: Scene, src: np.ndarray, entries: np.ndarray, want_regions: bool = False,
+                 packed: bool = False):
     """For every (source k, matrix entry e) of order 1/2: does TableBuilder::reach
     succeed (row of point_vis_table) and is the beam Full in the entry's
     plane — GPU regions + beam cascade in one batched call. Returns
-    (rows[nsrc, nent] bool, full[nsrc, nent] bool, regions or None, stats)."""
+    (rows[nsrc, nent] bool, full[nsrc, nent] bool, regions or None, stats);
+    with packed=True rows / full stay the library's bit rows (uint32
+    [nsrc, ceil(nent / 32)], bit e % 32 of word e // 32) — no host expansion
+    of big tables (config 3: 1.1e9 entries per table)."""
     src = np.ascontiguousarray(np.asarray(src, np.float64).reshape(-1, 3))
     ent = np.ascontiguousarray(entries, ENTRY_DTYPE)
     nsrc, nent = len(src), len(ent)
@@ -158,6 +162,8 @@ def point_tables(scene: Scene, src: np.ndarray, entries: np.ndarray, want_region
     st = _capi.visrt_stats()
     check(lib().visrt_point_tables(scene.h, nsrc, src.reshape(-1), nent, ent.ctypes.data, rows.ctypes.data,
                                    full.ctypes.data, None if regs is None else regs.ctypes.data, C.byref(st), None))
+    if packed:
+        return rows, full, regs, _stats_dict(st)
     unpack = lambda b: np.unpackbits(b.view(np.uint8), axis=1, bitorder="little")[:, :nent].astype(bool)
     return unpack(rows), unpack(full), regs, _stats_dict(st)
 

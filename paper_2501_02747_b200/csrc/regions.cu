@@ -498,12 +498,29 @@ __device__ __noinline__ int k4w_sweep(const DevScene& s, const SweepCtx& ctx, do
     return coop_any_hit<MAXV, 0, RES>(ctx, s.srec, make_segf(s, sx, sy, sz, bx, by, bz), sx, sy, sz, bx, by, bz, sf, -1, sf,
                               sv, tests, batches);
 }
+// One out-of-line copy of the exact predicate for the K4w helpers (i-cache:
+// ncu put 41 % of K4w's warp samples on stall_no_instruction).
+#ifndef VISRT_K4W_SEGNI
+#define VISRT_K4W_SEGNI 1
+#endif
+template <int MAXV>
+__device__ __noinline__ bool k4w_seg(const double* __restrict__ R, double ax, double ay, double az, double bx, double by,
+                                     double bz) {
+    return seg_hits<MAXV>(R, ax, ay, az, bx, by, bz);
+}
+template <int MAXV>
+__device__ __forceinline__ bool k4w_exact(const double* __restrict__ R, double ax, double ay, double az, double bx,
+                                          double by, double bz) {
+    if (VISRT_K4W_SEGNI) return k4w_seg<MAXV>(R, ax, ay, az, bx, by, bz);
+    return seg_hits<MAXV>(R, ax, ay, az, bx, by, bz);
+}
+
 template <int MAXV, int RES>
 __device__ __noinline__ bool k4w_blocked(const DevScene& s, const SweepCtx& ctx, int k, double sx, double sy,
                                          double sz, double qx, double qy, double qz, unsigned long long& tests) {
     if (!member_maybe<RES>(ctx, k, make_segf(s, sx, sy, sz, qx, qy, qz))) return false;
     ++tests;
-    return seg_hits<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
+    return k4w_exact<MAXV>(s.srec + static_cast<size_t>(k) * RecLayout<MAXV>::kStride, sx, sy, sz, qx, qy, qz);
 }
 
 // Development aid (-DVISRT_K4W_PROF): per-phase cycle and sweep counters of K4w.
@@ -810,7 +827,7 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
             bool hit = false;
             if (g < T && ov && !((blocked >> l) & 1u)) {
                 ++tests;
-                hit = seg_hits<MAXV>(s.srec + static_cast<size_t>(fl[jj * kFanCap + g - el]) * STRIDE, sx, sy, sz, ox,
+                hit = k4w_exact<MAXV>(s.srec + static_cast<size_t>(fl[jj * kFanCap + g - el]) * STRIDE, sx, sy, sz, ox,
                                      oy, oz);
             }
             blocked |= __reduce_or_sync(kFull, hit ? 1u << l : 0u);
@@ -953,7 +970,7 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                     // one sample mostly blocks its neighbours)
                     bool blk_any = false;
                     const double* R = s.srec + static_cast<size_t>(__float_as_int(b0.w)) * STRIDE;
-                    while (pending && sat_maybe4(b0, b1, g) && (++tests, seg_hits<MAXV>(R, sx, sy, sz, qx, qy, qz))) {
+                    while (pending && sat_maybe4(b0, b1, g) && (++tests, k4w_exact<MAXV>(R, sx, sy, sz, qx, qy, qz))) {
                         blk_any = true;
                         if (++j == 7) {
                             pending = false;   // every sample blocked: column hidden
@@ -1030,21 +1047,53 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
 #ifndef VISRT_K4W_MINB
 #define VISRT_K4W_MINB 2
 #endif
-#ifndef VISRT_K4W_PSCAN
-#define VISRT_K4W_PSCAN 1   // 1: lane-parallel column scan (scan_cols_warp); 0: 65 serial col_vis calls
-#endif
+// face_param of face f in working plane pl (src/vistable.cpp:84-98): the
+// projected segment a + u d and the (u, s) ring us[]; false = no face_param.
+template <int MAXV>
+__device__ __forceinline__ bool plane_param(const DevScene& s, int f, int nv, int pl, double& ax, double& ay,
+                                            double& dx, double& dy, double* us) {
+    if (!s.seg_ok[3 * f + pl]) return false;
+    const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;
+    ax = sg[0];
+    ay = sg[1];
+    dx = dsub(sg[2], sg[0]);
+    dy = dsub(sg[3], sg[1]);
+    const double len2 = dadd(dmul(dx, dx), dmul(dy, dy));
+    if (len2 <= kEps * kEps) return false;
+#pragma unroll 1
+    for (int q = 0; q < nv; ++q) face_us(s, f, pl, q, ax, ay, dx, dy, len2, us[2 * q], us[2 * q + 1]);
+    return true;
+}
+
+// K4w runs in two kernels so that each one's hot code stays small (ncu put
+// 41 % of the single kernel's warp samples on stall_no_instruction: its
+// 136 KB of code thrashed the instruction caches while warps sat in
+// different phases):
+//   k_point_regions_warp: back-face test + the 65-column scan of every plane
+//     (present / has final; a plane whose 65 columns are all visible gets
+//     sub = [0, 1] at once); planes with interior run boundaries are
+//     DEFERRED: their column masks go to a RefineTask;
+//   k_region_refine: warp per RefineTask — the run boundaries' bisections
+//     (refine_fan over the face's cone list, else per-sightline sweeps) and
+//     the first-largest interval -> sub / clipped of the deferred planes.
+struct RefineTask {
+    long long out;              // region record
+    long long k;                // source
+    int f, planes;              // face, deferred-plane bits
+    unsigned long long vis[3];  // columns 0..63 per plane
+    int vis64;                  // column 64 per plane (bits)
+    int pad;
+};
+
 template <int MAXV, int RES, int NT = kThreads, int MINB = VISRT_K4W_MINB>
 __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
-    constexpr int STRIDE = RecLayout<MAXV>::kStride;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar[1];
     __shared__ unsigned char surv_buf[NT / 32][64];
-    __shared__ int fan_buf[NT / 32][7 * kFanCap];   // per warp: refine_fan candidate lists
     const DevScene& s = a.s;
     const int n = s.n;
     const int lane = threadIdx.x & 31;
     const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
-    int* fan = fan_buf[threadIdx.x >> 5];
     unsigned char* sv = surv_buf[threadIdx.x >> 5];
     ConeBuf cbuf;   // this warp's cone list
     cbuf.cap = a.cone_buf ? a.cone_cap : 0;
@@ -1077,8 +1126,9 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
                                a.presence_of[a.paired ? t : li]);
         const long long tclk0 = K4CLK();
         int8_t present = 1;
-        int8_t has[3] = {0, 0, 0}, clp[3] = {0, 0, 0};
-        double sub[6] = {0, 0, 0, 0, 0, 0};
+        int8_t has[3] = {0, 0, 0};
+        int deferred = 0, dv64 = 0;
+        unsigned long long dvis[3] = {0, 0, 0};
         int coneL = kConeUnbuilt;   // this task's cone list: built at its first clear sample
         // back-face test (src/vistable.cpp:289-294)
         {
@@ -1089,69 +1139,143 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             else if (dist < 0.0) present = 0;
         }
         if (present == 1) K4P(9, 1);
-        for (int pl = 0; pl < 3 && present == 1; ++pl) {
-            if (!s.seg_ok[3 * f + pl]) continue;
-            const double* sg = s.seg + (static_cast<size_t>(f) * 3 + pl) * 6;
-            const double ax = sg[0], ay = sg[1];
-            const double dx = dsub(sg[2], sg[0]), dy = dsub(sg[3], sg[1]);
-            const double len2 = dadd(dmul(dx, dx), dmul(dy, dy));
-            if (len2 <= kEps * kEps) continue;   // no face_param in this plane
-            double us[2 * MAXV];
 #pragma unroll 1
-            for (int q = 0; q < nv; ++q) face_us(s, f, pl, q, ax, ay, dx, dy, len2, us[2 * q], us[2 * q + 1]);
-            // col_vis (src/vistable.cpp:146-159)
-            auto col_vis = [&](double u) -> bool {
-                return col_vis_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, u, sx, sy, sz, sf, sv, cache, tests,
-                                          queries, batches);
-            };
-            if (presence) {   // a visible column <=> a non-empty interval list
-                bool any = false;
-                if (VISRT_K4W_PSCAN) {
-                    bool v64;
-                    any = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, true,
-                                               v64, tests, queries, batches, f, cbuf, coneL) != 0ull ||
-                          v64;
-                } else {
-                    for (int i = 0; i < 65 && !any; ++i) any = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
-                }
-                if (!any) {
-                    present = 0;
-                    break;
-                }
-                has[pl] = 1;
-                continue;
-            }
-            unsigned long long vis = 0;
+        for (int pl = 0; pl < 3 && present == 1; ++pl) {
+            double ax, ay, dx, dy, us[2 * MAXV];
+            if (!plane_param<MAXV>(s, f, nv, pl, ax, ay, dx, dy, us)) continue;
+            // SCAN (src/vistable.cpp:175-176); presence: stop at the first visible column
             bool vis64 = false;
             const long long sclk0 = K4CLK();
-            if (VISRT_K4W_PSCAN) {
-                vis = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf, sv, cache, false, vis64,
-                                           tests, queries, batches, f, cbuf, coneL);
-            } else {
-                for (int i = 0; i < 65; ++i) {
-                    const bool v = col_vis(__ddiv_rn(static_cast<double>(i), 64.0));
-                    if (i < 64) vis |= static_cast<unsigned long long>(v) << i;
-                    else vis64 = v;
-                }
-            }
+            const unsigned long long vis = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf,
+                                                                     sv, cache, presence, vis64, tests, queries,
+                                                                     batches, f, cbuf, coneL);
             K4P(0, K4CLK() - sclk0);
+            if (vis == 0ull && !vis64) {
+                present = 0;   // fully hidden in this plane: no region
+                break;
+            }
+            has[pl] = 1;
+            if (!presence && !(vis == ~0ull && vis64)) {   // interior run boundaries: k_region_refine
+                deferred |= 1 << pl;
+                dvis[pl] = vis;
+                dv64 |= static_cast<int>(vis64) << pl;
+            }
+        }
+        if (present == 1 && !(has[0] | has[1] | has[2])) present = 0;
+        K4P(8, K4CLK() - tclk0);
+        if (present == 1) {
+            K4P(10, K4CLK() - tclk0);
+            K4P(11, 1);
+        }
+        if (lane == 0) {
+            visrt_region r;
+            r.present = present;
+            r.pad = 0;
+            for (int q = 0; q < 3; ++q) {
+                r.has[q] = present == 1 ? has[q] : 0;
+                r.clipped[q] = 0;   // a plane with every column visible: [0, 1], not clipped
+                const bool full = present == 1 && has[q] && !presence && !((deferred >> q) & 1);
+                r.sub[2 * q] = 0.0;
+                r.sub[2 * q + 1] = full ? 1.0 : 0.0;
+            }
+            a.out[rt.out] = r;
+            if (present == 1 && deferred) {
+                const unsigned long long slot = atomicAdd(a.refine_count, 1ull);
+                RefineTask q;
+                q.out = rt.out;
+                q.k = k;
+                q.f = f;
+                q.planes = deferred;
+                q.vis[0] = dvis[0];
+                q.vis[1] = dvis[1];
+                q.vis[2] = dvis[2];
+                q.vis64 = dv64;
+                q.pad = 0;
+                reinterpret_cast<RefineTask*>(a.refine_tasks)[slot] = q;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        tests += __shfl_down_sync(kFull, tests, o);
+        queries += __shfl_down_sync(kFull, queries, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&a.counter[1], tests);
+        atomicAdd(&a.counter[2], queries);
+    }
+#ifdef VISRT_K4W_PROF
+    __syncthreads();
+    if (threadIdx.x < 24) atomicAdd(&g_k4w_prof[threadIdx.x], k4w_sprof[threadIdx.x]);
+#endif
+}
+
+// The deferred planes of k_point_regions_warp: refine every interior run
+// boundary (src/vistable.cpp:163-172) and take the first largest interval
+// (175-192), warp per RefineTask.
+template <int MAXV, int RES, int NT = kThreads, int MINB = VISRT_K4W_MINB>
+__global__ void __launch_bounds__(NT, MINB) k_region_refine(RegionArgs a) {
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar[1];
+    __shared__ unsigned char surv_buf[NT / 32][64];
+    __shared__ int fan_buf[NT / 32][7 * kFanCap];   // per warp: refine_fan candidate lists
+    const DevScene& s = a.s;
+    const int lane = threadIdx.x & 31;
+    const SweepCtx ctx = sweep_setup<RES>(s, smem, bar);
+    int* fan = fan_buf[threadIdx.x >> 5];
+    unsigned char* sv = surv_buf[threadIdx.x >> 5];
+    ConeBuf cbuf;
+    cbuf.cap = a.cone_buf ? a.cone_cap : 0;
+    cbuf.g = a.cone_buf ? a.cone_buf + static_cast<size_t>((blockIdx.x * NT + threadIdx.x) >> 5) * 2 * a.cone_cap
+                        : nullptr;
+    unsigned long long tests = 0, queries = 0, batches = 0;
+    WCache cache;
+#ifdef VISRT_K4W_PROF
+    if (threadIdx.x < 24) k4w_sprof[threadIdx.x] = 0;
+    __syncthreads();
+#endif
+    const long long ntask = static_cast<long long>(*a.refine_count);
+    const RefineTask* tasks = reinterpret_cast<const RefineTask*>(a.refine_tasks);
+    for (;;) {
+        unsigned long long tw = 0;
+        if (lane == 0) tw = atomicAdd(a.refine_count + 1, 1ull);
+        const long long qi = static_cast<long long>(__shfl_sync(kFull, tw, 0));
+        if (qi >= ntask) break;
+        const RefineTask q = tasks[qi];
+        const int f = q.f;
+        const int sf = s.inv[f];
+        const int nv = s.nv[f];
+        const double sx = a.src[3 * q.k], sy = a.src[3 * q.k + 1], sz = a.src[3 * q.k + 2];
+        int coneL = kConeUnbuilt;
+        if (a.fan && cbuf.cap > 0) coneL = build_cone<MAXV, RES>(s, ctx, f, sx, sy, sz, sf, cbuf, batches);
+        double sub[6];
+        int8_t clp[3];
+#pragma unroll 1
+        for (int pl = 0; pl < 3; ++pl) {
+            if (!((q.planes >> pl) & 1)) continue;
+            double ax, ay, dx, dy, us[2 * MAXV];
+            plane_param<MAXV>(s, f, nv, pl, ax, ay, dx, dy, us);
+            const unsigned long long vis = q.vis[pl];
+            const bool vis64 = (q.vis64 >> pl) & 1;
             auto V = [&](int i) { return i == 64 ? vis64 : ((vis >> i) & 1ull) != 0; };
-            // refine (src/vistable.cpp:163-172)
             auto refine = [&](double lo, double hi, bool lo_vis) {
+                if (a.fan == 2) return lo;   // development aid (VISRT_K4W_FAN=2): time the scan alone, regions WRONG
                 const long long rclk0 = K4CLK();
                 int it = 0;
                 if (VISRT_K4W_FAN && a.fan &&
                     refine_fan<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, lo, hi, lo_vis, sx, sy, sz, sf, fan,
-                                     tests, queries, batches, it, cbuf, coneL)) {
+                                          tests, queries, batches, it, cbuf, coneL)) {
                     K4P(1, K4CLK() - rclk0);
                     K4P(6, 1);
                     K4P(7, it);
                     return dmul(0.5, dadd(lo, hi));
                 }
-                for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
+                for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {   // col_vis per midpoint (per-sightline sweeps)
                     const double mid = dmul(0.5, dadd(lo, hi));
-                    if (col_vis(mid) == lo_vis) lo = mid;
-                    else hi = mid;
+                    if (col_vis_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, mid, sx, sy, sz, sf, sv, cache,
+                                                tests, queries, batches) == lo_vis)
+                        lo = mid;
+                    else
+                        hi = mid;
                 }
                 K4P(1, K4CLK() - rclk0);
                 K4P(6, 1);
@@ -1187,31 +1311,19 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
                 }
                 i = j + 1;
             }
-            if (!have) {
-                present = 0;   // fully hidden in this plane: no region
-                break;
-            }
-            has[pl] = 1;
             sub[2 * pl] = b0;
             sub[2 * pl + 1] = b1;
             clp[pl] = (b0 > 1e-9 || b1 < 1.0 - 1e-9) ? 1 : 0;
         }
-        if (present == 1 && !(has[0] | has[1] | has[2])) present = 0;
-        K4P(8, K4CLK() - tclk0);
-        if (present == 1) {
-            K4P(10, K4CLK() - tclk0);
-            K4P(11, 1);
-        }
         if (lane == 0) {
-            visrt_region r;
-            r.present = present;
-            r.pad = 0;
-            for (int q = 0; q < 3; ++q) {
-                r.has[q] = present == 1 ? has[q] : 0;
-                r.clipped[q] = present == 1 ? clp[q] : 0;
-            }
-            for (int q = 0; q < 6; ++q) r.sub[q] = present == 1 ? sub[q] : 0.0;
-            a.out[rt.out] = r;
+            visrt_region* r = a.out + q.out;
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                if ((q.planes >> pl) & 1) {
+                    r->sub[2 * pl] = sub[2 * pl];
+                    r->sub[2 * pl + 1] = sub[2 * pl + 1];
+                    r->clipped[pl] = clp[pl];
+                }
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -1317,19 +1429,49 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
     a.face_major = warp ? face_major : 0;   // the lane kernel K4 walks source-major
     static const int fan = [] {   // VISRT_K4W_FAN=0: refine by per-sightline sweeps (A/B and tests)
         const char* e = std::getenv("VISRT_K4W_FAN");
-        return e && e[0] == '0' ? 0 : 1;
+        return e && e[0] == '0' ? 0 : (e && e[0] == '2' ? 2 : 1);
     }();
     a.fan = fan;
     if (warp && quant_mode_r() != 0 && a.s.n <= kQuantisedMaxBoxes && (quant_mode_r() == 2 || !res)) {
         int smem_sm = 0;
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
         const size_t qsm = sweep_smem_bytes(a.s.n, a.s.ntiles, kQuantised);
-        if (qsm + (kQThreadsK4 / 32) * 64 + 1024 <= static_cast<size_t>(smem_sm))
-            return launch_r(k_point_regions_warp<MAXV, kQuantised, kQThreadsK4, 1>, qsm, a, device, st, kQThreadsK4);
+        if (qsm + (kQThreadsK4 / 32) * 64 + 1024 <= static_cast<size_t>(smem_sm)) {
+            void* rt = nullptr;
+            if (!a.presence_only) {
+                rt = region_scratch_alloc(64 + static_cast<size_t>(a.ntasks) * sizeof(RefineTask));
+                a.refine_count = static_cast<unsigned long long*>(rt);
+                a.refine_tasks = static_cast<char*>(rt) + 64;
+                cudaError_t e2 = cudaMemsetAsync(rt, 0, 64, st);
+                if (e2 != cudaSuccess) return e2;
+            }
+            cudaError_t e1 =
+                launch_r(k_point_regions_warp<MAXV, kQuantised, kQThreadsK4, 1>, qsm, a, device, st, kQThreadsK4);
+            if (e1 == cudaSuccess && rt)
+                e1 = launch_r(k_region_refine<MAXV, kQuantised, kQThreadsK4, 1>, qsm, a, device, st, kQThreadsK4);
+            if (rt) region_scratch_release(rt, st);
+            return e1;
+        }
     }
-    if (warp)
-        return res ? launch_r(k_point_regions_warp<MAXV, kResident>, smem, a, device, st, kThreads, true)
-                   : launch_r(k_point_regions_warp<MAXV, kStreamed>, smem, a, device, st, kThreads, true);
+    if (warp) {
+        // scan kernel, then the refine kernel over the deferred planes it listed
+        void* rt = nullptr;
+        if (!a.presence_only) {
+            const size_t bytes = 64 + static_cast<size_t>(a.ntasks) * sizeof(RefineTask);
+            rt = region_scratch_alloc(bytes);
+            a.refine_count = static_cast<unsigned long long*>(rt);
+            a.refine_tasks = static_cast<char*>(rt) + 64;
+            cudaError_t e2 = cudaMemsetAsync(rt, 0, 64, st);
+            if (e2 != cudaSuccess) return e2;
+        }
+        cudaError_t e1 = res ? launch_r(k_point_regions_warp<MAXV, kResident>, smem, a, device, st, kThreads, true)
+                             : launch_r(k_point_regions_warp<MAXV, kStreamed>, smem, a, device, st, kThreads, true);
+        if (e1 == cudaSuccess && rt)
+            e1 = res ? launch_r(k_region_refine<MAXV, kResident>, smem, a, device, st, kThreads, true)
+                     : launch_r(k_region_refine<MAXV, kStreamed>, smem, a, device, st, kThreads, true);
+        if (rt) region_scratch_release(rt, st);
+        return e1;
+    }
     return res ? launch_r(k_point_regions<MAXV, true>, smem, a, device, st)
                : launch_r(k_point_regions<MAXV, false>, smem, a, device, st);
 }
