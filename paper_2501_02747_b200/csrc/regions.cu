@@ -764,9 +764,9 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
             const float R = static_cast<float>(0.5 * sqrt(e0 * e0 + e1 * e1 + e2 * e2) * 1.0001 + 1e-6);
             const SegF gj = make_segf(s, sx, sy, sz, c0, c1, c2);
             // the task's cone list holds every face that can block a sightline to
-            // the face: filter it (no hierarchy walk) when it has been built
-            cj = coneL >= 0 ? cone_filter(cbuf, coneL, gj, R, fl + j * kFanCap, kFanCap)
-                            : coop_collect<RES>(ctx, gj, R, sf, fl + j * kFanCap, kFanCap, batches);
+            // the face: filter it (without one — an overflowing cone — the
+            // caller bisects with per-sightline sweeps instead)
+            cj = coneL >= 0 ? cone_filter(cbuf, coneL, gj, R, fl + j * kFanCap, kFanCap) : -1;
             if (cj < 0) return false;
         }
         if (lane == j) my_cnt = cj;
