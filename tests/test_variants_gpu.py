@@ -8,7 +8,10 @@ on FULL matrices / region tables (sha-256 of the whole output):
   * K4w task walk: face-major (default) vs source-major
     (VISRT_K4W_FACEMAJOR=0), and the same three member-box residencies;
   * K4w refinement: fan candidate lists (default) vs one sweep per sightline
-    (VISRT_K4W_FAN=0).
+    (VISRT_K4W_FAN=0);
+  * K4w cone lists (the face's candidate list once it is partly visible,
+    default) vs every sample swept through the hierarchy (VISRT_K4W_CONE=0),
+    and a cone capacity small enough to overflow (VISRT_K4W_CONE=48).
 
 Each variant runs in its own process (the knobs are read once per process).
 """
@@ -81,6 +84,8 @@ REGION_VARIANTS = [
     {"VISRT_QUANT": 0, "VISRT_FORCE_STREAM": 1},
     {"VISRT_K4W_FACEMAJOR": 0},
     {"VISRT_K4W_FACEMAJOR": 0, "VISRT_QUANT": 2},
+    {"VISRT_K4W_CONE": 0},
+    {"VISRT_K4W_CONE": 48},
 ]
 
 

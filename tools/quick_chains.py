@@ -1,5 +1,6 @@
 """Quick order-2 chain timing (development aid)."""
-import sys, time
+import hashlib, sys, time
+import numpy as np
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2501_02747_b200 import scenes
 from paper_2501_02747_b200.core import Scene, chain_triples
@@ -11,4 +12,5 @@ for cfg in [int(a) for a in sys.argv[1:]] or [1, 2, 3]:
         tri, st = chain_triples(sc)
         t1 = time.perf_counter()
         print(f"cfg{cfg} N={wl.scene.nfaces}: admitted pairs {st['pairs']} candidate triples {st['candidates']} "
-              f"feasible {st['admitted']} kernel {st['ms']:.1f} ms wall {1e3*(t1-t0):.0f} ms", flush=True)
+              f"feasible {st['admitted']} kernel {st['ms']:.1f} ms wall {1e3*(t1-t0):.0f} ms "
+              f"sha {hashlib.sha256(np.ascontiguousarray(tri).tobytes()).hexdigest()[:16]}", flush=True)
