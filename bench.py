@@ -252,7 +252,8 @@ def secondary_measurements(stream: int, headline_cfg: int = 4):
                                   "sightlines": st["candidates"], "exact_tests": st["tests_exec"],
                                   "roofline": _hbm_roofline(arr.nbytes + sc.upload_bytes, st["ms"],
                                                             "region records written + scene state read once"),
-                                  "ncu": _committed_kernel_ncu("k4w_config5")}
+                                  "ncu": {"scan": _committed_kernel_ncu("k4w_scan_config5"),
+                                          "refine": _committed_kernel_ncu("k4w_refine_config5")}}
         tri, _ = chain_triples(sc)
         tr = Tracer(sc, 3, triples=tri)
         tr.trace_raw(wl5.tx[:4], wl5.rx[:4])

@@ -227,6 +227,15 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         // in Morton order (srec / sbox); the tree's unfolding reads the records
         // by face index (rec: no inv[] indirection on its dependent chain)
         const auto& rec = hs.maxv <= 4 ? hs.rec4 : hs.rec8;
+        // (first vertex, normal) per face, 48 B dense: the image tree's plane
+        // tests gather it per candidate (one sector pair instead of two lines)
+        std::vector<double> pn(static_cast<size_t>(hs.n) * 6);
+        for (int f = 0; f < hs.n; ++f)
+            for (int d = 0; d < 3; ++d) {
+                pn[6 * static_cast<size_t>(f) + d] = hs.pts[static_cast<size_t>(f) * VISRT_MAX_VERTS * 3 + d];
+                pn[6 * static_cast<size_t>(f) + 3 + d] = hs.normal[3 * static_cast<size_t>(f) + d];
+            }
+        const size_t o_pn = add(pn);
         const size_t o_rec = add(rec), o_samples = add(hs.samples), o_pts = add(hs.pts), o_normal = add(hs.normal),
                      o_seg = add(hs.seg), o_aabb = add(hs.aabb), o_nv = add(hs.nv), o_ns = add(hs.ns),
                      o_orient = add(hs.orient), o_seg_ok = add(hs.seg_ok), o_sbox = add(hs.sbox),
@@ -259,6 +268,7 @@ int visrt_scene_create(const visrt_facets_v1* f, int device, visrt_scene** out) 
         ds.samples = static_cast<const double*>(at(o_samples));
         ds.pts = static_cast<const double*>(at(o_pts));
         ds.normal = static_cast<const double*>(at(o_normal));
+        ds.pn = static_cast<const double*>(at(o_pn));
         ds.seg = static_cast<const double*>(at(o_seg));
         ds.aabb = static_cast<const double*>(at(o_aabb));
         ds.nv = static_cast<const int32_t*>(at(o_nv));

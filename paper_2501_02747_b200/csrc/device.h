@@ -18,6 +18,7 @@ struct DevScene {
     const double* samples = nullptr;
     const double* pts = nullptr;   // padded rings [n][8][3]
     const double* normal = nullptr;
+    const double* pn = nullptr;    // [n][6] first vertex + normal (image-tree plane tests)
     const double* seg = nullptr;   // [n][3][6]
     const double* aabb = nullptr;  // [n][6]
     const int32_t* nv = nullptr;

@@ -1180,7 +1180,13 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             }
             a.out[rt.out] = r;
             if (present == 1 && deferred) {
-                const unsigned long long slot = atomicAdd(a.refine_count, 1ull);
+                // tasks whose cone list overflowed refine by per-sightline sweeps
+                // (~30x dearer): listed from the END of the buffer so the refine
+                // kernel starts them first (no long tail behind cheap tasks)
+                const bool heavy = coneL == -1;
+                const unsigned long long slot =
+                    heavy ? static_cast<unsigned long long>(a.ntasks) - 1ull - atomicAdd(a.refine_count + 2, 1ull)
+                          : atomicAdd(a.refine_count, 1ull);
                 RefineTask q;
                 q.out = rt.out;
                 q.k = k;
@@ -1233,14 +1239,15 @@ __global__ void __launch_bounds__(NT, MINB) k_region_refine(RegionArgs a) {
     if (threadIdx.x < 24) k4w_sprof[threadIdx.x] = 0;
     __syncthreads();
 #endif
-    const long long ntask = static_cast<long long>(*a.refine_count);
+    const long long nheavy = static_cast<long long>(a.refine_count[2]);
+    const long long ntask = static_cast<long long>(a.refine_count[0]) + nheavy;
     const RefineTask* tasks = reinterpret_cast<const RefineTask*>(a.refine_tasks);
     for (;;) {
         unsigned long long tw = 0;
         if (lane == 0) tw = atomicAdd(a.refine_count + 1, 1ull);
         const long long qi = static_cast<long long>(__shfl_sync(kFull, tw, 0));
         if (qi >= ntask) break;
-        const RefineTask q = tasks[qi];
+        const RefineTask q = tasks[qi < nheavy ? a.ntasks - 1 - qi : qi - nheavy];   // heavy (buffer end) first
         const int f = q.f;
         const int sf = s.inv[f];
         const int nv = s.nv[f];

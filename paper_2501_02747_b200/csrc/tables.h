@@ -36,7 +36,8 @@ struct RegionArgs {
     int fan = 1;                            // K4w: refine run boundaries with fan candidate lists
     float4* cone_buf = nullptr;             // K4w: per-warp cone lists (cone_cap entries of 2 float4), set by the launcher
     int cone_cap = 0;
-    unsigned long long* refine_count = nullptr;   // K4w: [0] RefineTasks appended, [1] refine kernel cursor (launcher)
+    unsigned long long* refine_count = nullptr;   // K4w: [0] RefineTasks appended at the buffer front, [1] refine
+                                                  // kernel cursor, [2] heavy ones at its end (launcher, zeroed)
     void* refine_tasks = nullptr;                 // K4w: RefineTask[ntasks] (regions.cu), set by the launcher
 };
 

@@ -85,14 +85,13 @@ struct TreeArgs {
 };
 
 __device__ __forceinline__ double sdist_face(const DevScene& s, int f, double x, double y, double z) {
-    const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
-    const double* N = s.normal + 3 * static_cast<size_t>(f);
-    return dot_rel(x, y, z, P[0], P[1], P[2], N[0], N[1], N[2]);
+    const double* P = s.pn + 6 * static_cast<size_t>(f);   // first vertex, then the normal (dense, 48 B)
+    return dot_rel(x, y, z, P[0], P[1], P[2], P[3], P[4], P[5]);
 }
 
 // mirror_point (src/geom.cpp:122-124): p - n * (2 * signed_distance(p))
 __device__ __forceinline__ void mirror_face(const DevScene& s, int f, double& x, double& y, double& z) {
-    const double* N = s.normal + 3 * static_cast<size_t>(f);
+    const double* N = s.pn + 6 * static_cast<size_t>(f) + 3;
     const double d2 = dmul(2.0, sdist_face(s, f, x, y, z));
     x = dsub(x, dmul(N[0], d2));
     y = dsub(y, dmul(N[1], d2));
