@@ -309,7 +309,8 @@ __device__ __forceinline__ double dist3(const double* a, const double* b) {
 // a diffraction edge for the snapshot, Engine::attempt's second sequence
 // (ending at the edge's Fermat point) is unfolded too (383-394).
 template <int MAXV>
-__device__ void unfold_one(const TreeArgs& a, int snap, int d, const int* f, long long t, int kedge) {
+__device__ void unfold_one(const TreeArgs& a, int snap, int d, const int* f, long long t, int kedge,
+                           const double* pimg = nullptr) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const DevScene& s = a.s;
     {
@@ -319,18 +320,48 @@ __device__ void unfold_one(const TreeArgs& a, int snap, int d, const int* f, lon
         img[0][0] = T[0];
         img[0][1] = T[1];
         img[0][2] = T[2];
-        bool fwd = true;
-        for (int k = 0; k < d && fwd; ++k) {
-            if (sdist_face(s, f[k], img[k][0], img[k][1], img[k][2]) <= kEps) {
-                fwd = false;
-                break;
+        // The image chain img[k + 1] = mirror(img[k], f[k]) with the forward
+        // test signed_distance(f[k], img[k]) > kEps. With pimg (the parent's
+        // image = img[d - 1], the same mirror sequence: fused last level, not
+        // brute) every forward test is known to hold — each prefix node and
+        // this child passed it when created (tree_child's prune) — and only
+        // img[d] is formed now; img[1 .. d-1] follow once the first backward
+        // step (the most selective: it ends most sequences) has passed.
+        int have = d;   // img[0 .. have] valid
+        if (pimg) {
+            img[d][0] = pimg[0];
+            img[d][1] = pimg[1];
+            img[d][2] = pimg[2];
+            mirror_face(s, f[d - 1], img[d][0], img[d][1], img[d][2]);
+            have = 0;
+        } else {
+            bool fwd = true;
+            for (int k = 0; k < d && fwd; ++k) {
+                if (sdist_face(s, f[k], img[k][0], img[k][1], img[k][2]) <= kEps) {
+                    fwd = false;
+                    break;
+                }
+                img[k + 1][0] = img[k][0];
+                img[k + 1][1] = img[k][1];
+                img[k + 1][2] = img[k][2];
+                mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
             }
-            img[k + 1][0] = img[k][0];
-            img[k + 1][1] = img[k][1];
-            img[k + 1][2] = img[k][2];
-            mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
+            if (!fwd) return;
         }
-        if (!fwd) return;
+        auto complete_chain = [&]() {   // img[1 .. d-1] (img[d - 1] = the parent image)
+            for (int k = 0; k + 1 < d - 1; ++k) {
+                img[k + 1][0] = img[k][0];
+                img[k + 1][1] = img[k][1];
+                img[k + 1][2] = img[k][2];
+                mirror_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
+            }
+            if (d >= 2) {
+                img[d - 1][0] = pimg[0];
+                img[d - 1][1] = pimg[1];
+                img[d - 1][2] = pimg[2];
+            }
+            have = d;
+        };
         const int edge = a.keyed ? kedge : (a.snap_edge ? a.snap_edge[snap] : -1);
         for (int v = (a.keyed && kedge >= 0) ? 1 : 0; v < (edge >= 0 ? 2 : 1); ++v) {
             bool ok = true;
@@ -346,6 +377,7 @@ __device__ void unfold_one(const TreeArgs& a, int snap, int d, const int* f, lon
             double refl[4][3];
             double cx = target[0], cy = target[1], cz = target[2];
             for (int k = d - 1; k >= 0 && ok; --k) {
+                if (k + 1 < d && have < d) complete_chain();
                 const double da = sdist_face(s, f[k], cx, cy, cz);
                 const double db = sdist_face(s, f[k], img[k + 1][0], img[k + 1][1], img[k + 1][2]);
                 if (dmul(da, db) >= 0.0) {   // segment_plane_crossing, src/geom.cpp:182-189
@@ -442,6 +474,9 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
 #if VISRT_K6L_COMPACT
 __shared__ int k6l_buf[8][64];   // per warp (256 threads): pending children of the current parent
 #endif
+#ifndef VISRT_K6L_LAZY
+#define VISRT_K6L_LAZY 1   // 1: fused last level forms the children's image chains lazily (unfold_one pimg)
+#endif
 #ifndef VISRT_K6L_MINB
 #define VISRT_K6L_MINB 3   // CTAs per SM the fused last level's register budget targets (r01: 1/3/4 -> 3 best, -2 %)
 #endif
@@ -460,6 +495,10 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
         const Pool P = tree_pool(a, par, a.s.n);
         const int fp[4] = {par.f0, par.f1, par.f2, par.f3};
         unsigned long long c_all = 0;
+        // the parent image (= the children's img[d - 1]): lazy image chains
+        // (unfold_one), not for brute_force_trace (no prune: forward tests live)
+        const double pim[3] = {par.ix, par.iy, par.iz};
+        const double* pimg = (VISRT_K6L_LAZY && !a.brute && !a.keyed) ? pim : nullptr;
 #if VISRT_K6L_COMPACT
         // the children that pass the prune are compacted through shared memory
         // and unfolded 32 at a time (full lanes on the heavy unfold)
@@ -471,7 +510,7 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
             if (c >= 0) {
                 int f[4] = {fp[0], fp[1], fp[2], fp[3]};
                 f[P.d] = c;
-                unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1);
+                unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1, pimg);
             }
         };
         for (long long q0 = 0; q0 < P.npool; q0 += 32) {
@@ -501,7 +540,7 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
             if (ok) {
                 int f[4] = {fp[0], fp[1], fp[2], fp[3]};
                 f[P.d] = c;
-                unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1);
+                unfold_one<MAXV>(a, par.snap, P.d + 1, f, -1, -1, pimg);
             }
         }
 #endif
