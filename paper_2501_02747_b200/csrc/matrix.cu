@@ -284,7 +284,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_MORTON
 #define VISRT_K2W_MORTON 0
 #endif
-constexpr int kWC = VISRT_K2W_WC;
+#ifndef VISRT_K2W_WC_TILED
+#define VISRT_K2W_WC_TILED 6   // warp-cache entries of tiled launches (configs 3-5: r01 config 4 822 -> 803 ms)
+#endif
 
 // Development aid (-DVISRT_K2W_PROF): per-phase cycles of K2w (lane 0 of each warp).
 #ifdef VISRT_K2W_PROF
@@ -301,7 +303,7 @@ __device__ unsigned long long g_k2w_prof[16];
 #define K2CLK() 0ll
 #endif
 
-template <int MAXV, int RES, int MINB, int NT = kThreads>
+template <int MAXV, int RES, int MINB, int NT = kThreads, int kWC = VISRT_K2W_WC>
 __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     extern __shared__ __align__(128) float smem[];
@@ -421,6 +423,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
                     unres &= ~(1u << r);
             }
         };
+
         bool clear = false;
         const long long pclk0 = K2CLK();
         if (may_touch(s, pi, pj)) {   // a degenerate sightline is never blocked
@@ -878,9 +881,20 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         // register budget by occupancy: when shared memory already limits the
         // SM to <= 2 CTAs, take the 2-CTA register budget
         const bool two = smem + 1024 > static_cast<size_t>(smem_sm) / 3;
-        if (two)
+        // tiled launches (large all-pairs builds) keep VISRT_K2W_WC_TILED cached
+        // blockers, row grabs VISRT_K2W_WC (a larger cache costs config 2 ~3 %)
+        constexpr int WT = VISRT_K2W_WC_TILED;
+        if (two) {
+            if (a.tiled)
+                return res ? launch_persistent(k_pair_bits_warp<MAXV, true, 2, kThreads, WT>, smem, a, device, st)
+                           : launch_persistent(k_pair_bits_warp<MAXV, false, 2, kThreads, WT>, smem, a, device, st);
             return res ? launch_persistent(k_pair_bits_warp<MAXV, true, 2>, smem, a, device, st)
                        : launch_persistent(k_pair_bits_warp<MAXV, false, 2>, smem, a, device, st);
+        }
+        if (a.tiled)
+            return res ? launch_persistent(k_pair_bits_warp<MAXV, true, VISRT_K2W_MINB, kThreads, WT>, smem, a, device, st)
+                       : launch_persistent(k_pair_bits_warp<MAXV, false, VISRT_K2W_MINB, kThreads, WT>, smem, a, device,
+                                           st);
         return res ? launch_persistent(k_pair_bits_warp<MAXV, true, VISRT_K2W_MINB>, smem, a, device, st)
                    : launch_persistent(k_pair_bits_warp<MAXV, false, VISRT_K2W_MINB>, smem, a, device, st);
     }
