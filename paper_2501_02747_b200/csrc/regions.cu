@@ -1374,8 +1374,14 @@ static int cone_cap_r() {
     }();
     return c;
 }
-void* region_scratch_alloc(size_t bytes);                 // BlockCache (below)
-void region_scratch_release(void* p, cudaStream_t st);    // after the stream's queued work
+// per-launch scratch (cone lists, refine tasks): stream-ordered allocations
+// from the device's default pool (capi.cu pool_setup keeps freed blocks), so
+// no allocation synchronises the device inside a caller's timed region
+static void* region_scratch_alloc(size_t bytes, cudaStream_t st) {
+    void* p = nullptr;
+    return cudaMallocAsync(&p, bytes, st) == cudaSuccess ? p : nullptr;
+}
+static void region_scratch_release(void* p, cudaStream_t st) { cudaFreeAsync(p, st); }
 
 template <class K>
 static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a0, int device, cudaStream_t st,
@@ -1387,7 +1393,8 @@ static cudaError_t launch_r(K fn, size_t smem, const RegionArgs& a0, int device,
     const int grid = persistent_grid_r(reinterpret_cast<const void*>(fn), smem, device, threads);
     void* cb = nullptr;
     if (a.cone_cap > 0) {
-        cb = region_scratch_alloc(static_cast<size_t>(grid) * (threads / 32) * a.cone_cap * 32);
+        cb = region_scratch_alloc(static_cast<size_t>(grid) * (threads / 32) * a.cone_cap * 32, st);
+        if (!cb) return cudaErrorMemoryAllocation;
         a.cone_buf = static_cast<float4*>(cb);
     }
     fn<<<grid, threads, smem, st>>>(a);
@@ -1446,7 +1453,8 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
         if (qsm + (kQThreadsK4 / 32) * 64 + 1024 <= static_cast<size_t>(smem_sm)) {
             void* rt = nullptr;
             if (!a.presence_only) {
-                rt = region_scratch_alloc(64 + static_cast<size_t>(a.ntasks) * sizeof(RefineTask));
+                rt = region_scratch_alloc(64 + static_cast<size_t>(a.ntasks) * sizeof(RefineTask), st);
+                if (!rt) return cudaErrorMemoryAllocation;
                 a.refine_count = static_cast<unsigned long long*>(rt);
                 a.refine_tasks = static_cast<char*>(rt) + 64;
                 cudaError_t e2 = cudaMemsetAsync(rt, 0, 64, st);
@@ -1465,7 +1473,8 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
         void* rt = nullptr;
         if (!a.presence_only) {
             const size_t bytes = 64 + static_cast<size_t>(a.ntasks) * sizeof(RefineTask);
-            rt = region_scratch_alloc(bytes);
+            rt = region_scratch_alloc(bytes, st);
+            if (!rt) return cudaErrorMemoryAllocation;
             a.refine_count = static_cast<unsigned long long*>(rt);
             a.refine_tasks = static_cast<char*>(rt) + 64;
             cudaError_t e2 = cudaMemsetAsync(rt, 0, 64, st);
@@ -1749,17 +1758,6 @@ cudaError_t launch_beam_rows(const BeamArgs& a, cudaStream_t st) {
 // C-ABI entry (include/visrt.h)
 // ---------------------------------------------------------------------------
 #include "capi_internal.h"
-
-namespace visrt {
-void* region_scratch_alloc(size_t bytes) { return BlockCache::get().alloc(bytes); }
-// the block goes back to the cache once the stream has run everything queued so far
-void region_scratch_release(void* p, cudaStream_t st) {
-    if (cudaLaunchHostFunc(st, [](void* q) { BlockCache::get().release(q); }, p) != cudaSuccess) {
-        cudaStreamSynchronize(st);
-        BlockCache::get().release(p);
-    }
-}
-}  // namespace visrt
 
 extern "C" int visrt_point_regions(visrt_scene* sc, int64_t nsrc, const double* src_xyz, visrt_region* out,
                                    visrt_stats* stats, void* stream) {
