@@ -125,7 +125,7 @@ def point_regions_array(scene: Scene, src: np.ndarray, stream: int = 0):
     structured array [nsrc, nfaces] (present: 1 region / 0 none / -1 source on
     the face plane, the reference's VisibilityError) and the call stats."""
     src = np.ascontiguousarray(np.asarray(src, np.float64).reshape(-1, 3))
-    out = np.zeros((len(src), scene.n), REGION_DTYPE)
+    out = np.empty((len(src), scene.n), REGION_DTYPE)   # every record is written by the call
     st = _capi.visrt_stats()
     check(lib().visrt_point_regions(scene.h, len(src), src.reshape(-1),
                                     out.ctypes.data_as(C.POINTER(_capi.visrt_region)), C.byref(st),
@@ -311,7 +311,7 @@ def chain_triples(scene: Scene, admitted_bits: Optional[np.ndarray] = None):
     L = lib()
     check(L.visrt_chain_triples(scene.h, None if bits is None else bits.ctypes.data, None, 0, C.byref(cnt),
                                 C.byref(st), None))
-    out = np.zeros((max(cnt.value, 1), 3), np.int32)
+    out = np.empty((max(cnt.value, 1), 3), np.int32)   # the first cnt rows are written by the call
     check(L.visrt_chain_triples(scene.h, None if bits is None else bits.ctypes.data, out.ctypes.data,
                                 cnt.value, C.byref(cnt), C.byref(st), None))
     return out[: cnt.value], _stats_dict(st)

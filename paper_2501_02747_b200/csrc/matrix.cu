@@ -284,6 +284,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_MORTON
 #define VISRT_K2W_MORTON 0
 #endif
+#ifndef VISRT_K1_ROWS
+#define VISRT_K1_ROWS 1   // 1: K1 as row tiles + sort (k_prefilter_rows) for >= 2^25 pairs; 0: always the cub selection
+#endif
 #ifndef VISRT_K2W_WC_TILED
 #define VISRT_K2W_WC_TILED 6   // warp-cache entries of tiled launches (configs 3-5: r01 config 4 822 -> 803 ms)
 #endif
@@ -918,9 +921,154 @@ cudaError_t launch_pair_detail(const PairArgs& a, int device, cudaStream_t st) {
     return a.s.maxv <= 4 ? launch_detail_t<4>(a, device, st) : launch_detail_t<8>(a, device, st);
 }
 
+// K1 row tiles: the same gate as PrefilterOp with the pair loop reorganised
+// for the GPU — a block takes 8 consecutive reference faces (a warp each) and
+// walks their aim faces j > i in chunks of 32 staged once in shared memory
+// (first vertex + normal, the vertices, orientation, the plane segments'
+// directions): the chunk's face data is read from L2 once per 8 rows instead
+// of once per pair, and no pair index is ever decoded. Survivors are appended
+// with one atomic per warp (the caller sorts them into row-major order).
+constexpr int kK1Rows = 8;
+template <int MAXV>
+struct K1Face {
+    double pn[6];           // first vertex, normal
+    double v[MAXV * 3];     // vertices
+    double sd[3][2];        // plane segment directions (seg[4], seg[5]) per plane
+    int orient, nv, ok[3];
+};
+template <int MAXV>
+__global__ void __launch_bounds__(256) k_prefilter_rows(DevScene s, unsigned long long* out, unsigned long long* count,
+                                                         unsigned long long* cursor) {
+    __shared__ K1Face<MAXV> chunk[32];
+    __shared__ K1Face<MAXV> rowf[kK1Rows];
+    __shared__ long long tile_s;
+    const int n = s.n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ntile = (n + kK1Rows - 1) / kK1Rows;
+    auto load = [&](K1Face<MAXV>& F, int f, int part) {   // part: one of 8 slices of the face, by lane group
+        const double* P = s.pts + static_cast<size_t>(f) * VISRT_MAX_VERTS * 3;
+        if (part == 0) {
+            for (int d = 0; d < 3; ++d) F.pn[d] = P[d];
+            for (int d = 0; d < 3; ++d) F.pn[3 + d] = s.normal[3 * static_cast<size_t>(f) + d];
+            F.orient = s.orient[f];
+            F.nv = s.nv[f];
+        } else if (part == 1) {
+            for (int q = 0; q < MAXV * 3; ++q) F.v[q] = q < s.nv[f] * 3 ? P[q] : 0.0;
+        } else if (part == 2) {
+            for (int pl = 0; pl < 3; ++pl) {
+                F.ok[pl] = s.seg_ok[3 * f + pl];
+                F.sd[pl][0] = s.seg[(static_cast<size_t>(f) * 3 + pl) * 6 + 4];
+                F.sd[pl][1] = s.seg[(static_cast<size_t>(f) * 3 + pl) * 6 + 5];
+            }
+        }
+    };
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) tile_s = static_cast<long long>(atomicAdd(cursor, 1ull));
+        __syncthreads();
+        const long long tile = tile_s;
+        if (tile >= ntile) break;
+        const int i0 = static_cast<int>(tile) * kK1Rows;
+        // the block's 8 reference faces (3 slices each)
+        if (threadIdx.x < kK1Rows * 3) {
+            const int r = threadIdx.x / 3;
+            if (i0 + r < n) load(rowf[r], i0 + r, threadIdx.x % 3);
+        }
+        const int i = i0 + w;
+        for (int j0 = i0 + 1; j0 < n; j0 += 32) {
+            __syncthreads();
+            if (threadIdx.x < 96) {
+                const int c = threadIdx.x / 3;
+                if (j0 + c < n) load(chunk[c], j0 + c, threadIdx.x % 3);
+            }
+            __syncthreads();
+            const int j = j0 + lane;
+            bool keep = false;
+            if (i < n && j < n && j > i) {
+                const K1Face<MAXV>& A = rowf[w];
+                const K1Face<MAXV>& B = chunk[lane];
+                if (A.orient != 2 && B.orient != 2) {
+                    // mutually_front (src/vismatrix.cpp:160-169): a vertex of each strictly in front of the other
+                    bool fij = false, fji = false;
+                    for (int k = 0; k < B.nv && !fij; ++k)
+                        fij = dot_rel(B.v[3 * k], B.v[3 * k + 1], B.v[3 * k + 2], A.pn[0], A.pn[1], A.pn[2], A.pn[3],
+                                      A.pn[4], A.pn[5]) > kEps;
+                    if (fij)
+                        for (int k = 0; k < A.nv && !fji; ++k)
+                            fji = dot_rel(A.v[3 * k], A.v[3 * k + 1], A.v[3 * k + 2], B.pn[0], B.pn[1], B.pn[2],
+                                          B.pn[3], B.pn[4], B.pn[5]) > kEps;
+                    if (fij && fji)
+                        for (int pl = 0; pl < 3 && !keep; ++pl) {   // required_planes (171-181) non-empty
+                            if (!A.ok[pl] || !B.ok[pl]) continue;
+                            const double d = fabs(dadd(dmul(A.sd[pl][0], B.sd[pl][0]), dmul(A.sd[pl][1], B.sd[pl][1])));
+                            keep = d >= 1.0 - 1e-9 || d <= 1e-9;
+                        }
+                }
+            }
+            const unsigned b = __ballot_sync(kFull, keep);
+            if (b) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(count, static_cast<unsigned long long>(__popc(b)));
+                base = __shfl_sync(kFull, base, 0);
+                if (keep) {
+                    const long long row = static_cast<long long>(i) * (2LL * n - i - 1) / 2;   // pairs before row i
+                    out[base + __popc(b & ((1u << lane) - 1u))] = static_cast<unsigned long long>(row + (j - i - 1));
+                }
+            }
+        }
+    }
+}
+
 // Ordered compaction of the prefiltered pairs; returns the device count in *d_count.
 cudaError_t launch_prefilter(const DevScene& s, long long npairs, long long* d_sel, long long* d_count,
                              void*& temp, size_t& temp_bytes, cudaStream_t st) {
+    // row tiles pay off on big scenes (config 4: 10.6 -> 3.7 ms); below ~3e7
+    // pairs the ordered selection is as fast and needs no sort
+    if (VISRT_K1_ROWS && npairs >= (1LL << 25)) {
+        // row tiles -> unordered survivors in d_sel, then a radix sort back into
+        // the row-major (i, j) order PrefilterOp's ordered selection gives
+        cudaError_t e = cudaMemsetAsync(d_count, 0, 2 * sizeof(long long), st);   // [0] count, [1] tile cursor
+        if (e != cudaSuccess) return e;
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_count);
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (s.maxv <= 4) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prefilter_rows<4>, 256, 0);
+            k_prefilter_rows<4><<<sms * std::max(per, 1), 256, 0, st>>>(s, reinterpret_cast<unsigned long long*>(d_sel),
+                                                                      cnt, cnt + 1);
+        } else {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prefilter_rows<8>, 256, 0);
+            k_prefilter_rows<8><<<sms * std::max(per, 1), 256, 0, st>>>(s, reinterpret_cast<unsigned long long*>(d_sel),
+                                                                      cnt, cnt + 1);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        long long m = 0;
+        e = cudaMemcpyAsync(&m, d_count, sizeof(long long), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess || m <= 1) return e;
+        int bits = 1;
+        while (bits < 63 && (1LL << bits) < npairs) ++bits;
+        unsigned long long* keys = reinterpret_cast<unsigned long long*>(d_sel);
+        unsigned long long* sorted = nullptr;
+        e = cudaMallocAsync(&sorted, static_cast<size_t>(m) * sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        size_t need = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, need, keys, sorted, m, 0, bits, st);
+        if (need > temp_bytes) {
+            if (temp) cudaFree(temp);
+            e = cudaMalloc(&temp, need);
+            if (e != cudaSuccess) return e;
+            temp_bytes = need;
+        }
+        e = cub::DeviceRadixSort::SortKeys(temp, temp_bytes, keys, sorted, m, 0, bits, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(keys, sorted, static_cast<size_t>(m) * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToDevice, st);
+        cudaFreeAsync(sorted, st);
+        return e;
+    }
     thrust::counting_iterator<long long> in(0);
     PrefilterOp op{s};
     size_t need = 0;

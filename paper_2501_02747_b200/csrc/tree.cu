@@ -474,6 +474,9 @@ __global__ void __launch_bounds__(256) k_tree_unfold(TreeArgs a) {
 #if VISRT_K6L_COMPACT
 __shared__ int k6l_buf[8][64];   // per warp (256 threads): pending children of the current parent
 #endif
+#ifndef VISRT_K6L_GRAB
+#define VISRT_K6L_GRAB 4   // parents per grab of the fused last level's work cursor
+#endif
 #ifndef VISRT_K6L_LAZY
 #define VISRT_K6L_LAZY 1   // 1: fused last level forms the children's image chains lazily (unfold_one pimg)
 #endif
@@ -485,11 +488,17 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
                                                                    unsigned long long* pcur) {
     const int lane = threadIdx.x & 31;
     const long long nparents = a.in ? a.nin : a.nsnap;
+    long long pnext = 0, pend = 0;
     for (;;) {
-        // parents grabbed dynamically: pool sizes vary widely between parents
-        unsigned long long pw = 0;
-        if (lane == 0) pw = atomicAdd(pcur, 1ull);
-        const long long p = static_cast<long long>(__shfl_sync(kFull, pw, 0));
+        // parents grabbed dynamically (pool sizes vary widely between parents),
+        // VISRT_K6L_GRAB at a time: one global atomic per grab, not per parent
+        if (pnext == pend) {
+            unsigned long long pw = 0;
+            if (lane == 0) pw = atomicAdd(pcur, static_cast<unsigned long long>(VISRT_K6L_GRAB));
+            pnext = static_cast<long long>(__shfl_sync(kFull, pw, 0));
+            pend = min(pnext + VISRT_K6L_GRAB, nparents);
+        }
+        const long long p = pnext++;
         if (p >= nparents) break;
         const TreeNode par = tree_parent(a, p);
         const Pool P = tree_pool(a, par, a.s.n);
