@@ -119,13 +119,20 @@ REGION_DTYPE = np.dtype([("present", np.int8), ("has", np.int8, 3), ("clipped", 
                          ("sub", np.float64, 6)])
 
 
-def point_regions_array(scene: Scene, src: np.ndarray, stream: int = 0):
+def point_regions_array(scene: Scene, src: np.ndarray, stream: int = 0, out: Optional[np.ndarray] = None):
     """illuminated_region(src[k], face f) for every (k, f) — one batched GPU call
     (rt::illuminated_region, include/rt/vistable.hpp:116-117). Returns a
     structured array [nsrc, nfaces] (present: 1 region / 0 none / -1 source on
     the face plane, the reference's VisibilityError) and the call stats."""
     src = np.ascontiguousarray(np.asarray(src, np.float64).reshape(-1, 3))
-    out = np.empty((len(src), scene.n), REGION_DTYPE)   # every record is written by the call
+    # every record is written by the call; `out` (C-contiguous REGION_DTYPE,
+    # >= len(src) * n records) lets batch loops reuse one resident buffer
+    if out is None:
+        out = np.empty((len(src), scene.n), REGION_DTYPE)
+    else:
+        if out.dtype != REGION_DTYPE or not out.flags.c_contiguous or out.size < len(src) * scene.n:
+            raise ValueError("out must be a C-contiguous REGION_DTYPE array of at least len(src) * n records")
+        out = out.reshape(-1)[: len(src) * scene.n].reshape(len(src), scene.n)
     st = _capi.visrt_stats()
     check(lib().visrt_point_regions(scene.h, len(src), src.reshape(-1),
                                     out.ctypes.data_as(C.POINTER(_capi.visrt_region)), C.byref(st),

@@ -1047,6 +1047,9 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
 #ifndef VISRT_K4W_MINB
 #define VISRT_K4W_MINB 2
 #endif
+#ifndef VISRT_K4R_MINB
+#define VISRT_K4R_MINB 2   // CTAs per SM the refine kernel's register budget targets
+#endif
 // face_param of face f in working plane pl (src/vistable.cpp:84-98): the
 // projected segment a + u d and the (u, s) ring us[]; false = no face_param.
 template <int MAXV>
@@ -1483,8 +1486,10 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
         cudaError_t e1 = res ? launch_r(k_point_regions_warp<MAXV, kResident>, smem, a, device, st, kThreads, true)
                              : launch_r(k_point_regions_warp<MAXV, kStreamed>, smem, a, device, st, kThreads, true);
         if (e1 == cudaSuccess && rt)
-            e1 = res ? launch_r(k_region_refine<MAXV, kResident>, smem, a, device, st, kThreads, true)
-                     : launch_r(k_region_refine<MAXV, kStreamed>, smem, a, device, st, kThreads, true);
+            e1 = res ? launch_r(k_region_refine<MAXV, kResident, kThreads, VISRT_K4R_MINB>, smem, a, device, st, kThreads,
+                                true)
+                     : launch_r(k_region_refine<MAXV, kStreamed, kThreads, VISRT_K4R_MINB>, smem, a, device, st, kThreads,
+                                true);
         if (rt) region_scratch_release(rt, st);
         return e1;
     }

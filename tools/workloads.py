@@ -89,8 +89,9 @@ def regions(sc: Scene, src: np.ndarray, batch: int, out: dict, key: str):
     point_regions_array(sc, src[:2])
     s = Stage()
     present = 0
+    buf = np.empty(min(batch, len(src)) * sc.n, REGION_DTYPE)   # one resident host buffer for every batch
     for b in range(0, len(src), batch):
-        arr, st = point_regions_array(sc, src[b:b + batch])
+        arr, st = point_regions_array(sc, src[b:b + batch], out=buf)
         # present / has / clipped bytes + an xor of the sub bit patterns (cheap on 1e8+ regions)
         s.add(st["ms"], arr.view(np.uint8).reshape(-1, arr.dtype.itemsize)[:, :8],
               np.bitwise_xor.reduce(arr["sub"].reshape(-1).view(np.uint64)))
