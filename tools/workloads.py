@@ -23,7 +23,7 @@ import numpy as np
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2501_02747_b200 import scenes  # noqa: E402
 from paper_2501_02747_b200.core import (ENTRY_DTYPE, Scene, Tracer, chain_triples, point_regions_array,  # noqa: E402
-                                        point_tables, unpack_bits)
+                                        REGION_DTYPE, point_tables, unpack_bits)
 
 
 def order1_entries(sc: Scene, bits: np.ndarray) -> np.ndarray:
