@@ -17,6 +17,19 @@
 
 namespace visrt {
 
+#ifndef VISRT_K7_MINB
+#define VISRT_K7_MINB 5   // CTAs of 128 threads per SM the chain kernel's register budget targets (96 registers)
+#endif
+
+#ifdef VISRT_K7_STATS
+// development aid: triples reaching each stage of triple_feasible (total, clip a,
+// clip c, section non-empty sum of ns, hull non-empty, overlap, feasible)
+__device__ unsigned long long g_k7_stats[8];
+#define K7S(i, v) atomicAdd(&g_k7_stats[i], static_cast<unsigned long long>(v))
+#else
+#define K7S(i, v) ((void)0)
+#endif
+
 namespace {
 
 constexpr unsigned kAll = 0xffffffffu;
@@ -152,11 +165,14 @@ __device__ __noinline__ bool triple_feasible(const DevScene& s, int a, int b, in
     const double* N = s.normal + 3 * static_cast<size_t>(b);
     const PlaneD pl{face_pt(s, b, 0), {N[0], N[1], N[2]}};
     V3 pts[Caps<MAXV>::kPts];
+    K7S(0, 1);
     const int nl = clip_halfspace<MAXV>(s, a, pl, pts);
     if (nl < 2) return false;
+    K7S(1, 1);
     V3 tgt[Caps<MAXV>::kClip];
     const int nt = clip_halfspace<MAXV>(s, c, pl, tgt);
     if (nt < 2) return false;
+    K7S(2, 1);
     int np = nl;
     for (int i = 0; i < nt; ++i) {
         const double d2 = dmul(2.0, pl.sd(tgt[i]));   // mirror_point
@@ -188,11 +204,104 @@ __device__ __noinline__ bool triple_feasible(const DevScene& s, int a, int b, in
         }
     }
     V2 hull[2 * Caps<MAXV>::kSec];
+    K7S(3, ns);
     ns = convex_hull(sec, ns, hull);
     if (ns == 0) return false;
+    K7S(4, 1);
+    K7S(7, ns);
     V2 mid2d[VISRT_MAX_VERTS];
     const int nm = s.nv[b];
     for (int k = 0; k < nm; ++k) mid2d[k] = to2d(face_pt(s, b, k));
+    // convex_polygons_overlap_2d, src/geom.cpp:282-290
+    if (separating_axis(sec, ns, mid2d, nm) || separating_axis(mid2d, nm, sec, ns)) return false;
+    K7S(5, 1);
+    if (!has_finite_edge(sec, ns) && !has_finite_edge(mid2d, nm)) return v2norm(v2sub(sec[0], mid2d[0])) <= kEps;
+    K7S(6, 1);
+    return true;
+}
+
+// The (p, t) part of chain_triple_feasible, the same for every aim c of a
+// prefix pair: the plane of t, p clipped to it, the plane frame and t's
+// polygon in that frame. K7 forms it once per warp (shared memory) instead of
+// once per lane. ok = false: infeasible for every aim (p clips to < 2 points
+// or the frame degenerates), exactly where triple_feasible returns false.
+template <int MAXV>
+struct TriplePre {
+    PlaneD pl;
+    V3 u, v;
+    V3 pa[Caps<MAXV>::kClip];
+    double da[Caps<MAXV>::kClip];
+    V2 mid2d[VISRT_MAX_VERTS];
+    int nl, nm, ok;
+};
+
+template <int MAXV>
+__device__ __noinline__ void triple_pre(const DevScene& s, int a, int b, TriplePre<MAXV>& P) {
+    const double* N = s.normal + 3 * static_cast<size_t>(b);
+    P.pl = PlaneD{face_pt(s, b, 0), {N[0], N[1], N[2]}};
+    P.nl = clip_halfspace<MAXV>(s, a, P.pl, P.pa);
+    P.ok = P.nl >= 2;
+    // PlaneFrame::from_plane, src/geom.cpp:209-217
+    const V3 axis = fabs(P.pl.n.x) < 0.9 ? V3{1, 0, 0} : V3{0, 1, 0};
+    V3 u = v3cross(P.pl.n, axis);
+    const double un = __dsqrt_rn(v3dot(u, u));
+    if (un < kEps) {
+        P.ok = 0;
+        return;
+    }
+    u = {__ddiv_rn(u.x, un), __ddiv_rn(u.y, un), __ddiv_rn(u.z, un)};
+    P.u = u;
+    P.v = v3cross(P.pl.n, u);
+    for (int i = 0; i < P.nl; ++i) P.da[i] = P.pl.sd(P.pa[i]);
+    P.nm = s.nv[b];
+    for (int k = 0; k < P.nm; ++k) {
+        const V3 r = v3sub(face_pt(s, b, k), P.pl.p);
+        P.mid2d[k] = V2{v3dot(r, P.u), v3dot(r, P.v)};
+    }
+}
+
+// triple_feasible(p, t, c) given TriplePre(p, t) with ok set: the same
+// operations in the same order on the same values.
+template <int MAXV>
+__device__ __noinline__ bool triple_feasible_pre(const DevScene& s, const TriplePre<MAXV>& P, int c) {
+    const PlaneD pl = P.pl;
+    V3 pts[Caps<MAXV>::kPts];
+    V3 tgt[Caps<MAXV>::kClip];
+    const int nt = clip_halfspace<MAXV>(s, c, pl, tgt);
+    if (nt < 2) return false;
+    const int nl = P.nl;
+    for (int i = 0; i < nl; ++i) pts[i] = P.pa[i];
+    int np = nl;
+    for (int i = 0; i < nt; ++i) {
+        const double d2 = dmul(2.0, pl.sd(tgt[i]));   // mirror_point
+        pts[np++] = v3sub(tgt[i], v3mul(pl.n, d2));
+    }
+    const V3 u = P.u, v = P.v;
+    auto to2d = [&](V3 p) {
+        const V3 r = v3sub(p, pl.p);
+        return V2{v3dot(r, u), v3dot(r, v)};
+    };
+    // hull_plane_slice, src/geom.cpp:292-307
+    double d[Caps<MAXV>::kPts];
+    for (int i = 0; i < nl; ++i) d[i] = P.da[i];
+    for (int i = nl; i < np; ++i) d[i] = pl.sd(pts[i]);
+    V2 sec[Caps<MAXV>::kSec];
+    int ns = 0;
+    for (int i = 0; i < np; ++i) {
+        if (fabs(d[i]) <= kEps) sec[ns++] = to2d(pts[i]);
+        for (int j = i + 1; j < np; ++j) {
+            if ((d[i] > kEps && d[j] < -kEps) || (d[i] < -kEps && d[j] > kEps)) {
+                const double t = __ddiv_rn(d[i], dsub(d[i], d[j]));
+                sec[ns++] = to2d(v3add(pts[i], v3mul(v3sub(pts[j], pts[i]), t)));
+            }
+        }
+    }
+    V2 hull[2 * Caps<MAXV>::kSec];
+    ns = convex_hull(sec, ns, hull);
+    if (ns == 0) return false;
+    V2 mid2d[VISRT_MAX_VERTS];
+    const int nm = P.nm;
+    for (int k = 0; k < nm; ++k) mid2d[k] = P.mid2d[k];
     // convex_polygons_overlap_2d, src/geom.cpp:282-290
     if (separating_axis(sec, ns, mid2d, nm) || separating_axis(mid2d, nm, sec, ns)) return false;
     if (!has_finite_edge(sec, ns) && !has_finite_edge(mid2d, nm)) return v2norm(v2sub(sec[0], mid2d[0])) <= kEps;
@@ -370,9 +479,11 @@ struct ChainArgs {
 };
 
 template <int MAXV>
-__global__ void __launch_bounds__(128) k_chain_triples(ChainArgs a) {
+__global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_triples(ChainArgs a) {
     const DevScene& s = a.s;
     const int lane = threadIdx.x & 31;
+    __shared__ TriplePre<MAXV> pre_buf[4];   // per warp (128 threads)
+    TriplePre<MAXV>& pre = pre_buf[threadIdx.x >> 5];
     for (;;) {
         unsigned long long r = 0;
         if (lane == 0) r = atomicAdd(a.cursor, 1ull);
@@ -382,13 +493,17 @@ __global__ void __launch_bounds__(128) k_chain_triples(ChainArgs a) {
         const int t = a.idx1[r];
         const int lo = a.off1[t], hi = a.off1[t + 1];
         const int rp_pt = req_planes(s, p, t);
+        __syncwarp();
+        if (lane == 0) triple_pre<MAXV>(s, p, t, pre);   // the prefix pair's part, once
+        __syncwarp();
+        if (!pre.ok) continue;                           // no aim of (p, t) is feasible
         for (int q0 = lo; q0 < hi; q0 += 32) {
             const int q = q0 + lane;
             bool ok = false;
             int c = -1;
             if (q < hi) {
                 c = a.idx1[q];
-                ok = triple_feasible<MAXV>(s, p, t, c);
+                ok = triple_feasible_pre<MAXV>(s, pre, c);
                 if (ok) {
                     const int planes = req_planes(s, t, c) & rp_pt;
                     for (int pl = 0; pl < 3 && ok; ++pl)
@@ -442,6 +557,15 @@ __global__ void k_unpack_triples(const unsigned long long* key, long long m, int
 }  // namespace visrt
 
 using visrt::ck;
+
+#ifdef VISRT_K7_STATS
+extern "C" int visrt_debug_k7_stats(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, visrt::g_k7_stats, sizeof(visrt::g_k7_stats));
+    static const unsigned long long zero[8] = {};
+    return static_cast<int>(cudaMemcpyToSymbol(visrt::g_k7_stats, zero, sizeof(zero)));
+}
+#endif
 
 // Order-2 chains of build_matrix(scene, 2) as (p, t, a) triples, from the
 // admitted matrix (NULL: the scene's device bits of the last PREFILTERED call).
