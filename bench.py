@@ -278,7 +278,7 @@ def secondary_measurements(stream: int, headline_cfg: int = 4):
         sc.pair_visibility("prefiltered", copy_bits=False)
         tri, sch = chain_triples(sc)
         out["chains_config3"] = {"candidate_triples": sch["candidates"], "feasible": sch["admitted"],
-                                 "ms": sch["ms"]}
+                                 "ms": sch["ms"], "ncu": _committed_kernel_ncu("k7_config3")}
         tr = Tracer(sc, 3, triples=tri)
         tr.trace_raw(wl.tx[:4], wl.rx[:4])
         _, _, nodes, tst = tr.trace_raw(wl.tx[:50], wl.rx[:50])
