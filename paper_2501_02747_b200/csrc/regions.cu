@@ -779,15 +779,32 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
     T = __shfl_sync(kFull, T, 0);
     K4P(17, T);
     K4P(18, 1);
-    // Lane l < 7 evaluates sample jl = (l + rot) mod 7: the sample found clear
-    // by the previous step leads (neighbouring midpoints mostly share the
-    // verdict), and the step stops as soon as its verdict is known — a valid
-    // sample whose pairs are all tested without a hit (visible), or every
-    // valid sample blocked (hidden).
-    int rot = 0, jl = lane, cl = my_cnt, excl = 0;
+    // Each step deals its (sample, fan entry) pairs 32 per round in a rotated
+    // sample order — the sample found clear by the previous step leads
+    // (neighbouring midpoints mostly share the verdict). A lane's pair in
+    // rounds 0 and 1 is fixed for a given order (precomputed), every lane forms
+    // its own sample's end point from the step's column span (uniform), and the
+    // verdict is kept as per-SAMPLE bit masks: the step stops as soon as a
+    // sample has been tested against its whole fan without a hit (visible) or
+    // every sample is blocked (hidden) — the same verdict as testing all pairs.
+    int rot = 0, jl = 0, cl = 0, excl = 0;   // lane l < 7: sample jl of the order, its fan size, prefix
+    int pj0 = -1, pe0 = 0, pj1 = -1, pe1 = 0;
+    unsigned done0 = 0, done1 = 0, empty = 0;
+    auto owner = [&](int g, int& j, int& e) {   // all lanes: pair g of the order -> (sample, fan entry)
+        int l = 0;
+#pragma unroll
+        for (int k = 1; k < 7; ++k)
+            if (__shfl_sync(kFull, excl, k) <= g) l = k;
+        j = __shfl_sync(kFull, jl, l);
+        e = g - __shfl_sync(kFull, excl, l);
+        if (g >= T) j = -1;
+    };
+    auto done_by = [&](int r_end) {   // samples whose pairs all lie before pair r_end
+        return __reduce_or_sync(kFull, (lane < 7 && excl + cl <= r_end) ? 1u << jl : 0u);
+    };
     auto order = [&]() {
-        jl = lane < 7 ? (lane + rot >= 7 ? lane + rot - 7 : lane + rot) : lane;
-        cl = __shfl_sync(kFull, my_cnt, jl & 31);
+        jl = lane < 7 ? (lane + rot >= 7 ? lane + rot - 7 : lane + rot) : 0;
+        cl = __shfl_sync(kFull, my_cnt, jl);
         if (lane >= 7) cl = 0;
         excl = cl;
 #pragma unroll
@@ -796,60 +813,67 @@ __device__ __noinline__ bool refine_fan(const DevScene& s, const SweepCtx& ctx, 
             if (lane >= o) excl += v;
         }
         excl -= cl;
+        owner(lane, pj0, pe0);
+        owner(32 + lane, pj1, pe1);
+        done0 = done_by(32);
+        done1 = done_by(64);
+        empty = __reduce_or_sync(kFull, (lane < 7 && cl == 0) ? 1u << jl : 0u);
     };
     order();
     int it = 0;
     for (; it < 50 && dsub(hi, lo) > 1e-15; ++it) {
         const double mid = dmul(0.5, dadd(lo, hi));
-        double qx = 0, qy = 0, qz = 0;
         const long long sc0_ = K4CLK();
         // the step's column span once, its edges on lanes (column_span_warp)
         const double cu = mid < 0.0 ? 0.0 : (1.0 < mid ? 1.0 : mid);   // std::clamp
         double cs0, cs1;
         const bool span = column_span_warp(us, nv, cu, cs0, cs1);
-        const bool valid = lane < 7 && span;
-        if (valid) point_at(cu, cs0, cs1, jl, qx, qy, qz);
         K4P(22, K4CLK() - sc0_);
-        unsigned blocked = 0;   // bit l: lane l's sample is blocked
-        bool vis = __any_sync(kFull, valid && cl == 0);   // an empty fan: clear
-        int clear_lane = vis ? __ffs(__ballot_sync(kFull, valid && cl == 0)) - 1 : -1;
-        for (int r = 0; r < T && !vis; r += 32) {
-            const int g = r + lane;
-            int l = 0;
-#pragma unroll
-            for (int k = 1; k < 7; ++k)
-                if (__shfl_sync(kFull, excl, k) <= g) l = k;
-            const int el = __shfl_sync(kFull, excl, l);
-            const int jj = __shfl_sync(kFull, jl, l);
-            const double ox = __shfl_sync(kFull, qx, l), oy = __shfl_sync(kFull, qy, l),
-                         oz = __shfl_sync(kFull, qz, l);
-            const bool ov = __shfl_sync(kFull, valid, l);
-            bool hit = false;
-            if (g < T && ov && !((blocked >> l) & 1u)) {
-                ++tests;
-                hit = k4w_exact<MAXV>(s.srec + static_cast<size_t>(fl[jj * kFanCap + g - el]) * STRIDE, sx, sy, sz, ox,
-                                     oy, oz);
-            }
-            blocked |= __reduce_or_sync(kFull, hit ? 1u << l : 0u);
-            const bool open = valid && !((blocked >> lane) & 1u);
-            const unsigned done = __ballot_sync(kFull, open && excl + cl <= r + 32);
-            if (done) {   // a sample clear of its whole fan
+        unsigned blocked = 0;   // bit j: sample j is blocked
+        bool vis = false;
+        int clear_s = -1;
+        if (span) {   // no span: no sample, col_vis is false
+            if (empty) {   // a sample with an empty fan is clear
                 vis = true;
-                clear_lane = __ffs(done) - 1;
-            } else if (!__any_sync(kFull, open)) {
-                break;   // every sample blocked
+                clear_s = __ffs(empty) - 1;
+            }
+            for (int r = 0; r < T && !vis; r += 32) {
+                int j, e;
+                if (r == 0) {
+                    j = pj0;
+                    e = pe0;
+                } else if (r == 32) {
+                    j = pj1;
+                    e = pe1;
+                } else {
+                    owner(r + lane, j, e);
+                }
+                bool hit = false;
+                if (j >= 0 && !((blocked >> j) & 1u)) {
+                    double qx, qy, qz;
+                    point_at(cu, cs0, cs1, j, qx, qy, qz);
+                    ++tests;
+                    hit = k4w_exact<MAXV>(s.srec + static_cast<size_t>(fl[j * kFanCap + e]) * STRIDE, sx, sy, sz, qx,
+                                          qy, qz);
+                }
+                blocked |= __reduce_or_sync(kFull, hit ? 1u << j : 0u);
+                const unsigned dm = r == 0 ? done0 : (r == 32 ? done1 : done_by(r + 32));
+                const unsigned clr = dm & ~blocked & 0x7fu;
+                if (clr) {   // a sample clear of its whole fan
+                    vis = true;
+                    clear_s = __ffs(clr) - 1;
+                } else if ((~blocked & 0x7fu) == 0u) {
+                    break;   // every sample blocked
+                }
             }
         }
         K4P(23, K4CLK() - sc0_);
         queries += lane == 0 ? 7 : 0;
         if (vis == lo_vis) lo = mid;
         else hi = mid;
-        if (vis) {
-            const int nr = __shfl_sync(kFull, jl, clear_lane);
-            if (nr != rot) {
-                rot = nr;
-                order();
-            }
+        if (vis && clear_s != rot) {
+            rot = clear_s;
+            order();
         }
     }
     iters = it;
