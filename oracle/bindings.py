@@ -286,6 +286,8 @@ class RefOracle:
             L.vref_matrix_size.restype = C.c_int64
             L.vref_matrix_size.argtypes = [C.c_void_p]
             L.vref_matrix_entry.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(vref_entry)]
+            L.vref_matrix_chains.restype = C.c_int64
+            L.vref_matrix_chains.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, _i32p, C.c_int64]
             L.vref_illuminated_region.argtypes = [C.c_void_p, _f64p, C.c_int32, C.POINTER(vref_region)]
             L.vref_regions_batch.argtypes = [C.c_void_p, C.c_int64, _f64p, _i32p, C.POINTER(vref_region),
                                              C.c_int32]
@@ -422,6 +424,14 @@ class RefOracle:
             raise RuntimeError(self.lib().vref_last_error().decode())
         self._matrices.append(m)
         return m
+
+    def matrix_chains(self, m, order: int) -> np.ndarray:
+        """Chains (face indices) of every entry of one order, [k][order + 1]."""
+        L = self.lib()
+        n = L.vref_matrix_chains(self.h, m, order, np.zeros(1, np.int32), 0)
+        out = np.zeros((max(n, 1), order + 1), np.int32)
+        L.vref_matrix_chains(self.h, m, order, out, n)
+        return out[:n]
 
     def matrix_entries(self, m) -> List[dict]:
         L = self.lib()

@@ -378,6 +378,21 @@ int64_t vref_matrix_size(void* m) {
     return static_cast<int64_t>(static_cast<R::InterVisMatrix*>(m)->entries().size());
 }
 
+// the chains (face indices) of every entry of one order, flat [k][order + 1];
+// out == NULL: count only. Bulk form of vref_matrix_entry for big matrices.
+int64_t vref_matrix_chains(void* h, void* m, int32_t order, int32_t* out, int64_t cap) {
+    const R::Scene& s = static_cast<RefScene*>(h)->scene;
+    int64_t c = 0;
+    for (const R::InterVisEntry& e : static_cast<R::InterVisMatrix*>(m)->entries()) {
+        if (e.order != order) continue;
+        if (out && c < cap)
+            for (size_t q = 0; q < e.relation.chain.size() && q <= static_cast<size_t>(order); ++q)
+                out[c * (order + 1) + static_cast<int64_t>(q)] = s.face(e.relation.chain[q]).index;
+        ++c;
+    }
+    return c;
+}
+
 int32_t vref_matrix_entry(void* h, void* m, int64_t k, vref_entry* out) {
     const R::Scene& s = static_cast<RefScene*>(h)->scene;
     const R::InterVisEntry& e = static_cast<R::InterVisMatrix*>(m)->entries().at(static_cast<size_t>(k));

@@ -92,6 +92,7 @@ void vref_matrix_free(void* m);
 void vref_matrix_set_max_order(void* m, int32_t order);
 int64_t vref_matrix_size(void* m);
 int32_t vref_matrix_entry(void* h, void* m, int64_t k, vref_entry* out);
+int64_t vref_matrix_chains(void* h, void* m, int32_t order, int32_t* out, int64_t cap);
 int32_t vref_occlusion(void* h, int32_t i, int32_t j, int32_t* blockers, int32_t cap, int32_t* nblk);
 int32_t vref_illuminated_region(void* h, const double* src, int32_t face, vref_region* out);
 int64_t vref_point_vis_table(void* h, void* m, const double* src, int32_t max_order, vref_row* rows, int64_t cap);

@@ -34,6 +34,9 @@ Stages (reference functions cited against /root/reference/proj):
              with build_matrix(scene, 2) + set_max_order(3) for 100 seeded
              config-5 snapshots: node counts + every path.
   c3trace    the same for 100 seeded config-3 snapshots.
+  c3chains   every order-2 chain of build_matrix(scene, 2) on config 3
+             (src/vismatrix.cpp:715-797): count, sha256 and a 1/997 sample of
+             the sorted unique (p, t, a) triples.
   c5regions  illuminated_region for 100 seeded config-5 sources (50 Tx +
              50 Rx) x ALL 22,096 faces, in chunks of 4 sources
              (c5regions_<k>.npz): digests + present arrays, records of the
@@ -266,6 +269,22 @@ def stage_trace(cfg: int, k: int):
     print(f"  {len(ks)} snapshots in {time.time() - t:.0f} s, {off[-1]} paths, {nodes.sum()} nodes", flush=True)
 
 
+def stage_chains(cfg: int):
+    """Every order-2 chain (p, t, a) of build_matrix(scene, 2) (src/vismatrix.cpp:
+    715-797): the unique triples sorted lexicographically, kept as their count,
+    a sha256 of the int32 array and every 997th triple (the full set of config 3
+    is ~180 MB)."""
+    wl, r = ref(cfg)
+    t = time.time()
+    m = matrix(cfg, 2)
+    print(f"  build_matrix(scene, 2): {time.time() - t:.0f} s", flush=True)
+    c = r.matrix_chains(m, 2)
+    c = np.unique(c, axis=0).astype(np.int32)
+    save(f"c{cfg}chains", scene_sha=np.array(scene_sha(wl.scene)), count=np.array(len(c)),
+         sha=np.array(hashlib.sha256(np.ascontiguousarray(c).tobytes()).hexdigest()),
+         sample_idx=np.arange(0, len(c), 997, dtype=np.int64), sample=c[::997])
+
+
 STAGES = {
     "c3B": lambda: stage_matrix_B_all(3),
     "c3A": lambda: stage_matrix_A(3),
@@ -277,6 +296,7 @@ STAGES = {
     "c5trace": lambda: stage_trace(5, 100),
     "c3trace": lambda: stage_trace(3, 100),
     "c5regions": lambda: stage_regions(5, 100, chunk=4, records_chunks=1),
+    "c3chains": lambda: stage_chains(3),
 }
 
 
