@@ -99,6 +99,15 @@ int visrt_measure_peaks(int device, double* fp64_ops_per_s, double* fp32_flops_p
 #define VISRT_PAIRS_PREFILTERED 0x2u
 int visrt_pair_visibility(visrt_scene* scene, uint32_t flags, uint64_t* bits_host,
                           visrt_stats* stats, void* stream);
+/* Row block of the (B) matrix: only the pairs (i, j), i < j, with row0 <= i < row1 are
+ * decided (the build_matrix pair loop's outer range, src/vismatrix.cpp:640-675, cut into
+ * blocks). bits is still the full N x ceil(N/64) matrix, zero outside the block's pairs and
+ * symmetric inside, so the blocks of a partition OR (or integer-add: disjoint bits) together
+ * into the full matrix — the strong-scaling shard of one scene over several GPUs
+ * (dist.pair_row_blocks gives blocks of equal pair count). flags must be VISRT_PAIRS_ALL;
+ * stats count the block's pairs and reference tests. */
+int visrt_pair_visibility_rows(visrt_scene* scene, uint32_t flags, int32_t row0, int32_t row1,
+                               uint64_t* bits_host, visrt_stats* stats, void* stream);
 const uint64_t* visrt_matrix_bits_device(const visrt_scene* scene);
 /* Candidate list of the last PREFILTERED call (ordered by (i, j)), with the
  * verdict bit per candidate. Two-call sizing: pass NULL to get the count. */

@@ -26,7 +26,7 @@ _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 EXPORTS = [
     "visrt_last_error", "visrt_version", "visrt_scene_create", "visrt_scene_destroy",
     "visrt_scene_nfaces", "visrt_scene_ingest", "visrt_scene_upload_bytes", "visrt_measure_peaks",
-    "visrt_pair_visibility", "visrt_matrix_bits_device",
+    "visrt_pair_visibility", "visrt_pair_visibility_rows", "visrt_matrix_bits_device",
     "visrt_candidates", "visrt_pair_detail", "visrt_point_regions", "visrt_point_tables", "visrt_segments_clear",
     "visrt_chain_reach", "visrt_trajectory_table", "visrt_mobile_table_rows", "visrt_mobile_table_destroy",
     "visrt_chain_triples", "visrt_tracer_create",
@@ -127,6 +127,8 @@ def lib():
     L.visrt_measure_peaks.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.visrt_pair_visibility.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(visrt_stats),
                                         C.c_void_p]
+    L.visrt_pair_visibility_rows.argtypes = [C.c_void_p, C.c_uint32, C.c_int32, C.c_int32, C.c_void_p,
+                                             C.POINTER(visrt_stats), C.c_void_p]
     L.visrt_matrix_bits_device.restype = C.c_void_p
     L.visrt_matrix_bits_device.argtypes = [C.c_void_p]
     L.visrt_candidates.restype = C.c_int64

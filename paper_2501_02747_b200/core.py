@@ -79,15 +79,23 @@ class Scene:
         return normal.reshape(n, 3), orient, seg.reshape(n, 3, 6), ok.reshape(n, 3)
 
     # -- (1) matrix -------------------------------------------------------------
-    def pair_visibility(self, mode: str = "all", copy_bits: bool = True, stream: int = 0
+    def pair_visibility(self, mode: str = "all", copy_bits: bool = True, stream: int = 0,
+                        rows: Optional[Tuple[int, int]] = None
                         ) -> Tuple[Optional[np.ndarray], Dict[str, float]]:
         """(B) ``mode="all"``: bit(i,j) = occlusion_judgment(F_i, F_j).kind != Occluded for all
-        i<j. (A) ``mode="prefiltered"``: pair_admitted(i, j) of build_matrix(scene, 1)."""
+        i<j. (A) ``mode="prefiltered"``: pair_admitted(i, j) of build_matrix(scene, 1).
+        ``rows=(r0, r1)`` ((B) only): decide the pairs of reference rows r0 <= i < r1 alone; the
+        returned full-size matrix is zero elsewhere, so the blocks of a partition
+        (dist.pair_row_blocks) OR into the whole matrix — one scene sharded over several GPUs."""
         flags = {"all": _capi.VISRT_PAIRS_ALL, "prefiltered": _capi.VISRT_PAIRS_PREFILTERED}[mode]
         bits = np.zeros(self.n * self.words, np.uint64) if copy_bits else None
         st = _capi.visrt_stats()
-        check(lib().visrt_pair_visibility(self.h, flags, None if bits is None else bits.ctypes.data,
-                                          C.byref(st), C.c_void_p(stream) if stream else None))
+        bp = None if bits is None else bits.ctypes.data
+        sp = C.c_void_p(stream) if stream else None
+        if rows is None:
+            check(lib().visrt_pair_visibility(self.h, flags, bp, C.byref(st), sp))
+        else:
+            check(lib().visrt_pair_visibility_rows(self.h, flags, int(rows[0]), int(rows[1]), bp, C.byref(st), sp))
         return (None if bits is None else bits.reshape(self.n, self.words)), _stats_dict(st)
 
     def candidates(self):

@@ -323,8 +323,48 @@ const uint64_t* visrt_matrix_bits_device(const visrt_scene* s) {
     return s ? reinterpret_cast<const uint64_t*>(s->d_bits) : nullptr;
 }
 
+// Pairs (i, j), i < j, of rows [row0, row1) and their S(i,j)(N-2) reference tests.
+static void row_block_work(const visrt::HostScene& hs, int row0, int row1, long long& pairs, double& tests) {
+    const int n = hs.n;
+    pairs = 0;
+    double t = 0.0;
+    // count of faces per (nv, ns) class among j > i, swept from the last row up
+    std::vector<std::pair<std::pair<int, int>, long long>> cls;
+    for (int i = n - 1; i >= row0; --i) {
+        if (i < row1) {
+            for (const auto& c : cls)
+                t += static_cast<double>(visrt::sightline_count(hs.nv[i], hs.ns[i], c.first.first, c.first.second)) *
+                     c.second;
+            pairs += n - 1 - i;
+        }
+        const auto key = std::make_pair(hs.nv[i], hs.ns[i]);
+        auto it = std::find_if(cls.begin(), cls.end(), [&](const auto& c) { return c.first == key; });
+        if (it == cls.end()) cls.push_back({key, 1});
+        else ++it->second;
+    }
+    tests = t * (n - 2);
+}
+
+static int pair_visibility_impl(visrt_scene* sc, uint32_t flags, int32_t row0, int32_t row1, uint64_t* bits_host,
+                                visrt_stats* stats, void* stream);
+
 int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, visrt_stats* stats,
                           void* stream) {
+    return pair_visibility_impl(sc, flags, 0, 0, bits_host, stats, stream);
+}
+
+int visrt_pair_visibility_rows(visrt_scene* sc, uint32_t flags, int32_t row0, int32_t row1, uint64_t* bits_host,
+                               visrt_stats* stats, void* stream) {
+    const int n = sc ? sc->hs.n : 0;
+    if (sc && (row0 < 0 || row1 > n || row0 >= row1))
+        return guarded([&] { throw UsageError("row block must satisfy 0 <= row0 < row1 <= nfaces"); });
+    if (sc && (flags & VISRT_PAIRS_PREFILTERED))
+        return guarded([&] { throw UsageError("row blocks shard the all-pairs (B) matrix only"); });
+    return pair_visibility_impl(sc, flags, row0, row1, bits_host, stats, stream);
+}
+
+static int pair_visibility_impl(visrt_scene* sc, uint32_t flags, int32_t row0, int32_t row1, uint64_t* bits_host,
+                                visrt_stats* stats, void* stream) {
     return guarded([&] {
         if (!sc) throw UsageError("null scene");
         const bool pref = (flags & VISRT_PAIRS_PREFILTERED) != 0;
@@ -354,8 +394,15 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
             a.cbit = sc->d_cbit;
         } else {
             a.npairs = npairs;
+            if (row1) {   // a row block: absolute pair indices [pbegin, npairs)
+                auto before = [n](long long r) { return r * (2LL * n - r - 1) / 2; };   // pairs in rows < r
+                a.row0 = row0;
+                a.row1 = row1;
+                a.pbegin = before(row0);
+                a.npairs = before(row1);
+            }
         }
-        if (a.npairs > 0) ck(visrt::launch_pair_bits(a, sc->device, st), "k_pair_bits");
+        if (a.npairs - a.pbegin > 0) ck(visrt::launch_pair_bits(a, sc->device, st), "k_pair_bits");
         ck(cudaEventRecord(sc->ev1, st), "event");
         unsigned long long counters[4] = {0, 0, 0, 0};
         ck(cudaMemcpyAsync(counters, sc->d_counter, sizeof(counters), cudaMemcpyDeviceToHost, st), "D2H ctr");
@@ -420,6 +467,12 @@ int visrt_pair_visibility(visrt_scene* sc, uint32_t flags, uint64_t* bits_host, 
                 }
                 stats->tests_alg = t * (n - 2);
                 stats->admitted = admitted;
+            } else if (row1) {
+                long long bp = 0;
+                row_block_work(sc->hs, row0, row1, bp, stats->tests_alg);
+                stats->pairs = bp;
+                stats->candidates = bp;
+                stats->admitted = -1;
             } else {
                 stats->tests_alg = tests_alg_all(sc->hs);
                 stats->admitted = -1;

@@ -220,6 +220,11 @@ __device__ __noinline__ bool triple_feasible(const DevScene& s, int a, int b, in
     return true;
 }
 
+#ifndef VISRT_K7_SCREEN
+#define VISRT_K7_SCREEN 1   // 0: kernel 1 passes every candidate on (A/B: the screen must not change the triples)
+#endif
+constexpr int kPreAx = 4;   // axes of t's polygon the screen tests (the first two non-degenerate edges)
+
 // The (p, t) part of chain_triple_feasible, the same for every aim c of a
 // prefix pair: the plane of t, p clipped to it, the plane frame and t's
 // polygon in that frame. K7 forms it once per warp (shared memory) instead of
@@ -232,7 +237,11 @@ struct TriplePre {
     V3 pa[Caps<MAXV>::kClip];
     double da[Caps<MAXV>::kClip];
     V2 mid2d[VISRT_MAX_VERTS];
-    int nl, nm, ok;
+    // the first kPreAx axes separating_axis(mid2d, ., sec, .) tests (edge normal,
+    // edge direction of t's polygon) and t's own extents on them
+    V2 axis[kPreAx];
+    double amin[kPreAx], amax[kPreAx];
+    int nl, nm, ok, nax;
 };
 
 template <int MAXV>
@@ -258,35 +267,42 @@ __device__ __noinline__ void triple_pre(const DevScene& s, int a, int b, TripleP
         const V3 r = v3sub(face_pt(s, b, k), P.pl.p);
         P.mid2d[k] = V2{v3dot(r, P.u), v3dot(r, P.v)};
     }
+    // separating_axis(mid2d, nm, ...)'s axes in its own order and arithmetic
+    // (src/geom.cpp:257-270), with axis_separates' extents of mid2d
+    P.nax = 0;
+    for (int k = 0; k < kPreAx; ++k) P.axis[k] = V2{0.0, 0.0};
+    for (int i = 0; i < P.nm && P.nax + 2 <= kPreAx; ++i) {
+        const V2 e = v2sub(P.mid2d[(i + 1) % P.nm], P.mid2d[i]);
+        const double len = v2norm(e);
+        if (len <= 1e-12) continue;
+        const V2 ax2[2] = {{__ddiv_rn(-e.y, len), __ddiv_rn(e.x, len)}, {__ddiv_rn(e.x, len), __ddiv_rn(e.y, len)}};
+        for (int h = 0; h < 2; ++h) {
+            double lo = 1e300, hi = -1e300;
+            for (int k = 0; k < P.nm; ++k) {
+                const double d = v2dot(P.mid2d[k], ax2[h]);
+                lo = smin(lo, d);
+                hi = smax(hi, d);
+            }
+            P.axis[P.nax] = ax2[h];
+            P.amin[P.nax] = lo;
+            P.amax[P.nax] = hi;
+            ++P.nax;
+        }
+    }
 }
 
-// triple_feasible(p, t, c) given TriplePre(p, t) with ok set: the same
-// operations in the same order on the same values.
+// hull_plane_slice's section points (src/geom.cpp:292-307) in the reference's
+// order, written to sec; returns their count.
 template <int MAXV>
-__device__ __noinline__ bool triple_feasible_pre(const DevScene& s, const TriplePre<MAXV>& P, int c) {
-    const PlaneD pl = P.pl;
-    V3 pts[Caps<MAXV>::kPts];
-    V3 tgt[Caps<MAXV>::kClip];
-    const int nt = clip_halfspace<MAXV>(s, c, pl, tgt);
-    if (nt < 2) return false;
-    const int nl = P.nl;
-    for (int i = 0; i < nl; ++i) pts[i] = P.pa[i];
-    int np = nl;
-    for (int i = 0; i < nt; ++i) {
-        const double d2 = dmul(2.0, pl.sd(tgt[i]));   // mirror_point
-        pts[np++] = v3sub(tgt[i], v3mul(pl.n, d2));
-    }
+__device__ __forceinline__ int section_points(const TriplePre<MAXV>& P, const V3* pts, const double* d, int np,
+                                              V2* sec) {
+    const PlaneD& pl = P.pl;
     const V3 u = P.u, v = P.v;
+    int ns = 0;
     auto to2d = [&](V3 p) {
         const V3 r = v3sub(p, pl.p);
         return V2{v3dot(r, u), v3dot(r, v)};
     };
-    // hull_plane_slice, src/geom.cpp:292-307
-    double d[Caps<MAXV>::kPts];
-    for (int i = 0; i < nl; ++i) d[i] = P.da[i];
-    for (int i = nl; i < np; ++i) d[i] = pl.sd(pts[i]);
-    V2 sec[Caps<MAXV>::kSec];
-    int ns = 0;
     for (int i = 0; i < np; ++i) {
         if (fabs(d[i]) <= kEps) sec[ns++] = to2d(pts[i]);
         for (int j = i + 1; j < np; ++j) {
@@ -296,16 +312,128 @@ __device__ __noinline__ bool triple_feasible_pre(const DevScene& s, const Triple
             }
         }
     }
+    return ns;
+}
+
+// The screen of K7's first kernel: is chain_triple_feasible(p, t, c) false because
+// an axis of t's polygon separates it from the section? The same section points
+// as section_points (each from the same operands in the same operation order; a
+// crossing keeps the lower index as its base point), enumerated through sign
+// masks instead of the np^2 pair loop and reduced to their extents on the prefix
+// pair's axes — nothing is stored. A separating axis of t's polygon over ALL
+// section points separates it from their hull too: the hull's vertices are a
+// subset of the points (sort, tolerance-unique and the monotone chain only drop
+// points), so its extent on an axis lies inside theirs and
+// axis_separates(mid2d, ., hull, ., axis) holds a fortiori, i.e.
+// convex_polygons_overlap_2d is false; an empty section is infeasible as well.
+template <int MAXV>
+__device__ __forceinline__ bool section_separated(const TriplePre<MAXV>& P, const V3* pts, const double* d, int np) {
+    const PlaneD& pl = P.pl;
+    const V3 u = P.u, v = P.v;
+    unsigned pos = 0, neg = 0, zero = 0;
+    for (int i = 0; i < np; ++i) {
+        const double di = d[i];
+        if (fabs(di) <= kEps) zero |= 1u << i;
+        else if (di > kEps) pos |= 1u << i;
+        else if (di < -kEps) neg |= 1u << i;
+    }
+    double emin[kPreAx], emax[kPreAx];
+#pragma unroll
+    for (int k = 0; k < kPreAx; ++k) {
+        emin[k] = 1e300;
+        emax[k] = -1e300;
+    }
+    auto ext = [&](V3 p) {
+        const V3 r = v3sub(p, pl.p);
+        const V2 q{v3dot(r, u), v3dot(r, v)};
+#pragma unroll
+        for (int k = 0; k < kPreAx; ++k) {
+            const double e = v2dot(q, P.axis[k]);
+            emin[k] = smin(emin[k], e);
+            emax[k] = smax(emax[k], e);
+        }
+    };
+    if ((zero | pos | neg) == 0u || (zero == 0u && (pos == 0u || neg == 0u))) return true;   // empty section
+    for (unsigned m = zero; m; m &= m - 1) ext(pts[__ffs(m) - 1]);
+    for (unsigned mi = pos | neg; mi; mi &= mi - 1) {
+        const int i = __ffs(mi) - 1;
+        const V3 pi = pts[i];
+        const double di = d[i];
+        for (unsigned m = (((pos >> i) & 1u) ? neg : pos) & ~((2u << i) - 1u); m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const double t = __ddiv_rn(di, dsub(di, d[j]));
+            ext(v3add(pi, v3mul(v3sub(pts[j], pi), t)));
+        }
+    }
+    bool sep = false;
+#pragma unroll
+    for (int k = 0; k < kPreAx; ++k)
+        if (k < P.nax) sep |= P.amax[k] < dsub(emin[k], kEps) || emax[k] < dsub(P.amin[k], kEps);
+    return sep;
+}
+
+// The aim's part of chain_triple_feasible's point set: c clipped to t's plane and
+// mirrored through it, appended to the prefix pair's clipped polygon (pts, d of
+// np points). Returns np, or 0 when c clips to < 2 points (infeasible).
+template <int MAXV>
+__device__ __forceinline__ int triple_points(const DevScene& s, const TriplePre<MAXV>& P, int c, V3* pts, double* d) {
+    const PlaneD pl = P.pl;
+    V3 tgt[Caps<MAXV>::kClip];
+    const int nt = clip_halfspace<MAXV>(s, c, pl, tgt);
+    if (nt < 2) return 0;
+    const int nl = P.nl;
+    for (int i = 0; i < nl; ++i) {
+        pts[i] = P.pa[i];
+        d[i] = P.da[i];
+    }
+    int np = nl;
+    for (int i = 0; i < nt; ++i) {
+        const double d2 = dmul(2.0, pl.sd(tgt[i]));   // mirror_point
+        pts[np] = v3sub(tgt[i], v3mul(pl.n, d2));
+        d[np] = pl.sd(pts[np]);
+        ++np;
+    }
+    return np;
+}
+
+// triple_feasible(p, t, c) given TriplePre(p, t) with ok set: the same
+// operations in the same order on the same values.
+template <int MAXV>
+__device__ __noinline__ bool triple_feasible_pre(const DevScene& s, const TriplePre<MAXV>& P, int c) {
+    V3 pts[Caps<MAXV>::kPts];
+    double d[Caps<MAXV>::kPts];
+    K7S(0, 1);
+    const int np = triple_points<MAXV>(s, P, c, pts, d);
+    if (np == 0) return false;
+    K7S(2, 1);
+    V2 sec[Caps<MAXV>::kSec];
+    int ns = section_points<MAXV>(P, pts, d, np, sec);
     V2 hull[2 * Caps<MAXV>::kSec];
+    K7S(3, ns);
     ns = convex_hull(sec, ns, hull);
     if (ns == 0) return false;
+    K7S(4, 1);
+    K7S(7, ns);
     V2 mid2d[VISRT_MAX_VERTS];
     const int nm = P.nm;
     for (int k = 0; k < nm; ++k) mid2d[k] = P.mid2d[k];
     // convex_polygons_overlap_2d, src/geom.cpp:282-290
     if (separating_axis(sec, ns, mid2d, nm) || separating_axis(mid2d, nm, sec, ns)) return false;
+    K7S(5, 1);
     if (!has_finite_edge(sec, ns) && !has_finite_edge(mid2d, nm)) return v2norm(v2sub(sec[0], mid2d[0])) <= kEps;
     return true;
+}
+
+// K7's screen for one aim: true = chain_triple_feasible(p, t, c) is certainly
+// false (c clips away, or section_separated); false = undecided, kernel 2 runs
+// the full predicate.
+template <int MAXV>
+__device__ __noinline__ bool triple_screened_out(const DevScene& s, const TriplePre<MAXV>& P, int c) {
+    V3 pts[Caps<MAXV>::kPts];
+    double d[Caps<MAXV>::kPts];
+    const int np = triple_points<MAXV>(s, P, c, pts, d);
+    if (np == 0) return true;
+    return section_separated<MAXV>(P, pts, d, np);
 }
 
 // ---- interval sets, src/vismatrix.cpp:43-97 (<= 4 intervals here) ----
@@ -471,15 +599,28 @@ struct ChainArgs {
     const int32_t* off1;
     const int32_t* idx1;
     const int32_t* pair_p;      // directed admitted pair (p, t) per rank
+    const long long* word_off;  // first survivor word of each prefix pair (ceil(aims / 32) words each)
+    uint32_t* surv;             // kernel 1 -> kernel 2: bit = the aim passed the screen
     long long npairs;
     int32_t* out;               // triples (p, t, a)
     unsigned long long* nout;
     long long cap;
-    unsigned long long* cursor;
+    unsigned long long* cursor; // [0] kernel 1, [1] kernel 2
 };
 
+// K7 runs as two kernels over the same warp-per-prefix-pair walk (a warp takes a
+// directed admitted pair (p, t), lanes take the admitted aims of t):
+//   k_chain_screen  every candidate: clip + mirror + the section's extents on t's
+//                   axes (triple_screened_out) — no section, hull or sort buffers,
+//                   ~1.3k SASS instructions; leaves one survivor bit per aim;
+//   k_chain_decide  survivors only (config 3: 20 % of the candidates), compacted so
+//                   that every lane holds one: the full chain_triple_feasible and
+//                   second_order_check, warp-compacted triples.
+// One kernel doing both kept 95 KB of code live with warps in every phase (ncu:
+// no_instruction the top stall, 6.1 warps per issue) and sized its local-memory
+// frame (sec + hull: 6.5 KB per thread) for candidates that never reach the hull.
 template <int MAXV>
-__global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_triples(ChainArgs a) {
+__global__ void __launch_bounds__(128, 6) k_chain_screen(ChainArgs a) {
     const DevScene& s = a.s;
     const int lane = threadIdx.x & 31;
     __shared__ TriplePre<MAXV> pre_buf[4];   // per warp (128 threads)
@@ -492,16 +633,66 @@ __global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_triples(ChainArgs 
         const int p = a.pair_p[r];
         const int t = a.idx1[r];
         const int lo = a.off1[t], hi = a.off1[t + 1];
-        const int rp_pt = req_planes(s, p, t);
         __syncwarp();
         if (lane == 0) triple_pre<MAXV>(s, p, t, pre);   // the prefix pair's part, once
         __syncwarp();
-        if (!pre.ok) continue;                           // no aim of (p, t) is feasible
-        for (int q0 = lo; q0 < hi; q0 += 32) {
+        if (!pre.ok) continue;                           // no aim of (p, t) is feasible (words stay 0)
+        uint32_t* w = a.surv + a.word_off[r];
+        for (int q0 = lo; q0 < hi; q0 += 32, ++w) {
             const int q = q0 + lane;
+            const bool keep = q < hi && !(VISRT_K7_SCREEN && triple_screened_out<MAXV>(s, pre, a.idx1[q]));
+            const unsigned m = __ballot_sync(kAll, keep);
+            if (lane == 0) *w = m;
+        }
+    }
+}
+
+template <int MAXV>
+__global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_decide(ChainArgs a) {
+    const DevScene& s = a.s;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    __shared__ TriplePre<MAXV> pre_buf[4];   // per warp (128 threads)
+    __shared__ int queue_buf[4][64];         // per warp: survivor positions waiting for a full batch
+    TriplePre<MAXV>& pre = pre_buf[threadIdx.x >> 5];
+    int* queue = queue_buf[threadIdx.x >> 5];
+    for (;;) {
+        unsigned long long r = 0;
+        if (lane == 0) r = atomicAdd(a.cursor + 1, 1ull);
+        r = __shfl_sync(kAll, r, 0);
+        if (static_cast<long long>(r) >= a.npairs) break;
+        const int t = a.idx1[r];
+        const int lo = a.off1[t], hi = a.off1[t + 1];
+        const int nw = (hi - lo + 31) >> 5;
+        const uint32_t* w = a.surv + a.word_off[r];
+        bool any = false;
+        for (int k = lane; k < nw; k += 32) any |= w[k] != 0u;
+        if (!__any_sync(kAll, any)) continue;            // every aim screened out
+        const int p = a.pair_p[r];
+        const int rp_pt = req_planes(s, p, t);
+        __syncwarp();
+        if (lane == 0) triple_pre<MAXV>(s, p, t, pre);
+        __syncwarp();
+        int count = 0;                                   // queued survivors (warp-uniform)
+        for (int k = 0; k < nw || count > 0; ++k) {
+            if (k < nw) {
+                const unsigned m = w[k];
+                if ((m >> lane) & 1u) queue[count + __popc(m & lt)] = lo + 32 * k + lane;
+                count += __popc(m);
+                __syncwarp();
+                if (count < 32 && k + 1 < nw) continue;  // wait for a full batch
+            }
+            // the first min(32, count) queued aims, one per lane
+            const int take = min(count, 32);
+            const int q = lane < take ? queue[lane] : -1;
+            const int rest = lane < count - take ? queue[take + lane] : 0;
+            __syncwarp();
+            if (lane < count - take) queue[lane] = rest;
+            count -= take;
+            __syncwarp();
             bool ok = false;
             int c = -1;
-            if (q < hi) {
+            if (q >= 0) {
                 c = a.idx1[q];
                 ok = triple_feasible_pre<MAXV>(s, pre, c);
                 if (ok) {
@@ -516,7 +707,7 @@ __global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_triples(ChainArgs 
             if (lane == 0) base = atomicAdd(a.nout, static_cast<unsigned long long>(__popc(m)));
             base = __shfl_sync(kAll, base, 0);
             if (ok) {
-                const long long slot = static_cast<long long>(base) + __popc(m & ((1u << lane) - 1u));
+                const long long slot = static_cast<long long>(base) + __popc(m & lt);
                 if (slot < a.cap) {
                     a.out[3 * slot] = p;
                     a.out[3 * slot + 1] = t;
@@ -534,6 +725,15 @@ __global__ void k_triples_feasible(DevScene s, long long n, const int32_t* t, ui
     for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<long long>(gridDim.x) * blockDim.x)
         out[k] = triple_feasible<MAXV>(s, t[3 * k], t[3 * k + 1], t[3 * k + 2]) ? 1 : 0;
+}
+
+__global__ void k_popc_words(const uint32_t* w, long long n, unsigned long long* total) {
+    unsigned long long c = 0;
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<long long>(gridDim.x) * blockDim.x)
+        c += __popc(w[k]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(kAll, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
 __global__ void k_pack_triples(const int32_t* t, long long m, unsigned long long* key) {
@@ -622,8 +822,15 @@ extern "C" int visrt_chain_triples(visrt_scene* sc, const uint64_t* admitted_bit
             }
             off1[p + 1] = static_cast<int32_t>(idx1.size());
         }
-        long long total = 0;
-        for (size_t r = 0; r < idx1.size(); ++r) total += off1[idx1[r] + 1] - off1[idx1[r]];
+        long long total = 0, words32 = 0;
+        std::vector<long long> word_off(idx1.size() + 1, 0);
+        for (size_t r = 0; r < idx1.size(); ++r) {
+            const long long aims = off1[idx1[r] + 1] - off1[idx1[r]];
+            total += aims;
+            word_off[r] = words32;
+            words32 += (aims + 31) / 32;
+        }
+        word_off[idx1.size()] = words32;
         std::vector<void*> tmp;
         visrt::FreeGuard guard{tmp};
         auto up = [&](const std::vector<int32_t>& v) {
@@ -637,27 +844,43 @@ extern "C" int visrt_chain_triples(visrt_scene* sc, const uint64_t* admitted_bit
         a.idx1 = up(idx1);
         a.pair_p = up(pp);
         a.npairs = static_cast<long long>(idx1.size());
-        a.cap = std::max<long long>(total, 1);
-        a.out = visrt::dalloc<int32_t>(static_cast<size_t>(a.cap) * 3, tmp);
-        unsigned long long* ctr = visrt::dalloc<unsigned long long>(2, tmp);
+        {
+            long long* d_wo = visrt::dalloc<long long>(word_off.size(), tmp);
+            ck(cudaMemcpy(d_wo, word_off.data(), word_off.size() * 8, cudaMemcpyHostToDevice), "H2D");
+            a.word_off = d_wo;
+        }
+        a.surv = visrt::dalloc<uint32_t>(static_cast<size_t>(std::max<long long>(words32, 1)), tmp);
+        ck(cudaMemsetAsync(a.surv, 0, static_cast<size_t>(std::max<long long>(words32, 1)) * 4, st), "memset");
+        unsigned long long* ctr = visrt::dalloc<unsigned long long>(4, tmp);
         a.nout = ctr;
         a.cursor = ctr + 1;
-        ck(cudaMemsetAsync(ctr, 0, 16, st), "memset");
+        ck(cudaMemsetAsync(ctr, 0, 32, st), "memset");
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, visrt::scene_device(sc));
+        unsigned long long* d_surv_count = ctr + 3;
+        auto run2 = [&](auto screen, auto decide) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, screen, 128, 0);
+            screen<<<sms * std::max(per, 1), 128, 0, st>>>(a);
+            ck(cudaGetLastError(), "k_chain_screen");
+            // survivors bound the triples: count them, then size the output
+            const long long nw = std::max<long long>(words32, 1);
+            visrt::k_popc_words<<<std::min<long long>((nw + 255) / 256, 148 * 8), 256, 0, st>>>(a.surv, nw, d_surv_count);
+            unsigned long long nsurv = 0;
+            ck(cudaMemcpyAsync(&nsurv, d_surv_count, 8, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            a.cap = std::max<long long>(static_cast<long long>(nsurv), 1);
+            a.out = visrt::dalloc<int32_t>(static_cast<size_t>(a.cap) * 3, tmp);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, decide, 128, 0);
+            decide<<<sms * std::max(per, 1), 128, 0, st>>>(a);
+            ck(cudaGetLastError(), "k_chain_decide");
+        };
         if (a.npairs > 0) {
-            if (ds.maxv <= 4) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, visrt::k_chain_triples<4>, 128, 0);
-                visrt::k_chain_triples<4><<<sms * std::max(per, 1), 128, 0, st>>>(a);
-            } else {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, visrt::k_chain_triples<8>, 128, 0);
-                visrt::k_chain_triples<8><<<sms * std::max(per, 1), 128, 0, st>>>(a);
-            }
-            ck(cudaGetLastError(), "k_chain_triples");
+            if (ds.maxv <= 4) run2(visrt::k_chain_screen<4>, visrt::k_chain_decide<4>);
+            else run2(visrt::k_chain_screen<8>, visrt::k_chain_decide<8>);
         }
         cudaEventRecord(e1, st);
         unsigned long long nout = 0;

@@ -93,6 +93,11 @@ struct PairArgs {
     int32_t tiled;                   // K2w: 1 = grabs are VISRT_K2W_TR x VISRT_K2W_TC tiles (all pairs)
     int32_t stride;                  // K2w profiling aid: decide every stride-th pair only (VISRT_K2_STRIDE, default 1)
     int32_t nocull;                  // K2w: 1 = no fp32 culling, every occluder tested exactly (VISRT_NOCULL)
+    // row block [row0, row1) of the i<j triangle (visrt_pair_visibility_rows; row1 = 0: every row).
+    // The host starts the work cursor at the block's first pair / tile: all-pairs walks
+    // count absolute pair indices in [pbegin, npairs), tiled walks tiles below tile_end.
+    int32_t row0, row1;
+    long long pbegin, tile_end;
 };
 
 // ---------------------------------------------------------------------------
@@ -119,10 +124,43 @@ __device__ unsigned long long g_seg_stats[8];
 #else
 #define SEG_STAT(k) ((void)0)
 #endif
+#ifndef VISRT_SEG_V2
+#define VISRT_SEG_V2 1   // 1: occluder records read as double2 words (LDG.E.128)
+#endif
 template <int MAXV>
 __device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax, double ay,
                                          double az, double bx, double by, double bz) {
     SEG_STAT(0);
+#if VISRT_SEG_V2
+    // the record as 16-B words (records are 16-B multiples on a 256-B aligned
+    // base): 14 LDG.E.128 instead of 27 LDG.E.64 for a quad; an edge's six
+    // doubles start on an odd double, so its first one rides in the previous
+    // stage's last word
+    const double2* __restrict__ V = reinterpret_cast<const double2*>(R);
+    const double2 v0 = V[0], v1 = V[1], v2 = V[2];
+    const double Px = v0.x, Py = v0.y, Pz = v1.x;
+    const double nx = v1.y, ny = v2.x, nz = v2.y;
+    const double da = dot_rel(ax, ay, az, Px, Py, Pz, nx, ny, nz);
+    const double db = dot_rel(bx, by, bz, Px, Py, Pz, nx, ny, nz);
+    if (fabs(da) <= kEps || fabs(db) <= kEps) return SEG_STAT(1), false;
+    if (dmul(da, db) > 0.0) return SEG_STAT(2), false;
+    const double t = __ddiv_rn(da, dsub(da, db));
+    const double px = dadd(ax, dmul(dsub(bx, ax), t));
+    const double py = dadd(ay, dmul(dsub(by, ay), t));
+    const double pz = dadd(az, dmul(dsub(bz, az), t));
+    if (fabs(dot_rel(px, py, pz, Px, Py, Pz, nx, ny, nz)) > kEps) return SEG_STAT(3), false;
+    const double2 v3 = V[3], v4 = V[4];
+    if (dot_rel(px, py, pz, Px, Py, Pz, v3.x, v3.y, v4.x) < -kEps) return SEG_STAT(4), false;
+    double e0 = v4.y;
+#pragma unroll
+    for (int k = 1; k < MAXV; ++k) {
+        const double2 w0 = V[3 * k + 2], w1 = V[3 * k + 3], w2 = V[3 * k + 4];
+        if (dot_rel(px, py, pz, e0, w0.x, w0.y, w1.x, w1.y, w2.x) < -kEps) return SEG_STAT(5), false;
+        e0 = w2.y;
+    }
+    SEG_STAT(6);
+    return true;
+#else
     const double Px = R[0], Py = R[1], Pz = R[2];
     const double nx = R[3], ny = R[4], nz = R[5];
     const double da = dot_rel(ax, ay, az, Px, Py, Pz, nx, ny, nz);
@@ -142,6 +180,7 @@ __device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax
     }
     SEG_STAT(6);
     return true;
+#endif
 }
 
 // Unordered pair index p (i < j, row-major upper triangle) -> (i, j).

@@ -326,7 +326,9 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
     int tI = 0, tJ = 0, tl = 0, tl_end = 0;   // tiled grabs: current tile origin and cursor
     const bool tiled = a.tiled != 0;
     const int ntc = (n + VISRT_K2W_TC - 1) / VISRT_K2W_TC;
-    const long long ntiles_all = static_cast<long long>((n + VISRT_K2W_TR - 1) / VISRT_K2W_TR) * ntc;
+    const long long ntiles_all =
+        a.tile_end ? a.tile_end : static_cast<long long>((n + VISRT_K2W_TR - 1) / VISRT_K2W_TR) * ntc;
+    const int row_end = a.row1 ? a.row1 : n;
     for (;;) {
         long long p = 0;
         int pi = 0, pj = 0;
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
                 const int l = tl++;
                 pi = tI + l / VISRT_K2W_TC;
                 pj = tJ + l % VISRT_K2W_TC;
-                got = pi < n && pj < n && pj > pi;
+                got = pi >= a.row0 && pi < row_end && pj < n && pj > pi;
             }
             if (done) break;
         } else {
@@ -846,7 +848,7 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
     a.nocull = nocull;
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
-    a.stride = a.ci ? 1 : stride;
+    a.stride = (a.ci || a.row1) ? 1 : stride;   // the profiling stride walks whole all-pairs matrices only
     // all-pairs rows share the reference face over long runs; candidate lists are
     // short and sparse, where big grabs only unbalance the tail
     a.chunk = a.ci ? VISRT_K2W_CHUNK_CAND : VISRT_K2W_CHUNK;
@@ -858,14 +860,27 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const long long warps = static_cast<long long>(sms) * 3 * (kThreads / 32);
-        a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(a.chunk, a.npairs / (8 * warps))));
+        const long long work = a.npairs - a.pbegin;   // pairs this launch decides
+        a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(a.chunk, work / (8 * warps))));
         // VISRT_K2W_TILED=0/1 forces the grab shape (tests run the tiled walk on small scenes)
         static const int tiled_env = [] {
             const char* e = std::getenv("VISRT_K2W_TILED");
             return e ? std::atoi(e) : -1;
         }();
-        const bool big = tiled_env >= 0 ? tiled_env == 1 : a.npairs >= 512 * warps;
+        const bool big = tiled_env >= 0 ? tiled_env == 1 : work >= 512 * warps;
         a.tiled = (VISRT_K2W_TR > 1 && !a.ci && a.stride == 1 && big) ? 1 : 0;
+        // the cursor's start value: the block's first tile (tiled) or first pair
+        const int ntc = (a.s.n + VISRT_K2W_TC - 1) / VISRT_K2W_TC;
+        long long start = a.pbegin;
+        if (a.tiled && a.row1) {
+            start = static_cast<long long>(a.row0 / VISRT_K2W_TR) * ntc;
+            a.tile_end = static_cast<long long>((a.row1 + VISRT_K2W_TR - 1) / VISRT_K2W_TR) * ntc;
+        }
+        if (start) {
+            const unsigned long long s0 = static_cast<unsigned long long>(start);
+            cudaError_t e = cudaMemcpyAsync(a.counter, &s0, sizeof(s0), cudaMemcpyHostToDevice, st);   // pageable: staged before return
+            if (e != cudaSuccess) return e;
+        }
     }
     if (a.stride > 1) a.npairs = (a.npairs + a.stride - 1) / a.stride;
     // K2w keeps the member boxes resident only while 3 CTAs still fit per SM:

@@ -61,3 +61,21 @@ def gather_bit_rows(rows, device=None):
     out = [torch.empty_like(rows) for _ in range(dist.get_world_size())]
     dist.all_gather(out, rows)
     return out
+
+
+def merge_bit_blocks(bits, device=None):
+    """The full (B) matrix from the ranks' row blocks (Scene.pair_visibility(rows=...)):
+    every rank holds a full-size uint64 matrix that is zero outside its own pairs, so an
+    integer SUM all-reduce of the words is their OR (disjoint bits never carry) — one
+    collective of N x ceil(N/64) x 8 bytes (config 4: 61 MB) over NVLink. `bits` is a
+    numpy uint64 array; returns the merged array."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return bits
+    t = torch.from_numpy(np.ascontiguousarray(bits).view(np.int64).copy())
+    if device is not None:
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().numpy().view(np.uint64).reshape(bits.shape)

@@ -42,6 +42,18 @@ def _worker(rank, world, port, q):
     ms, units = reduce_step_metrics(10.0 + rank, 1000.0 * (rank + 1))
     rows = torch.full((2, 3), rank, dtype=torch.int64)
     got = gather_bit_rows(rows)
+    # row-block merge: each rank's matrix carries its own (disjoint) bits, top bit included
+    import numpy as np
+    from paper_2501_02747_b200.dist import merge_bit_blocks
+    mine = np.zeros((4, 2), np.uint64)
+    mine[rank, 0] = np.uint64(1) << np.uint64(63 if rank == 0 else 5)
+    mine[3, 1] = np.uint64(0xF0 if rank == 0 else 0x0F)
+    merged = merge_bit_blocks(mine)
+    expect = np.zeros((4, 2), np.uint64)
+    expect[0, 0] = np.uint64(1) << np.uint64(63)
+    expect[1, 0] = np.uint64(1) << np.uint64(5)
+    expect[3, 1] = np.uint64(0xFF)
+    assert (merged == expect).all()
     q.put((rank, ms, units, [int(t[0, 0]) for t in got]))
     dist.barrier()
     dist.destroy_process_group()

@@ -13,6 +13,7 @@ compared bit for bit.
   * config 3 point_vis_table, 50 sources         (src/vistable.cpp:478-521)
   * config 3 trajectory_vis_table, 100 m          (src/vistable.cpp:845-987)
   * config 3 / 5 order-3 traces, 100 snapshots each (src/raytracer.cpp:496-514)
+  * config 3 order-2 chains: all 15,021,972 triples     (src/vismatrix.cpp:715-797)
 """
 import glob
 import hashlib
@@ -109,6 +110,21 @@ def test_config4_matrix_B_seeded_pairs():
     pi, pj = d["pi"], d["pj"]
     np.testing.assert_array_equal(M[pi, pj], d["kinds"] != 2)
     np.testing.assert_array_equal(M[pi, pj], M[pj, pi])
+
+
+def test_config3_chains_all():
+    """Every order-2 chain of build_matrix(scene, 2) on config 3 (src/vismatrix.cpp:715-797):
+    15.0 M (p, t, a) triples, compared by count, sha-256 of the sorted int32 array and a
+    1/997 sample."""
+    d = fixture("c3chains")
+    wl = workload(3, d)
+    with Scene(wl.scene) as sc:
+        bits, _ = sc.pair_visibility("prefiltered")
+        tri, _ = chain_triples(sc, bits)
+    tri = np.ascontiguousarray(tri, np.int32)
+    assert len(tri) == int(d["count"])
+    np.testing.assert_array_equal(tri[d["sample_idx"]], d["sample"])
+    assert hashlib.sha256(tri.tobytes()).hexdigest() == str(d["sha"])
 
 
 def _regions_check(cfg, d, sc):

@@ -77,6 +77,29 @@ def test_matrix_config4_quantised_vs_streamed():
     assert q[:2] == st[:2]
 
 
+ROWS = ("import sys, json, hashlib; import numpy as np; sys.path.insert(0, %r);"
+        "from paper_2501_02747_b200 import scenes;"
+        "from paper_2501_02747_b200.core import Scene;"
+        "from paper_2501_02747_b200.dist import pair_row_blocks;"
+        "sc = Scene(scenes.workload(%d).scene); full, st = sc.pair_visibility('all');"
+        "acc = np.zeros_like(full); pairs = 0; tests = 0.0; overlap = 0\n"
+        "for r0, r1 in pair_row_blocks(sc.n, %d):\n"
+        "    if r1 <= r0: continue\n"
+        "    b, s = sc.pair_visibility('all', rows=(r0, r1)); overlap += int(np.bitwise_count(acc & b).sum());"
+        " acc |= b; pairs += s['pairs']; tests += s['tests_alg']\n"
+        "print(json.dumps([bool((acc == full).all()), overlap, pairs == st['pairs'],"
+        " abs(tests - st['tests_alg']) <= 1e-9 * st['tests_alg']]))")
+
+
+@pytest.mark.parametrize("cfg,world,env", [(1, 3, {}), (2, 4, {}), (2, 5, {"VISRT_K2W_TILED": 1}),
+                                           (3, 2, {}), (3, 7, {"VISRT_K2W_TILED": 0})])
+def test_matrix_row_blocks_or_to_the_full_matrix(cfg, world, env):
+    """visrt_pair_visibility_rows: the row blocks of a partition (the strong-scaling
+    shard of one scene) carry disjoint bits and OR into the full (B) matrix, for the
+    row-grab and the tiled K2w walk; their pair and reference-test counts add up."""
+    assert run(ROWS % (ROOT, cfg, world), **env) == [True, 0, True, True]
+
+
 REGION_VARIANTS = [
     {},
     {"VISRT_K4W_FAN": 0},

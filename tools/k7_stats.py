@@ -12,6 +12,6 @@ for cfg in [int(a) for a in sys.argv[1:]] or [3]:
         tri, st = chain_triples(sc)
         lib().visrt_debug_k7_stats(out)
     o = list(out)
-    print(f"cfg{cfg}: candidates {st['candidates']} feasible-calls {o[0]} clip-a ok {o[1]} clip-c ok {o[2]} "
+    print(f"cfg{cfg}: candidates {st['candidates']} feasible-calls {o[0]} past pre-reject {o[1]} clip-c ok {o[2]} "
           f"mean section {o[3]/max(o[2],1):.1f} hull ok {o[4]} mean hull {o[7]/max(o[4],1):.1f} overlap {o[5]} "
           f"finite {o[6]} triples {len(tri)} ms {st['ms']:.1f}", flush=True)
