@@ -223,6 +223,9 @@ __device__ __noinline__ bool triple_feasible(const DevScene& s, int a, int b, in
 #ifndef VISRT_K7_SCREEN
 #define VISRT_K7_SCREEN 1   // 0: kernel 1 passes every candidate on (A/B: the screen must not change the triples)
 #endif
+#ifndef VISRT_K7_MASKS
+#define VISRT_K7_MASKS 1   // decide kernel: the section's crossing pairs from sign masks (same pairs, same order)
+#endif
 constexpr int kPreAx = 4;   // axes of t's polygon the screen tests (the first two non-degenerate edges)
 
 // The (p, t) part of chain_triple_feasible, the same for every aim c of a
@@ -303,6 +306,30 @@ __device__ __forceinline__ int section_points(const TriplePre<MAXV>& P, const V3
         const V3 r = v3sub(p, pl.p);
         return V2{v3dot(r, u), v3dot(r, v)};
     };
+#if VISRT_K7_MASKS
+    // the same (i, j) pairs in the same order, found through sign masks instead
+    // of np^2 comparisons: point i is on the plane (emitted first) or strictly on
+    // one side, and then crosses with every later point strictly on the other
+    unsigned pos = 0, neg = 0;
+    for (int i = 0; i < np; ++i) {
+        if (d[i] > kEps) pos |= 1u << i;
+        else if (d[i] < -kEps) neg |= 1u << i;
+    }
+    for (int i = 0; i < np; ++i) {
+        const unsigned bi = 1u << i;
+        if (!((pos | neg) & bi)) {
+            if (fabs(d[i]) <= kEps) sec[ns++] = to2d(pts[i]);
+            continue;
+        }
+        const V3 pi = pts[i];
+        const double di = d[i];
+        for (unsigned m = ((pos & bi) ? neg : pos) & ~((bi << 1) - 1u); m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const double t = __ddiv_rn(di, dsub(di, d[j]));
+            sec[ns++] = to2d(v3add(pi, v3mul(v3sub(pts[j], pi), t)));
+        }
+    }
+#else
     for (int i = 0; i < np; ++i) {
         if (fabs(d[i]) <= kEps) sec[ns++] = to2d(pts[i]);
         for (int j = i + 1; j < np; ++j) {
@@ -312,6 +339,7 @@ __device__ __forceinline__ int section_points(const TriplePre<MAXV>& P, const V3
             }
         }
     }
+#endif
     return ns;
 }
 

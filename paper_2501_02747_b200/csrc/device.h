@@ -127,17 +127,11 @@ __device__ unsigned long long g_seg_stats[8];
 #ifndef VISRT_SEG_V2
 #define VISRT_SEG_V2 1   // 1: occluder records read as double2 words (LDG.E.128)
 #endif
+// The predicate on a record whose plane words (P, n: V[0..2]) the caller holds
+// already — a warp-uniform occluder tested on many sightlines loads them once.
 template <int MAXV>
-__device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax, double ay,
-                                         double az, double bx, double by, double bz) {
-    SEG_STAT(0);
-#if VISRT_SEG_V2
-    // the record as 16-B words (records are 16-B multiples on a 256-B aligned
-    // base): 14 LDG.E.128 instead of 27 LDG.E.64 for a quad; an edge's six
-    // doubles start on an odd double, so its first one rides in the previous
-    // stage's last word
-    const double2* __restrict__ V = reinterpret_cast<const double2*>(R);
-    const double2 v0 = V[0], v1 = V[1], v2 = V[2];
+__device__ __forceinline__ bool seg_hits_pn(const double2* __restrict__ V, double2 v0, double2 v1, double2 v2,
+                                            double ax, double ay, double az, double bx, double by, double bz) {
     const double Px = v0.x, Py = v0.y, Pz = v1.x;
     const double nx = v1.y, ny = v2.x, nz = v2.y;
     const double da = dot_rel(ax, ay, az, Px, Py, Pz, nx, ny, nz);
@@ -160,6 +154,19 @@ __device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax
     }
     SEG_STAT(6);
     return true;
+}
+template <int MAXV>
+__device__ __forceinline__ bool seg_hits(const double* __restrict__ R, double ax, double ay,
+                                         double az, double bx, double by, double bz) {
+    SEG_STAT(0);
+#if VISRT_SEG_V2
+    // the record as 16-B words (records are 16-B multiples on a 256-B aligned
+    // base): 14 LDG.E.128 instead of 27 LDG.E.64 for a quad; an edge's six
+    // doubles start on an odd double, so its first one rides in the previous
+    // stage's last word
+    const double2* __restrict__ V = reinterpret_cast<const double2*>(R);
+    const double2 v0 = V[0], v1 = V[1], v2 = V[2];
+    return seg_hits_pn<MAXV>(V, v0, v1, v2, ax, ay, az, bx, by, bz);
 #else
     const double Px = R[0], Py = R[1], Pz = R[2];
     const double nx = R[3], ny = R[4], nz = R[5];

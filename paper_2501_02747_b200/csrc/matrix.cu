@@ -287,6 +287,12 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K1_ROWS
 #define VISRT_K1_ROWS 1   // 1: K1 as row tiles + sort (k_prefilter_rows) for >= 2^25 pairs; 0: always the cub selection
 #endif
+#ifndef VISRT_K2W_PRELOAD
+#define VISRT_K2W_PRELOAD 1   // settling passes load the (warp-uniform) blocker's plane words once per blocker
+#endif
+#ifndef VISRT_K2W_RLOOP
+#define VISRT_K2W_RLOOP 1     // the round's blockers settle through one loop (one inlined resolve site)
+#endif
 #ifndef VISRT_K2W_WC_TILED
 #define VISRT_K2W_WC_TILED 6   // warp-cache entries of tiled launches (configs 3-5: r01 config 4 822 -> 803 ms)
 #endif
@@ -420,12 +426,23 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
         };
         // settle every unresolved sightline blocked by occluder k (Morton index)
         auto resolve = [&](int k) {
+#if VISRT_K2W_PRELOAD && VISRT_SEG_V2
+            // k is warp-uniform: its plane words are loaded once, ahead of the
+            // sightlines' own loads, not once per sightline behind them
+            const double2* V = reinterpret_cast<const double2*>(s.srec + static_cast<size_t>(k) * STRIDE);
+            const double2 v0 = V[0], v1 = V[1], v2 = V[2];
+#endif
             for (unsigned m = unres; m; m &= m - 1) {
                 const int r = __ffs(m) - 1;
                 ends(lane + 32 * r);
-                if ((!VISRT_K2W_RSAT || a.nocull || member_maybe(ctx, k, make_segf(s, ax, ay, az, bx, by, bz))) &&
-                    exact(k))
-                    unres &= ~(1u << r);
+                if (!(!VISRT_K2W_RSAT || a.nocull || member_maybe(ctx, k, make_segf(s, ax, ay, az, bx, by, bz))))
+                    continue;
+#if VISRT_K2W_PRELOAD && VISRT_SEG_V2
+                ++tests;
+                if (seg_hits_pn<MAXV>(V, v0, v1, v2, ax, ay, az, bx, by, bz)) unres &= ~(1u << r);
+#else
+                if (exact(k)) unres &= ~(1u << r);
+#endif
             }
         };
 
@@ -594,10 +611,21 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
             if (lane == L) unres &= ~(1u << r0);   // the swept sightline: its sweep found `hit` blocking it
             if (lane == wc_next) wc = hit;
             wc_next = wc_next + 1 == kWC ? 0 : wc_next + 1;
+#if VISRT_K2W_MULTI && VISRT_K2W_RLOOP
+            // one resolve site for the round's blockers (code size: the predicate
+            // and the sightline set-up are inlined once, not three times)
+            for (int hq = 0; hq < 3; ++hq) {
+                const int hk = hq == 0 ? hit : (hq == 1 ? hit2 : hit3);
+                if (hk < 0) break;   // hit3 is only set after hit2
+                if (hq > 0 && !__any_sync(kFull, unres != 0)) break;
+                resolve(hk);
+            }
+#else
             resolve(hit);
 #if VISRT_K2W_MULTI
             if (hit2 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit2);
             if (hit3 >= 0 && __any_sync(kFull, unres != 0)) resolve(hit3);
+#endif
 #endif
             K2P(6, K2CLK() - rclk0);
         }

@@ -564,57 +564,6 @@ struct WCache {
     }
 };
 
-// Whole-face shadow certificate. true: occluder k (Morton index) blocks the
-// sightline from S to EVERY sample point illuminated_region can take on face f
-// (src/vistable.cpp:146-159: lifted points of f's plane segment, inside f's
-// (u, s) polygon, i.e. within ~1e-8 m of conv(vertices of f) — plane_segment
-// admits faces whose projection is collinear to 1e-9 (|d| + 1) / |d|), so every
-// column of every plane is hidden and the region is absent, exactly what the
-// 65 x 7 per-sample decisions would give. Proof by margins, per vertex V of f
-// (lanes 0..nv-1), in plain FP64 (rounding ~1e-12 of the quantities compared):
-//   * S and V lie strictly on opposite sides of k's plane, |da|, |db| >= 1e-3 m
-//     (the exact predicate's plane checks use kEps = 1e-9);
-//   * |da - db| >= 1e-3 |V - S|: the crossing point moves <= 1e3 x as far as the
-//     far end does, so a 1e-8 m deviation of a sample from conv(f) moves it
-//     <= 1e-5 m (this bound is concave in the far end: it holds on conv(f));
-//   * the crossing point of S -> V lies >= 1e-3 m inside every edge of k the
-//     exact predicate tests. With da - db of one sign over f, "edge distance
-//     >= m" is a linear inequality in the far end, so it holds for every point
-//     of conv(f) once it holds at the vertices.
-// Then segment_face_intersection(S, Q, k) is a hit for every sample Q, with
-// three orders of magnitude between the margins and its tolerances.
-template <int MAXV>
-__device__ __forceinline__ bool face_shadowed(const DevScene& s, int k, int f, int nv, double sx, double sy,
-                                              double sz) {
-    constexpr int STRIDE = RecLayout<MAXV>::kStride;
-    constexpr double kM = 1e-3;
-    const int lane = threadIdx.x & 31;
-    bool ok = true;
-    if (lane < nv) {
-        const double* R = s.srec + static_cast<size_t>(k) * STRIDE;
-        const double* V = s.pts + (static_cast<size_t>(f) * VISRT_MAX_VERTS + lane) * 3;
-        const double vx = V[0], vy = V[1], vz = V[2];
-        const double da = (sx - R[0]) * R[3] + (sy - R[1]) * R[4] + (sz - R[2]) * R[5];
-        const double db = (vx - R[0]) * R[3] + (vy - R[1]) * R[4] + (vz - R[2]) * R[5];
-        const double ex = vx - sx, ey = vy - sy, ez = vz - sz;
-        const double dd = da - db;
-        ok = ((da >= kM && db <= -kM) || (da <= -kM && db >= kM)) &&
-             dd * dd >= 1e-6 * (ex * ex + ey * ey + ez * ez);
-        if (ok) {
-            const double t = da / dd;
-            const double px = sx + ex * t, py = sy + ey * t, pz = sz + ez * t;
-#pragma unroll
-            for (int e = 0; e < MAXV; ++e) {
-                const double* A = e == 0 ? R : R + 9 + (e - 1) * 6;        // edge start (a_0 = P)
-                const double* I = e == 0 ? R + 6 : R + 12 + (e - 1) * 6;   // inward normal
-                const bool skipped = I[0] == 0.0 && I[1] == 0.0 && I[2] == 0.0;   // an edge the predicate skips
-                ok &= skipped || (px - A[0]) * I[0] + (py - A[1]) * I[1] + (pz - A[2]) * I[2] >= kM;
-            }
-        }
-    }
-    return __all_sync(kFull, ok);
-}
-
 #ifndef VISRT_K4W_PCOL
 #define VISRT_K4W_PCOL 1   // 1: col_vis decides its 7 samples on 7 lanes; 0: one sample after the other
 #endif
@@ -978,7 +927,7 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                                                           WCache& cache, bool stop_at_first, bool& vis64,
                                                           unsigned long long& tests, unsigned long long& queries,
                                                           unsigned long long& batches, int f, ConeBuf cbuf,
-                                                          int& coneL, int shadow_tries) {
+                                                          int& coneL) {
     constexpr int STRIDE = RecLayout<MAXV>::kStride;
     const int lane = threadIdx.x & 31;
     unsigned long long vis = 0;
@@ -1104,11 +1053,6 @@ __device__ __noinline__ unsigned long long scan_cols_warp(const DevScene& s, con
                 }
             } else {
                 cache.put(h);
-                // a blocker that shadows the whole face settles every column of every plane
-                if (shadow_tries > 0 && vis == 0ull) {
-                    --shadow_tries;
-                    if (face_shadowed<MAXV>(s, h, f, nv, sx, sy, sz)) return 0ull;
-                }
                 if (lane == L) {   // the sweep proved this sample blocked
                     if (++j == 7) pending = false;
                     else point();
@@ -1222,14 +1166,6 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             else if (dist < 0.0) present = 0;
         }
         if (present == 1) K4P(9, 1);
-        // a cached blocker that shadows the whole face: no column of any plane is
-        // visible, the region is absent (face_shadowed)
-        if (present == 1 && a.shadow) {
-            for (int i = 0; i < VISRT_K4W_WC && present == 1; ++i) {
-                const int kc = cache.entry(i);
-                if (kc >= 0 && kc != sf && face_shadowed<MAXV>(s, kc, f, nv, sx, sy, sz)) present = 0;
-            }
-        }
 #pragma unroll 1
         for (int pl = 0; pl < 3 && present == 1; ++pl) {
             double ax, ay, dx, dy, us[2 * MAXV];
@@ -1239,7 +1175,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_regions_warp(RegionArgs a) {
             const long long sclk0 = K4CLK();
             const unsigned long long vis = scan_cols_warp<MAXV, RES>(s, ctx, us, nv, pl, ax, ay, dx, dy, sx, sy, sz, sf,
                                                                      sv, cache, presence, vis64, tests, queries,
-                                                                     batches, f, cbuf, coneL, a.shadow ? 2 : 0);
+                                                                     batches, f, cbuf, coneL);
             K4P(0, K4CLK() - sclk0);
             if (vis == 0ull && !vis64) {
                 present = 0;   // fully hidden in this plane: no region
@@ -1537,11 +1473,6 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
         return e && e[0] == '0' ? 0 : (e && e[0] == '2' ? 2 : 1);
     }();
     a.fan = fan;
-    static const int shadow = [] {
-        const char* e = std::getenv("VISRT_K4W_SHADOW");
-        return e && e[0] == '0' ? 0 : 1;
-    }();
-    a.shadow = shadow;
     if (warp && quant_mode_r() != 0 && a.s.n <= kQuantisedMaxBoxes && (quant_mode_r() == 2 || !res)) {
         int smem_sm = 0;
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);

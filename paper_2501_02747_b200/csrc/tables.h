@@ -34,7 +34,6 @@ struct RegionArgs {
     int chunk = 1;                          // K4w: consecutive tasks per warp grab (set by the launcher)
     int face_major = 1;                     // walk order of the all-faces / face-list modes (see above)
     int fan = 1;                            // K4w: refine run boundaries with fan candidate lists
-    int shadow = 1;                         // K4w: whole-face shadow certificate (regions.cu face_shadowed; VISRT_K4W_SHADOW=0 off)
     float4* cone_buf = nullptr;             // K4w: per-warp cone lists (cone_cap entries of 2 float4), set by the launcher
     int cone_cap = 0;
     unsigned long long* refine_count = nullptr;   // K4w: [0] RefineTasks appended at the buffer front, [1] refine

@@ -9,8 +9,6 @@ on FULL matrices / region tables (sha-256 of the whole output):
     (VISRT_K4W_FACEMAJOR=0), and the same three member-box residencies;
   * K4w refinement: fan candidate lists (default) vs one sweep per sightline
     (VISRT_K4W_FAN=0);
-  * K4w whole-face shadow certificate (default) vs every sample decided
-    (VISRT_K4W_SHADOW=0);
   * K4w cone lists (the face's candidate list once it is partly visible,
     default) vs every sample swept through the hierarchy (VISRT_K4W_CONE=0),
     and a cone capacity small enough to overflow (VISRT_K4W_CONE=48).
@@ -111,7 +109,6 @@ REGION_VARIANTS = [
     {"VISRT_K4W_FACEMAJOR": 0, "VISRT_QUANT": 2},
     {"VISRT_K4W_CONE": 0},
     {"VISRT_K4W_CONE": 48},
-    {"VISRT_K4W_SHADOW": 0},
 ]
 
 
