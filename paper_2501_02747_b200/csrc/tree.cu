@@ -480,9 +480,6 @@ __shared__ int k6l_buf[8][64];   // per warp (256 threads): pending children of 
 #ifndef VISRT_K6L_LAZY
 #define VISRT_K6L_LAZY 1   // 1: fused last level forms the children's image chains lazily (unfold_one pimg)
 #endif
-#ifndef VISRT_K6L_RXCULL
-#define VISRT_K6L_RXCULL 1   // 1: fused last level drops children the receiver is not strictly in front of before the unfold
-#endif
 #ifndef VISRT_K6L_MINB
 #define VISRT_K6L_MINB 3   // CTAs per SM the fused last level's register budget targets (r01: 1/3/4 -> 3 best, -2 %)
 #endif
@@ -514,9 +511,6 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
 #if VISRT_K6L_COMPACT
         // the children that pass the prune are compacted through shared memory
         // and unfolded 32 at a time (full lanes on the heavy unfold)
-        const bool rxcull = pimg != nullptr && a.snap_edge == nullptr;
-        const double* RxP = a.rx_fixed ? a.rx : a.rx + 3 * static_cast<size_t>(par.snap);
-        const double rx0 = RxP[0], rx1 = RxP[1], rx2 = RxP[2];
         int* buf = k6l_buf[threadIdx.x >> 5];
         int pend = 0;
         auto unfold_batch = [&](int m) {
@@ -532,22 +526,9 @@ __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, u
             const long long q = q0 + lane;
             int c = -1, rank;
             const bool ok = q < P.npool && tree_child(a, par, P, q, c, rank);
-            c_all += __popc(__ballot_sync(kFull, ok));   // every pruned-in child is a node (nodes_expanded)
-            // Receiver-side cull with the plane the prune just read: the child's
-            // sequence ends at its first backward step when the receiver is not
-            // strictly in front of c. That step tests da * db >= 0 with
-            // da = sd(c, Rx) and db = sd(c, mirror(image, c)) = -sd(c, image) up
-            // to rounding (~1e-11 m at km coordinates), so with the prune's
-            // sd(c, image) above 1e-6 m db is certainly negative and da <= 0
-            // makes the product >= 0: no sequence, nothing to unfold. (Snapshots
-            // with a diffraction edge unfold a second sequence to another
-            // target: not culled.)
-            bool keep = ok;
-            if (VISRT_K6L_RXCULL && ok && rxcull &&
-                sdist_face(a.s, c, par.ix, par.iy, par.iz) > 1e-6 && sdist_face(a.s, c, rx0, rx1, rx2) <= 0.0)
-                keep = false;
-            const unsigned ob = __ballot_sync(kFull, keep);
-            if (keep) buf[pend + __popc(ob & ((1u << lane) - 1u))] = c;
+            const unsigned ob = __ballot_sync(kFull, ok);
+            c_all += __popc(ob);
+            if (ok) buf[pend + __popc(ob & ((1u << lane) - 1u))] = c;
             pend += __popc(ob);
             __syncwarp();
             if (pend >= 32) {
