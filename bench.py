@@ -278,7 +278,8 @@ def secondary_measurements(stream: int, headline_cfg: int = 4):
         sc.pair_visibility("prefiltered", copy_bits=False)
         tri, sch = chain_triples(sc)
         out["chains_config3"] = {"candidate_triples": sch["candidates"], "feasible": sch["admitted"],
-                                 "ms": sch["ms"], "ncu": _committed_kernel_ncu("k7_config3")}
+                                 "ms": sch["ms"], "ncu": {"screen": _committed_kernel_ncu("k7_screen_config3"),
+                                                          "decide": _committed_kernel_ncu("k7_decide_config3")}}
         tr = Tracer(sc, 3, triples=tri)
         tr.trace_raw(wl.tx[:4], wl.rx[:4])
         _, _, nodes, tst = tr.trace_raw(wl.tx[:50], wl.rx[:50])
@@ -452,6 +453,13 @@ def run_visrt(args, rank, world):
         ncu = _committed_ncu(args.config)
         ops_per_test = ncu.get("fp64_thread_ops_per_exact_test") or FLOPS_PER_TEST
         achieved = ops_per_test * execd / (kern * 1e-3) / 1e12
+        # ncu's FP64-pipe share of the calibration launch, carried to this run's time and work
+        pipe_frac = None
+        try:
+            pipe_frac = (ncu["ncu_sol"]["fp64_pipe_pct"] / 100.0) * (ncu["duration_ms"] / kern) * \
+                        (execd / ncu["exact_tests"])
+        except (KeyError, TypeError, ZeroDivisionError):
+            pass
         wl_desc = {2: "config2: 1 km city, 200 boxes + 16x16 tiles, N=1256 facets",
                    3: "config3: 2 km Manhattan grid, 500 boxes + 16x16 tiles, N=2756 facets",
                    4: "config4: 4 km city, 2000 convex prisms + 32x32 tiles, N=22096 facets"}.get(
@@ -477,6 +485,13 @@ def run_visrt(args, rank, world):
                          "basis": "EXECUTED work: in-run exact-test count x FP64 thread ops per exact test "
                                   "(calibrated by ncu on this kernel, see ncu.source) / kernel time; peak = in-run "
                                   "DADD/DMUL microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
+                         "fp64_pipe": {"frac": pipe_frac,
+                                       "basis": "share of cycles the FP64 pipe is busy: ncu sm__pipe_fp64_cycles_active of "
+                                                "the committed capture of this launch (ncu.source), scaled by this run's "
+                                                "exact-test count and kernel time. Above `frac` because FP64 warp "
+                                                "instructions occupy the pipe with idle lanes (ncu.ncu_sol."
+                                                "active_threads_per_inst of 32) and the pipe also executes DSETP compares, "
+                                                "DMNMX and F2F conversions, which `frac` does not count as work"},
                          "executed_exact_tests": execd,
                          "executed_exact_tests_per_s": execd / (kern * 1e-3),
                          "reference_equivalent": {"achieved": ref_equiv, "frac": ref_equiv / peak,

@@ -3,6 +3,8 @@ bench.py labels as `"source": "committed ncu ..."` (profiles/<name>_ncu.json).
 
     python tools/ncu_calib.py REPORT.ncu-rep NAME "workload text" [EXACT_TESTS]
 
+NCU_ROW=k selects the k-th captured launch of a report that holds several (default 0).
+
 EXACT_TESTS = the exact segment-vs-face tests the captured launch ran (the
 library's stats['tests_exec'] printed by the captured command); with it the
 JSON carries fp64_thread_ops_per_exact_test = FP64 thread instructions
@@ -32,7 +34,8 @@ def main():
     rep, name, workload = sys.argv[1], sys.argv[2], sys.argv[3]
     tests = float(sys.argv[4]) if len(sys.argv) > 4 else None
     h, units, rows = raw(rep)
-    d = dict(zip(h, rows[0]))
+    import os
+    d = dict(zip(h, rows[int(os.environ.get("NCU_ROW", "0"))]))
     cyc = num(d, "sm__cycles_elapsed.avg")
     fp64 = 0.0
     for op, w in (("dadd", 1), ("dmul", 1), ("dfma", 2)):

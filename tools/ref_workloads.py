@@ -95,8 +95,61 @@ def run(cfg: int) -> dict:
     return out
 
 
+def all_pairs(n):
+    i, j = np.triu_indices(n, 1)
+    return i.astype(np.int32), j.astype(np.int32)
+
+
+def run_full(cfg: int) -> dict:
+    """r02: the stages SURVEY.md section 8(d) calls feasible, run IN FULL (or on the stated large
+    sample) instead of extrapolated from a few hundred units: config 2 / 3 (B) on every pair,
+    config 4 (A) = build_matrix(scene, 1), config-3 regions and order-1 tables for 200 of the
+    2,000 sources x every facet, config-3 order-3 traces for 100 snapshots and config-5 order-3
+    traces for every snapshot (both after the reference's own build_matrix(scene, 2))."""
+    wl = scenes.workload(cfg)
+    soup = wl.scene
+    n = soup.nfaces
+    r = bindings.RefOracle(soup)
+    out = {"config": cfg, "facets": n, "cores": CORES, "kind": "reference", "mode": "full"}
+    rng = np.random.default_rng(100 + cfg)
+    if cfg in (2, 3):
+        pi, pj = all_pairs(n)
+        _, dt = timed(lambda: r.occlusion_batch(pi, pj, threads=CORES))
+        out["matrix_B_pairs"] = len(pi)
+        out["matrix_B_s"] = round(dt, 2)
+    if cfg in (3, 4):
+        m1, dt = timed(lambda: r.build_matrix(1))
+        out["matrix_A_s"] = round(dt, 2)
+    if cfg == 3:
+        sel = np.concatenate([wl.tx[::10], wl.rx[::10]])   # 200 of the 2,000 sources
+        _, dt = timed(lambda: pool_map(lambda p: r.point_vis_table(m1, p, 1), list(sel)))
+        out["tables_order1_sources"] = len(sel)
+        out["tables_order1_s"] = round(dt, 2)
+        face = np.tile(np.arange(n, dtype=np.int32), len(sel))
+        src = np.repeat(sel, n, axis=0)
+        arr = (bindings.vref_region * len(face))()   # the C call alone (no per-record Python objects)
+        flat = np.ascontiguousarray(src, np.float64).reshape(-1)
+        _, dt = timed(lambda: r.lib().vref_regions_batch(r.h, len(face), flat, face, arr, CORES))
+        out["regions_sources"] = len(sel)
+        out["regions"] = int(len(face))
+        out["regions_s"] = round(dt, 2)
+    if cfg in (3, 5):
+        m2, dt = timed(lambda: r.build_matrix(2))
+        out["matrix_order2_s"] = round(dt, 2)
+        r.lib().vref_matrix_set_max_order(m2, 3)
+        acc = r.accel(m2, 3)
+        ks = list(range(0, len(wl.tx), 10)) if cfg == 3 else list(range(len(wl.tx)))
+        res, dt = timed(lambda: pool_map(lambda k: r.trace(acc, wl.tx[k], wl.rx[k])[1][0], ks))
+        out["trees_order3_snapshots"] = len(ks)
+        out["trees_order3_s"] = round(dt, 2)
+        out["trees_order3_nodes"] = int(np.sum(res))
+    return out
+
+
 if __name__ == "__main__":
     if not bindings.have_ref():
         bindings.build(ref=True)
-    for c in [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]:
-        print(json.dumps(run(c)), flush=True)
+    args = [a for a in sys.argv[1:] if a != "--full"]
+    fn = run_full if "--full" in sys.argv[1:] else run
+    for c in [int(a) for a in args] or [1, 2, 3, 4, 5]:
+        print(json.dumps(fn(c)), flush=True)

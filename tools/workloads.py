@@ -98,9 +98,9 @@ def pinned_records(count: int) -> np.ndarray:
 
 def regions(sc: Scene, src: np.ndarray, batch: int, out: dict, key: str):
     point_regions_array(sc, src[:2])
+    buf = pinned_records(min(batch, len(src)) * sc.n)   # one resident, page-locked host buffer for every batch
     s = Stage()
     present = 0
-    buf = pinned_records(min(batch, len(src)) * sc.n)   # one resident, page-locked host buffer for every batch
     for b in range(0, len(src), batch):
         arr, st = point_regions_array(sc, src[b:b + batch], out=buf)
         t = time.perf_counter()
