@@ -244,6 +244,7 @@ struct TriplePre {
     // edge direction of t's polygon) and t's own extents on them
     V2 axis[kPreAx];
     double amin[kPreAx], amax[kPreAx];
+    unsigned apos, aneg, azero;   // signs of da[]: strictly in front / behind / on t's plane (bit i)
     int nl, nm, ok, nax;
 };
 
@@ -264,7 +265,14 @@ __device__ __noinline__ void triple_pre(const DevScene& s, int a, int b, TripleP
     u = {__ddiv_rn(u.x, un), __ddiv_rn(u.y, un), __ddiv_rn(u.z, un)};
     P.u = u;
     P.v = v3cross(P.pl.n, u);
-    for (int i = 0; i < P.nl; ++i) P.da[i] = P.pl.sd(P.pa[i]);
+    P.apos = P.aneg = P.azero = 0u;
+    for (int i = 0; i < P.nl; ++i) {
+        const double di = P.pl.sd(P.pa[i]);
+        P.da[i] = di;
+        if (fabs(di) <= kEps) P.azero |= 1u << i;
+        else if (di > kEps) P.apos |= 1u << i;
+        else if (di < -kEps) P.aneg |= 1u << i;
+    }
     P.nm = s.nv[b];
     for (int k = 0; k < P.nm; ++k) {
         const V3 r = v3sub(face_pt(s, b, k), P.pl.p);
@@ -355,16 +363,22 @@ __device__ __forceinline__ int section_points(const TriplePre<MAXV>& P, const V3
 // axis_separates(mid2d, ., hull, ., axis) holds a fortiori, i.e.
 // convex_polygons_overlap_2d is false; an empty section is infeasible as well.
 template <int MAXV>
-__device__ __forceinline__ bool section_separated(const TriplePre<MAXV>& P, const V3* pts, const double* d, int np) {
+__device__ __forceinline__ bool section_separated(const TriplePre<MAXV>& P, const V3* cp, const double* cd, int nt) {
+    // point i < nl: the prefix pair's clipped polygon (shared memory, signs known);
+    // point nl + k: the aim's clipped and mirrored point k (local)
     const PlaneD& pl = P.pl;
     const V3 u = P.u, v = P.v;
-    unsigned pos = 0, neg = 0, zero = 0;
-    for (int i = 0; i < np; ++i) {
-        const double di = d[i];
-        if (fabs(di) <= kEps) zero |= 1u << i;
-        else if (di > kEps) pos |= 1u << i;
-        else if (di < -kEps) neg |= 1u << i;
+    const int nl = P.nl;
+    unsigned pos = P.apos, neg = P.aneg, zero = P.azero;
+    for (int k = 0; k < nt; ++k) {
+        const double dk = cd[k];
+        if (fabs(dk) <= kEps) zero |= 1u << (nl + k);
+        else if (dk > kEps) pos |= 1u << (nl + k);
+        else if (dk < -kEps) neg |= 1u << (nl + k);
     }
+    if (zero == 0u && (pos == 0u || neg == 0u)) return true;   // empty section: infeasible
+    auto pt = [&](int i) { return i < nl ? P.pa[i] : cp[i - nl]; };
+    auto sd = [&](int i) { return i < nl ? P.da[i] : cd[i - nl]; };
     double emin[kPreAx], emax[kPreAx];
 #pragma unroll
     for (int k = 0; k < kPreAx; ++k) {
@@ -381,16 +395,17 @@ __device__ __forceinline__ bool section_separated(const TriplePre<MAXV>& P, cons
             emax[k] = smax(emax[k], e);
         }
     };
-    if ((zero | pos | neg) == 0u || (zero == 0u && (pos == 0u || neg == 0u))) return true;   // empty section
-    for (unsigned m = zero; m; m &= m - 1) ext(pts[__ffs(m) - 1]);
+    for (unsigned m = zero; m; m &= m - 1) ext(pt(__ffs(m) - 1));
     for (unsigned mi = pos | neg; mi; mi &= mi - 1) {
         const int i = __ffs(mi) - 1;
-        const V3 pi = pts[i];
-        const double di = d[i];
-        for (unsigned m = (((pos >> i) & 1u) ? neg : pos) & ~((2u << i) - 1u); m; m &= m - 1) {
+        const unsigned opp = (((pos >> i) & 1u) ? neg : pos) & ~((2u << i) - 1u);
+        if (!opp) continue;
+        const V3 pi = pt(i);
+        const double di = sd(i);
+        for (unsigned m = opp; m; m &= m - 1) {
             const int j = __ffs(m) - 1;
-            const double t = __ddiv_rn(di, dsub(di, d[j]));
-            ext(v3add(pi, v3mul(v3sub(pts[j], pi), t)));
+            const double t = __ddiv_rn(di, dsub(di, sd(j)));
+            ext(v3add(pi, v3mul(v3sub(pt(j), pi), t)));
         }
     }
     bool sep = false;
@@ -457,11 +472,17 @@ __device__ __noinline__ bool triple_feasible_pre(const DevScene& s, const Triple
 // the full predicate.
 template <int MAXV>
 __device__ __noinline__ bool triple_screened_out(const DevScene& s, const TriplePre<MAXV>& P, int c) {
-    V3 pts[Caps<MAXV>::kPts];
-    double d[Caps<MAXV>::kPts];
-    const int np = triple_points<MAXV>(s, P, c, pts, d);
-    if (np == 0) return true;
-    return section_separated<MAXV>(P, pts, d, np);
+    const PlaneD pl = P.pl;
+    V3 cp[Caps<MAXV>::kClip];      // c clipped to t's plane, then mirrored through it in place
+    double cd[Caps<MAXV>::kClip];
+    const int nt = clip_halfspace<MAXV>(s, c, pl, cp);
+    if (nt < 2) return true;
+    for (int i = 0; i < nt; ++i) {   // the same operations as triple_points
+        const double d2 = dmul(2.0, pl.sd(cp[i]));   // mirror_point
+        cp[i] = v3sub(cp[i], v3mul(pl.n, d2));
+        cd[i] = pl.sd(cp[i]);
+    }
+    return section_separated<MAXV>(P, cp, cd, nt);
 }
 
 // ---- interval sets, src/vismatrix.cpp:43-97 (<= 4 intervals here) ----
