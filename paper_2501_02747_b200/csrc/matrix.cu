@@ -260,8 +260,17 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_HISLOT
 #define VISRT_K2W_HISLOT 0  // 1: sweep the highest-slot unresolved sightline first (r01: -1 % config 2, +4 % config 3)
 #endif
+// Large all-pairs launches grab tr x tc tiles of the pair matrix (PairArgs::tr, tc). The launcher
+// picks the shape by scene size (r02 sweeps, tools/r02_t9.sh / r02_t11.sh): 2 x 16 with a 6-entry
+// warp cache while the member boxes are shared-memory resident (config 3: 12.1 ms; 8 x 8 / 16 x 8
+// +3..13 %), 16 x 8 with an 8-entry cache for the streamed big scenes (config 4: 804 -> 757 ms; 8 x 8
+// 760-769, 8 x 16 802, 16 x 16 803, 32 x 32 919). VISRT_K2W_TR / VISRT_K2W_TC / VISRT_K2W_WCT (6 | 8)
+// override at run time (tests force every shape on small scenes).
+#ifndef VISRT_K2W_TMORTON
+#define VISRT_K2W_TMORTON 0
+#endif
 #ifndef VISRT_K2W_TR
-#define VISRT_K2W_TR 2      // large all-pairs launches grab TR x TC tiles of the pair matrix
+#define VISRT_K2W_TR 2      // default tile shape of the resident scenes
 #endif
 #ifndef VISRT_K2W_TC
 #define VISRT_K2W_TC 16
@@ -331,15 +340,15 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
     long long pnext = 0, pend = 0;
     int tI = 0, tJ = 0, tl = 0, tl_end = 0;   // tiled grabs: current tile origin and cursor
     const bool tiled = a.tiled != 0;
-    const int ntc = (n + VISRT_K2W_TC - 1) / VISRT_K2W_TC;
-    const long long ntiles_all =
-        a.tile_end ? a.tile_end : static_cast<long long>((n + VISRT_K2W_TR - 1) / VISRT_K2W_TR) * ntc;
+    const int TR = a.tr, TC = a.tc;
+    const int ntc = tiled ? (n + TC - 1) / TC : 1;
+    const long long ntiles_all = !tiled ? 0 : a.tile_end ? a.tile_end : static_cast<long long>((n + TR - 1) / TR) * ntc;
     const int row_end = a.row1 ? a.row1 : n;
     for (;;) {
         long long p = 0;
         int pi = 0, pj = 0;
         if (tiled) {
-            // a warp takes a VISRT_K2W_TR x VISRT_K2W_TC tile of the pair matrix
+            // a warp takes a TR x TC tile of the pair matrix
             // (neighbouring reference AND aim faces: the warp cache stays warm)
             bool got = false, done = false;
             while (!got) {
@@ -351,18 +360,26 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
                         done = true;
                         break;
                     }
-                    tI = static_cast<int>(T / ntc) * VISRT_K2W_TR;
-                    tJ = static_cast<int>(T % ntc) * VISRT_K2W_TC;
+                    tI = static_cast<int>(T / ntc) * TR;
+                    tJ = static_cast<int>(T % ntc) * TC;
                     tl = 0;
-                    tl_end = tJ + VISRT_K2W_TC - 1 > tI ? VISRT_K2W_TR * VISRT_K2W_TC : 0;   // skip tiles below the diagonal
+                    tl_end = tJ + TC - 1 > tI ? TR * TC : 0;   // skip tiles below the diagonal
                     continue;
                 }
                 const int l = tl++;
-                pi = tI + l / VISRT_K2W_TC;
-                pj = tJ + l % VISRT_K2W_TC;
+                pi = tI + l / TC;
+                pj = tJ + l % TC;
                 got = pi >= a.row0 && pi < row_end && pj < n && pj > pi;
             }
             if (done) break;
+            if (a.tmorton) {
+                // the tile is a block of Morton positions: its reference and aim faces
+                // are spatial neighbours (index neighbours are only building-mates);
+                // every unordered pair still comes up once, oriented lower index first
+                const int oi = s.perm[pi], oj = s.perm[pj];
+                pi = oi < oj ? oi : oj;
+                pj = oi < oj ? oj : oi;
+            }
         } else {
         // a warp takes VISRT_K2W_CHUNK consecutive pairs at a time: row-major
         // neighbours share the reference face (and its blockers: warp cache)
@@ -896,13 +913,21 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
             return e ? std::atoi(e) : -1;
         }();
         const bool big = tiled_env >= 0 ? tiled_env == 1 : work >= 512 * warps;
-        a.tiled = (VISRT_K2W_TR > 1 && !a.ci && a.stride == 1 && big) ? 1 : 0;
+        a.tiled = (!a.ci && a.stride == 1 && big) ? 1 : 0;
+        // tile shape by scene size (see VISRT_K2W_TR above); env overrides
+        static const int tr_env = [] { const char* e = std::getenv("VISRT_K2W_TR"); return e ? std::atoi(e) : 0; }();
+        static const int tc_env = [] { const char* e = std::getenv("VISRT_K2W_TC"); return e ? std::atoi(e) : 0; }();
+        const bool big_scene = a.s.n > kResidentMaxBoxes;
+        a.tr = tr_env > 0 ? tr_env : (big_scene ? 16 : VISRT_K2W_TR);
+        a.tc = tc_env > 0 ? tc_env : (big_scene ? 8 : VISRT_K2W_TC);
+        static const int tmorton_env = [] { const char* e = std::getenv("VISRT_K2W_TMORTON"); return e ? std::atoi(e) : -1; }();
+        a.tmorton = (tmorton_env >= 0 ? tmorton_env == 1 : VISRT_K2W_TMORTON != 0) && !a.row1 ? 1 : 0;   // row blocks cut face rows
         // the cursor's start value: the block's first tile (tiled) or first pair
-        const int ntc = (a.s.n + VISRT_K2W_TC - 1) / VISRT_K2W_TC;
+        const int ntc = (a.s.n + a.tc - 1) / a.tc;
         long long start = a.pbegin;
         if (a.tiled && a.row1) {
-            start = static_cast<long long>(a.row0 / VISRT_K2W_TR) * ntc;
-            a.tile_end = static_cast<long long>((a.row1 + VISRT_K2W_TR - 1) / VISRT_K2W_TR) * ntc;
+            start = static_cast<long long>(a.row0 / a.tr) * ntc;
+            a.tile_end = static_cast<long long>((a.row1 + a.tr - 1) / a.tr) * ntc;
         }
         if (start) {
             const unsigned long long s0 = static_cast<unsigned long long>(start);
@@ -930,6 +955,11 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         // tiled launches (large all-pairs builds) keep VISRT_K2W_WC_TILED cached
         // blockers, row grabs VISRT_K2W_WC (a larger cache costs config 2 ~3 %)
         constexpr int WT = VISRT_K2W_WC_TILED;
+        // streamed big scenes (config 4/5): 16 x 8 tiles with an 8-entry cache
+        static const int wct_env = [] { const char* e = std::getenv("VISRT_K2W_WCT"); return e ? std::atoi(e) : 0; }();
+        const int wct = wct_env > 0 ? wct_env : (a.s.n > kResidentMaxBoxes ? 8 : WT);
+        if (a.tiled && !two && !res && wct == 8)
+            return launch_persistent(k_pair_bits_warp<MAXV, false, VISRT_K2W_MINB, kThreads, 8>, smem, a, device, st);
         if (two) {
             if (a.tiled)
                 return res ? launch_persistent(k_pair_bits_warp<MAXV, true, 2, kThreads, WT>, smem, a, device, st)

@@ -4,7 +4,8 @@ on FULL matrices / region tables (sha-256 of the whole output):
   * K2w member boxes: fp32 resident (N <= 6,144), streamed with the group
     level, and 8-bit quantised in shared memory (sweep.h qsat; the default
     for 6,144 < N <= 24,576, forced on small scenes with VISRT_QUANT=2);
-  * K2w grabs: 16-pair rows vs 2 x 16 pair-matrix tiles (VISRT_K2W_TILED);
+  * K2w grabs: 16-pair rows vs pair-matrix tiles (VISRT_K2W_TILED) of the resident
+    (2 x 16) and the big-scene (16 x 8, 8-entry cache) shapes and an odd one (5 x 3);
   * K4w task walk: face-major (default) vs source-major
     (VISRT_K4W_FACEMAJOR=0), and the same three member-box residencies;
   * K4w refinement: fan candidate lists (default) vs one sweep per sightline
@@ -56,6 +57,10 @@ MATRIX_VARIANTS = [
     {"VISRT_K2W_TILED": 1},
     {"VISRT_K2W_TILED": 1, "VISRT_QUANT": 2},
     {"VISRT_K2W_TILED": 0, "VISRT_QUANT": 0, "VISRT_FORCE_STREAM": 1},
+    # the big-scene launch shape (16 x 8 tiles, 8-entry cache, streamed boxes) forced on small scenes
+    {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 16, "VISRT_K2W_TC": 8, "VISRT_K2W_WCT": 8, "VISRT_QUANT": 0,
+     "VISRT_FORCE_STREAM": 1},
+    {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 5, "VISRT_K2W_TC": 3},
 ]
 
 
@@ -90,7 +95,7 @@ def test_matrix_full_size_brute_force_vs_culled(cfg):
     """The whole (B) matrix of configs 3 and 4 (3.8 M / 244 M pairs) built twice: with the
     fp32 culling hierarchy, blocker caches and grouped sweeps (default), and brute force
     (VISRT_NOCULL=1: every culling test passes, every occluder reached runs the exact FP64
-    predicate — config 4: ~270x the exact tests, about a minute). Culling is only allowed to
+    predicate — config 4: ~270x the exact tests, ~15 s). Culling is only allowed to
     skip work, never to change a verdict: the bit matrices are identical."""
     code = MATRIX_B % (ROOT, cfg)
     culled = run(code)
@@ -114,6 +119,7 @@ ROWS = ("import sys, json, hashlib; import numpy as np; sys.path.insert(0, %r);"
 
 
 @pytest.mark.parametrize("cfg,world,env", [(1, 3, {}), (2, 4, {}), (2, 5, {"VISRT_K2W_TILED": 1}),
+                                           (2, 3, {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 16, "VISRT_K2W_TC": 8}),
                                            (3, 2, {}), (3, 7, {"VISRT_K2W_TILED": 0})])
 def test_matrix_row_blocks_or_to_the_full_matrix(cfg, world, env):
     """visrt_pair_visibility_rows: the row blocks of a partition (the strong-scaling
