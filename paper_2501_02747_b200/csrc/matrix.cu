@@ -260,12 +260,9 @@ __global__ void __launch_bounds__(kThreads, VISRT_K2_MINB) k_pair_bits(PairArgs 
 #ifndef VISRT_K2W_HISLOT
 #define VISRT_K2W_HISLOT 0  // 1: sweep the highest-slot unresolved sightline first (r01: -1 % config 2, +4 % config 3)
 #endif
-// Large all-pairs launches grab tr x tc tiles of the pair matrix (PairArgs::tr, tc). The launcher
-// picks the shape by scene size (r02 sweeps, tools/r02_t9.sh / r02_t11.sh): 2 x 16 with a 6-entry
-// warp cache while the member boxes are shared-memory resident (config 3: 12.1 ms; 8 x 8 / 16 x 8
-// +3..13 %), 16 x 8 with an 8-entry cache for the streamed big scenes (config 4: 804 -> 757 ms; 8 x 8
-// 760-769, 8 x 16 802, 16 x 16 803, 32 x 32 919). VISRT_K2W_TR / VISRT_K2W_TC / VISRT_K2W_WCT (6 | 8)
-// override at run time (tests force every shape on small scenes).
+// Large all-pairs launches grab tr x tc tiles of the pair matrix (PairArgs::tr, tc, tmorton); the
+// launcher picks the shape by scene (launch_bits_t). VISRT_K2W_TR / VISRT_K2W_TC / VISRT_K2W_TMORTON /
+// VISRT_K2W_WCT (6 | 8) override at run time (tests force every shape on small scenes).
 #ifndef VISRT_K2W_TMORTON
 #define VISRT_K2W_TMORTON 0
 #endif
@@ -912,16 +909,24 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
             const char* e = std::getenv("VISRT_K2W_TILED");
             return e ? std::atoi(e) : -1;
         }();
-        const bool big = tiled_env >= 0 ? tiled_env == 1 : work >= 512 * warps;
-        a.tiled = (!a.ci && a.stride == 1 && big) ? 1 : 0;
-        // tile shape by scene size (see VISRT_K2W_TR above); env overrides
+        // Grab shape by scene (r02 sweeps, tools/r02_t9/t11..t15.sh; every shape gives the same bits):
+        //  * streamed big scenes (config 4/5): 64 x 2 tiles of face INDICES — a long run of
+        //    reference faces against two aim faces — with an 8-entry cache (config 4: 2 x 16
+        //    804 ms, 16 x 8 760, 32 x 4 736, 64 x 2 733, 128 x 1 833; Morton tiles 749-778);
+        //  * resident scenes (configs 2/3): rows of MORTON positions, 1 x tc with tc = pairs per
+        //    warp / 14 in [8, 48] (config 3: index 2 x 16 12.2 ms -> Morton 1 x 48 11.0 ms;
+        //    config 2: 16-pair index rows 3.75 ms -> Morton 1 x 16 3.45 ms).
         static const int tr_env = [] { const char* e = std::getenv("VISRT_K2W_TR"); return e ? std::atoi(e) : 0; }();
         static const int tc_env = [] { const char* e = std::getenv("VISRT_K2W_TC"); return e ? std::atoi(e) : 0; }();
-        const bool big_scene = a.s.n > kResidentMaxBoxes;
-        a.tr = tr_env > 0 ? tr_env : (big_scene ? 16 : VISRT_K2W_TR);
-        a.tc = tc_env > 0 ? tc_env : (big_scene ? 8 : VISRT_K2W_TC);
         static const int tmorton_env = [] { const char* e = std::getenv("VISRT_K2W_TMORTON"); return e ? std::atoi(e) : -1; }();
-        a.tmorton = (tmorton_env >= 0 ? tmorton_env == 1 : VISRT_K2W_TMORTON != 0) && !a.row1 ? 1 : 0;   // row blocks cut face rows
+        const bool big_scene = a.s.n > kResidentMaxBoxes;
+        const long long per_warp = work / warps;
+        const bool big = tiled_env >= 0 ? tiled_env == 1 : (big_scene ? per_warp >= 512 : per_warp >= 8 * 14);
+        a.tiled = (!a.ci && a.stride == 1 && big) ? 1 : 0;
+        a.tr = tr_env > 0 ? tr_env : (big_scene ? 64 : 1);
+        a.tc = tc_env > 0 ? tc_env
+                          : (big_scene ? 2 : static_cast<int>(std::min<long long>(48, std::max<long long>(8, per_warp / 14))));
+        a.tmorton = (tmorton_env >= 0 ? tmorton_env == 1 : !big_scene) && !a.row1 ? 1 : 0;   // row blocks cut face rows
         // the cursor's start value: the block's first tile (tiled) or first pair
         const int ntc = (a.s.n + a.tc - 1) / a.tc;
         long long start = a.pbegin;
