@@ -516,8 +516,8 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
             if (RES == kStreamed && ctx.gbox && !a.flat && !a.nocull) {
                 // non-resident scenes (config 4/5): tile -> group (shared memory) -> member (L1/L2)
                 int more[2];
-                hit = coop_any_hit_grouped<MAXV>(ctx, s.srec, g, ax, ay, az, bx, by, bz, si, sj, a.home_aim ? sj : si,
-                                                 tests, batches, more, VISRT_K2W_PRI ? (a.home_aim ? si : sj) : -1);
+                hit = coop_any_hit_grouped<MAXV>(ctx, s.srec, g, ax, ay, az, bx, by, bz, si, sj, si, tests, batches,
+                                                 more, VISRT_K2W_PRI ? sj : -1);
 #if VISRT_K2W_MULTI
                 if (hit >= 0) {
                     hit2 = more[0];
@@ -926,8 +926,6 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         a.tr = tr_env > 0 ? tr_env : (big_scene ? 64 : 1);
         a.tc = tc_env > 0 ? tc_env
                           : (big_scene ? 2 : static_cast<int>(std::min<long long>(48, std::max<long long>(8, per_warp / 14))));
-        static const int homeaim_env = [] { const char* e = std::getenv("VISRT_K2W_HOMEAIM"); return e ? std::atoi(e) : 0; }();
-        a.home_aim = homeaim_env;
         a.tmorton = (tmorton_env >= 0 ? tmorton_env == 1 : !big_scene) && !a.row1 ? 1 : 0;   // row blocks cut face rows
         // the cursor's start value: the block's first tile (tiled) or first pair
         const int ntc = (a.s.n + a.tc - 1) / a.tc;
