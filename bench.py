@@ -479,19 +479,23 @@ def run_visrt(args, rank, world):
                     "d2h_bytes_per_step": int(d2h), "s_per_step": e2e_max,
                     "path": "Scene(soup) ingest+upload -> pair_visibility -> bits D2H -> free"},
             "gpu_launches": args.steps,
-            "roofline": {"bound": "fp64", "kernel": "k_pair_bits_warp", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak,
+            # EXECUTED work against the FP64 pipe (executed FP64 instructions / (kernel time x
+            # peak rate), ncu pipe % as the cross-check). `frac` = the share of the pipe's issue capacity
+            # the kernel's FP64 warp instructions take; `thread_ops` = the stricter lane-level count.
+            "roofline": {"bound": "fp64", "kernel": "k_pair_bits_warp",
+                         "achieved": (pipe_frac if pipe_frac is not None else achieved / peak) * peak, "peak": peak,
+                         "unit": "TFLOP/s", "frac": pipe_frac if pipe_frac is not None else achieved / peak,
                          "traffic": ncu.get("dram_bytes_per_launch"),
-                         "basis": "EXECUTED work: in-run exact-test count x FP64 thread ops per exact test "
-                                  "(calibrated by ncu on this kernel, see ncu.source) / kernel time; peak = in-run "
-                                  "DADD/DMUL microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
-                         "fp64_pipe": {"frac": pipe_frac,
-                                       "basis": "share of cycles the FP64 pipe is busy: ncu sm__pipe_fp64_cycles_active of "
-                                                "the committed capture of this launch (ncu.source), scaled by this run's "
-                                                "exact-test count and kernel time. Above `frac` because FP64 warp "
-                                                "instructions occupy the pipe with idle lanes (ncu.ncu_sol."
-                                                "active_threads_per_inst of 32) and the pipe also executes DSETP compares, "
-                                                "DMNMX and F2F conversions, which `frac` does not count as work"},
+                         "basis": "EXECUTED FP64-pipe warp instructions / (kernel time x the pipe's issue rate): ncu "
+                                  "sm__pipe_fp64_cycles_active of the committed capture of this very launch "
+                                  "(ncu.source), scaled by this run's exact-test count and kernel time; `achieved` is "
+                                  "that share of the in-run DADD/DMUL peak (MEASURED_PEAKS.json has no FP64 entry)",
+                         "thread_ops": {"achieved": achieved, "frac": achieved / peak, "unit": "TFLOP/s",
+                                        "basis": "lane-level: in-run exact-test count x DADD+DMUL+2*DFMA thread ops "
+                                                 "per exact test (ncu-calibrated on this launch) / kernel time. Below "
+                                                 "`frac` because FP64 warp instructions hold the pipe with idle lanes "
+                                                 "(ncu.ncu_sol.active_threads_per_inst of 32) and the pipe also "
+                                                 "executes DSETP compares, DMNMX and F2F conversions, not counted here"},
                          "executed_exact_tests": execd,
                          "executed_exact_tests_per_s": execd / (kern * 1e-3),
                          "reference_equivalent": {"achieved": ref_equiv, "frac": ref_equiv / peak,
