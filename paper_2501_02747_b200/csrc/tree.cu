@@ -481,7 +481,7 @@ __shared__ int k6l_buf[8][64];   // per warp (256 threads): pending children of 
 #define VISRT_K6L_LAZY 1   // 1: fused last level forms the children's image chains lazily (unfold_one pimg)
 #endif
 #ifndef VISRT_K6L_MINB
-#define VISRT_K6L_MINB 3   // CTAs per SM the fused last level's register budget targets (r01: 1/3/4 -> 3 best, -2 %)
+#define VISRT_K6L_MINB 2   // CTAs per SM the fused last level's register budget targets (r02 final sweep, config 3 order 3 per 50 snapshots: 2 -> 16.5 ms, 3 -> 17.2, 4 -> 19.5)
 #endif
 template <int MAXV>
 __global__ void __launch_bounds__(256, VISRT_K6L_MINB) k_tree_last(TreeArgs a, unsigned long long* cnt,
