@@ -92,6 +92,7 @@ struct PairArgs {
     int32_t chunk;                   // K2w: consecutive pairs per warp grab
     int32_t tiled;                   // K2w: 1 = grabs are tr x tc tiles of the pair matrix (all pairs)
     int32_t tr, tc;                  // K2w: tile shape (reference faces x aim faces), set by the launcher
+    int32_t serp;                    // K2w: 1 = tiles are walked boustrophedon (consecutive pairs always share a face)
     int32_t tmorton;                 // K2w: 1 = tiles cut the pair matrix in Morton positions (spatial neighbours), not face indices
     int32_t stride;                  // K2w profiling aid: decide every stride-th pair only (VISRT_K2_STRIDE, default 1)
     int32_t nocull;                  // K2w: 1 = no fp32 culling, every occluder tested exactly (VISRT_NOCULL)

@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pair_bits_warp(PairArgs a) {
                 const int l = tl++;
                 pi = tI + l / TC;
                 pj = tJ + l % TC;
+                if (a.serp && ((l / TC) & 1)) pj = tJ + TC - 1 - l % TC;
                 got = pi >= a.row0 && pi < row_end && pj < n && pj > pi;
             }
             if (done) break;
@@ -910,9 +911,11 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
             return e ? std::atoi(e) : -1;
         }();
         // Grab shape by scene (r02 sweeps, tools/r02_t9/t11..t15.sh; every shape gives the same bits):
-        //  * streamed big scenes (config 4/5): 64 x 2 tiles of face INDICES — a long run of
-        //    reference faces against two aim faces — with an 8-entry cache (config 4: 2 x 16
-        //    804 ms, 16 x 8 760, 32 x 4 736, 64 x 2 733, 128 x 1 833; Morton tiles 749-778);
+        //  * streamed big scenes (config 4/5): 48 x 4 tiles of face INDICES — a long run of
+        //    reference faces against four aim faces — walked boustrophedon (consecutive pairs
+        //    always share a face), with an 8-entry cache (config 4: 2 x 16 804 ms, 16 x 8 760,
+        //    32 x 4 736, 64 x 2 733, 128 x 1 833; Morton tiles 749-778; boustrophedon 64 x 2 733,
+        //    64 x 4 723, 48 x 4 722, 64 x 6 735);
         //  * resident scenes (configs 2/3): rows of MORTON positions, 1 x tc with tc = pairs per
         //    warp / 14 in [8, 48] (config 3: index 2 x 16 12.2 ms -> Morton 1 x 48 11.0 ms;
         //    config 2: 16-pair index rows 3.75 ms -> Morton 1 x 16 3.45 ms).
@@ -923,9 +926,11 @@ static cudaError_t launch_bits_t(const PairArgs& a0, int device, cudaStream_t st
         const long long per_warp = work / warps;
         const bool big = tiled_env >= 0 ? tiled_env == 1 : (big_scene ? per_warp >= 512 : per_warp >= 8 * 14);
         a.tiled = (!a.ci && a.stride == 1 && big) ? 1 : 0;
-        a.tr = tr_env > 0 ? tr_env : (big_scene ? 64 : 1);
+        a.tr = tr_env > 0 ? tr_env : (big_scene ? 48 : 1);
         a.tc = tc_env > 0 ? tc_env
-                          : (big_scene ? 2 : static_cast<int>(std::min<long long>(48, std::max<long long>(8, per_warp / 14))));
+                          : (big_scene ? 4 : static_cast<int>(std::min<long long>(48, std::max<long long>(8, per_warp / 14))));
+        static const int serp_env = [] { const char* e = std::getenv("VISRT_K2W_SERP"); return e ? std::atoi(e) : -1; }();
+        a.serp = serp_env >= 0 ? serp_env : (big_scene ? 1 : 0);
         a.tmorton = (tmorton_env >= 0 ? tmorton_env == 1 : !big_scene) && !a.row1 ? 1 : 0;   // row blocks cut face rows
         // the cursor's start value: the block's first tile (tiled) or first pair
         const int ntc = (a.s.n + a.tc - 1) / a.tc;

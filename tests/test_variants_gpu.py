@@ -60,7 +60,8 @@ MATRIX_VARIANTS = [
     # the big-scene launch shape (16 x 8 tiles, 8-entry cache, streamed boxes) forced on small scenes
     {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 16, "VISRT_K2W_TC": 8, "VISRT_K2W_WCT": 8, "VISRT_QUANT": 0,
      "VISRT_FORCE_STREAM": 1},
-    {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 5, "VISRT_K2W_TC": 3},
+    {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 5, "VISRT_K2W_TC": 3, "VISRT_K2W_SERP": 1},
+    {"VISRT_K2W_TILED": 1, "VISRT_K2W_TR": 48, "VISRT_K2W_TC": 4, "VISRT_K2W_SERP": 1, "VISRT_K2W_TMORTON": 0},
 ]
 
 
