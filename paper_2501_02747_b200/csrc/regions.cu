@@ -546,7 +546,7 @@ __device__ unsigned long long g_k4w_prof[24];
 #define VISRT_K4W_WC 3   // warp blocker-cache entries, most recent first (r01, face-major walk, 1/2/3/4 swept: 3 best overall)
 #endif
 #ifndef VISRT_K4W_CHUNK
-#define VISRT_K4W_CHUNK 1   // consecutive (source, face) tasks per warp grab (r01: 8/16 measured slower: heavy faces cluster)
+#define VISRT_K4W_CHUNK 1   // consecutive (source, face) tasks per warp grab on the streamed big scenes (x 4 on resident scenes, see launch_regions_t)
 #endif
 // Warp blocker cache: lane q < VISRT_K4W_WC holds entry q (Morton index or
 // -1); `next` is the warp-uniform insertion slot. Entries are distinct.
@@ -1448,7 +1448,12 @@ static cudaError_t launch_regions_t(const RegionArgs& a0, int device, cudaStream
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const long long warps = static_cast<long long>(sms) * 2 * (kThreads / 32);
-        a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(VISRT_K4W_CHUNK, a.ntasks / (8 * warps))));
+        // resident scenes take 4 consecutive tasks per grab (one face, 4 neighbouring snapshots: the
+        // warp cache stays warm; r02, config 3 2,000 x 2,756 regions: 1 -> 116.5 ms, 2 -> 111.3, 4 -> 109.4,
+        // 8 -> 109.3, 16 -> 110.9); the streamed big scenes keep 1 (config 5, 500 snapshots: 1 -> 412 ms,
+        // 2 -> 423, 4 -> 442, 8 -> 463: heavy faces cluster and the tail grows)
+        const int want = a.s.n > kResidentMaxBoxes ? VISRT_K4W_CHUNK : 4 * VISRT_K4W_CHUNK;
+        a.chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(want, a.ntasks / (8 * warps))));
     }
     const char* e = std::getenv("VISRT_FORCE_STREAM");
     const bool res = !(e && e[0] == '1') && a.s.n <= kResidentMaxBoxes;
