@@ -223,6 +223,9 @@ __device__ __noinline__ bool triple_feasible(const DevScene& s, int a, int b, in
 #ifndef VISRT_K7_SCREEN
 #define VISRT_K7_SCREEN 1   // 0: kernel 1 passes every candidate on (A/B: the screen must not change the triples)
 #endif
+#ifndef VISRT_K7_SPLIT2
+#define VISRT_K7_SPLIT2 1   // second_order_check runs as a third kernel over the hull-feasible triples
+#endif
 #ifndef VISRT_K7_MASKS
 #define VISRT_K7_MASKS 1   // decide kernel: the section's crossing pairs from sign masks (same pairs, same order)
 #endif
@@ -718,7 +721,9 @@ __global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_decide(ChainArgs a
         for (int k = lane; k < nw; k += 32) any |= w[k] != 0u;
         if (!__any_sync(kAll, any)) continue;            // every aim screened out
         const int p = a.pair_p[r];
+#if !VISRT_K7_SPLIT2
         const int rp_pt = req_planes(s, p, t);
+#endif
         __syncwarp();
         if (lane == 0) triple_pre<MAXV>(s, p, t, pre);
         __syncwarp();
@@ -744,11 +749,13 @@ __global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_decide(ChainArgs a
             if (q >= 0) {
                 c = a.idx1[q];
                 ok = triple_feasible_pre<MAXV>(s, pre, c);
+#if !VISRT_K7_SPLIT2
                 if (ok) {
                     const int planes = req_planes(s, t, c) & rp_pt;
                     for (int pl = 0; pl < 3 && ok; ++pl)
                         if (planes >> pl & 1) ok = second_order_reachable(s, p, t, c, pl);
                 }
+#endif
             }
             const unsigned m = __ballot_sync(kAll, ok);
             if (!m) continue;
@@ -762,6 +769,41 @@ __global__ void __launch_bounds__(128, VISRT_K7_MINB) k_chain_decide(ChainArgs a
                     a.out[3 * slot + 1] = t;
                     a.out[3 * slot + 2] = c;
                 }
+            }
+        }
+    }
+}
+
+// K7's third kernel (VISRT_K7_SPLIT2): second_order_check in every working plane the
+// prefix pair and the aim pair share, thread per chain_triple_feasible triple — its
+// 1.3k instructions of interval arithmetic stay out of the decide kernel's footprint.
+__global__ void __launch_bounds__(256) k_chain_second(DevScene s, const int32_t* in, long long n, int32_t* out,
+                                                      unsigned long long* nout, long long cap) {
+    const int lane = threadIdx.x & 31;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long k0 = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) - lane; k0 < n; k0 += stride) {
+        const long long k = k0 + lane;
+        bool ok = k < n;
+        int p = 0, t = 0, c = 0;
+        if (ok) {
+            p = in[3 * k];
+            t = in[3 * k + 1];
+            c = in[3 * k + 2];
+            const int planes = req_planes(s, t, c) & req_planes(s, p, t);
+            for (int pl = 0; pl < 3 && ok; ++pl)
+                if (planes >> pl & 1) ok = second_order_reachable(s, p, t, c, pl);
+        }
+        const unsigned m = __ballot_sync(kAll, ok);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(nout, static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(kAll, base, 0);
+        if (ok) {
+            const long long slot = static_cast<long long>(base) + __popc(m & ((1u << lane) - 1u));
+            if (slot < cap) {
+                out[3 * slot] = p;
+                out[3 * slot + 1] = t;
+                out[3 * slot + 2] = c;
             }
         }
     }
@@ -926,6 +968,21 @@ extern "C" int visrt_chain_triples(visrt_scene* sc, const uint64_t* admitted_bit
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, decide, 128, 0);
             decide<<<sms * std::max(per, 1), 128, 0, st>>>(a);
             ck(cudaGetLastError(), "k_chain_decide");
+#if VISRT_K7_SPLIT2
+            // the hull-feasible triples through second_order_check, compacted into a second buffer
+            unsigned long long n1 = 0;
+            ck(cudaMemcpyAsync(&n1, a.nout, 8, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            if (n1) {
+                int32_t* out2 = visrt::dalloc<int32_t>(static_cast<size_t>(n1) * 3, tmp);
+                ck(cudaMemsetAsync(a.nout, 0, 8, st), "memset");
+                const long long m1 = static_cast<long long>(n1);
+                visrt::k_chain_second<<<static_cast<int>(std::min<long long>((m1 + 255) / 256, 148 * 8)), 256, 0, st>>>(
+                    a.s, a.out, m1, out2, a.nout, m1);
+                ck(cudaGetLastError(), "k_chain_second");
+                a.out = out2;
+            }
+#endif
         };
         if (a.npairs > 0) {
             if (ds.maxv <= 4) run2(visrt::k_chain_screen<4>, visrt::k_chain_decide<4>);
