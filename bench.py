@@ -279,7 +279,8 @@ def secondary_measurements(stream: int, headline_cfg: int = 4):
         tri, sch = chain_triples(sc)
         out["chains_config3"] = {"candidate_triples": sch["candidates"], "feasible": sch["admitted"],
                                  "ms": sch["ms"], "ncu": {"screen": _committed_kernel_ncu("k7_screen_config3"),
-                                                          "decide": _committed_kernel_ncu("k7_decide_config3")}}
+                                                          "decide": _committed_kernel_ncu("k7_decide_config3"),
+                                                          "second": _committed_kernel_ncu("k7_second_config3")}}
         tr = Tracer(sc, 3, triples=tri)
         tr.trace_raw(wl.tx[:4], wl.rx[:4])
         _, _, nodes, tst = tr.trace_raw(wl.tx[:50], wl.rx[:50])
